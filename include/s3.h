@@ -1,0 +1,208 @@
+/* s3.h -- C ABI of the B200-native S^3 length-aware KV-cache decode step.
+ *
+ * S^3 (arXiv 2306.06000): each sequence's KV slot is sized by its PREDICTED
+ * output length (PAPER.md:153-178 [§3 Design]).  One iteration of the hot
+ * path is four calls:
+ *
+ *   s3_decode_step    length-masked multi-head decode attention over each
+ *                     slot's contiguous KV rows, fused with the KV append and
+ *                     the overrun detection
+ *   s3_evict_compact  eviction of overruns to pinned host memory and the
+ *                     row-shift compaction of survivors
+ *   s3_admit          first-fit-decreasing admission of queued requests into
+ *                     the freed capacity, doubling the reservation of evicted
+ *                     ones
+ *   s3_kv_init        binds the arena and creates the context.
+ *
+ * Conventions
+ * -----------
+ * - Every function returns s3_status; nothing throws or longjmps across the ABI.
+ * - Data layout: the KV arena is bf16
+ *   [R][L][2][H][D] -- one token ROW holds all layers' K and V of that token,
+ *   kvpt = 4*L*H*D bytes ("4 l d_h bytes per token").  A
+ *   sequence owns rows [off, off+cap); rows [off, off+len) are resident.
+ *   Slots are kept in arena order (batch index b increases with off).
+ * - q / k_new / v_new are bf16 [nl][B][H][D]; out is fp32 [nl][B][H][D]; B is
+ *   the running batch size (s3_batch_size), b the batch index.
+ * - All device pointers are on cfg.device; all device work is ordered on
+ *   cfg.stream (a cudaStream_t, e.g. torch's current stream).
+ * - Ownership: the caller allocates and frees every buffer in s3_buffers
+ *   (sizes from s3_workspace_query).  The context owns host scheduling state,
+ *   a side stream, CUDA events and small pinned host staging buffers.
+ * - Errors: S3_E_INVAL / S3_E_UNSCHEDULABLE leave the state unchanged.
+ *   S3_E_CUDA poisons the context: afterwards only s3_kv_destroy and
+ *   s3_last_error are valid.  S3_E_STATE = call out of order (e.g. two decode
+ *   steps without an s3_evict_compact in between).
+ * - One context per GPU / process.  Calls are not reentrant.
+ */
+#ifndef S3_H
+#define S3_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  S3_OK = 0,
+  S3_E_INVAL = 1,          /* bad argument or config                                 */
+  S3_E_NOMEM = 2,          /* caller buffer / host store too small                   */
+  S3_E_CUDA = 3,           /* CUDA runtime error (context poisoned)                  */
+  S3_E_STATE = 5,          /* call out of order / logic error          */
+  S3_E_UNSCHEDULABLE = 6   /* reservation larger than the whole arena  */
+} s3_status;
+
+/* Per-slot status after a decode step (R11). */
+enum { S3_RUNNING = 0, S3_FINISHED = 1, S3_OVERRUN = 2 };
+
+#define S3_NCOUNTERS 8
+/* Counter row exchanged between ranks:
+ * 0 free_rows, 1 running, 2 free_slots, 3 evicted_waiting, 4 fresh_waiting
+ * (identical on every rank), 5 finished_total, 6 evicted_total, 7 tokens_total */
+
+typedef struct s3_ctx s3_ctx;
+
+typedef struct {
+  int32_t num_layers, num_heads, head_dim;  /* L, H, D; head_dim in {64,128,256}; H*D <= 8192 */
+  int32_t max_seq_len;                      /* cap on P + output (2048 for GPT-J runs)         */
+  int64_t arena_rows;                       /* R >= max_seq_len                                */
+  int32_t max_running;                      /* metadata capacity B_max (admission stops there) */
+  int32_t chunk_rows;                       /* attention split-K chunk C in rows (0 = 512)     */
+  int32_t move_chunk_bytes;                 /* compaction chunk S (0 = 32768; multiple of 16)  */
+  int32_t device;                           /* CUDA device ordinal                             */
+  void*   stream;                           /* cudaStream_t for all device work                */
+  int32_t rank, world;                      /* multi-GPU partition by sequence (world >= 1)    */
+  uint64_t synth_seed;                      /* generator seed for the prompt-fill stand-in     */
+} s3_config;
+
+typedef struct {                            /* caller-owned memory                             */
+  void* arena;      int64_t arena_bytes;    /* device, >= R * kvpt, 256-B aligned              */
+  void* workspace;  int64_t workspace_bytes;/* device, >= s3_workspace_query's figure          */
+  void* staging;    int64_t staging_bytes;  /* device eviction staging (0 => synchronous D2H)  */
+  void* host_store; int64_t host_store_bytes; /* pinned host memory for evicted KV             */
+} s3_buffers;
+
+/* Byte sizes of the caller buffers for cfg.  staging_min is the size that
+ * always lets one max-length eviction stage (max_seq_len * kvpt).          */
+s3_status s3_workspace_query(const s3_config* cfg, int64_t* arena_bytes, int64_t* workspace_bytes,
+                             int64_t* staging_min, int64_t* host_store_min);
+
+/* Validate cfg, bind the buffers, create the side stream and events. */
+s3_status s3_kv_init(const s3_config* cfg, const s3_buffers* bufs, s3_ctx** out);
+s3_status s3_kv_destroy(s3_ctx* ctx);
+const char* s3_last_error(const s3_ctx* ctx);   /* static text; never NULL */
+
+/* ---- request pool ("A text generation query arrives in a
+ * request pool in the host DRAM") -------------------------------------- */
+typedef struct { int64_t req_id; int32_t prompt_len, alloc_out; } s3_request;
+/* Adds fresh requests; reservation cap = prompt_len + alloc_out rows
+ * (R4).  S3_E_INVAL if prompt_len < 0, alloc_out < 1 or the cap
+ * exceeds max_seq_len; S3_E_UNSCHEDULABLE if cap > arena_rows.  With
+ * world > 1 every rank must submit the same requests in the same order.   */
+s3_status s3_submit(s3_ctx* ctx, const s3_request* reqs, int32_t n);
+
+/* ---- (a)+(b): decode attention + append + overrun detection -----------
+ * For every running slot b and layer l in [l0, l0+nl): write k_new/v_new
+ * into row off_b + len_b and compute
+ *     out[l][b][h] = softmax( q K^T / sqrt(D) ) V   over rows 0..len_b
+ * (PAPER.md:106 [§2.1]; R1 self-inclusive, R2 per-head D).
+ * eos (device uint8 [B]) is read only when l0+nl == L: then len, gen += 1
+ * and status_b = FINISHED if eos_b, else OVERRUN if len_b == cap_b, else
+ * RUNNING ("not finished but used up its reserved memory").
+ * Stream-ordered on cfg.stream, no host synchronisation.                   */
+s3_status s3_decode_step(s3_ctx* ctx, int32_t l0, int32_t nl, const void* q, const void* k_new,
+                         const void* v_new, const uint8_t* eos, float* out);
+
+/* ---- (c)+(d): eviction + row-shift compaction ------------------------- */
+typedef struct {
+  int64_t req_id;
+  int32_t batch_index, prompt_len, gen_len, len, cap_rows, new_cap_rows;
+  int64_t host_off;          /* byte offset of its rows [len][L][2][H][D] in host_store */
+} s3_evicted;
+typedef struct {
+  int32_t n_before, n_finished, n_evicted, n_kept;
+  int64_t tail_rows;         /* sum of kept caps = first free row                        */
+  int64_t d2h_bytes;         /* sum over evicted of len*kvpt (== S_P, len == cap)         */
+  int64_t moved_bytes;       /* sum over moved survivors of len*kvpt (one way)            */
+  int64_t paper_pcie_bytes;  /* sum over evicted i of 2 S_P(x_i)   */
+  int64_t paper_hbm_bytes;   /* sum over evicted i of 2 sum_{j>i} S_P(x_j)  */
+  int32_t first_hole;        /* batch index of the first non-running slot, or n_before   */
+  int32_t sync_evict;        /* 1 if staging was too small and the D2H ran in-stream      */
+} s3_evict_report;
+/* Consumes the statuses of the last complete decode step: overruns' resident
+ * KV goes to host_store (async D2H on the side stream, staged through
+ * `staging`), survivors are shifted up in place preserving order
+ * ("shifts the rows below the blank one so that all rows are stored
+ * contiguously"), finished and evicted slots leave (R6), and
+ * evicted requests re-enter the pool with cap <- min(2 cap, max_seq_len)
+ * (R5).  perm[b] = new batch index or -1; evicted / finished_ids list the
+ * leavers in batch order.  Each output array may be NULL, else it must hold
+ * n_before entries.  Synchronises the host once on a small report readback. */
+s3_status s3_evict_compact(s3_ctx* ctx, s3_evict_report* rep, int32_t* perm, s3_evicted* evicted,
+                           int64_t* finished_ids);
+/* Blocks until the host copy of every eviction so far is complete.        */
+s3_status s3_evict_wait(s3_ctx* ctx);
+
+/* ---- (e): admission by first-fit decreasing --------------------------- */
+typedef struct {
+  int32_t n_admitted, n_fresh, n_reloaded, n_batch;
+  int64_t tail_rows;
+  int64_t fill_bytes;        /* prompt rows written for fresh admissions (prefill stand-in) */
+  int64_t h2d_bytes;         /* evicted KV reloaded from host_store                        */
+} s3_admit_report;
+/* world == 1: one FFD over the whole pool, fresh and evicted alike, sorted
+ * by (cap desc, req_id asc), skip-and-continue, into free = R - tail rows
+ * (R7-R9).  Admitted slots are appended at the
+ * tail in scan order; fresh ones get their P prompt rows, evicted ones get
+ * their host rows back.  admitted_ids (may be NULL) receives the admitted
+ * req ids in placement order (capacity: max_running).                     */
+s3_status s3_admit(s3_ctx* ctx, s3_admit_report* rep, int64_t* admitted_ids);
+/* world > 1 (R26), called in this order each step:
+ *   s3_admit_home    re-admit this rank's evicted requests (local FFD);
+ *   s3_counters_local + an all-reduce(sum) of the [world][S3_NCOUNTERS]
+ *                    matrix by the caller (torch.distributed / NCCL);
+ *   s3_admit_shared  multi-bin FFD of the shared fresh pool over ranks
+ *                    (free rows = column 0, free slots = column 2). */
+s3_status s3_admit_home(s3_ctx* ctx, s3_admit_report* rep, int64_t* admitted_ids);
+s3_status s3_admit_shared(s3_ctx* ctx, const int64_t* counters_all /* [world][S3_NCOUNTERS] */,
+                          s3_admit_report* rep, int64_t* admitted_ids);
+s3_status s3_counters_local(const s3_ctx* ctx, int64_t row[S3_NCOUNTERS]);
+
+/* ---- pure host planning helpers (no device work; callable without a GPU) */
+/* Single-bin FFD: admitted[i] = 1 if item i is admitted.  Returns count.  */
+int32_t s3_plan_ffd(int32_t n, const int64_t* cap, const int64_t* req_id, int64_t free_rows,
+                    int32_t max_items, uint8_t* admitted);
+/* Multi-bin FFD: rank[i] = bin or -1; free_rows / free_slots updated.      */
+int32_t s3_plan_ffd_multibin(int32_t n, const int64_t* cap, const int64_t* req_id, int32_t world,
+                             int64_t* free_rows, int64_t* free_slots, int32_t* rank);
+
+/* ---- views ------------------------------------------------------------ */
+typedef struct { int64_t req_id; int32_t prompt_len, gen_len, len, cap_rows; int64_t off; } s3_slot;
+s3_status s3_batch_size(const s3_ctx* ctx, int32_t* B);
+s3_status s3_batch_view(const s3_ctx* ctx, s3_slot* slots /* [B] */, int32_t* B);
+
+/* ---- timing of the two dominant kernels (CUDA events on cfg.stream) ----- */
+typedef struct {
+  int64_t kernel_launches;          /* every kernel this context launched (always counted) */
+  int64_t attn_launches, move_launches;
+  double attn_ms, move_ms;          /* summed kernel durations                   */
+  double attn_bytes, move_bytes;    /* algorithmic bytes of those launches        */
+} s3_profile;
+s3_status s3_profile_enable(s3_ctx* ctx, int32_t on);   /* also resets the sums */
+s3_status s3_profile_get(s3_ctx* ctx, s3_profile* prof); /* synchronises          */
+
+/* ---- synthetic stand-ins (harness, not the method) ---------------------
+ * s3_synth_inputs: the model's QKV projection + sampler stand-in; writes q,
+ * k_new, v_new for layers [l0, l0+nl) at position len_b of every slot from
+ * the counter-based generator and
+ * eos_b = (gen_b + 1 == out_len_by_req[req_b]).  out_len_by_req: device
+ * int32 [n_req] indexed by req_id.                                          */
+s3_status s3_synth_inputs(s3_ctx* ctx, int32_t l0, int32_t nl, const int32_t* out_len_by_req,
+                          int64_t n_req, void* q, void* k_new, void* v_new, uint8_t* eos);
+/* Counts resident arena rows (all layers, K and V) that differ from the
+ * generator (invariant P2).  Synchronises.                                  */
+s3_status s3_verify_resident(s3_ctx* ctx, int64_t* bad_rows);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* S3_H */

@@ -84,6 +84,7 @@ def lib():
             "s3o_admit_home": (i32, [P, P]),
             "s3o_admit_shared": (i32, [P, i32, i32, P, P, P]),
             "s3o_counters": (None, [P, P]),
+            "s3o_attend_generated": (None, [P, i64, i32, i32, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(_lib, name)
@@ -145,6 +146,15 @@ def gen_q(L, H, D, max_len, seed, req, l, pos) -> np.ndarray:
     cfg = Config(L, H, D, max_len, max_len, 1, seed)
     out = np.zeros(H * D, dtype=np.uint16)
     lib().s3o_gen_q(C.byref(cfg), req, l, pos, _p(out))
+    return out.reshape(H, D)
+
+
+def attend_generated(L, H, D, max_len, seed, req, pos, l) -> np.ndarray:
+    """fp64 attention of request req at position pos, layer l, when its rows
+    are the generator's (see s3o_attend_generated)."""
+    cfg = Config(L, H, D, max_len, max_len, 1, seed)
+    out = np.zeros(H * D, dtype=np.float64)
+    lib().s3o_attend_generated(C.byref(cfg), req, pos, l, _p(out))
     return out.reshape(H, D)
 
 

@@ -280,6 +280,34 @@ void s3o_make_inputs(const s3o_state* s, const int32_t* out_len_by_req, uint16_t
   }
 }
 
+/* softmax(q K^T / sqrt(D)) V for one layer, all heads, over n rows; row j's
+ * K (all heads) starts at K0 + j*stride, V likewise.       */
+static void attend(const uint16_t* q_hd, const uint16_t* K0, const uint16_t* V0, int64_t stride,
+                   int32_t n, int32_t H, int32_t D, double* sc, double* out_hd) {
+  const double inv_sqrt_d = 1.0 / sqrt((double)D);
+  for (int32_t h = 0; h < H; ++h) {
+    const uint16_t* qh = q_hd + (int64_t)h * D;
+    /* scores s_j = q . K_j / sqrt(D), j = 0..n-1 */
+    double m = -INFINITY;
+    for (int32_t j = 0; j < n; ++j) {
+      const uint16_t* kj = K0 + j * stride + (int64_t)h * D;
+      double acc = 0.0;
+      for (int32_t d = 0; d < D; ++d) acc += bf16_to_double(qh[d]) * bf16_to_double(kj[d]);
+      sc[j] = acc * inv_sqrt_d;
+      if (sc[j] > m) m = sc[j];
+    }
+    /* softmax weights and the weighted sum of V */
+    double den = 0.0;
+    for (int32_t j = 0; j < n; ++j) { sc[j] = exp(sc[j] - m); den += sc[j]; }
+    double* o = out_hd + (int64_t)h * D;
+    for (int32_t d = 0; d < D; ++d) {
+      double acc = 0.0;
+      for (int32_t j = 0; j < n; ++j) acc += sc[j] * bf16_to_double(V0[j * stride + (int64_t)h * D + d]);
+      o[d] = acc / den;
+    }
+  }
+}
+
 /* One decode iteration for every running sequence.
  *
  * PAPER.md:103-109 [§2.1]: h_out = softmax(q_i K^T / sqrt(d_h)) V.  Reading
@@ -294,7 +322,6 @@ int s3o_decode(s3o_state* s, const uint16_t* q, const uint16_t* k, const uint16_
   if (s->status_valid) return 5;  /* previous statuses not yet consumed */
   const int32_t H = s->c.H, D = s->c.D, L = s->c.L;
   const int64_t HD = (int64_t)H * D;
-  const double inv_sqrt_d = 1.0 / sqrt((double)D);
   double* sc = (double*)malloc(sizeof(double) * (size_t)(s->c.max_len + 1));
   for (int32_t b = 0; b < s->B; ++b) {
     s3o_slot* sl = &s->slots[b];
@@ -305,28 +332,9 @@ int s3o_decode(s3o_state* s, const uint16_t* q, const uint16_t* k, const uint16_
       /* append: row off+pos <- (k_new, v_new) */
       memcpy(row_ptr(s, sl->off + pos, l, 0), k + io, sizeof(uint16_t) * (size_t)HD);
       memcpy(row_ptr(s, sl->off + pos, l, 1), v + io, sizeof(uint16_t) * (size_t)HD);
-      for (int32_t h = 0; h < H; ++h) {
-        const uint16_t* qh = q + io + (int64_t)h * D;
-        /* scores s_j = q . K_j / sqrt(D), j = 0..pos */
-        double m = -INFINITY;
-        for (int32_t j = 0; j <= pos; ++j) {
-          const uint16_t* kj = row_ptr(s, sl->off + j, l, 0) + (int64_t)h * D;
-          double acc = 0.0;
-          for (int32_t d = 0; d < D; ++d) acc += bf16_to_double(qh[d]) * bf16_to_double(kj[d]);
-          sc[j] = acc * inv_sqrt_d;
-          if (sc[j] > m) m = sc[j];
-        }
-        /* softmax weights and weighted sum of V */
-        double den = 0.0;
-        for (int32_t j = 0; j <= pos; ++j) { sc[j] = exp(sc[j] - m); den += sc[j]; }
-        double* o = out + io + (int64_t)h * D;
-        for (int32_t d = 0; d < D; ++d) {
-          double acc = 0.0;
-          for (int32_t j = 0; j <= pos; ++j)
-            acc += sc[j] * bf16_to_double(row_ptr(s, sl->off + j, l, 1)[(int64_t)h * D + d]);
-          o[d] = acc / den;
-        }
-      }
+      /* attend over rows 0..pos (self included, R1) */
+      attend(q + io, row_ptr(s, sl->off, l, 0), row_ptr(s, sl->off, l, 1), s->row_elems, pos + 1,
+             H, D, sc, out + io);
     }
     sl->len += 1;
     sl->gen += 1;
@@ -553,4 +561,22 @@ void s3o_counters(const s3o_state* s, int64_t row[8]) {
   row[5] = s->finished_total;
   row[6] = s->evicted_total;
   row[7] = s->tokens_total;
+}
+
+/* Attention of request `req` at position `pos` of layer l when its rows are
+ * the generator's (invariant P2): K_j = G(req,l,0,j), V_j = G(req,l,1,j) for
+ * j = 0..pos, q = Q(req,l,pos).  Lets tests check sampled outputs of a
+ * full-size GPU run one at a time.  out: double [H][D].                    */
+void s3o_attend_generated(const s3o_config* c, int64_t req, int32_t pos, int32_t l, double* out_hd) {
+  const int64_t HD = (int64_t)c->H * c->D;
+  uint16_t* rows = (uint16_t*)malloc(sizeof(uint16_t) * (size_t)((pos + 1) * 2 * HD));
+  uint16_t* q = (uint16_t*)malloc(sizeof(uint16_t) * (size_t)HD);
+  double* sc = (double*)malloc(sizeof(double) * (size_t)(pos + 1));
+  for (int32_t j = 0; j <= pos; ++j) {
+    s3o_gen_kv(c, req, l, 0, j, rows + (int64_t)j * 2 * HD);
+    s3o_gen_kv(c, req, l, 1, j, rows + (int64_t)j * 2 * HD + HD);
+  }
+  s3o_gen_q(c, req, l, pos, q);
+  attend(q, rows, rows + HD, 2 * HD, pos + 1, c->H, c->D, sc, out_hd);
+  free(sc); free(q); free(rows);
 }

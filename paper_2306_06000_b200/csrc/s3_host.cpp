@@ -1,0 +1,812 @@
+// s3_host.cpp -- host control plane behind include/s3.h.
+//
+// Owns the request pool, the first-fit-decreasing scheduler
+// (PAPER.md:164-166), the supervisor's bookkeeping (free
+// capacity, eviction, doubling) and the host mirror of the slot table.  All
+// device work goes to the kernels in s3_kernels.cu on cfg.stream; eviction
+// D2H copies ride a side stream.  One host synchronisation per step: the
+// keep-scan report readback in s3_evict_compact.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <new>
+#include <vector>
+
+#include "../../include/s3.h"
+#include "s3_internal.h"
+
+using namespace s3;
+
+namespace {
+
+constexpr int64_t kAlign = 256;
+inline int64_t align_up(int64_t x, int64_t a = kAlign) { return (x + a - 1) / a * a; }
+
+// FFD order: reservation (cap) descending, then req_id ascending (R7).
+struct Key {
+  int64_t cap, req;
+  bool operator<(const Key& o) const { return cap != o.cap ? cap > o.cap : req < o.req; }
+};
+
+struct EventBox {
+  cudaEvent_t ev = nullptr;
+  EventBox() { cudaEventCreateWithFlags(&ev, cudaEventDisableTiming); }
+  ~EventBox() { if (ev) cudaEventDestroy(ev); }
+};
+
+struct Item {
+  int64_t req;
+  int32_t prompt, gen, cap;
+  int32_t evicted;          // 1: KV lives in host_store
+  int64_t host_off, host_bytes;
+  int32_t host_rows;
+  std::shared_ptr<EventBox> ready;   // D2H completion
+};
+
+using Pool = std::map<Key, Item>;
+
+// One-pass FFD with skip-and-continue, implemented as "repeatedly take the
+// first item in FFD order that fits": an item skipped once never fits later
+// because free capacity only shrinks.  fits(cap) -> bin index or -1;
+// max_fit() -> the largest cap any bin can take now.
+template <class MaxFit, class Fit, class Take>
+int64_t ffd_scan(Pool& pool, MaxFit max_fit, Fit fit, Take take) {
+  int64_t count = 0;
+  for (;;) {
+    const int64_t mf = max_fit();
+    if (mf <= 0) break;
+    auto it = pool.lower_bound(Key{mf, INT64_MIN});
+    if (it == pool.end()) break;
+    const int bin = fit(it->first.cap);
+    if (bin < 0) break;   // cannot happen: max_fit bounds it
+    Item item = it->second;
+    pool.erase(it);
+    take(bin, item);
+    ++count;
+  }
+  return count;
+}
+
+struct Prof {
+  bool on = false;
+  std::vector<cudaEvent_t> free_events;
+  struct Pending { cudaEvent_t a, b; double bytes; int kind; };
+  std::vector<Pending> pending;
+  int64_t attn_launches = 0, move_launches = 0;
+  double attn_ms = 0, move_ms = 0, attn_bytes = 0, move_bytes = 0;
+  cudaEvent_t get() {
+    if (!free_events.empty()) { cudaEvent_t e = free_events.back(); free_events.pop_back(); return e; }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
+
+}  // namespace
+
+struct s3_ctx {
+  s3_config cfg{};
+  Shape sh{};
+  int32_t C = 512;
+  int64_t S = 32768;
+  s3_buffers buf{};
+  cudaStream_t st = nullptr, side = nullptr;
+  int num_sms = 148;
+  int grid_attn = 148, grid_combine = 592, grid_move = 592;
+  // device carve
+  DSlot* slots[2] = {nullptr, nullptr};
+  int cur = 0;
+  Unit* units = nullptr;
+  Split* splits = nullptr;
+  float* partials = nullptr;
+  int32_t* ctrl = nullptr;
+  int64_t* ctrl64 = nullptr;
+  MoveEntry* entries = nullptr;
+  uint32_t* flags = nullptr;
+  uint8_t* report_dev = nullptr;
+  unsigned long long* verify_count = nullptr;
+  // pinned host
+  uint8_t* h_report = nullptr;
+  uint8_t* h_upload = nullptr;
+  int64_t upload_cap = 0, upload_used = 0;
+  // host mirror (arena order)
+  std::vector<DSlot> slots_h;
+  int64_t tail = 0;
+  // pools
+  Pool pool;        // world == 1: everything; world > 1: the shared fresh pool
+  Pool home;        // world > 1: this rank's evicted requests
+  int64_t n_evicted_waiting = 0;
+  // host store allocator (first fit) + deferred frees
+  std::map<int64_t, int64_t> free_blocks;
+  std::vector<std::pair<int64_t, int64_t>> deferred_free;
+  std::shared_ptr<EventBox> last_stage_d2h;
+  // state
+  bool status_pending = false;
+  uint32_t epoch = 0;
+  int64_t finished_total = 0, evicted_total = 0, tokens_total = 0;
+  int64_t launches = 0;     // kernels launched by this context
+  bool poisoned = false;
+  const char* err = "ok";
+  Prof prof;
+};
+
+namespace {
+
+s3_status fail(s3_ctx* c, s3_status s, const char* msg) {
+  if (c) {
+    c->err = msg;
+    if (s == S3_E_CUDA) c->poisoned = true;
+  }
+  return s;
+}
+
+#define CK(expr, msg)                                             \
+  do {                                                            \
+    cudaError_t e__ = (expr);                                     \
+    if (e__ != cudaSuccess) return fail(ctx, S3_E_CUDA, msg);     \
+  } while (0)
+
+bool validate(const s3_config* c) {
+  if (!c) return false;
+  if (c->num_layers < 1 || c->num_heads < 1) return false;
+  if (c->head_dim != 64 && c->head_dim != 128 && c->head_dim != 256) return false;
+  if ((int64_t)c->num_heads * c->head_dim > 8192) return false;
+  if (c->max_seq_len < 1 || c->arena_rows < c->max_seq_len) return false;
+  if (c->arena_rows > INT32_MAX) return false;
+  if (c->max_running < 1 || c->max_running > 65535) return false;
+  if (c->chunk_rows < 0 || c->move_chunk_bytes < 0 || c->move_chunk_bytes % 16) return false;
+  if (c->move_chunk_bytes > 0 && (c->move_chunk_bytes < 1024 || c->move_chunk_bytes > 196608)) return false;
+  if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return false;
+  return true;
+}
+
+Shape make_shape(const s3_config* c) {
+  Shape s;
+  s.L = c->num_layers; s.H = c->num_heads; s.D = c->head_dim; s.max_len = c->max_seq_len;
+  s.row_elems = 2LL * s.L * s.H * s.D;
+  s.kvpt = 4LL * s.L * s.H * s.D;
+  return s;
+}
+
+struct Carve {
+  int64_t slots, units, splits, partials, ctrl, ctrl64, entries, flags, report, verify, total;
+};
+
+Carve carve(const s3_config* c) {
+  const Shape sh = make_shape(c);
+  const int64_t C = c->chunk_rows ? c->chunk_rows : 512;
+  const int64_t S = c->move_chunk_bytes ? c->move_chunk_bytes : 32768;
+  const int64_t R = c->arena_rows, Bm = c->max_running;
+  const int64_t units_max = R / C + Bm + 2;
+  const int64_t parts_max = 2 * (R / C) + 2;
+  const int64_t flags_max = (R * sh.kvpt) / S + Bm + 2;
+  Carve k;
+  int64_t o = 0;
+  k.slots = o;    o += align_up(2 * Bm * (int64_t)sizeof(DSlot));
+  k.units = o;    o += align_up(units_max * (int64_t)sizeof(Unit));
+  k.splits = o;   o += align_up(Bm * (int64_t)sizeof(Split));
+  k.partials = o; o += align_up(parts_max * sh.L * sh.H * (int64_t)(sh.D + 4) * 4);
+  k.ctrl = o;     o += align_up(CTRL_WORDS * 4);
+  k.ctrl64 = o;   o += align_up(CTRL64_WORDS * 8);
+  k.entries = o;  o += align_up((Bm + 1) * (int64_t)sizeof(MoveEntry));
+  k.flags = o;    o += align_up(flags_max * 4);
+  k.report = o;   o += align_up(report_bytes((int32_t)Bm));
+  k.verify = o;   o += align_up(8);
+  k.total = o;
+  return k;
+}
+
+// ---- host store allocator -------------------------------------------------
+int64_t hs_alloc(s3_ctx* c, int64_t n) {
+  n = align_up(n);
+  for (auto it = c->free_blocks.begin(); it != c->free_blocks.end(); ++it) {
+    if (it->second >= n) {
+      const int64_t off = it->first, sz = it->second;
+      c->free_blocks.erase(it);
+      if (sz > n) c->free_blocks[off + n] = sz - n;
+      return off;
+    }
+  }
+  return -1;
+}
+
+void hs_free(s3_ctx* c, int64_t off, int64_t n) {
+  n = align_up(n);
+  auto it = c->free_blocks.emplace(off, n).first;
+  auto nx = std::next(it);
+  if (nx != c->free_blocks.end() && it->first + it->second == nx->first) {
+    it->second += nx->second;
+    c->free_blocks.erase(nx);
+  }
+  if (it != c->free_blocks.begin()) {
+    auto pv = std::prev(it);
+    if (pv->first + pv->second == it->first) {
+      pv->second += it->second;
+      c->free_blocks.erase(it);
+    }
+  }
+}
+
+void flush_deferred(s3_ctx* c) {   // call only when cfg.stream is idle
+  for (auto& p : c->deferred_free) hs_free(c, p.first, p.second);
+  c->deferred_free.clear();
+}
+
+void prof_collect(s3_ctx* c) {     // call only when cfg.stream is idle
+  for (auto& p : c->prof.pending) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, p.a, p.b);
+    if (p.kind == 0) { c->prof.attn_ms += ms; c->prof.attn_bytes += p.bytes; c->prof.attn_launches++; }
+    else { c->prof.move_ms += ms; c->prof.move_bytes += p.bytes; c->prof.move_launches++; }
+    c->prof.free_events.push_back(p.a);
+    c->prof.free_events.push_back(p.b);
+  }
+  c->prof.pending.clear();
+}
+
+uint8_t* upload_reserve(s3_ctx* c, int64_t n) {
+  n = align_up(n, 64);
+  if (c->upload_used + n > c->upload_cap) {
+    if (cudaStreamSynchronize(c->st) != cudaSuccess) return nullptr;
+    c->upload_used = 0;
+  }
+  uint8_t* p = c->h_upload + c->upload_used;
+  c->upload_used += n;
+  return p;
+}
+
+// Place admitted items at the tail (appended in scan order, R9):
+// fresh -> prompt rows by k_fill; evicted -> H2D reload after its D2H event.
+s3_status place_items(s3_ctx* ctx, const std::vector<Item>& items, s3_admit_report* rep,
+                      int64_t* admitted_ids) {
+  s3_admit_report r{};
+  if (!items.empty()) {
+    const int32_t B0 = (int32_t)ctx->slots_h.size();
+    const int32_t n = (int32_t)items.size();
+    uint8_t* up = upload_reserve(ctx, (int64_t)n * sizeof(DSlot) + (int64_t)n * 4 + 64);
+    if (!up) return fail(ctx, S3_E_CUDA, "upload sync failed");
+    DSlot* rec = reinterpret_cast<DSlot*>(up);
+    int32_t* fill = reinterpret_cast<int32_t*>(up + align_up((int64_t)n * sizeof(DSlot), 64));
+    int32_t n_fill = 0, max_prompt = 0;
+    for (int32_t i = 0; i < n; ++i) {
+      const Item& it = items[i];
+      DSlot s;
+      s.req = it.req; s.prompt = it.prompt; s.cap = it.cap; s.off = (int32_t)ctx->tail; s.status = 0;
+      if (it.evicted) {
+        s.gen = it.gen;
+        s.len = it.host_rows;
+        CK(cudaStreamWaitEvent(ctx->st, it.ready->ev, 0), "wait D2H event");
+        CK(cudaMemcpyAsync((uint8_t*)ctx->buf.arena + (int64_t)s.off * ctx->sh.kvpt,
+                           (uint8_t*)ctx->buf.host_store + it.host_off, it.host_bytes,
+                           cudaMemcpyHostToDevice, ctx->st), "reload H2D");
+        ctx->deferred_free.emplace_back(it.host_off, it.host_bytes);
+        ctx->n_evicted_waiting--;
+        r.n_reloaded++;
+        r.h2d_bytes += it.host_bytes;
+      } else {
+        s.gen = 0;
+        s.len = it.prompt;
+        fill[n_fill++] = B0 + i;
+        max_prompt = std::max(max_prompt, it.prompt);
+        r.n_fresh++;
+        r.fill_bytes += (int64_t)it.prompt * ctx->sh.kvpt;
+      }
+      rec[i] = s;
+      ctx->slots_h.push_back(s);
+      ctx->tail += it.cap;
+      if (admitted_ids) admitted_ids[i] = it.req;
+    }
+    DSlot* dst = ctx->slots[ctx->cur] + B0;
+    CK(cudaMemcpyAsync(dst, rec, (size_t)n * sizeof(DSlot), cudaMemcpyHostToDevice, ctx->st), "slot upload");
+    if (n_fill) {
+      int32_t* dfill = reinterpret_cast<int32_t*>(ctx->units);   // units are rebuilt every decode step
+      CK(cudaMemcpyAsync(dfill, fill, (size_t)n_fill * 4, cudaMemcpyHostToDevice, ctx->st), "fill upload");
+      CK(launch_fill(ctx->sh, ctx->cfg.synth_seed, ctx->slots[ctx->cur], dfill, n_fill, max_prompt,
+                     (uint16_t*)ctx->buf.arena, ctx->st), "k_fill");
+      ctx->launches += 1;
+    }
+    r.n_admitted = n;
+  }
+  r.n_batch = (int32_t)ctx->slots_h.size();
+  r.tail_rows = ctx->tail;
+  if (rep) *rep = r;
+  return S3_OK;
+}
+
+s3_status check_ctx(s3_ctx* ctx) {
+  if (!ctx) return S3_E_INVAL;
+  if (ctx->poisoned) return S3_E_CUDA;
+  return S3_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// ABI
+// ===========================================================================
+extern "C" {
+
+s3_status s3_workspace_query(const s3_config* cfg, int64_t* arena_b, int64_t* ws_b, int64_t* staging_min,
+                             int64_t* host_min) {
+  if (!validate(cfg)) return S3_E_INVAL;
+  const Shape sh = make_shape(cfg);
+  if (arena_b) *arena_b = cfg->arena_rows * sh.kvpt;
+  if (ws_b) *ws_b = carve(cfg).total;
+  if (staging_min) *staging_min = (int64_t)cfg->max_seq_len * sh.kvpt;
+  if (host_min) *host_min = align_up((int64_t)cfg->max_seq_len * sh.kvpt);
+  return S3_OK;
+}
+
+s3_status s3_kv_init(const s3_config* cfg, const s3_buffers* b, s3_ctx** out) {
+  if (!out || !b || !validate(cfg)) return S3_E_INVAL;
+  *out = nullptr;
+  const Shape sh = make_shape(cfg);
+  const Carve k = carve(cfg);
+  if (!b->arena || b->arena_bytes < cfg->arena_rows * sh.kvpt) return S3_E_NOMEM;
+  if (!b->workspace || b->workspace_bytes < k.total) return S3_E_NOMEM;
+  if (((uintptr_t)b->arena | (uintptr_t)b->workspace) % kAlign) return S3_E_INVAL;
+  if (b->staging && ((uintptr_t)b->staging % 16)) return S3_E_INVAL;
+  if (!b->host_store || b->host_store_bytes < 1) return S3_E_NOMEM;
+  s3_ctx* ctx = new (std::nothrow) s3_ctx();
+  if (!ctx) return S3_E_NOMEM;
+  ctx->cfg = *cfg;
+  ctx->sh = sh;
+  ctx->C = cfg->chunk_rows ? cfg->chunk_rows : 512;
+  ctx->S = cfg->move_chunk_bytes ? cfg->move_chunk_bytes : 32768;
+  ctx->buf = *b;
+  ctx->st = (cudaStream_t)cfg->stream;
+  auto bail = [&](const char* m) { ctx->err = m; s3_kv_destroy(ctx); return S3_E_CUDA; };
+  if (cudaSetDevice(cfg->device) != cudaSuccess) return bail("cudaSetDevice");
+  if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess) return bail("side stream");
+  int dev = cfg->device;
+  cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, dev);
+  int occ = 1;
+  const void* ka = attn_kernel_ptr(sh);
+  if (!ka) return bail("head_dim");
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ka, attn_block_threads(sh), 0);
+  ctx->grid_attn = ctx->num_sms * std::max(1, occ);
+  ctx->grid_combine = ctx->num_sms * 4;
+  if (ctx->S > 48 * 1024)
+    cudaFuncSetAttribute(move_kernel_ptr(), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->S);
+  int occm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occm, move_kernel_ptr(), 256, (size_t)ctx->S);
+  ctx->grid_move = ctx->num_sms * std::max(1, occm);
+  uint8_t* ws = (uint8_t*)b->workspace;
+  ctx->slots[0] = reinterpret_cast<DSlot*>(ws + k.slots);
+  ctx->slots[1] = ctx->slots[0] + cfg->max_running;
+  ctx->units = reinterpret_cast<Unit*>(ws + k.units);
+  ctx->splits = reinterpret_cast<Split*>(ws + k.splits);
+  ctx->partials = reinterpret_cast<float*>(ws + k.partials);
+  ctx->ctrl = reinterpret_cast<int32_t*>(ws + k.ctrl);
+  ctx->ctrl64 = reinterpret_cast<int64_t*>(ws + k.ctrl64);
+  ctx->entries = reinterpret_cast<MoveEntry*>(ws + k.entries);
+  ctx->flags = reinterpret_cast<uint32_t*>(ws + k.flags);
+  ctx->report_dev = ws + k.report;
+  ctx->verify_count = reinterpret_cast<unsigned long long*>(ws + k.verify);
+  if (cudaMemsetAsync(ws + k.ctrl, 0, CTRL_WORDS * 4, ctx->st) != cudaSuccess) return bail("memset");
+  if (cudaMemsetAsync(ws + k.flags, 0, (size_t)(k.report - k.flags), ctx->st) != cudaSuccess) return bail("memset");
+  const int64_t rb = report_bytes(cfg->max_running);
+  if (cudaHostAlloc((void**)&ctx->h_report, (size_t)rb, cudaHostAllocDefault) != cudaSuccess) return bail("pinned");
+  ctx->upload_cap = align_up(4 * ((int64_t)cfg->max_running * (sizeof(DSlot) + 4) + 4096));
+  if (cudaHostAlloc((void**)&ctx->h_upload, (size_t)ctx->upload_cap, cudaHostAllocDefault) != cudaSuccess)
+    return bail("pinned");
+  ctx->free_blocks[0] = b->host_store_bytes / kAlign * kAlign;
+  if (cudaStreamSynchronize(ctx->st) != cudaSuccess) return bail("sync");
+  *out = ctx;
+  return S3_OK;
+}
+
+s3_status s3_kv_destroy(s3_ctx* ctx) {
+  if (!ctx) return S3_E_INVAL;
+  if (ctx->st) cudaStreamSynchronize(ctx->st);
+  if (ctx->side) cudaStreamSynchronize(ctx->side);
+  ctx->pool.clear();
+  ctx->home.clear();
+  ctx->last_stage_d2h.reset();
+  for (auto& p : ctx->prof.pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
+  for (auto e : ctx->prof.free_events) cudaEventDestroy(e);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
+  if (ctx->h_report) cudaFreeHost(ctx->h_report);
+  if (ctx->h_upload) cudaFreeHost(ctx->h_upload);
+  delete ctx;
+  return S3_OK;
+}
+
+const char* s3_last_error(const s3_ctx* ctx) { return ctx ? ctx->err : "null context"; }
+
+s3_status s3_submit(s3_ctx* ctx, const s3_request* reqs, int32_t n) {
+  if (s3_status s = check_ctx(ctx)) return s;
+  if (n < 0 || (n > 0 && !reqs)) return fail(ctx, S3_E_INVAL, "submit: bad arguments");
+  for (int32_t i = 0; i < n; ++i) {
+    const s3_request& r = reqs[i];
+    if (r.prompt_len < 0 || r.alloc_out < 1 || (int64_t)r.prompt_len + r.alloc_out > ctx->cfg.max_seq_len)
+      return fail(ctx, S3_E_INVAL, "submit: bad request");
+    if ((int64_t)r.prompt_len + r.alloc_out > ctx->cfg.arena_rows)
+      return fail(ctx, S3_E_UNSCHEDULABLE, "submit: reservation larger than the arena");
+    if (ctx->pool.count(Key{(int64_t)r.prompt_len + r.alloc_out, r.req_id}))
+      return fail(ctx, S3_E_INVAL, "submit: duplicate request");
+  }
+  for (int32_t i = 0; i < n; ++i) {
+    const s3_request& r = reqs[i];
+    Item it{};
+    it.req = r.req_id; it.prompt = r.prompt_len; it.gen = 0; it.cap = r.prompt_len + r.alloc_out;
+    it.evicted = 0; it.host_off = -1;
+    ctx->pool.emplace(Key{it.cap, it.req}, it);
+  }
+  return S3_OK;
+}
+
+s3_status s3_decode_step(s3_ctx* ctx, int32_t l0, int32_t nl, const void* q, const void* k_new,
+                         const void* v_new, const uint8_t* eos, float* out) {
+  if (s3_status s = check_ctx(ctx)) return s;
+  if (ctx->status_pending) return fail(ctx, S3_E_STATE, "decode_step: statuses not consumed");
+  if (l0 < 0 || nl < 1 || l0 + nl > ctx->sh.L) return fail(ctx, S3_E_INVAL, "decode_step: layer range");
+  const bool finalize = (l0 + nl == ctx->sh.L);
+  const int32_t B = (int32_t)ctx->slots_h.size();
+  if (B > 0) {
+    if (!q || !k_new || !v_new || !out || (finalize && !eos)) return fail(ctx, S3_E_INVAL, "decode_step: null");
+    CK(launch_prep(ctx->sh, ctx->slots[ctx->cur], B, ctx->C, eos, finalize ? 1 : 0, ctx->units, ctx->splits,
+                   ctx->ctrl, ctx->st), "k_prep");
+    ctx->launches += 3;   // k_prep, k_attn, k_combine
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (ctx->prof.on) { e0 = ctx->prof.get(); e1 = ctx->prof.get(); cudaEventRecord(e0, ctx->st); }
+    CK(launch_attn(ctx->sh, (const uint16_t*)q, (const uint16_t*)k_new, (const uint16_t*)v_new,
+                   (uint16_t*)ctx->buf.arena, out, ctx->partials, ctx->units, ctx->splits, ctx->ctrl, B, l0, nl,
+                   ctx->grid_attn, ctx->grid_combine, ctx->st), "k_attn");
+    if (ctx->prof.on) {
+      cudaEventRecord(e1, ctx->st);
+      int64_t sum_len = 0;
+      for (const DSlot& s : ctx->slots_h) sum_len += s.len;
+      const double HD = (double)ctx->sh.H * ctx->sh.D;
+      // algorithmic bytes: prior rows K+V, new row write,
+      // k_new+v_new read, q read (bf16), out write (fp32)
+      const double bytes = nl * HD * (4.0 * (double)sum_len + 4.0 * B + 4.0 * B + 2.0 * B + 4.0 * B);
+      ctx->prof.pending.push_back({e0, e1, bytes, 0});
+    }
+  }
+  if (finalize) {
+    for (DSlot& s : ctx->slots_h) { s.len += 1; s.gen += 1; }
+    ctx->tokens_total += B;
+    ctx->status_pending = true;
+  }
+  return S3_OK;
+}
+
+s3_status s3_evict_compact(s3_ctx* ctx, s3_evict_report* rep, int32_t* perm, s3_evicted* evicted,
+                           int64_t* finished_ids) {
+  if (s3_status s = check_ctx(ctx)) return s;
+  if (!rep) return fail(ctx, S3_E_INVAL, "evict_compact: null report");
+  if (!ctx->status_pending) return fail(ctx, S3_E_STATE, "evict_compact: no completed decode step");
+  const int32_t B = (int32_t)ctx->slots_h.size();
+  s3_evict_report r{};
+  r.n_before = B;
+  r.first_hole = B;
+  if (B == 0) {
+    ctx->status_pending = false;
+    *rep = r;
+    return S3_OK;
+  }
+  const Shape& sh = ctx->sh;
+  CK(launch_keep_scan(sh, ctx->slots[ctx->cur], ctx->slots[1 - ctx->cur], B, ctx->S, ctx->report_dev,
+                      ctx->entries, ctx->ctrl64, ctx->st), "k_keep_scan");
+  ctx->launches += 1;
+  CK(cudaMemcpyAsync(ctx->h_report, ctx->report_dev, (size_t)report_bytes(B), cudaMemcpyDeviceToHost, ctx->st),
+     "report D2H");
+  CK(cudaStreamSynchronize(ctx->st), "report sync");
+  flush_deferred(ctx);
+  prof_collect(ctx);
+  ctx->upload_used = 0;
+  const DReportHeader* h = reinterpret_cast<const DReportHeader*>(ctx->h_report);
+  const int32_t* dperm = reinterpret_cast<const int32_t*>(ctx->h_report + report_perm_off(B));
+  const DEvicted* dev = reinterpret_cast<const DEvicted*>(ctx->h_report + report_ev_off(B));
+  const int64_t* dfin = reinterpret_cast<const int64_t*>(ctx->h_report + report_fin_off(B));
+  if (h->n_before != B || h->n_kept + h->n_finished + h->n_evicted != B)
+    return fail(ctx, S3_E_CUDA, "evict_compact: inconsistent device report");
+
+  // host store for every evictee (before any device move is enqueued)
+  std::vector<int64_t> hoff(h->n_evicted);
+  for (int32_t i = 0; i < h->n_evicted; ++i) {
+    hoff[i] = hs_alloc(ctx, (int64_t)dev[i].len * sh.kvpt);
+    if (hoff[i] < 0) return fail(ctx, S3_E_CUDA, "evict_compact: host store exhausted");
+  }
+  const bool staged = h->n_evicted > 0 && ctx->buf.staging && h->d2h_bytes <= ctx->buf.staging_bytes;
+  std::shared_ptr<EventBox> d2h_done;
+  if (h->n_evicted > 0) {
+    d2h_done = std::make_shared<EventBox>();
+    if (!staged) {
+      // synchronous fallback: copy straight from the arena before rows move
+      for (int32_t i = 0; i < h->n_evicted; ++i) {
+        const DSlot& s = ctx->slots_h[dev[i].b];
+        CK(cudaMemcpyAsync((uint8_t*)ctx->buf.host_store + hoff[i],
+                           (uint8_t*)ctx->buf.arena + (int64_t)s.off * sh.kvpt, (size_t)dev[i].len * sh.kvpt,
+                           cudaMemcpyDeviceToHost, ctx->st), "evict D2H (sync)");
+      }
+      CK(cudaEventRecord(d2h_done->ev, ctx->st), "event");
+    } else if (ctx->last_stage_d2h) {
+      // staging is reused: the previous step's D2H from it must be done
+      CK(cudaStreamWaitEvent(ctx->st, ctx->last_stage_d2h->ev, 0), "wait staging");
+    }
+  }
+  if (h->n_chunks > 0) {
+    ctx->epoch++;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (ctx->prof.on) { e0 = ctx->prof.get(); e1 = ctx->prof.get(); cudaEventRecord(e0, ctx->st); }
+    const int grid = (int)std::min<int64_t>(h->n_chunks, ctx->grid_move);
+    CK(launch_move((uint8_t*)ctx->buf.arena, (uint8_t*)ctx->buf.staging, ctx->entries, h->n_entries, h->n_chunks,
+                   ctx->S, ctx->ctrl64, ctx->flags, ctx->epoch, staged ? 1 : 0, grid, ctx->st), "k_move");
+    ctx->launches += 1;
+    if (ctx->prof.on) {
+      cudaEventRecord(e1, ctx->st);
+      const double bytes = 2.0 * (double)h->moved_bytes + (staged ? 2.0 * (double)h->d2h_bytes : 0.0);
+      ctx->prof.pending.push_back({e0, e1, bytes, 1});
+    }
+  }
+  if (staged) {
+    cudaEvent_t k4;
+    CK(cudaEventCreateWithFlags(&k4, cudaEventDisableTiming), "event");
+    CK(cudaEventRecord(k4, ctx->st), "event");
+    CK(cudaStreamWaitEvent(ctx->side, k4, 0), "side wait");
+    cudaEventDestroy(k4);
+    for (int32_t i = 0; i < h->n_evicted; ++i)
+      CK(cudaMemcpyAsync((uint8_t*)ctx->buf.host_store + hoff[i], (uint8_t*)ctx->buf.staging + dev[i].stage_off,
+                         (size_t)dev[i].len * sh.kvpt, cudaMemcpyDeviceToHost, ctx->side), "evict D2H");
+    CK(cudaEventRecord(d2h_done->ev, ctx->side), "event");
+    ctx->last_stage_d2h = d2h_done;
+  }
+  // requeue evicted requests with doubled reservation (R5), in batch order
+  int64_t pcie = 0;
+  for (int32_t i = 0; i < h->n_evicted; ++i) {
+    const DEvicted& e = dev[i];
+    Item it{};
+    it.req = e.req; it.prompt = e.prompt; it.gen = e.gen;
+    it.cap = std::min<int64_t>(2LL * e.cap, ctx->cfg.max_seq_len);
+    it.evicted = 1;
+    it.host_off = hoff[i];
+    it.host_bytes = (int64_t)e.len * sh.kvpt;
+    it.host_rows = e.len;
+    it.ready = d2h_done;
+    pcie += 2LL * e.cap * sh.kvpt;
+    (ctx->cfg.world > 1 ? ctx->home : ctx->pool).emplace(Key{it.cap, it.req}, it);
+    ctx->n_evicted_waiting++;
+    if (evicted) {
+      s3_evicted& o = evicted[i];
+      o.req_id = e.req; o.batch_index = e.b; o.prompt_len = e.prompt; o.gen_len = e.gen; o.len = e.len;
+      o.cap_rows = e.cap; o.new_cap_rows = it.cap; o.host_off = hoff[i];
+    }
+  }
+  // host mirror: stable compaction
+  std::vector<DSlot> kept;
+  kept.reserve(h->n_kept);
+  int64_t run = 0;
+  for (int32_t b = 0; b < B; ++b) {
+    if (dperm[b] >= 0) {
+      DSlot s = ctx->slots_h[b];
+      s.off = (int32_t)run;
+      run += s.cap;
+      kept.push_back(s);
+    }
+    if (perm) perm[b] = dperm[b];
+  }
+  if (run != h->tail || (int32_t)kept.size() != h->n_kept)
+    return fail(ctx, S3_E_CUDA, "evict_compact: host/device mirror mismatch");
+  ctx->slots_h.swap(kept);
+  ctx->tail = run;
+  ctx->cur = 1 - ctx->cur;
+  ctx->status_pending = false;
+  if (finished_ids) std::memcpy(finished_ids, dfin, sizeof(int64_t) * (size_t)h->n_finished);
+  ctx->finished_total += h->n_finished;
+  ctx->evicted_total += h->n_evicted;
+  r.n_finished = h->n_finished;
+  r.n_evicted = h->n_evicted;
+  r.n_kept = h->n_kept;
+  r.tail_rows = h->tail;
+  r.d2h_bytes = h->d2h_bytes;
+  r.moved_bytes = h->moved_bytes;
+  r.paper_pcie_bytes = pcie;
+  r.paper_hbm_bytes = h->hbm_bytes;
+  r.first_hole = h->first_hole;
+  r.sync_evict = (h->n_evicted > 0 && !staged) ? 1 : 0;
+  *rep = r;
+  return S3_OK;
+}
+
+s3_status s3_evict_wait(s3_ctx* ctx) {
+  if (s3_status s = check_ctx(ctx)) return s;
+  CK(cudaStreamSynchronize(ctx->side), "side sync");
+  CK(cudaStreamSynchronize(ctx->st), "sync");
+  flush_deferred(ctx);
+  return S3_OK;
+}
+
+s3_status s3_admit(s3_ctx* ctx, s3_admit_report* rep, int64_t* admitted_ids) {
+  if (s3_status s = check_ctx(ctx)) return s;
+  if (ctx->status_pending) return fail(ctx, S3_E_STATE, "admit: statuses not consumed");
+  if (ctx->cfg.world != 1) return fail(ctx, S3_E_STATE, "admit: world > 1 uses admit_home/admit_shared");
+  int64_t free_rows = ctx->cfg.arena_rows - ctx->tail;
+  int64_t slots_left = ctx->cfg.max_running - (int64_t)ctx->slots_h.size();
+  std::vector<Item> taken;
+  ffd_scan(
+      ctx->pool, [&] { return slots_left > 0 ? free_rows : 0; },
+      [&](int64_t cap) { return cap <= free_rows ? 0 : -1; },
+      [&](int, const Item& it) { free_rows -= it.cap; slots_left--; taken.push_back(it); });
+  return place_items(ctx, taken, rep, admitted_ids);
+}
+
+s3_status s3_admit_home(s3_ctx* ctx, s3_admit_report* rep, int64_t* admitted_ids) {
+  if (s3_status s = check_ctx(ctx)) return s;
+  if (ctx->status_pending) return fail(ctx, S3_E_STATE, "admit_home: statuses not consumed");
+  int64_t free_rows = ctx->cfg.arena_rows - ctx->tail;
+  int64_t slots_left = ctx->cfg.max_running - (int64_t)ctx->slots_h.size();
+  std::vector<Item> taken;
+  ffd_scan(
+      ctx->home, [&] { return slots_left > 0 ? free_rows : 0; },
+      [&](int64_t cap) { return cap <= free_rows ? 0 : -1; },
+      [&](int, const Item& it) { free_rows -= it.cap; slots_left--; taken.push_back(it); });
+  return place_items(ctx, taken, rep, admitted_ids);
+}
+
+s3_status s3_admit_shared(s3_ctx* ctx, const int64_t* counters_all, s3_admit_report* rep,
+                          int64_t* admitted_ids) {
+  if (s3_status s = check_ctx(ctx)) return s;
+  if (ctx->status_pending) return fail(ctx, S3_E_STATE, "admit_shared: statuses not consumed");
+  if (!counters_all) return fail(ctx, S3_E_INVAL, "admit_shared: null counters");
+  const int W = ctx->cfg.world;
+  std::vector<int64_t> fr(W), sl(W);
+  for (int r = 0; r < W; ++r) { fr[r] = counters_all[r * S3_NCOUNTERS + 0]; sl[r] = counters_all[r * S3_NCOUNTERS + 2]; }
+  if (fr[ctx->cfg.rank] != ctx->cfg.arena_rows - ctx->tail)
+    return fail(ctx, S3_E_STATE, "admit_shared: counters do not match this rank");
+  std::vector<Item> taken;
+  ffd_scan(
+      ctx->pool,
+      [&] {
+        int64_t m = 0;
+        for (int r = 0; r < W; ++r) if (sl[r] > 0) m = std::max(m, fr[r]);
+        return m;
+      },
+      [&](int64_t cap) {
+        for (int r = 0; r < W; ++r) if (sl[r] > 0 && cap <= fr[r]) return r;
+        return -1;
+      },
+      [&](int bin, const Item& it) {
+        fr[bin] -= it.cap;
+        sl[bin]--;
+        if (bin == ctx->cfg.rank) taken.push_back(it);
+      });
+  return place_items(ctx, taken, rep, admitted_ids);
+}
+
+s3_status s3_counters_local(const s3_ctx* ctx, int64_t row[S3_NCOUNTERS]) {
+  if (!ctx || !row) return S3_E_INVAL;
+  row[0] = ctx->cfg.arena_rows - ctx->tail;
+  row[1] = (int64_t)ctx->slots_h.size();
+  row[2] = ctx->cfg.max_running - (int64_t)ctx->slots_h.size();
+  row[3] = ctx->n_evicted_waiting;
+  row[4] = (int64_t)ctx->pool.size() - (ctx->cfg.world > 1 ? 0 : ctx->n_evicted_waiting);
+  row[5] = ctx->finished_total;
+  row[6] = ctx->evicted_total;
+  row[7] = ctx->tokens_total;
+  return S3_OK;
+}
+
+int32_t s3_plan_ffd(int32_t n, const int64_t* cap, const int64_t* req_id, int64_t free_rows, int32_t max_items,
+                    uint8_t* admitted) {
+  Pool pool;
+  std::map<int64_t, int32_t> idx;
+  for (int32_t i = 0; i < n; ++i) {
+    Item it{};
+    it.req = req_id[i]; it.cap = (int32_t)cap[i];
+    pool.emplace(Key{cap[i], req_id[i]}, it);
+    idx[req_id[i]] = i;
+    admitted[i] = 0;
+  }
+  int64_t left = max_items;
+  return (int32_t)ffd_scan(
+      pool, [&] { return left > 0 ? free_rows : 0; }, [&](int64_t c) { return c <= free_rows ? 0 : -1; },
+      [&](int, const Item& it) { free_rows -= it.cap; left--; admitted[idx[it.req]] = 1; });
+}
+
+int32_t s3_plan_ffd_multibin(int32_t n, const int64_t* cap, const int64_t* req_id, int32_t world,
+                             int64_t* free_rows, int64_t* free_slots, int32_t* rank) {
+  Pool pool;
+  std::map<int64_t, int32_t> idx;
+  for (int32_t i = 0; i < n; ++i) {
+    Item it{};
+    it.req = req_id[i]; it.cap = (int32_t)cap[i];
+    pool.emplace(Key{cap[i], req_id[i]}, it);
+    idx[req_id[i]] = i;
+    rank[i] = -1;
+  }
+  return (int32_t)ffd_scan(
+      pool,
+      [&] {
+        int64_t m = 0;
+        for (int r = 0; r < world; ++r) if (free_slots[r] > 0) m = std::max(m, free_rows[r]);
+        return m;
+      },
+      [&](int64_t c) {
+        for (int r = 0; r < world; ++r) if (free_slots[r] > 0 && c <= free_rows[r]) return r;
+        return -1;
+      },
+      [&](int bin, const Item& it) {
+        free_rows[bin] -= it.cap;
+        free_slots[bin]--;
+        rank[idx[it.req]] = bin;
+      });
+}
+
+s3_status s3_batch_size(const s3_ctx* ctx, int32_t* B) {
+  if (!ctx || !B) return S3_E_INVAL;
+  *B = (int32_t)ctx->slots_h.size();
+  return S3_OK;
+}
+
+s3_status s3_batch_view(const s3_ctx* ctx, s3_slot* slots, int32_t* B) {
+  if (!ctx || !B) return S3_E_INVAL;
+  *B = (int32_t)ctx->slots_h.size();
+  if (slots)
+    for (int32_t i = 0; i < *B; ++i) {
+      const DSlot& s = ctx->slots_h[i];
+      slots[i].req_id = s.req; slots[i].prompt_len = s.prompt; slots[i].gen_len = s.gen;
+      slots[i].len = s.len; slots[i].cap_rows = s.cap; slots[i].off = s.off;
+    }
+  return S3_OK;
+}
+
+s3_status s3_profile_enable(s3_ctx* ctx, int32_t on) {
+  if (s3_status s = check_ctx(ctx)) return s;
+  CK(cudaStreamSynchronize(ctx->st), "sync");
+  prof_collect(ctx);
+  ctx->prof.on = on != 0;
+  ctx->prof.attn_launches = ctx->prof.move_launches = 0;
+  ctx->prof.attn_ms = ctx->prof.move_ms = ctx->prof.attn_bytes = ctx->prof.move_bytes = 0;
+  return S3_OK;
+}
+
+s3_status s3_profile_get(s3_ctx* ctx, s3_profile* p) {
+  if (s3_status s = check_ctx(ctx)) return s;
+  if (!p) return fail(ctx, S3_E_INVAL, "profile_get: null");
+  CK(cudaStreamSynchronize(ctx->st), "sync");
+  prof_collect(ctx);
+  p->kernel_launches = ctx->launches;
+  p->attn_launches = ctx->prof.attn_launches;
+  p->move_launches = ctx->prof.move_launches;
+  p->attn_ms = ctx->prof.attn_ms;
+  p->move_ms = ctx->prof.move_ms;
+  p->attn_bytes = ctx->prof.attn_bytes;
+  p->move_bytes = ctx->prof.move_bytes;
+  return S3_OK;
+}
+
+s3_status s3_synth_inputs(s3_ctx* ctx, int32_t l0, int32_t nl, const int32_t* out_len_by_req, int64_t n_req,
+                          void* q, void* k_new, void* v_new, uint8_t* eos) {
+  if (s3_status s = check_ctx(ctx)) return s;
+  if (l0 < 0 || nl < 1 || l0 + nl > ctx->sh.L) return fail(ctx, S3_E_INVAL, "synth: layer range");
+  const int32_t B = (int32_t)ctx->slots_h.size();
+  if (B == 0) return S3_OK;
+  if (!q || !k_new || !v_new || !eos || !out_len_by_req) return fail(ctx, S3_E_INVAL, "synth: null");
+  CK(launch_synth(ctx->sh, ctx->cfg.synth_seed, ctx->slots[ctx->cur], B, l0, nl, out_len_by_req, n_req,
+                  (uint16_t*)q, (uint16_t*)k_new, (uint16_t*)v_new, eos, ctx->st), "k_synth");
+  ctx->launches += 1;
+  return S3_OK;
+}
+
+s3_status s3_verify_resident(s3_ctx* ctx, int64_t* bad) {
+  if (s3_status s = check_ctx(ctx)) return s;
+  if (!bad) return fail(ctx, S3_E_INVAL, "verify: null");
+  const int32_t B = (int32_t)ctx->slots_h.size();
+  CK(cudaMemsetAsync(ctx->verify_count, 0, 8, ctx->st), "memset");
+  CK(launch_verify(ctx->sh, ctx->cfg.synth_seed, ctx->slots[ctx->cur], B, (const uint16_t*)ctx->buf.arena,
+                   ctx->verify_count, ctx->st), "k_verify");
+  unsigned long long v = 0;
+  CK(cudaMemcpyAsync(&v, ctx->verify_count, 8, cudaMemcpyDeviceToHost, ctx->st), "D2H");
+  CK(cudaStreamSynchronize(ctx->st), "sync");
+  *bad = (int64_t)v;
+  return S3_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,99 @@
+// s3_internal.h -- shared between the host control plane (s3_host.cpp) and
+// the device kernels (s3_kernels.cu).  Not part of the public ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace s3 {
+
+// Device slot record (AoS, 32 B), kept in arena order.
+struct DSlot {
+  int64_t req;
+  int32_t prompt, gen, len, cap, off, status;
+};
+static_assert(sizeof(DSlot) == 32, "DSlot must be 32 B");
+
+// One attention work unit: rows [r0, r1) of slot b's resident rows, plus the
+// new (appended) row when has_new.  part < 0: the unit covers the whole slot
+// and writes `out` directly; else it writes partial (m, l, acc) record `part`.
+struct Unit {
+  int32_t b, r0, r1, part;
+  int32_t off, len, has_new, pad;
+};
+static_assert(sizeof(Unit) == 32, "Unit must be 32 B");
+
+struct Split {          // a slot whose attention is split over k units
+  int32_t b, part0, k, pad;
+};
+
+enum { MOVE_ARENA = 0, MOVE_STAGE = 1 };
+struct MoveEntry {      // one contiguous byte range to move, sources in arena order
+  int64_t src, dst, bytes, chunk0;
+  int32_t kind, pad0;
+  int64_t pad1;
+};
+static_assert(sizeof(MoveEntry) == 48, "MoveEntry must be 48 B");
+
+// ctrl words (int32 unless noted)
+enum { CTRL_N_UNITS = 0, CTRL_N_SPLITS = 1, CTRL_ITEM = 2, CTRL_SPLIT_ITEM = 3, CTRL_WORDS = 16 };
+// int64 ctrl words (separate array)
+enum { CTRL64_TICKET = 0, CTRL64_N_CHUNKS = 1, CTRL64_WORDS = 8 };
+
+// Packed report written by the keep-scan kernel; header then, for the
+// pre-compaction batch size B: perm int32[B] | DEvicted[B] | int64 fin[B].
+struct DReportHeader {
+  int32_t n_before, n_finished, n_evicted, n_kept;
+  int64_t tail, d2h_bytes, moved_bytes, pcie_bytes, hbm_bytes;
+  int64_t n_chunks;
+  int32_t n_entries, first_hole;
+  int64_t pad[7];
+};
+static_assert(sizeof(DReportHeader) == 128, "header 128 B");
+struct DEvicted {
+  int64_t req;
+  int32_t b, prompt, gen, len, cap, pad;
+  int64_t stage_off;
+};
+static_assert(sizeof(DEvicted) == 40, "DEvicted 40 B");
+
+#ifdef __CUDACC__
+#define S3_HD __host__ __device__
+#else
+#define S3_HD
+#endif
+S3_HD inline int64_t report_perm_off(int32_t) { return sizeof(DReportHeader); }
+S3_HD inline int64_t report_ev_off(int32_t B) { return (sizeof(DReportHeader) + 4 * (int64_t)B + 15) / 16 * 16; }
+S3_HD inline int64_t report_fin_off(int32_t B) { return report_ev_off(B) + (int64_t)sizeof(DEvicted) * B; }
+S3_HD inline int64_t report_bytes(int32_t B) { return report_fin_off(B) + 8 * (int64_t)B; }
+
+struct Shape {
+  int32_t L, H, D, max_len;
+  int64_t row_elems;     // 2*L*H*D bf16 elements per token row
+  int64_t kvpt;          // bytes per token row
+};
+
+// ---- kernel launchers (s3_kernels.cu) ----------------------------------
+cudaError_t launch_prep(const Shape& sh, DSlot* slots, int32_t B, int32_t C, const uint8_t* eos,
+                        int32_t finalize, Unit* units, Split* splits, int32_t* ctrl, cudaStream_t st);
+cudaError_t launch_attn(const Shape& sh, const uint16_t* q, const uint16_t* k_new, const uint16_t* v_new,
+                        uint16_t* arena, float* out, float* partials, const Unit* units,
+                        const Split* splits, int32_t* ctrl, int32_t B, int32_t l0, int32_t nl,
+                        int32_t grid_attn, int32_t grid_combine, cudaStream_t st);
+cudaError_t launch_keep_scan(const Shape& sh, const DSlot* cur, DSlot* next, int32_t B, int64_t S,
+                             void* report, MoveEntry* entries, int64_t* ctrl64, cudaStream_t st);
+cudaError_t launch_move(uint8_t* arena, uint8_t* staging, const MoveEntry* entries, int32_t n_entries,
+                        int64_t n_chunks, int64_t S, int64_t* ctrl64, uint32_t* flags, uint32_t epoch,
+                        int32_t staging_enabled, int32_t grid, cudaStream_t st);
+cudaError_t launch_fill(const Shape& sh, uint64_t seed, const DSlot* slots, const int32_t* list,
+                        int32_t n, int32_t max_prompt, uint16_t* arena, cudaStream_t st);
+cudaError_t launch_synth(const Shape& sh, uint64_t seed, const DSlot* slots, int32_t B, int32_t l0,
+                         int32_t nl, const int32_t* out_len_by_req, int64_t n_req, uint16_t* q,
+                         uint16_t* k, uint16_t* v, uint8_t* eos, cudaStream_t st);
+cudaError_t launch_verify(const Shape& sh, uint64_t seed, const DSlot* slots, int32_t B,
+                          const uint16_t* arena, unsigned long long* bad, cudaStream_t st);
+
+int attn_block_threads(const Shape& sh);
+const void* attn_kernel_ptr(const Shape& sh);
+const void* move_kernel_ptr();
+
+}  // namespace s3

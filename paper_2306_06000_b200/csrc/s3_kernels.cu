@@ -1,0 +1,769 @@
+// s3_kernels.cu -- sm_100a device kernels of the S^3 decode step.
+//
+//   k_prep       per-step work list (split-K units over each slot's rows) and
+//                the overrun/finish detection epilogue
+//   k_attn       length-masked decode attention + KV append
+//   k_combine    merge of split-K partials
+//   k_keep_scan  keep flags -> prefix sums -> new offsets, permutation,
+//                eviction list, move list
+//   k_move       ordered in-place row-shift compaction (+ eviction staging)
+//   k_fill       prompt-row fill for fresh admissions (prefill stand-in)
+//   k_synth      q / k_new / v_new / eos stand-in (harness)
+//   k_verify     resident rows == generator (invariant P2, tests)
+//
+// Design notes are in DESIGN.md ("Kernels").  Everything here is HBM-bound
+// integer / fp32-FMA work: decode attention has M = 1 per head (MHA), so the
+// tensor cores have nothing to contract.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "s3_internal.h"
+
+namespace s3 {
+
+// ---------------------------------------------------------------------------
+// small PTX helpers
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint4 ld_stream(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ uint4 ld_plain(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_v4(void* p, uint4 v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void unpack8(uint4 u, float (&f)[8]) {
+  f[0] = __uint_as_float(u.x << 16); f[1] = __uint_as_float(u.x & 0xffff0000u);
+  f[2] = __uint_as_float(u.y << 16); f[3] = __uint_as_float(u.y & 0xffff0000u);
+  f[4] = __uint_as_float(u.z << 16); f[5] = __uint_as_float(u.z & 0xffff0000u);
+  f[6] = __uint_as_float(u.w << 16); f[7] = __uint_as_float(u.w & 0xffff0000u);
+}
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Block-wide exclusive scan of NV int64 values per thread (1024 threads max).
+// ---------------------------------------------------------------------------
+template <int NV>
+__device__ void block_excl_scan(long long (&x)[NV], long long (&total)[NV]) {
+  __shared__ long long warp_sums[32][NV];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarps = (blockDim.x + 31) >> 5;
+  long long incl[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    long long v = x[i];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      long long n = __shfl_up_sync(0xffffffffu, v, o);
+      if (lane >= o) v += n;
+    }
+    incl[i] = v;
+  }
+  if (lane == 31)
+#pragma unroll
+    for (int i = 0; i < NV; ++i) warp_sums[warp][i] = incl[i];
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      long long v = lane < nwarps ? warp_sums[lane][i] : 0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        long long n = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += n;
+      }
+      if (lane < nwarps) warp_sums[lane][i] = v;   // inclusive over warps
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    long long before = warp == 0 ? 0 : warp_sums[warp - 1][i];
+    total[i] = warp_sums[nwarps - 1][i];
+    x[i] = before + incl[i] - x[i];
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// Counter-based generator
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+// 8 bf16 values (one 16-byte vector) for element group d8 of (req,l,kv,pos,h).
+__device__ __forceinline__ uint4 gen8(const Shape& sh, uint64_t seed, uint64_t tag, int64_t req,
+                                      int l, int kv, int pos, int h, int d8, float scale) {
+  const uint64_t g =
+      (((((uint64_t)req * sh.L + l) * 2u + kv) * (uint64_t)sh.max_len + pos) * sh.H + h) *
+          (uint64_t)(sh.D / 8) + d8;
+  const uint64_t z = splitmix64(seed ^ (tag << 60) ^ g);
+  uint32_t w[4];
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const int k0 = (int)((z >> (16 * p)) & 0xFF) - 128;
+    const int k1 = (int)((z >> (16 * p + 8)) & 0xFF) - 128;
+    const uint32_t b0 = __float_as_uint((float)k0 * scale) >> 16;
+    const uint32_t b1 = __float_as_uint((float)k1 * scale) >> 16;
+    w[p] = b0 | (b1 << 16);
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// ---------------------------------------------------------------------------
+// k_prep: work list + detection.  One CTA of 1024 threads; B is small
+// (<= max_running), this runs in a few microseconds.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_prep(DSlot* __restrict__ slots, int32_t B, int32_t C,
+                                               const uint8_t* __restrict__ eos, int32_t finalize,
+                                               Unit* __restrict__ units, Split* __restrict__ splits,
+                                               int32_t* __restrict__ ctrl) {
+  const int per = (B + blockDim.x - 1) / blockDim.x;
+  const int b0 = threadIdx.x * per, b1 = min(B, b0 + per);
+  long long x[3] = {0, 0, 0};  // units, splits, parts
+  for (int b = b0; b < b1; ++b) {
+    const int k = (slots[b].len + 1 + C - 1) / C;
+    x[0] += k;
+    x[1] += k > 1;
+    x[2] += k > 1 ? k : 0;
+  }
+  long long tot[3];
+  block_excl_scan<3>(x, tot);
+  long long u = x[0], s = x[1], p = x[2];
+  for (int b = b0; b < b1; ++b) {
+    DSlot sl = slots[b];
+    const int k = (sl.len + 1 + C - 1) / C;
+    for (int i = 0; i < k; ++i) {
+      Unit un;
+      un.b = b;
+      un.r0 = i * C;
+      un.r1 = min((i + 1) * C, sl.len);
+      un.part = k > 1 ? (int)(p + i) : -1;
+      un.off = sl.off;
+      un.len = sl.len;
+      un.has_new = (i == k - 1);
+      un.pad = 0;
+      units[u + i] = un;
+    }
+    if (k > 1) {
+      Split sp;
+      sp.b = b; sp.part0 = (int)p; sp.k = k; sp.pad = 0;
+      splits[s] = sp;
+      ++s;
+      p += k;
+    }
+    u += k;
+    if (finalize) {
+      sl.len += 1;
+      sl.gen += 1;
+      sl.status = eos[b] ? 1 : (sl.len == sl.cap ? 2 : 0);
+      slots[b] = sl;
+    }
+  }
+  if (threadIdx.x == 0) {
+    ctrl[CTRL_N_UNITS] = (int)tot[0];
+    ctrl[CTRL_N_SPLITS] = (int)tot[1];
+    ctrl[CTRL_ITEM] = 0;
+    ctrl[CTRL_SPLIT_ITEM] = 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_attn: persistent, dynamically scheduled over items (unit, layer).
+// Each head is served by D/8 lanes; each lane owns 8 consecutive elements of
+// the head (one 16-byte vector of K and of V per row).  Rows are streamed in
+// groups of G with the next group's loads in flight while the current group
+// is reduced: scores via lane-group xor shuffles, then an online softmax in
+// the log2 domain (q is pre-scaled by log2(e)/sqrt(D)).
+// ---------------------------------------------------------------------------
+struct AttnArgs {
+  Shape sh;
+  const uint16_t* q;
+  const uint16_t* k_new;
+  const uint16_t* v_new;
+  uint16_t* arena;
+  float* out;
+  float* partials;
+  const Unit* units;
+  int32_t* ctrl;
+  int32_t B, l0, nl;
+  float qscale;
+};
+
+template <int D, int G>
+__device__ __forceinline__ void attn_rows(const uint4 (&kc)[G], const uint4 (&vc)[G], int nvalid,
+                                          const float (&qf)[8], float& m, float& s, float (&acc)[8]) {
+  constexpr int LPH = D / 8;
+  float sc[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    float kf[8];
+    unpack8(kc[g], kf);
+    float d = 0.f;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) d = fmaf(qf[e], kf[e], d);
+    sc[g] = d;
+  }
+#pragma unroll
+  for (int o = LPH / 2; o > 0; o >>= 1)
+#pragma unroll
+    for (int g = 0; g < G; ++g) sc[g] += __shfl_xor_sync(0xffffffffu, sc[g], o);
+  float mx = m;
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    if (g >= nvalid) sc[g] = -INFINITY;
+    mx = fmaxf(mx, sc[g]);
+  }
+  const float corr = ex2(m - mx);
+  s *= corr;
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] *= corr;
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const float pr = ex2(sc[g] - mx);
+    float vf[8];
+    unpack8(vc[g], vf);
+    s += pr;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = fmaf(pr, vf[e], acc[e]);
+  }
+  m = mx;
+}
+
+template <int D>
+__global__ void __launch_bounds__(512, 1) k_attn(AttnArgs a) {
+  constexpr int LPH = D / 8;    // lanes per head
+  constexpr int HPW = 32 / LPH; // heads per warp
+  constexpr int G = 4;          // rows per group
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int head = warp * HPW + lane / LPH;
+  const int sub = lane % LPH;
+  const int H = a.sh.H;
+  const bool active = head < H;
+  const int hh = active ? head : H - 1;
+  const int64_t HD = (int64_t)H * D;
+  const int64_t rowE = a.sh.row_elems;
+  __shared__ int s_item;
+  const int n_units = a.ctrl[CTRL_N_UNITS];
+  const int total = n_units * a.nl;
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(&a.ctrl[CTRL_ITEM], 1);
+    __syncthreads();
+    const int item = s_item;
+    __syncthreads();
+    if (item >= total) break;
+    const int u = item / a.nl;
+    const int li = item - u * a.nl;
+    const int l = a.l0 + li;
+    const Unit un = a.units[u];
+    const uint16_t* kbase = a.arena + (int64_t)un.off * rowE + (int64_t)l * 2 * HD + hh * D + sub * 8;
+    const uint16_t* vbase = kbase + HD;
+    const int64_t io = ((int64_t)li * a.B + un.b) * HD + hh * D + sub * 8;
+    float qf[8];
+    unpack8(ld_plain(a.q + io), qf);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) qf[e] *= a.qscale;
+    float m = -INFINITY, s = 0.f, acc[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+
+    uint4 kc[G], vc[G];
+    int j = un.r0;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const bool ok = j + g < un.r1;
+      kc[g] = ok ? ld_stream(kbase + (int64_t)(j + g) * rowE) : make_uint4(0, 0, 0, 0);
+      vc[g] = ok ? ld_stream(vbase + (int64_t)(j + g) * rowE) : make_uint4(0, 0, 0, 0);
+    }
+    while (j < un.r1) {
+      const int jn = j + G;
+      uint4 kn[G], vn[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const bool ok = jn + g < un.r1;
+        kn[g] = ok ? ld_stream(kbase + (int64_t)(jn + g) * rowE) : make_uint4(0, 0, 0, 0);
+        vn[g] = ok ? ld_stream(vbase + (int64_t)(jn + g) * rowE) : make_uint4(0, 0, 0, 0);
+      }
+      attn_rows<D, G>(kc, vc, min(G, un.r1 - j), qf, m, s, acc);
+#pragma unroll
+      for (int g = 0; g < G; ++g) { kc[g] = kn[g]; vc[g] = vn[g]; }
+      j = jn;
+    }
+    if (un.has_new) {
+      // append: row off+len <- (k_new, v_new), and attend to it from registers
+      const uint4 kr = ld_plain(a.k_new + io);
+      const uint4 vr = ld_plain(a.v_new + io);
+      if (active) {
+        st_v4((void*)(kbase + (int64_t)un.len * rowE), kr);
+        st_v4((void*)(vbase + (int64_t)un.len * rowE), vr);
+      }
+      uint4 k1[1] = {kr}, v1[1] = {vr};
+      attn_rows<D, 1>(k1, v1, 1, qf, m, s, acc);
+    }
+    if (active) {
+      if (un.part < 0) {
+        const float inv = 1.f / s;
+        float4* o = reinterpret_cast<float4*>(a.out + io);
+        o[0] = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+        o[1] = make_float4(acc[4] * inv, acc[5] * inv, acc[6] * inv, acc[7] * inv);
+      } else {
+        float* pr = a.partials + (((int64_t)un.part * a.nl + li) * H + hh) * (D + 4);
+        float4* o = reinterpret_cast<float4*>(pr + sub * 8);
+        o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+        o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+        if (sub == 0) { pr[D] = m; pr[D + 1] = s; }
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_combine: out = sum_i 2^(m_i - M) acc_i / sum_i 2^(m_i - M) l_i
+// ---------------------------------------------------------------------------
+template <int D>
+__global__ void __launch_bounds__(256) k_combine(const Split* __restrict__ splits,
+                                                 const float* __restrict__ partials,
+                                                 float* __restrict__ out, int32_t* ctrl, int32_t H,
+                                                 int32_t B, int32_t nl) {
+  constexpr int EPL = D / 32;   // elements per lane
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __shared__ int s_item;
+  const int total = ctrl[CTRL_N_SPLITS] * nl;
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(&ctrl[CTRL_SPLIT_ITEM], 1);
+    __syncthreads();
+    const int item = s_item;
+    __syncthreads();
+    if (item >= total) break;
+    const Split sp = splits[item / nl];
+    const int li = item % nl;
+    for (int h = warp; h < H; h += nw) {
+      float M = -INFINITY;
+      for (int i = 0; i < sp.k; ++i)
+        M = fmaxf(M, partials[(((int64_t)(sp.part0 + i) * nl + li) * H + h) * (D + 4) + D]);
+      float acc[EPL], L = 0.f;
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) acc[e] = 0.f;
+      for (int i = 0; i < sp.k; ++i) {
+        const float* pr = partials + (((int64_t)(sp.part0 + i) * nl + li) * H + h) * (D + 4);
+        const float w = ex2(pr[D] - M);
+        L += w * pr[D + 1];
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) acc[e] = fmaf(w, pr[lane * EPL + e], acc[e]);
+      }
+      const float inv = 1.f / L;
+      float* o = out + (((int64_t)li * B + sp.b) * H + h) * D + lane * EPL;
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) o[e] = acc[e] * inv;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_keep_scan: one CTA.  keep_b = (status == RUNNING); exclusive scans give
+// new_idx, new_off (= sum of kept caps before b), evicted index and staging
+// offset, finished index; a second scan numbers the move entries (moved
+// survivors and evicted slots, in arena order) and their chunks.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_keep_scan(Shape sh, const DSlot* __restrict__ cur,
+                                                    DSlot* __restrict__ next, int32_t B, int64_t S,
+                                                    uint8_t* __restrict__ report,
+                                                    MoveEntry* __restrict__ entries,
+                                                    int64_t* __restrict__ ctrl64) {
+  __shared__ int s_first_hole;
+  __shared__ unsigned long long s_hbm;
+  if (threadIdx.x == 0) { s_first_hole = B; s_hbm = 0; }
+  const int per = (B + blockDim.x - 1) / blockDim.x;
+  const int b0 = threadIdx.x * per, b1 = min(B, b0 + per);
+  const int64_t kvpt = sh.kvpt;
+  // pass A: keep, keep*cap, fin, ev, ev*len*kvpt, cap, ev*cap
+  long long x[6] = {0, 0, 0, 0, 0, 0};
+  for (int b = b0; b < b1; ++b) {
+    const DSlot sl = cur[b];
+    const int keep = sl.status == 0, fin = sl.status == 1, ev = sl.status == 2;
+    x[0] += keep;
+    x[1] += keep ? sl.cap : 0;
+    x[2] += fin;
+    x[3] += ev;
+    x[4] += ev ? (long long)sl.len * kvpt : 0;
+    x[5] += sl.cap;
+  }
+  long long tot[6];
+  block_excl_scan<6>(x, tot);
+  int32_t* perm = reinterpret_cast<int32_t*>(report + report_perm_off(B));
+  DEvicted* evl = reinterpret_cast<DEvicted*>(report + report_ev_off(B));
+  int64_t* finl = reinterpret_cast<int64_t*>(report + report_fin_off(B));
+  // pass B: move entries
+  long long y[3] = {0, 0, 0};   // entries, chunks, moved bytes
+  {
+    long long keep_i = x[0], keepcap = x[1], fin_i = x[2], ev_i = x[3], evb = x[4], capx = x[5];
+    unsigned long long hbm = 0;
+    int first = B;
+    for (int b = b0; b < b1; ++b) {
+      DSlot sl = cur[b];
+      const int keep = sl.status == 0;
+      if (!keep && b < first) first = b;
+      if (keep) {
+        perm[b] = (int)keep_i;
+        const int64_t new_off = keepcap;
+        const int64_t bytes = (int64_t)sl.len * kvpt;
+        if (new_off != sl.off && bytes > 0) { y[0] += 1; y[1] += (bytes + S - 1) / S; y[2] += bytes; }
+        sl.off = (int32_t)new_off;
+        sl.status = 0;
+        next[keep_i] = sl;
+        ++keep_i;
+        keepcap += sl.cap;
+      } else {
+        perm[b] = -1;
+        if (sl.status == 1) {
+          finl[fin_i++] = sl.req;
+        } else {
+          const int64_t bytes = (int64_t)sl.len * kvpt;
+          DEvicted e;
+          e.req = sl.req; e.b = b; e.prompt = sl.prompt; e.gen = sl.gen; e.len = sl.len;
+          e.cap = sl.cap; e.pad = 0; e.stage_off = evb;
+          evl[ev_i++] = e;
+          evb += bytes;
+          hbm += 2ull * (unsigned long long)(tot[5] - capx - sl.cap) * (unsigned long long)kvpt;
+          if (bytes > 0) { y[0] += 1; y[1] += (bytes + S - 1) / S; }
+        }
+      }
+      capx += sl.cap;
+    }
+    if (first < B) atomicMin(&s_first_hole, first);
+    if (hbm) atomicAdd(&s_hbm, hbm);
+  }
+  long long ytot[3];
+  block_excl_scan<3>(y, ytot);
+  {
+    long long e_i = y[0], chunk = y[1];
+    long long keepcap = x[1], evb = x[4];
+    for (int b = b0; b < b1; ++b) {
+      const DSlot sl = cur[b];
+      const int64_t bytes = (int64_t)sl.len * kvpt;
+      if (sl.status == 0) {
+        const int64_t new_off = keepcap;
+        if (new_off != sl.off && bytes > 0) {
+          MoveEntry me;
+          me.src = (int64_t)sl.off * kvpt; me.dst = new_off * kvpt; me.bytes = bytes;
+          me.chunk0 = chunk; me.kind = MOVE_ARENA; me.pad0 = 0; me.pad1 = 0;
+          entries[e_i++] = me;
+          chunk += (bytes + S - 1) / S;
+        }
+        keepcap += sl.cap;
+      } else if (sl.status == 2) {
+        if (bytes > 0) {
+          MoveEntry me;
+          me.src = (int64_t)sl.off * kvpt; me.dst = evb; me.bytes = bytes;
+          me.chunk0 = chunk; me.kind = MOVE_STAGE; me.pad0 = 0; me.pad1 = 0;
+          entries[e_i++] = me;
+          chunk += (bytes + S - 1) / S;
+        }
+        evb += bytes;
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    DReportHeader* h = reinterpret_cast<DReportHeader*>(report);
+    h->n_before = B;
+    h->n_finished = (int)tot[2];
+    h->n_evicted = (int)tot[3];
+    h->n_kept = (int)tot[0];
+    h->tail = tot[1];
+    h->d2h_bytes = tot[4];
+    h->moved_bytes = ytot[2];
+    h->pcie_bytes = 0;
+    h->hbm_bytes = (int64_t)s_hbm;
+    h->n_chunks = ytot[1];
+    h->n_entries = (int)ytot[0];
+    h->first_hole = s_first_hole;
+    ctrl64[CTRL64_TICKET] = 0;
+    ctrl64[CTRL64_N_CHUNKS] = ytot[1];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_move: ordered in-place compaction.  Chunks (S bytes) are numbered in
+// source order (= arena order); a CTA takes chunk tickets in that order,
+// reads its chunk into shared memory, publishes "read done", then -- only for
+// arena destinations -- waits until every chunk whose SOURCE overlaps its
+// DESTINATION has been read, and writes.  Every source lies at or above its
+// destination, so those chunks all hold earlier tickets and never wait on
+// later ones: no deadlock.  Evicted slots are chunks
+// too (copied to the staging buffer), so survivors never overwrite an
+// evicted row before it has been staged.
+// ---------------------------------------------------------------------------
+__device__ int find_entry(const MoveEntry* __restrict__ e, int n, int64_t t) {
+  int lo = 0, hi = n - 1;               // largest i with chunk0 <= t
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (e[mid].chunk0 <= t) lo = mid; else hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ void wait_sources(const MoveEntry* __restrict__ e, int n, int64_t S, int64_t d0,
+                             int64_t d1, int64_t self, const uint32_t* flags, uint32_t epoch) {
+  int lo = 0, hi = n;                   // first entry with src + bytes > d0
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (e[mid].src + e[mid].bytes > d0) hi = mid; else lo = mid + 1;
+  }
+  for (int i = lo; i < n && e[i].src < d1; ++i) {
+    const int64_t src = e[i].src, nch = (e[i].bytes + S - 1) / S;
+    const int64_t c_lo = d0 > src ? (d0 - src) / S : 0;
+    const int64_t c_hi = min(nch - 1, (d1 - 1 - src) / S);
+    for (int64_t c = c_lo; c <= c_hi; ++c) {
+      const int64_t k = e[i].chunk0 + c;
+      if (k == self) continue;
+      while (ld_acquire_u32(flags + k) != epoch) __nanosleep(64);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) k_move(uint8_t* __restrict__ arena, uint8_t* __restrict__ staging,
+                                              const MoveEntry* __restrict__ entries, int32_t n_entries,
+                                              int64_t n_chunks, int64_t S, int64_t* ctrl64,
+                                              uint32_t* flags, uint32_t epoch, int32_t staging_enabled) {
+  extern __shared__ uint4 buf[];
+  __shared__ long long s_t;
+  __shared__ int s_e;
+  for (;;) {
+    if (threadIdx.x == 0) {
+      const long long t = atomicAdd(reinterpret_cast<unsigned long long*>(&ctrl64[CTRL64_TICKET]), 1ull);
+      s_t = t;
+      s_e = t < n_chunks ? find_entry(entries, n_entries, t) : 0;
+    }
+    __syncthreads();
+    const int64_t t = s_t;
+    if (t >= n_chunks) break;
+    const MoveEntry me = entries[s_e];
+    const int64_t pos = (t - me.chunk0) * S;
+    const int64_t nb = min(S, me.bytes - pos);
+    const int nv = (int)(nb >> 4);
+    const uint8_t* src = arena + me.src + pos;
+    const bool copy = me.kind == MOVE_ARENA || staging_enabled;
+    if (copy)
+      for (int i = threadIdx.x; i < nv; i += blockDim.x) buf[i] = ld_stream(src + 16 * (int64_t)i);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      st_release_u32(flags + t, epoch);
+      if (me.kind == MOVE_ARENA)
+        wait_sources(entries, n_entries, S, me.dst + pos, me.dst + pos + nb, t, flags, epoch);
+    }
+    __syncthreads();
+    if (copy) {
+      uint8_t* dst = (me.kind == MOVE_ARENA ? arena : staging) + me.dst + pos;
+      for (int i = threadIdx.x; i < nv; i += blockDim.x) st_v4(dst + 16 * (int64_t)i, buf[i]);
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_fill: prompt rows 0..P-1 of freshly admitted slots (stand-in for the
+// model's prefill).  grid = (row groups, admitted slots).
+// ---------------------------------------------------------------------------
+constexpr int FILL_ROWS = 4;
+__global__ void __launch_bounds__(256) k_fill(Shape sh, uint64_t seed, const DSlot* __restrict__ slots,
+                                              const int32_t* __restrict__ list, uint16_t* __restrict__ arena) {
+  const DSlot sl = slots[list[blockIdx.y]];
+  const int p0 = blockIdx.x * FILL_ROWS;
+  if (p0 >= sl.prompt) return;
+  const int p1 = min(sl.prompt, p0 + FILL_ROWS);
+  const int D8 = sh.D / 8;
+  const int per_row = sh.L * 2 * sh.H * D8;   // 16-byte vectors per row
+  const int total = (p1 - p0) * per_row;
+  for (int i = threadIdx.x; i < total; i += blockDim.x) {
+    const int pos = p0 + i / per_row;
+    int r = i % per_row;
+    const int d8 = r % D8; r /= D8;
+    const int h = r % sh.H; r /= sh.H;
+    const int kv = r % 2;
+    const int l = r / 2;
+    const uint4 v = gen8(sh, seed, 0, sl.req, l, kv, pos, h, d8, 1.f / 128.f);
+    st_v4(arena + ((int64_t)sl.off + pos) * sh.row_elems + ((int64_t)(l * 2 + kv) * sh.H + h) * sh.D + d8 * 8, v);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_synth: q / k_new / v_new [nl][B][H][D] at position len_b, and eos.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_synth(Shape sh, uint64_t seed, const DSlot* __restrict__ slots,
+                                               int32_t B, int32_t l0, int32_t nl,
+                                               const int32_t* __restrict__ out_len, int64_t n_req,
+                                               uint16_t* q, uint16_t* k, uint16_t* v, uint8_t* eos) {
+  const int D8 = sh.D / 8;
+  const int64_t total = (int64_t)nl * B * sh.H * D8;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i;
+    const int d8 = (int)(r % D8); r /= D8;
+    const int h = (int)(r % sh.H); r /= sh.H;
+    const int b = (int)(r % B);
+    const int li = (int)(r / B);
+    const DSlot sl = slots[b];
+    const int l = l0 + li;
+    const int64_t o = i * 8;
+    st_v4(k + o, gen8(sh, seed, 0, sl.req, l, 0, sl.len, h, d8, 1.f / 128.f));
+    st_v4(v + o, gen8(sh, seed, 0, sl.req, l, 1, sl.len, h, d8, 1.f / 128.f));
+    st_v4(q + o, gen8(sh, seed, 1, sl.req, l, 0, sl.len, h, d8, 1.f / 32.f));
+    if (i < B) {
+      const DSlot s2 = slots[i];
+      const int O = (s2.req >= 0 && s2.req < n_req) ? out_len[s2.req] : 0x7fffffff;
+      eos[i] = (uint8_t)(s2.gen + 1 == O);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// k_verify: count 16-byte vectors of resident rows that differ from G.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_verify(Shape sh, uint64_t seed, const DSlot* __restrict__ slots,
+                                                const uint16_t* __restrict__ arena,
+                                                unsigned long long* bad) {
+  const DSlot sl = slots[blockIdx.y];
+  const int D8 = sh.D / 8;
+  const int64_t per_row = (int64_t)sh.L * 2 * sh.H * D8;
+  const int64_t total = (int64_t)sl.len * per_row;
+  unsigned long long nbad = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int pos = (int)(i / per_row);
+    int64_t r = i % per_row;
+    const int d8 = (int)(r % D8); r /= D8;
+    const int h = (int)(r % sh.H); r /= sh.H;
+    const int kv = (int)(r % 2);
+    const int l = (int)(r / 2);
+    const uint4 want = gen8(sh, seed, 0, sl.req, l, kv, pos, h, d8, 1.f / 128.f);
+    const uint4 got = ld_plain(arena + ((int64_t)sl.off + pos) * sh.row_elems +
+                               ((int64_t)(l * 2 + kv) * sh.H + h) * sh.D + d8 * 8);
+    nbad += (want.x != got.x) | (want.y != got.y) | (want.z != got.z) | (want.w != got.w);
+  }
+  if (nbad) atomicAdd(bad, nbad);
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+int attn_block_threads(const Shape& sh) {
+  const int lanes = sh.H * sh.D / 8;
+  return ((lanes + 31) / 32) * 32;
+}
+
+const void* attn_kernel_ptr(const Shape& sh) {
+  switch (sh.D) {
+    case 64: return (const void*)k_attn<64>;
+    case 128: return (const void*)k_attn<128>;
+    case 256: return (const void*)k_attn<256>;
+    default: return nullptr;
+  }
+}
+const void* move_kernel_ptr() { return (const void*)k_move; }
+
+cudaError_t launch_prep(const Shape& sh, DSlot* slots, int32_t B, int32_t C, const uint8_t* eos,
+                        int32_t finalize, Unit* units, Split* splits, int32_t* ctrl, cudaStream_t st) {
+  (void)sh;
+  k_prep<<<1, 1024, 0, st>>>(slots, B, C, eos, finalize, units, splits, ctrl);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_attn(const Shape& sh, const uint16_t* q, const uint16_t* k_new, const uint16_t* v_new,
+                        uint16_t* arena, float* out, float* partials, const Unit* units,
+                        const Split* splits, int32_t* ctrl, int32_t B, int32_t l0, int32_t nl,
+                        int32_t grid_attn, int32_t grid_combine, cudaStream_t st) {
+  AttnArgs a;
+  a.sh = sh; a.q = q; a.k_new = k_new; a.v_new = v_new; a.arena = arena; a.out = out;
+  a.partials = partials; a.units = units; a.ctrl = ctrl; a.B = B; a.l0 = l0; a.nl = nl;
+  a.qscale = 1.4426950408889634f / sqrtf((float)sh.D);
+  const int threads = attn_block_threads(sh);
+  switch (sh.D) {
+    case 64:
+      k_attn<64><<<grid_attn, threads, 0, st>>>(a);
+      k_combine<64><<<grid_combine, 256, 0, st>>>(splits, partials, out, ctrl, sh.H, B, nl);
+      break;
+    case 128:
+      k_attn<128><<<grid_attn, threads, 0, st>>>(a);
+      k_combine<128><<<grid_combine, 256, 0, st>>>(splits, partials, out, ctrl, sh.H, B, nl);
+      break;
+    case 256:
+      k_attn<256><<<grid_attn, threads, 0, st>>>(a);
+      k_combine<256><<<grid_combine, 256, 0, st>>>(splits, partials, out, ctrl, sh.H, B, nl);
+      break;
+    default:
+      return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_keep_scan(const Shape& sh, const DSlot* cur, DSlot* next, int32_t B, int64_t S,
+                             void* report, MoveEntry* entries, int64_t* ctrl64, cudaStream_t st) {
+  k_keep_scan<<<1, 1024, 0, st>>>(sh, cur, next, B, S, (uint8_t*)report, entries, ctrl64);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_move(uint8_t* arena, uint8_t* staging, const MoveEntry* entries, int32_t n_entries,
+                        int64_t n_chunks, int64_t S, int64_t* ctrl64, uint32_t* flags, uint32_t epoch,
+                        int32_t staging_enabled, int32_t grid, cudaStream_t st) {
+  k_move<<<grid, 256, (size_t)S, st>>>(arena, staging, entries, n_entries, n_chunks, S, ctrl64, flags,
+                                        epoch, staging_enabled);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill(const Shape& sh, uint64_t seed, const DSlot* slots, const int32_t* list,
+                        int32_t n, int32_t max_prompt, uint16_t* arena, cudaStream_t st) {
+  if (n <= 0 || max_prompt <= 0) return cudaSuccess;
+  dim3 grid((max_prompt + FILL_ROWS - 1) / FILL_ROWS, n);
+  k_fill<<<grid, 256, 0, st>>>(sh, seed, slots, list, arena);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_synth(const Shape& sh, uint64_t seed, const DSlot* slots, int32_t B, int32_t l0,
+                         int32_t nl, const int32_t* out_len_by_req, int64_t n_req, uint16_t* q,
+                         uint16_t* k, uint16_t* v, uint8_t* eos, cudaStream_t st) {
+  if (B <= 0) return cudaSuccess;
+  const int64_t total = (int64_t)nl * B * sh.H * (sh.D / 8);
+  const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 16);
+  k_synth<<<(int)blocks, 256, 0, st>>>(sh, seed, slots, B, l0, nl, out_len_by_req, n_req, q, k, v, eos);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_verify(const Shape& sh, uint64_t seed, const DSlot* slots, int32_t B,
+                          const uint16_t* arena, unsigned long long* bad, cudaStream_t st) {
+  if (B <= 0) return cudaSuccess;
+  dim3 grid(64, B);
+  k_verify<<<grid, 256, 0, st>>>(sh, seed, slots, arena, bad);
+  return cudaGetLastError();
+}
+
+}  // namespace s3

@@ -1,0 +1,189 @@
+"""S3Engine: buffer allocation (torch) + the per-iteration call sequence.
+
+This is the public Python API a user drives.  It allocates the caller-owned
+buffers of include/s3.h with torch (device memory, pinned host memory, the
+current stream) and calls the four ABI entry points in the order the paper's
+iteration-level loop implies:
+
+    decode (attention + append + detect) -> evict + compact -> admit
+
+Every step of the method runs inside libs3.so; nothing here computes.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import s3 as abi
+
+
+@dataclass
+class StepStats:
+    batch: int
+    tokens: int
+    finished: int
+    evicted: int
+    admitted: int
+    d2h_bytes: int
+    moved_bytes: int
+    paper_pcie_bytes: int
+    paper_hbm_bytes: int
+    reload_bytes: int
+    fill_bytes: int
+
+
+class S3Engine:
+    def __init__(self, num_layers, num_heads, head_dim, max_seq_len, arena_rows, max_running,
+                 chunk_rows=0, move_chunk_bytes=0, device=0, rank=0, world=1, seed=1,
+                 staging_bytes=None, host_store_bytes=None, io_rows=None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("S3Engine needs a CUDA device (no CPU fallback)")
+        self.device = torch.device("cuda", device)
+        torch.cuda.set_device(self.device)
+        self.L, self.H, self.D = num_layers, num_heads, head_dim
+        self.max_running = max_running
+        self.world, self.rank = world, rank
+        self.stream = torch.cuda.current_stream(self.device)
+        self.cfg = abi.s3_config(
+            num_layers=num_layers, num_heads=num_heads, head_dim=head_dim, max_seq_len=max_seq_len,
+            arena_rows=arena_rows, max_running=max_running, chunk_rows=chunk_rows,
+            move_chunk_bytes=move_chunk_bytes, device=device, stream=self.stream.cuda_stream,
+            rank=rank, world=world, synth_seed=seed)
+        arena_b, ws_b, st_min, hs_min = abi.s3_workspace_query(self.cfg)
+        self.kvpt = 4 * num_layers * num_heads * head_dim
+        self.arena = torch.empty(arena_b, dtype=torch.uint8, device=self.device)
+        self.workspace = torch.empty(ws_b, dtype=torch.uint8, device=self.device)
+        st_b = st_min if staging_bytes is None else staging_bytes
+        self.staging = torch.empty(max(st_b, 16), dtype=torch.uint8, device=self.device)
+        hs_b = max(hs_min, host_store_bytes or 4 * hs_min)
+        self.host_store = torch.empty(hs_b, dtype=torch.uint8, pin_memory=True)
+        bufs = abi.s3_buffers(self.arena.data_ptr(), arena_b, self.workspace.data_ptr(), ws_b,
+                              self.staging.data_ptr() if st_b > 0 else None, st_b,
+                              self.host_store.data_ptr(), hs_b)
+        self.ctx = abi.s3_kv_init(self.cfg, bufs)
+        rows = io_rows or max_running
+        n = num_layers * rows * num_heads * head_dim
+        self.q = torch.empty(n, dtype=torch.bfloat16, device=self.device)
+        self.k_new = torch.empty(n, dtype=torch.bfloat16, device=self.device)
+        self.v_new = torch.empty(n, dtype=torch.bfloat16, device=self.device)
+        self.out = torch.empty(n, dtype=torch.float32, device=self.device)
+        self.eos = torch.empty(max(rows, 1), dtype=torch.uint8, device=self.device)
+        self.out_len = None
+        self.counters = np.zeros(abi.S3_NCOUNTERS, np.int64)
+
+    # ---- lifecycle -----------------------------------------------------
+    def close(self):
+        if getattr(self, "ctx", None):
+            abi.s3_kv_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- pool ----------------------------------------------------------
+    def submit(self, req_id, prompt, alloc, out_len=None):
+        """Submit requests; out_len (actual output lengths) feeds only the
+        synthetic sampler stand-in (s3_synth_inputs), never the method."""
+        n = len(req_id)
+        arr = (abi.s3_request * n)()
+        for i in range(n):
+            arr[i].req_id = int(req_id[i])
+            arr[i].prompt_len = int(prompt[i])
+            arr[i].alloc_out = int(alloc[i])
+        abi.s3_submit(self.ctx, arr)
+        if out_len is not None:
+            o = np.full(int(np.max(req_id)) + 1, 1 << 30, np.int32)
+            o[np.asarray(req_id)] = np.asarray(out_len, np.int32)
+            self.out_len = torch.from_numpy(o).to(self.device)
+
+    # ---- the four calls --------------------------------------------------
+    @property
+    def B(self) -> int:
+        return abi.s3_batch_size(self.ctx)
+
+    def synth_inputs(self, l0=0, nl=None):
+        nl = self.L - l0 if nl is None else nl
+        abi.s3_synth_inputs(self.ctx, l0, nl, self.out_len, self.q, self.k_new, self.v_new, self.eos)
+
+    def decode(self, l0=0, nl=None, q=None, k_new=None, v_new=None, eos=None, out=None):
+        nl = self.L - l0 if nl is None else nl
+        abi.s3_decode_step(self.ctx, l0, nl, self.q if q is None else q, self.k_new if k_new is None else k_new,
+                           self.v_new if v_new is None else v_new, self.eos if eos is None else eos,
+                           self.out if out is None else out)
+
+    def evict_compact(self):
+        return abi.s3_evict_compact(self.ctx, self.B)
+
+    def admit(self):
+        if self.world == 1:
+            return abi.s3_admit(self.ctx, self.max_running)
+        raise RuntimeError("world > 1: use admit_home / exchange / admit_shared")
+
+    def admit_home(self):
+        return abi.s3_admit_home(self.ctx, self.max_running)
+
+    def counters_local(self) -> np.ndarray:
+        abi.s3_counters_local(self.ctx, self.counters)
+        return self.counters.copy()
+
+    def admit_shared(self, counters_all: np.ndarray):
+        return abi.s3_admit_shared(self.ctx, self.max_running, np.ascontiguousarray(counters_all, np.int64))
+
+    def batch_view(self):
+        return abi.s3_batch_view(self.ctx)
+
+    def verify_resident(self) -> int:
+        return abi.s3_verify_resident(self.ctx)
+
+    def evict_wait(self):
+        abi.s3_evict_wait(self.ctx)
+
+    def profile(self, on: bool):
+        abi.s3_profile_enable(self.ctx, on)
+
+    def profile_get(self):
+        return abi.s3_profile_get(self.ctx)
+
+    # ---- one iteration (world == 1) ---------------------------------------
+    def step(self, exchange=None) -> StepStats:
+        """synth inputs -> decode -> evict+compact -> admit.  `exchange` is a
+        callable(local_row int64[8]) -> all rows int64[world, 8] (an
+        all-reduce done by the caller's process group) used when world > 1."""
+        B = self.B
+        if B:
+            self.synth_inputs()
+        self.decode()
+        rep, perm, ev, fin = self.evict_compact()
+        if self.world == 1:
+            arep, _ = self.admit()
+            reload_b, fill_b, n_adm = arep.h2d_bytes, arep.fill_bytes, arep.n_admitted
+        else:
+            hrep, _ = self.admit_home()
+            allrows = exchange(self.counters_local())
+            srep, _ = self.admit_shared(allrows)
+            reload_b = hrep.h2d_bytes + srep.h2d_bytes
+            fill_b = hrep.fill_bytes + srep.fill_bytes
+            n_adm = hrep.n_admitted + srep.n_admitted
+        return StepStats(B, B, rep.n_finished, rep.n_evicted, n_adm, rep.d2h_bytes, rep.moved_bytes,
+                         rep.paper_pcie_bytes, rep.paper_hbm_bytes, reload_b, fill_b)
+
+    def initial_admit(self, exchange=None):
+        if self.world == 1:
+            return self.admit()
+        self.admit_home()
+        return self.admit_shared(exchange(self.counters_local()))
+
+    def arena_rows_view(self) -> torch.Tensor:
+        """The arena as bf16 [R][L][2][H][D] (a view, no copy)."""
+        R = self.cfg.arena_rows
+        return self.arena.view(torch.bfloat16).view(R, self.L, 2, self.H, self.D)
+
+    def host_rows(self, host_off: int, rows: int) -> torch.Tensor:
+        n = rows * self.kvpt
+        return self.host_store[host_off:host_off + n].view(torch.bfloat16).view(rows, self.L, 2, self.H, self.D)

@@ -1,0 +1,182 @@
+"""GPU path vs oracle parity (-m gpu).  Every call goes through the C ABI.
+
+Bar: bit-exact for slots, offsets, permutations,
+eviction lists, byte counters, arena rows and evicted host bytes; attention
+within 2e-3 relative error per (layer, slot, head):
+    max_d |o_gpu - o_ref| / max(max_d |o_ref|, 2^-20) <= 2e-3.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import s3synth
+
+pytestmark = pytest.mark.gpu
+
+TOL = 2e-3
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    from paper_2306_06000_b200 import build
+    build.build()
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def rel_err(out_gpu: np.ndarray, ref: np.ndarray) -> float:
+    """Max over (l, b, h) of the per-head relative error."""
+    if ref.size == 0:
+        return 0.0
+    num = np.abs(out_gpu - ref).max(axis=-1)
+    den = np.maximum(np.abs(ref).max(axis=-1), 2.0**-20)
+    return float((num / den).max())
+
+
+def u16(t: torch.Tensor) -> np.ndarray:
+    return t.view(torch.int16).cpu().numpy().view(np.uint16)
+
+
+def lockstep(trace, L, H, D, R, C=0, S=0, max_running=4096, staging=True, feed_oracle_inputs=False,
+             max_steps=100000, check_arena=True):
+    from paper_2306_06000_b200.engine import S3Engine
+    eng = S3Engine(L, H, D, trace.max_seq_len, R, max_running, chunk_rows=C, move_chunk_bytes=S,
+                   staging_bytes=None if staging else 0, host_store_bytes=64 << 20)
+    orc = oracle.Oracle(L, H, D, trace.max_seq_len, R, max_running=max_running)
+    eng.submit(trace.req_id, trace.prompt, trace.alloc, trace.out)
+    orc.submit(trace.req_id, trace.prompt, trace.alloc)
+    _, adm_g = eng.admit()
+    adm_o = orc.admit()
+    assert adm_g == adm_o
+    worst, steps, stats = 0.0, 0, dict(evictions=0, moved=0, splits=0)
+    HD = H * D
+    while True:
+        c = orc.counters()
+        if orc.B == 0 and c[3] + c[4] == 0:
+            assert eng.B == 0
+            break
+        assert steps < max_steps
+        B = orc.B
+        assert eng.batch_view() == orc.batch(), f"step {steps}: batch views differ"
+        q, k, v, eos = orc.make_inputs(trace.out)
+        n = L * B * HD
+        if B:
+            if feed_oracle_inputs:
+                eng.q[:n].copy_(torch.from_numpy(q.reshape(-1).view(np.int16)).view(torch.bfloat16))
+                eng.k_new[:n].copy_(torch.from_numpy(k.reshape(-1).view(np.int16)).view(torch.bfloat16))
+                eng.v_new[:n].copy_(torch.from_numpy(v.reshape(-1).view(np.int16)).view(torch.bfloat16))
+                eng.eos[:B].copy_(torch.from_numpy(eos))
+            else:
+                eng.synth_inputs()
+                # T0 at run time: the CUDA generator equals the oracle's
+                assert np.array_equal(u16(eng.q[:n]), q.reshape(-1))
+                assert np.array_equal(u16(eng.k_new[:n]), k.reshape(-1))
+                assert np.array_equal(u16(eng.v_new[:n]), v.reshape(-1))
+                assert np.array_equal(eng.eos[:B].cpu().numpy(), eos)
+        ref, st = orc.decode(q, k, v, eos)
+        eng.decode()
+        if B:
+            got = eng.out[:n].cpu().numpy().reshape(L, B, H, D).astype(np.float64)
+            err = rel_err(got, ref)
+            worst = max(worst, err)
+            assert err <= TOL, f"step {steps}: attention rel err {err}"
+        rep_o, perm_o, ev_o, fin_o = orc.evict_compact()
+        rep_g, perm_g, ev_g, fin_g = eng.evict_compact()
+        for f in ["n_before", "n_finished", "n_evicted", "n_kept", "d2h_bytes", "moved_bytes",
+                  "paper_pcie_bytes", "paper_hbm_bytes", "first_hole"]:
+            assert getattr(rep_g, f) == getattr(rep_o, f), (steps, f)
+        assert rep_g.tail_rows == rep_o.tail
+        assert perm_g == list(perm_o)
+        assert [int(x) for x in fin_g] == [int(x) for x in fin_o]
+        assert [(e.req_id, e.batch_index, e.prompt_len, e.gen_len, e.len, e.cap_rows, e.new_cap_rows)
+                for e in ev_g] == [tuple(e) for e in ev_o]
+        if ev_g:
+            eng.evict_wait()
+            for e in ev_g:
+                host_g = u16(eng.host_rows(e.host_off, e.len).reshape(-1))
+                assert np.array_equal(host_g, orc.host_kv(e.req_id).reshape(-1))
+        stats["evictions"] += rep_o.n_evicted
+        stats["moved"] += rep_o.moved_bytes
+        _, adm_g = eng.admit()
+        adm_o = orc.admit()
+        assert adm_g == adm_o, f"step {steps}: admissions differ"
+        if check_arena:
+            A_o = orc.arena()
+            A_g = eng.arena_rows_view()
+            for (req, P, gen, ln, cap, off) in orc.batch():
+                assert np.array_equal(u16(A_g[off:off + ln].reshape(-1)), A_o[off:off + ln].reshape(-1)), \
+                    f"step {steps}: arena rows of req {req} differ"
+        steps += 1
+    assert eng.verify_resident() == 0
+    eng.close()
+    return dict(steps=steps, worst=worst, **stats)
+
+
+def test_c0_full_run():
+    t = s3synth.c0_trace()
+    r = lockstep(t, 1, 2, 64, 64, C=4, S=1024)
+    assert r["steps"] == 32 and r["evictions"] == 3
+
+
+def test_c0prime_full_run_oracle_inputs():
+    t = s3synth.c0prime_trace()
+    r = lockstep(t, 1, 2, 64, 64, C=3, S=1024, feed_oracle_inputs=True)
+    assert r["steps"] == 32
+
+
+def test_c0_sync_eviction_path():
+    t = s3synth.c0_trace()
+    r = lockstep(t, 1, 2, 64, 64, C=64, S=1024, staging=False)
+    assert r["evictions"] == 3
+
+
+def test_gptj_heads_reduced_layers_with_evictions():
+    # GPT-J head shape (H=16, D=256), 2 layers; small chunks -> many split-K
+    # tiles with ragged tails; small move chunks -> overlapping ordered moves.
+    t = s3synth.make_trace(60, seed=3, policy="short", p=0.3, max_seq_len=160, prompt_max=40)
+    r = lockstep(t, 2, 16, 256, 700, C=16, S=4096, max_steps=400)
+    assert r["evictions"] > 0 and r["moved"] > 0
+    print("worst rel err", r["worst"])
+
+
+def test_head_dim_128():
+    t = s3synth.make_trace(40, seed=4, policy="short", p=0.2, max_seq_len=96, prompt_max=20)
+    lockstep(t, 3, 4, 128, 400, C=8, S=2048)
+
+
+def test_max_running_limit_and_p0():
+    t = s3synth.make_trace(50, seed=7, policy="bucket", max_seq_len=128, prompt_max=20)
+    r = lockstep(t, 1, 2, 64, 2000, C=32, S=1024, max_running=8)
+    assert r["evictions"] == 0             # P4: no short predictions -> no penalty
+
+
+def test_gptj_full_shape_long_sequences():
+    # Full GPT-J KV shape (L=28, H=16, D=256), a few long prompts: checks the
+    # default chunk C=512 split and the full row stride; 2 steps.
+    P = np.array([1500, 900, 511, 2, 1200], np.int32)
+    O = np.array([30, 40, 2, 50, 60], np.int32)
+    t = s3synth.Trace(np.arange(5, dtype=np.int64), P, O, O.copy(), 2048)
+    from paper_2306_06000_b200.engine import S3Engine
+    L, H, D = 28, 16, 256
+    R = 4500
+    eng = S3Engine(L, H, D, 2048, R, 64, host_store_bytes=64 << 20)
+    eng.submit(t.req_id, t.prompt, t.alloc, t.out)
+    eng.admit()
+    for step in range(2):
+        slots = eng.batch_view()
+        eng.synth_inputs()
+        eng.decode()
+        B = len(slots)
+        out = eng.out[:L * B * H * D].view(L, B, H, D)
+        for b, (req, Pb, gen, ln, cap, off) in enumerate(slots):
+            for l in (0, 13, 27):
+                ref = oracle.attend_generated(L, H, D, 2048, 1, req, ln, l)
+                err = rel_err(out[l, b].cpu().numpy().astype(np.float64)[None], ref[None])
+                assert err <= TOL, (step, req, l, err)
+        eng.evict_compact()
+        eng.admit()
+    assert eng.verify_resident() == 0
+    eng.close()

@@ -530,3 +530,19 @@ def test_multirank_plan_consistency(oracle_lib):
             o.evict_compact()
     assert sorted(owner) == list(range(t.n))          # every request admitted once, fresh
     assert tokens == int(t.out.sum())                 # conservation across ranks
+
+
+def test_attend_generated_matches_state_machine(oracle_lib):
+    # P2: the state machine's arena rows are the generator's, so its decode
+    # output equals the pure-function attention of (req, pos, l).
+    L, H, D = 2, 2, 64
+    o = oracle.Oracle(L, H, D, 64, 128)
+    o.submit(np.arange(3), [0, 5, 17], [9, 9, 9])
+    o.admit()
+    q, k, v, eos = o.make_inputs(np.full(3, 100, np.int32))
+    pre = o.batch()
+    out, _ = o.decode(q, k, v, eos)
+    for b, (req, P, gen, ln, cap, off) in enumerate(pre):
+        for l in range(L):
+            ref = oracle.attend_generated(L, H, D, 64, 1, req, ln, l)
+            assert np.array_equal(out[l, b], ref)
