@@ -47,6 +47,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--arena-gb", type=float, default=0.0, help="cap the arena (e.g. for ncu replay)")
     return ap.parse_args()
 
 
@@ -220,6 +221,8 @@ def run_s3(args):
     reserve = 6 << 30
     R = int((free_b - io_bytes - staging - reserve - (2 << 30)) // kvpt)
     R = min(R, (1 << 31) - 1)
+    if args.arena_gb > 0:
+        R = min(R, int(args.arena_gb * 1e9 // kvpt))
     eng = S3Engine(L, H, D, GPTJ["max_len"], R, max_running, device=local, rank=rank, world=world,
                    seed=args.seed, staging_bytes=staging, host_store_bytes=(16 << 30) if p > 0 else (1 << 30))
 

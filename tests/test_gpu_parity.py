@@ -137,7 +137,7 @@ def test_gptj_heads_reduced_layers_with_evictions():
     # GPT-J head shape (H=16, D=256), 2 layers; small chunks -> many split-K
     # tiles with ragged tails; small move chunks -> overlapping ordered moves.
     t = s3synth.make_trace(60, seed=3, policy="short", p=0.3, max_seq_len=160, prompt_max=40)
-    r = lockstep(t, 2, 16, 256, 700, C=16, S=4096, max_steps=400)
+    r = lockstep(t, 2, 16, 256, 1200, C=16, S=4096, max_steps=3000)
     assert r["evictions"] > 0 and r["moved"] > 0
     print("worst rel err", r["worst"])
 
@@ -179,4 +179,49 @@ def test_gptj_full_shape_long_sequences():
         eng.evict_compact()
         eng.admit()
     assert eng.verify_resident() == 0
+    eng.close()
+
+
+def test_bench_configuration_sampled():
+    """The bench's launch configuration at full size (C1: GPT-J KV, 8192
+    requests, ~160 GB arena, default C and S): sampled outputs against the
+    oracle's fp64 attention one at a time, resident rows against the
+    generator (P2), and the slot-table invariants after every step."""
+    from paper_2306_06000_b200.engine import S3Engine
+    L, H, D, M = 28, 16, 256, 2048
+    kvpt = 4 * L * H * D
+    t = s3synth.make_trace(8192, seed=1, policy="short", p=0.1, max_seq_len=M)
+    max_running = 8192
+    free_b, _ = torch.cuda.mem_get_info()
+    R = int((free_b - max_running * L * H * D * 10 - (4 << 30) - (8 << 30)) // kvpt)
+    eng = S3Engine(L, H, D, M, R, max_running, staging_bytes=4 << 30, host_store_bytes=8 << 30)
+    eng.submit(t.req_id, t.prompt, t.alloc, t.out)
+    eng.admit()
+    rng = np.random.default_rng(0)
+    evictions = 0
+    for step in range(40):
+        slots = eng.batch_view()
+        B = len(slots)
+        offs = [s[5] for s in slots]
+        assert offs == sorted(offs)
+        assert all(slots[i][5] + slots[i][4] <= (slots[i + 1][5] if i + 1 < B else R) for i in range(B))
+        assert all(s[3] < s[4] for s in slots)          # len < cap before a decode
+        eng.synth_inputs()
+        eng.decode()
+        if step % 8 == 0:
+            lens = np.array([s[3] for s in slots])
+            pick = set(rng.choice(B, 6, replace=False).tolist()) | {int(lens.argmax()), int(lens.argmin())}
+            out = eng.out[:L * B * H * D].view(L, B, H, D)
+            for b in sorted(pick):
+                req, P, gen, ln, cap, off = slots[b]
+                for l in (0, 27):
+                    ref = oracle.attend_generated(L, H, D, M, 1, req, ln, l)
+                    err = rel_err(out[l, b].cpu().numpy().astype(np.float64)[None], ref[None])
+                    assert err <= TOL, (step, req, ln, l, err)
+        rep, perm, ev, fin = eng.evict_compact()
+        evictions += rep.n_evicted
+        eng.admit()
+        if step % 10 == 9:
+            assert eng.verify_resident() == 0, step
+    print("evictions", evictions)
     eng.close()
