@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--arena-gb", type=float, default=0.0, help="cap the arena (e.g. for ncu replay)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend of the counter exchange (gloo: tests sharing one GPU)")
     return ap.parse_args()
 
 
@@ -197,12 +199,17 @@ def run_s3(args):
     if world != args.gpus:
         if args.gpus > 1:
             raise SystemExit("--gpus N > 1 must be launched with torchrun (WORLD_SIZE = N)")
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
+    cdev = dev if args.dist_backend == "nccl" else torch.device("cpu")
 
     from paper_2306_06000_b200 import build
     build.build()
@@ -218,6 +225,8 @@ def run_s3(args):
     io_bytes = max_running * L * H * D * (3 * 2 + 4)
     staging = 4 << 30
     free_b, _ = torch.cuda.mem_get_info(dev)
+    if torch.cuda.device_count() < world:
+        free_b //= world                                  # ranks share a device (tests only)
     reserve = 6 << 30
     R = int((free_b - io_bytes - staging - reserve - (2 << 30)) // kvpt)
     R = min(R, (1 << 31) - 1)
@@ -228,7 +237,7 @@ def run_s3(args):
 
     exchange = None
     if world > 1:
-        mat = torch.zeros(world, 8, dtype=torch.int64, device=dev)
+        mat = torch.zeros(world, 8, dtype=torch.int64, device=cdev)
 
         def exchange(row):
             mat.zero_()
@@ -271,10 +280,10 @@ def run_s3(args):
     eng.profile(False)
     ms_max, tok_sum = ms, tokens
     if dist:
-        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+        tt = torch.tensor([ms], dtype=torch.float64, device=cdev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms_max = float(tt.item())
-        tk = torch.tensor([tokens], dtype=torch.int64, device=dev)
+        tk = torch.tensor([tokens], dtype=torch.int64, device=cdev)
         dist.all_reduce(tk)
         tok_sum = int(tk.item())
     value = tok_sum / (ms_max / 1e3)
@@ -283,7 +292,7 @@ def run_s3(args):
     # ---- e2e through the public API with host buffers ----------------------
     e2e = None
     if not args.no_e2e:
-        e2e = e2e_leg(eng, exchange, dist, dev, min(args.steps, 50), world)
+        e2e = e2e_leg(eng, exchange, dist, cdev, min(args.steps, 50), world)
 
     peak, peak_kind = load_peak()
     attn_gbs = prof.attn_bytes / (prof.attn_ms / 1e3) / 1e9 if prof.attn_ms > 0 else 0.0

@@ -107,6 +107,8 @@ struct s3_ctx {
   int32_t* ctrl = nullptr;
   int64_t* ctrl64 = nullptr;
   MoveEntry* entries = nullptr;
+  int32_t* key_chunk0 = nullptr;
+  int32_t* key_src = nullptr;
   uint32_t* flags = nullptr;
   uint8_t* report_dev = nullptr;
   unsigned long long* verify_count = nullptr;
@@ -160,7 +162,7 @@ bool validate(const s3_config* c) {
   if (c->arena_rows > INT32_MAX) return false;
   if (c->max_running < 1 || c->max_running > 65535) return false;
   if (c->chunk_rows < 0 || c->move_chunk_bytes < 0 || c->move_chunk_bytes % 16) return false;
-  if (c->move_chunk_bytes > 0 && (c->move_chunk_bytes < 1024 || c->move_chunk_bytes > 196608)) return false;
+  if (c->move_chunk_bytes > 0 && (c->move_chunk_bytes < 1024 || c->move_chunk_bytes > 36864)) return false;
   if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return false;
   return true;
 }
@@ -174,7 +176,7 @@ Shape make_shape(const s3_config* c) {
 }
 
 struct Carve {
-  int64_t slots, units, splits, partials, ctrl, ctrl64, entries, flags, report, verify, total;
+  int64_t slots, units, splits, partials, ctrl, ctrl64, entries, keys, flags, report, verify, total;
 };
 
 Carve carve(const s3_config* c) {
@@ -194,6 +196,7 @@ Carve carve(const s3_config* c) {
   k.ctrl = o;     o += align_up(CTRL_WORDS * 4);
   k.ctrl64 = o;   o += align_up(CTRL64_WORDS * 8);
   k.entries = o;  o += align_up((Bm + 1) * (int64_t)sizeof(MoveEntry));
+  k.keys = o;     o += align_up(2 * (Bm + 2) * 4);
   k.flags = o;    o += align_up(flags_max * 4);
   k.report = o;   o += align_up(report_bytes((int32_t)Bm));
   k.verify = o;   o += align_up(8);
@@ -371,11 +374,8 @@ s3_status s3_kv_init(const s3_config* cfg, const s3_buffers* b, s3_ctx** out) {
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ka, attn_block_threads(sh), 0);
   ctx->grid_attn = ctx->num_sms * std::max(1, occ);
   ctx->grid_combine = ctx->num_sms * 4;
-  if (ctx->S > 48 * 1024)
-    cudaFuncSetAttribute(move_kernel_ptr(), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ctx->S);
-  int occm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occm, move_kernel_ptr(), 256, (size_t)ctx->S);
-  ctx->grid_move = ctx->num_sms * std::max(1, occm);
+  cudaFuncSetAttribute(move_kernel_ptr(), cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+  ctx->grid_move = ctx->num_sms;   // one CTA per SM (its buffers fill most of shared memory)
   uint8_t* ws = (uint8_t*)b->workspace;
   ctx->slots[0] = reinterpret_cast<DSlot*>(ws + k.slots);
   ctx->slots[1] = ctx->slots[0] + cfg->max_running;
@@ -385,6 +385,8 @@ s3_status s3_kv_init(const s3_config* cfg, const s3_buffers* b, s3_ctx** out) {
   ctx->ctrl = reinterpret_cast<int32_t*>(ws + k.ctrl);
   ctx->ctrl64 = reinterpret_cast<int64_t*>(ws + k.ctrl64);
   ctx->entries = reinterpret_cast<MoveEntry*>(ws + k.entries);
+  ctx->key_chunk0 = reinterpret_cast<int32_t*>(ws + k.keys);
+  ctx->key_src = ctx->key_chunk0 + (cfg->max_running + 2);
   ctx->flags = reinterpret_cast<uint32_t*>(ws + k.flags);
   ctx->report_dev = ws + k.report;
   ctx->verify_count = reinterpret_cast<unsigned long long*>(ws + k.verify);
@@ -493,7 +495,7 @@ s3_status s3_evict_compact(s3_ctx* ctx, s3_evict_report* rep, int32_t* perm, s3_
   }
   const Shape& sh = ctx->sh;
   CK(launch_keep_scan(sh, ctx->slots[ctx->cur], ctx->slots[1 - ctx->cur], B, ctx->S, ctx->report_dev,
-                      ctx->entries, ctx->ctrl64, ctx->st), "k_keep_scan");
+                      ctx->entries, ctx->key_chunk0, ctx->key_src, ctx->ctrl64, ctx->st), "k_keep_scan");
   ctx->launches += 1;
   CK(cudaMemcpyAsync(ctx->h_report, ctx->report_dev, (size_t)report_bytes(B), cudaMemcpyDeviceToHost, ctx->st),
      "report D2H");
@@ -536,9 +538,10 @@ s3_status s3_evict_compact(s3_ctx* ctx, s3_evict_report* rep, int32_t* perm, s3_
     ctx->epoch++;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx->prof.on) { e0 = ctx->prof.get(); e1 = ctx->prof.get(); cudaEventRecord(e0, ctx->st); }
-    const int grid = (int)std::min<int64_t>(h->n_chunks, ctx->grid_move);
-    CK(launch_move((uint8_t*)ctx->buf.arena, (uint8_t*)ctx->buf.staging, ctx->entries, h->n_entries, h->n_chunks,
-                   ctx->S, ctx->ctrl64, ctx->flags, ctx->epoch, staged ? 1 : 0, grid, ctx->st), "k_move");
+    const int grid = (int)std::min<int64_t>((h->n_chunks + 2 * 3 - 1) / (2 * 3), ctx->grid_move);
+    CK(launch_move((uint8_t*)ctx->buf.arena, (uint8_t*)ctx->buf.staging, ctx->entries, ctx->key_chunk0,
+                   ctx->key_src, h->n_entries, h->n_chunks, ctx->S, sh.kvpt, ctx->ctrl64, ctx->flags, ctx->epoch,
+                   staged ? 1 : 0, grid, ctx->st), "k_move");
     ctx->launches += 1;
     if (ctx->prof.on) {
       cudaEventRecord(e1, ctx->st);

@@ -80,10 +80,13 @@ cudaError_t launch_attn(const Shape& sh, const uint16_t* q, const uint16_t* k_ne
                         const Split* splits, int32_t* ctrl, int32_t B, int32_t l0, int32_t nl,
                         int32_t grid_attn, int32_t grid_combine, cudaStream_t st);
 cudaError_t launch_keep_scan(const Shape& sh, const DSlot* cur, DSlot* next, int32_t B, int64_t S,
-                             void* report, MoveEntry* entries, int64_t* ctrl64, cudaStream_t st);
-cudaError_t launch_move(uint8_t* arena, uint8_t* staging, const MoveEntry* entries, int32_t n_entries,
-                        int64_t n_chunks, int64_t S, int64_t* ctrl64, uint32_t* flags, uint32_t epoch,
-                        int32_t staging_enabled, int32_t grid, cudaStream_t st);
+                             void* report, MoveEntry* entries, int32_t* key_chunk0, int32_t* key_src,
+                             int64_t* ctrl64, cudaStream_t st);
+cudaError_t launch_move(uint8_t* arena, uint8_t* staging, const MoveEntry* entries, const int32_t* key_chunk0,
+                        const int32_t* key_src, int32_t n_entries, int64_t n_chunks, int64_t S, int64_t kvpt,
+                        int64_t* ctrl64, uint32_t* flags, uint32_t epoch, int32_t staging_enabled, int32_t grid,
+                        cudaStream_t st);
+int move_smem_bytes(int64_t S, int32_t n_entries, int32_t* keys_in_smem);
 cudaError_t launch_fill(const Shape& sh, uint64_t seed, const DSlot* slots, const int32_t* list,
                         int32_t n, int32_t max_prompt, uint16_t* arena, cudaStream_t st);
 cudaError_t launch_synth(const Shape& sh, uint64_t seed, const DSlot* slots, int32_t B, int32_t l0,

@@ -397,6 +397,8 @@ __global__ void __launch_bounds__(1024) k_keep_scan(Shape sh, const DSlot* __res
                                                     DSlot* __restrict__ next, int32_t B, int64_t S,
                                                     uint8_t* __restrict__ report,
                                                     MoveEntry* __restrict__ entries,
+                                                    int32_t* __restrict__ key_chunk0,
+                                                    int32_t* __restrict__ key_src,
                                                     int64_t* __restrict__ ctrl64) {
   __shared__ int s_first_hole;
   __shared__ unsigned long long s_hbm;
@@ -475,6 +477,8 @@ __global__ void __launch_bounds__(1024) k_keep_scan(Shape sh, const DSlot* __res
           MoveEntry me;
           me.src = (int64_t)sl.off * kvpt; me.dst = new_off * kvpt; me.bytes = bytes;
           me.chunk0 = chunk; me.kind = MOVE_ARENA; me.pad0 = 0; me.pad1 = 0;
+          key_chunk0[e_i] = (int32_t)chunk;
+          key_src[e_i] = sl.off;
           entries[e_i++] = me;
           chunk += (bytes + S - 1) / S;
         }
@@ -484,6 +488,8 @@ __global__ void __launch_bounds__(1024) k_keep_scan(Shape sh, const DSlot* __res
           MoveEntry me;
           me.src = (int64_t)sl.off * kvpt; me.dst = evb; me.bytes = bytes;
           me.chunk0 = chunk; me.kind = MOVE_STAGE; me.pad0 = 0; me.pad1 = 0;
+          key_chunk0[e_i] = (int32_t)chunk;
+          key_src[e_i] = sl.off;
           entries[e_i++] = me;
           chunk += (bytes + S - 1) / S;
         }
@@ -508,86 +514,199 @@ __global__ void __launch_bounds__(1024) k_keep_scan(Shape sh, const DSlot* __res
     h->first_hole = s_first_hole;
     ctrl64[CTRL64_TICKET] = 0;
     ctrl64[CTRL64_N_CHUNKS] = ytot[1];
+    key_chunk0[ytot[0]] = (int32_t)ytot[1];
   }
 }
 
 // ---------------------------------------------------------------------------
-// k_move: ordered in-place compaction.  Chunks (S bytes) are numbered in
-// source order (= arena order); a CTA takes chunk tickets in that order,
-// reads its chunk into shared memory, publishes "read done", then -- only for
-// arena destinations -- waits until every chunk whose SOURCE overlaps its
-// DESTINATION has been read, and writes.  Every source lies at or above its
-// destination, so those chunks all hold earlier tickets and never wait on
-// later ones: no deadlock.  Evicted slots are chunks
-// too (copied to the staging buffer), so survivors never overwrite an
-// evicted row before it has been staged.
+// k_move: ordered in-place compaction (+ eviction staging) on the TMA bulk
+// copy engine.
+//
+// The bytes to move form "entries" (moved survivors and evicted slots) in
+// SOURCE order (= arena order), cut into chunks of S bytes numbered in that
+// order.  Every CTA runs MV_NP independent (producer, consumer) thread pairs,
+// each with MV_NB shared-memory buffers:
+//   producer: take the next chunk ticket (atomic), cp.async.bulk G->S of its
+//             source, completion on an mbarrier;
+//   consumer: when the bytes have landed, publish "read done" for the chunk
+//             (st.release), then -- only for arena destinations -- wait
+//             (ld.acquire) until every chunk whose SOURCE overlaps this
+//             chunk's DESTINATION has been read, and cp.async.bulk S->G.
+// Every source lies at or above its destination, so the awaited chunks hold
+// earlier tickets; the smallest unpublished ticket always sits at the head
+// of its consumer and is published as soon as its load lands, so the wait
+// chain strictly decreases and cannot deadlock.
 // ---------------------------------------------------------------------------
-__device__ int find_entry(const MoveEntry* __restrict__ e, int n, int64_t t) {
-  int lo = 0, hi = n - 1;               // largest i with chunk0 <= t
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      " .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst_smem)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src_smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src_smem)),
+               "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
+constexpr int MV_NP = 3;   // producer/consumer pairs per CTA
+constexpr int MV_NB = 2;   // buffers per pair
+
+struct MoveArgs {
+  uint8_t* arena;
+  uint8_t* staging;
+  const MoveEntry* entries;
+  const int32_t* key_chunk0;   // [n_entries + 1], last = n_chunks
+  const int32_t* key_src;      // [n_entries] source row
+  int32_t n_entries;
+  int32_t keys_in_smem;
+  int64_t n_chunks, S, kvpt;
+  int64_t* ctrl64;
+  uint32_t* flags;
+  uint32_t epoch;
+  int32_t staging_enabled;
+};
+
+__device__ __forceinline__ int chunk_entry(const int32_t* kc, int n, int64_t t) {
+  int lo = 0, hi = n - 1;               // largest e with kc[e] <= t
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
-    if (e[mid].chunk0 <= t) lo = mid; else hi = mid - 1;
+    if (kc[mid] <= t) lo = mid; else hi = mid - 1;
   }
   return lo;
 }
 
-__device__ void wait_sources(const MoveEntry* __restrict__ e, int n, int64_t S, int64_t d0,
-                             int64_t d1, int64_t self, const uint32_t* flags, uint32_t epoch) {
-  int lo = 0, hi = n;                   // first entry with src + bytes > d0
+// Wait until every chunk whose source overlaps [d0, d1) (arena bytes) has
+// been read.  Entry i covers at most [src_i, src_i + nch_i*S); that bound is
+// non-decreasing in i, so the first candidate is found by binary search.
+__device__ void wait_sources(const int32_t* kc, const int32_t* ks, int n, int64_t kvpt, int64_t S,
+                             int64_t d0, int64_t d1, int64_t self, const uint32_t* flags, uint32_t epoch) {
+  int lo = 0, hi = n;
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
-    if (e[mid].src + e[mid].bytes > d0) hi = mid; else lo = mid + 1;
+    if ((int64_t)ks[mid] * kvpt + (int64_t)(kc[mid + 1] - kc[mid]) * S > d0) hi = mid; else lo = mid + 1;
   }
-  for (int i = lo; i < n && e[i].src < d1; ++i) {
-    const int64_t src = e[i].src, nch = (e[i].bytes + S - 1) / S;
+  for (int i = lo; i < n && (int64_t)ks[i] * kvpt < d1; ++i) {
+    const int64_t src = (int64_t)ks[i] * kvpt, nch = kc[i + 1] - kc[i];
     const int64_t c_lo = d0 > src ? (d0 - src) / S : 0;
     const int64_t c_hi = min(nch - 1, (d1 - 1 - src) / S);
     for (int64_t c = c_lo; c <= c_hi; ++c) {
-      const int64_t k = e[i].chunk0 + c;
+      const int64_t k = kc[i] + c;
       if (k == self) continue;
-      while (ld_acquire_u32(flags + k) != epoch) __nanosleep(64);
+      while (ld_acquire_u32(flags + k) != epoch) __nanosleep(32);
     }
   }
 }
 
-__global__ void __launch_bounds__(256) k_move(uint8_t* __restrict__ arena, uint8_t* __restrict__ staging,
-                                              const MoveEntry* __restrict__ entries, int32_t n_entries,
-                                              int64_t n_chunks, int64_t S, int64_t* ctrl64,
-                                              uint32_t* flags, uint32_t epoch, int32_t staging_enabled) {
-  extern __shared__ uint4 buf[];
-  __shared__ long long s_t;
-  __shared__ int s_e;
-  for (;;) {
-    if (threadIdx.x == 0) {
-      const long long t = atomicAdd(reinterpret_cast<unsigned long long*>(&ctrl64[CTRL64_TICKET]), 1ull);
-      s_t = t;
-      s_e = t < n_chunks ? find_entry(entries, n_entries, t) : 0;
-    }
-    __syncthreads();
-    const int64_t t = s_t;
-    if (t >= n_chunks) break;
-    const MoveEntry me = entries[s_e];
-    const int64_t pos = (t - me.chunk0) * S;
-    const int64_t nb = min(S, me.bytes - pos);
-    const int nv = (int)(nb >> 4);
-    const uint8_t* src = arena + me.src + pos;
-    const bool copy = me.kind == MOVE_ARENA || staging_enabled;
-    if (copy)
-      for (int i = threadIdx.x; i < nv; i += blockDim.x) buf[i] = ld_stream(src + 16 * (int64_t)i);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      st_release_u32(flags + t, epoch);
-      if (me.kind == MOVE_ARENA)
-        wait_sources(entries, n_entries, S, me.dst + pos, me.dst + pos + nb, t, flags, epoch);
-    }
-    __syncthreads();
-    if (copy) {
-      uint8_t* dst = (me.kind == MOVE_ARENA ? arena : staging) + me.dst + pos;
-      for (int i = threadIdx.x; i < nv; i += blockDim.x) st_v4(dst + 16 * (int64_t)i, buf[i]);
-    }
-    __syncthreads();
+__global__ void __launch_bounds__(64 * MV_NP) k_move(MoveArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int64_t S = a.S;
+  uint8_t* bufs = smem;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)MV_NP * MV_NB * S);
+  uint64_t* empty = full + MV_NP * MV_NB;
+  long long* tix = reinterpret_cast<long long*>(empty + MV_NP * MV_NB);
+  int32_t* ent = reinterpret_cast<int32_t*>(tix + MV_NP * MV_NB);
+  int32_t* skeys = ent + MV_NP * MV_NB;
+  const int n = a.n_entries;
+  const int32_t* kc = a.key_chunk0;
+  const int32_t* ks = a.key_src;
+  if (a.keys_in_smem) {
+    for (int i = threadIdx.x; i <= n; i += blockDim.x) skeys[i] = a.key_chunk0[i];
+    for (int i = threadIdx.x; i < n; i += blockDim.x) skeys[n + 1 + i] = a.key_src[i];
+    kc = skeys;
+    ks = skeys + n + 1;
   }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < MV_NP * MV_NB; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane != 0) return;
+  const int pair = warp >> 1;
+  uint8_t* pb = bufs + (size_t)pair * MV_NB * S;
+  uint64_t* pf = full + pair * MV_NB;
+  uint64_t* pe = empty + pair * MV_NB;
+  long long* pt = tix + pair * MV_NB;
+  int32_t* pen = ent + pair * MV_NB;
+  unsigned long long* ticket = reinterpret_cast<unsigned long long*>(&a.ctrl64[CTRL64_TICKET]);
+  if ((warp & 1) == 0) {
+    // ---------------- producer ----------------
+    for (int k = 0;; ++k) {
+      const int i = k % MV_NB;
+      const uint32_t ph = (uint32_t)(k / MV_NB) & 1u;
+      mbar_wait(&pe[i], ph ^ 1u);                    // buffer free (passes at once on first use)
+      const long long t = (long long)atomicAdd(ticket, 1ull);
+      pt[i] = t;
+      if (t >= a.n_chunks) { mbar_arrive(&pf[i]); break; }
+      const int e = chunk_entry(kc, n, t);
+      pen[i] = e;
+      const MoveEntry me = a.entries[e];
+      const int64_t pos = (t - kc[e]) * S;
+      const uint32_t nb = (uint32_t)min(S, me.bytes - pos);
+      if (me.kind == MOVE_ARENA || a.staging_enabled) {
+        mbar_arrive_expect_tx(&pf[i], nb);
+        bulk_g2s(pb + (size_t)i * S, a.arena + me.src + pos, nb, &pf[i]);
+      } else {
+        mbar_arrive(&pf[i]);                         // evicted, not staged: nothing to copy
+      }
+    }
+  } else {
+    // ---------------- consumer ----------------
+    for (int k = 0;; ++k) {
+      const int i = k % MV_NB;
+      const uint32_t ph = (uint32_t)(k / MV_NB) & 1u;
+      mbar_wait(&pf[i], ph);
+      const long long t = pt[i];
+      if (t >= a.n_chunks) break;
+      const int e = pen[i];
+      const MoveEntry me = a.entries[e];
+      const int64_t pos = (t - kc[e]) * S;
+      const uint32_t nb = (uint32_t)min(S, me.bytes - pos);
+      st_release_u32(a.flags + t, a.epoch);          // source chunk t has been read
+      if (me.kind == MOVE_ARENA) {
+        wait_sources(kc, ks, n, a.kvpt, S, me.dst + pos, me.dst + pos + nb, t, a.flags, a.epoch);
+        asm volatile("fence.proxy.async;" ::: "memory");
+        bulk_s2g(a.arena + me.dst + pos, pb + (size_t)i * S, nb);
+      } else if (a.staging_enabled) {
+        bulk_s2g(a.staging + me.dst + pos, pb + (size_t)i * S, nb);
+      }
+      mbar_arrive(&pe[i]);
+    }
+  }
+}
+
+int move_smem_bytes(int64_t S, int32_t n_entries, int32_t* keys_in_smem) {
+  const int64_t base = (int64_t)MV_NP * MV_NB * (S + 8 + 8 + 8 + 4);
+  const int64_t keys = 4LL * (2LL * n_entries + 1);
+  const int64_t limit = 227 * 1024;
+  *keys_in_smem = base + keys <= limit;
+  return (int)(base + (*keys_in_smem ? keys : 0));
 }
 
 // ---------------------------------------------------------------------------
@@ -727,16 +846,22 @@ cudaError_t launch_attn(const Shape& sh, const uint16_t* q, const uint16_t* k_ne
 }
 
 cudaError_t launch_keep_scan(const Shape& sh, const DSlot* cur, DSlot* next, int32_t B, int64_t S,
-                             void* report, MoveEntry* entries, int64_t* ctrl64, cudaStream_t st) {
-  k_keep_scan<<<1, 1024, 0, st>>>(sh, cur, next, B, S, (uint8_t*)report, entries, ctrl64);
+                             void* report, MoveEntry* entries, int32_t* key_chunk0, int32_t* key_src,
+                             int64_t* ctrl64, cudaStream_t st) {
+  k_keep_scan<<<1, 1024, 0, st>>>(sh, cur, next, B, S, (uint8_t*)report, entries, key_chunk0, key_src, ctrl64);
   return cudaGetLastError();
 }
 
-cudaError_t launch_move(uint8_t* arena, uint8_t* staging, const MoveEntry* entries, int32_t n_entries,
-                        int64_t n_chunks, int64_t S, int64_t* ctrl64, uint32_t* flags, uint32_t epoch,
-                        int32_t staging_enabled, int32_t grid, cudaStream_t st) {
-  k_move<<<grid, 256, (size_t)S, st>>>(arena, staging, entries, n_entries, n_chunks, S, ctrl64, flags,
-                                        epoch, staging_enabled);
+cudaError_t launch_move(uint8_t* arena, uint8_t* staging, const MoveEntry* entries, const int32_t* key_chunk0,
+                        const int32_t* key_src, int32_t n_entries, int64_t n_chunks, int64_t S, int64_t kvpt,
+                        int64_t* ctrl64, uint32_t* flags, uint32_t epoch, int32_t staging_enabled, int32_t grid,
+                        cudaStream_t st) {
+  MoveArgs a;
+  a.arena = arena; a.staging = staging; a.entries = entries; a.key_chunk0 = key_chunk0; a.key_src = key_src;
+  a.n_entries = n_entries; a.n_chunks = n_chunks; a.S = S; a.kvpt = kvpt; a.ctrl64 = ctrl64; a.flags = flags;
+  a.epoch = epoch; a.staging_enabled = staging_enabled;
+  const int smem = move_smem_bytes(S, n_entries, &a.keys_in_smem);
+  k_move<<<grid, 64 * MV_NP, (size_t)smem, st>>>(a);
   return cudaGetLastError();
 }
 
