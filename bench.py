@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--arena-gb", type=float, default=0.0, help="cap the arena (e.g. for ncu replay)")
+    ap.add_argument("--attn", default="tma", choices=["tma", "regs"], help="attention kernel variant")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend of the counter exchange (gloo: tests sharing one GPU)")
     return ap.parse_args()
@@ -233,7 +234,8 @@ def run_s3(args):
     if args.arena_gb > 0:
         R = min(R, int(args.arena_gb * 1e9 // kvpt))
     eng = S3Engine(L, H, D, GPTJ["max_len"], R, max_running, device=local, rank=rank, world=world,
-                   seed=args.seed, staging_bytes=staging, host_store_bytes=(16 << 30) if p > 0 else (1 << 30))
+                   seed=args.seed, staging_bytes=staging, host_store_bytes=(16 << 30) if p > 0 else (1 << 30),
+                   attn_variant=0 if args.attn == "tma" else 1)
 
     exchange = None
     if world > 1:
@@ -316,7 +318,7 @@ def run_s3(args):
                 "l2": "working set (tens of GB per step) >> 126 MB L2; no flush needed",
             },
             "roofline": {
-                "bound": "hbm", "kernel": "k_attn+k_combine (decode attention)",
+                "bound": "hbm", "kernel": ("k_attn_tma" if args.attn == "tma" else "k_attn") + "+k_combine (decode attention)",
                 "achieved": attn_gbs, "peak": peak, "unit": "GB/s", "frac": attn_gbs / peak,
                 "peak_source": peak_kind,
                 "traffic": tr.get("dram_bytes_per_launch") if tr else None,

@@ -72,6 +72,8 @@ typedef struct {
   void*   stream;                           /* cudaStream_t for all device work                */
   int32_t rank, world;                      /* multi-GPU partition by sequence (world >= 1)    */
   uint64_t synth_seed;                      /* generator seed for the prompt-fill stand-in     */
+  int32_t attn_variant;                     /* 0 = TMA-staged ring (default), 1 = register stream */
+  int32_t reserved0;
 } s3_config;
 
 typedef struct {                            /* caller-owned memory                             */

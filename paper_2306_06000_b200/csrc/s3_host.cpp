@@ -164,6 +164,7 @@ bool validate(const s3_config* c) {
   if (c->chunk_rows < 0 || c->move_chunk_bytes < 0 || c->move_chunk_bytes % 16) return false;
   if (c->move_chunk_bytes > 0 && (c->move_chunk_bytes < 1024 || c->move_chunk_bytes > 36864)) return false;
   if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return false;
+  if (c->attn_variant < 0 || c->attn_variant > 1) return false;
   return true;
 }
 
@@ -373,6 +374,14 @@ s3_status s3_kv_init(const s3_config* cfg, const s3_buffers* b, s3_ctx** out) {
   if (!ka) return bail("head_dim");
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ka, attn_block_threads(sh), 0);
   ctx->grid_attn = ctx->num_sms * std::max(1, occ);
+  if (cfg->attn_variant == 0 && attn_tma_stages(sh) >= 2) {
+    const int smem = attn_tma_smem(sh, attn_tma_stages(sh));
+    if (cudaFuncSetAttribute(attn_tma_kernel_ptr(sh), cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+      return bail("attn smem attribute");
+    int occ2 = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, attn_tma_kernel_ptr(sh), attn_block_threads(sh) + 32, smem);
+    ctx->grid_attn = ctx->num_sms * std::max(1, occ2);
+  }
   ctx->grid_combine = ctx->num_sms * 4;
   cudaFuncSetAttribute(move_kernel_ptr(), cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
   ctx->grid_move = ctx->num_sms;   // one CTA per SM (its buffers fill most of shared memory)
@@ -459,7 +468,7 @@ s3_status s3_decode_step(s3_ctx* ctx, int32_t l0, int32_t nl, const void* q, con
     if (ctx->prof.on) { e0 = ctx->prof.get(); e1 = ctx->prof.get(); cudaEventRecord(e0, ctx->st); }
     CK(launch_attn(ctx->sh, (const uint16_t*)q, (const uint16_t*)k_new, (const uint16_t*)v_new,
                    (uint16_t*)ctx->buf.arena, out, ctx->partials, ctx->units, ctx->splits, ctx->ctrl, B, l0, nl,
-                   ctx->grid_attn, ctx->grid_combine, ctx->st), "k_attn");
+                   ctx->grid_attn, ctx->grid_combine, ctx->cfg.attn_variant, ctx->st), "k_attn");
     if (ctx->prof.on) {
       cudaEventRecord(e1, ctx->st);
       int64_t sum_len = 0;

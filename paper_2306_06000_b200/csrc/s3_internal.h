@@ -78,7 +78,7 @@ cudaError_t launch_prep(const Shape& sh, DSlot* slots, int32_t B, int32_t C, con
 cudaError_t launch_attn(const Shape& sh, const uint16_t* q, const uint16_t* k_new, const uint16_t* v_new,
                         uint16_t* arena, float* out, float* partials, const Unit* units,
                         const Split* splits, int32_t* ctrl, int32_t B, int32_t l0, int32_t nl,
-                        int32_t grid_attn, int32_t grid_combine, cudaStream_t st);
+                        int32_t grid_attn, int32_t grid_combine, int32_t variant, cudaStream_t st);
 cudaError_t launch_keep_scan(const Shape& sh, const DSlot* cur, DSlot* next, int32_t B, int64_t S,
                              void* report, MoveEntry* entries, int32_t* key_chunk0, int32_t* key_src,
                              int64_t* ctrl64, cudaStream_t st);
@@ -96,6 +96,9 @@ cudaError_t launch_verify(const Shape& sh, uint64_t seed, const DSlot* slots, in
                           const uint16_t* arena, unsigned long long* bad, cudaStream_t st);
 
 int attn_block_threads(const Shape& sh);
+int attn_tma_stages(const Shape& sh);
+int attn_tma_smem(const Shape& sh, int ns);
+const void* attn_tma_kernel_ptr(const Shape& sh);
 const void* attn_kernel_ptr(const Shape& sh);
 const void* move_kernel_ptr();
 

@@ -710,6 +710,192 @@ int move_smem_bytes(int64_t S, int32_t n_entries, int32_t* keys_in_smem) {
 }
 
 // ---------------------------------------------------------------------------
+// k_attn_tma: the same computation as k_attn with the KV stream staged by
+// the TMA bulk-copy engine.  One producer warp (one elected thread) takes
+// items (unit, layer) from the queue and streams each item's rows -- one
+// contiguous 4*H*D-byte layer-row (K of all heads, then V) per
+// cp.async.bulk -- plus the item's q into an AT_NS-stage shared-memory ring
+// (mbarrier full/empty per stage).  H*D/256 consumer warps (D/8 lanes per
+// head) read K/V from shared memory with 128-bit loads and run the same
+// online softmax as k_attn.  The ring keeps up to AT_NS*AT_RPS rows per SM
+// in flight without spending registers on them.
+// ---------------------------------------------------------------------------
+constexpr int AT_RPS = 4;      // rows per stage
+constexpr int AT_NS_MAX = 8;
+
+struct StageHdr {
+  int32_t item, r0, n, flags;  // flags: 1 = first stage of the item, 2 = last, 4 = unit has the new row
+  int32_t b, part, off, len;   // the item's unit (so consumers never load it from global)
+};
+
+__device__ __forceinline__ uint4 lds128(const void* p) {
+  uint4 r;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "r"(smem_u32(p)));
+  return r;
+}
+
+template <int D>
+__global__ void __launch_bounds__(544, 1) k_attn_tma(AttnArgs a, int32_t ns) {
+  constexpr int LPH = D / 8;
+  constexpr int HPW = 32 / LPH;
+  extern __shared__ __align__(128) uint8_t smem[];
+  const int H = a.sh.H;
+  const int64_t HD = (int64_t)H * D;
+  const int64_t rowB = 4 * HD;                     // one layer-row: K and V of all heads
+  const int64_t stageB = AT_RPS * rowB + 2 * HD;   // rows + q of the item
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + ns * stageB);
+  uint64_t* empty = full + ns;
+  StageHdr* hdr = reinterpret_cast<StageHdr*>(empty + ns);
+  const int nwarps = blockDim.x >> 5;
+  const int nwc = nwarps - 1;                      // consumer warps; the last warp produces
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < ns; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], nwc); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int n_units = a.ctrl[CTRL_N_UNITS];
+  const int total = n_units * a.nl;
+  const uint8_t* arena = reinterpret_cast<const uint8_t*>(a.arena);
+  if (warp == nwc) {
+    // ------------------------------ producer ------------------------------
+    if (lane == 0) {
+      int k = 0;
+      for (;;) {
+        const int item = atomicAdd(&a.ctrl[CTRL_ITEM], 1);
+        if (item >= total) {
+          const int st = k % ns;
+          mbar_wait(&empty[st], ((uint32_t)(k / ns) & 1u) ^ 1u);
+          hdr[st].item = -1;
+          mbar_arrive(&full[st]);
+          break;
+        }
+        const int u = item / a.nl, li = item - u * a.nl;
+        const Unit un = a.units[u];
+        const uint8_t* base = arena + (int64_t)un.off * a.sh.kvpt + (int64_t)(a.l0 + li) * rowB;
+        const uint16_t* qsrc = a.q + ((int64_t)li * a.B + un.b) * HD;
+        int r = un.r0;
+        do {
+          const int st = k % ns;
+          mbar_wait(&empty[st], ((uint32_t)(k / ns) & 1u) ^ 1u);
+          const int n = min(AT_RPS, un.r1 - r);
+          const bool first = r == un.r0;
+          hdr[st].item = item; hdr[st].r0 = r; hdr[st].n = n;
+          hdr[st].flags = (first ? 1 : 0) | (r + n >= un.r1 ? 2 : 0) | (un.has_new ? 4 : 0);
+          hdr[st].b = un.b; hdr[st].part = un.part; hdr[st].off = un.off; hdr[st].len = un.len;
+          const uint32_t tx = (uint32_t)(n * rowB + (first ? 2 * HD : 0));
+          uint8_t* sb = smem + st * stageB;
+          if (tx) {
+            mbar_arrive_expect_tx(&full[st], tx);
+            if (first) bulk_g2s(sb + AT_RPS * rowB, qsrc, (uint32_t)(2 * HD), &full[st]);
+            for (int i = 0; i < n; ++i)
+              bulk_g2s(sb + i * rowB, base + (int64_t)(r + i) * a.sh.kvpt, (uint32_t)rowB, &full[st]);
+          } else {
+            mbar_arrive(&full[st]);
+          }
+          r += n;
+          ++k;
+        } while (r < un.r1);
+      }
+    }
+    return;
+  }
+  // -------------------------------- consumers --------------------------------
+  const int head = warp * HPW + lane / LPH;
+  const int sub = lane % LPH;
+  const bool active = head < H;
+  const int hh = active ? head : H - 1;
+  const int64_t rowE = a.sh.row_elems;
+  float qf[8], m = -INFINITY, ssum = 0.f, acc[8];
+  int li = 0;
+  for (int k = 0;; ++k) {
+    const int st = k % ns;
+    mbar_wait(&full[st], (uint32_t)(k / ns) & 1u);
+    const StageHdr h = hdr[st];
+    if (h.item < 0) break;
+    const uint8_t* sb = smem + st * stageB;
+    if (h.flags & 1) {
+      li = h.item % a.nl;
+      unpack8(lds128(sb + AT_RPS * rowB + (hh * D + sub * 8) * 2), qf);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) { qf[e] *= a.qscale; acc[e] = 0.f; }
+      m = -INFINITY;
+      ssum = 0.f;
+    }
+    const int64_t io = ((int64_t)li * a.B + h.b) * HD + hh * D + sub * 8;
+    uint4 kr = make_uint4(0, 0, 0, 0), vr = kr;
+    const bool last_new = (h.flags & 2) && (h.flags & 4);
+    if (last_new) {              // issue the new row's loads early; used after the stage
+      kr = ld_plain(a.k_new + io);
+      vr = ld_plain(a.v_new + io);
+    }
+    if (h.n > 0) {
+      uint4 kc[AT_RPS], vc[AT_RPS];
+#pragma unroll
+      for (int i = 0; i < AT_RPS; ++i) {
+        if (i < h.n) {
+          kc[i] = lds128(sb + i * rowB + (hh * D + sub * 8) * 2);
+          vc[i] = lds128(sb + i * rowB + (HD + hh * D + sub * 8) * 2);
+        } else {
+          kc[i] = make_uint4(0, 0, 0, 0);
+          vc[i] = kc[i];
+        }
+      }
+      attn_rows<D, AT_RPS>(kc, vc, h.n, qf, m, ssum, acc);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+    if (h.flags & 2) {
+      if (last_new) {
+        uint16_t* kdst = a.arena + (int64_t)(h.off + h.len) * rowE + (int64_t)(a.l0 + li) * 2 * HD + hh * D + sub * 8;
+        if (active) {
+          st_v4(kdst, kr);
+          st_v4(kdst + HD, vr);
+        }
+        uint4 k1[1] = {kr}, v1[1] = {vr};
+        attn_rows<D, 1>(k1, v1, 1, qf, m, ssum, acc);
+      }
+      if (active) {
+        if (h.part < 0) {
+          const float inv = 1.f / ssum;
+          float4* o = reinterpret_cast<float4*>(a.out + io);
+          o[0] = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+          o[1] = make_float4(acc[4] * inv, acc[5] * inv, acc[6] * inv, acc[7] * inv);
+        } else {
+          float* pr = a.partials + (((int64_t)h.part * a.nl + li) * H + hh) * (D + 4);
+          float4* o = reinterpret_cast<float4*>(pr + sub * 8);
+          o[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+          o[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+          if (sub == 0) { pr[D] = m; pr[D + 1] = ssum; }
+        }
+      }
+    }
+  }
+}
+
+int attn_tma_stages(const Shape& sh) {
+  const int64_t HD = (int64_t)sh.H * sh.D;
+  const int64_t stageB = AT_RPS * 4 * HD + 2 * HD;
+  const int64_t per = stageB + 16 + sizeof(StageHdr);
+  const int64_t ns = (227 * 1024 - 64) / per;
+  return (int)std::min<int64_t>(ns, AT_NS_MAX);
+}
+int attn_tma_smem(const Shape& sh, int ns) {
+  const int64_t HD = (int64_t)sh.H * sh.D;
+  return (int)(ns * (AT_RPS * 4 * HD + 2 * HD) + ns * (16 + (int64_t)sizeof(StageHdr)));
+}
+const void* attn_tma_kernel_ptr(const Shape& sh) {
+  switch (sh.D) {
+    case 64: return (const void*)k_attn_tma<64>;
+    case 128: return (const void*)k_attn_tma<128>;
+    case 256: return (const void*)k_attn_tma<256>;
+    default: return nullptr;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // k_fill: prompt rows 0..P-1 of freshly admitted slots (stand-in for the
 // model's prefill).  grid = (row groups, admitted slots).
 // ---------------------------------------------------------------------------
@@ -820,23 +1006,29 @@ cudaError_t launch_prep(const Shape& sh, DSlot* slots, int32_t B, int32_t C, con
 cudaError_t launch_attn(const Shape& sh, const uint16_t* q, const uint16_t* k_new, const uint16_t* v_new,
                         uint16_t* arena, float* out, float* partials, const Unit* units,
                         const Split* splits, int32_t* ctrl, int32_t B, int32_t l0, int32_t nl,
-                        int32_t grid_attn, int32_t grid_combine, cudaStream_t st) {
+                        int32_t grid_attn, int32_t grid_combine, int32_t variant, cudaStream_t st) {
   AttnArgs a;
   a.sh = sh; a.q = q; a.k_new = k_new; a.v_new = v_new; a.arena = arena; a.out = out;
   a.partials = partials; a.units = units; a.ctrl = ctrl; a.B = B; a.l0 = l0; a.nl = nl;
   a.qscale = 1.4426950408889634f / sqrtf((float)sh.D);
   const int threads = attn_block_threads(sh);
+  const int ns = attn_tma_stages(sh);
+  const bool tma = variant == 0 && ns >= 2;
+  const int smem = tma ? attn_tma_smem(sh, ns) : 0;
   switch (sh.D) {
     case 64:
-      k_attn<64><<<grid_attn, threads, 0, st>>>(a);
+      if (tma) k_attn_tma<64><<<grid_attn, threads + 32, smem, st>>>(a, ns);
+      else k_attn<64><<<grid_attn, threads, 0, st>>>(a);
       k_combine<64><<<grid_combine, 256, 0, st>>>(splits, partials, out, ctrl, sh.H, B, nl);
       break;
     case 128:
-      k_attn<128><<<grid_attn, threads, 0, st>>>(a);
+      if (tma) k_attn_tma<128><<<grid_attn, threads + 32, smem, st>>>(a, ns);
+      else k_attn<128><<<grid_attn, threads, 0, st>>>(a);
       k_combine<128><<<grid_combine, 256, 0, st>>>(splits, partials, out, ctrl, sh.H, B, nl);
       break;
     case 256:
-      k_attn<256><<<grid_attn, threads, 0, st>>>(a);
+      if (tma) k_attn_tma<256><<<grid_attn, threads + 32, smem, st>>>(a, ns);
+      else k_attn<256><<<grid_attn, threads, 0, st>>>(a);
       k_combine<256><<<grid_combine, 256, 0, st>>>(splits, partials, out, ctrl, sh.H, B, nl);
       break;
     default:
