@@ -291,6 +291,9 @@ def run_s3(args):
     value = tok_sum / (ms_max / 1e3)
     launches = prof.kernel_launches - p0.kernel_launches
 
+    # ---- per-phase breakdown (after the timed region; CUDA events) ---------
+    phases = phase_breakdown(eng, exchange, world, min(args.steps, 20))
+
     # ---- e2e through the public API with host buffers ----------------------
     e2e = None
     if not args.no_e2e:
@@ -332,6 +335,7 @@ def run_s3(args):
             },
             "tokens": tok_sum, "finished": totals["finished"], "admitted": totals["admitted"],
             "gpu_launches": launches,
+            "phases_ms_per_step": phases,
             "clocks": clk,
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -340,6 +344,34 @@ def run_s3(args):
     eng.close()
     if dist:
         dist.destroy_process_group()
+
+
+def phase_breakdown(eng, exchange, world, steps):
+    """Mean device time per step of each call (events on the launch stream;
+    host work between calls lands in the following phase)."""
+    import torch
+    names = ["synth_inputs", "decode", "evict_compact", "admit"]
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(names) + 1)]
+    acc = dict.fromkeys(names, 0.0)
+    for _ in range(steps):
+        ev[0].record()
+        if eng.B:
+            eng.synth_inputs()
+        ev[1].record()
+        eng.decode()
+        ev[2].record()
+        eng.evict_compact()
+        ev[3].record()
+        if world == 1:
+            eng.admit()
+        else:
+            eng.admit_home()
+            eng.admit_shared(exchange(eng.counters_local()))
+        ev[4].record()
+        torch.cuda.synchronize()
+        for i, n in enumerate(names):
+            acc[n] += ev[i].elapsed_time(ev[i + 1])
+    return {n: round(v / max(steps, 1), 4) for n, v in acc.items()}
 
 
 def e2e_leg(eng, exchange, dist, dev, steps, world):

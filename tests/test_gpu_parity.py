@@ -228,3 +228,71 @@ def test_bench_configuration_sampled():
             assert eng.verify_resident() == 0, step
     print("evictions", evictions)
     eng.close()
+
+
+def test_layer_group_calls():
+    """s3_decode_step over layer groups [0,1), [1,3), [3,4): the append and the
+    detection happen only with the last group; results equal one full call."""
+    from paper_2306_06000_b200.engine import S3Engine
+    L, H, D, M, R = 4, 4, 128, 96, 600
+    t = s3synth.make_trace(30, seed=12, policy="short", p=0.3, max_seq_len=M, prompt_max=20)
+    eng = S3Engine(L, H, D, M, R, 64, chunk_rows=8, move_chunk_bytes=2048, host_store_bytes=16 << 20)
+    orc = oracle.Oracle(L, H, D, M, R, max_running=64)
+    eng.submit(t.req_id, t.prompt, t.alloc, t.out)
+    orc.submit(t.req_id, t.prompt, t.alloc)
+    assert eng.admit()[1] == orc.admit()
+    HD = H * D
+    for step in range(40):
+        B = orc.B
+        if B == 0:
+            break
+        q, k, v, eos = orc.make_inputs(t.out)
+        ref, _ = orc.decode(q, k, v, eos)
+        eng.synth_inputs()
+        for (l0, nl) in [(0, 1), (1, 2), (3, 1)]:
+            o = l0 * B * HD
+            eng.decode(l0, nl, q=eng.q[o:], k_new=eng.k_new[o:], v_new=eng.v_new[o:], out=eng.out[o:])
+        got = eng.out[:L * B * HD].cpu().numpy().reshape(L, B, H, D).astype(np.float64)
+        assert rel_err(got, ref) <= TOL
+        rg = eng.evict_compact()
+        ro = orc.evict_compact()
+        assert rg[1] == list(ro[1]) and rg[0].d2h_bytes == ro[0].d2h_bytes
+        assert eng.admit()[1] == orc.admit()
+        assert eng.batch_view() == orc.batch()
+    assert eng.verify_resident() == 0
+    eng.close()
+
+
+def test_abi_error_codes_and_empty_batch():
+    from paper_2306_06000_b200 import s3 as abi
+    from paper_2306_06000_b200.engine import S3Engine
+    eng = S3Engine(1, 2, 64, 64, 64, 8, host_store_bytes=1 << 20)
+    # empty batch: a decode step and an evict/compact are legal no-ops
+    eng.decode()
+    rep, perm, ev, fin = eng.evict_compact()
+    assert rep.n_before == 0 and rep.tail_rows == 0 and perm == [] and ev == []
+    with pytest.raises(abi.S3Error) as e:          # no decode since the last evict
+        eng.evict_compact()
+    assert e.value.code == abi.S3_E_STATE
+    with pytest.raises(abi.S3Error) as e:          # prompt + alloc > max_seq_len
+        eng.submit([0], [60], [10])
+    assert e.value.code == abi.S3_E_INVAL
+    with pytest.raises(abi.S3Error) as e:          # alloc < 1
+        eng.submit([0], [3], [0])
+    assert e.value.code == abi.S3_E_INVAL
+    eng.submit([0, 1], [3, 4], [5, 6], [9, 9])
+    eng.admit()
+    with pytest.raises(abi.S3Error) as e:          # layer range
+        abi.s3_decode_step(eng.ctx, 0, 2, eng.q, eng.k_new, eng.v_new, eng.eos, eng.out)
+    assert e.value.code == abi.S3_E_INVAL
+    eng.synth_inputs()
+    eng.decode()
+    with pytest.raises(abi.S3Error) as e:          # statuses not consumed
+        eng.decode()
+    assert e.value.code == abi.S3_E_STATE
+    with pytest.raises(abi.S3Error) as e:
+        eng.admit()
+    assert e.value.code == abi.S3_E_STATE
+    rep, perm, ev, fin = eng.evict_compact()     # state intact after the errors
+    assert rep.n_before == 2
+    eng.close()
