@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--arena-gb", type=float, default=0.0, help="cap the arena (e.g. for ncu replay)")
     ap.add_argument("--attn", default="tma", choices=["tma", "regs"], help="attention kernel variant")
+    ap.add_argument("--compact", default="fused", choices=["fused", "pass"],
+                    help="row shift as a separate k_move pass, or fused into the attention pass")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend of the counter exchange (gloo: tests sharing one GPU)")
     return ap.parse_args()
@@ -235,7 +237,7 @@ def run_s3(args):
         R = min(R, int(args.arena_gb * 1e9 // kvpt))
     eng = S3Engine(L, H, D, GPTJ["max_len"], R, max_running, device=local, rank=rank, world=world,
                    seed=args.seed, staging_bytes=staging, host_store_bytes=(16 << 30) if p > 0 else (1 << 30),
-                   attn_variant=0 if args.attn == "tma" else 1)
+                   attn_variant=0 if args.attn == "tma" else 1, compact_mode=0 if args.compact == "fused" else 1)
 
     exchange = None
     if world > 1:
@@ -300,7 +302,9 @@ def run_s3(args):
         e2e = e2e_leg(eng, exchange, dist, cdev, min(args.steps, 50), world)
 
     peak, peak_kind = load_peak()
-    attn_gbs = prof.attn_bytes / (prof.attn_ms / 1e3) / 1e9 if prof.attn_ms > 0 else 0.0
+    # the attention launches of fused steps also write the shifted / staged rows
+    attn_kernel_bytes = prof.attn_bytes + prof.fused_move_bytes
+    attn_gbs = attn_kernel_bytes / (prof.attn_ms / 1e3) / 1e9 if prof.attn_ms > 0 else 0.0
     move_gbs = prof.move_bytes / (prof.move_ms / 1e3) / 1e9 if prof.move_ms > 0 else 0.0
     tr = traffic_from_profiles()
     if rank == 0:
@@ -321,14 +325,18 @@ def run_s3(args):
                 "l2": "working set (tens of GB per step) >> 126 MB L2; no flush needed",
             },
             "roofline": {
-                "bound": "hbm", "kernel": ("k_attn_tma" if args.attn == "tma" else "k_attn") + "+k_combine (decode attention)",
+                "bound": "hbm", "kernel": ("k_attn_tma" if args.attn == "tma" else "k_attn") + "+k_combine (decode attention"
+                          + (" fused with the row shift)" if args.compact == "fused" else ")"),
                 "achieved": attn_gbs, "peak": peak, "unit": "GB/s", "frac": attn_gbs / peak,
                 "peak_source": peak_kind,
                 "traffic": tr.get("dram_bytes_per_launch") if tr else None,
-                "algorithmic_bytes_per_launch": prof.attn_bytes / max(prof.attn_launches, 1),
+                "algorithmic_bytes_per_launch": attn_kernel_bytes / max(prof.attn_launches, 1),
+                "attention_bytes_per_launch": prof.attn_bytes / max(prof.attn_launches, 1),
+                "fused_shift_bytes_per_launch": prof.fused_move_bytes / max(prof.attn_launches, 1),
                 "share_of_step": prof.attn_ms / ms,
             },
             "evict_compact": {
+                "mode": args.compact, "fused_steps": prof.fused_steps, "fused_move_bytes": prof.fused_move_bytes,
                 "gbs": move_gbs, "frac": move_gbs / peak, "ms": prof.move_ms, "launches": prof.move_launches,
                 "moved_bytes": totals["moved"], "d2h_bytes": totals["d2h"], "evicted": totals["evicted"],
                 "paper_pcie_bytes": totals["pcie"], "paper_hbm_bytes": totals["hbm"],

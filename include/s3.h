@@ -73,7 +73,11 @@ typedef struct {
   int32_t rank, world;                      /* multi-GPU partition by sequence (world >= 1)    */
   uint64_t synth_seed;                      /* generator seed for the prompt-fill stand-in     */
   int32_t attn_variant;                     /* 0 = TMA-staged ring (default), 1 = register stream */
-  int32_t reserved0;
+  int32_t compact_mode;                     /* 0 = row shift fused into the decode step's
+                                               attention pass when the step is whole (l0 = 0,
+                                               nl = L) and the evictees fit in staging
+                                               (default); 1 = separate ordered-move pass in
+                                               s3_evict_compact                               */
 } s3_config;
 
 typedef struct {                            /* caller-owned memory                             */
@@ -185,9 +189,11 @@ s3_status s3_batch_view(const s3_ctx* ctx, s3_slot* slots /* [B] */, int32_t* B)
 /* ---- timing of the two dominant kernels (CUDA events on cfg.stream) ----- */
 typedef struct {
   int64_t kernel_launches;          /* every kernel this context launched (always counted) */
-  int64_t attn_launches, move_launches;
+  int64_t attn_launches, move_launches, fused_steps;
   double attn_ms, move_ms;          /* summed kernel durations                   */
   double attn_bytes, move_bytes;    /* algorithmic bytes of those launches        */
+  double fused_move_bytes;          /* row-shift + staging bytes written by the attention
+                                       launches of fused steps (part of their traffic)  */
 } s3_profile;
 s3_status s3_profile_enable(s3_ctx* ctx, int32_t on);   /* also resets the sums */
 s3_status s3_profile_get(s3_ctx* ctx, s3_profile* prof); /* synchronises          */

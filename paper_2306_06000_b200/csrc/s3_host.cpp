@@ -77,8 +77,8 @@ struct Prof {
   std::vector<cudaEvent_t> free_events;
   struct Pending { cudaEvent_t a, b; double bytes; int kind; };
   std::vector<Pending> pending;
-  int64_t attn_launches = 0, move_launches = 0;
-  double attn_ms = 0, move_ms = 0, attn_bytes = 0, move_bytes = 0;
+  int64_t attn_launches = 0, move_launches = 0, fused_steps = 0;
+  double attn_ms = 0, move_ms = 0, attn_bytes = 0, move_bytes = 0, fused_move_bytes = 0;
   cudaEvent_t get() {
     if (!free_events.empty()) { cudaEvent_t e = free_events.back(); free_events.pop_back(); return e; }
     cudaEvent_t e;
@@ -109,6 +109,10 @@ struct s3_ctx {
   MoveEntry* entries = nullptr;
   int32_t* key_chunk0 = nullptr;
   int32_t* key_src = nullptr;
+  DepDesc* desc = nullptr;
+  unsigned long long* progress = nullptr;
+  uint32_t attn_epoch = 0;
+  bool fused_pending = false;   // the pending statuses came from a fused decode step
   uint32_t* flags = nullptr;
   uint8_t* report_dev = nullptr;
   unsigned long long* verify_count = nullptr;
@@ -165,6 +169,7 @@ bool validate(const s3_config* c) {
   if (c->move_chunk_bytes > 0 && (c->move_chunk_bytes < 1024 || c->move_chunk_bytes > 36864)) return false;
   if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return false;
   if (c->attn_variant < 0 || c->attn_variant > 1) return false;
+  if (c->compact_mode < 0 || c->compact_mode > 1) return false;
   return true;
 }
 
@@ -177,7 +182,7 @@ Shape make_shape(const s3_config* c) {
 }
 
 struct Carve {
-  int64_t slots, units, splits, partials, ctrl, ctrl64, entries, keys, flags, report, verify, total;
+  int64_t slots, units, splits, partials, ctrl, ctrl64, entries, keys, desc, progress, flags, report, verify, total;
 };
 
 Carve carve(const s3_config* c) {
@@ -198,6 +203,8 @@ Carve carve(const s3_config* c) {
   k.ctrl64 = o;   o += align_up(CTRL64_WORDS * 8);
   k.entries = o;  o += align_up((Bm + 1) * (int64_t)sizeof(MoveEntry));
   k.keys = o;     o += align_up(2 * (Bm + 2) * 4);
+  k.desc = o;     o += align_up((R / AT_RPS + units_max + 2) * (int64_t)sizeof(DepDesc));
+  k.progress = o; o += align_up(units_max * sh.L * 8);
   k.flags = o;    o += align_up(flags_max * 4);
   k.report = o;   o += align_up(report_bytes((int32_t)Bm));
   k.verify = o;   o += align_up(8);
@@ -379,7 +386,7 @@ s3_status s3_kv_init(const s3_config* cfg, const s3_buffers* b, s3_ctx** out) {
     if (cudaFuncSetAttribute(attn_tma_kernel_ptr(sh), cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
       return bail("attn smem attribute");
     int occ2 = 1;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, attn_tma_kernel_ptr(sh), attn_block_threads(sh) + 32, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, attn_tma_kernel_ptr(sh), attn_block_threads(sh) + 64, smem);
     ctx->grid_attn = ctx->num_sms * std::max(1, occ2);
   }
   ctx->grid_combine = ctx->num_sms * 4;
@@ -396,12 +403,15 @@ s3_status s3_kv_init(const s3_config* cfg, const s3_buffers* b, s3_ctx** out) {
   ctx->entries = reinterpret_cast<MoveEntry*>(ws + k.entries);
   ctx->key_chunk0 = reinterpret_cast<int32_t*>(ws + k.keys);
   ctx->key_src = ctx->key_chunk0 + (cfg->max_running + 2);
+  ctx->desc = reinterpret_cast<DepDesc*>(ws + k.desc);
+  ctx->progress = reinterpret_cast<unsigned long long*>(ws + k.progress);
   ctx->flags = reinterpret_cast<uint32_t*>(ws + k.flags);
   ctx->report_dev = ws + k.report;
   ctx->verify_count = reinterpret_cast<unsigned long long*>(ws + k.verify);
   if (cudaMemsetAsync(ws + k.ctrl, 0, CTRL_WORDS * 4, ctx->st) != cudaSuccess) return bail("memset");
   if (cudaMemsetAsync(ws + k.flags, 0, (size_t)(k.report - k.flags), ctx->st) != cudaSuccess) return bail("memset");
-  const int64_t rb = report_bytes(cfg->max_running);
+  if (cudaMemsetAsync(ws + k.progress, 0, (size_t)(k.flags - k.progress), ctx->st) != cudaSuccess) return bail("memset");
+  const int64_t rb = report_bytes(cfg->max_running) + 64;
   if (cudaHostAlloc((void**)&ctx->h_report, (size_t)rb, cudaHostAllocDefault) != cudaSuccess) return bail("pinned");
   ctx->upload_cap = align_up(4 * ((int64_t)cfg->max_running * (sizeof(DSlot) + 4) + 4096));
   if (cudaHostAlloc((void**)&ctx->h_upload, (size_t)ctx->upload_cap, cudaHostAllocDefault) != cudaSuccess)
@@ -459,16 +469,32 @@ s3_status s3_decode_step(s3_ctx* ctx, int32_t l0, int32_t nl, const void* q, con
   if (l0 < 0 || nl < 1 || l0 + nl > ctx->sh.L) return fail(ctx, S3_E_INVAL, "decode_step: layer range");
   const bool finalize = (l0 + nl == ctx->sh.L);
   const int32_t B = (int32_t)ctx->slots_h.size();
+  // fuse the row shift into this attention pass when the step is whole
+  const bool fuse = finalize && l0 == 0 && ctx->cfg.compact_mode == 0 && ctx->cfg.attn_variant == 0 &&
+                    attn_tma_stages(ctx->sh) >= 2 && B > 0;
   if (B > 0) {
     if (!q || !k_new || !v_new || !out || (finalize && !eos)) return fail(ctx, S3_E_INVAL, "decode_step: null");
-    CK(launch_prep(ctx->sh, ctx->slots[ctx->cur], B, ctx->C, eos, finalize ? 1 : 0, ctx->units, ctx->splits,
-                   ctx->ctrl, ctx->st), "k_prep");
-    ctx->launches += 3;   // k_prep, k_attn, k_combine
+    if (fuse && ctx->last_stage_d2h)   // staging is rewritten: the previous step's D2H from it must be done
+      CK(cudaStreamWaitEvent(ctx->st, ctx->last_stage_d2h->ev, 0), "wait staging");
+    PrepArgs pa;
+    pa.sh = ctx->sh; pa.slots = ctx->slots[ctx->cur]; pa.next = ctx->slots[1 - ctx->cur]; pa.B = B; pa.C = ctx->C;
+    pa.eos = eos; pa.finalize = finalize ? 1 : 0; pa.fuse = fuse ? 1 : 0;
+    pa.staging_bytes = ctx->buf.staging ? ctx->buf.staging_bytes : 0;
+    pa.units = ctx->units; pa.splits = ctx->splits; pa.ctrl = ctx->ctrl; pa.report = ctx->report_dev;
+    CK(launch_prep(pa, ctx->st), "k_prep");
+    ctx->launches += 1;
+    if (fuse) {
+      CK(launch_deps(ctx->units, ctx->ctrl, ctx->desc, ctx->num_sms * 4, ctx->st), "k_deps");
+      ctx->launches += 1;
+    }
+    ctx->attn_epoch++;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx->prof.on) { e0 = ctx->prof.get(); e1 = ctx->prof.get(); cudaEventRecord(e0, ctx->st); }
     CK(launch_attn(ctx->sh, (const uint16_t*)q, (const uint16_t*)k_new, (const uint16_t*)v_new,
-                   (uint16_t*)ctx->buf.arena, out, ctx->partials, ctx->units, ctx->splits, ctx->ctrl, B, l0, nl,
-                   ctx->grid_attn, ctx->grid_combine, ctx->cfg.attn_variant, ctx->st), "k_attn");
+                   (uint16_t*)ctx->buf.arena, (uint8_t*)ctx->buf.staging, out, ctx->partials, ctx->units, ctx->splits,
+                   ctx->desc, ctx->progress, ctx->attn_epoch, ctx->ctrl, B, l0, nl, ctx->grid_attn,
+                   ctx->grid_combine, ctx->cfg.attn_variant, ctx->st), "k_attn");
+    ctx->launches += 2;   // attention, combine
     if (ctx->prof.on) {
       cudaEventRecord(e1, ctx->st);
       int64_t sum_len = 0;
@@ -480,6 +506,7 @@ s3_status s3_decode_step(s3_ctx* ctx, int32_t l0, int32_t nl, const void* q, con
       ctx->prof.pending.push_back({e0, e1, bytes, 0});
     }
   }
+  ctx->fused_pending = fuse;
   if (finalize) {
     for (DSlot& s : ctx->slots_h) { s.len += 1; s.gen += 1; }
     ctx->tokens_total += B;
@@ -503,16 +530,29 @@ s3_status s3_evict_compact(s3_ctx* ctx, s3_evict_report* rep, int32_t* perm, s3_
     return S3_OK;
   }
   const Shape& sh = ctx->sh;
-  CK(launch_keep_scan(sh, ctx->slots[ctx->cur], ctx->slots[1 - ctx->cur], B, ctx->S, ctx->report_dev,
-                      ctx->entries, ctx->key_chunk0, ctx->key_src, ctx->ctrl64, ctx->st), "k_keep_scan");
-  ctx->launches += 1;
-  CK(cudaMemcpyAsync(ctx->h_report, ctx->report_dev, (size_t)report_bytes(B), cudaMemcpyDeviceToHost, ctx->st),
-     "report D2H");
-  CK(cudaStreamSynchronize(ctx->st), "report sync");
+  const DReportHeader* h = reinterpret_cast<const DReportHeader*>(ctx->h_report);
+  bool fused = false;
+  if (ctx->fused_pending) {
+    // the decode step ran the keep-scan; read its report (and its verdict)
+    CK(cudaMemcpyAsync(ctx->h_report, ctx->report_dev, (size_t)report_bytes(B), cudaMemcpyDeviceToHost, ctx->st),
+       "report D2H");
+    CK(cudaMemcpyAsync(ctx->h_report + report_bytes(B), ctx->ctrl + CTRL_FUSED, 4, cudaMemcpyDeviceToHost, ctx->st),
+       "fused flag D2H");
+    CK(cudaStreamSynchronize(ctx->st), "report sync");
+    fused = *reinterpret_cast<const int32_t*>(ctx->h_report + report_bytes(B)) == 1;
+  }
+  if (!fused) {
+    CK(launch_keep_scan(sh, ctx->slots[ctx->cur], ctx->slots[1 - ctx->cur], B, ctx->S, ctx->report_dev,
+                        ctx->entries, ctx->key_chunk0, ctx->key_src, ctx->ctrl64, ctx->st), "k_keep_scan");
+    ctx->launches += 1;
+    CK(cudaMemcpyAsync(ctx->h_report, ctx->report_dev, (size_t)report_bytes(B), cudaMemcpyDeviceToHost, ctx->st),
+       "report D2H");
+    CK(cudaStreamSynchronize(ctx->st), "report sync");
+  }
+  ctx->fused_pending = false;
   flush_deferred(ctx);
   prof_collect(ctx);
   ctx->upload_used = 0;
-  const DReportHeader* h = reinterpret_cast<const DReportHeader*>(ctx->h_report);
   const int32_t* dperm = reinterpret_cast<const int32_t*>(ctx->h_report + report_perm_off(B));
   const DEvicted* dev = reinterpret_cast<const DEvicted*>(ctx->h_report + report_ev_off(B));
   const int64_t* dfin = reinterpret_cast<const int64_t*>(ctx->h_report + report_fin_off(B));
@@ -526,6 +566,10 @@ s3_status s3_evict_compact(s3_ctx* ctx, s3_evict_report* rep, int32_t* perm, s3_
     if (hoff[i] < 0) return fail(ctx, S3_E_CUDA, "evict_compact: host store exhausted");
   }
   const bool staged = h->n_evicted > 0 && ctx->buf.staging && h->d2h_bytes <= ctx->buf.staging_bytes;
+  if (fused && ctx->prof.on) {
+    ctx->prof.fused_steps++;
+    ctx->prof.fused_move_bytes += (double)h->moved_bytes + (double)h->d2h_bytes;
+  }
   std::shared_ptr<EventBox> d2h_done;
   if (h->n_evicted > 0) {
     d2h_done = std::make_shared<EventBox>();
@@ -538,12 +582,12 @@ s3_status s3_evict_compact(s3_ctx* ctx, s3_evict_report* rep, int32_t* perm, s3_
                            cudaMemcpyDeviceToHost, ctx->st), "evict D2H (sync)");
       }
       CK(cudaEventRecord(d2h_done->ev, ctx->st), "event");
-    } else if (ctx->last_stage_d2h) {
+    } else if (ctx->last_stage_d2h && !fused) {
       // staging is reused: the previous step's D2H from it must be done
       CK(cudaStreamWaitEvent(ctx->st, ctx->last_stage_d2h->ev, 0), "wait staging");
     }
   }
-  if (h->n_chunks > 0) {
+  if (!fused && h->n_chunks > 0) {
     ctx->epoch++;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx->prof.on) { e0 = ctx->prof.get(); e1 = ctx->prof.get(); cudaEventRecord(e0, ctx->st); }
@@ -774,8 +818,9 @@ s3_status s3_profile_enable(s3_ctx* ctx, int32_t on) {
   CK(cudaStreamSynchronize(ctx->st), "sync");
   prof_collect(ctx);
   ctx->prof.on = on != 0;
-  ctx->prof.attn_launches = ctx->prof.move_launches = 0;
+  ctx->prof.attn_launches = ctx->prof.move_launches = ctx->prof.fused_steps = 0;
   ctx->prof.attn_ms = ctx->prof.move_ms = ctx->prof.attn_bytes = ctx->prof.move_bytes = 0;
+  ctx->prof.fused_move_bytes = 0;
   return S3_OK;
 }
 
@@ -791,6 +836,8 @@ s3_status s3_profile_get(s3_ctx* ctx, s3_profile* p) {
   p->move_ms = ctx->prof.move_ms;
   p->attn_bytes = ctx->prof.attn_bytes;
   p->move_bytes = ctx->prof.move_bytes;
+  p->fused_steps = ctx->prof.fused_steps;
+  p->fused_move_bytes = ctx->prof.fused_move_bytes;
   return S3_OK;
 }
 

@@ -16,11 +16,27 @@ static_assert(sizeof(DSlot) == 32, "DSlot must be 32 B");
 // One attention work unit: rows [r0, r1) of slot b's resident rows, plus the
 // new (appended) row when has_new.  part < 0: the unit covers the whole slot
 // and writes `out` directly; else it writes partial (m, l, acc) record `part`.
+//
+// Fused attend-and-shift (compact_mode 0): mode says where the unit's rows go
+// while they stream through shared memory: 0 = stay (only the new row is
+// written, at off+len), 1 = move to arena rows dst+r, 2 = copy to the
+// staging buffer at byte dst + r*kvpt (evicted), 3 = nowhere (finished).
+enum { UNIT_STAY = 0, UNIT_MOVE = 1, UNIT_STAGE = 2, UNIT_DROP = 3 };
 struct Unit {
   int32_t b, r0, r1, part;
-  int32_t off, len, has_new, pad;
+  int32_t off, len, has_new, mode;
+  int64_t dst;
+  int32_t stage_base, pad;
 };
-static_assert(sizeof(Unit) == 32, "Unit must be 32 B");
+static_assert(sizeof(Unit) == 48, "Unit must be 48 B");
+
+// Per ring stage of a moving unit: the source units whose rows overlap the
+// stage's destination rows, and how many of their rows must have been read
+// (units strictly between ua and ub must be read completely).
+struct DepDesc {
+  int32_t ua, need_a, ub, need_b;
+};
+constexpr int AT_RPS = 4;      // rows per attention ring stage
 
 struct Split {          // a slot whose attention is split over k units
   int32_t b, part0, k, pad;
@@ -35,7 +51,8 @@ struct MoveEntry {      // one contiguous byte range to move, sources in arena o
 static_assert(sizeof(MoveEntry) == 48, "MoveEntry must be 48 B");
 
 // ctrl words (int32 unless noted)
-enum { CTRL_N_UNITS = 0, CTRL_N_SPLITS = 1, CTRL_ITEM = 2, CTRL_SPLIT_ITEM = 3, CTRL_WORDS = 16 };
+enum { CTRL_N_UNITS = 0, CTRL_N_SPLITS = 1, CTRL_ITEM = 2, CTRL_SPLIT_ITEM = 3, CTRL_FUSED = 4,
+       CTRL_N_STAGES = 5, CTRL_WORDS = 16 };
 // int64 ctrl words (separate array)
 enum { CTRL64_TICKET = 0, CTRL64_N_CHUNKS = 1, CTRL64_WORDS = 8 };
 
@@ -46,7 +63,8 @@ struct DReportHeader {
   int64_t tail, d2h_bytes, moved_bytes, pcie_bytes, hbm_bytes;
   int64_t n_chunks;
   int32_t n_entries, first_hole;
-  int64_t pad[7];
+  int32_t fused, reserved;     // fused: the decode step already moved / staged the rows
+  int64_t pad[6];
 };
 static_assert(sizeof(DReportHeader) == 128, "header 128 B");
 struct DEvicted {
@@ -73,12 +91,26 @@ struct Shape {
 };
 
 // ---- kernel launchers (s3_kernels.cu) ----------------------------------
-cudaError_t launch_prep(const Shape& sh, DSlot* slots, int32_t B, int32_t C, const uint8_t* eos,
-                        int32_t finalize, Unit* units, Split* splits, int32_t* ctrl, cudaStream_t st);
+struct PrepArgs {
+  Shape sh;
+  DSlot* slots;        // current table (updated in place when not fused)
+  DSlot* next;         // gathered table for the next step (fused only)
+  int32_t B, C;
+  const uint8_t* eos;
+  int32_t finalize, fuse;
+  int64_t staging_bytes;
+  Unit* units;
+  Split* splits;
+  int32_t* ctrl;
+  uint8_t* report;
+};
+cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st);
+cudaError_t launch_deps(const Unit* units, const int32_t* ctrl, DepDesc* desc, int32_t grid, cudaStream_t st);
 cudaError_t launch_attn(const Shape& sh, const uint16_t* q, const uint16_t* k_new, const uint16_t* v_new,
-                        uint16_t* arena, float* out, float* partials, const Unit* units,
-                        const Split* splits, int32_t* ctrl, int32_t B, int32_t l0, int32_t nl,
-                        int32_t grid_attn, int32_t grid_combine, int32_t variant, cudaStream_t st);
+                        uint16_t* arena, uint8_t* staging, float* out, float* partials, const Unit* units,
+                        const Split* splits, const DepDesc* desc, unsigned long long* progress, uint32_t epoch,
+                        int32_t* ctrl, int32_t B, int32_t l0, int32_t nl, int32_t grid_attn, int32_t grid_combine,
+                        int32_t variant, cudaStream_t st);
 cudaError_t launch_keep_scan(const Shape& sh, const DSlot* cur, DSlot* next, int32_t B, int64_t S,
                              void* report, MoveEntry* entries, int32_t* key_chunk0, int32_t* key_src,
                              int64_t* ctrl64, cudaStream_t st);

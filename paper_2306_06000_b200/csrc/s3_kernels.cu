@@ -139,28 +139,76 @@ __device__ __forceinline__ uint4 gen8(const Shape& sh, uint64_t seed, uint64_t t
 }
 
 // ---------------------------------------------------------------------------
-// k_prep: work list + detection.  One CTA of 1024 threads; B is small
-// (<= max_running), this runs in a few microseconds.
+// k_prep: one CTA of 1024 threads (B <= max_running; a few microseconds).
+//  * detection (R11): when finalize, status_b = FINISHED if
+//    eos_b, else OVERRUN if len_b + 1 == cap_b, else RUNNING;
+//  * work list: slot b's len_b + 1 rows (with the new one) are cut into
+//    ceil((len_b+1)/C) units (split-K); per unit, ceil(rows/AT_RPS) ring
+//    stages;
+//  * fused step (fuse && finalize && the evicted bytes fit in staging): the
+//    keep-scan runs here, before the attention kernel, so that kernel can
+//    write every survivor's rows straight to its compacted offset (the
+//    paper's row shift) and every evictee's rows to the
+//    staging buffer while it streams them.  Exclusive scans give new_off
+//    (sum of kept caps before b), the permutation, evicted / finished lists
+//    and the packed report; the gathered slot table goes to `next`.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(1024) k_prep(DSlot* __restrict__ slots, int32_t B, int32_t C,
-                                               const uint8_t* __restrict__ eos, int32_t finalize,
-                                               Unit* __restrict__ units, Split* __restrict__ splits,
-                                               int32_t* __restrict__ ctrl) {
+__global__ void __launch_bounds__(1024) k_prep(PrepArgs a) {
+  __shared__ int s_first_hole;
+  __shared__ unsigned long long s_hbm, s_moved;
+  if (threadIdx.x == 0) { s_first_hole = a.B; s_hbm = 0; s_moved = 0; }
+  const int B = a.B, C = a.C;
+  const int64_t kvpt = a.sh.kvpt;
   const int per = (B + blockDim.x - 1) / blockDim.x;
   const int b0 = threadIdx.x * per, b1 = min(B, b0 + per);
-  long long x[3] = {0, 0, 0};  // units, splits, parts
+  // x: 0 units, 1 splits, 2 parts, 3 stages, 4 keep, 5 keep*cap, 6 fin, 7 ev, 8 ev bytes, 9 cap
+  long long x[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   for (int b = b0; b < b1; ++b) {
-    const int k = (slots[b].len + 1 + C - 1) / C;
+    const DSlot sl = a.slots[b];
+    const int k = (sl.len + 1 + C - 1) / C;
     x[0] += k;
     x[1] += k > 1;
     x[2] += k > 1 ? k : 0;
+    for (int i = 0; i < k; ++i) {
+      const int rows = min((i + 1) * C, sl.len) - i * C;
+      x[3] += rows > 0 ? (rows + AT_RPS - 1) / AT_RPS : 1;
+    }
+    const int st = !a.finalize ? 0 : (a.eos[b] ? 1 : (sl.len + 1 == sl.cap ? 2 : 0));
+    x[4] += st == 0;
+    x[5] += st == 0 ? sl.cap : 0;
+    x[6] += st == 1;
+    x[7] += st == 2;
+    x[8] += st == 2 ? (long long)(sl.len + 1) * kvpt : 0;
+    x[9] += sl.cap;
   }
-  long long tot[3];
-  block_excl_scan<3>(x, tot);
-  long long u = x[0], s = x[1], p = x[2];
+  long long tot[10];
+  block_excl_scan<10>(x, tot);
+  const bool fused = a.fuse && a.finalize && tot[8] <= a.staging_bytes;
+  int32_t* perm = reinterpret_cast<int32_t*>(a.report + report_perm_off(B));
+  DEvicted* evl = reinterpret_cast<DEvicted*>(a.report + report_ev_off(B));
+  int64_t* finl = reinterpret_cast<int64_t*>(a.report + report_fin_off(B));
+  long long u = x[0], sp = x[1], p = x[2], stg = x[3];
+  long long keep_i = x[4], keepcap = x[5], fin_i = x[6], ev_i = x[7], evb = x[8], capx = x[9];
+  unsigned long long hbm = 0, moved = 0;
+  int first = B;
   for (int b = b0; b < b1; ++b) {
-    DSlot sl = slots[b];
+    DSlot sl = a.slots[b];
     const int k = (sl.len + 1 + C - 1) / C;
+    const int st = !a.finalize ? 0 : (a.eos[b] ? 1 : (sl.len + 1 == sl.cap ? 2 : 0));
+    int mode = UNIT_STAY;
+    int64_t dst = sl.off;
+    if (fused) {
+      if (st == 0) {
+        mode = keepcap == sl.off ? UNIT_STAY : UNIT_MOVE;
+        dst = keepcap;
+      } else if (st == 2) {
+        mode = UNIT_STAGE;
+        dst = evb;
+      } else {
+        mode = UNIT_DROP;
+        dst = 0;
+      }
+    }
     for (int i = 0; i < k; ++i) {
       Unit un;
       un.b = b;
@@ -170,29 +218,131 @@ __global__ void __launch_bounds__(1024) k_prep(DSlot* __restrict__ slots, int32_
       un.off = sl.off;
       un.len = sl.len;
       un.has_new = (i == k - 1);
+      un.mode = mode;
+      un.dst = dst;
+      un.stage_base = (int)stg;
       un.pad = 0;
-      units[u + i] = un;
+      a.units[u + i] = un;
+      const int rows = un.r1 - un.r0;
+      stg += rows > 0 ? (rows + AT_RPS - 1) / AT_RPS : 1;
     }
     if (k > 1) {
-      Split sp;
-      sp.b = b; sp.part0 = (int)p; sp.k = k; sp.pad = 0;
-      splits[s] = sp;
-      ++s;
+      Split spl;
+      spl.b = b; spl.part0 = (int)p; spl.k = k; spl.pad = 0;
+      a.splits[sp] = spl;
+      ++sp;
       p += k;
     }
     u += k;
-    if (finalize) {
+    if (a.finalize) {
       sl.len += 1;
       sl.gen += 1;
-      sl.status = eos[b] ? 1 : (sl.len == sl.cap ? 2 : 0);
-      slots[b] = sl;
+      sl.status = st;
+    }
+    if (!fused) {
+      if (a.finalize) a.slots[b] = sl;
+      continue;
+    }
+    // ---- fused keep-scan outputs ----
+    if (st != 0 && b < first) first = b;
+    if (st == 0) {
+      perm[b] = (int)keep_i;
+      if (mode == UNIT_MOVE) moved += (unsigned long long)sl.len * kvpt;
+      sl.off = (int32_t)keepcap;
+      sl.status = 0;
+      a.next[keep_i] = sl;
+      ++keep_i;
+      keepcap += sl.cap;
+    } else {
+      perm[b] = -1;
+      if (st == 1) {
+        finl[fin_i++] = sl.req;
+      } else {
+        DEvicted e;
+        e.req = sl.req; e.b = b; e.prompt = sl.prompt; e.gen = sl.gen; e.len = sl.len;
+        e.cap = sl.cap; e.pad = 0; e.stage_off = evb;
+        evl[ev_i++] = e;
+        evb += (int64_t)sl.len * kvpt;
+        hbm += 2ull * (unsigned long long)(tot[9] - capx - sl.cap) * (unsigned long long)kvpt;
+      }
+    }
+    capx += sl.cap;
+  }
+  if (fused) {
+    if (first < B) atomicMin(&s_first_hole, first);
+    if (hbm) atomicAdd(&s_hbm, hbm);
+    if (moved) atomicAdd(&s_moved, moved);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    a.ctrl[CTRL_N_UNITS] = (int)tot[0];
+    a.ctrl[CTRL_N_SPLITS] = (int)tot[1];
+    a.ctrl[CTRL_ITEM] = 0;
+    a.ctrl[CTRL_SPLIT_ITEM] = 0;
+    a.ctrl[CTRL_FUSED] = fused ? 1 : 0;
+    a.ctrl[CTRL_N_STAGES] = (int)tot[3];
+    if (fused) {
+      DReportHeader* h = reinterpret_cast<DReportHeader*>(a.report);
+      h->n_before = B;
+      h->n_finished = (int)tot[6];
+      h->n_evicted = (int)tot[7];
+      h->n_kept = (int)tot[4];
+      h->tail = tot[5];
+      h->d2h_bytes = tot[8];
+      h->moved_bytes = (int64_t)s_moved;
+      h->pcie_bytes = 0;
+      h->hbm_bytes = (int64_t)s_hbm;
+      h->n_chunks = 0;
+      h->n_entries = 0;
+      h->first_hole = s_first_hole;
+      h->fused = 1;
+      h->reserved = 0;
     }
   }
-  if (threadIdx.x == 0) {
-    ctrl[CTRL_N_UNITS] = (int)tot[0];
-    ctrl[CTRL_N_SPLITS] = (int)tot[1];
-    ctrl[CTRL_ITEM] = 0;
-    ctrl[CTRL_SPLIT_ITEM] = 0;
+}
+
+// ---------------------------------------------------------------------------
+// k_deps: for every ring stage of a MOVE unit, the source units whose rows
+// overlap the stage's destination rows [d0, d1) (the new row included in a
+// unit's last stage).  Sources are the units' arena rows [off+r0, off+r1),
+// sorted and disjoint in unit order, so a binary search finds the first.
+// One warp per unit, lanes over its stages.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_deps(const Unit* __restrict__ units, const int32_t* __restrict__ ctrl,
+                                              DepDesc* __restrict__ desc) {
+  const int n_units = ctrl[CTRL_N_UNITS];
+  const int lane = threadIdx.x & 31;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int ui = gw; ui < n_units; ui += nw) {
+    const Unit un = units[ui];
+    const int rows = un.r1 - un.r0;
+    const int ns = rows > 0 ? (rows + AT_RPS - 1) / AT_RPS : 1;
+    for (int s = lane; s < ns; s += 32) {
+      DepDesc d;
+      d.ua = -1; d.need_a = 0; d.ub = -1; d.need_b = 0;
+      if (un.mode == UNIT_MOVE) {
+        const int n = max(0, min(AT_RPS, rows - s * AT_RPS));
+        const int64_t d0 = un.dst + un.r0 + (int64_t)s * AT_RPS;
+        const int64_t d1 = d0 + n + ((s == ns - 1 && un.has_new) ? 1 : 0);
+        int lo = 0, hi = n_units;              // first unit with source end > d0
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          const Unit& m = units[mid];
+          if ((int64_t)m.off + m.r1 > d0) hi = mid; else lo = mid + 1;
+        }
+        for (int v = lo; v < n_units; ++v) {
+          const Unit& m = units[v];
+          const int64_t s0 = (int64_t)m.off + m.r0, s1 = (int64_t)m.off + m.r1;
+          if (s0 >= d1) break;
+          if (s1 <= s0 || s1 <= d0) continue;  // empty source or no overlap
+          const int need = (int)(min(d1, s1) - s0);
+          if (d.ua < 0) { d.ua = v; d.need_a = need; }
+          d.ub = v; d.need_b = need;
+        }
+      }
+      desc[un.stage_base + s] = d;
+    }
   }
 }
 
@@ -210,9 +360,13 @@ struct AttnArgs {
   const uint16_t* k_new;
   const uint16_t* v_new;
   uint16_t* arena;
+  uint8_t* staging;
   float* out;
   float* partials;
   const Unit* units;
+  const DepDesc* desc;
+  unsigned long long* progress;
+  uint32_t epoch;
   int32_t* ctrl;
   int32_t B, l0, nl;
   float qscale;
@@ -710,23 +864,37 @@ int move_smem_bytes(int64_t S, int32_t n_entries, int32_t* keys_in_smem) {
 }
 
 // ---------------------------------------------------------------------------
-// k_attn_tma: the same computation as k_attn with the KV stream staged by
-// the TMA bulk-copy engine.  One producer warp (one elected thread) takes
-// items (unit, layer) from the queue and streams each item's rows -- one
-// contiguous 4*H*D-byte layer-row (K of all heads, then V) per
-// cp.async.bulk -- plus the item's q into an AT_NS-stage shared-memory ring
-// (mbarrier full/empty per stage).  H*D/256 consumer warps (D/8 lanes per
-// head) read K/V from shared memory with 128-bit loads and run the same
-// online softmax as k_attn.  The ring keeps up to AT_NS*AT_RPS rows per SM
-// in flight without spending registers on them.
+// k_attn_tma: decode attention with the KV stream staged by the TMA bulk
+// copy engine, fused with the row shift.
+//
+//  producer warp (1 thread): takes items (unit, layer) from the queue and
+//    streams each item's rows -- one contiguous 4*H*D-byte layer-row (K of all
+//    heads, then V) per cp.async.bulk -- plus the item's q into an
+//    ns-stage shared-memory ring (mbarrier full/empty per stage);
+//  consumer warps (H*D/256; D/8 lanes per head): 128-bit loads from the
+//    stage, online softmax; at the item's end append the new row (k_new,
+//    v_new) at its final position and write out / the split-K partial;
+//  storer warp (1 thread): when a stage lands, publishes the item's read
+//    progress (st.release), and for MOVE units waits (ld.acquire) until every
+//    source unit overlapping the stage's destination rows has been read that
+//    far (k_deps), then bulk-stores the stage's rows to their compacted rows;
+//    STAGE units (evicted) are bulk-stored to the staging buffer.
+// Deadlock freedom: items are handed out in unit order and every destination
+// row lies at or below its source row, so a stage only waits on items with
+// smaller tickets (or on rows of its own item that are already in shared
+// memory); the smallest waiting item always progresses.
 // ---------------------------------------------------------------------------
-constexpr int AT_RPS = 4;      // rows per stage
 constexpr int AT_NS_MAX = 8;
+constexpr unsigned long long PROG_FULL = 0x80000000ull;
 
 struct StageHdr {
+  DepDesc dep;                 // filled by the TMA engine (16 B, same transaction as the rows)
   int32_t item, r0, n, flags;  // flags: 1 = first stage of the item, 2 = last, 4 = unit has the new row
   int32_t b, part, off, len;   // the item's unit (so consumers never load it from global)
+  int32_t mode, unit_r0, dep_ok, pad;   // dep_ok: storer's "destination free" stamp (stage seq + 1)
+  int64_t dst, pad2;
 };
+static_assert(sizeof(StageHdr) % 16 == 0, "StageHdr must keep 16-B alignment");
 
 __device__ __forceinline__ uint4 lds128(const void* p) {
   uint4 r;
@@ -735,9 +903,22 @@ __device__ __forceinline__ uint4 lds128(const void* p) {
                : "r"(smem_u32(p)));
   return r;
 }
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void bulk_s2g_nocommit(void* dst, const void* src_smem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(smem_u32(src_smem)),
+               "r"(bytes)
+               : "memory");
+}
 
 template <int D>
-__global__ void __launch_bounds__(544, 1) k_attn_tma(AttnArgs a, int32_t ns) {
+__global__ void __launch_bounds__(576, 1) k_attn_tma(AttnArgs a, int32_t ns) {
   constexpr int LPH = D / 8;
   constexpr int HPW = 32 / LPH;
   extern __shared__ __align__(128) uint8_t smem[];
@@ -745,14 +926,21 @@ __global__ void __launch_bounds__(544, 1) k_attn_tma(AttnArgs a, int32_t ns) {
   const int64_t HD = (int64_t)H * D;
   const int64_t rowB = 4 * HD;                     // one layer-row: K and V of all heads
   const int64_t stageB = AT_RPS * rowB + 2 * HD;   // rows + q of the item
+  const int64_t kvpt = a.sh.kvpt;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + ns * stageB);
   uint64_t* empty = full + ns;
   StageHdr* hdr = reinterpret_cast<StageHdr*>(empty + ns);
   const int nwarps = blockDim.x >> 5;
-  const int nwc = nwarps - 1;                      // consumer warps; the last warp produces
+  const int nwc = nwarps - 2;                      // consumer warps; then producer, storer
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // the storer takes part in the ring only when this step moves rows
+  const bool fused = a.ctrl[CTRL_FUSED] != 0;
   if (threadIdx.x == 0) {
-    for (int i = 0; i < ns; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], nwc); }
+    for (int i = 0; i < ns; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], nwc + (fused ? 1 : 0));
+      hdr[i].dep_ok = 0;
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
@@ -774,31 +962,105 @@ __global__ void __launch_bounds__(544, 1) k_attn_tma(AttnArgs a, int32_t ns) {
         }
         const int u = item / a.nl, li = item - u * a.nl;
         const Unit un = a.units[u];
-        const uint8_t* base = arena + (int64_t)un.off * a.sh.kvpt + (int64_t)(a.l0 + li) * rowB;
+        const uint8_t* base = arena + (int64_t)un.off * kvpt + (int64_t)(a.l0 + li) * rowB;
         const uint16_t* qsrc = a.q + ((int64_t)li * a.B + un.b) * HD;
-        int r = un.r0;
+        int r = un.r0, s = 0;
         do {
           const int st = k % ns;
           mbar_wait(&empty[st], ((uint32_t)(k / ns) & 1u) ^ 1u);
           const int n = min(AT_RPS, un.r1 - r);
           const bool first = r == un.r0;
-          hdr[st].item = item; hdr[st].r0 = r; hdr[st].n = n;
-          hdr[st].flags = (first ? 1 : 0) | (r + n >= un.r1 ? 2 : 0) | (un.has_new ? 4 : 0);
-          hdr[st].b = un.b; hdr[st].part = un.part; hdr[st].off = un.off; hdr[st].len = un.len;
-          const uint32_t tx = (uint32_t)(n * rowB + (first ? 2 * HD : 0));
+          StageHdr& h = hdr[st];
+          h.item = item; h.r0 = r; h.n = n;
+          h.flags = (first ? 1 : 0) | (r + n >= un.r1 ? 2 : 0) | (un.has_new ? 4 : 0);
+          h.b = un.b; h.part = un.part; h.off = un.off; h.len = un.len;
+          h.mode = un.mode; h.unit_r0 = un.r0; h.dst = un.dst;
+          const bool mv = un.mode == UNIT_MOVE;
+          const uint32_t tx = (uint32_t)(n * rowB + (first ? 2 * HD : 0) + (mv ? sizeof(DepDesc) : 0));
           uint8_t* sb = smem + st * stageB;
           if (tx) {
             mbar_arrive_expect_tx(&full[st], tx);
+            if (mv) bulk_g2s(&h.dep, a.desc + un.stage_base + s, (uint32_t)sizeof(DepDesc), &full[st]);
             if (first) bulk_g2s(sb + AT_RPS * rowB, qsrc, (uint32_t)(2 * HD), &full[st]);
             for (int i = 0; i < n; ++i)
-              bulk_g2s(sb + i * rowB, base + (int64_t)(r + i) * a.sh.kvpt, (uint32_t)rowB, &full[st]);
+              bulk_g2s(sb + i * rowB, base + (int64_t)(r + i) * kvpt, (uint32_t)rowB, &full[st]);
           } else {
             mbar_arrive(&full[st]);
           }
           r += n;
+          ++s;
           ++k;
         } while (r < un.r1);
       }
+    }
+    return;
+  }
+  if (warp == nwc + 1) {
+    // ------------------------------- storer -------------------------------
+    if (lane == 0 && fused) {
+      int pending = -1;                 // stage whose stores may still read shared memory
+      int64_t seen_item = -1;           // progress cache: last observed source item / value
+      unsigned long long seen_val = 0;
+      for (int k = 0;; ++k) {
+        const int st = k % ns;
+        mbar_wait(&full[st], (uint32_t)(k / ns) & 1u);
+        StageHdr& hs = hdr[st];
+        const StageHdr h = hs;
+        if (h.item < 0) break;
+        const int li = h.item % a.nl;
+        const unsigned long long done =
+            (unsigned long long)(h.r0 + h.n - h.unit_r0) | ((h.flags & 2) ? PROG_FULL : 0ull);
+        // the stage's bytes are in shared memory (mbarrier observed): the
+        // source rows may be overwritten from now on
+        st_relaxed_u64(a.progress + h.item, ((unsigned long long)a.epoch << 32) | done);
+        bool stores = false;
+        if (h.mode == UNIT_MOVE) {
+          // destination rows free?  (own-item rows are already in shared memory)
+          const DepDesc& d = h.dep;
+          if (d.ua >= 0) {
+            for (int v = d.ua; v <= d.ub; ++v) {
+              const int need = v == d.ua ? d.need_a : (v == d.ub ? d.need_b : -1);
+              const int64_t it = (int64_t)v * a.nl + li;
+              if (it == h.item) continue;
+              for (;;) {
+                if (it != seen_item) { seen_item = it; seen_val = ld_acquire_u64(a.progress + it); }
+                const unsigned long long x = seen_val;
+                if ((uint32_t)(x >> 32) == a.epoch && ((x & PROG_FULL) || (need >= 0 && (int)(x & 0x7fffffffull) >= need)))
+                  break;
+                __nanosleep(32);
+                seen_val = ld_acquire_u64(a.progress + it);
+              }
+            }
+          }
+          asm volatile("fence.proxy.async;" ::: "memory");
+          *reinterpret_cast<volatile int32_t*>(&hs.dep_ok) = k + 1;
+          stores = h.n > 0;
+        } else if (h.mode == UNIT_STAGE) {
+          stores = h.n > 0;
+        }
+        if (stores) {
+          uint8_t* dbase = h.mode == UNIT_MOVE
+                               ? reinterpret_cast<uint8_t*>(a.arena) + (h.dst + h.r0) * kvpt
+                               : a.staging + h.dst + (int64_t)h.r0 * kvpt;
+          const uint8_t* sb = smem + st * stageB;
+          for (int i = 0; i < h.n; ++i)
+            bulk_s2g_nocommit(dbase + (int64_t)i * kvpt + (int64_t)(a.l0 + li) * rowB, sb + i * rowB,
+                              (uint32_t)rowB);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+        // release the previous stage once its stores have read shared memory
+        if (pending >= 0) {
+          if (stores) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+          else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          mbar_arrive(&empty[pending]);
+          pending = -1;
+        }
+        if (stores) pending = st;
+        else mbar_arrive(&empty[st]);
+      }
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      if (pending >= 0) mbar_arrive(&empty[pending]);
+      asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
     return;
   }
@@ -849,8 +1111,19 @@ __global__ void __launch_bounds__(544, 1) k_attn_tma(AttnArgs a, int32_t ns) {
     if (lane == 0) mbar_arrive(&empty[st]);
     if (h.flags & 2) {
       if (last_new) {
-        uint16_t* kdst = a.arena + (int64_t)(h.off + h.len) * rowE + (int64_t)(a.l0 + li) * 2 * HD + hh * D + sub * 8;
-        if (active) {
+        // append: the new row goes where the slot's rows end up
+        uint16_t* kdst = nullptr;
+        const int64_t lofs = (int64_t)(a.l0 + li) * 2 * HD + hh * D + sub * 8;
+        if (h.mode == UNIT_STAY) {
+          kdst = a.arena + (int64_t)(h.off + h.len) * rowE + lofs;
+        } else if (h.mode == UNIT_MOVE) {
+          // the storer stamps the stage once its destination rows (new row included) are free
+          while (*reinterpret_cast<volatile int32_t*>(&hdr[st].dep_ok) < k + 1) __nanosleep(20);
+          kdst = a.arena + (h.dst + h.len) * rowE + lofs;
+        } else if (h.mode == UNIT_STAGE) {
+          kdst = reinterpret_cast<uint16_t*>(a.staging + h.dst + (int64_t)h.len * kvpt) + lofs;
+        }
+        if (active && kdst) {
           st_v4(kdst, kr);
           st_v4(kdst + HD, vr);
         }
@@ -996,20 +1269,25 @@ const void* attn_kernel_ptr(const Shape& sh) {
 }
 const void* move_kernel_ptr() { return (const void*)k_move; }
 
-cudaError_t launch_prep(const Shape& sh, DSlot* slots, int32_t B, int32_t C, const uint8_t* eos,
-                        int32_t finalize, Unit* units, Split* splits, int32_t* ctrl, cudaStream_t st) {
-  (void)sh;
-  k_prep<<<1, 1024, 0, st>>>(slots, B, C, eos, finalize, units, splits, ctrl);
+cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st) {
+  k_prep<<<1, 1024, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_deps(const Unit* units, const int32_t* ctrl, DepDesc* desc, int32_t grid, cudaStream_t st) {
+  k_deps<<<grid, 256, 0, st>>>(units, ctrl, desc);
   return cudaGetLastError();
 }
 
 cudaError_t launch_attn(const Shape& sh, const uint16_t* q, const uint16_t* k_new, const uint16_t* v_new,
-                        uint16_t* arena, float* out, float* partials, const Unit* units,
-                        const Split* splits, int32_t* ctrl, int32_t B, int32_t l0, int32_t nl,
-                        int32_t grid_attn, int32_t grid_combine, int32_t variant, cudaStream_t st) {
+                        uint16_t* arena, uint8_t* staging, float* out, float* partials, const Unit* units,
+                        const Split* splits, const DepDesc* desc, unsigned long long* progress, uint32_t epoch,
+                        int32_t* ctrl, int32_t B, int32_t l0, int32_t nl, int32_t grid_attn, int32_t grid_combine,
+                        int32_t variant, cudaStream_t st) {
   AttnArgs a;
-  a.sh = sh; a.q = q; a.k_new = k_new; a.v_new = v_new; a.arena = arena; a.out = out;
-  a.partials = partials; a.units = units; a.ctrl = ctrl; a.B = B; a.l0 = l0; a.nl = nl;
+  a.sh = sh; a.q = q; a.k_new = k_new; a.v_new = v_new; a.arena = arena; a.staging = staging; a.out = out;
+  a.partials = partials; a.units = units; a.desc = desc; a.progress = progress; a.epoch = epoch;
+  a.ctrl = ctrl; a.B = B; a.l0 = l0; a.nl = nl;
   a.qscale = 1.4426950408889634f / sqrtf((float)sh.D);
   const int threads = attn_block_threads(sh);
   const int ns = attn_tma_stages(sh);
@@ -1017,17 +1295,17 @@ cudaError_t launch_attn(const Shape& sh, const uint16_t* q, const uint16_t* k_ne
   const int smem = tma ? attn_tma_smem(sh, ns) : 0;
   switch (sh.D) {
     case 64:
-      if (tma) k_attn_tma<64><<<grid_attn, threads + 32, smem, st>>>(a, ns);
+      if (tma) k_attn_tma<64><<<grid_attn, threads + 64, smem, st>>>(a, ns);
       else k_attn<64><<<grid_attn, threads, 0, st>>>(a);
       k_combine<64><<<grid_combine, 256, 0, st>>>(splits, partials, out, ctrl, sh.H, B, nl);
       break;
     case 128:
-      if (tma) k_attn_tma<128><<<grid_attn, threads + 32, smem, st>>>(a, ns);
+      if (tma) k_attn_tma<128><<<grid_attn, threads + 64, smem, st>>>(a, ns);
       else k_attn<128><<<grid_attn, threads, 0, st>>>(a);
       k_combine<128><<<grid_combine, 256, 0, st>>>(splits, partials, out, ctrl, sh.H, B, nl);
       break;
     case 256:
-      if (tma) k_attn_tma<256><<<grid_attn, threads + 32, smem, st>>>(a, ns);
+      if (tma) k_attn_tma<256><<<grid_attn, threads + 64, smem, st>>>(a, ns);
       else k_attn<256><<<grid_attn, threads, 0, st>>>(a);
       k_combine<256><<<grid_combine, 256, 0, st>>>(splits, partials, out, ctrl, sh.H, B, nl);
       break;

@@ -33,7 +33,7 @@ class s3_config(C.Structure):
                 ("max_seq_len", C.c_int32), ("arena_rows", C.c_int64), ("max_running", C.c_int32),
                 ("chunk_rows", C.c_int32), ("move_chunk_bytes", C.c_int32), ("device", C.c_int32),
                 ("stream", C.c_void_p), ("rank", C.c_int32), ("world", C.c_int32),
-                ("synth_seed", C.c_uint64), ("attn_variant", C.c_int32), ("reserved0", C.c_int32)]
+                ("synth_seed", C.c_uint64), ("attn_variant", C.c_int32), ("compact_mode", C.c_int32)]
 
 
 class s3_buffers(C.Structure):
@@ -73,8 +73,8 @@ class s3_slot(C.Structure):
 
 class s3_profile(C.Structure):
     _fields_ = [("kernel_launches", C.c_int64), ("attn_launches", C.c_int64), ("move_launches", C.c_int64),
-                ("attn_ms", C.c_double), ("move_ms", C.c_double),
-                ("attn_bytes", C.c_double), ("move_bytes", C.c_double)]
+                ("fused_steps", C.c_int64), ("attn_ms", C.c_double), ("move_ms", C.c_double),
+                ("attn_bytes", C.c_double), ("move_bytes", C.c_double), ("fused_move_bytes", C.c_double)]
 
 
 P = C.c_void_p

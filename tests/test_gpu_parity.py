@@ -41,10 +41,11 @@ def u16(t: torch.Tensor) -> np.ndarray:
 
 
 def lockstep(trace, L, H, D, R, C=0, S=0, max_running=4096, staging=True, feed_oracle_inputs=False,
-             max_steps=100000, check_arena=True, attn_variant=0):
+             max_steps=100000, check_arena=True, attn_variant=0, compact_mode=0):
     from paper_2306_06000_b200.engine import S3Engine
     eng = S3Engine(L, H, D, trace.max_seq_len, R, max_running, chunk_rows=C, move_chunk_bytes=S,
-                   staging_bytes=None if staging else 0, host_store_bytes=64 << 20, attn_variant=attn_variant)
+                   staging_bytes=None if staging else 0, host_store_bytes=64 << 20, attn_variant=attn_variant,
+                   compact_mode=compact_mode)
     orc = oracle.Oracle(L, H, D, trace.max_seq_len, R, max_running=max_running)
     eng.submit(trace.req_id, trace.prompt, trace.alloc, trace.out)
     orc.submit(trace.req_id, trace.prompt, trace.alloc)
@@ -115,10 +116,10 @@ def lockstep(trace, L, H, D, R, C=0, S=0, max_running=4096, staging=True, feed_o
     return dict(steps=steps, worst=worst, **stats)
 
 
-@pytest.mark.parametrize("variant", [0, 1])
-def test_c0_full_run(variant):
+@pytest.mark.parametrize("variant,mode", [(0, 0), (0, 1), (1, 1)])
+def test_c0_full_run(variant, mode):
     t = s3synth.c0_trace()
-    r = lockstep(t, 1, 2, 64, 64, C=4, S=1024, attn_variant=variant)
+    r = lockstep(t, 1, 2, 64, 64, C=4, S=1024, attn_variant=variant, compact_mode=mode)
     assert r["steps"] == 32 and r["evictions"] == 3
 
 
@@ -134,20 +135,32 @@ def test_c0_sync_eviction_path():
     assert r["evictions"] == 3
 
 
-@pytest.mark.parametrize("variant", [0, 1])
-def test_gptj_heads_reduced_layers_with_evictions(variant):
+@pytest.mark.parametrize("variant,mode", [(0, 0), (0, 1), (1, 1)])
+def test_gptj_heads_reduced_layers_with_evictions(variant, mode):
     # GPT-J head shape (H=16, D=256), 2 layers; small chunks -> many split-K
     # tiles with ragged tails; small move chunks -> overlapping ordered moves.
     t = s3synth.make_trace(60, seed=3, policy="short", p=0.3, max_seq_len=160, prompt_max=40)
-    r = lockstep(t, 2, 16, 256, 1200, C=16, S=4096, max_steps=3000, attn_variant=variant)
+    r = lockstep(t, 2, 16, 256, 1200, C=16, S=4096, max_steps=3000, attn_variant=variant, compact_mode=mode)
     assert r["evictions"] > 0 and r["moved"] > 0
     print("worst rel err", r["worst"])
 
 
-@pytest.mark.parametrize("variant", [0, 1])
-def test_head_dim_128(variant):
+@pytest.mark.parametrize("variant,mode", [(0, 0), (1, 1)])
+def test_head_dim_128(variant, mode):
     t = s3synth.make_trace(40, seed=4, policy="short", p=0.2, max_seq_len=96, prompt_max=20)
-    lockstep(t, 3, 4, 128, 400, C=8, S=2048, attn_variant=variant)
+    lockstep(t, 3, 4, 128, 400, C=8, S=2048, attn_variant=variant, compact_mode=mode)
+
+
+def test_tiny_slots_dense_moves():
+    # many 1-3 row slots and frequent finishes: stage destinations overlap
+    # several source units (the middle-unit wait of k_deps), shifts of 1 row
+    rng = np.random.default_rng(17)
+    n = 120
+    P = rng.integers(0, 3, n).astype(np.int32)
+    O = rng.integers(1, 6, n).astype(np.int32)
+    alloc = np.where(rng.random(n) < 0.3, np.maximum(1, O - 2), O).astype(np.int32)
+    t = s3synth.Trace(np.arange(n, dtype=np.int64), P, O, alloc, 64)
+    lockstep(t, 2, 4, 64, 96, C=2, S=1024, compact_mode=0)
 
 
 def test_max_running_limit_and_p0():
