@@ -330,6 +330,8 @@ def run_s3(args):
                 "achieved": attn_gbs, "peak": peak, "unit": "GB/s", "frac": attn_gbs / peak,
                 "peak_source": peak_kind,
                 "traffic": tr.get("dram_bytes_per_launch") if tr else None,
+                "traffic_over_algorithmic": tr.get("traffic_over_algorithmic") if tr else None,
+                "traffic_window": tr.get("window") if tr else None,
                 "algorithmic_bytes_per_launch": attn_kernel_bytes / max(prof.attn_launches, 1),
                 "attention_bytes_per_launch": prof.attn_bytes / max(prof.attn_launches, 1),
                 "fused_shift_bytes_per_launch": prof.fused_move_bytes / max(prof.attn_launches, 1),
