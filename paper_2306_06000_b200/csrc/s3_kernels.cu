@@ -908,6 +908,14 @@ __device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+__device__ __forceinline__ void st_release_cta_s32(int32_t* p, int32_t v) {
+  asm volatile("st.release.cta.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+__device__ __forceinline__ int32_t ld_acquire_cta_s32(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.acquire.cta.shared::cta.b32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+  return v;
+}
 __device__ __forceinline__ void st_relaxed_u64(unsigned long long* p, unsigned long long v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -1033,7 +1041,7 @@ __global__ void __launch_bounds__(576, 1) k_attn_tma(AttnArgs a, int32_t ns) {
             }
           }
           asm volatile("fence.proxy.async;" ::: "memory");
-          *reinterpret_cast<volatile int32_t*>(&hs.dep_ok) = k + 1;
+          st_release_cta_s32(&hs.dep_ok, k + 1);   // consumers may now write the new row
           stores = h.n > 0;
         } else if (h.mode == UNIT_STAGE) {
           stores = h.n > 0;
@@ -1118,7 +1126,7 @@ __global__ void __launch_bounds__(576, 1) k_attn_tma(AttnArgs a, int32_t ns) {
           kdst = a.arena + (int64_t)(h.off + h.len) * rowE + lofs;
         } else if (h.mode == UNIT_MOVE) {
           // the storer stamps the stage once its destination rows (new row included) are free
-          while (*reinterpret_cast<volatile int32_t*>(&hdr[st].dep_ok) < k + 1) __nanosleep(20);
+          while (ld_acquire_cta_s32(&hdr[st].dep_ok) < k + 1) __nanosleep(20);
           kdst = a.arena + (h.dst + h.len) * rowE + lofs;
         } else if (h.mode == UNIT_STAGE) {
           kdst = reinterpret_cast<uint16_t*>(a.staging + h.dst + (int64_t)h.len * kvpt) + lofs;

@@ -41,7 +41,7 @@ def u16(t: torch.Tensor) -> np.ndarray:
 
 
 def lockstep(trace, L, H, D, R, C=0, S=0, max_running=4096, staging=True, feed_oracle_inputs=False,
-             max_steps=100000, check_arena=True, attn_variant=0, compact_mode=0):
+             max_steps=100000, check_arena=True, attn_variant=0, compact_mode=0, poison=False):
     from paper_2306_06000_b200.engine import S3Engine
     eng = S3Engine(L, H, D, trace.max_seq_len, R, max_running, chunk_rows=C, move_chunk_bytes=S,
                    staging_bytes=None if staging else 0, host_store_bytes=64 << 20, attn_variant=attn_variant,
@@ -62,6 +62,13 @@ def lockstep(trace, L, H, D, R, C=0, S=0, max_running=4096, staging=True, feed_o
         assert steps < max_steps
         B = orc.B
         assert eng.batch_view() == orc.batch(), f"step {steps}: batch views differ"
+        if poison:
+            # T5: every arena row that is not resident (slack, free tail, vacated
+            # rows) becomes bf16 NaN; a kernel that reads one leaks NaN into out
+            resident = torch.zeros(R, dtype=torch.bool)
+            for (_, _, _, ln, _, off) in orc.batch():
+                resident[off:off + ln] = True
+            eng.arena_rows_view()[(~resident).to(eng.device)] = float("nan")
         q, k, v, eos = orc.make_inputs(trace.out)
         n = L * B * HD
         if B:
@@ -309,3 +316,20 @@ def test_abi_error_codes_and_empty_batch():
     rep, perm, ev, fin = eng.evict_compact()     # state intact after the errors
     assert rep.n_before == 2
     eng.close()
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_nan_poisoned_non_resident_rows(mode):
+    t = s3synth.make_trace(50, seed=23, policy="short", p=0.3, max_seq_len=128, prompt_max=24)
+    r = lockstep(t, 2, 4, 128, 700, C=8, S=2048, compact_mode=mode, poison=True)
+    assert r["evictions"] > 0
+
+
+def test_zero_length_prompts():
+    # P = 0 requests (SPEC.md:43 allows prompt_tokens >= 0): the first decode
+    # attends only to its own new row (P1(i) on the GPU path).
+    P = np.array([0, 0, 3, 0, 5, 1], np.int32)
+    O = np.array([4, 1, 6, 9, 2, 7], np.int32)
+    alloc = np.array([2, 1, 6, 9, 2, 3], np.int32)
+    t = s3synth.Trace(np.arange(6, dtype=np.int64), P, O, alloc, 64)
+    lockstep(t, 2, 4, 64, 64, C=2, S=1024)
