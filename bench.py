@@ -307,6 +307,24 @@ def run_s3(args):
     attn_gbs = attn_kernel_bytes / (prof.attn_ms / 1e3) / 1e9 if prof.attn_ms > 0 else 0.0
     move_gbs = prof.move_bytes / (prof.move_ms / 1e3) / 1e9 if prof.move_ms > 0 else 0.0
     tr = traffic_from_profiles()
+    pcie = pcie_peaks(dev)
+    # generation / penalty / overhead per step (the paper's Fig. 6 split,
+    # PAPER.md:294): the attention kernel's time is split by its bytes
+    step_ms = ms / args.steps
+    attn_tot = prof.attn_bytes + prof.fused_move_bytes
+    gen_ms = prof.attn_ms * (prof.attn_bytes / attn_tot if attn_tot else 1.0)
+    shift_ms = prof.attn_ms - gen_ms
+    pen_ms = shift_ms + prof.move_ms + prof.h2d_ms
+    split = {
+        "generation_ms_per_step": round(gen_ms / args.steps, 4),
+        "penalty_ms_per_step": round(pen_ms / args.steps, 4),
+        "overhead_ms_per_step": round(max(0.0, step_ms - (gen_ms + pen_ms) / args.steps), 4),
+        "penalty_parts_ms_total": {"row_shift_in_attention": round(shift_ms, 3), "k_move": round(prof.move_ms, 3),
+                                   "reload_h2d": round(prof.h2d_ms, 3),
+                                   "evict_d2h_async_not_on_path": round(prof.d2h_ms, 3)},
+        "note": "generation includes the synthetic-input kernel under overhead; shares of ms_per_step",
+    }
+    split["penalty_plus_overhead_share"] = round(1.0 - split["generation_ms_per_step"] / step_ms, 4)
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline and world == 1:
@@ -346,6 +364,13 @@ def run_s3(args):
             "tokens": tok_sum, "finished": totals["finished"], "admitted": totals["admitted"],
             "gpu_launches": launches,
             "phases_ms_per_step": phases,
+            "latency_split": split,
+            "pcie": {
+                "peak_gbs": pcie, "source": "pinned 1 GiB cudaMemcpyAsync, best of 5 (in-harness)",
+                "evict_d2h_gbs": round(prof.d2h_bytes / (prof.d2h_ms / 1e3) / 1e9, 2) if prof.d2h_ms else None,
+                "reload_h2d_gbs": round(prof.h2d_bytes / (prof.h2d_ms / 1e3) / 1e9, 2) if prof.h2d_ms else None,
+                "evict_d2h_bytes": prof.d2h_bytes, "reload_h2d_bytes": prof.h2d_bytes,
+            },
             "clocks": clk,
             "cpu_baseline": cpu,
             "e2e": e2e,
@@ -354,6 +379,28 @@ def run_s3(args):
     eng.close()
     if dist:
         dist.destroy_process_group()
+
+
+def pcie_peaks(dev, nbytes=1 << 30, reps=5):
+    """Pinned host <-> device copy bandwidth (best of `reps`, CUDA events)."""
+    import torch
+    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    best = {"h2d": 0.0, "d2h": 0.0}
+    for _ in range(reps):
+        for kind in ("h2d", "d2h"):
+            e0.record()
+            if kind == "h2d":
+                d.copy_(h, non_blocking=True)
+            else:
+                h.copy_(d, non_blocking=True)
+            e1.record()
+            torch.cuda.synchronize()
+            best[kind] = max(best[kind], nbytes / (e0.elapsed_time(e1) / 1e3) / 1e9)
+    del h, d
+    return {k: round(v, 2) for k, v in best.items()}
 
 
 def phase_breakdown(eng, exchange, world, steps):

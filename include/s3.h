@@ -194,6 +194,9 @@ typedef struct {
   double attn_bytes, move_bytes;    /* algorithmic bytes of those launches        */
   double fused_move_bytes;          /* row-shift + staging bytes written by the attention
                                        launches of fused steps (part of their traffic)  */
+  int64_t d2h_copies, h2d_copies;   /* eviction D2H batches / reload H2D copies timed   */
+  double d2h_ms, d2h_bytes;         /* eviction copies (side stream, overlapped)        */
+  double h2d_ms, h2d_bytes;         /* reload copies (main stream)                       */
 } s3_profile;
 s3_status s3_profile_enable(s3_ctx* ctx, int32_t on);   /* also resets the sums */
 s3_status s3_profile_get(s3_ctx* ctx, s3_profile* prof); /* synchronises          */

@@ -77,8 +77,9 @@ struct Prof {
   std::vector<cudaEvent_t> free_events;
   struct Pending { cudaEvent_t a, b; double bytes; int kind; };
   std::vector<Pending> pending;
-  int64_t attn_launches = 0, move_launches = 0, fused_steps = 0;
+  int64_t attn_launches = 0, move_launches = 0, fused_steps = 0, d2h_copies = 0, h2d_copies = 0;
   double attn_ms = 0, move_ms = 0, attn_bytes = 0, move_bytes = 0, fused_move_bytes = 0;
+  double d2h_ms = 0, d2h_bytes = 0, h2d_ms = 0, h2d_bytes = 0;
   cudaEvent_t get() {
     if (!free_events.empty()) { cudaEvent_t e = free_events.back(); free_events.pop_back(); return e; }
     cudaEvent_t e;
@@ -248,16 +249,20 @@ void flush_deferred(s3_ctx* c) {   // call only when cfg.stream is idle
   c->deferred_free.clear();
 }
 
-void prof_collect(s3_ctx* c) {     // call only when cfg.stream is idle
+void prof_collect(s3_ctx* c) {     // call when cfg.stream is idle; side-stream pairs may still run
+  std::vector<Prof::Pending> keep;
   for (auto& p : c->prof.pending) {
+    if (cudaEventQuery(p.b) != cudaSuccess) { keep.push_back(p); continue; }
     float ms = 0.f;
     cudaEventElapsedTime(&ms, p.a, p.b);
     if (p.kind == 0) { c->prof.attn_ms += ms; c->prof.attn_bytes += p.bytes; c->prof.attn_launches++; }
-    else { c->prof.move_ms += ms; c->prof.move_bytes += p.bytes; c->prof.move_launches++; }
+    else if (p.kind == 1) { c->prof.move_ms += ms; c->prof.move_bytes += p.bytes; c->prof.move_launches++; }
+    else if (p.kind == 2) { c->prof.d2h_ms += ms; c->prof.d2h_bytes += p.bytes; c->prof.d2h_copies++; }
+    else { c->prof.h2d_ms += ms; c->prof.h2d_bytes += p.bytes; c->prof.h2d_copies++; }
     c->prof.free_events.push_back(p.a);
     c->prof.free_events.push_back(p.b);
   }
-  c->prof.pending.clear();
+  c->prof.pending.swap(keep);
 }
 
 uint8_t* upload_reserve(s3_ctx* c, int64_t n) {
@@ -292,9 +297,15 @@ s3_status place_items(s3_ctx* ctx, const std::vector<Item>& items, s3_admit_repo
         s.gen = it.gen;
         s.len = it.host_rows;
         CK(cudaStreamWaitEvent(ctx->st, it.ready->ev, 0), "wait D2H event");
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (ctx->prof.on) { e0 = ctx->prof.get(); e1 = ctx->prof.get(); cudaEventRecord(e0, ctx->st); }
         CK(cudaMemcpyAsync((uint8_t*)ctx->buf.arena + (int64_t)s.off * ctx->sh.kvpt,
                            (uint8_t*)ctx->buf.host_store + it.host_off, it.host_bytes,
                            cudaMemcpyHostToDevice, ctx->st), "reload H2D");
+        if (ctx->prof.on) {
+          cudaEventRecord(e1, ctx->st);
+          ctx->prof.pending.push_back({e0, e1, (double)it.host_bytes, 3});
+        }
         ctx->deferred_free.emplace_back(it.host_off, it.host_bytes);
         ctx->n_evicted_waiting--;
         r.n_reloaded++;
@@ -575,11 +586,17 @@ s3_status s3_evict_compact(s3_ctx* ctx, s3_evict_report* rep, int32_t* perm, s3_
     d2h_done = std::make_shared<EventBox>();
     if (!staged) {
       // synchronous fallback: copy straight from the arena before rows move
+      cudaEvent_t e0 = nullptr, e1 = nullptr;
+      if (ctx->prof.on) { e0 = ctx->prof.get(); e1 = ctx->prof.get(); cudaEventRecord(e0, ctx->st); }
       for (int32_t i = 0; i < h->n_evicted; ++i) {
         const DSlot& s = ctx->slots_h[dev[i].b];
         CK(cudaMemcpyAsync((uint8_t*)ctx->buf.host_store + hoff[i],
                            (uint8_t*)ctx->buf.arena + (int64_t)s.off * sh.kvpt, (size_t)dev[i].len * sh.kvpt,
                            cudaMemcpyDeviceToHost, ctx->st), "evict D2H (sync)");
+      }
+      if (ctx->prof.on) {
+        cudaEventRecord(e1, ctx->st);
+        ctx->prof.pending.push_back({e0, e1, (double)h->d2h_bytes, 2});
       }
       CK(cudaEventRecord(d2h_done->ev, ctx->st), "event");
     } else if (ctx->last_stage_d2h && !fused) {
@@ -608,9 +625,15 @@ s3_status s3_evict_compact(s3_ctx* ctx, s3_evict_report* rep, int32_t* perm, s3_
     CK(cudaEventRecord(k4, ctx->st), "event");
     CK(cudaStreamWaitEvent(ctx->side, k4, 0), "side wait");
     cudaEventDestroy(k4);
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (ctx->prof.on) { e0 = ctx->prof.get(); e1 = ctx->prof.get(); cudaEventRecord(e0, ctx->side); }
     for (int32_t i = 0; i < h->n_evicted; ++i)
       CK(cudaMemcpyAsync((uint8_t*)ctx->buf.host_store + hoff[i], (uint8_t*)ctx->buf.staging + dev[i].stage_off,
                          (size_t)dev[i].len * sh.kvpt, cudaMemcpyDeviceToHost, ctx->side), "evict D2H");
+    if (ctx->prof.on) {
+      cudaEventRecord(e1, ctx->side);
+      ctx->prof.pending.push_back({e0, e1, (double)h->d2h_bytes, 2});
+    }
     CK(cudaEventRecord(d2h_done->ev, ctx->side), "event");
     ctx->last_stage_d2h = d2h_done;
   }
@@ -816,11 +839,14 @@ s3_status s3_batch_view(const s3_ctx* ctx, s3_slot* slots, int32_t* B) {
 s3_status s3_profile_enable(s3_ctx* ctx, int32_t on) {
   if (s3_status s = check_ctx(ctx)) return s;
   CK(cudaStreamSynchronize(ctx->st), "sync");
+  CK(cudaStreamSynchronize(ctx->side), "side sync");
   prof_collect(ctx);
   ctx->prof.on = on != 0;
   ctx->prof.attn_launches = ctx->prof.move_launches = ctx->prof.fused_steps = 0;
   ctx->prof.attn_ms = ctx->prof.move_ms = ctx->prof.attn_bytes = ctx->prof.move_bytes = 0;
   ctx->prof.fused_move_bytes = 0;
+  ctx->prof.d2h_copies = ctx->prof.h2d_copies = 0;
+  ctx->prof.d2h_ms = ctx->prof.d2h_bytes = ctx->prof.h2d_ms = ctx->prof.h2d_bytes = 0;
   return S3_OK;
 }
 
@@ -828,6 +854,7 @@ s3_status s3_profile_get(s3_ctx* ctx, s3_profile* p) {
   if (s3_status s = check_ctx(ctx)) return s;
   if (!p) return fail(ctx, S3_E_INVAL, "profile_get: null");
   CK(cudaStreamSynchronize(ctx->st), "sync");
+  CK(cudaStreamSynchronize(ctx->side), "side sync");
   prof_collect(ctx);
   p->kernel_launches = ctx->launches;
   p->attn_launches = ctx->prof.attn_launches;
@@ -838,6 +865,9 @@ s3_status s3_profile_get(s3_ctx* ctx, s3_profile* p) {
   p->move_bytes = ctx->prof.move_bytes;
   p->fused_steps = ctx->prof.fused_steps;
   p->fused_move_bytes = ctx->prof.fused_move_bytes;
+  p->d2h_copies = ctx->prof.d2h_copies; p->h2d_copies = ctx->prof.h2d_copies;
+  p->d2h_ms = ctx->prof.d2h_ms; p->d2h_bytes = ctx->prof.d2h_bytes;
+  p->h2d_ms = ctx->prof.h2d_ms; p->h2d_bytes = ctx->prof.h2d_bytes;
   return S3_OK;
 }
 

@@ -74,7 +74,9 @@ class s3_slot(C.Structure):
 class s3_profile(C.Structure):
     _fields_ = [("kernel_launches", C.c_int64), ("attn_launches", C.c_int64), ("move_launches", C.c_int64),
                 ("fused_steps", C.c_int64), ("attn_ms", C.c_double), ("move_ms", C.c_double),
-                ("attn_bytes", C.c_double), ("move_bytes", C.c_double), ("fused_move_bytes", C.c_double)]
+                ("attn_bytes", C.c_double), ("move_bytes", C.c_double), ("fused_move_bytes", C.c_double),
+                ("d2h_copies", C.c_int64), ("h2d_copies", C.c_int64), ("d2h_ms", C.c_double),
+                ("d2h_bytes", C.c_double), ("h2d_ms", C.c_double), ("h2d_bytes", C.c_double)]
 
 
 P = C.c_void_p
