@@ -39,7 +39,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
-    ap.add_argument("--config", default="c1", choices=["c1", "c2", "c3"])
+    ap.add_argument("--config", default="c1", choices=["c1", "c2", "c3", "c4"])
     ap.add_argument("--p", type=float, default=0.1, help="short-prediction probability (c2)")
     ap.add_argument("--policy", default=None, help="override allocation policy")
     ap.add_argument("--impl", default="s3", choices=["s3", "reference"])
@@ -61,8 +61,10 @@ def workload(args):
         policy, p = "oracle", 0.0
     elif args.config == "c2":
         policy, p = "short", args.p
-    else:
+    elif args.config == "c3":
         policy, p = "maxlen", 0.0
+    else:                      # c4: 64k-request pool, bucket predictor, strong scaling over ranks
+        policy, p = "bucket", 0.0
     if args.policy:
         policy = args.policy
     return policy, p
@@ -220,7 +222,9 @@ def run_s3(args):
     from paper_2306_06000_b200.engine import S3Engine
 
     policy, p = workload(args)
-    n_req = args.requests * world                         # weak scaling: fixed work per GPU
+    # weak scaling (fixed work per GPU) except C4, a fixed 65,536-request pool
+    n_req = 65536 if args.config == "c4" else args.requests * world
+    scaling = "strong" if args.config == "c4" else "weak"
     t = s3synth.make_trace(n_req, seed=args.seed, policy=policy, p=p, max_seq_len=GPTJ["max_len"])
     L, H, D = GPTJ["L"], GPTJ["H"], GPTJ["D"]
     kvpt = 4 * L * H * D
@@ -333,11 +337,13 @@ def run_s3(args):
         line = {
             "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "scaling": scaling, "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {
                 "workload": f"{args.config.upper()}: GPT-J-6B-shaped KV (L=28, H=16, D=256, bf16 KV, fp32 "
                             f"accumulate), {args.requests} Alpaca-like requests per GPU, {policy} allocation"
-                            + (f" p={p}" if p else ""),
+                            + (f" p={p}" if p else "") if args.config != "c4" else
+                            "C4: GPT-J-6B-shaped KV, 65,536-request Alpaca-like pool partitioned by sequence over "
+                            f"{world} GPU(s), bucket predictor",
                 "requests_total": n_req, "arena_rows_per_gpu": R, "arena_gb_per_gpu": round(R * kvpt / 1e9, 1),
                 "mean_batch": float(np.mean(batch_sizes)), "parallelism": f"sequence-partitioned x{world}",
                 "l2": "working set (tens of GB per step) >> 126 MB L2; no flush needed",
@@ -437,18 +443,21 @@ def e2e_leg(eng, exchange, dist, dev, steps, world):
     the attention output goes back to pinned host memory (D2H inside)."""
     import torch
     L, H, D = eng.L, eng.H, eng.D
-    n = L * eng.max_running * H * D
+    # pinned buffers sized for the batch this run actually reaches (+50 %)
+    n = L * min(eng.max_running, int(1.5 * max(eng.B, 1)) + 64) * H * D
     hq = torch.empty(n, dtype=torch.bfloat16, pin_memory=True)
     hk = torch.empty(n, dtype=torch.bfloat16, pin_memory=True)
     hv = torch.empty(n, dtype=torch.bfloat16, pin_memory=True)
     he = torch.empty(eng.max_running, dtype=torch.uint8, pin_memory=True)
     ho = torch.empty(n, dtype=torch.float32, pin_memory=True)
-    total_ms, tokens, h2d, d2h = 0.0, 0, 0, 0
+    total_ms, tokens, h2d, d2h, done = 0.0, 0, 0, 0, 0
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     for _ in range(steps):
         B = eng.B
         m = L * B * H * D
+        if m > n:
+            break
         if B:
             eng.synth_inputs()                 # producer of this step's inputs (untimed)
             hq[:m].copy_(eng.q[:m]); hk[:m].copy_(eng.k_new[:m]); hv[:m].copy_(eng.v_new[:m])
@@ -477,6 +486,7 @@ def e2e_leg(eng, exchange, dist, dev, steps, world):
         tokens += B
         h2d += 3 * m * 2 + B
         d2h += m * 4
+        done += 1
     ms = total_ms
     tok = tokens
     if dist:
@@ -487,8 +497,8 @@ def e2e_leg(eng, exchange, dist, dev, steps, world):
         dist.all_reduce(tk)
         tok = int(tk.item())
     return {"value": tok / (ms / 1e3) if ms > 0 else 0.0, "unit": "tokens/s",
-            "h2d_bytes_per_step": h2d // max(steps, 1), "d2h_bytes_per_step": d2h // max(steps, 1),
-            "steps": steps}
+            "h2d_bytes_per_step": h2d // max(done, 1), "d2h_bytes_per_step": d2h // max(done, 1),
+            "steps": done}
 
 
 def main():
