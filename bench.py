@@ -456,8 +456,12 @@ def e2e_leg(eng, exchange, dist, dev, steps, world):
     for _ in range(steps):
         B = eng.B
         m = L * B * H * D
-        if m > n:
-            break
+        if m > n:                              # batch grew: re-pin (rare, outside the timed region)
+            n = int(1.5 * m)
+            hq = torch.empty(n, dtype=torch.bfloat16, pin_memory=True)
+            hk = torch.empty(n, dtype=torch.bfloat16, pin_memory=True)
+            hv = torch.empty(n, dtype=torch.bfloat16, pin_memory=True)
+            ho = torch.empty(n, dtype=torch.float32, pin_memory=True)
         if B:
             eng.synth_inputs()                 # producer of this step's inputs (untimed)
             hq[:m].copy_(eng.q[:m]); hk[:m].copy_(eng.k_new[:m]); hv[:m].copy_(eng.v_new[:m])
