@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--arena-gb", type=float, default=0.0, help="cap the arena (e.g. for ncu replay)")
     ap.add_argument("--attn", default="tma", choices=["tma", "regs"], help="attention kernel variant")
+    ap.add_argument("--model", default="none", choices=["none", "gptj"],
+                    help="gptj: random-weight GPT-J layers (cuBLAS GEMMs) around the path (SURVEY NEXT-2)")
     ap.add_argument("--compact", default="fused", choices=["fused", "pass"],
                     help="row shift as a separate k_move pass, or fused into the attention pass")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
@@ -234,7 +236,7 @@ def run_s3(args):
     free_b, _ = torch.cuda.mem_get_info(dev)
     if torch.cuda.device_count() < world:
         free_b //= world                                  # ranks share a device (tests only)
-    reserve = 6 << 30
+    reserve = (6 << 30) + ((16 << 30) if args.model == "gptj" else 0)
     R = int((free_b - io_bytes - staging - reserve - (2 << 30)) // kvpt)
     R = min(R, (1 << 31) - 1)
     if args.arena_gb > 0:
@@ -255,8 +257,18 @@ def run_s3(args):
 
     eng.submit(t.req_id, t.prompt, t.alloc, t.out)
     eng.initial_admit(exchange)
+    proxy = None
+    if args.model == "gptj":
+        from paper_2306_06000_b200.model_proxy import GPTJProxy
+        proxy = GPTJProxy(eng)
+
+    def step():
+        if proxy is None:
+            return eng.step(exchange)
+        return model_step(eng, proxy, exchange, world)
+
     for _ in range(args.warmup):
-        eng.step(exchange)
+        step()
     torch.cuda.synchronize()
     eng.profile(True)
     p0 = eng.profile_get()
@@ -272,7 +284,7 @@ def run_s3(args):
     totals = dict(d2h=0, moved=0, evicted=0, finished=0, admitted=0, reload=0, fill=0, pcie=0, hbm=0)
     batch_sizes = []
     for _ in range(args.steps):
-        s = eng.step(exchange)
+        s = step()
         tokens += s.tokens
         batch_sizes.append(s.batch)
         totals["d2h"] += s.d2h_bytes; totals["moved"] += s.moved_bytes; totals["evicted"] += s.evicted
@@ -298,11 +310,11 @@ def run_s3(args):
     launches = prof.kernel_launches - p0.kernel_launches
 
     # ---- per-phase breakdown (after the timed region; CUDA events) ---------
-    phases = phase_breakdown(eng, exchange, world, min(args.steps, 20))
+    phases = phase_breakdown(eng, exchange, world, min(args.steps, 20)) if proxy is None else None
 
     # ---- e2e through the public API with host buffers ----------------------
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and proxy is None:
         e2e = e2e_leg(eng, exchange, dist, cdev, min(args.steps, 50), world)
 
     peak, peak_kind = load_peak()
@@ -370,6 +382,12 @@ def run_s3(args):
             "tokens": tok_sum, "finished": totals["finished"], "admitted": totals["admitted"],
             "gpu_launches": launches,
             "phases_ms_per_step": phases,
+            "model_proxy": None if proxy is None else {
+                "kind": "GPT-J-6B shapes, random bf16 weights, cuBLAS GEMMs (QKV, O, FFN) at M = B",
+                "weight_gb": round(proxy.weight_bytes / 1e9, 2),
+                "gemm_tflop_per_step": round(proxy.flops(float(np.mean(batch_sizes))) / 1e12, 3),
+                "attention_share_of_step": round(prof.attn_ms / ms, 4),
+            },
             "latency_split": split,
             "pcie": {
                 "peak_gbs": pcie, "source": "pinned 1 GiB cudaMemcpyAsync, best of 5 (in-harness)",
@@ -385,6 +403,24 @@ def run_s3(args):
     eng.close()
     if dist:
         dist.destroy_process_group()
+
+
+def model_step(eng, proxy, exchange, world):
+    """One iteration with the GPT-J proxy: per-layer decode inside the model,
+    then evict+compact and admit."""
+    from paper_2306_06000_b200.engine import StepStats
+    B = proxy.decode_step()
+    rep, perm, ev, fin = eng.evict_compact()
+    if world == 1:
+        arep, _ = eng.admit()
+        reload_b, fill_b, n_adm = arep.h2d_bytes, arep.fill_bytes, arep.n_admitted
+    else:
+        hrep, _ = eng.admit_home()
+        srep, _ = eng.admit_shared(exchange(eng.counters_local()))
+        reload_b, fill_b = hrep.h2d_bytes + srep.h2d_bytes, hrep.fill_bytes + srep.fill_bytes
+        n_adm = hrep.n_admitted + srep.n_admitted
+    return StepStats(B, B, rep.n_finished, rep.n_evicted, n_adm, rep.d2h_bytes, rep.moved_bytes,
+                     rep.paper_pcie_bytes, rep.paper_hbm_bytes, reload_b, fill_b)
 
 
 def pcie_peaks(dev, nbytes=1 << 30, reps=5):

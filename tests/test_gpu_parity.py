@@ -333,3 +333,30 @@ def test_zero_length_prompts():
     alloc = np.array([2, 1, 6, 9, 2, 3], np.int32)
     t = s3synth.Trace(np.arange(6, dtype=np.int64), P, O, alloc, 64)
     lockstep(t, 2, 4, 64, 64, C=2, S=1024)
+
+
+def test_model_proxy_runs_per_layer_path():
+    """NEXT-2 proxy: random-weight GEMMs around per-layer decode calls; the
+    path must stay consistent (finite outputs, token conservation)."""
+    from paper_2306_06000_b200.engine import S3Engine
+    from paper_2306_06000_b200.model_proxy import GPTJProxy
+    t = s3synth.make_trace(40, seed=31, policy="short", p=0.2, max_seq_len=128, prompt_max=16)
+    eng = S3Engine(3, 4, 64, 128, 600, 64, chunk_rows=16, host_store_bytes=16 << 20)
+    proxy = GPTJProxy(eng, d_ff=1024)
+    eng.submit(t.req_id, t.prompt, t.alloc, t.out)
+    eng.admit()
+    tokens, done = 0, False
+    for _ in range(5000):
+        c = eng.counters_local()
+        if eng.B == 0 and c[3] + c[4] == 0:
+            done = True
+            break
+        B = proxy.decode_step()
+        tokens += B
+        if B:
+            assert torch.isfinite(eng.out[:B * 256]).all()
+        eng.evict_compact()
+        eng.admit()
+    assert done
+    assert tokens == int(t.out.sum())
+    eng.close()
