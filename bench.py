@@ -283,8 +283,14 @@ def run_s3(args):
     tokens = 0
     totals = dict(d2h=0, moved=0, evicted=0, finished=0, admitted=0, reload=0, fill=0, pcie=0, hbm=0)
     batch_sizes = []
+    below_ratios = []          # per eviction event: rows below / resident reserved rows ("m/2")
+    prev_tail = eng.counters_local()
+    prev_tail = R - int(prev_tail[0])
     for _ in range(args.steps):
         s = step()
+        if s.evicted and prev_tail > 0:
+            below_ratios.append((s.paper_hbm_bytes / 2 / kvpt) / (s.evicted * prev_tail))
+        prev_tail = R - int(eng.counters_local()[0])
         tokens += s.tokens
         batch_sizes.append(s.batch)
         totals["d2h"] += s.d2h_bytes; totals["moved"] += s.moved_bytes; totals["evicted"] += s.evicted
@@ -378,6 +384,8 @@ def run_s3(args):
                 "gbs": move_gbs, "frac": move_gbs / peak, "ms": prof.move_ms, "launches": prof.move_launches,
                 "moved_bytes": totals["moved"], "d2h_bytes": totals["d2h"], "evicted": totals["evicted"],
                 "paper_pcie_bytes": totals["pcie"], "paper_hbm_bytes": totals["hbm"],
+                "rows_below_over_resident_mean": (round(float(np.mean(below_ratios)), 4) if below_ratios else None),
+                "rows_below_events": len(below_ratios),
             },
             "tokens": tok_sum, "finished": totals["finished"], "admitted": totals["admitted"],
             "gpu_launches": launches,
