@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--arena-gb", type=float, default=0.0, help="cap the arena (e.g. for ncu replay)")
     ap.add_argument("--attn", default="tma", choices=["tma", "regs"], help="attention kernel variant")
+    ap.add_argument("--compact-policy", default="every", choices=["every", "on-demand"],
+                    help="row shift every step (the paper) or only when the pool could use the rows (R27)")
     ap.add_argument("--model", default="none", choices=["none", "gptj"],
                     help="gptj: random-weight GPT-J layers (cuBLAS GEMMs) around the path (SURVEY NEXT-2)")
     ap.add_argument("--compact", default="fused", choices=["fused", "pass"],
@@ -243,7 +245,8 @@ def run_s3(args):
         R = min(R, int(args.arena_gb * 1e9 // kvpt))
     eng = S3Engine(L, H, D, GPTJ["max_len"], R, max_running, device=local, rank=rank, world=world,
                    seed=args.seed, staging_bytes=staging, host_store_bytes=(16 << 30) if p > 0 else (1 << 30),
-                   attn_variant=0 if args.attn == "tma" else 1, compact_mode=0 if args.compact == "fused" else 1)
+                   attn_variant=0 if args.attn == "tma" else 1, compact_mode=0 if args.compact == "fused" else 1,
+                   compact_policy=0 if args.compact_policy == "every" else 1)
 
     exchange = None
     if world > 1:

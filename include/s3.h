@@ -78,6 +78,10 @@ typedef struct {
                                                nl = L) and the evictees fit in staging
                                                (default); 1 = separate ordered-move pass in
                                                s3_evict_compact                               */
+  int32_t compact_policy;                   /* 0 = shift every step (the paper, R6);
+                                               1 = on demand: only when the request pool is
+                                               non-empty after the step's evictions (R27)     */
+  int32_t reserved1;
 } s3_config;
 
 typedef struct {                            /* caller-owned memory                             */

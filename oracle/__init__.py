@@ -32,7 +32,8 @@ def build(force: bool = False) -> str:
 
 class Config(C.Structure):
     _fields_ = [("L", C.c_int32), ("H", C.c_int32), ("D", C.c_int32), ("max_len", C.c_int32),
-                ("R", C.c_int64), ("max_running", C.c_int32), ("seed", C.c_uint64)]
+                ("R", C.c_int64), ("max_running", C.c_int32), ("seed", C.c_uint64),
+                ("compact_policy", C.c_int32), ("reserved", C.c_int32)]
 
 
 class Slot(C.Structure):
@@ -136,14 +137,14 @@ def ffd_multibin(caps, reqs, free_by_rank, slots_by_rank) -> np.ndarray:
 
 
 def gen_kv(L, H, D, max_len, seed, req, l, kv, pos) -> np.ndarray:
-    cfg = Config(L, H, D, max_len, max_len, 1, seed)
+    cfg = Config(L, H, D, max_len, max_len, 1, seed, 0, 0)
     out = np.zeros(H * D, dtype=np.uint16)
     lib().s3o_gen_kv(C.byref(cfg), req, l, kv, pos, _p(out))
     return out.reshape(H, D)
 
 
 def gen_q(L, H, D, max_len, seed, req, l, pos) -> np.ndarray:
-    cfg = Config(L, H, D, max_len, max_len, 1, seed)
+    cfg = Config(L, H, D, max_len, max_len, 1, seed, 0, 0)
     out = np.zeros(H * D, dtype=np.uint16)
     lib().s3o_gen_q(C.byref(cfg), req, l, pos, _p(out))
     return out.reshape(H, D)
@@ -152,7 +153,7 @@ def gen_q(L, H, D, max_len, seed, req, l, pos) -> np.ndarray:
 def attend_generated(L, H, D, max_len, seed, req, pos, l) -> np.ndarray:
     """fp64 attention of request req at position pos, layer l, when its rows
     are the generator's (see s3o_attend_generated)."""
-    cfg = Config(L, H, D, max_len, max_len, 1, seed)
+    cfg = Config(L, H, D, max_len, max_len, 1, seed, 0, 0)
     out = np.zeros(H * D, dtype=np.float64)
     lib().s3o_attend_generated(C.byref(cfg), req, pos, l, _p(out))
     return out.reshape(H, D)
@@ -165,11 +166,11 @@ def bf16_bits_to_f64(bits: np.ndarray) -> np.ndarray:
 class Oracle:
     """The oracle state machine (one per simulated rank)."""
 
-    def __init__(self, L, H, D, max_len, R, max_running=1 << 20, seed=1):
+    def __init__(self, L, H, D, max_len, R, max_running=1 << 20, seed=1, compact_policy=0):
         self.L, self.H, self.D, self.max_len, self.R = L, H, D, max_len, R
         self.seed = seed
         self.max_running = max_running
-        self.cfg = Config(L, H, D, max_len, R, max_running, seed)
+        self.cfg = Config(L, H, D, max_len, R, max_running, seed, compact_policy, 0)
         self.h = lib().s3o_create(C.byref(self.cfg))
         if not self.h:
             raise ValueError("invalid oracle config")

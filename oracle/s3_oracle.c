@@ -405,19 +405,27 @@ int s3o_evict_compact(s3o_state* s, s3o_report* rep, int32_t* perm, s3o_evicted*
     }
   }
   /* Compaction in batch (= arena) order.  dst <= src, so a forward memmove
-   * of each survivor in order is safe. */
+   * of each survivor in order is safe.  Policy "on demand" (R27):
+   * shift only when the pool is non-empty after this step's evictions, i.e.
+   * when an admission could use the freed rows; otherwise survivors keep
+   * their rows and the tail is the end of the last survivor's slot. */
+  const int do_compact = s->c.compact_policy == 0 || s->npool > 0;
   int64_t new_tail = 0;
   int32_t nb = 0;
   for (int32_t b = 0; b < s->B; ++b) {
     s3o_slot sl = s->slots[b];
     if (s->status[b] == S3O_RUNNING) {
-      if (new_tail != sl.off) {
-        memmove(s->arena + new_tail * s->row_elems, s->arena + sl.off * s->row_elems,
-                sizeof(uint16_t) * (size_t)(sl.len * s->row_elems));
-        rep->moved_bytes += (int64_t)sl.len * kvpt;
+      if (do_compact) {
+        if (new_tail != sl.off) {
+          memmove(s->arena + new_tail * s->row_elems, s->arena + sl.off * s->row_elems,
+                  sizeof(uint16_t) * (size_t)(sl.len * s->row_elems));
+          rep->moved_bytes += (int64_t)sl.len * kvpt;
+        }
+        sl.off = new_tail;
+        new_tail += sl.cap;
+      } else {
+        new_tail = sl.off + sl.cap;
       }
-      sl.off = new_tail;
-      new_tail += sl.cap;
       if (perm) perm[b] = nb;
       s->slots[nb++] = sl;
     } else if (perm) {

@@ -171,6 +171,7 @@ bool validate(const s3_config* c) {
   if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return false;
   if (c->attn_variant < 0 || c->attn_variant > 1) return false;
   if (c->compact_mode < 0 || c->compact_mode > 1) return false;
+  if (c->compact_policy < 0 || c->compact_policy > 1) return false;
   return true;
 }
 
@@ -490,6 +491,8 @@ s3_status s3_decode_step(s3_ctx* ctx, int32_t l0, int32_t nl, const void* q, con
     PrepArgs pa;
     pa.sh = ctx->sh; pa.slots = ctx->slots[ctx->cur]; pa.next = ctx->slots[1 - ctx->cur]; pa.B = B; pa.C = ctx->C;
     pa.eos = eos; pa.finalize = finalize ? 1 : 0; pa.fuse = fuse ? 1 : 0;
+    pa.compact_policy = ctx->cfg.compact_policy;
+    pa.pool_nonempty = (ctx->pool.size() + ctx->home.size()) > 0 ? 1 : 0;
     pa.staging_bytes = ctx->buf.staging ? ctx->buf.staging_bytes : 0;
     pa.units = ctx->units; pa.splits = ctx->splits; pa.ctrl = ctx->ctrl; pa.report = ctx->report_dev;
     CK(launch_prep(pa, ctx->st), "k_prep");
@@ -554,7 +557,8 @@ s3_status s3_evict_compact(s3_ctx* ctx, s3_evict_report* rep, int32_t* perm, s3_
   }
   if (!fused) {
     CK(launch_keep_scan(sh, ctx->slots[ctx->cur], ctx->slots[1 - ctx->cur], B, ctx->S, ctx->report_dev,
-                        ctx->entries, ctx->key_chunk0, ctx->key_src, ctx->ctrl64, ctx->st), "k_keep_scan");
+                        ctx->entries, ctx->key_chunk0, ctx->key_src, ctx->ctrl64, ctx->cfg.compact_policy,
+                        (ctx->pool.size() + ctx->home.size()) > 0 ? 1 : 0, ctx->st), "k_keep_scan");
     ctx->launches += 1;
     CK(cudaMemcpyAsync(ctx->h_report, ctx->report_dev, (size_t)report_bytes(B), cudaMemcpyDeviceToHost, ctx->st),
        "report D2H");
@@ -665,8 +669,12 @@ s3_status s3_evict_compact(s3_ctx* ctx, s3_evict_report* rep, int32_t* perm, s3_
   for (int32_t b = 0; b < B; ++b) {
     if (dperm[b] >= 0) {
       DSlot s = ctx->slots_h[b];
-      s.off = (int32_t)run;
-      run += s.cap;
+      if (h->compacted) {
+        s.off = (int32_t)run;
+        run += s.cap;
+      } else {
+        run = (int64_t)s.off + s.cap;            // holes stay (R27); tail = end of the last slot
+      }
       kept.push_back(s);
     }
     if (perm) perm[b] = dperm[b];

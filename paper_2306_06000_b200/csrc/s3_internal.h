@@ -63,7 +63,8 @@ struct DReportHeader {
   int64_t tail, d2h_bytes, moved_bytes, pcie_bytes, hbm_bytes;
   int64_t n_chunks;
   int32_t n_entries, first_hole;
-  int32_t fused, reserved;     // fused: the decode step already moved / staged the rows
+  int32_t fused, compacted;    // fused: the decode step already moved / staged the rows;
+                               // compacted: survivors were shifted to prefix-sum offsets
   int64_t pad[6];
 };
 static_assert(sizeof(DReportHeader) == 128, "header 128 B");
@@ -98,6 +99,7 @@ struct PrepArgs {
   int32_t B, C;
   const uint8_t* eos;
   int32_t finalize, fuse;
+  int32_t compact_policy, pool_nonempty;   // on-demand compaction inputs (R27)
   int64_t staging_bytes;
   Unit* units;
   Split* splits;
@@ -113,7 +115,7 @@ cudaError_t launch_attn(const Shape& sh, const uint16_t* q, const uint16_t* k_ne
                         int32_t variant, cudaStream_t st);
 cudaError_t launch_keep_scan(const Shape& sh, const DSlot* cur, DSlot* next, int32_t B, int64_t S,
                              void* report, MoveEntry* entries, int32_t* key_chunk0, int32_t* key_src,
-                             int64_t* ctrl64, cudaStream_t st);
+                             int64_t* ctrl64, int32_t compact_policy, int32_t pool_nonempty, cudaStream_t st);
 cudaError_t launch_move(uint8_t* arena, uint8_t* staging, const MoveEntry* entries, const int32_t* key_chunk0,
                         const int32_t* key_src, int32_t n_entries, int64_t n_chunks, int64_t S, int64_t kvpt,
                         int64_t* ctrl64, uint32_t* flags, uint32_t epoch, int32_t staging_enabled, int32_t grid,

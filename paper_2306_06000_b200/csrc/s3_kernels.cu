@@ -156,7 +156,8 @@ __device__ __forceinline__ uint4 gen8(const Shape& sh, uint64_t seed, uint64_t t
 __global__ void __launch_bounds__(1024) k_prep(PrepArgs a) {
   __shared__ int s_first_hole;
   __shared__ unsigned long long s_hbm, s_moved;
-  if (threadIdx.x == 0) { s_first_hole = a.B; s_hbm = 0; s_moved = 0; }
+  __shared__ long long s_end;
+  if (threadIdx.x == 0) { s_first_hole = a.B; s_hbm = 0; s_moved = 0; s_end = 0; }
   const int B = a.B, C = a.C;
   const int64_t kvpt = a.sh.kvpt;
   const int per = (B + blockDim.x - 1) / blockDim.x;
@@ -184,12 +185,15 @@ __global__ void __launch_bounds__(1024) k_prep(PrepArgs a) {
   long long tot[10];
   block_excl_scan<10>(x, tot);
   const bool fused = a.fuse && a.finalize && tot[8] <= a.staging_bytes;
+  // R27: shift unless the policy is on-demand and nobody could use the rows
+  const bool compact = a.compact_policy == 0 || a.pool_nonempty || tot[7] > 0;
   int32_t* perm = reinterpret_cast<int32_t*>(a.report + report_perm_off(B));
   DEvicted* evl = reinterpret_cast<DEvicted*>(a.report + report_ev_off(B));
   int64_t* finl = reinterpret_cast<int64_t*>(a.report + report_fin_off(B));
   long long u = x[0], sp = x[1], p = x[2], stg = x[3];
   long long keep_i = x[4], keepcap = x[5], fin_i = x[6], ev_i = x[7], evb = x[8], capx = x[9];
   unsigned long long hbm = 0, moved = 0;
+  long long end = 0;
   int first = B;
   for (int b = b0; b < b1; ++b) {
     DSlot sl = a.slots[b];
@@ -199,8 +203,9 @@ __global__ void __launch_bounds__(1024) k_prep(PrepArgs a) {
     int64_t dst = sl.off;
     if (fused) {
       if (st == 0) {
-        mode = keepcap == sl.off ? UNIT_STAY : UNIT_MOVE;
-        dst = keepcap;
+        const int64_t noff = compact ? keepcap : sl.off;
+        mode = noff == sl.off ? UNIT_STAY : UNIT_MOVE;
+        dst = noff;
       } else if (st == 2) {
         mode = UNIT_STAGE;
         dst = evb;
@@ -248,8 +253,9 @@ __global__ void __launch_bounds__(1024) k_prep(PrepArgs a) {
     if (st == 0) {
       perm[b] = (int)keep_i;
       if (mode == UNIT_MOVE) moved += (unsigned long long)sl.len * kvpt;
-      sl.off = (int32_t)keepcap;
+      sl.off = (int32_t)dst;
       sl.status = 0;
+      end = max(end, (long long)sl.off + sl.cap);
       a.next[keep_i] = sl;
       ++keep_i;
       keepcap += sl.cap;
@@ -272,6 +278,7 @@ __global__ void __launch_bounds__(1024) k_prep(PrepArgs a) {
     if (first < B) atomicMin(&s_first_hole, first);
     if (hbm) atomicAdd(&s_hbm, hbm);
     if (moved) atomicAdd(&s_moved, moved);
+    if (end) atomicMax(&s_end, end);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -287,7 +294,7 @@ __global__ void __launch_bounds__(1024) k_prep(PrepArgs a) {
       h->n_finished = (int)tot[6];
       h->n_evicted = (int)tot[7];
       h->n_kept = (int)tot[4];
-      h->tail = tot[5];
+      h->tail = compact ? tot[5] : s_end;
       h->d2h_bytes = tot[8];
       h->moved_bytes = (int64_t)s_moved;
       h->pcie_bytes = 0;
@@ -296,7 +303,7 @@ __global__ void __launch_bounds__(1024) k_prep(PrepArgs a) {
       h->n_entries = 0;
       h->first_hole = s_first_hole;
       h->fused = 1;
-      h->reserved = 0;
+      h->compacted = compact ? 1 : 0;
     }
   }
 }
@@ -553,10 +560,12 @@ __global__ void __launch_bounds__(1024) k_keep_scan(Shape sh, const DSlot* __res
                                                     MoveEntry* __restrict__ entries,
                                                     int32_t* __restrict__ key_chunk0,
                                                     int32_t* __restrict__ key_src,
-                                                    int64_t* __restrict__ ctrl64) {
+                                                    int64_t* __restrict__ ctrl64,
+                                                    int32_t compact_policy, int32_t pool_nonempty) {
   __shared__ int s_first_hole;
   __shared__ unsigned long long s_hbm;
-  if (threadIdx.x == 0) { s_first_hole = B; s_hbm = 0; }
+  __shared__ long long s_end;
+  if (threadIdx.x == 0) { s_first_hole = B; s_hbm = 0; s_end = 0; }
   const int per = (B + blockDim.x - 1) / blockDim.x;
   const int b0 = threadIdx.x * per, b1 = min(B, b0 + per);
   const int64_t kvpt = sh.kvpt;
@@ -574,6 +583,7 @@ __global__ void __launch_bounds__(1024) k_keep_scan(Shape sh, const DSlot* __res
   }
   long long tot[6];
   block_excl_scan<6>(x, tot);
+  const bool compact = compact_policy == 0 || pool_nonempty || tot[3] > 0;   // R27
   int32_t* perm = reinterpret_cast<int32_t*>(report + report_perm_off(B));
   DEvicted* evl = reinterpret_cast<DEvicted*>(report + report_ev_off(B));
   int64_t* finl = reinterpret_cast<int64_t*>(report + report_fin_off(B));
@@ -582,6 +592,7 @@ __global__ void __launch_bounds__(1024) k_keep_scan(Shape sh, const DSlot* __res
   {
     long long keep_i = x[0], keepcap = x[1], fin_i = x[2], ev_i = x[3], evb = x[4], capx = x[5];
     unsigned long long hbm = 0;
+    long long end = 0;
     int first = B;
     for (int b = b0; b < b1; ++b) {
       DSlot sl = cur[b];
@@ -589,11 +600,12 @@ __global__ void __launch_bounds__(1024) k_keep_scan(Shape sh, const DSlot* __res
       if (!keep && b < first) first = b;
       if (keep) {
         perm[b] = (int)keep_i;
-        const int64_t new_off = keepcap;
+        const int64_t new_off = compact ? keepcap : sl.off;
         const int64_t bytes = (int64_t)sl.len * kvpt;
         if (new_off != sl.off && bytes > 0) { y[0] += 1; y[1] += (bytes + S - 1) / S; y[2] += bytes; }
         sl.off = (int32_t)new_off;
         sl.status = 0;
+        end = max(end, (long long)new_off + sl.cap);
         next[keep_i] = sl;
         ++keep_i;
         keepcap += sl.cap;
@@ -616,6 +628,7 @@ __global__ void __launch_bounds__(1024) k_keep_scan(Shape sh, const DSlot* __res
     }
     if (first < B) atomicMin(&s_first_hole, first);
     if (hbm) atomicAdd(&s_hbm, hbm);
+    if (end) atomicMax(&s_end, end);
   }
   long long ytot[3];
   block_excl_scan<3>(y, ytot);
@@ -626,7 +639,7 @@ __global__ void __launch_bounds__(1024) k_keep_scan(Shape sh, const DSlot* __res
       const DSlot sl = cur[b];
       const int64_t bytes = (int64_t)sl.len * kvpt;
       if (sl.status == 0) {
-        const int64_t new_off = keepcap;
+        const int64_t new_off = compact ? keepcap : sl.off;
         if (new_off != sl.off && bytes > 0) {
           MoveEntry me;
           me.src = (int64_t)sl.off * kvpt; me.dst = new_off * kvpt; me.bytes = bytes;
@@ -658,7 +671,7 @@ __global__ void __launch_bounds__(1024) k_keep_scan(Shape sh, const DSlot* __res
     h->n_finished = (int)tot[2];
     h->n_evicted = (int)tot[3];
     h->n_kept = (int)tot[0];
-    h->tail = tot[1];
+    h->tail = compact ? tot[1] : s_end;
     h->d2h_bytes = tot[4];
     h->moved_bytes = ytot[2];
     h->pcie_bytes = 0;
@@ -666,6 +679,8 @@ __global__ void __launch_bounds__(1024) k_keep_scan(Shape sh, const DSlot* __res
     h->n_chunks = ytot[1];
     h->n_entries = (int)ytot[0];
     h->first_hole = s_first_hole;
+    h->fused = 0;
+    h->compacted = compact ? 1 : 0;
     ctrl64[CTRL64_TICKET] = 0;
     ctrl64[CTRL64_N_CHUNKS] = ytot[1];
     key_chunk0[ytot[0]] = (int32_t)ytot[1];
@@ -1325,8 +1340,9 @@ cudaError_t launch_attn(const Shape& sh, const uint16_t* q, const uint16_t* k_ne
 
 cudaError_t launch_keep_scan(const Shape& sh, const DSlot* cur, DSlot* next, int32_t B, int64_t S,
                              void* report, MoveEntry* entries, int32_t* key_chunk0, int32_t* key_src,
-                             int64_t* ctrl64, cudaStream_t st) {
-  k_keep_scan<<<1, 1024, 0, st>>>(sh, cur, next, B, S, (uint8_t*)report, entries, key_chunk0, key_src, ctrl64);
+                             int64_t* ctrl64, int32_t compact_policy, int32_t pool_nonempty, cudaStream_t st) {
+  k_keep_scan<<<1, 1024, 0, st>>>(sh, cur, next, B, S, (uint8_t*)report, entries, key_chunk0, key_src, ctrl64,
+                                  compact_policy, pool_nonempty);
   return cudaGetLastError();
 }
 

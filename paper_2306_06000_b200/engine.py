@@ -38,7 +38,8 @@ class StepStats:
 class S3Engine:
     def __init__(self, num_layers, num_heads, head_dim, max_seq_len, arena_rows, max_running,
                  chunk_rows=0, move_chunk_bytes=0, device=0, rank=0, world=1, seed=1,
-                 staging_bytes=None, host_store_bytes=None, io_rows=None, attn_variant=0, compact_mode=0):
+                 staging_bytes=None, host_store_bytes=None, io_rows=None, attn_variant=0, compact_mode=0,
+                 compact_policy=0):
         if not torch.cuda.is_available():
             raise RuntimeError("S3Engine needs a CUDA device (no CPU fallback)")
         self.device = torch.device("cuda", device)
@@ -51,7 +52,8 @@ class S3Engine:
             num_layers=num_layers, num_heads=num_heads, head_dim=head_dim, max_seq_len=max_seq_len,
             arena_rows=arena_rows, max_running=max_running, chunk_rows=chunk_rows,
             move_chunk_bytes=move_chunk_bytes, device=device, stream=self.stream.cuda_stream,
-            rank=rank, world=world, synth_seed=seed, attn_variant=attn_variant, compact_mode=compact_mode)
+            rank=rank, world=world, synth_seed=seed, attn_variant=attn_variant, compact_mode=compact_mode,
+            compact_policy=compact_policy)
         arena_b, ws_b, st_min, hs_min = abi.s3_workspace_query(self.cfg)
         self.kvpt = 4 * num_layers * num_heads * head_dim
         self.arena = torch.empty(arena_b, dtype=torch.uint8, device=self.device)

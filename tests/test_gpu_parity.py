@@ -41,12 +41,13 @@ def u16(t: torch.Tensor) -> np.ndarray:
 
 
 def lockstep(trace, L, H, D, R, C=0, S=0, max_running=4096, staging=True, feed_oracle_inputs=False,
-             max_steps=100000, check_arena=True, attn_variant=0, compact_mode=0, poison=False):
+             max_steps=100000, check_arena=True, attn_variant=0, compact_mode=0, poison=False,
+             compact_policy=0):
     from paper_2306_06000_b200.engine import S3Engine
     eng = S3Engine(L, H, D, trace.max_seq_len, R, max_running, chunk_rows=C, move_chunk_bytes=S,
                    staging_bytes=None if staging else 0, host_store_bytes=64 << 20, attn_variant=attn_variant,
-                   compact_mode=compact_mode)
-    orc = oracle.Oracle(L, H, D, trace.max_seq_len, R, max_running=max_running)
+                   compact_mode=compact_mode, compact_policy=compact_policy)
+    orc = oracle.Oracle(L, H, D, trace.max_seq_len, R, max_running=max_running, compact_policy=compact_policy)
     eng.submit(trace.req_id, trace.prompt, trace.alloc, trace.out)
     orc.submit(trace.req_id, trace.prompt, trace.alloc)
     _, adm_g = eng.admit()
@@ -360,3 +361,11 @@ def test_model_proxy_runs_per_layer_path():
     assert done
     assert tokens == int(t.out.sum())
     eng.close()
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_on_demand_compaction_policy(mode):
+    # R27 on the GPU path (fused and separate pass), through the drain phase
+    t = s3synth.make_trace(60, seed=41, policy="short", p=0.3, max_seq_len=128, prompt_max=24)
+    r = lockstep(t, 2, 16, 256, 900, C=16, S=4096, compact_mode=mode, compact_policy=1, poison=True)
+    assert r["evictions"] > 0

@@ -546,3 +546,37 @@ def test_attend_generated_matches_state_machine(oracle_lib):
         for l in range(L):
             ref = oracle.attend_generated(L, H, D, 64, 1, req, ln, l)
             assert np.array_equal(out[l, b], ref)
+
+
+@pytest.mark.parametrize("policy,p", [("short", 0.3), ("oracle", 0.0)])
+def test_on_demand_compaction_same_schedule(oracle_lib, policy, p):
+    # R27: compacting only when the pool is non-empty after the step's
+    # evictions changes no admission, eviction or output -- only offsets
+    # while the pool is empty -- and never moves more bytes.
+    t = s3synth.make_trace(120, seed=19, policy=policy, p=p, max_seq_len=128, prompt_max=20)
+    logs = {}
+    for pol in (0, 1):
+        o = oracle.Oracle(1, 2, 64, 128, 700, compact_policy=pol)
+        o.submit(t.req_id, t.prompt, t.alloc)
+        ev = [("admit", tuple(o.admit()))]
+        outs, moved, holes = [], 0, 0
+        while True:
+            c = o.counters()
+            if o.B == 0 and c[3] + c[4] == 0:
+                break
+            q, k, v, eos = o.make_inputs(t.out)
+            out, st = o.decode(q, k, v, eos)
+            outs.append(out.copy())
+            rep, perm, e, fin = o.evict_compact()
+            moved += rep.moved_bytes
+            ev.append(("step", tuple(perm), tuple(x[0] for x in e), tuple(int(f) for f in fin)))
+            ev.append(("admit", tuple(o.admit())))
+            b = o.batch()
+            if b and b[0][5] != 0 or any(b[i][5] + b[i][4] != b[i + 1][5] for i in range(len(b) - 1)):
+                holes += 1
+        logs[pol] = (ev, outs, moved, holes)
+    assert logs[0][0] == logs[1][0]
+    assert all(np.array_equal(a, b) for a, b in zip(logs[0][1], logs[1][1]))
+    assert logs[1][2] <= logs[0][2]
+    assert logs[0][3] == 0            # every-step policy: never a hole after a step
+    assert logs[1][3] > 0             # on demand: holes persist in the drain phase
