@@ -251,12 +251,20 @@ def run_s3(args):
     exchange = None
     if world > 1:
         mat = torch.zeros(world, 8, dtype=torch.int64, device=cdev)
+        # its own stream: the exchange must not wait for this step's attention kernel
+        xstream = torch.cuda.Stream(device=dev) if cdev.type == "cuda" else None
 
         def exchange(row):
-            mat.zero_()
-            mat[rank].copy_(torch.from_numpy(row))
-            dist.all_reduce(mat)                          # NCCL over NVLink: the counter exchange
-            return mat.cpu().numpy()
+            if xstream is None:
+                mat.zero_()
+                mat[rank] = torch.from_numpy(row)
+                dist.all_reduce(mat)
+                return mat.numpy().copy()
+            with torch.cuda.stream(xstream):
+                mat.zero_()
+                mat[rank].copy_(torch.from_numpy(row))
+                dist.all_reduce(mat)                      # NCCL over NVLink: the counter exchange
+                return mat.cpu().numpy()
 
     eng.submit(t.req_id, t.prompt, t.alloc, t.out)
     eng.initial_admit(exchange)

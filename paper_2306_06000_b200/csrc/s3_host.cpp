@@ -130,7 +130,9 @@ struct s3_ctx {
   int64_t n_evicted_waiting = 0;
   // host store allocator (first fit) + deferred frees
   std::map<int64_t, int64_t> free_blocks;
-  std::vector<std::pair<int64_t, int64_t>> deferred_free;
+  struct Deferred { int64_t off, bytes; std::shared_ptr<EventBox> done; };
+  std::vector<Deferred> deferred_free;      // host-store ranges freed once their reload H2D completed
+  cudaEvent_t ev_report = nullptr;          // after the fused step's report readback
   std::shared_ptr<EventBox> last_stage_d2h;
   // state
   bool status_pending = false;
@@ -245,9 +247,13 @@ void hs_free(s3_ctx* c, int64_t off, int64_t n) {
   }
 }
 
-void flush_deferred(s3_ctx* c) {   // call only when cfg.stream is idle
-  for (auto& p : c->deferred_free) hs_free(c, p.first, p.second);
-  c->deferred_free.clear();
+void flush_deferred(s3_ctx* c) {   // free host-store ranges whose reload copy has completed
+  std::vector<s3_ctx::Deferred> keep;
+  for (auto& d : c->deferred_free) {
+    if (d.done && cudaEventQuery(d.done->ev) != cudaSuccess) { keep.push_back(d); continue; }
+    hs_free(c, d.off, d.bytes);
+  }
+  c->deferred_free.swap(keep);
 }
 
 void prof_collect(s3_ctx* c) {     // call when cfg.stream is idle; side-stream pairs may still run
@@ -307,7 +313,7 @@ s3_status place_items(s3_ctx* ctx, const std::vector<Item>& items, s3_admit_repo
           cudaEventRecord(e1, ctx->st);
           ctx->prof.pending.push_back({e0, e1, (double)it.host_bytes, 3});
         }
-        ctx->deferred_free.emplace_back(it.host_off, it.host_bytes);
+        ctx->deferred_free.push_back({it.host_off, it.host_bytes, nullptr});
         ctx->n_evicted_waiting--;
         r.n_reloaded++;
         r.h2d_bytes += it.host_bytes;
@@ -323,6 +329,12 @@ s3_status place_items(s3_ctx* ctx, const std::vector<Item>& items, s3_admit_repo
       ctx->slots_h.push_back(s);
       ctx->tail += it.cap;
       if (admitted_ids) admitted_ids[i] = it.req;
+    }
+    if (r.n_reloaded) {              // the reloads' host ranges may be reused once this event fires
+      auto done = std::make_shared<EventBox>();
+      CK(cudaEventRecord(done->ev, ctx->st), "event");
+      for (auto& d : ctx->deferred_free)
+        if (!d.done) d.done = done;
     }
     DSlot* dst = ctx->slots[ctx->cur] + B0;
     CK(cudaMemcpyAsync(dst, rec, (size_t)n * sizeof(DSlot), cudaMemcpyHostToDevice, ctx->st), "slot upload");
@@ -386,6 +398,7 @@ s3_status s3_kv_init(const s3_config* cfg, const s3_buffers* b, s3_ctx** out) {
   auto bail = [&](const char* m) { ctx->err = m; s3_kv_destroy(ctx); return S3_E_CUDA; };
   if (cudaSetDevice(cfg->device) != cudaSuccess) return bail("cudaSetDevice");
   if (cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking) != cudaSuccess) return bail("side stream");
+  if (cudaEventCreateWithFlags(&ctx->ev_report, cudaEventDisableTiming) != cudaSuccess) return bail("event");
   int dev = cfg->device;
   cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, dev);
   int occ = 1;
@@ -443,6 +456,8 @@ s3_status s3_kv_destroy(s3_ctx* ctx) {
   ctx->last_stage_d2h.reset();
   for (auto& p : ctx->prof.pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
   for (auto e : ctx->prof.free_events) cudaEventDestroy(e);
+  ctx->deferred_free.clear();
+  if (ctx->ev_report) cudaEventDestroy(ctx->ev_report);
   if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->h_report) cudaFreeHost(ctx->h_report);
   if (ctx->h_upload) cudaFreeHost(ctx->h_upload);
@@ -498,6 +513,13 @@ s3_status s3_decode_step(s3_ctx* ctx, int32_t l0, int32_t nl, const void* q, con
     CK(launch_prep(pa, ctx->st), "k_prep");
     ctx->launches += 1;
     if (fuse) {
+      // the keep-scan report is final now: read it back while attention runs, so the
+      // host's eviction bookkeeping and FFD overlap the attention kernel
+      CK(cudaMemcpyAsync(ctx->h_report, ctx->report_dev, (size_t)report_bytes(B), cudaMemcpyDeviceToHost,
+                         ctx->st), "report D2H");
+      CK(cudaMemcpyAsync(ctx->h_report + report_bytes(B), ctx->ctrl + CTRL_FUSED, 4, cudaMemcpyDeviceToHost,
+                         ctx->st), "fused flag D2H");
+      CK(cudaEventRecord(ctx->ev_report, ctx->st), "event");
       CK(launch_deps(ctx->units, ctx->ctrl, ctx->desc, ctx->num_sms * 4, ctx->st), "k_deps");
       ctx->launches += 1;
     }
@@ -547,12 +569,9 @@ s3_status s3_evict_compact(s3_ctx* ctx, s3_evict_report* rep, int32_t* perm, s3_
   const DReportHeader* h = reinterpret_cast<const DReportHeader*>(ctx->h_report);
   bool fused = false;
   if (ctx->fused_pending) {
-    // the decode step ran the keep-scan; read its report (and its verdict)
-    CK(cudaMemcpyAsync(ctx->h_report, ctx->report_dev, (size_t)report_bytes(B), cudaMemcpyDeviceToHost, ctx->st),
-       "report D2H");
-    CK(cudaMemcpyAsync(ctx->h_report + report_bytes(B), ctx->ctrl + CTRL_FUSED, 4, cudaMemcpyDeviceToHost, ctx->st),
-       "fused flag D2H");
-    CK(cudaStreamSynchronize(ctx->st), "report sync");
+    // the decode step ran the keep-scan and copied its report back before the
+    // attention kernel: wait for that copy only, not for the attention pass
+    CK(cudaEventSynchronize(ctx->ev_report), "report sync");
     fused = *reinterpret_cast<const int32_t*>(ctx->h_report + report_bytes(B)) == 1;
   }
   if (!fused) {
@@ -578,6 +597,11 @@ s3_status s3_evict_compact(s3_ctx* ctx, s3_evict_report* rep, int32_t* perm, s3_
   std::vector<int64_t> hoff(h->n_evicted);
   for (int32_t i = 0; i < h->n_evicted; ++i) {
     hoff[i] = hs_alloc(ctx, (int64_t)dev[i].len * sh.kvpt);
+    if (hoff[i] < 0) {               // ranges still pinned by in-flight reloads: drain them and retry
+      CK(cudaStreamSynchronize(ctx->st), "sync");
+      flush_deferred(ctx);
+      hoff[i] = hs_alloc(ctx, (int64_t)dev[i].len * sh.kvpt);
+    }
     if (hoff[i] < 0) return fail(ctx, S3_E_CUDA, "evict_compact: host store exhausted");
   }
   const bool staged = h->n_evicted > 0 && ctx->buf.staging && h->d2h_bytes <= ctx->buf.staging_bytes;

@@ -369,3 +369,25 @@ def test_on_demand_compaction_policy(mode):
     t = s3synth.make_trace(60, seed=41, policy="short", p=0.3, max_seq_len=128, prompt_max=24)
     r = lockstep(t, 2, 16, 256, 900, C=16, S=4096, compact_mode=mode, compact_policy=1, poison=True)
     assert r["evictions"] > 0
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_randomized_configurations(seed):
+    """Property sweep: random shapes, chunk sizes, move chunks, policies,
+    compaction modes, kernel variants, staging on/off; full runs in lockstep."""
+    rng = np.random.default_rng(1000 + seed)
+    D = int(rng.choice([64, 128, 256]))
+    H = int(rng.choice([1, 2, 4, 8])) if D < 256 else int(rng.choice([1, 2, 4]))
+    L = int(rng.integers(1, 4))
+    M = int(rng.choice([64, 96, 160]))
+    n = int(rng.integers(10, 50))
+    pol = str(rng.choice(["short", "bucket", "oracle", "maxlen"]))
+    t = s3synth.make_trace(n, seed=seed, policy=pol, p=0.3, max_seq_len=M, prompt_max=M // 4)
+    R = int(M * rng.integers(1, 6))
+    variant = int(rng.integers(0, 2))
+    mode = int(rng.integers(0, 2)) if variant == 0 else 1
+    r = lockstep(t, L, H, D, R, C=int(rng.choice([2, 5, 16, 64])), S=int(rng.choice([1024, 4096, 32768])),
+                 max_running=int(rng.choice([4, 16, 4096])), staging=bool(rng.integers(0, 2)),
+                 attn_variant=variant, compact_mode=mode, compact_policy=int(rng.integers(0, 2)),
+                 poison=bool(rng.integers(0, 2)))
+    print(seed, dict(L=L, H=H, D=D, M=M, n=n, pol=pol, R=R), r)
