@@ -29,7 +29,12 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "decode tokens/s + achieved HBM GB/s vs peak; evict+compact GB/s; 1/2/4/8 GPU"
-GPTJ = dict(L=28, H=16, D=256, max_len=2048)
+GPTJ = dict(L=28, H=16, D=256, max_len=2048, Hkv=16)
+SHAPES = {
+    "gptj": GPTJ,
+    # grouped-query KV: LLaMA-3-8B-shaped attention
+    "llama3-8b": dict(L=32, H=32, D=128, max_len=2048, Hkv=8),
+}
 REQ_PER_GPU = 8192
 FALLBACK_HBM_GBS = 6650.0   # /opt/skills/guides/B200_PROFILING.md fallback
 
@@ -47,6 +52,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--seed", type=int, default=1)
+    ap.add_argument("--shape", default="gptj", choices=sorted(SHAPES))
     ap.add_argument("--arena-gb", type=float, default=0.0, help="cap the arena (e.g. for ncu replay)")
     ap.add_argument("--attn", default="tma", choices=["tma", "regs"], help="attention kernel variant")
     ap.add_argument("--compact-policy", default="every", choices=["every", "on-demand"],
@@ -230,10 +236,11 @@ def run_s3(args):
     n_req = 65536 if args.config == "c4" else args.requests * world
     scaling = "strong" if args.config == "c4" else "weak"
     t = s3synth.make_trace(n_req, seed=args.seed, policy=policy, p=p, max_seq_len=GPTJ["max_len"])
-    L, H, D = GPTJ["L"], GPTJ["H"], GPTJ["D"]
-    kvpt = 4 * L * H * D
-    max_running = 8192
-    io_bytes = max_running * L * H * D * (3 * 2 + 4)
+    shp = SHAPES[args.shape]
+    L, H, D, Hkv = shp["L"], shp["H"], shp["D"], shp["Hkv"]
+    kvpt = 4 * L * Hkv * D
+    max_running = 8192 if args.shape == "gptj" else 16384
+    io_bytes = max_running * L * D * (H * 2 + 2 * Hkv * 2 + H * 4)
     staging = 4 << 30
     free_b, _ = torch.cuda.mem_get_info(dev)
     if torch.cuda.device_count() < world:
@@ -244,6 +251,7 @@ def run_s3(args):
     if args.arena_gb > 0:
         R = min(R, int(args.arena_gb * 1e9 // kvpt))
     eng = S3Engine(L, H, D, GPTJ["max_len"], R, max_running, device=local, rank=rank, world=world,
+                   num_kv_heads=0 if Hkv == H else Hkv,
                    seed=args.seed, staging_bytes=staging, host_store_bytes=(16 << 30) if p > 0 else (1 << 30),
                    attn_variant=0 if args.attn == "tma" else 1, compact_mode=0 if args.compact == "fused" else 1,
                    compact_policy=0 if args.compact_policy == "every" else 1)
@@ -368,7 +376,8 @@ def run_s3(args):
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": scaling, "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {
-                "workload": f"{args.config.upper()}: GPT-J-6B-shaped KV (L=28, H=16, D=256, bf16 KV, fp32 "
+                "workload": f"{args.config.upper()}: " + ("GPT-J-6B-shaped KV (L=28, H=16, D=256" if args.shape == "gptj"
+                            else f"{args.shape} KV (L={L}, H={H}, H_kv={Hkv}, D={D}") + ", bf16 KV, fp32 "
                             f"accumulate), {args.requests} Alpaca-like requests per GPU, {policy} allocation"
                             + (f" p={p}" if p else "") if args.config != "c4" else
                             "C4: GPT-J-6B-shaped KV, 65,536-request Alpaca-like pool partitioned by sequence over "

@@ -18,12 +18,13 @@
  * -----------
  * - Every function returns s3_status; nothing throws or longjmps across the ABI.
  * - Data layout: the KV arena is bf16
- *   [R][L][2][H][D] -- one token ROW holds all layers' K and V of that token,
- *   kvpt = 4*L*H*D bytes ("4 l d_h bytes per token").  A
+ *   [R][L][2][H_kv][D] -- one token ROW holds all layers' K and V of that
+ *   token, kvpt = 4*L*H_kv*D bytes ("4 l d_h bytes per token").  A
  *   sequence owns rows [off, off+cap); rows [off, off+len) are resident.
  *   Slots are kept in arena order (batch index b increases with off).
- * - q / k_new / v_new are bf16 [nl][B][H][D]; out is fp32 [nl][B][H][D]; B is
- *   the running batch size (s3_batch_size), b the batch index.
+ * - q is bf16 [nl][B][H][D], k_new / v_new bf16 [nl][B][H_kv][D] (H_kv = H
+ *   unless num_kv_heads is set); out is fp32 [nl][B][H][D]; B is the running
+ *   batch size (s3_batch_size), b the batch index.  Pointers 16-B aligned.
  * - All device pointers are on cfg.device; all device work is ordered on
  *   cfg.stream (a cudaStream_t, e.g. torch's current stream).
  * - Ownership: the caller allocates and frees every buffer in s3_buffers
@@ -62,7 +63,7 @@ enum { S3_RUNNING = 0, S3_FINISHED = 1, S3_OVERRUN = 2 };
 typedef struct s3_ctx s3_ctx;
 
 typedef struct {
-  int32_t num_layers, num_heads, head_dim;  /* L, H, D; head_dim in {64,128,256}; H*D <= 8192 */
+  int32_t num_layers, num_heads, head_dim;  /* L, H, D; head_dim in {64,128,256}; H*D <= 4096 */
   int32_t max_seq_len;                      /* cap on P + output (2048 for GPT-J runs)         */
   int64_t arena_rows;                       /* R >= max_seq_len                                */
   int32_t max_running;                      /* metadata capacity B_max (admission stops there) */
@@ -81,7 +82,9 @@ typedef struct {
   int32_t compact_policy;                   /* 0 = shift every step (the paper, R6);
                                                1 = on demand: only when the request pool is
                                                non-empty after the step's evictions (R27)     */
-  int32_t reserved1;
+  int32_t num_kv_heads;                     /* KV heads H_kv (0 = num_heads; must divide it):
+                                               grouped-query / multi-query KV, query head h
+                                               reads KV head h / (H / H_kv); kvpt = 4*L*H_kv*D */
 } s3_config;
 
 typedef struct {                            /* caller-owned memory                             */

@@ -33,7 +33,7 @@ def build(force: bool = False) -> str:
 class Config(C.Structure):
     _fields_ = [("L", C.c_int32), ("H", C.c_int32), ("D", C.c_int32), ("max_len", C.c_int32),
                 ("R", C.c_int64), ("max_running", C.c_int32), ("seed", C.c_uint64),
-                ("compact_policy", C.c_int32), ("reserved", C.c_int32)]
+                ("compact_policy", C.c_int32), ("Hkv", C.c_int32)]
 
 
 class Slot(C.Structure):
@@ -136,11 +136,12 @@ def ffd_multibin(caps, reqs, free_by_rank, slots_by_rank) -> np.ndarray:
     return who
 
 
-def gen_kv(L, H, D, max_len, seed, req, l, kv, pos) -> np.ndarray:
-    cfg = Config(L, H, D, max_len, max_len, 1, seed, 0, 0)
-    out = np.zeros(H * D, dtype=np.uint16)
+def gen_kv(L, H, D, max_len, seed, req, l, kv, pos, Hkv=0) -> np.ndarray:
+    cfg = Config(L, H, D, max_len, max_len, 1, seed, 0, Hkv)
+    nh = Hkv or H
+    out = np.zeros(nh * D, dtype=np.uint16)
     lib().s3o_gen_kv(C.byref(cfg), req, l, kv, pos, _p(out))
-    return out.reshape(H, D)
+    return out.reshape(nh, D)
 
 
 def gen_q(L, H, D, max_len, seed, req, l, pos) -> np.ndarray:
@@ -150,10 +151,10 @@ def gen_q(L, H, D, max_len, seed, req, l, pos) -> np.ndarray:
     return out.reshape(H, D)
 
 
-def attend_generated(L, H, D, max_len, seed, req, pos, l) -> np.ndarray:
+def attend_generated(L, H, D, max_len, seed, req, pos, l, Hkv=0) -> np.ndarray:
     """fp64 attention of request req at position pos, layer l, when its rows
     are the generator's (see s3o_attend_generated)."""
-    cfg = Config(L, H, D, max_len, max_len, 1, seed, 0, 0)
+    cfg = Config(L, H, D, max_len, max_len, 1, seed, 0, Hkv)
     out = np.zeros(H * D, dtype=np.float64)
     lib().s3o_attend_generated(C.byref(cfg), req, pos, l, _p(out))
     return out.reshape(H, D)
@@ -166,16 +167,17 @@ def bf16_bits_to_f64(bits: np.ndarray) -> np.ndarray:
 class Oracle:
     """The oracle state machine (one per simulated rank)."""
 
-    def __init__(self, L, H, D, max_len, R, max_running=1 << 20, seed=1, compact_policy=0):
+    def __init__(self, L, H, D, max_len, R, max_running=1 << 20, seed=1, compact_policy=0, Hkv=0):
         self.L, self.H, self.D, self.max_len, self.R = L, H, D, max_len, R
+        self.Hkv = Hkv or H
         self.seed = seed
         self.max_running = max_running
-        self.cfg = Config(L, H, D, max_len, R, max_running, seed, compact_policy, 0)
+        self.cfg = Config(L, H, D, max_len, R, max_running, seed, compact_policy, Hkv)
         self.h = lib().s3o_create(C.byref(self.cfg))
         if not self.h:
             raise ValueError("invalid oracle config")
-        self.row_elems = 2 * L * H * D
-        self.kvpt = 4 * L * H * D
+        self.row_elems = 2 * L * self.Hkv * D
+        self.kvpt = 4 * L * self.Hkv * D
         self.n_submitted = 0
 
     def __del__(self):
@@ -206,7 +208,7 @@ class Oracle:
         ptr = lib().s3o_arena(self.h)
         n = self.R * self.row_elems
         return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_uint16)), shape=(n,)).reshape(
-            self.R, self.L, 2, self.H, self.D)
+            self.R, self.L, 2, self.Hkv, self.D)
 
     def host_kv(self, req):
         ptr = C.c_void_p()
@@ -215,19 +217,20 @@ class Oracle:
             return None
         n = rows * self.row_elems
         return np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_uint16)), shape=(n,)).reshape(
-            rows, self.L, 2, self.H, self.D).copy()
+            rows, self.L, 2, self.Hkv, self.D).copy()
 
     def make_inputs(self, out_len_by_req):
         B = self.B
         n = self.L * B * self.H * self.D
+        nk = self.L * B * self.Hkv * self.D
         q = np.zeros(max(n, 1), np.uint16)
-        k = np.zeros(max(n, 1), np.uint16)
-        v = np.zeros(max(n, 1), np.uint16)
+        k = np.zeros(max(nk, 1), np.uint16)
+        v = np.zeros(max(nk, 1), np.uint16)
         eos = np.zeros(max(B, 1), np.uint8)
         o = np.ascontiguousarray(out_len_by_req, dtype=np.int32)
         lib().s3o_make_inputs(self.h, _p(o), _p(q), _p(k), _p(v), _p(eos))
-        shp = (self.L, B, self.H, self.D)
-        return q[:n].reshape(shp), k[:n].reshape(shp), v[:n].reshape(shp), eos[:B]
+        return (q[:n].reshape(self.L, B, self.H, self.D), k[:nk].reshape(self.L, B, self.Hkv, self.D),
+                v[:nk].reshape(self.L, B, self.Hkv, self.D), eos[:B])
 
     def decode(self, q, k, v, eos):
         B = self.B

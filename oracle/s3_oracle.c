@@ -61,12 +61,16 @@ static uint16_t float_to_bf16_bits_exact(float f) {
   return (uint16_t)(u >> 16);   /* values here have <= 8 significant bits */
 }
 
+static int32_t kv_heads(const s3o_config* c) { return c->Hkv > 0 ? c->Hkv : c->H; }
+
+/* tag 0 (K/V rows) runs over the Hkv KV heads, tag 1 (q) over the H query heads */
 static void gen_values(const s3o_config* c, int tag, int64_t req, int32_t l, int32_t kv,
                        int32_t pos, float denom, uint16_t* out_hd) {
-  for (int32_t h = 0; h < c->H; ++h) {
+  const int32_t nh = tag == 0 ? kv_heads(c) : c->H;
+  for (int32_t h = 0; h < nh; ++h) {
     for (int32_t d8 = 0; d8 < c->D / 8; ++d8) {
       uint64_t g = (((((uint64_t)req * (uint64_t)c->L + (uint64_t)l) * 2u + (uint64_t)kv)
-                     * (uint64_t)c->max_len + (uint64_t)pos) * (uint64_t)c->H + (uint64_t)h)
+                     * (uint64_t)c->max_len + (uint64_t)pos) * (uint64_t)nh + (uint64_t)h)
                    * (uint64_t)(c->D / 8) + (uint64_t)d8;
       uint64_t z = s3o_splitmix64(c->seed ^ ((uint64_t)tag << 60) ^ g);
       for (int j = 0; j < 8; ++j) {
@@ -191,11 +195,12 @@ struct s3o_state {
 
 s3o_state* s3o_create(const s3o_config* c) {
   if (c->L < 1 || c->H < 1 || c->D < 8 || c->D % 8 || c->max_len < 1 || c->R < c->max_len ||
-      c->max_running < 1)
+      c->max_running < 1 || c->Hkv < 0 || (c->Hkv > 0 && c->H % c->Hkv))
     return NULL;
   s3o_state* s = (s3o_state*)calloc(1, sizeof(s3o_state));
   s->c = *c;
-  s->row_elems = 2LL * c->L * c->H * c->D;
+  if (s->c.Hkv == 0) s->c.Hkv = c->H;
+  s->row_elems = 2LL * c->L * s->c.Hkv * c->D;
   s->arena = (uint16_t*)calloc((size_t)(c->R * s->row_elems), sizeof(uint16_t));
   s->slots = (s3o_slot*)calloc((size_t)c->max_running, sizeof(s3o_slot));
   s->status = (uint8_t*)calloc((size_t)c->max_running, 1);
@@ -258,39 +263,41 @@ int64_t s3o_host_kv(const s3o_state* s, int64_t req, const uint16_t** kv) {
 }
 
 static uint16_t* row_ptr(s3o_state* s, int64_t row, int32_t l, int32_t kv) {
-  return s->arena + row * s->row_elems + ((int64_t)l * 2 + kv) * s->c.H * s->c.D;
+  return s->arena + row * s->row_elems + ((int64_t)l * 2 + kv) * s->c.Hkv * s->c.D;
 }
 
 /* Inputs of one decode step: for slot b at position pos = len_b,
  * k_new/v_new = KV(req, l, kv, pos) and q = Q(req, l, pos); the sampler's
  * EOS fires when this token is the request's last one (gen + 1 == O).
- * Layout of q, k, v: [L][B][H][D].                                         */
+ * Layout: q [L][B][H][D], k and v [L][B][Hkv][D].                          */
 void s3o_make_inputs(const s3o_state* s, const int32_t* out_len_by_req, uint16_t* q,
                      uint16_t* k, uint16_t* v, uint8_t* eos) {
-  const int64_t HD = (int64_t)s->c.H * s->c.D;
+  const int64_t HD = (int64_t)s->c.H * s->c.D, KD = (int64_t)s->c.Hkv * s->c.D;
   for (int32_t b = 0; b < s->B; ++b) {
     const s3o_slot* sl = &s->slots[b];
     for (int32_t l = 0; l < s->c.L; ++l) {
-      int64_t o = ((int64_t)l * s->B + b) * HD;
-      s3o_gen_kv(&s->c, sl->req, l, 0, sl->len, k + o);
-      s3o_gen_kv(&s->c, sl->req, l, 1, sl->len, v + o);
-      s3o_gen_q(&s->c, sl->req, l, sl->len, q + o);
+      s3o_gen_kv(&s->c, sl->req, l, 0, sl->len, k + ((int64_t)l * s->B + b) * KD);
+      s3o_gen_kv(&s->c, sl->req, l, 1, sl->len, v + ((int64_t)l * s->B + b) * KD);
+      s3o_gen_q(&s->c, sl->req, l, sl->len, q + ((int64_t)l * s->B + b) * HD);
     }
     eos[b] = (uint8_t)(sl->gen + 1 == out_len_by_req[sl->req]);
   }
 }
 
-/* softmax(q K^T / sqrt(D)) V for one layer, all heads, over n rows; row j's
- * K (all heads) starts at K0 + j*stride, V likewise.       */
+/* softmax(q K^T / sqrt(D)) V for one layer, all H query heads, over n rows;
+ * row j's K (all Hkv KV heads) starts at K0 + j*stride, V likewise; query
+ * head h uses KV head h / (H/Hkv) (grouped-query attention; Hkv = H is MHA)
+ * (PAPER.md:106).                                                          */
 static void attend(const uint16_t* q_hd, const uint16_t* K0, const uint16_t* V0, int64_t stride,
-                   int32_t n, int32_t H, int32_t D, double* sc, double* out_hd) {
+                   int32_t n, int32_t H, int32_t Hkv, int32_t D, double* sc, double* out_hd) {
   const double inv_sqrt_d = 1.0 / sqrt((double)D);
   for (int32_t h = 0; h < H; ++h) {
     const uint16_t* qh = q_hd + (int64_t)h * D;
+    const int64_t kvo = (int64_t)(h / (H / Hkv)) * D;
     /* scores s_j = q . K_j / sqrt(D), j = 0..n-1 */
     double m = -INFINITY;
     for (int32_t j = 0; j < n; ++j) {
-      const uint16_t* kj = K0 + j * stride + (int64_t)h * D;
+      const uint16_t* kj = K0 + j * stride + kvo;
       double acc = 0.0;
       for (int32_t d = 0; d < D; ++d) acc += bf16_to_double(qh[d]) * bf16_to_double(kj[d]);
       sc[j] = acc * inv_sqrt_d;
@@ -302,7 +309,7 @@ static void attend(const uint16_t* q_hd, const uint16_t* K0, const uint16_t* V0,
     double* o = out_hd + (int64_t)h * D;
     for (int32_t d = 0; d < D; ++d) {
       double acc = 0.0;
-      for (int32_t j = 0; j < n; ++j) acc += sc[j] * bf16_to_double(V0[j * stride + (int64_t)h * D + d]);
+      for (int32_t j = 0; j < n; ++j) acc += sc[j] * bf16_to_double(V0[j * stride + kvo + d]);
       o[d] = acc / den;
     }
   }
@@ -320,8 +327,8 @@ static void attend(const uint16_t* q_hd, const uint16_t* K0, const uint16_t* V0,
 int s3o_decode(s3o_state* s, const uint16_t* q, const uint16_t* k, const uint16_t* v,
                const uint8_t* eos, double* out, uint8_t* status_out) {
   if (s->status_valid) return 5;  /* previous statuses not yet consumed */
-  const int32_t H = s->c.H, D = s->c.D, L = s->c.L;
-  const int64_t HD = (int64_t)H * D;
+  const int32_t H = s->c.H, D = s->c.D, L = s->c.L, Hkv = s->c.Hkv;
+  const int64_t HD = (int64_t)H * D, KD = (int64_t)Hkv * D;
   double* sc = (double*)malloc(sizeof(double) * (size_t)(s->c.max_len + 1));
   for (int32_t b = 0; b < s->B; ++b) {
     s3o_slot* sl = &s->slots[b];
@@ -329,12 +336,13 @@ int s3o_decode(s3o_state* s, const uint16_t* q, const uint16_t* k, const uint16_
     const int32_t pos = sl->len;
     for (int32_t l = 0; l < L; ++l) {
       const int64_t io = ((int64_t)l * s->B + b) * HD;
+      const int64_t ko = ((int64_t)l * s->B + b) * KD;
       /* append: row off+pos <- (k_new, v_new) */
-      memcpy(row_ptr(s, sl->off + pos, l, 0), k + io, sizeof(uint16_t) * (size_t)HD);
-      memcpy(row_ptr(s, sl->off + pos, l, 1), v + io, sizeof(uint16_t) * (size_t)HD);
+      memcpy(row_ptr(s, sl->off + pos, l, 0), k + ko, sizeof(uint16_t) * (size_t)KD);
+      memcpy(row_ptr(s, sl->off + pos, l, 1), v + ko, sizeof(uint16_t) * (size_t)KD);
       /* attend over rows 0..pos (self included, R1) */
       attend(q + io, row_ptr(s, sl->off, l, 0), row_ptr(s, sl->off, l, 1), s->row_elems, pos + 1,
-             H, D, sc, out + io);
+             H, Hkv, D, sc, out + io);
     }
     sl->len += 1;
     sl->gen += 1;
@@ -368,7 +376,7 @@ int s3o_decode(s3o_state* s, const uint16_t* q, const uint16_t* k, const uint16_
 int s3o_evict_compact(s3o_state* s, s3o_report* rep, int32_t* perm, s3o_evicted* ev,
                       int64_t* finished) {
   if (!s->status_valid) return 5;
-  const int64_t kvpt = s3o_kv_bytes_per_token(s->c.L, s->c.H, s->c.D);
+  const int64_t kvpt = s3o_kv_bytes_per_token(s->c.L, s->c.Hkv, s->c.D);
   memset(rep, 0, sizeof(*rep));
   rep->n_before = s->B;
   rep->first_hole = s->B;
@@ -576,15 +584,16 @@ void s3o_counters(const s3o_state* s, int64_t row[8]) {
  * j = 0..pos, q = Q(req,l,pos).  Lets tests check sampled outputs of a
  * full-size GPU run one at a time.  out: double [H][D].                    */
 void s3o_attend_generated(const s3o_config* c, int64_t req, int32_t pos, int32_t l, double* out_hd) {
-  const int64_t HD = (int64_t)c->H * c->D;
-  uint16_t* rows = (uint16_t*)malloc(sizeof(uint16_t) * (size_t)((pos + 1) * 2 * HD));
-  uint16_t* q = (uint16_t*)malloc(sizeof(uint16_t) * (size_t)HD);
+  const int32_t Hkv = kv_heads(c);
+  const int64_t KD = (int64_t)Hkv * c->D;
+  uint16_t* rows = (uint16_t*)malloc(sizeof(uint16_t) * (size_t)((pos + 1) * 2 * KD));
+  uint16_t* q = (uint16_t*)malloc(sizeof(uint16_t) * (size_t)((int64_t)c->H * c->D));
   double* sc = (double*)malloc(sizeof(double) * (size_t)(pos + 1));
   for (int32_t j = 0; j <= pos; ++j) {
-    s3o_gen_kv(c, req, l, 0, j, rows + (int64_t)j * 2 * HD);
-    s3o_gen_kv(c, req, l, 1, j, rows + (int64_t)j * 2 * HD + HD);
+    s3o_gen_kv(c, req, l, 0, j, rows + (int64_t)j * 2 * KD);
+    s3o_gen_kv(c, req, l, 1, j, rows + (int64_t)j * 2 * KD + KD);
   }
   s3o_gen_q(c, req, l, pos, q);
-  attend(q, rows, rows + HD, 2 * HD, pos + 1, c->H, c->D, sc, out_hd);
+  attend(q, rows, rows + KD, 2 * KD, pos + 1, c->H, Hkv, c->D, sc, out_hd);
   free(sc); free(q); free(rows);
 }

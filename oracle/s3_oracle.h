@@ -24,7 +24,7 @@ typedef struct {
   int32_t max_running;    /* metadata capacity (admission stops at it)   */
   uint64_t seed;          /* synthetic value generator seed              */
   int32_t compact_policy; /* 0 = every step (R6), 1 = on demand (R27)    */
-  int32_t reserved;
+  int32_t Hkv;            /* KV heads (0 = H); query head h reads KV head h / (H/Hkv) */
 } s3o_config;
 
 enum { S3O_RUNNING = 0, S3O_FINISHED = 1, S3O_OVERRUN = 2 };

@@ -164,7 +164,8 @@ bool validate(const s3_config* c) {
   if (!c) return false;
   if (c->num_layers < 1 || c->num_heads < 1) return false;
   if (c->head_dim != 64 && c->head_dim != 128 && c->head_dim != 256) return false;
-  if ((int64_t)c->num_heads * c->head_dim > 8192) return false;
+  if ((int64_t)c->num_heads * c->head_dim > 4096) return false;   // <= 16 head warps per attention CTA
+  if (c->num_kv_heads < 0 || (c->num_kv_heads > 0 && c->num_heads % c->num_kv_heads)) return false;
   if (c->max_seq_len < 1 || c->arena_rows < c->max_seq_len) return false;
   if (c->arena_rows > INT32_MAX) return false;
   if (c->max_running < 1 || c->max_running > 65535) return false;
@@ -180,8 +181,10 @@ bool validate(const s3_config* c) {
 Shape make_shape(const s3_config* c) {
   Shape s;
   s.L = c->num_layers; s.H = c->num_heads; s.D = c->head_dim; s.max_len = c->max_seq_len;
-  s.row_elems = 2LL * s.L * s.H * s.D;
-  s.kvpt = 4LL * s.L * s.H * s.D;
+  s.Hkv = c->num_kv_heads > 0 ? c->num_kv_heads : c->num_heads;
+  s.pad = 0;
+  s.row_elems = 2LL * s.L * s.Hkv * s.D;
+  s.kvpt = 4LL * s.L * s.Hkv * s.D;
   return s;
 }
 
@@ -535,10 +538,10 @@ s3_status s3_decode_step(s3_ctx* ctx, int32_t l0, int32_t nl, const void* q, con
       cudaEventRecord(e1, ctx->st);
       int64_t sum_len = 0;
       for (const DSlot& s : ctx->slots_h) sum_len += s.len;
-      const double HD = (double)ctx->sh.H * ctx->sh.D;
-      // algorithmic bytes: prior rows K+V, new row write,
-      // k_new+v_new read, q read (bf16), out write (fp32)
-      const double bytes = nl * HD * (4.0 * (double)sum_len + 4.0 * B + 4.0 * B + 2.0 * B + 4.0 * B);
+      const double HD = (double)ctx->sh.H * ctx->sh.D, KD = (double)ctx->sh.Hkv * ctx->sh.D;
+      // algorithmic bytes: prior rows K+V (KV heads), new row
+      // write, k_new+v_new read, q read (bf16, query heads), out write (fp32)
+      const double bytes = nl * (KD * (4.0 * (double)sum_len + 4.0 * B + 4.0 * B) + HD * (2.0 * B + 4.0 * B));
       ctx->prof.pending.push_back({e0, e1, bytes, 0});
     }
   }

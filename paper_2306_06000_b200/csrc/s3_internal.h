@@ -87,7 +87,8 @@ S3_HD inline int64_t report_bytes(int32_t B) { return report_fin_off(B) + 8 * (i
 
 struct Shape {
   int32_t L, H, D, max_len;
-  int64_t row_elems;     // 2*L*H*D bf16 elements per token row
+  int32_t Hkv, pad;      // KV heads (grouped-query attention; Hkv == H is MHA)
+  int64_t row_elems;     // 2*L*Hkv*D bf16 elements per token row
   int64_t kvpt;          // bytes per token row
 };
 

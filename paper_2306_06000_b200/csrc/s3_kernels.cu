@@ -120,10 +120,12 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
   return z ^ (z >> 31);
 }
 // 8 bf16 values (one 16-byte vector) for element group d8 of (req,l,kv,pos,h).
+// tag 0 (K/V rows) indexes the Hkv KV heads, tag 1 (q) the H query heads.
 __device__ __forceinline__ uint4 gen8(const Shape& sh, uint64_t seed, uint64_t tag, int64_t req,
                                       int l, int kv, int pos, int h, int d8, float scale) {
+  const uint64_t nh = tag == 0 ? (uint64_t)sh.Hkv : (uint64_t)sh.H;
   const uint64_t g =
-      (((((uint64_t)req * sh.L + l) * 2u + kv) * (uint64_t)sh.max_len + pos) * sh.H + h) *
+      (((((uint64_t)req * sh.L + l) * 2u + kv) * (uint64_t)sh.max_len + pos) * nh + h) *
           (uint64_t)(sh.D / 8) + d8;
   const uint64_t z = splitmix64(seed ^ (tag << 60) ^ g);
   uint32_t w[4];
@@ -430,7 +432,9 @@ __global__ void __launch_bounds__(512, 1) k_attn(AttnArgs a) {
   const int H = a.sh.H;
   const bool active = head < H;
   const int hh = active ? head : H - 1;
-  const int64_t HD = (int64_t)H * D;
+  const int hk = hh / (H / a.sh.Hkv);             // this query head's KV head
+  const bool kv_writer = active && hh % (H / a.sh.Hkv) == 0;
+  const int64_t HD = (int64_t)H * D, KD = (int64_t)a.sh.Hkv * D;
   const int64_t rowE = a.sh.row_elems;
   __shared__ int s_item;
   const int n_units = a.ctrl[CTRL_N_UNITS];
@@ -445,9 +449,10 @@ __global__ void __launch_bounds__(512, 1) k_attn(AttnArgs a) {
     const int li = item - u * a.nl;
     const int l = a.l0 + li;
     const Unit un = a.units[u];
-    const uint16_t* kbase = a.arena + (int64_t)un.off * rowE + (int64_t)l * 2 * HD + hh * D + sub * 8;
-    const uint16_t* vbase = kbase + HD;
+    const uint16_t* kbase = a.arena + (int64_t)un.off * rowE + (int64_t)l * 2 * KD + hk * D + sub * 8;
+    const uint16_t* vbase = kbase + KD;
     const int64_t io = ((int64_t)li * a.B + un.b) * HD + hh * D + sub * 8;
+    const int64_t iok = ((int64_t)li * a.B + un.b) * KD + hk * D + sub * 8;
     float qf[8];
     unpack8(ld_plain(a.q + io), qf);
 #pragma unroll
@@ -480,9 +485,9 @@ __global__ void __launch_bounds__(512, 1) k_attn(AttnArgs a) {
     }
     if (un.has_new) {
       // append: row off+len <- (k_new, v_new), and attend to it from registers
-      const uint4 kr = ld_plain(a.k_new + io);
-      const uint4 vr = ld_plain(a.v_new + io);
-      if (active) {
+      const uint4 kr = ld_plain(a.k_new + iok);
+      const uint4 vr = ld_plain(a.v_new + iok);
+      if (kv_writer) {
         st_v4((void*)(kbase + (int64_t)un.len * rowE), kr);
         st_v4((void*)(vbase + (int64_t)un.len * rowE), vr);
       }
@@ -946,9 +951,9 @@ __global__ void __launch_bounds__(576, 1) k_attn_tma(AttnArgs a, int32_t ns) {
   constexpr int HPW = 32 / LPH;
   extern __shared__ __align__(128) uint8_t smem[];
   const int H = a.sh.H;
-  const int64_t HD = (int64_t)H * D;
-  const int64_t rowB = 4 * HD;                     // one layer-row: K and V of all heads
-  const int64_t stageB = AT_RPS * rowB + 2 * HD;   // rows + q of the item
+  const int64_t HD = (int64_t)H * D, KD = (int64_t)a.sh.Hkv * D;
+  const int64_t rowB = 4 * KD;                     // one layer-row: K and V of all KV heads
+  const int64_t stageB = AT_RPS * rowB + 2 * HD;   // rows + q of the item (H query heads)
   const int64_t kvpt = a.sh.kvpt;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + ns * stageB);
   uint64_t* empty = full + ns;
@@ -1092,6 +1097,8 @@ __global__ void __launch_bounds__(576, 1) k_attn_tma(AttnArgs a, int32_t ns) {
   const int sub = lane % LPH;
   const bool active = head < H;
   const int hh = active ? head : H - 1;
+  const int hk = hh / (H / a.sh.Hkv);             // this query head's KV head
+  const bool kv_writer = active && hh % (H / a.sh.Hkv) == 0;
   const int64_t rowE = a.sh.row_elems;
   float qf[8], m = -INFINITY, ssum = 0.f, acc[8];
   int li = 0;
@@ -1110,19 +1117,20 @@ __global__ void __launch_bounds__(576, 1) k_attn_tma(AttnArgs a, int32_t ns) {
       ssum = 0.f;
     }
     const int64_t io = ((int64_t)li * a.B + h.b) * HD + hh * D + sub * 8;
+    const int64_t iok = ((int64_t)li * a.B + h.b) * KD + hk * D + sub * 8;
     uint4 kr = make_uint4(0, 0, 0, 0), vr = kr;
     const bool last_new = (h.flags & 2) && (h.flags & 4);
     if (last_new) {              // issue the new row's loads early; used after the stage
-      kr = ld_plain(a.k_new + io);
-      vr = ld_plain(a.v_new + io);
+      kr = ld_plain(a.k_new + iok);
+      vr = ld_plain(a.v_new + iok);
     }
     if (h.n > 0) {
       uint4 kc[AT_RPS], vc[AT_RPS];
 #pragma unroll
       for (int i = 0; i < AT_RPS; ++i) {
         if (i < h.n) {
-          kc[i] = lds128(sb + i * rowB + (hh * D + sub * 8) * 2);
-          vc[i] = lds128(sb + i * rowB + (HD + hh * D + sub * 8) * 2);
+          kc[i] = lds128(sb + i * rowB + (hk * D + sub * 8) * 2);
+          vc[i] = lds128(sb + i * rowB + (KD + hk * D + sub * 8) * 2);
         } else {
           kc[i] = make_uint4(0, 0, 0, 0);
           vc[i] = kc[i];
@@ -1136,7 +1144,7 @@ __global__ void __launch_bounds__(576, 1) k_attn_tma(AttnArgs a, int32_t ns) {
       if (last_new) {
         // append: the new row goes where the slot's rows end up
         uint16_t* kdst = nullptr;
-        const int64_t lofs = (int64_t)(a.l0 + li) * 2 * HD + hh * D + sub * 8;
+        const int64_t lofs = (int64_t)(a.l0 + li) * 2 * KD + hk * D + sub * 8;
         if (h.mode == UNIT_STAY) {
           kdst = a.arena + (int64_t)(h.off + h.len) * rowE + lofs;
         } else if (h.mode == UNIT_MOVE) {
@@ -1146,9 +1154,9 @@ __global__ void __launch_bounds__(576, 1) k_attn_tma(AttnArgs a, int32_t ns) {
         } else if (h.mode == UNIT_STAGE) {
           kdst = reinterpret_cast<uint16_t*>(a.staging + h.dst + (int64_t)h.len * kvpt) + lofs;
         }
-        if (active && kdst) {
+        if (kv_writer && kdst) {
           st_v4(kdst, kr);
-          st_v4(kdst + HD, vr);
+          st_v4(kdst + KD, vr);
         }
         uint4 k1[1] = {kr}, v1[1] = {vr};
         attn_rows<D, 1>(k1, v1, 1, qf, m, ssum, acc);
@@ -1172,15 +1180,15 @@ __global__ void __launch_bounds__(576, 1) k_attn_tma(AttnArgs a, int32_t ns) {
 }
 
 int attn_tma_stages(const Shape& sh) {
-  const int64_t HD = (int64_t)sh.H * sh.D;
-  const int64_t stageB = AT_RPS * 4 * HD + 2 * HD;
+  const int64_t HD = (int64_t)sh.H * sh.D, KD = (int64_t)sh.Hkv * sh.D;
+  const int64_t stageB = AT_RPS * 4 * KD + 2 * HD;
   const int64_t per = stageB + 16 + sizeof(StageHdr);
   const int64_t ns = (227 * 1024 - 64) / per;
   return (int)std::min<int64_t>(ns, AT_NS_MAX);
 }
 int attn_tma_smem(const Shape& sh, int ns) {
-  const int64_t HD = (int64_t)sh.H * sh.D;
-  return (int)(ns * (AT_RPS * 4 * HD + 2 * HD) + ns * (16 + (int64_t)sizeof(StageHdr)));
+  const int64_t HD = (int64_t)sh.H * sh.D, KD = (int64_t)sh.Hkv * sh.D;
+  return (int)(ns * (AT_RPS * 4 * KD + 2 * HD) + ns * (16 + (int64_t)sizeof(StageHdr)));
 }
 const void* attn_tma_kernel_ptr(const Shape& sh) {
   switch (sh.D) {
@@ -1203,17 +1211,17 @@ __global__ void __launch_bounds__(256) k_fill(Shape sh, uint64_t seed, const DSl
   if (p0 >= sl.prompt) return;
   const int p1 = min(sl.prompt, p0 + FILL_ROWS);
   const int D8 = sh.D / 8;
-  const int per_row = sh.L * 2 * sh.H * D8;   // 16-byte vectors per row
+  const int per_row = sh.L * 2 * sh.Hkv * D8;   // 16-byte vectors per row
   const int total = (p1 - p0) * per_row;
   for (int i = threadIdx.x; i < total; i += blockDim.x) {
     const int pos = p0 + i / per_row;
     int r = i % per_row;
     const int d8 = r % D8; r /= D8;
-    const int h = r % sh.H; r /= sh.H;
+    const int h = r % sh.Hkv; r /= sh.Hkv;
     const int kv = r % 2;
     const int l = r / 2;
     const uint4 v = gen8(sh, seed, 0, sl.req, l, kv, pos, h, d8, 1.f / 128.f);
-    st_v4(arena + ((int64_t)sl.off + pos) * sh.row_elems + ((int64_t)(l * 2 + kv) * sh.H + h) * sh.D + d8 * 8, v);
+    st_v4(arena + ((int64_t)sl.off + pos) * sh.row_elems + ((int64_t)(l * 2 + kv) * sh.Hkv + h) * sh.D + d8 * 8, v);
   }
 }
 
@@ -1225,20 +1233,27 @@ __global__ void __launch_bounds__(256) k_synth(Shape sh, uint64_t seed, const DS
                                                const int32_t* __restrict__ out_len, int64_t n_req,
                                                uint16_t* q, uint16_t* k, uint16_t* v, uint8_t* eos) {
   const int D8 = sh.D / 8;
-  const int64_t total = (int64_t)nl * B * sh.H * D8;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+  const int64_t tq = (int64_t)nl * B * sh.H * D8;     // q: [nl][B][H][D]
+  const int64_t tk = (int64_t)nl * B * sh.Hkv * D8;   // k_new, v_new: [nl][B][Hkv][D]
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tq + tk;
        i += (int64_t)gridDim.x * blockDim.x) {
-    int64_t r = i;
+    const bool isq = i < tq;
+    const int64_t j = isq ? i : i - tq;
+    const int nh = isq ? sh.H : sh.Hkv;
+    int64_t r = j;
     const int d8 = (int)(r % D8); r /= D8;
-    const int h = (int)(r % sh.H); r /= sh.H;
+    const int h = (int)(r % nh); r /= nh;
     const int b = (int)(r % B);
     const int li = (int)(r / B);
     const DSlot sl = slots[b];
     const int l = l0 + li;
-    const int64_t o = i * 8;
-    st_v4(k + o, gen8(sh, seed, 0, sl.req, l, 0, sl.len, h, d8, 1.f / 128.f));
-    st_v4(v + o, gen8(sh, seed, 0, sl.req, l, 1, sl.len, h, d8, 1.f / 128.f));
-    st_v4(q + o, gen8(sh, seed, 1, sl.req, l, 0, sl.len, h, d8, 1.f / 32.f));
+    const int64_t o = j * 8;
+    if (isq) {
+      st_v4(q + o, gen8(sh, seed, 1, sl.req, l, 0, sl.len, h, d8, 1.f / 32.f));
+    } else {
+      st_v4(k + o, gen8(sh, seed, 0, sl.req, l, 0, sl.len, h, d8, 1.f / 128.f));
+      st_v4(v + o, gen8(sh, seed, 0, sl.req, l, 1, sl.len, h, d8, 1.f / 128.f));
+    }
     if (i < B) {
       const DSlot s2 = slots[i];
       const int O = (s2.req >= 0 && s2.req < n_req) ? out_len[s2.req] : 0x7fffffff;
@@ -1255,7 +1270,7 @@ __global__ void __launch_bounds__(256) k_verify(Shape sh, uint64_t seed, const D
                                                 unsigned long long* bad) {
   const DSlot sl = slots[blockIdx.y];
   const int D8 = sh.D / 8;
-  const int64_t per_row = (int64_t)sh.L * 2 * sh.H * D8;
+  const int64_t per_row = (int64_t)sh.L * 2 * sh.Hkv * D8;
   const int64_t total = (int64_t)sl.len * per_row;
   unsigned long long nbad = 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -1263,12 +1278,12 @@ __global__ void __launch_bounds__(256) k_verify(Shape sh, uint64_t seed, const D
     const int pos = (int)(i / per_row);
     int64_t r = i % per_row;
     const int d8 = (int)(r % D8); r /= D8;
-    const int h = (int)(r % sh.H); r /= sh.H;
+    const int h = (int)(r % sh.Hkv); r /= sh.Hkv;
     const int kv = (int)(r % 2);
     const int l = (int)(r / 2);
     const uint4 want = gen8(sh, seed, 0, sl.req, l, kv, pos, h, d8, 1.f / 128.f);
     const uint4 got = ld_plain(arena + ((int64_t)sl.off + pos) * sh.row_elems +
-                               ((int64_t)(l * 2 + kv) * sh.H + h) * sh.D + d8 * 8);
+                               ((int64_t)(l * 2 + kv) * sh.Hkv + h) * sh.D + d8 * 8);
     nbad += (want.x != got.x) | (want.y != got.y) | (want.z != got.z) | (want.w != got.w);
   }
   if (nbad) atomicAdd(bad, nbad);
@@ -1371,7 +1386,7 @@ cudaError_t launch_synth(const Shape& sh, uint64_t seed, const DSlot* slots, int
                          int32_t nl, const int32_t* out_len_by_req, int64_t n_req, uint16_t* q,
                          uint16_t* k, uint16_t* v, uint8_t* eos, cudaStream_t st) {
   if (B <= 0) return cudaSuccess;
-  const int64_t total = (int64_t)nl * B * sh.H * (sh.D / 8);
+  const int64_t total = (int64_t)nl * B * (sh.H + sh.Hkv) * (sh.D / 8);
   const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 16);
   k_synth<<<(int)blocks, 256, 0, st>>>(sh, seed, slots, B, l0, nl, out_len_by_req, n_req, q, k, v, eos);
   return cudaGetLastError();

@@ -39,12 +39,13 @@ class S3Engine:
     def __init__(self, num_layers, num_heads, head_dim, max_seq_len, arena_rows, max_running,
                  chunk_rows=0, move_chunk_bytes=0, device=0, rank=0, world=1, seed=1,
                  staging_bytes=None, host_store_bytes=None, io_rows=None, attn_variant=0, compact_mode=0,
-                 compact_policy=0):
+                 compact_policy=0, num_kv_heads=0):
         if not torch.cuda.is_available():
             raise RuntimeError("S3Engine needs a CUDA device (no CPU fallback)")
         self.device = torch.device("cuda", device)
         torch.cuda.set_device(self.device)
         self.L, self.H, self.D = num_layers, num_heads, head_dim
+        self.Hkv = num_kv_heads or num_heads
         self.max_running = max_running
         self.world, self.rank = world, rank
         self.stream = torch.cuda.current_stream(self.device)
@@ -53,9 +54,9 @@ class S3Engine:
             arena_rows=arena_rows, max_running=max_running, chunk_rows=chunk_rows,
             move_chunk_bytes=move_chunk_bytes, device=device, stream=self.stream.cuda_stream,
             rank=rank, world=world, synth_seed=seed, attn_variant=attn_variant, compact_mode=compact_mode,
-            compact_policy=compact_policy)
+            compact_policy=compact_policy, num_kv_heads=num_kv_heads)
         arena_b, ws_b, st_min, hs_min = abi.s3_workspace_query(self.cfg)
-        self.kvpt = 4 * num_layers * num_heads * head_dim
+        self.kvpt = 4 * num_layers * self.Hkv * head_dim
         self.arena = torch.empty(arena_b, dtype=torch.uint8, device=self.device)
         self.workspace = torch.empty(ws_b, dtype=torch.uint8, device=self.device)
         st_b = st_min if staging_bytes is None else staging_bytes
@@ -68,9 +69,10 @@ class S3Engine:
         self.ctx = abi.s3_kv_init(self.cfg, bufs)
         rows = io_rows or max_running
         n = num_layers * rows * num_heads * head_dim
+        nk = num_layers * rows * self.Hkv * head_dim
         self.q = torch.empty(n, dtype=torch.bfloat16, device=self.device)
-        self.k_new = torch.empty(n, dtype=torch.bfloat16, device=self.device)
-        self.v_new = torch.empty(n, dtype=torch.bfloat16, device=self.device)
+        self.k_new = torch.empty(nk, dtype=torch.bfloat16, device=self.device)
+        self.v_new = torch.empty(nk, dtype=torch.bfloat16, device=self.device)
         self.out = torch.empty(n, dtype=torch.float32, device=self.device)
         self.eos = torch.empty(max(rows, 1), dtype=torch.uint8, device=self.device)
         self.out_len = None
@@ -184,8 +186,8 @@ class S3Engine:
     def arena_rows_view(self) -> torch.Tensor:
         """The arena as bf16 [R][L][2][H][D] (a view, no copy)."""
         R = self.cfg.arena_rows
-        return self.arena.view(torch.bfloat16).view(R, self.L, 2, self.H, self.D)
+        return self.arena.view(torch.bfloat16).view(R, self.L, 2, self.Hkv, self.D)
 
     def host_rows(self, host_off: int, rows: int) -> torch.Tensor:
         n = rows * self.kvpt
-        return self.host_store[host_off:host_off + n].view(torch.bfloat16).view(rows, self.L, 2, self.H, self.D)
+        return self.host_store[host_off:host_off + n].view(torch.bfloat16).view(rows, self.L, 2, self.Hkv, self.D)

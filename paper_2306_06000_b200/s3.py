@@ -34,7 +34,7 @@ class s3_config(C.Structure):
                 ("chunk_rows", C.c_int32), ("move_chunk_bytes", C.c_int32), ("device", C.c_int32),
                 ("stream", C.c_void_p), ("rank", C.c_int32), ("world", C.c_int32),
                 ("synth_seed", C.c_uint64), ("attn_variant", C.c_int32), ("compact_mode", C.c_int32),
-                ("compact_policy", C.c_int32), ("reserved1", C.c_int32)]
+                ("compact_policy", C.c_int32), ("num_kv_heads", C.c_int32)]
 
 
 class s3_buffers(C.Structure):

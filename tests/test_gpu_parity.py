@@ -42,12 +42,13 @@ def u16(t: torch.Tensor) -> np.ndarray:
 
 def lockstep(trace, L, H, D, R, C=0, S=0, max_running=4096, staging=True, feed_oracle_inputs=False,
              max_steps=100000, check_arena=True, attn_variant=0, compact_mode=0, poison=False,
-             compact_policy=0):
+             compact_policy=0, Hkv=0):
     from paper_2306_06000_b200.engine import S3Engine
     eng = S3Engine(L, H, D, trace.max_seq_len, R, max_running, chunk_rows=C, move_chunk_bytes=S,
                    staging_bytes=None if staging else 0, host_store_bytes=64 << 20, attn_variant=attn_variant,
-                   compact_mode=compact_mode, compact_policy=compact_policy)
-    orc = oracle.Oracle(L, H, D, trace.max_seq_len, R, max_running=max_running, compact_policy=compact_policy)
+                   compact_mode=compact_mode, compact_policy=compact_policy, num_kv_heads=Hkv)
+    orc = oracle.Oracle(L, H, D, trace.max_seq_len, R, max_running=max_running, compact_policy=compact_policy,
+                        Hkv=Hkv)
     eng.submit(trace.req_id, trace.prompt, trace.alloc, trace.out)
     orc.submit(trace.req_id, trace.prompt, trace.alloc)
     _, adm_g = eng.admit()
@@ -55,6 +56,7 @@ def lockstep(trace, L, H, D, R, C=0, S=0, max_running=4096, staging=True, feed_o
     assert adm_g == adm_o
     worst, steps, stats = 0.0, 0, dict(evictions=0, moved=0, splits=0)
     HD = H * D
+    KD = (Hkv or H) * D
     while True:
         c = orc.counters()
         if orc.B == 0 and c[3] + c[4] == 0:
@@ -72,18 +74,19 @@ def lockstep(trace, L, H, D, R, C=0, S=0, max_running=4096, staging=True, feed_o
             eng.arena_rows_view()[(~resident).to(eng.device)] = float("nan")
         q, k, v, eos = orc.make_inputs(trace.out)
         n = L * B * HD
+        nk = L * B * KD
         if B:
             if feed_oracle_inputs:
                 eng.q[:n].copy_(torch.from_numpy(q.reshape(-1).view(np.int16)).view(torch.bfloat16))
-                eng.k_new[:n].copy_(torch.from_numpy(k.reshape(-1).view(np.int16)).view(torch.bfloat16))
-                eng.v_new[:n].copy_(torch.from_numpy(v.reshape(-1).view(np.int16)).view(torch.bfloat16))
+                eng.k_new[:nk].copy_(torch.from_numpy(k.reshape(-1).view(np.int16)).view(torch.bfloat16))
+                eng.v_new[:nk].copy_(torch.from_numpy(v.reshape(-1).view(np.int16)).view(torch.bfloat16))
                 eng.eos[:B].copy_(torch.from_numpy(eos))
             else:
                 eng.synth_inputs()
                 # T0 at run time: the CUDA generator equals the oracle's
                 assert np.array_equal(u16(eng.q[:n]), q.reshape(-1))
-                assert np.array_equal(u16(eng.k_new[:n]), k.reshape(-1))
-                assert np.array_equal(u16(eng.v_new[:n]), v.reshape(-1))
+                assert np.array_equal(u16(eng.k_new[:nk]), k.reshape(-1))
+                assert np.array_equal(u16(eng.v_new[:nk]), v.reshape(-1))
                 assert np.array_equal(eng.eos[:B].cpu().numpy(), eos)
         ref, st = orc.decode(q, k, v, eos)
         eng.decode()
@@ -391,3 +394,12 @@ def test_randomized_configurations(seed):
                  attn_variant=variant, compact_mode=mode, compact_policy=int(rng.integers(0, 2)),
                  poison=bool(rng.integers(0, 2)))
     print(seed, dict(L=L, H=H, D=D, M=M, n=n, pol=pol, R=R), r)
+
+
+@pytest.mark.parametrize("H,Hkv,D,variant,mode", [(8, 2, 128, 0, 0), (8, 2, 128, 1, 1), (4, 1, 64, 0, 0),
+                                                  (16, 4, 256, 0, 1), (32, 8, 128, 0, 0)])
+def test_grouped_query_kv(H, Hkv, D, variant, mode):
+    """NEXT-4: grouped-query / multi-query KV through the whole path."""
+    t = s3synth.make_trace(40, seed=51, policy="short", p=0.3, max_seq_len=128, prompt_max=24)
+    r = lockstep(t, 2, H, D, 800, C=8, S=2048, attn_variant=variant, compact_mode=mode, Hkv=Hkv, poison=True)
+    assert r["evictions"] > 0

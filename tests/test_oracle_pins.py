@@ -580,3 +580,29 @@ def test_on_demand_compaction_same_schedule(oracle_lib, policy, p):
     assert logs[1][2] <= logs[0][2]
     assert logs[0][3] == 0            # every-step policy: never a hole after a step
     assert logs[1][3] > 0             # on demand: holes persist in the drain phase
+
+
+@pytest.mark.parametrize("H,Hkv", [(8, 2), (4, 1), (4, 4)])
+def test_gqa_attention_matches_sdpa_with_repeated_kv(oracle_lib, H, Hkv):
+    # NEXT-4: grouped-query attention = MHA with each KV head repeated for its
+    # H/Hkv query heads (library cross-check, torch SDPA in fp64).
+    L, D = 2, 64
+    o = oracle.Oracle(L, H, D, 64, 128, Hkv=Hkv)
+    o.submit(np.arange(3), [1, 9, 30], [4, 4, 4])
+    o.admit()
+    q, k, v, eos = o.make_inputs(np.full(3, 100, np.int32))
+    assert k.shape == (L, 3, Hkv, D) and q.shape == (L, 3, H, D)
+    out, _ = o.decode(q, k, v, eos)
+    A = o.arena()
+    G = H // Hkv
+    for b, (req, P, gen, ln, cap, off) in enumerate(o.batch()):
+        for l in range(L):
+            K = torch.from_numpy(oracle.bf16_bits_to_f64(A[off:off + ln, l, 0])).permute(1, 0, 2)
+            V = torch.from_numpy(oracle.bf16_bits_to_f64(A[off:off + ln, l, 1])).permute(1, 0, 2)
+            K = K.repeat_interleave(G, dim=0)
+            V = V.repeat_interleave(G, dim=0)
+            Q = torch.from_numpy(oracle.bf16_bits_to_f64(q[l, b]))[:, None, :]
+            ref = torch.nn.functional.scaled_dot_product_attention(Q, K, V)[:, 0, :].numpy()
+            assert np.allclose(out[l, b], ref, rtol=0, atol=1e-12)
+    # kvpt shrinks with the KV heads (PAPER.md:111 formula with d_h -> Hkv*D)
+    assert o.kvpt == 4 * L * Hkv * D

@@ -1,0 +1,5 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 2400 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 900 python bench.py --shape llama3-8b --requests 32768 --no-cpu-baseline --no-e2e --steps 100 > gpurun_out/bench_llama.log 2>&1; echo "rc=$?" >> gpurun_out/bench_llama.log
+timeout 900 python bench.py --no-cpu-baseline --no-e2e > gpurun_out/bench_c1.log 2>&1
