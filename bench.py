@@ -54,7 +54,9 @@ def parse():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--shape", default="gptj", choices=sorted(SHAPES))
     ap.add_argument("--arena-gb", type=float, default=0.0, help="cap the arena (e.g. for ncu replay)")
-    ap.add_argument("--attn", default="tma", choices=["tma", "regs"], help="attention kernel variant")
+    ap.add_argument("--attn", default="tma", choices=["tma", "regs", "tc"],
+                    help="attention kernel: tma (TMA ring, default), regs (register streaming), "
+                         "tc (tcgen05 tensor cores, grouped KV with D = 128)")
     ap.add_argument("--compact-policy", default="every", choices=["every", "on-demand"],
                     help="row shift every step (the paper) or only when the pool could use the rows (R27)")
     ap.add_argument("--model", default="none", choices=["none", "gptj"],
@@ -253,7 +255,8 @@ def run_s3(args):
     eng = S3Engine(L, H, D, GPTJ["max_len"], R, max_running, device=local, rank=rank, world=world,
                    num_kv_heads=0 if Hkv == H else Hkv,
                    seed=args.seed, staging_bytes=staging, host_store_bytes=(16 << 30) if p > 0 else (1 << 30),
-                   attn_variant=0 if args.attn == "tma" else 1, compact_mode=0 if args.compact == "fused" else 1,
+                   attn_variant={"tma": 0, "regs": 1, "tc": 2}[args.attn],
+                   compact_mode=0 if args.compact == "fused" else 1,
                    compact_policy=0 if args.compact_policy == "every" else 1)
 
     exchange = None
@@ -387,8 +390,9 @@ def run_s3(args):
                 "l2": "working set (tens of GB per step) >> 126 MB L2; no flush needed",
             },
             "roofline": {
-                "bound": "hbm", "kernel": ("k_attn_tma" if args.attn == "tma" else "k_attn") + "+k_combine (decode attention"
-                          + (" fused with the row shift)" if args.compact == "fused" else ")"),
+                "bound": "hbm", "kernel": {"tma": "k_attn_tma", "regs": "k_attn", "tc": "k_attn_tc (tcgen05)"}[args.attn]
+                          + "+k_combine (decode attention"
+                          + (" fused with the row shift)" if args.compact == "fused" and args.attn == "tma" else ")"),
                 "achieved": attn_gbs, "peak": peak, "unit": "GB/s", "frac": attn_gbs / peak,
                 "peak_source": peak_kind,
                 "traffic": tr.get("dram_bytes_per_launch") if tr else None,

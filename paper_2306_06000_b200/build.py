@@ -10,7 +10,8 @@ CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libs3.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
-SOURCES = [os.path.join(CSRC, "s3_kernels.cu"), os.path.join(CSRC, "s3_host.cpp")]
+SOURCES = [os.path.join(CSRC, "s3_kernels.cu"), os.path.join(CSRC, "s3_attn_tc.cu"),
+           os.path.join(CSRC, "s3_host.cpp")]
 DEPS = SOURCES + [os.path.join(CSRC, "s3_internal.h"), os.path.join(INCLUDE, "s3.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -1,0 +1,504 @@
+// s3_attn_tc.cu -- grouped-query / multi-query decode attention on the 5th-gen
+// tensor cores (tcgen05 + TMEM + TMA).  attn_variant 2; D = 128, 2 <= G <= 16
+// query heads per KV head.
+//
+// With grouped KV the G query heads that share KV head g turn the decode
+// GEMV into a real contraction per 128-row tile of that head's rows:
+//     S^T [128 x 16]  = K_tile [128 x D] . Q_g^T [D x 16]      (A K-major, B K-major)
+//     O^T [D x 16]   += V_tile^T [D x 128] . P^T [128 x 16]    (A MN-major, B K-major)
+// (16 = G padded to the MMA N granularity).  Per CTA (persistent, one per
+// SM) four roles:
+//   producer warp : items (unit, layer, KV head) from the atomic queue; TMA
+//                   tensor loads (128B swizzle) of the tile's K and V rows in
+//                   16-row boxes (only the groups holding valid rows) and of
+//                   the group's q rows, into a 3-stage ring;
+//   MMA warp      : one thread issues tcgen05.mma (kind::f16, M 128, N 16,
+//                   K 16 per instruction), commits to mbarriers;
+//   softmax warps : 4 warps = 128 TMEM lanes; lane j holds row j of S^T:
+//                   mask rows >= nvalid, column max / sum across the 128
+//                   lanes, online softmax in the log2 domain, P (bf16,
+//                   swizzled) to shared memory, zero V rows >= nvalid (NaN
+//                   safety), rescale O^T in TMEM; after the last tile of an
+//                   item lane d holds O^T[d][:] and writes out / the split-K
+//                   partial (same records as k_combine reads).
+// The new token's K/V row is appended to the arena by k_append before this
+// kernel, so every tile reads rows straight from the arena.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "s3_internal.h"
+
+namespace s3 {
+namespace {
+
+constexpr int TM = 128;                     // rows per tile (MMA M)
+constexpr int NQ = 16;                      // query columns per KV head (MMA N)
+constexpr int DH = 128;                     // head dim
+constexpr int NST = 3;                      // K/V ring stages
+constexpr int KV_BYTES = TM * DH * 2;       // 32 KB: two 64-column blocks of [128 rows x 128 B]
+constexpr int Q_BYTES = NQ * DH * 2;        // 4 KB:  two blocks of [16 rows x 128 B]
+constexpr int STAGE_BYTES = 2 * KV_BYTES + Q_BYTES;   // 68 KB (multiple of 1024)
+constexpr int P_BYTES = NQ * TM * 2;        // 4 KB:  two blocks (j 0-63, 64-127) of [16 rows x 128 B]
+constexpr int PBUF_BYTES = 2 * P_BYTES;     // P as bf16 hi + lo parts (P = hi + lo to ~16 bits)
+constexpr float LAZY_THR = 8.0f;            // rescale only if a score beats the running max by 2^8
+constexpr int TMEM_COLS = 64;               // S0 [0,16), S1 [16,32), O [32,48)
+
+struct TcHdr {
+  int32_t item, r0, nvalid, flags;          // flags: 1 = first tile of the item, 2 = last
+  int32_t b, part, li, g;
+};
+
+struct TcSmem {                             // after the ring and the two P buffers
+  uint64_t kv_full[NST], kv_empty[NST], s_full[2], s_empty[2], p_full, o_done;
+  TcHdr hdr[NST];
+  float red[2][4][NQ];
+  int32_t flag[4];
+  uint32_t tmem_base;
+};
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mb_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void mb_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void mb_expect(uint64_t* b, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\nW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W_%=;\n}\n" ::"r"(
+          su32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+          "r"(su32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(su32(bar))
+      : "memory");
+}
+// UMMA shared-memory descriptor: 128B swizzle, version 1 (sm_100)
+__device__ __forceinline__ uint64_t sdesc(const void* p, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((su32(p) >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// instruction descriptor: bf16 x bf16 -> f32, M 128, N 16
+__host__ __device__ constexpr uint32_t idesc(int a_mn_major) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn_major << 15) | ((uint32_t)(NQ >> 3) << 17) |
+         ((uint32_t)(TM >> 4) << 24);
+}
+__device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(id), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.b64 [%0];" ::"l"((uint64_t)su32(b)) : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t addr, float (&v)[NQ]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(addr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_st16(uint32_t addr, const float (&v)[NQ]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          addr),
+      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+      "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+      "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])),
+      "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
+      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
+      "r"(__float_as_uint(v[15]))
+      : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ float ex2f(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void softmax_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+// column-wise reduction over the 128 softmax lanes (max or sum)
+template <bool MAX>
+__device__ __forceinline__ void col_reduce(float (&v)[NQ], float (&red)[4][NQ], int wq, int lane) {
+#pragma unroll
+  for (int c = 0; c < NQ; ++c) {
+    float x = v[c];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float y = __shfl_xor_sync(0xffffffffu, x, o);
+      x = MAX ? fmaxf(x, y) : x + y;
+    }
+    v[c] = x;
+  }
+  if (lane == 0)
+#pragma unroll
+    for (int c = 0; c < NQ; ++c) red[wq][c] = v[c];
+  softmax_bar();
+#pragma unroll
+  for (int c = 0; c < NQ; ++c)
+    v[c] = MAX ? fmaxf(fmaxf(red[0][c], red[1][c]), fmaxf(red[2][c], red[3][c]))
+               : (red[0][c] + red[1][c]) + (red[2][c] + red[3][c]);
+  softmax_bar();
+}
+
+struct TcArgs {
+  int32_t H, Hkv, G, B, l0, nl;
+  float qscale;
+  float* out;
+  float* partials;
+  const Unit* units;
+  int32_t* ctrl;
+};
+
+__global__ void __launch_bounds__(192, 1) k_attn_tc(const __grid_constant__ CUtensorMap map_kv,
+                                                    const __grid_constant__ CUtensorMap map_q, TcArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* pbuf = smem + NST * STAGE_BYTES;
+  TcSmem& S = *reinterpret_cast<TcSmem*>(pbuf + 2 * PBUF_BYTES);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) {
+    for (int i = 0; i < NST; ++i) { mb_init(&S.kv_full[i], 1); mb_init(&S.kv_empty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mb_init(&S.s_full[i], 1); mb_init(&S.s_empty[i], 4); }
+    mb_init(&S.p_full, 4);
+    mb_init(&S.o_done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&S.tmem_base)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = S.tmem_base;
+  const int total = a.ctrl[CTRL_N_UNITS] * a.nl * a.Hkv;
+  const int row_cols = 2 * a.Hkv * DH;      // elements of one layer inside a token row
+
+  if (warp == 0) {
+    // ------------------------------ producer ------------------------------
+    if (lane == 0) {
+      int t = 0;
+      for (;;) {
+        const int item = atomicAdd(&a.ctrl[CTRL_ITEM], 1);
+        if (item >= total) {
+          const int st = t % NST;
+          mb_wait(&S.kv_empty[st], ((uint32_t)(t / NST) & 1u) ^ 1u);
+          S.hdr[st].item = -1;
+          mb_arrive(&S.kv_full[st]);
+          break;
+        }
+        const int g = item % a.Hkv;
+        const int rest = item / a.Hkv;
+        const int li = rest % a.nl, u = rest / a.nl;
+        const Unit un = a.units[u];
+        const int nrows = (un.r1 - un.r0) + (un.has_new ? 1 : 0);   // new row already in the arena
+        const int colk = (a.l0 + li) * row_cols + g * DH;
+        const int colv = colk + a.Hkv * DH;
+        const int qrow = (li * a.B + un.b) * a.H + g * a.G;
+        for (int r = 0; r < nrows; r += TM) {
+          const int st = t % NST;
+          mb_wait(&S.kv_empty[st], ((uint32_t)(t / NST) & 1u) ^ 1u);
+          const int nv = min(TM, nrows - r);
+          TcHdr& h = S.hdr[st];
+          h.item = item; h.r0 = un.r0 + r; h.nvalid = nv;
+          h.flags = (r == 0 ? 1 : 0) | (r + TM >= nrows ? 2 : 0);
+          h.b = un.b; h.part = un.part; h.li = li; h.g = g;
+          const int groups = (nv + 15) / 16;
+          uint8_t* sk = smem + st * STAGE_BYTES;
+          uint8_t* sv = sk + KV_BYTES;
+          uint8_t* sq = sv + KV_BYTES;
+          mb_expect(&S.kv_full[st], (uint32_t)(groups * 16 * 128 * 2 * 2 + Q_BYTES));
+          const int row0 = un.off + un.r0 + r;
+          for (int gr = 0; gr < groups; ++gr)
+#pragma unroll
+            for (int kb = 0; kb < 2; ++kb) {
+              tma2d(sk + kb * 16384 + gr * 2048, &map_kv, colk + kb * 64, row0 + gr * 16, &S.kv_full[st]);
+              tma2d(sv + kb * 16384 + gr * 2048, &map_kv, colv + kb * 64, row0 + gr * 16, &S.kv_full[st]);
+            }
+#pragma unroll
+          for (int kb = 0; kb < 2; ++kb) tma2d(sq + kb * 2048, &map_q, kb * 64, qrow, &S.kv_full[st]);
+          ++t;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // -------------------------------- MMA ---------------------------------
+    // One tile of lookahead: S^T(t+1) is issued before O^T(t), so the softmax
+    // of tile t overlaps the next tile's QK^T.  tcgen05.commit covers every
+    // earlier MMA, so s_full(t+2) still implies O^T(t) is done (P buffer t&1
+    // free) and o_done orders the rescale / epilogue reads of O^T.
+    if (lane == 0) {
+      constexpr uint32_t id_s = idesc(0), id_o = idesc(1);
+      auto issue_s = [&](int t) {
+        const int st = t % NST, sb = t & 1;
+        mb_wait(&S.s_empty[sb], ((uint32_t)(t >> 1) & 1u) ^ 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint8_t* sk = smem + st * STAGE_BYTES;
+        const uint8_t* sq = sk + 2 * KV_BYTES;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {            // S^T = K . Q^T over d in steps of 16
+          const int kb = k >> 2, ko = (k & 3) * 32;
+          mma(tmem + sb * 16, sdesc(sk + kb * 16384 + ko, 16, 1024), sdesc(sq + kb * 2048 + ko, 16, 1024), id_s,
+              k > 0);
+        }
+        commit(&S.s_full[sb]);
+      };
+      mb_wait(&S.kv_full[0], 0u);
+      if (S.hdr[0].item < 0) {
+        mb_arrive(&S.s_full[0]);
+      } else {
+        issue_s(0);
+        for (int t = 0;; ++t) {
+          const int st = t % NST, st1 = (t + 1) % NST;
+          mb_wait(&S.kv_full[st1], (uint32_t)((t + 1) / NST) & 1u);
+          const bool end = S.hdr[st1].item < 0;
+          if (!end) issue_s(t + 1);
+          const bool first = S.hdr[st].flags & 1;
+          mb_wait(&S.p_full, (uint32_t)t & 1u);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint8_t* sv = smem + st * STAGE_BYTES + KV_BYTES;
+          const uint8_t* sp = pbuf + (t & 1) * PBUF_BYTES;
+#pragma unroll
+          for (int part = 0; part < 2; ++part)     // O^T += V^T . (P_hi + P_lo)^T over rows in steps of 16
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const int kb = k >> 2, ko = (k & 3) * 32;
+              mma(tmem + 32, sdesc(sv + k * 2048, 16384, 1024),
+                  sdesc(sp + part * P_BYTES + kb * 2048 + ko, 16, 1024), id_o, (first && part == 0 && k == 0) ? 0u : 1u);
+            }
+          commit(&S.o_done);
+          commit(&S.kv_empty[st]);
+          if (end) { mb_arrive(&S.s_full[(t + 1) & 1]); break; }
+        }
+      }
+    }
+  } else {
+    // ------------------------------ softmax -------------------------------
+    // Lazy running max (log2 domain): the column max is reduced across the
+    // 128 lanes only on an item's first tile or when some score exceeds the
+    // running max by more than LAZY_THR; otherwise p = 2^(s - m) <= 2^8 and
+    // nothing is rescaled.  Each lane keeps its own row's partial sums; they
+    // are reduced once, in the epilogue.
+    const int wq = warp - 2;                          // 0..3
+    const int lq = warp & 3;                          // TMEM lane quarter this warp may access
+    const int row = lq * 32 + lane;                   // TMEM lane = tile row (S) = head-dim index (O)
+    const uint32_t lane_base = tmem + ((uint32_t)(lq * 32) << 16);
+    float m[NQ], lrow[NQ];
+#pragma unroll
+    for (int c = 0; c < NQ; ++c) { m[c] = -INFINITY; lrow[c] = 0.f; }
+    for (int t = 0;; ++t) {
+      const int sb = t & 1;
+      mb_wait(&S.s_full[sb], (uint32_t)(t >> 1) & 1u);
+      const TcHdr h = S.hdr[t % NST];
+      if (h.item < 0) break;
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      float s[NQ];
+      tmem_ld16(lane_base + sb * 16, s);
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mb_arrive(&S.s_empty[sb]);
+      const bool first = h.flags & 1;
+      const bool valid = row < h.nvalid;
+#pragma unroll
+      for (int c = 0; c < NQ; ++c) s[c] = valid ? s[c] * a.qscale : -INFINITY;
+      // does any score need a larger running max?
+      bool need = first;
+      if (!first) {
+        bool over = false;
+#pragma unroll
+        for (int c = 0; c < NQ; ++c) over |= s[c] > m[c] + LAZY_THR;
+        const bool wover = __any_sync(0xffffffffu, over);
+        if (lane == 0) S.flag[wq] = wover;
+        softmax_bar();
+        need = S.flag[0] | S.flag[1] | S.flag[2] | S.flag[3];
+        softmax_bar();
+      }
+      float corr[NQ];
+      bool rescale = false;
+      if (need) {
+        float mt[NQ];
+#pragma unroll
+        for (int c = 0; c < NQ; ++c) mt[c] = s[c];
+        col_reduce<true>(mt, S.red[0], wq, lane);
+#pragma unroll
+        for (int c = 0; c < NQ; ++c) {
+          const float mn = first ? mt[c] : fmaxf(m[c], mt[c]);
+          corr[c] = first ? 0.f : ex2f(m[c] - mn);
+          m[c] = mn;
+          lrow[c] = first ? 0.f : lrow[c] * corr[c];
+        }
+        rescale = !first;
+      }
+      // P = 2^(s - m) as bf16 hi + lo; row c (query column), column j = row; 128B swizzle
+      uint8_t* sp = pbuf + (t & 1) * PBUF_BYTES + (row >> 6) * 2048;
+      const uint32_t jj2 = (uint32_t)(row & 63) * 2u;
+#pragma unroll
+      for (int c = 0; c < NQ; ++c) {
+        const float pv = ex2f(s[c] - m[c]);
+        lrow[c] += pv;
+        const __nv_bfloat16 hi = __float2bfloat16_rn(pv);
+        const __nv_bfloat16 lo = __float2bfloat16_rn(pv - __bfloat162float(hi));
+        const uint32_t byte = (uint32_t)c * 128u + jj2;
+        const uint32_t sw = byte ^ ((uint32_t)(c & 7) << 4);
+        *reinterpret_cast<__nv_bfloat16*>(sp + sw) = hi;
+        *reinterpret_cast<__nv_bfloat16*>(sp + P_BYTES + sw) = lo;
+      }
+      if (!valid) {                                 // rows past the slot's resident rows: V := 0
+        uint8_t* sv = smem + (t % NST) * STAGE_BYTES + KV_BYTES;
+#pragma unroll
+        for (int kb = 0; kb < 2; ++kb)
+#pragma unroll
+          for (int ch = 0; ch < 8; ++ch)
+            *reinterpret_cast<uint4*>(sv + kb * 16384 + row * 128 + ch * 16) = make_uint4(0, 0, 0, 0);
+      }
+      if (rescale) {                                // O^T *= corr once the previous tile's MMA is done
+        mb_wait(&S.o_done, (uint32_t)(t - 1) & 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        float o[NQ];
+        tmem_ld16(lane_base + 32, o);
+#pragma unroll
+        for (int c = 0; c < NQ; ++c) o[c] *= corr[c];
+        tmem_st16(lane_base + 32, o);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mb_arrive(&S.p_full);
+      if (h.flags & 2) {                            // epilogue: lane = head-dim index d
+        float l[NQ];
+#pragma unroll
+        for (int c = 0; c < NQ; ++c) l[c] = lrow[c];
+        col_reduce<false>(l, S.red[1], wq, lane);
+        mb_wait(&S.o_done, (uint32_t)t & 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        float o[NQ];
+        tmem_ld16(lane_base + 32, o);
+        const int d = row;
+#pragma unroll
+        for (int c = 0; c < NQ; ++c) {
+          if (c >= a.G) break;
+          const int hq = h.g * a.G + c;
+          if (h.part < 0) {
+            a.out[((int64_t)(h.li * a.B + h.b) * a.H + hq) * DH + d] = o[c] / l[c];
+          } else {
+            float* pr = a.partials + (((int64_t)h.part * a.nl + h.li) * a.H + hq) * (DH + 4);
+            pr[d] = o[c];
+            if (d == 0) { pr[DH] = m[c]; pr[DH + 1] = l[c]; }
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+}
+
+// k_append: the new token's K/V row goes to row off+len before k_attn_tc reads it
+__global__ void __launch_bounds__(256) k_append(Shape sh, const DSlot* __restrict__ slots, int32_t B, int32_t l0,
+                                                int32_t nl, const uint16_t* __restrict__ k_new,
+                                                const uint16_t* __restrict__ v_new, uint16_t* __restrict__ arena) {
+  const int D8 = sh.D / 8;
+  const int64_t total = (int64_t)nl * B * sh.Hkv * D8;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t r = i;
+    const int d8 = (int)(r % D8); r /= D8;
+    const int g = (int)(r % sh.Hkv); r /= sh.Hkv;
+    const int b = (int)(r % B);
+    const int li = (int)(r / B);
+    const DSlot s = slots[b];
+    uint16_t* dst = arena + ((int64_t)s.off + s.len) * sh.row_elems + ((int64_t)(l0 + li) * 2 * sh.Hkv + g) * sh.D + d8 * 8;
+    const uint4 kk = *reinterpret_cast<const uint4*>(k_new + i * 8);
+    const uint4 vv = *reinterpret_cast<const uint4*>(v_new + i * 8);
+    *reinterpret_cast<uint4*>(dst) = kk;
+    *reinterpret_cast<uint4*>(dst + (int64_t)sh.Hkv * sh.D) = vv;
+  }
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encoder() {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeTiledFn)p;
+  }
+  return fn;
+}
+
+// 2-D bf16 map: `cols` elements per row, `rows` rows, `pitch` bytes; boxes of 64 x 16, 128B swizzle
+bool encode_2d(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint64_t pitch) {
+  EncodeTiledFn enc = encoder();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {pitch};
+  cuuint32_t box[2] = {64, 16};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+int attn_tc_smem() { return NST * STAGE_BYTES + 2 * PBUF_BYTES + (int)sizeof(TcSmem) + 1024; }
+const void* attn_tc_kernel_ptr() { return (const void*)k_attn_tc; }
+
+bool attn_tc_supported(const Shape& sh) {
+  const int G = sh.Hkv > 0 ? sh.H / sh.Hkv : 0;
+  return sh.D == DH && G >= 2 && G <= NQ && sh.H % sh.Hkv == 0 && encoder() != nullptr;
+}
+
+cudaError_t launch_append(const Shape& sh, const DSlot* slots, int32_t B, int32_t l0, int32_t nl,
+                          const uint16_t* k_new, const uint16_t* v_new, uint16_t* arena, cudaStream_t st) {
+  const int64_t tot = (int64_t)nl * B * sh.Hkv * (sh.D / 8);
+  const int blocks = (int)std::min<int64_t>((tot + 255) / 256, 148 * 8);
+  k_append<<<blocks, 256, 0, st>>>(sh, slots, B, l0, nl, k_new, v_new, arena);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_attn_tc(const Shape& sh, const uint16_t* q, uint16_t* arena, int64_t arena_rows, float* out,
+                           float* partials, const Unit* units, const Split* splits, int32_t* ctrl, int32_t B,
+                           int32_t l0, int32_t nl, int32_t grid_attn, int32_t grid_combine, cudaStream_t st) {
+  CUtensorMap map_kv, map_q;
+  if (!encode_2d(&map_kv, arena, (uint64_t)sh.row_elems, (uint64_t)arena_rows, (uint64_t)sh.kvpt))
+    return cudaErrorInvalidValue;
+  if (!encode_2d(&map_q, q, (uint64_t)sh.D, (uint64_t)nl * B * sh.H, (uint64_t)sh.D * 2)) return cudaErrorInvalidValue;
+  TcArgs a;
+  a.H = sh.H; a.Hkv = sh.Hkv; a.G = sh.H / sh.Hkv; a.B = B; a.l0 = l0; a.nl = nl;
+  a.qscale = 1.4426950408889634f / sqrtf((float)sh.D);
+  a.out = out; a.partials = partials; a.units = units; a.ctrl = ctrl;
+  k_attn_tc<<<grid_attn, 192, attn_tc_smem(), st>>>(map_kv, map_q, a);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return launch_combine(sh, splits, partials, out, ctrl, B, nl, grid_combine, st);
+}
+
+}  // namespace s3

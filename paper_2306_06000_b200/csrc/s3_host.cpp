@@ -172,7 +172,7 @@ bool validate(const s3_config* c) {
   if (c->chunk_rows < 0 || c->move_chunk_bytes < 0 || c->move_chunk_bytes % 16) return false;
   if (c->move_chunk_bytes > 0 && (c->move_chunk_bytes < 1024 || c->move_chunk_bytes > 36864)) return false;
   if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return false;
-  if (c->attn_variant < 0 || c->attn_variant > 1) return false;
+  if (c->attn_variant < 0 || c->attn_variant > 2) return false;
   if (c->compact_mode < 0 || c->compact_mode > 1) return false;
   if (c->compact_policy < 0 || c->compact_policy > 1) return false;
   return true;
@@ -409,6 +409,13 @@ s3_status s3_kv_init(const s3_config* cfg, const s3_buffers* b, s3_ctx** out) {
   if (!ka) return bail("head_dim");
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ka, attn_block_threads(sh), 0);
   ctx->grid_attn = ctx->num_sms * std::max(1, occ);
+  if (cfg->attn_variant == 2) {
+    if (!attn_tc_supported(sh)) return bail("attn_variant 2 needs head_dim 128 and 2..16 query heads per KV head");
+    if (cudaFuncSetAttribute(attn_tc_kernel_ptr(), cudaFuncAttributeMaxDynamicSharedMemorySize, attn_tc_smem()) !=
+        cudaSuccess)
+      return bail("attn_tc smem attribute");
+    ctx->grid_attn = ctx->num_sms;
+  }
   if (cfg->attn_variant == 0 && attn_tma_stages(sh) >= 2) {
     const int smem = attn_tma_smem(sh, attn_tma_stages(sh));
     if (cudaFuncSetAttribute(attn_tma_kernel_ptr(sh), cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
@@ -506,6 +513,11 @@ s3_status s3_decode_step(s3_ctx* ctx, int32_t l0, int32_t nl, const void* q, con
     if (!q || !k_new || !v_new || !out || (finalize && !eos)) return fail(ctx, S3_E_INVAL, "decode_step: null");
     if (fuse && ctx->last_stage_d2h)   // staging is rewritten: the previous step's D2H from it must be done
       CK(cudaStreamWaitEvent(ctx->st, ctx->last_stage_d2h->ev, 0), "wait staging");
+    if (ctx->cfg.attn_variant == 2) {   // the tensor-core kernel reads the new row from the arena
+      CK(launch_append(ctx->sh, ctx->slots[ctx->cur], B, l0, nl, (const uint16_t*)k_new, (const uint16_t*)v_new,
+                       (uint16_t*)ctx->buf.arena, ctx->st), "k_append");
+      ctx->launches += 1;
+    }
     PrepArgs pa;
     pa.sh = ctx->sh; pa.slots = ctx->slots[ctx->cur]; pa.next = ctx->slots[1 - ctx->cur]; pa.B = B; pa.C = ctx->C;
     pa.eos = eos; pa.finalize = finalize ? 1 : 0; pa.fuse = fuse ? 1 : 0;
@@ -529,10 +541,15 @@ s3_status s3_decode_step(s3_ctx* ctx, int32_t l0, int32_t nl, const void* q, con
     ctx->attn_epoch++;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx->prof.on) { e0 = ctx->prof.get(); e1 = ctx->prof.get(); cudaEventRecord(e0, ctx->st); }
-    CK(launch_attn(ctx->sh, (const uint16_t*)q, (const uint16_t*)k_new, (const uint16_t*)v_new,
-                   (uint16_t*)ctx->buf.arena, (uint8_t*)ctx->buf.staging, out, ctx->partials, ctx->units, ctx->splits,
-                   ctx->desc, ctx->progress, ctx->attn_epoch, ctx->ctrl, B, l0, nl, ctx->grid_attn,
-                   ctx->grid_combine, ctx->cfg.attn_variant, ctx->st), "k_attn");
+    if (ctx->cfg.attn_variant == 2)
+      CK(launch_attn_tc(ctx->sh, (const uint16_t*)q, (uint16_t*)ctx->buf.arena, ctx->cfg.arena_rows, out,
+                        ctx->partials, ctx->units, ctx->splits, ctx->ctrl, B, l0, nl, ctx->grid_attn,
+                        ctx->grid_combine, ctx->st), "k_attn_tc");
+    else
+      CK(launch_attn(ctx->sh, (const uint16_t*)q, (const uint16_t*)k_new, (const uint16_t*)v_new,
+                     (uint16_t*)ctx->buf.arena, (uint8_t*)ctx->buf.staging, out, ctx->partials, ctx->units,
+                     ctx->splits, ctx->desc, ctx->progress, ctx->attn_epoch, ctx->ctrl, B, l0, nl, ctx->grid_attn,
+                     ctx->grid_combine, ctx->cfg.attn_variant, ctx->st), "k_attn");
     ctx->launches += 2;   // attention, combine
     if (ctx->prof.on) {
       cudaEventRecord(e1, ctx->st);

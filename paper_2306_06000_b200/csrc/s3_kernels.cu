@@ -1353,6 +1353,17 @@ cudaError_t launch_attn(const Shape& sh, const uint16_t* q, const uint16_t* k_ne
   return cudaGetLastError();
 }
 
+cudaError_t launch_combine(const Shape& sh, const Split* splits, float* partials, float* out, int32_t* ctrl,
+                           int32_t B, int32_t nl, int32_t grid, cudaStream_t st) {
+  switch (sh.D) {
+    case 64: k_combine<64><<<grid, 256, 0, st>>>(splits, partials, out, ctrl, sh.H, B, nl); break;
+    case 128: k_combine<128><<<grid, 256, 0, st>>>(splits, partials, out, ctrl, sh.H, B, nl); break;
+    case 256: k_combine<256><<<grid, 256, 0, st>>>(splits, partials, out, ctrl, sh.H, B, nl); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
 cudaError_t launch_keep_scan(const Shape& sh, const DSlot* cur, DSlot* next, int32_t B, int64_t S,
                              void* report, MoveEntry* entries, int32_t* key_chunk0, int32_t* key_src,
                              int64_t* ctrl64, int32_t compact_policy, int32_t pool_nonempty, cudaStream_t st) {

@@ -403,3 +403,13 @@ def test_grouped_query_kv(H, Hkv, D, variant, mode):
     t = s3synth.make_trace(40, seed=51, policy="short", p=0.3, max_seq_len=128, prompt_max=24)
     r = lockstep(t, 2, H, D, 800, C=8, S=2048, attn_variant=variant, compact_mode=mode, Hkv=Hkv, poison=True)
     assert r["evictions"] > 0
+
+
+@pytest.mark.parametrize("H,Hkv,C,policy", [(8, 2, 512, "short"), (32, 8, 48, "short"), (16, 1, 128, "bucket"),
+                                            (4, 2, 7, "short")])
+def test_grouped_query_kv_tensor_cores(H, Hkv, C, policy):
+    """attn_variant 2: tcgen05/TMEM/TMA kernel for grouped KV (D = 128); C
+    small -> split-K units and tile tails; NaN-poisoned slack rows."""
+    t = s3synth.make_trace(40, seed=53, policy=policy, p=0.3, max_seq_len=320, prompt_max=200)
+    r = lockstep(t, 2, H, 128, 1600, C=C, S=2048, attn_variant=2, Hkv=Hkv, poison=True)
+    print("worst", r["worst"])

@@ -18,13 +18,16 @@ sys.path.insert(0, ROOT)
 
 from paper_2306_06000_b200.engine import S3Engine  # noqa: E402
 
-CASES = [  # (name, L, H, Hkv, D, B, P)
+CASES = [  # (name, L, H, Hkv, D, B, P, attn_variant)
     ("gptj long", 28, 16, 16, 256, 64, 1900),
     ("gptj mid", 28, 16, 16, 256, 1024, 200),
     ("gptj short", 28, 16, 16, 256, 4096, 24),
     ("gptj B=8", 28, 16, 16, 256, 8, 1900),
     ("llama3-8b gqa", 32, 32, 8, 128, 2048, 400),
     ("mqa H=16 D=128", 32, 16, 1, 128, 2048, 400),
+    ("llama3-8b gqa tc", 32, 32, 8, 128, 2048, 400, 2),
+    ("llama3-8b gqa tc short", 32, 32, 8, 128, 8192, 40, 2),
+    ("mqa H=16 D=128 tc", 32, 16, 1, 128, 2048, 400, 2),
 ]
 
 
@@ -34,13 +37,15 @@ def main():
     args = ap.parse_args()
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
-    for name, L, H, Hkv, D, B, P in CASES:
+    for case in CASES:
+        name, L, H, Hkv, D, B, P = case[:7]
+        variant = case[7] if len(case) > 7 else 0
         kvpt = 4 * L * Hkv * D
         R = max(2048, B * (P + args.steps + 8))
         if R * kvpt > 150e9:
             continue
         eng = S3Engine(L, H, D, 2048, R, max(B, 16), num_kv_heads=0 if Hkv == H else Hkv,
-                       host_store_bytes=64 << 20)
+                       host_store_bytes=64 << 20, attn_variant=variant)
         n = B
         eng.submit(np.arange(n), np.full(n, P), np.full(n, args.steps + 8), np.full(n, 10_000))
         eng.admit()

@@ -1,0 +1,4 @@
+cd $GRAFT_REPO_ROOT
+mkdir -p gpurun_out
+timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -s -k "tensor_cores" > gpurun_out/pytest_tc.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_tc.log
+timeout 900 python tools/attn_sweep.py > gpurun_out/attn_sweep.log 2>&1; echo "rc=$?" >> gpurun_out/attn_sweep.log
