@@ -45,15 +45,16 @@ constexpr int STAGE_BYTES = 2 * KV_BYTES + Q_BYTES;   // 68 KB (multiple of 1024
 constexpr int P_BYTES = NQ * TM * 2;        // 4 KB:  two blocks (j 0-63, 64-127) of [16 rows x 128 B]
 constexpr int PBUF_BYTES = 2 * P_BYTES;     // P as bf16 hi + lo parts (P = hi + lo to ~16 bits)
 constexpr float LAZY_THR = 8.0f;            // rescale only if a score beats the running max by 2^8
-constexpr int TMEM_COLS = 64;               // S0 [0,16), S1 [16,32), O [32,48)
+constexpr int TMEM_COLS = 64;               // S0 [0,16), S1 [16,32), O0 [32,48), O1 [48,64)
 
 struct TcHdr {
   int32_t item, r0, nvalid, flags;          // flags: 1 = first tile of the item, 2 = last
   int32_t b, part, li, g;
+  int32_t iseq, pad[3];                     // per-CTA item sequence number: O buffer = iseq & 1
 };
 
 struct TcSmem {                             // after the ring and the two P buffers
-  uint64_t kv_full[NST], kv_empty[NST], s_full[2], s_empty[2], p_full, o_done;
+  uint64_t kv_full[NST], kv_empty[NST], s_full[2], s_empty[2], p_full, o_done, o_fin[2], o_free[2];
   TcHdr hdr[NST];
   float red[2][4][NQ];
   int32_t flag[4];
@@ -114,6 +115,23 @@ __device__ __forceinline__ void tmem_ld16(uint32_t addr, float (&v)[NQ]) {
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
+__device__ __forceinline__ void tmem_ld8(uint32_t addr, float (&v)[8]) {
+  uint32_t r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(addr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_st8(uint32_t addr, const float (&v)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(addr),
+               "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
+               "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
+               "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7]))
+               : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void tmem_st16(uint32_t addr, const float (&v)[NQ]) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
@@ -127,6 +145,14 @@ __device__ __forceinline__ void tmem_st16(uint32_t addr, const float (&v)[NQ]) {
       : "memory");
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
+template <int NC>
+__device__ __forceinline__ void tmem_ld(uint32_t addr, float (&v)[NC]) {
+  if constexpr (NC == 16) tmem_ld16(addr, v); else tmem_ld8(addr, v);
+}
+template <int NC>
+__device__ __forceinline__ void tmem_st(uint32_t addr, const float (&v)[NC]) {
+  if constexpr (NC == 16) tmem_st16(addr, v); else tmem_st8(addr, v);
+}
 __device__ __forceinline__ float ex2f(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -134,27 +160,65 @@ __device__ __forceinline__ float ex2f(float x) {
 }
 __device__ __forceinline__ void softmax_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
-// column-wise reduction over the 128 softmax lanes (max or sum)
+// Column-wise reduction of 16 values per lane over the 128 softmax lanes.
+// Within a warp a transposed butterfly halves the vector at each step (8 + 4
+// + 2 + 1 + 1 shuffles); lane l ends with column 8*b4 + 4*b3 + 2*b2 + b1 of
+// its bits.  Warp partials meet in shared memory; every lane gets all 16.
 template <bool MAX>
-__device__ __forceinline__ void col_reduce(float (&v)[NQ], float (&red)[4][NQ], int wq, int lane) {
+__device__ __forceinline__ float rop(float x, float y) { return MAX ? fmaxf(x, y) : x + y; }
+
+template <bool MAX, int NC>
+__device__ __forceinline__ void col_reduce(float (&v)[NC], float (&red)[4][NQ], int wq, int lane) {
+  // NC = 16: 8 + 4 + 2 + 1 + 1 shuffles; NC = 8: 4 + 2 + 1 + 1 + 1
+  float a8[8], a4[4], a2[2], a1;
+  const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4, h2 = lane & 2;
+  int col;
+  if constexpr (NC == 16) {
 #pragma unroll
-  for (int c = 0; c < NQ; ++c) {
-    float x = v[c];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      const float y = __shfl_xor_sync(0xffffffffu, x, o);
-      x = MAX ? fmaxf(x, y) : x + y;
+    for (int i = 0; i < 8; ++i) {
+      const float send = h16 ? v[i] : v[8 + i];
+      const float keep = h16 ? v[8 + i] : v[i];
+      a8[i] = rop<MAX>(keep, __shfl_xor_sync(0xffffffffu, send, 16));
     }
-    v[c] = x;
-  }
-  if (lane == 0)
+  } else {
 #pragma unroll
-    for (int c = 0; c < NQ; ++c) red[wq][c] = v[c];
+    for (int i = 0; i < 8; ++i) a8[i] = v[i];
+  }
+  const int o8 = NC == 16 ? 8 : 16;               // NC = 8: the first split uses lane bit 4
+  const bool b8 = NC == 16 ? h8 : h16;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float send = b8 ? a8[i] : a8[4 + i];
+    const float keep = b8 ? a8[4 + i] : a8[i];
+    a4[i] = rop<MAX>(keep, __shfl_xor_sync(0xffffffffu, send, o8));
+  }
+  const int o4 = NC == 16 ? 4 : 8;
+  const bool b4 = NC == 16 ? h4 : h8;
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const float send = b4 ? a4[i] : a4[2 + i];
+    const float keep = b4 ? a4[2 + i] : a4[i];
+    a2[i] = rop<MAX>(keep, __shfl_xor_sync(0xffffffffu, send, o4));
+  }
+  const int o2 = NC == 16 ? 2 : 4;
+  const bool b2 = NC == 16 ? h2 : h4;
+  {
+    const float send = b2 ? a2[0] : a2[1];
+    const float keep = b2 ? a2[1] : a2[0];
+    a1 = rop<MAX>(keep, __shfl_xor_sync(0xffffffffu, send, o2));
+  }
+  if constexpr (NC == 16) {
+    a1 = rop<MAX>(a1, __shfl_xor_sync(0xffffffffu, a1, 1));
+    col = (h16 ? 8 : 0) + (h8 ? 4 : 0) + (h4 ? 2 : 0) + (h2 ? 1 : 0);
+  } else {
+    a1 = rop<MAX>(a1, __shfl_xor_sync(0xffffffffu, a1, 2));
+    a1 = rop<MAX>(a1, __shfl_xor_sync(0xffffffffu, a1, 1));
+    col = (h16 ? 4 : 0) + (h8 ? 2 : 0) + (h4 ? 1 : 0);
+  }
+  if (!(lane & (NC == 16 ? 1 : 3))) red[wq][col] = a1;
   softmax_bar();
 #pragma unroll
-  for (int c = 0; c < NQ; ++c)
-    v[c] = MAX ? fmaxf(fmaxf(red[0][c], red[1][c]), fmaxf(red[2][c], red[3][c]))
-               : (red[0][c] + red[1][c]) + (red[2][c] + red[3][c]);
+  for (int c = 0; c < NC; ++c) v[c] = rop<MAX>(rop<MAX>(red[0][c], red[1][c]), rop<MAX>(red[2][c], red[3][c]));
   softmax_bar();
 }
 
@@ -167,6 +231,7 @@ struct TcArgs {
   int32_t* ctrl;
 };
 
+template <int NC>   // query columns the softmax handles: G padded to 8 or 16 (the MMA always has N = 16)
 __global__ void __launch_bounds__(192, 1) k_attn_tc(const __grid_constant__ CUtensorMap map_kv,
                                                     const __grid_constant__ CUtensorMap map_q, TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -179,8 +244,14 @@ __global__ void __launch_bounds__(192, 1) k_attn_tc(const __grid_constant__ CUte
     for (int i = 0; i < 2; ++i) { mb_init(&S.s_full[i], 1); mb_init(&S.s_empty[i], 4); }
     mb_init(&S.p_full, 4);
     mb_init(&S.o_done, 1);
+    for (int i = 0; i < 2; ++i) { mb_init(&S.o_fin[i], 1); mb_init(&S.o_free[i], 4); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  // V buffers start at zero: rows a tile does not load keep finite (zero or earlier valid) data
+  for (int st = 0; st < NST; ++st)
+    for (int i = tid; i < KV_BYTES / 16; i += blockDim.x)
+      reinterpret_cast<uint4*>(smem + st * STAGE_BYTES + KV_BYTES)[i] = make_uint4(0, 0, 0, 0);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&S.tmem_base)),
                  "r"(TMEM_COLS));
@@ -190,53 +261,56 @@ __global__ void __launch_bounds__(192, 1) k_attn_tc(const __grid_constant__ CUte
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = S.tmem_base;
-  const int total = a.ctrl[CTRL_N_UNITS] * a.nl * a.Hkv;
   const int row_cols = 2 * a.Hkv * DH;      // elements of one layer inside a token row
 
   if (warp == 0) {
     // ------------------------------ producer ------------------------------
+    // One atomic per (unit, layer) covers its H_kv items (item = (u*nl + li)*H_kv + g),
+    // so the queue and unit-record latencies are paid once per H_kv tiles.
     if (lane == 0) {
-      int t = 0;
+      int t = 0, iseq = 0;
+      const int groups_total = a.ctrl[CTRL_N_UNITS] * a.nl;
       for (;;) {
-        const int item = atomicAdd(&a.ctrl[CTRL_ITEM], 1);
-        if (item >= total) {
+        const int w = atomicAdd(&a.ctrl[CTRL_ITEM], 1);
+        if (w >= groups_total) {
           const int st = t % NST;
           mb_wait(&S.kv_empty[st], ((uint32_t)(t / NST) & 1u) ^ 1u);
           S.hdr[st].item = -1;
           mb_arrive(&S.kv_full[st]);
           break;
         }
-        const int g = item % a.Hkv;
-        const int rest = item / a.Hkv;
-        const int li = rest % a.nl, u = rest / a.nl;
+        const int li = w % a.nl, u = w / a.nl;
         const Unit un = a.units[u];
         const int nrows = (un.r1 - un.r0) + (un.has_new ? 1 : 0);   // new row already in the arena
-        const int colk = (a.l0 + li) * row_cols + g * DH;
-        const int colv = colk + a.Hkv * DH;
-        const int qrow = (li * a.B + un.b) * a.H + g * a.G;
-        for (int r = 0; r < nrows; r += TM) {
-          const int st = t % NST;
-          mb_wait(&S.kv_empty[st], ((uint32_t)(t / NST) & 1u) ^ 1u);
-          const int nv = min(TM, nrows - r);
-          TcHdr& h = S.hdr[st];
-          h.item = item; h.r0 = un.r0 + r; h.nvalid = nv;
-          h.flags = (r == 0 ? 1 : 0) | (r + TM >= nrows ? 2 : 0);
-          h.b = un.b; h.part = un.part; h.li = li; h.g = g;
-          const int groups = (nv + 15) / 16;
-          uint8_t* sk = smem + st * STAGE_BYTES;
-          uint8_t* sv = sk + KV_BYTES;
-          uint8_t* sq = sv + KV_BYTES;
-          mb_expect(&S.kv_full[st], (uint32_t)(groups * 16 * 128 * 2 * 2 + Q_BYTES));
-          const int row0 = un.off + un.r0 + r;
-          for (int gr = 0; gr < groups; ++gr)
+        for (int g = 0; g < a.Hkv; ++g, ++iseq) {
+          const int item = w * a.Hkv + g;
+          const int colk = (a.l0 + li) * row_cols + g * DH;
+          const int colv = colk + a.Hkv * DH;
+          const int qrow = (li * a.B + un.b) * a.H + g * a.G;
+          for (int r = 0; r < nrows; r += TM) {
+            const int st = t % NST;
+            mb_wait(&S.kv_empty[st], ((uint32_t)(t / NST) & 1u) ^ 1u);
+            const int nv = min(TM, nrows - r);
+            TcHdr& h = S.hdr[st];
+            h.item = item; h.r0 = un.r0 + r; h.nvalid = nv;
+            h.flags = (r == 0 ? 1 : 0) | (r + TM >= nrows ? 2 : 0);
+            h.b = un.b; h.part = un.part; h.li = li; h.g = g; h.iseq = iseq;
+            const int groups = (nv + 15) / 16;
+            uint8_t* sk = smem + st * STAGE_BYTES;
+            uint8_t* sv = sk + KV_BYTES;
+            uint8_t* sq = sv + KV_BYTES;
+            mb_expect(&S.kv_full[st], (uint32_t)(groups * 16 * 128 * 2 * 2 + Q_BYTES));
+            const int row0 = un.off + un.r0 + r;
+            for (int gr = 0; gr < groups; ++gr)
 #pragma unroll
-            for (int kb = 0; kb < 2; ++kb) {
-              tma2d(sk + kb * 16384 + gr * 2048, &map_kv, colk + kb * 64, row0 + gr * 16, &S.kv_full[st]);
-              tma2d(sv + kb * 16384 + gr * 2048, &map_kv, colv + kb * 64, row0 + gr * 16, &S.kv_full[st]);
-            }
+              for (int kb = 0; kb < 2; ++kb) {
+                tma2d(sk + kb * 16384 + gr * 2048, &map_kv, colk + kb * 64, row0 + gr * 16, &S.kv_full[st]);
+                tma2d(sv + kb * 16384 + gr * 2048, &map_kv, colv + kb * 64, row0 + gr * 16, &S.kv_full[st]);
+              }
 #pragma unroll
-          for (int kb = 0; kb < 2; ++kb) tma2d(sq + kb * 2048, &map_q, kb * 64, qrow, &S.kv_full[st]);
-          ++t;
+            for (int kb = 0; kb < 2; ++kb) tma2d(sq + kb * 2048, &map_q, kb * 64, qrow, &S.kv_full[st]);
+            ++t;
+          }
         }
       }
     }
@@ -273,6 +347,10 @@ __global__ void __launch_bounds__(192, 1) k_attn_tc(const __grid_constant__ CUte
           const bool end = S.hdr[st1].item < 0;
           if (!end) issue_s(t + 1);
           const bool first = S.hdr[st].flags & 1;
+          const bool last = S.hdr[st].flags & 2;
+          const int iseq = S.hdr[st].iseq, ob = iseq & 1;
+          if (first)   // O buffer ob must have been read by the epilogue of item iseq - 2
+            mb_wait(&S.o_free[ob], ((uint32_t)(iseq >> 1) & 1u) ^ 1u);
           mb_wait(&S.p_full, (uint32_t)t & 1u);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint8_t* sv = smem + st * STAGE_BYTES + KV_BYTES;
@@ -282,10 +360,11 @@ __global__ void __launch_bounds__(192, 1) k_attn_tc(const __grid_constant__ CUte
 #pragma unroll
             for (int k = 0; k < 8; ++k) {
               const int kb = k >> 2, ko = (k & 3) * 32;
-              mma(tmem + 32, sdesc(sv + k * 2048, 16384, 1024),
+              mma(tmem + 32 + 16 * ob, sdesc(sv + k * 2048, 16384, 1024),
                   sdesc(sp + part * P_BYTES + kb * 2048 + ko, 16, 1024), id_o, (first && part == 0 && k == 0) ? 0u : 1u);
             }
           commit(&S.o_done);
+          if (last) commit(&S.o_fin[ob]);
           commit(&S.kv_empty[st]);
           if (end) { mb_arrive(&S.s_full[(t + 1) & 1]); break; }
         }
@@ -302,45 +381,75 @@ __global__ void __launch_bounds__(192, 1) k_attn_tc(const __grid_constant__ CUte
     const int lq = warp & 3;                          // TMEM lane quarter this warp may access
     const int row = lq * 32 + lane;                   // TMEM lane = tile row (S) = head-dim index (O)
     const uint32_t lane_base = tmem + ((uint32_t)(lq * 32) << 16);
-    float m[NQ], lrow[NQ];
+    float m[NC], lrow[NC];
 #pragma unroll
-    for (int c = 0; c < NQ; ++c) { m[c] = -INFINITY; lrow[c] = 0.f; }
+    for (int c = 0; c < NC; ++c) { m[c] = -INFINITY; lrow[c] = 0.f; }
+    // the finished item whose epilogue waits until the next tile's P is handed over
+    bool pend = false;
+    TcHdr ph;
+    float pm[NC], pl[NC];
+    auto epilogue = [&]() {
+      col_reduce<false, NC>(pl, S.red[1], wq, lane);
+      const int ob = ph.iseq & 1;
+      mb_wait(&S.o_fin[ob], (uint32_t)(ph.iseq >> 1) & 1u);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      float o[NC];
+      tmem_ld<NC>(lane_base + 32 + 16 * ob, o);
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mb_arrive(&S.o_free[ob]);
+      const int d = row;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        if (c >= a.G) break;
+        const int hq = ph.g * a.G + c;
+        if (ph.part < 0) {
+          a.out[((int64_t)(ph.li * a.B + ph.b) * a.H + hq) * DH + d] = o[c] / pl[c];
+        } else {
+          float* pr = a.partials + (((int64_t)ph.part * a.nl + ph.li) * a.H + hq) * (DH + 4);
+          pr[d] = o[c];
+          if (d == 0) { pr[DH] = pm[c]; pr[DH + 1] = pl[c]; }
+        }
+      }
+      pend = false;
+    };
     for (int t = 0;; ++t) {
       const int sb = t & 1;
       mb_wait(&S.s_full[sb], (uint32_t)(t >> 1) & 1u);
       const TcHdr h = S.hdr[t % NST];
       if (h.item < 0) break;
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      float s[NQ];
-      tmem_ld16(lane_base + sb * 16, s);
+      float s[NC];
+      tmem_ld<NC>(lane_base + sb * 16, s);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mb_arrive(&S.s_empty[sb]);
       const bool first = h.flags & 1;
       const bool valid = row < h.nvalid;
+      const int ob = h.iseq & 1;
 #pragma unroll
-      for (int c = 0; c < NQ; ++c) s[c] = valid ? s[c] * a.qscale : -INFINITY;
+      for (int c = 0; c < NC; ++c) s[c] = valid ? s[c] * a.qscale : -INFINITY;
       // does any score need a larger running max?
       bool need = first;
       if (!first) {
         bool over = false;
 #pragma unroll
-        for (int c = 0; c < NQ; ++c) over |= s[c] > m[c] + LAZY_THR;
+        for (int c = 0; c < NC; ++c) over |= s[c] > m[c] + LAZY_THR;
         const bool wover = __any_sync(0xffffffffu, over);
         if (lane == 0) S.flag[wq] = wover;
         softmax_bar();
         need = S.flag[0] | S.flag[1] | S.flag[2] | S.flag[3];
         softmax_bar();
       }
-      float corr[NQ];
+      float corr[NC];
       bool rescale = false;
       if (need) {
-        float mt[NQ];
+        float mt[NC];
 #pragma unroll
-        for (int c = 0; c < NQ; ++c) mt[c] = s[c];
-        col_reduce<true>(mt, S.red[0], wq, lane);
+        for (int c = 0; c < NC; ++c) mt[c] = s[c];
+        col_reduce<true, NC>(mt, S.red[0], wq, lane);
 #pragma unroll
-        for (int c = 0; c < NQ; ++c) {
+        for (int c = 0; c < NC; ++c) {
           const float mn = first ? mt[c] : fmaxf(m[c], mt[c]);
           corr[c] = first ? 0.f : ex2f(m[c] - mn);
           m[c] = mn;
@@ -352,7 +461,7 @@ __global__ void __launch_bounds__(192, 1) k_attn_tc(const __grid_constant__ CUte
       uint8_t* sp = pbuf + (t & 1) * PBUF_BYTES + (row >> 6) * 2048;
       const uint32_t jj2 = (uint32_t)(row & 63) * 2u;
 #pragma unroll
-      for (int c = 0; c < NQ; ++c) {
+      for (int c = 0; c < NC; ++c) {
         const float pv = ex2f(s[c] - m[c]);
         lrow[c] += pv;
         const __nv_bfloat16 hi = __float2bfloat16_rn(pv);
@@ -362,7 +471,7 @@ __global__ void __launch_bounds__(192, 1) k_attn_tc(const __grid_constant__ CUte
         *reinterpret_cast<__nv_bfloat16*>(sp + sw) = hi;
         *reinterpret_cast<__nv_bfloat16*>(sp + P_BYTES + sw) = lo;
       }
-      if (!valid) {                                 // rows past the slot's resident rows: V := 0
+      if (!valid && row < ((h.nvalid + 15) & ~15)) { // loaded rows past the slot's resident rows: V := 0
         uint8_t* sv = smem + (t % NST) * STAGE_BYTES + KV_BYTES;
 #pragma unroll
         for (int kb = 0; kb < 2; ++kb)
@@ -373,41 +482,26 @@ __global__ void __launch_bounds__(192, 1) k_attn_tc(const __grid_constant__ CUte
       if (rescale) {                                // O^T *= corr once the previous tile's MMA is done
         mb_wait(&S.o_done, (uint32_t)(t - 1) & 1u);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        float o[NQ];
-        tmem_ld16(lane_base + 32, o);
+        float o[NC];
+        tmem_ld<NC>(lane_base + 32 + 16 * ob, o);
 #pragma unroll
-        for (int c = 0; c < NQ; ++c) o[c] *= corr[c];
-        tmem_st16(lane_base + 32, o);
+        for (int c = 0; c < NC; ++c) o[c] *= corr[c];
+        tmem_st<NC>(lane_base + 32 + 16 * ob, o);
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mb_arrive(&S.p_full);
-      if (h.flags & 2) {                            // epilogue: lane = head-dim index d
-        float l[NQ];
+      if (pend) epilogue();                         // the previous item, overlapped with this tile's MMA
+      if (h.flags & 2) {
+        pend = true;
+        ph = h;
 #pragma unroll
-        for (int c = 0; c < NQ; ++c) l[c] = lrow[c];
-        col_reduce<false>(l, S.red[1], wq, lane);
-        mb_wait(&S.o_done, (uint32_t)t & 1u);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        float o[NQ];
-        tmem_ld16(lane_base + 32, o);
-        const int d = row;
-#pragma unroll
-        for (int c = 0; c < NQ; ++c) {
-          if (c >= a.G) break;
-          const int hq = h.g * a.G + c;
-          if (h.part < 0) {
-            a.out[((int64_t)(h.li * a.B + h.b) * a.H + hq) * DH + d] = o[c] / l[c];
-          } else {
-            float* pr = a.partials + (((int64_t)h.part * a.nl + h.li) * a.H + hq) * (DH + 4);
-            pr[d] = o[c];
-            if (d == 0) { pr[DH] = m[c]; pr[DH + 1] = l[c]; }
-          }
-        }
-        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        for (int c = 0; c < NC; ++c) { pm[c] = m[c]; pl[c] = lrow[c]; }
       }
     }
+    if (pend) epilogue();
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -469,7 +563,7 @@ bool encode_2d(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, u
 }  // namespace
 
 int attn_tc_smem() { return NST * STAGE_BYTES + 2 * PBUF_BYTES + (int)sizeof(TcSmem) + 1024; }
-const void* attn_tc_kernel_ptr() { return (const void*)k_attn_tc; }
+const void* attn_tc_kernel_ptr(int nc) { return nc == 8 ? (const void*)k_attn_tc<8> : (const void*)k_attn_tc<16>; }
 
 bool attn_tc_supported(const Shape& sh) {
   const int G = sh.Hkv > 0 ? sh.H / sh.Hkv : 0;
@@ -495,7 +589,8 @@ cudaError_t launch_attn_tc(const Shape& sh, const uint16_t* q, uint16_t* arena, 
   a.H = sh.H; a.Hkv = sh.Hkv; a.G = sh.H / sh.Hkv; a.B = B; a.l0 = l0; a.nl = nl;
   a.qscale = 1.4426950408889634f / sqrtf((float)sh.D);
   a.out = out; a.partials = partials; a.units = units; a.ctrl = ctrl;
-  k_attn_tc<<<grid_attn, 192, attn_tc_smem(), st>>>(map_kv, map_q, a);
+  if (a.G <= 8) k_attn_tc<8><<<grid_attn, 192, attn_tc_smem(), st>>>(map_kv, map_q, a);
+  else k_attn_tc<16><<<grid_attn, 192, attn_tc_smem(), st>>>(map_kv, map_q, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   return launch_combine(sh, splits, partials, out, ctrl, B, nl, grid_combine, st);
