@@ -54,9 +54,9 @@ def parse():
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--shape", default="gptj", choices=sorted(SHAPES))
     ap.add_argument("--arena-gb", type=float, default=0.0, help="cap the arena (e.g. for ncu replay)")
-    ap.add_argument("--attn", default="tma", choices=["tma", "regs", "tc"],
-                    help="attention kernel: tma (TMA ring, default), regs (register streaming), "
-                         "tc (tcgen05 tensor cores, grouped KV with D = 128)")
+    ap.add_argument("--attn", default="auto", choices=["auto", "tma", "regs", "tc"],
+                    help="attention kernel: tma (TMA ring), regs (register streaming), tc (tcgen05 tensor "
+                         "cores, grouped KV with D = 128); auto = tc for grouped KV with D = 128, else tma")
     ap.add_argument("--compact-policy", default="every", choices=["every", "on-demand"],
                     help="row shift every step (the paper) or only when the pool could use the rows (R27)")
     ap.add_argument("--model", default="none", choices=["none", "gptj"],
@@ -240,6 +240,8 @@ def run_s3(args):
     t = s3synth.make_trace(n_req, seed=args.seed, policy=policy, p=p, max_seq_len=GPTJ["max_len"])
     shp = SHAPES[args.shape]
     L, H, D, Hkv = shp["L"], shp["H"], shp["D"], shp["Hkv"]
+    if args.attn == "auto":
+        args.attn = "tc" if (Hkv < H and D == 128 and 2 <= H // Hkv <= 16) else "tma"
     kvpt = 4 * L * Hkv * D
     max_running = 8192 if args.shape == "gptj" else 16384
     io_bytes = max_running * L * D * (H * 2 + 2 * Hkv * 2 + H * 4)
