@@ -34,11 +34,14 @@ CASES = [  # (name, L, H, Hkv, D, B, P, attn_variant)
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--case", default=None, help="run only cases whose name contains this")
     args = ap.parse_args()
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
     for case in CASES:
         name, L, H, Hkv, D, B, P = case[:7]
+        if args.case and args.case not in name:
+            continue
         variant = case[7] if len(case) > 7 else 0
         kvpt = 4 * L * Hkv * D
         R = max(2048, B * (P + args.steps + 8))
