@@ -374,13 +374,14 @@ def test_on_demand_compaction_policy(mode):
     assert r["evictions"] > 0
 
 
-@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("seed", range(12))
 def test_randomized_configurations(seed):
     """Property sweep: random shapes, chunk sizes, move chunks, policies,
     compaction modes, kernel variants, staging on/off; full runs in lockstep."""
     rng = np.random.default_rng(1000 + seed)
     D = int(rng.choice([64, 128, 256]))
     H = int(rng.choice([1, 2, 4, 8])) if D < 256 else int(rng.choice([1, 2, 4]))
+    Hkv = int(rng.choice([h for h in (1, 2, 4, 8) if h <= H and H % h == 0]))
     L = int(rng.integers(1, 4))
     M = int(rng.choice([64, 96, 160]))
     n = int(rng.integers(10, 50))
@@ -388,12 +389,14 @@ def test_randomized_configurations(seed):
     t = s3synth.make_trace(n, seed=seed, policy=pol, p=0.3, max_seq_len=M, prompt_max=M // 4)
     R = int(M * rng.integers(1, 6))
     variant = int(rng.integers(0, 2))
+    if D == 128 and 2 <= H // Hkv <= 16 and rng.random() < 0.5:
+        variant = 2                     # tensor cores for grouped KV
     mode = int(rng.integers(0, 2)) if variant == 0 else 1
     r = lockstep(t, L, H, D, R, C=int(rng.choice([2, 5, 16, 64])), S=int(rng.choice([1024, 4096, 32768])),
                  max_running=int(rng.choice([4, 16, 4096])), staging=bool(rng.integers(0, 2)),
                  attn_variant=variant, compact_mode=mode, compact_policy=int(rng.integers(0, 2)),
-                 poison=bool(rng.integers(0, 2)))
-    print(seed, dict(L=L, H=H, D=D, M=M, n=n, pol=pol, R=R), r)
+                 poison=bool(rng.integers(0, 2)), Hkv=Hkv)
+    print(seed, dict(L=L, H=H, Hkv=Hkv, D=D, M=M, n=n, pol=pol, R=R, variant=variant), r)
 
 
 @pytest.mark.parametrize("H,Hkv,D,variant,mode", [(8, 2, 128, 0, 0), (8, 2, 128, 1, 1), (4, 1, 64, 0, 0),
