@@ -90,11 +90,12 @@ def load_peak():
         return FALLBACK_HBM_GBS, "fallback"
 
 
-def traffic_from_profiles():
-    """dram bytes per attention launch from the committed ncu --set full capture."""
+def traffic_from_profiles(key):
+    """dram bytes per attention launch from the committed ncu capture of this
+    bench configuration (shape/attn/config), or None if none was captured."""
     try:
         with open(os.path.join(ROOT, "profiles", "attn_traffic.json")) as f:
-            return json.load(f)
+            return json.load(f)["captures"].get(key)
     except Exception:
         return None
 
@@ -352,7 +353,7 @@ def run_s3(args):
     attn_kernel_bytes = prof.attn_bytes + prof.fused_move_bytes
     attn_gbs = attn_kernel_bytes / (prof.attn_ms / 1e3) / 1e9 if prof.attn_ms > 0 else 0.0
     move_gbs = prof.move_bytes / (prof.move_ms / 1e3) / 1e9 if prof.move_ms > 0 else 0.0
-    tr = traffic_from_profiles()
+    tr = traffic_from_profiles(f"{args.shape}/{args.attn}/{args.config}")
     pcie = pcie_peaks(dev)
     # generation / penalty / overhead per step (the paper's Fig. 6 split,
     # PAPER.md:294): the attention kernel's time is split by its bytes
@@ -394,7 +395,8 @@ def run_s3(args):
             "roofline": {
                 "bound": "hbm", "kernel": {"tma": "k_attn_tma", "regs": "k_attn", "tc": "k_attn_tc (tcgen05)"}[args.attn]
                           + "+k_combine (decode attention"
-                          + (" fused with the row shift)" if args.compact == "fused" and args.attn == "tma" else ")"),
+                          + (" fused with the row shift)" if args.compact == "fused" and args.attn in ("tma", "tc")
+                             else ")"),
                 "achieved": attn_gbs, "peak": peak, "unit": "GB/s", "frac": attn_gbs / peak,
                 "peak_source": peak_kind,
                 "traffic": tr.get("dram_bytes_per_launch") if tr else None,

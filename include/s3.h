@@ -67,7 +67,7 @@ typedef struct {
   int32_t max_seq_len;                      /* cap on P + output (2048 for GPT-J runs)         */
   int64_t arena_rows;                       /* R >= max_seq_len                                */
   int32_t max_running;                      /* metadata capacity B_max (admission stops there) */
-  int32_t chunk_rows;                       /* attention split-K chunk C in rows (0 = 512)     */
+  int32_t chunk_rows;                       /* attention split-K chunk C in rows (0 = 512; <= 32768) */
   int32_t move_chunk_bytes;                 /* compaction chunk S (0 = 32768; 1024..36864, %16)*/
   int32_t device;                           /* CUDA device ordinal                             */
   void*   stream;                           /* cudaStream_t for all device work                */

@@ -21,8 +21,23 @@
 //                   safety), rescale O^T in TMEM; after the last tile of an
 //                   item lane d holds O^T[d][:] and writes out / the split-K
 //                   partial (same records as k_combine reads).
+//   storer warp   : (fused steps only) the row shift of SURVEY §8 row (d),
+//                   done on the tiles already in shared memory -- see below.
 // The new token's K/V row is appended to the arena by k_append before this
 // kernel, so every tile reads rows straight from the arena.
+//
+// Fused row shift (same protocol as k_attn_tma, at tile granularity): when a
+// tile lands the storer publishes its unit-layer's read progress
+// (head * 2^16 + rows, monotone because a CTA walks a unit-layer's KV heads
+// in order); for a MOVE tile it waits until every other unit whose source
+// rows overlap the tile's destination rows (k_deps, tc mode) has read that
+// far, then writes the tile's whole 16-row groups back with TMA tensor stores
+// through the same swizzled map and the ragged tail rows with a warp copy
+// that undoes the 128B swizzle; STAGE (evicted) tiles go to the staging
+// buffer the same way.  The stage is released (kv_empty) only after the
+// stores have read shared memory.  Deadlock freedom is the k_attn_tma
+// argument: tickets are taken in unit order and destinations lie at or below
+// their sources.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -50,8 +65,13 @@ constexpr int TMEM_COLS = 64;               // S0 [0,16), S1 [16,32), O0 [32,48)
 struct TcHdr {
   int32_t item, r0, nvalid, flags;          // flags: 1 = first tile of the item, 2 = last
   int32_t b, part, li, g;
-  int32_t iseq, pad[3];                     // per-CTA item sequence number: O buffer = iseq & 1
+  int32_t iseq, mode, drow;                 // iseq: per-CTA item sequence number (O buffer = iseq & 1)
+  uint32_t prog;                            // read progress this tile completes (storer)
+  DepDesc dep;                              // MOVE tiles: filled by the TMA engine with the tile
 };
+static_assert(sizeof(TcHdr) % 16 == 0, "TcHdr.dep must stay 16-B aligned");
+constexpr uint32_t TC_PROG_FULL = 0x80000000u;
+constexpr int TC_HEAD_STRIDE = 1 << 16;      // progress = head * 2^16 + rows (unit rows < 2^16)
 
 struct TcSmem {                             // after the ring and the two P buffers
   uint64_t kv_full[NST], kv_empty[NST], s_full[2], s_empty[2], p_full, o_done, o_fin[2], o_free[2];
@@ -77,6 +97,25 @@ __device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t parity) {
           su32(b)),
       "r"(parity)
       : "memory");
+}
+__device__ __forceinline__ void bulk_g2s16(void* dst, const void* src, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 16, [%2];" ::"r"(
+                   su32(dst)),
+               "l"(src), "r"(su32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tma2d_store(const CUtensorMap* map, int c0, int c1, const void* src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(map), "r"(c0),
+               "r"(c1), "r"(su32(src))
+               : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acq_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_rlx_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 __device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
   asm volatile(
@@ -229,18 +268,30 @@ struct TcArgs {
   float* partials;
   const Unit* units;
   int32_t* ctrl;
+  // fused row shift
+  uint8_t* arena;
+  uint8_t* staging;
+  int64_t kvpt;
+  const DepDesc* desc;
+  unsigned long long* progress;
+  uint32_t epoch;
 };
 
 template <int NC>   // query columns the softmax handles: G padded to 8 or 16 (the MMA always has N = 16)
-__global__ void __launch_bounds__(192, 1) k_attn_tc(const __grid_constant__ CUtensorMap map_kv,
-                                                    const __grid_constant__ CUtensorMap map_q, TcArgs a) {
+__global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ CUtensorMap map_kv,
+                                                    const __grid_constant__ CUtensorMap map_q,
+                                                    const __grid_constant__ CUtensorMap map_stage, TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  // 1024-B alignment for the 128B-swizzle atoms, by pointer arithmetic so the
+  // compiler keeps the shared-memory address space (LDS/STS, not generic LD/ST)
+  uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   uint8_t* pbuf = smem + NST * STAGE_BYTES;
   TcSmem& S = *reinterpret_cast<TcSmem*>(pbuf + 2 * PBUF_BYTES);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // the storer takes part in the ring only when this step shifts rows
+  const bool fused = a.ctrl[CTRL_FUSED] != 0;
   if (tid == 0) {
-    for (int i = 0; i < NST; ++i) { mb_init(&S.kv_full[i], 1); mb_init(&S.kv_empty[i], 1); }
+    for (int i = 0; i < NST; ++i) { mb_init(&S.kv_full[i], 1); mb_init(&S.kv_empty[i], fused ? 2 : 1); }
     for (int i = 0; i < 2; ++i) { mb_init(&S.s_full[i], 1); mb_init(&S.s_empty[i], 4); }
     mb_init(&S.p_full, 4);
     mb_init(&S.o_done, 1);
@@ -282,6 +333,9 @@ __global__ void __launch_bounds__(192, 1) k_attn_tc(const __grid_constant__ CUte
         const int li = w % a.nl, u = w / a.nl;
         const Unit un = a.units[u];
         const int nrows = (un.r1 - un.r0) + (un.has_new ? 1 : 0);   // new row already in the arena
+        const bool mv = un.mode == UNIT_MOVE;
+        // destination row of the unit's first row: arena row (MOVE) or staging row (STAGE)
+        const int drow0 = (int)(mv ? un.dst : un.dst / a.kvpt) + un.r0;
         for (int g = 0; g < a.Hkv; ++g, ++iseq) {
           const int item = w * a.Hkv + g;
           const int colk = (a.l0 + li) * row_cols + g * DH;
@@ -295,11 +349,15 @@ __global__ void __launch_bounds__(192, 1) k_attn_tc(const __grid_constant__ CUte
             h.item = item; h.r0 = un.r0 + r; h.nvalid = nv;
             h.flags = (r == 0 ? 1 : 0) | (r + TM >= nrows ? 2 : 0);
             h.b = un.b; h.part = un.part; h.li = li; h.g = g; h.iseq = iseq;
+            h.mode = un.mode; h.drow = drow0 + r;
+            h.prog = (uint32_t)(g * TC_HEAD_STRIDE + r + nv) | (g == a.Hkv - 1 && r + TM >= nrows ? TC_PROG_FULL : 0u);
             const int groups = (nv + 15) / 16;
             uint8_t* sk = smem + st * STAGE_BYTES;
             uint8_t* sv = sk + KV_BYTES;
             uint8_t* sq = sv + KV_BYTES;
-            mb_expect(&S.kv_full[st], (uint32_t)(groups * 16 * 128 * 2 * 2 + Q_BYTES));
+            const bool dep = fused && mv;
+            mb_expect(&S.kv_full[st], (uint32_t)(groups * 16 * 128 * 2 * 2 + Q_BYTES + (dep ? 16 : 0)));
+            if (dep) bulk_g2s16(&h.dep, a.desc + un.stage_base + r / TM, &S.kv_full[st]);
             const int row0 = un.off + un.r0 + r;
             for (int gr = 0; gr < groups; ++gr)
 #pragma unroll
@@ -370,6 +428,82 @@ __global__ void __launch_bounds__(192, 1) k_attn_tc(const __grid_constant__ CUte
         }
       }
     }
+  } else if (warp == 6) {
+    // ------------------------------- storer -------------------------------
+    if (fused) {
+      int pending = -1;                   // stage whose bulk stores may still read shared memory
+      for (int t = 0;; ++t) {
+        const int st = t % NST;
+        mb_wait(&S.kv_full[st], (uint32_t)(t / NST) & 1u);
+        const TcHdr h = S.hdr[st];
+        if (h.item < 0) break;
+        const int w = h.item / a.Hkv;     // unit-layer ticket = progress slot
+        if (lane == 0) {
+          // the tile's rows are in shared memory: its source rows may be overwritten
+          st_rlx_u64(a.progress + w, ((unsigned long long)a.epoch << 32) | h.prog);
+          if (h.mode == UNIT_MOVE && h.dep.ua >= 0) {
+            const uint32_t gbase = (uint32_t)(h.g * TC_HEAD_STRIDE);
+            for (int v = h.dep.ua; v <= h.dep.ub; ++v) {
+              const int need = v == h.dep.ua ? h.dep.need_a : (v == h.dep.ub ? h.dep.need_b : -1);
+              const int it = v * a.nl + h.li;
+              if (it == w) continue;      // own rows: earlier tiles of this head, already read
+              for (;;) {
+                const unsigned long long x = ld_acq_u64(a.progress + it);
+                const uint32_t lo = (uint32_t)x;
+                if ((uint32_t)(x >> 32) == a.epoch && ((lo & TC_PROG_FULL) || (need >= 0 && lo >= gbase + need)))
+                  break;
+                __nanosleep(32);
+              }
+            }
+          }
+        }
+        __syncwarp();
+        const bool stores = (h.mode == UNIT_MOVE || h.mode == UNIT_STAGE) && h.nvalid > 0;
+        if (stores) {
+          const uint8_t* sk = smem + st * STAGE_BYTES;
+          const int colk = (a.l0 + h.li) * 2 * a.Hkv * DH + h.g * DH;   // elements
+          const int colv = colk + a.Hkv * DH;
+          const int full_groups = h.nvalid >> 4;
+          if (lane == 0) {
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            const CUtensorMap* map = h.mode == UNIT_MOVE ? &map_kv : &map_stage;
+            for (int gr = 0; gr < full_groups; ++gr)
+#pragma unroll
+              for (int kb = 0; kb < 2; ++kb) {
+                tma2d_store(map, colk + kb * 64, h.drow + gr * 16, sk + kb * 16384 + gr * 2048);
+                tma2d_store(map, colv + kb * 64, h.drow + gr * 16, sk + KV_BYTES + kb * 16384 + gr * 2048);
+              }
+          }
+          // ragged tail rows: one 16-B chunk per lane (K/V, 64-column block, chunk)
+          const int kv = lane >> 4, kb = (lane >> 3) & 1, c = lane & 7;
+          uint8_t* gbase = (h.mode == UNIT_MOVE ? a.arena : a.staging) +
+                           (int64_t)(kv ? colv : colk) * 2 + kb * 128 + c * 16;
+          for (int row = full_groups * 16; row < h.nvalid; ++row) {
+            const uint4 x = *reinterpret_cast<const uint4*>(sk + kv * KV_BYTES + kb * 16384 + row * 128 +
+                                                            ((c ^ (row & 7)) << 4));
+            *reinterpret_cast<uint4*>(gbase + (int64_t)(h.drow + row) * a.kvpt) = x;
+          }
+          __syncwarp();
+        }
+        if (lane == 0) {
+          if (stores) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+          // release the previous stage once its stores have read shared memory
+          if (pending >= 0) {
+            if (stores) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            mb_arrive(&S.kv_empty[pending]);
+            pending = -1;
+          }
+          if (stores) pending = st;
+          else mb_arrive(&S.kv_empty[st]);
+        }
+      }
+      if (lane == 0) {
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        if (pending >= 0) mb_arrive(&S.kv_empty[pending]);
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+      }
+    }
   } else {
     // ------------------------------ softmax -------------------------------
     // Lazy running max (log2 domain): the column max is reduced across the
@@ -386,7 +520,7 @@ __global__ void __launch_bounds__(192, 1) k_attn_tc(const __grid_constant__ CUte
     for (int c = 0; c < NC; ++c) { m[c] = -INFINITY; lrow[c] = 0.f; }
     // the finished item whose epilogue waits until the next tile's P is handed over
     bool pend = false;
-    TcHdr ph;
+    TcHdr ph = {};
     float pm[NC], pl[NC];
     auto epilogue = [&]() {
       col_reduce<false, NC>(pl, S.red[1], wq, lane);
@@ -578,19 +712,31 @@ cudaError_t launch_append(const Shape& sh, const DSlot* slots, int32_t B, int32_
   return cudaGetLastError();
 }
 
-cudaError_t launch_attn_tc(const Shape& sh, const uint16_t* q, uint16_t* arena, int64_t arena_rows, float* out,
-                           float* partials, const Unit* units, const Split* splits, int32_t* ctrl, int32_t B,
-                           int32_t l0, int32_t nl, int32_t grid_attn, int32_t grid_combine, cudaStream_t st) {
-  CUtensorMap map_kv, map_q;
+cudaError_t launch_attn_tc(const Shape& sh, const uint16_t* q, uint16_t* arena, int64_t arena_rows,
+                           uint8_t* staging, int64_t staging_bytes, float* out, float* partials, const Unit* units,
+                           const Split* splits, const DepDesc* desc, unsigned long long* progress, uint32_t epoch,
+                           int32_t* ctrl, int32_t B, int32_t l0, int32_t nl, int32_t grid_attn, int32_t grid_combine,
+                           cudaStream_t st) {
+  CUtensorMap map_kv, map_q, map_stage;
   if (!encode_2d(&map_kv, arena, (uint64_t)sh.row_elems, (uint64_t)arena_rows, (uint64_t)sh.kvpt))
     return cudaErrorInvalidValue;
   if (!encode_2d(&map_q, q, (uint64_t)sh.D, (uint64_t)nl * B * sh.H, (uint64_t)sh.D * 2)) return cudaErrorInvalidValue;
+  // staging rows (evicted slots' KV, token-major like the arena); without staging k_prep never fuses an eviction
+  const int64_t stage_rows = staging ? staging_bytes / sh.kvpt : 0;
+  if (stage_rows > 0) {
+    if (!encode_2d(&map_stage, staging, (uint64_t)sh.row_elems, (uint64_t)stage_rows, (uint64_t)sh.kvpt))
+      return cudaErrorInvalidValue;
+  } else {
+    map_stage = map_kv;
+  }
   TcArgs a;
   a.H = sh.H; a.Hkv = sh.Hkv; a.G = sh.H / sh.Hkv; a.B = B; a.l0 = l0; a.nl = nl;
   a.qscale = 1.4426950408889634f / sqrtf((float)sh.D);
   a.out = out; a.partials = partials; a.units = units; a.ctrl = ctrl;
-  if (a.G <= 8) k_attn_tc<8><<<grid_attn, 192, attn_tc_smem(), st>>>(map_kv, map_q, a);
-  else k_attn_tc<16><<<grid_attn, 192, attn_tc_smem(), st>>>(map_kv, map_q, a);
+  a.arena = reinterpret_cast<uint8_t*>(arena); a.staging = staging; a.kvpt = sh.kvpt;
+  a.desc = desc; a.progress = progress; a.epoch = epoch;
+  if (a.G <= 8) k_attn_tc<8><<<grid_attn, 224, attn_tc_smem(), st>>>(map_kv, map_q, map_stage, a);
+  else k_attn_tc<16><<<grid_attn, 224, attn_tc_smem(), st>>>(map_kv, map_q, map_stage, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   return launch_combine(sh, splits, partials, out, ctrl, B, nl, grid_combine, st);

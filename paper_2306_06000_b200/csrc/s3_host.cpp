@@ -169,7 +169,7 @@ bool validate(const s3_config* c) {
   if (c->max_seq_len < 1 || c->arena_rows < c->max_seq_len) return false;
   if (c->arena_rows > INT32_MAX) return false;
   if (c->max_running < 1 || c->max_running > 65535) return false;
-  if (c->chunk_rows < 0 || c->move_chunk_bytes < 0 || c->move_chunk_bytes % 16) return false;
+  if (c->chunk_rows < 0 || c->chunk_rows > 32768 || c->move_chunk_bytes < 0 || c->move_chunk_bytes % 16) return false;
   if (c->move_chunk_bytes > 0 && (c->move_chunk_bytes < 1024 || c->move_chunk_bytes > 36864)) return false;
   if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return false;
   if (c->attn_variant < 0 || c->attn_variant > 2) return false;
@@ -508,8 +508,8 @@ s3_status s3_decode_step(s3_ctx* ctx, int32_t l0, int32_t nl, const void* q, con
   const bool finalize = (l0 + nl == ctx->sh.L);
   const int32_t B = (int32_t)ctx->slots_h.size();
   // fuse the row shift into this attention pass when the step is whole
-  const bool fuse = finalize && l0 == 0 && ctx->cfg.compact_mode == 0 && ctx->cfg.attn_variant == 0 &&
-                    attn_tma_stages(ctx->sh) >= 2 && B > 0;
+  const bool fuse = finalize && l0 == 0 && ctx->cfg.compact_mode == 0 && B > 0 &&
+                    ((ctx->cfg.attn_variant == 0 && attn_tma_stages(ctx->sh) >= 2) || ctx->cfg.attn_variant == 2);
   if (B > 0) {
     if (!q || !k_new || !v_new || !out || (finalize && !eos)) return fail(ctx, S3_E_INVAL, "decode_step: null");
     if (fuse && ctx->last_stage_d2h)   // staging is rewritten: the previous step's D2H from it must be done
@@ -536,16 +536,18 @@ s3_status s3_decode_step(s3_ctx* ctx, int32_t l0, int32_t nl, const void* q, con
       CK(cudaMemcpyAsync(ctx->h_report + report_bytes(B), ctx->ctrl + CTRL_FUSED, 4, cudaMemcpyDeviceToHost,
                          ctx->st), "fused flag D2H");
       CK(cudaEventRecord(ctx->ev_report, ctx->st), "event");
-      CK(launch_deps(ctx->units, ctx->ctrl, ctx->desc, ctx->num_sms * 4, ctx->st), "k_deps");
+      CK(launch_deps(ctx->units, ctx->ctrl, ctx->desc, ctx->cfg.attn_variant == 2 ? 1 : 0, ctx->num_sms * 4,
+                     ctx->st), "k_deps");
       ctx->launches += 1;
     }
     ctx->attn_epoch++;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx->prof.on) { e0 = ctx->prof.get(); e1 = ctx->prof.get(); cudaEventRecord(e0, ctx->st); }
     if (ctx->cfg.attn_variant == 2)
-      CK(launch_attn_tc(ctx->sh, (const uint16_t*)q, (uint16_t*)ctx->buf.arena, ctx->cfg.arena_rows, out,
-                        ctx->partials, ctx->units, ctx->splits, ctx->ctrl, B, l0, nl, ctx->grid_attn,
-                        ctx->grid_combine, ctx->st), "k_attn_tc");
+      CK(launch_attn_tc(ctx->sh, (const uint16_t*)q, (uint16_t*)ctx->buf.arena, ctx->cfg.arena_rows,
+                        (uint8_t*)ctx->buf.staging, ctx->buf.staging ? ctx->buf.staging_bytes : 0, out, ctx->partials,
+                        ctx->units, ctx->splits, ctx->desc, ctx->progress, ctx->attn_epoch, ctx->ctrl, B, l0, nl,
+                        ctx->grid_attn, ctx->grid_combine, ctx->st), "k_attn_tc");
     else
       CK(launch_attn(ctx->sh, (const uint16_t*)q, (const uint16_t*)k_new, (const uint16_t*)v_new,
                      (uint16_t*)ctx->buf.arena, (uint8_t*)ctx->buf.staging, out, ctx->partials, ctx->units,

@@ -316,33 +316,36 @@ __global__ void __launch_bounds__(1024) k_prep(PrepArgs a) {
 // unit's last stage).  Sources are the units' arena rows [off+r0, off+r1),
 // sorted and disjoint in unit order, so a binary search finds the first.
 // One warp per unit, lanes over its stages.
+// tc = 1 (k_attn_tc): stages are 128-row tiles and the new row is already in
+// the arena (k_append), so it is a source row of its unit and a tile row.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_deps(const Unit* __restrict__ units, const int32_t* __restrict__ ctrl,
-                                              DepDesc* __restrict__ desc) {
+                                              DepDesc* __restrict__ desc, int32_t tc) {
   const int n_units = ctrl[CTRL_N_UNITS];
   const int lane = threadIdx.x & 31;
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int nw = (gridDim.x * blockDim.x) >> 5;
+  const int tile = tc ? 128 : AT_RPS;
   for (int ui = gw; ui < n_units; ui += nw) {
     const Unit un = units[ui];
-    const int rows = un.r1 - un.r0;
-    const int ns = rows > 0 ? (rows + AT_RPS - 1) / AT_RPS : 1;
+    const int rows = un.r1 - un.r0 + (tc ? un.has_new : 0);
+    const int ns = rows > 0 ? (rows + tile - 1) / tile : 1;
     for (int s = lane; s < ns; s += 32) {
       DepDesc d;
       d.ua = -1; d.need_a = 0; d.ub = -1; d.need_b = 0;
       if (un.mode == UNIT_MOVE) {
-        const int n = max(0, min(AT_RPS, rows - s * AT_RPS));
-        const int64_t d0 = un.dst + un.r0 + (int64_t)s * AT_RPS;
-        const int64_t d1 = d0 + n + ((s == ns - 1 && un.has_new) ? 1 : 0);
+        const int n = max(0, min(tile, rows - s * tile));
+        const int64_t d0 = un.dst + un.r0 + (int64_t)s * tile;
+        const int64_t d1 = d0 + n + ((!tc && s == ns - 1 && un.has_new) ? 1 : 0);
         int lo = 0, hi = n_units;              // first unit with source end > d0
         while (lo < hi) {
           const int mid = (lo + hi) >> 1;
           const Unit& m = units[mid];
-          if ((int64_t)m.off + m.r1 > d0) hi = mid; else lo = mid + 1;
+          if ((int64_t)m.off + m.r1 + (tc ? m.has_new : 0) > d0) hi = mid; else lo = mid + 1;
         }
         for (int v = lo; v < n_units; ++v) {
           const Unit& m = units[v];
-          const int64_t s0 = (int64_t)m.off + m.r0, s1 = (int64_t)m.off + m.r1;
+          const int64_t s0 = (int64_t)m.off + m.r0, s1 = (int64_t)m.off + m.r1 + (tc ? m.has_new : 0);
           if (s0 >= d1) break;
           if (s1 <= s0 || s1 <= d0) continue;  // empty source or no overlap
           const int need = (int)(min(d1, s1) - s0);
@@ -1312,8 +1315,9 @@ cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_deps(const Unit* units, const int32_t* ctrl, DepDesc* desc, int32_t grid, cudaStream_t st) {
-  k_deps<<<grid, 256, 0, st>>>(units, ctrl, desc);
+cudaError_t launch_deps(const Unit* units, const int32_t* ctrl, DepDesc* desc, int32_t tc, int32_t grid,
+                        cudaStream_t st) {
+  k_deps<<<grid, 256, 0, st>>>(units, ctrl, desc, tc);
   return cudaGetLastError();
 }
 

@@ -47,6 +47,7 @@ def lockstep(trace, L, H, D, R, C=0, S=0, max_running=4096, staging=True, feed_o
     eng = S3Engine(L, H, D, trace.max_seq_len, R, max_running, chunk_rows=C, move_chunk_bytes=S,
                    staging_bytes=None if staging else 0, host_store_bytes=64 << 20, attn_variant=attn_variant,
                    compact_mode=compact_mode, compact_policy=compact_policy, num_kv_heads=Hkv)
+    eng.profile(True)
     orc = oracle.Oracle(L, H, D, trace.max_seq_len, R, max_running=max_running, compact_policy=compact_policy,
                         Hkv=Hkv)
     eng.submit(trace.req_id, trace.prompt, trace.alloc, trace.out)
@@ -123,6 +124,7 @@ def lockstep(trace, L, H, D, R, C=0, S=0, max_running=4096, staging=True, feed_o
                     f"step {steps}: arena rows of req {req} differ"
         steps += 1
     assert eng.verify_resident() == 0
+    stats["fused_steps"] = eng.profile_get().fused_steps
     eng.close()
     return dict(steps=steps, worst=worst, **stats)
 
@@ -408,11 +410,23 @@ def test_grouped_query_kv(H, Hkv, D, variant, mode):
     assert r["evictions"] > 0
 
 
-@pytest.mark.parametrize("H,Hkv,C,policy", [(8, 2, 512, "short"), (32, 8, 48, "short"), (16, 1, 128, "bucket"),
-                                            (4, 2, 7, "short")])
-def test_grouped_query_kv_tensor_cores(H, Hkv, C, policy):
+@pytest.mark.parametrize("H,Hkv,C,policy,mode,staging", [
+    (8, 2, 512, "short", 0, True), (32, 8, 48, "short", 0, True), (16, 1, 128, "bucket", 0, True),
+    (4, 2, 7, "short", 0, True), (8, 2, 64, "short", 1, True), (8, 2, 512, "short", 0, False)])
+def test_grouped_query_kv_tensor_cores(H, Hkv, C, policy, mode, staging):
     """attn_variant 2: tcgen05/TMEM/TMA kernel for grouped KV (D = 128); C
-    small -> split-K units and tile tails; NaN-poisoned slack rows."""
+    small -> split-K units and tile tails; NaN-poisoned slack rows.  mode 0:
+    the row shift and the eviction staging are fused into the kernel (TMA
+    tensor stores + ragged-tail warp copy; checked row by row against the
+    oracle's arena and host copies every step); mode 1: separate k_move
+    pass; no staging: evictions fall back to the unfused path."""
     t = s3synth.make_trace(40, seed=53, policy=policy, p=0.3, max_seq_len=320, prompt_max=200)
-    r = lockstep(t, 2, H, 128, 1600, C=C, S=2048, attn_variant=2, Hkv=Hkv, poison=True)
-    print("worst", r["worst"])
+    r = lockstep(t, 2, H, 128, 1600, C=C, S=2048, attn_variant=2, Hkv=Hkv, poison=True, compact_mode=mode,
+                 staging=staging)
+    print("worst", r["worst"], "fused", r["fused_steps"], "of", r["steps"], "evictions", r["evictions"])
+    if policy == "short":
+        assert r["evictions"] > 0
+    if mode == 0 and staging:
+        assert r["fused_steps"] >= 0.9 * r["steps"]   # unfused only when a step's evictions overflow staging
+    if mode == 1:
+        assert r["fused_steps"] == 0
