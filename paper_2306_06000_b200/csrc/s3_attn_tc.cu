@@ -261,6 +261,16 @@ __device__ __forceinline__ void col_reduce(float (&v)[NC], float (&red)[4][NQ], 
   softmax_bar();
 }
 
+// tensor maps: arena and staging rows in boxes of 128 / 64 / 32 / 16 rows x 64
+// columns (a tile's valid 16-row groups go out as a binary decomposition, so a
+// full tile is one box per 64-column block instead of eight)
+constexpr int NBOX = 4;
+struct TcMaps {
+  CUtensorMap kv[NBOX];      // box rows 128 >> i
+  CUtensorMap stage[NBOX];
+  CUtensorMap q;             // 16 rows
+};
+
 struct TcArgs {
   int32_t H, Hkv, G, B, l0, nl;
   float qscale;
@@ -278,9 +288,7 @@ struct TcArgs {
 };
 
 template <int NC>   // query columns the softmax handles: G padded to 8 or 16 (the MMA always has N = 16)
-__global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ CUtensorMap map_kv,
-                                                    const __grid_constant__ CUtensorMap map_q,
-                                                    const __grid_constant__ CUtensorMap map_stage, TcArgs a) {
+__global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMaps maps, TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-B alignment for the 128B-swizzle atoms, by pointer arithmetic so the
   // compiler keeps the shared-memory address space (LDS/STS, not generic LD/ST)
@@ -359,14 +367,22 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ CUte
             mb_expect(&S.kv_full[st], (uint32_t)(groups * 16 * 128 * 2 * 2 + Q_BYTES + (dep ? 16 : 0)));
             if (dep) bulk_g2s16(&h.dep, a.desc + un.stage_base + r / TM, &S.kv_full[st]);
             const int row0 = un.off + un.r0 + r;
-            for (int gr = 0; gr < groups; ++gr)
+            int done = 0;                 // 16-row groups, largest boxes first
 #pragma unroll
-              for (int kb = 0; kb < 2; ++kb) {
-                tma2d(sk + kb * 16384 + gr * 2048, &map_kv, colk + kb * 64, row0 + gr * 16, &S.kv_full[st]);
-                tma2d(sv + kb * 16384 + gr * 2048, &map_kv, colv + kb * 64, row0 + gr * 16, &S.kv_full[st]);
+            for (int i = 0; i < NBOX; ++i) {
+              const int bg = 8 >> i;
+              if (groups - done >= bg) {
+                const CUtensorMap* m = &maps.kv[i];
+#pragma unroll
+                for (int kb = 0; kb < 2; ++kb) {
+                  tma2d(sk + kb * 16384 + done * 2048, m, colk + kb * 64, row0 + done * 16, &S.kv_full[st]);
+                  tma2d(sv + kb * 16384 + done * 2048, m, colv + kb * 64, row0 + done * 16, &S.kv_full[st]);
+                }
+                done += bg;
               }
+            }
 #pragma unroll
-            for (int kb = 0; kb < 2; ++kb) tma2d(sq + kb * 2048, &map_q, kb * 64, qrow, &S.kv_full[st]);
+            for (int kb = 0; kb < 2; ++kb) tma2d(sq + kb * 2048, &maps.q, kb * 64, qrow, &S.kv_full[st]);
             ++t;
           }
         }
@@ -466,13 +482,20 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ CUte
           const int full_groups = h.nvalid >> 4;
           if (lane == 0) {
             asm volatile("fence.proxy.async.global;" ::: "memory");
-            const CUtensorMap* map = h.mode == UNIT_MOVE ? &map_kv : &map_stage;
-            for (int gr = 0; gr < full_groups; ++gr)
+            const CUtensorMap* map = h.mode == UNIT_MOVE ? maps.kv : maps.stage;
+            int done = 0;
 #pragma unroll
-              for (int kb = 0; kb < 2; ++kb) {
-                tma2d_store(map, colk + kb * 64, h.drow + gr * 16, sk + kb * 16384 + gr * 2048);
-                tma2d_store(map, colv + kb * 64, h.drow + gr * 16, sk + KV_BYTES + kb * 16384 + gr * 2048);
+            for (int i = 0; i < NBOX; ++i) {
+              const int bg = 8 >> i;
+              if (full_groups - done >= bg) {
+#pragma unroll
+                for (int kb = 0; kb < 2; ++kb) {
+                  tma2d_store(map + i, colk + kb * 64, h.drow + done * 16, sk + kb * 16384 + done * 2048);
+                  tma2d_store(map + i, colv + kb * 64, h.drow + done * 16, sk + KV_BYTES + kb * 16384 + done * 2048);
+                }
+                done += bg;
               }
+            }
           }
           // ragged tail rows: one 16-B chunk per lane (K/V, 64-column block, chunk)
           const int kv = lane >> 4, kb = (lane >> 3) & 1, c = lane & 7;
@@ -681,13 +704,13 @@ EncodeTiledFn encoder() {
   return fn;
 }
 
-// 2-D bf16 map: `cols` elements per row, `rows` rows, `pitch` bytes; boxes of 64 x 16, 128B swizzle
-bool encode_2d(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint64_t pitch) {
+// 2-D bf16 map: `cols` elements per row, `rows` rows, `pitch` bytes; boxes of 64 x box_rows, 128B swizzle
+bool encode_2d(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint64_t pitch, uint32_t box_rows = 16) {
   EncodeTiledFn enc = encoder();
   if (!enc) return false;
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {pitch};
-  cuuint32_t box[2] = {64, 16};
+  cuuint32_t box[2] = {64, box_rows};
   cuuint32_t es[2] = {1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -717,26 +740,29 @@ cudaError_t launch_attn_tc(const Shape& sh, const uint16_t* q, uint16_t* arena, 
                            const Split* splits, const DepDesc* desc, unsigned long long* progress, uint32_t epoch,
                            int32_t* ctrl, int32_t B, int32_t l0, int32_t nl, int32_t grid_attn, int32_t grid_combine,
                            cudaStream_t st) {
-  CUtensorMap map_kv, map_q, map_stage;
-  if (!encode_2d(&map_kv, arena, (uint64_t)sh.row_elems, (uint64_t)arena_rows, (uint64_t)sh.kvpt))
-    return cudaErrorInvalidValue;
-  if (!encode_2d(&map_q, q, (uint64_t)sh.D, (uint64_t)nl * B * sh.H, (uint64_t)sh.D * 2)) return cudaErrorInvalidValue;
+  TcMaps maps;
   // staging rows (evicted slots' KV, token-major like the arena); without staging k_prep never fuses an eviction
   const int64_t stage_rows = staging ? staging_bytes / sh.kvpt : 0;
-  if (stage_rows > 0) {
-    if (!encode_2d(&map_stage, staging, (uint64_t)sh.row_elems, (uint64_t)stage_rows, (uint64_t)sh.kvpt))
+  for (int i = 0; i < NBOX; ++i) {
+    if (!encode_2d(&maps.kv[i], arena, (uint64_t)sh.row_elems, (uint64_t)arena_rows, (uint64_t)sh.kvpt, 128u >> i))
       return cudaErrorInvalidValue;
-  } else {
-    map_stage = map_kv;
+    if (stage_rows > 0) {
+      if (!encode_2d(&maps.stage[i], staging, (uint64_t)sh.row_elems, (uint64_t)stage_rows, (uint64_t)sh.kvpt,
+                     128u >> i))
+        return cudaErrorInvalidValue;
+    } else {
+      maps.stage[i] = maps.kv[i];
+    }
   }
+  if (!encode_2d(&maps.q, q, (uint64_t)sh.D, (uint64_t)nl * B * sh.H, (uint64_t)sh.D * 2)) return cudaErrorInvalidValue;
   TcArgs a;
   a.H = sh.H; a.Hkv = sh.Hkv; a.G = sh.H / sh.Hkv; a.B = B; a.l0 = l0; a.nl = nl;
   a.qscale = 1.4426950408889634f / sqrtf((float)sh.D);
   a.out = out; a.partials = partials; a.units = units; a.ctrl = ctrl;
   a.arena = reinterpret_cast<uint8_t*>(arena); a.staging = staging; a.kvpt = sh.kvpt;
   a.desc = desc; a.progress = progress; a.epoch = epoch;
-  if (a.G <= 8) k_attn_tc<8><<<grid_attn, 224, attn_tc_smem(), st>>>(map_kv, map_q, map_stage, a);
-  else k_attn_tc<16><<<grid_attn, 224, attn_tc_smem(), st>>>(map_kv, map_q, map_stage, a);
+  if (a.G <= 8) k_attn_tc<8><<<grid_attn, 224, attn_tc_smem(), st>>>(maps, a);
+  else k_attn_tc<16><<<grid_attn, 224, attn_tc_smem(), st>>>(maps, a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   return launch_combine(sh, splits, partials, out, ctrl, B, nl, grid_combine, st);
