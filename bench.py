@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--requests", type=int, default=REQ_PER_GPU, help="requests per GPU")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-chunks", type=int, default=0, help="H2D pipeline depth of the e2e leg (0 = 16)")
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--shape", default="gptj", choices=sorted(SHAPES))
     ap.add_argument("--arena-gb", type=float, default=0.0, help="cap the arena (e.g. for ncu replay)")
@@ -346,7 +347,7 @@ def run_s3(args):
     # ---- e2e through the public API with host buffers ----------------------
     e2e = None
     if not args.no_e2e and proxy is None:
-        e2e = e2e_leg(eng, exchange, dist, cdev, min(args.steps, 50), world)
+        e2e = e2e_leg(eng, exchange, dist, cdev, min(args.steps, 50), world, args.e2e_chunks)
 
     peak, peak_kind = load_peak()
     # the attention launches of fused steps also write the shifted / staged rows
@@ -509,47 +510,42 @@ def phase_breakdown(eng, exchange, world, steps):
     return {n: round(v / max(steps, 1), 4) for n, v in acc.items()}
 
 
-def e2e_leg(eng, exchange, dist, dev, steps, world):
-    """Same metric through S3Engine with HOST buffers: each step's q/k_new/
-    v_new/eos come from pinned host memory (H2D inside the timed region) and
-    the attention output goes back to pinned host memory (D2H inside)."""
+def e2e_leg(eng, exchange, dist, dev, steps, world, chunks=0):
+    """Same metric through the C ABI with HOST buffers (s3_decode_step_host):
+    each step's q/k_new/v_new/eos come from pinned host memory (H2D inside
+    the timed region, pipelined with the attention kernel in `chunks` batch
+    ranges) and the attention output is written to pinned host memory by the
+    kernels (D2H over PCIe inside the timed region)."""
     import torch
-    L, H, D = eng.L, eng.H, eng.D
+    L, H, D, Hkv = eng.L, eng.H, eng.D, eng.Hkv
     # pinned buffers sized for the batch this run actually reaches (+50 %)
-    n = L * min(eng.max_running, int(1.5 * max(eng.B, 1)) + 64) * H * D
-    hq = torch.empty(n, dtype=torch.bfloat16, pin_memory=True)
-    hk = torch.empty(n, dtype=torch.bfloat16, pin_memory=True)
-    hv = torch.empty(n, dtype=torch.bfloat16, pin_memory=True)
+    rows = min(eng.max_running, int(1.5 * max(eng.B, 1)) + 64)
+
+    def pin(rows):
+        return (torch.empty(L * rows * H * D, dtype=torch.bfloat16, pin_memory=True),
+                torch.empty(L * rows * Hkv * D, dtype=torch.bfloat16, pin_memory=True),
+                torch.empty(L * rows * Hkv * D, dtype=torch.bfloat16, pin_memory=True),
+                torch.empty(L * rows * H * D, dtype=torch.float32, pin_memory=True))
+    hq, hk, hv, ho = pin(rows)
     he = torch.empty(eng.max_running, dtype=torch.uint8, pin_memory=True)
-    ho = torch.empty(n, dtype=torch.float32, pin_memory=True)
     total_ms, tokens, h2d, d2h, done = 0.0, 0, 0, 0, 0
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     for _ in range(steps):
         B = eng.B
-        m = L * B * H * D
-        if m > n:                              # batch grew: re-pin (rare, outside the timed region)
-            n = int(1.5 * m)
-            hq = torch.empty(n, dtype=torch.bfloat16, pin_memory=True)
-            hk = torch.empty(n, dtype=torch.bfloat16, pin_memory=True)
-            hv = torch.empty(n, dtype=torch.bfloat16, pin_memory=True)
-            ho = torch.empty(n, dtype=torch.float32, pin_memory=True)
+        m, mk = L * B * H * D, L * B * Hkv * D
+        if B > rows:                           # batch grew: re-pin (rare, outside the timed region)
+            rows = min(eng.max_running, int(1.5 * B))
+            hq, hk, hv, ho = pin(rows)
         if B:
             eng.synth_inputs()                 # producer of this step's inputs (untimed)
-            hq[:m].copy_(eng.q[:m]); hk[:m].copy_(eng.k_new[:m]); hv[:m].copy_(eng.v_new[:m])
+            hq[:m].copy_(eng.q[:m]); hk[:mk].copy_(eng.k_new[:mk]); hv[:mk].copy_(eng.v_new[:mk])
             he[:B].copy_(eng.eos[:B])
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
         e0.record()
-        if B:
-            eng.q[:m].copy_(hq[:m], non_blocking=True)
-            eng.k_new[:m].copy_(hk[:m], non_blocking=True)
-            eng.v_new[:m].copy_(hv[:m], non_blocking=True)
-            eng.eos[:B].copy_(he[:B], non_blocking=True)
-        eng.decode()
-        if B:
-            ho[:m].copy_(eng.out[:m], non_blocking=True)
+        eng.decode_host(hq, hk, hv, he, ho, chunks=chunks)
         eng.evict_compact()
         if world == 1:
             eng.admit()
@@ -560,7 +556,7 @@ def e2e_leg(eng, exchange, dist, dev, steps, world):
         torch.cuda.synchronize()
         total_ms += e0.elapsed_time(e1)
         tokens += B
-        h2d += 3 * m * 2 + B
+        h2d += (m + 2 * mk) * 2 + B
         d2h += m * 4
         done += 1
     ms = total_ms
@@ -574,7 +570,8 @@ def e2e_leg(eng, exchange, dist, dev, steps, world):
         tok = int(tk.item())
     return {"value": tok / (ms / 1e3) if ms > 0 else 0.0, "unit": "tokens/s",
             "h2d_bytes_per_step": h2d // max(done, 1), "d2h_bytes_per_step": d2h // max(done, 1),
-            "steps": done}
+            "steps": done, "api": "s3_decode_step_host (C ABI, pinned host buffers)",
+            "chunks": chunks or 16}
 
 
 def main():

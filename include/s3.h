@@ -125,6 +125,34 @@ s3_status s3_submit(s3_ctx* ctx, const s3_request* reqs, int32_t n);
 s3_status s3_decode_step(s3_ctx* ctx, int32_t l0, int32_t nl, const void* q, const void* k_new,
                          const void* v_new, const uint8_t* eos, float* out);
 
+/* The same whole step (l0 = 0, nl = L) fed from HOST memory: the call a
+ * serving loop makes when the model's q / k_new / v_new / eos arrive from the
+ * host and the attention output goes back to it.
+ *   q, k_new, v_new, eos : pinned host (cudaHostAlloc / torch pin_memory),
+ *                          layouts as s3_decode_step with nl = L, read-only;
+ *   out                  : pinned host fp32 [L][B][H][D]; the attention
+ *                          kernels write it directly over PCIe (mapped
+ *                          pinned memory), so no separate D2H copy runs;
+ *   q_dev, k_new_dev, v_new_dev, eos_dev : caller-owned device landing
+ *                          buffers of the same sizes;
+ *   chunks               : H2D pipeline depth (0 = 16, at most 64).
+ * The H2D copies are split into `chunks` contiguous batch ranges on a copy
+ * stream; after each range lands a stream write sets a ready word that the
+ * attention kernel's producer waits on (acquire) before it touches that
+ * range, so the copies overlap the HBM stream of earlier ranges.  Where the
+ * attention variant cannot wait on ready words (attn_variant 1 / 2, or no
+ * stream-memory-operation support), the copies complete before the kernel.
+ * All buffers are in use until cfg.stream reaches the end of this call's
+ * work (synchronise cfg.stream before reading `out` or reusing inputs).
+ * S3_E_INVAL if a host pointer is not pinned or a landing buffer is NULL.  */
+typedef struct {
+  const void* q; const void* k_new; const void* v_new; const uint8_t* eos;
+  float* out;
+  void* q_dev; void* k_new_dev; void* v_new_dev; uint8_t* eos_dev;
+  int32_t chunks;
+} s3_host_io;
+s3_status s3_decode_step_host(s3_ctx* ctx, const s3_host_io* io);
+
 /* ---- (c)+(d): eviction + row-shift compaction ------------------------- */
 typedef struct {
   int64_t req_id;

@@ -25,6 +25,21 @@ using namespace s3;
 namespace {
 
 constexpr int64_t kAlign = 256;
+constexpr int32_t kMaxFeedChunks = 64;    // s3_decode_step_host pipeline depth limit
+
+// cuStreamWriteValue32 through the runtime's driver entry point (no -lcuda)
+typedef int (*WriteValue32Fn)(cudaStream_t, unsigned long long, unsigned int, unsigned int);
+WriteValue32Fn write_value32() {
+  static WriteValue32Fn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return (WriteValue32Fn) nullptr;
+    return (WriteValue32Fn)p;
+  }();
+  return fn;
+}
 inline int64_t align_up(int64_t x, int64_t a = kAlign) { return (x + a - 1) / a * a; }
 
 // FFD order: reservation (cap) descending, then req_id ascending (R7).
@@ -117,6 +132,12 @@ struct s3_ctx {
   uint32_t* flags = nullptr;
   uint8_t* report_dev = nullptr;
   unsigned long long* verify_count = nullptr;
+  // host-fed steps (s3_decode_step_host): copy stream, per-chunk ready words
+  uint32_t* ready = nullptr;
+  cudaStream_t hio = nullptr;
+  cudaEvent_t ev_hio_start = nullptr, ev_hio_done = nullptr;
+  uint32_t feed_epoch = 0;
+  Feed feed;                    // set only for the duration of a host-fed decode call
   // pinned host
   uint8_t* h_report = nullptr;
   uint8_t* h_upload = nullptr;
@@ -189,7 +210,8 @@ Shape make_shape(const s3_config* c) {
 }
 
 struct Carve {
-  int64_t slots, units, splits, partials, ctrl, ctrl64, entries, keys, desc, progress, flags, report, verify, total;
+  int64_t slots, units, splits, partials, ctrl, ctrl64, entries, keys, desc, progress, flags, report, verify, ready,
+      total;
 };
 
 Carve carve(const s3_config* c) {
@@ -215,6 +237,7 @@ Carve carve(const s3_config* c) {
   k.flags = o;    o += align_up(flags_max * 4);
   k.report = o;   o += align_up(report_bytes((int32_t)Bm));
   k.verify = o;   o += align_up(8);
+  k.ready = o;    o += align_up(kMaxFeedChunks * 4);
   k.total = o;
   return k;
 }
@@ -444,6 +467,8 @@ s3_status s3_kv_init(const s3_config* cfg, const s3_buffers* b, s3_ctx** out) {
   ctx->flags = reinterpret_cast<uint32_t*>(ws + k.flags);
   ctx->report_dev = ws + k.report;
   ctx->verify_count = reinterpret_cast<unsigned long long*>(ws + k.verify);
+  ctx->ready = reinterpret_cast<uint32_t*>(ws + k.ready);
+  if (cudaMemsetAsync(ws + k.ready, 0, kMaxFeedChunks * 4, ctx->st) != cudaSuccess) return bail("memset");
   if (cudaMemsetAsync(ws + k.ctrl, 0, CTRL_WORDS * 4, ctx->st) != cudaSuccess) return bail("memset");
   if (cudaMemsetAsync(ws + k.flags, 0, (size_t)(k.report - k.flags), ctx->st) != cudaSuccess) return bail("memset");
   if (cudaMemsetAsync(ws + k.progress, 0, (size_t)(k.flags - k.progress), ctx->st) != cudaSuccess) return bail("memset");
@@ -469,6 +494,9 @@ s3_status s3_kv_destroy(s3_ctx* ctx) {
   for (auto e : ctx->prof.free_events) cudaEventDestroy(e);
   ctx->deferred_free.clear();
   if (ctx->ev_report) cudaEventDestroy(ctx->ev_report);
+  if (ctx->hio) { cudaStreamSynchronize(ctx->hio); cudaStreamDestroy(ctx->hio); }
+  if (ctx->ev_hio_start) cudaEventDestroy(ctx->ev_hio_start);
+  if (ctx->ev_hio_done) cudaEventDestroy(ctx->ev_hio_done);
   if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->h_report) cudaFreeHost(ctx->h_report);
   if (ctx->h_upload) cudaFreeHost(ctx->h_upload);
@@ -552,7 +580,7 @@ s3_status s3_decode_step(s3_ctx* ctx, int32_t l0, int32_t nl, const void* q, con
       CK(launch_attn(ctx->sh, (const uint16_t*)q, (const uint16_t*)k_new, (const uint16_t*)v_new,
                      (uint16_t*)ctx->buf.arena, (uint8_t*)ctx->buf.staging, out, ctx->partials, ctx->units,
                      ctx->splits, ctx->desc, ctx->progress, ctx->attn_epoch, ctx->ctrl, B, l0, nl, ctx->grid_attn,
-                     ctx->grid_combine, ctx->cfg.attn_variant, ctx->st), "k_attn");
+                     ctx->grid_combine, ctx->cfg.attn_variant, ctx->feed, ctx->st), "k_attn");
     ctx->launches += 2;   // attention, combine
     if (ctx->prof.on) {
       cudaEventRecord(e1, ctx->st);
@@ -571,6 +599,72 @@ s3_status s3_decode_step(s3_ctx* ctx, int32_t l0, int32_t nl, const void* q, con
     ctx->tokens_total += B;
     ctx->status_pending = true;
   }
+  return S3_OK;
+}
+
+namespace {
+bool is_pinned_host(const void* p, void** dev_ptr = nullptr) {
+  cudaPointerAttributes at{};
+  if (!p || cudaPointerGetAttributes(&at, p) != cudaSuccess) { cudaGetLastError(); return false; }
+  if (at.type != cudaMemoryTypeHost) return false;
+  if (dev_ptr) *dev_ptr = at.devicePointer;
+  return at.devicePointer != nullptr;
+}
+}  // namespace
+
+s3_status s3_decode_step_host(s3_ctx* ctx, const s3_host_io* io) {
+  if (s3_status s = check_ctx(ctx)) return s;
+  if (!io) return fail(ctx, S3_E_INVAL, "decode_step_host: null io");
+  if (ctx->status_pending) return fail(ctx, S3_E_STATE, "decode_step: statuses not consumed");
+  const int32_t B = (int32_t)ctx->slots_h.size();
+  const int32_t L = ctx->sh.L;
+  if (B == 0) return s3_decode_step(ctx, 0, L, nullptr, nullptr, nullptr, nullptr, nullptr);
+  void* out_dev = nullptr;
+  if (!is_pinned_host(io->q) || !is_pinned_host(io->k_new) || !is_pinned_host(io->v_new) ||
+      !is_pinned_host(io->eos) || !is_pinned_host(io->out, &out_dev))
+    return fail(ctx, S3_E_INVAL, "decode_step_host: host buffers must be pinned");
+  if (!io->q_dev || !io->k_new_dev || !io->v_new_dev || !io->eos_dev)
+    return fail(ctx, S3_E_INVAL, "decode_step_host: null device landing buffer");
+  if (io->chunks < 0) return fail(ctx, S3_E_INVAL, "decode_step_host: chunks < 0");
+  if (!ctx->hio) {
+    CK(cudaStreamCreateWithFlags(&ctx->hio, cudaStreamNonBlocking), "copy stream");
+    CK(cudaEventCreateWithFlags(&ctx->ev_hio_start, cudaEventDisableTiming), "event");
+    CK(cudaEventCreateWithFlags(&ctx->ev_hio_done, cudaEventDisableTiming), "event");
+  }
+  // the detection in k_prep reads eos first: a tiny in-stream copy
+  CK(cudaMemcpyAsync(io->eos_dev, io->eos, (size_t)B, cudaMemcpyHostToDevice, ctx->st), "eos H2D");
+  // the landing buffers are free once the previous step's kernels (earlier on cfg.stream) are done
+  CK(cudaEventRecord(ctx->ev_hio_start, ctx->st), "event");
+  CK(cudaStreamWaitEvent(ctx->hio, ctx->ev_hio_start, 0), "wait");
+  WriteValue32Fn wv = write_value32();
+  const bool pipe = wv && ctx->cfg.attn_variant == 0 && attn_tma_stages(ctx->sh) >= 2;
+  int32_t nch = pipe ? std::min(io->chunks ? io->chunks : 16, kMaxFeedChunks) : 1;
+  nch = std::max(1, std::min(nch, B));
+  const int32_t cb = (B + nch - 1) / nch;
+  nch = (B + cb - 1) / cb;
+  const uint32_t epoch = ++ctx->feed_epoch;
+  const size_t wq = (size_t)ctx->sh.H * ctx->sh.D * 2, wk = (size_t)ctx->sh.Hkv * ctx->sh.D * 2;
+  for (int32_t c = 0; c < nch; ++c) {
+    const int32_t b0 = c * cb, nb = std::min(B, b0 + cb) - b0;
+    // [L][B][heads][D]: one strided copy per tensor covers slots [b0, b0+nb) of every layer
+    CK(cudaMemcpy2DAsync((uint8_t*)io->q_dev + b0 * wq, B * wq, (const uint8_t*)io->q + b0 * wq, B * wq, nb * wq,
+                         (size_t)L, cudaMemcpyHostToDevice, ctx->hio), "q H2D");
+    CK(cudaMemcpy2DAsync((uint8_t*)io->k_new_dev + b0 * wk, B * wk, (const uint8_t*)io->k_new + b0 * wk, B * wk,
+                         nb * wk, (size_t)L, cudaMemcpyHostToDevice, ctx->hio), "k_new H2D");
+    CK(cudaMemcpy2DAsync((uint8_t*)io->v_new_dev + b0 * wk, B * wk, (const uint8_t*)io->v_new + b0 * wk, B * wk,
+                         nb * wk, (size_t)L, cudaMemcpyHostToDevice, ctx->hio), "v_new H2D");
+    if (pipe && wv(ctx->hio, (unsigned long long)(uintptr_t)(ctx->ready + c), epoch, 0) != 0)
+      return fail(ctx, S3_E_CUDA, "decode_step_host: stream write");
+  }
+  CK(cudaEventRecord(ctx->ev_hio_done, ctx->hio), "event");
+  if (!pipe) CK(cudaStreamWaitEvent(ctx->st, ctx->ev_hio_done, 0), "wait");
+  if (pipe) { ctx->feed.ready = ctx->ready; ctx->feed.cb = cb; ctx->feed.epoch = epoch; }
+  const s3_status rc = s3_decode_step(ctx, 0, L, io->q_dev, io->k_new_dev, io->v_new_dev, io->eos_dev,
+                                      static_cast<float*>(out_dev));
+  ctx->feed = Feed{};
+  if (rc != S3_OK) return rc;
+  // completion of cfg.stream implies the copies are done too
+  CK(cudaStreamWaitEvent(ctx->st, ctx->ev_hio_done, 0), "wait");
   return S3_OK;
 }
 

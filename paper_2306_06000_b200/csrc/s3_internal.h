@@ -110,11 +110,19 @@ struct PrepArgs {
 cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st);
 cudaError_t launch_deps(const Unit* units, const int32_t* ctrl, DepDesc* desc, int32_t tc, int32_t grid,
                         cudaStream_t st);
+// Host-fed step (s3_decode_step_host): slot b's q / k_new / v_new have landed
+// once ready[b / cb] reaches epoch (written by the copy stream).  ready ==
+// nullptr: inputs are resident before the launch.
+struct Feed {
+  const uint32_t* ready = nullptr;
+  int32_t cb = 1;
+  uint32_t epoch = 0;
+};
 cudaError_t launch_attn(const Shape& sh, const uint16_t* q, const uint16_t* k_new, const uint16_t* v_new,
                         uint16_t* arena, uint8_t* staging, float* out, float* partials, const Unit* units,
                         const Split* splits, const DepDesc* desc, unsigned long long* progress, uint32_t epoch,
                         int32_t* ctrl, int32_t B, int32_t l0, int32_t nl, int32_t grid_attn, int32_t grid_combine,
-                        int32_t variant, cudaStream_t st);
+                        int32_t variant, const Feed& feed, cudaStream_t st);
 cudaError_t launch_keep_scan(const Shape& sh, const DSlot* cur, DSlot* next, int32_t B, int64_t S,
                              void* report, MoveEntry* entries, int32_t* key_chunk0, int32_t* key_src,
                              int64_t* ctrl64, int32_t compact_policy, int32_t pool_nonempty, cudaStream_t st);

@@ -40,6 +40,32 @@ __device__ __forceinline__ uint4 ld_plain(const void* p) {
                : "l"(p));
   return r;
 }
+// coherent (L2) load: for inputs that land while the kernel runs (host-fed step)
+__device__ __forceinline__ uint4 ld_cg(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p)
+               : "memory");
+  return r;
+}
+// Wait until a ready word written by the copy stream reaches `epoch`
+// (s3_decode_step_host).  A word that never arrives is a host bug: trap after
+// 20 s instead of hanging the device.
+__device__ __noinline__ void wait_ready(const uint32_t* p, uint32_t epoch) {
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    if ((int32_t)(v - epoch) >= 0) break;
+    __nanosleep(200);
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 20000000000ull) __trap();
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");   // the bulk copies that follow read the landed bytes
+}
 __device__ __forceinline__ void st_v4(void* p, uint4 v) {
   asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
                "r"(v.w)
@@ -382,6 +408,7 @@ struct AttnArgs {
   int32_t* ctrl;
   int32_t B, l0, nl;
   float qscale;
+  Feed feed;             // host-fed step: per-chunk ready words (s3_decode_step_host)
 };
 
 template <int D, int G>
@@ -982,6 +1009,7 @@ __global__ void __launch_bounds__(576, 1) k_attn_tma(AttnArgs a, int32_t ns) {
     // ------------------------------ producer ------------------------------
     if (lane == 0) {
       int k = 0;
+      int ready_max = -1;               // host-fed step: highest chunk known to have landed
       for (;;) {
         const int item = atomicAdd(&a.ctrl[CTRL_ITEM], 1);
         if (item >= total) {
@@ -993,6 +1021,11 @@ __global__ void __launch_bounds__(576, 1) k_attn_tma(AttnArgs a, int32_t ns) {
         }
         const int u = item / a.nl, li = item - u * a.nl;
         const Unit un = a.units[u];
+        if (a.feed.ready) {
+          // chunks land in order: waiting for this unit's chunk covers every earlier one
+          const int c = un.b / a.feed.cb;
+          if (c > ready_max) { wait_ready(a.feed.ready + c, a.feed.epoch); ready_max = c; }
+        }
         const uint8_t* base = arena + (int64_t)un.off * kvpt + (int64_t)(a.l0 + li) * rowB;
         const uint16_t* qsrc = a.q + ((int64_t)li * a.B + un.b) * HD;
         int r = un.r0, s = 0;
@@ -1124,8 +1157,13 @@ __global__ void __launch_bounds__(576, 1) k_attn_tma(AttnArgs a, int32_t ns) {
     uint4 kr = make_uint4(0, 0, 0, 0), vr = kr;
     const bool last_new = (h.flags & 2) && (h.flags & 4);
     if (last_new) {              // issue the new row's loads early; used after the stage
-      kr = ld_plain(a.k_new + iok);
-      vr = ld_plain(a.v_new + iok);
+      if (a.feed.ready) {        // landed during this kernel (ordered by the producer's acquire)
+        kr = ld_cg(a.k_new + iok);
+        vr = ld_cg(a.v_new + iok);
+      } else {
+        kr = ld_plain(a.k_new + iok);
+        vr = ld_plain(a.v_new + iok);
+      }
     }
     if (h.n > 0) {
       uint4 kc[AT_RPS], vc[AT_RPS];
@@ -1325,8 +1363,9 @@ cudaError_t launch_attn(const Shape& sh, const uint16_t* q, const uint16_t* k_ne
                         uint16_t* arena, uint8_t* staging, float* out, float* partials, const Unit* units,
                         const Split* splits, const DepDesc* desc, unsigned long long* progress, uint32_t epoch,
                         int32_t* ctrl, int32_t B, int32_t l0, int32_t nl, int32_t grid_attn, int32_t grid_combine,
-                        int32_t variant, cudaStream_t st) {
+                        int32_t variant, const Feed& feed, cudaStream_t st) {
   AttnArgs a;
+  a.feed = feed;
   a.sh = sh; a.q = q; a.k_new = k_new; a.v_new = v_new; a.arena = arena; a.staging = staging; a.out = out;
   a.partials = partials; a.units = units; a.desc = desc; a.progress = progress; a.epoch = epoch;
   a.ctrl = ctrl; a.B = B; a.l0 = l0; a.nl = nl;

@@ -80,6 +80,12 @@ class s3_profile(C.Structure):
                 ("d2h_bytes", C.c_double), ("h2d_ms", C.c_double), ("h2d_bytes", C.c_double)]
 
 
+class s3_host_io(C.Structure):
+    _fields_ = [("q", C.c_void_p), ("k_new", C.c_void_p), ("v_new", C.c_void_p), ("eos", C.c_void_p),
+                ("out", C.c_void_p), ("q_dev", C.c_void_p), ("k_new_dev", C.c_void_p),
+                ("v_new_dev", C.c_void_p), ("eos_dev", C.c_void_p), ("chunks", C.c_int32)]
+
+
 P = C.c_void_p
 _i32, _i64 = C.c_int32, C.c_int64
 _SIGS = {
@@ -89,6 +95,7 @@ _SIGS = {
     "s3_last_error": (C.c_char_p, [P]),
     "s3_submit": (C.c_int, [P, P, _i32]),
     "s3_decode_step": (C.c_int, [P, _i32, _i32, P, P, P, P, P]),
+    "s3_decode_step_host": (C.c_int, [P, P]),
     "s3_evict_compact": (C.c_int, [P, P, P, P, P]),
     "s3_evict_wait": (C.c_int, [P]),
     "s3_admit": (C.c_int, [P, P, P]),
@@ -173,6 +180,13 @@ def s3_submit(ctx, reqs):
 def s3_decode_step(ctx, l0, nl, q, k_new, v_new, eos, out):
     _check(lib().s3_decode_step(ctx, l0, nl, _ptr(q), _ptr(k_new), _ptr(v_new), _ptr(eos), _ptr(out)),
            "s3_decode_step", ctx)
+
+
+def s3_decode_step_host(ctx, q, k_new, v_new, eos, out, q_dev, k_new_dev, v_new_dev, eos_dev, chunks=0):
+    """q/k_new/v_new/eos/out: pinned host tensors; *_dev: device landing buffers."""
+    io = s3_host_io(_ptr(q), _ptr(k_new), _ptr(v_new), _ptr(eos), _ptr(out), _ptr(q_dev), _ptr(k_new_dev),
+                    _ptr(v_new_dev), _ptr(eos_dev), int(chunks))
+    _check(lib().s3_decode_step_host(ctx, C.byref(io)), "s3_decode_step_host", ctx)
 
 
 def s3_evict_compact(ctx, n_before: int):

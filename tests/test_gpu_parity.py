@@ -42,7 +42,7 @@ def u16(t: torch.Tensor) -> np.ndarray:
 
 def lockstep(trace, L, H, D, R, C=0, S=0, max_running=4096, staging=True, feed_oracle_inputs=False,
              max_steps=100000, check_arena=True, attn_variant=0, compact_mode=0, poison=False,
-             compact_policy=0, Hkv=0):
+             compact_policy=0, Hkv=0, host_io=False, chunks=0):
     from paper_2306_06000_b200.engine import S3Engine
     eng = S3Engine(L, H, D, trace.max_seq_len, R, max_running, chunk_rows=C, move_chunk_bytes=S,
                    staging_bytes=None if staging else 0, host_store_bytes=64 << 20, attn_variant=attn_variant,
@@ -58,6 +58,13 @@ def lockstep(trace, L, H, D, R, C=0, S=0, max_running=4096, staging=True, feed_o
     worst, steps, stats = 0.0, 0, dict(evictions=0, moved=0, splits=0)
     HD = H * D
     KD = (Hkv or H) * D
+    if host_io:
+        # s3_decode_step_host: pinned host inputs and output
+        hq = torch.empty(eng.q.numel(), dtype=torch.bfloat16, pin_memory=True)
+        hk = torch.empty(eng.k_new.numel(), dtype=torch.bfloat16, pin_memory=True)
+        hv = torch.empty(eng.v_new.numel(), dtype=torch.bfloat16, pin_memory=True)
+        he = torch.empty(eng.eos.numel(), dtype=torch.uint8, pin_memory=True)
+        ho = torch.empty(eng.out.numel(), dtype=torch.float32, pin_memory=True)
     while True:
         c = orc.counters()
         if orc.B == 0 and c[3] + c[4] == 0:
@@ -90,9 +97,22 @@ def lockstep(trace, L, H, D, R, C=0, S=0, max_running=4096, staging=True, feed_o
                 assert np.array_equal(u16(eng.v_new[:nk]), v.reshape(-1))
                 assert np.array_equal(eng.eos[:B].cpu().numpy(), eos)
         ref, st = orc.decode(q, k, v, eos)
-        eng.decode()
+        if host_io:
+            if B:
+                hq[:n].copy_(eng.q[:n]); hk[:nk].copy_(eng.k_new[:nk]); hv[:nk].copy_(eng.v_new[:nk])
+                he[:B].copy_(eng.eos[:B])
+                ho[:n].fill_(float("nan"))
+                # NaN-poison the landing buffers: a kernel that reads a chunk before
+                # its copy landed leaks NaN into out
+                eng.q.fill_(float("nan")); eng.k_new.fill_(float("nan")); eng.v_new.fill_(float("nan"))
+                eng.eos.fill_(0)
+            torch.cuda.synchronize()
+            eng.decode_host(hq, hk, hv, he, ho, chunks=chunks)
+            torch.cuda.synchronize()
+        else:
+            eng.decode()
         if B:
-            got = eng.out[:n].cpu().numpy().reshape(L, B, H, D).astype(np.float64)
+            got = (ho[:n] if host_io else eng.out[:n]).cpu().numpy().reshape(L, B, H, D).astype(np.float64)
             err = rel_err(got, ref)
             worst = max(worst, err)
             assert err <= TOL, f"step {steps}: attention rel err {err}"
@@ -430,3 +450,18 @@ def test_grouped_query_kv_tensor_cores(H, Hkv, C, policy, mode, staging):
         assert r["fused_steps"] >= 0.9 * r["steps"]   # unfused only when a step's evictions overflow staging
     if mode == 1:
         assert r["fused_steps"] == 0
+
+
+@pytest.mark.parametrize("variant,chunks,C", [(0, 0, 16), (0, 64, 0), (0, 3, 16), (1, 0, 16), (2, 0, 16)])
+def test_host_fed_decode_step(variant, chunks, C):
+    """s3_decode_step_host: pinned host q/k_new/v_new/eos in, pinned host out,
+    H2D pipelined with the attention kernel through per-chunk ready words
+    (TMA variant) or completed before it (other variants); device landing
+    buffers NaN-poisoned before every step."""
+    if variant == 2:
+        H, Hkv, D = 8, 2, 128
+    else:
+        H, Hkv, D = 4, 0, 64
+    t = s3synth.make_trace(48, seed=7, policy="short", p=0.3, max_seq_len=256, prompt_max=64)
+    r = lockstep(t, 2, H, D, 2048, C=C, host_io=True, chunks=chunks, attn_variant=variant, Hkv=Hkv)
+    assert r["steps"] > 20 and r["worst"] <= TOL
