@@ -531,6 +531,7 @@ def e2e_leg(eng, exchange, dist, dev, steps, world, chunks=0):
     total_ms, tokens, h2d, d2h, done = 0.0, 0, 0, 0, 0
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    eng.profile(True)                          # attention-kernel span inside the e2e step (explains it)
     for _ in range(steps):
         B = eng.B
         m, mk = L * B * H * D, L * B * Hkv * D
@@ -559,6 +560,8 @@ def e2e_leg(eng, exchange, dist, dev, steps, world, chunks=0):
         h2d += (m + 2 * mk) * 2 + B
         d2h += m * 4
         done += 1
+    prof = eng.profile_get()
+    eng.profile(False)
     ms = total_ms
     tok = tokens
     if dist:
@@ -571,7 +574,9 @@ def e2e_leg(eng, exchange, dist, dev, steps, world, chunks=0):
     return {"value": tok / (ms / 1e3) if ms > 0 else 0.0, "unit": "tokens/s",
             "h2d_bytes_per_step": h2d // max(done, 1), "d2h_bytes_per_step": d2h // max(done, 1),
             "steps": done, "api": "s3_decode_step_host (C ABI, pinned host buffers)",
-            "chunks": chunks or 16}
+            "chunks": chunks or 16, "ms_per_step": round(total_ms / max(done, 1), 3),
+            "attn_kernel_ms_per_step": round(prof.attn_ms / max(done, 1), 3),
+            "pcie_gbs": round((h2d + d2h) / max(total_ms, 1e-9) / 1e6, 2)}
 
 
 def main():
