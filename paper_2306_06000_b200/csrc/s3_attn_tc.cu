@@ -10,8 +10,14 @@
 // SM) four roles:
 //   producer warp : items (unit, layer, KV head) from the atomic queue; TMA
 //                   tensor loads (128B swizzle) of the tile's K and V rows in
-//                   16-row boxes (only the groups holding valid rows) and of
-//                   the group's q rows, into a 3-stage ring;
+//                   128/64/32/16-row boxes (only the groups holding valid
+//                   rows) and of the group's q rows, into a 3-stage ring.
+//                   Short units pack np = 2..NC/G KV heads into one tile,
+//                   one segment of 128/np rows per head: the q box already
+//                   holds those heads' np*G query rows, and the softmax masks
+//                   S^T block-diagonally (segment s meets only columns
+//                   [sG, (s+1)G)), so one MMA pair and one softmax pass serve
+//                   np heads;
 //   MMA warp      : one thread issues tcgen05.mma (kind::f16, M 128, N 16,
 //                   K 16 per instruction), commits to mbarriers;
 //   softmax warps : 4 warps = 128 TMEM lanes; lane j holds row j of S^T:
@@ -44,6 +50,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "s3_internal.h"
 
@@ -63,7 +70,8 @@ constexpr float LAZY_THR = 8.0f;            // rescale only if a score beats the
 constexpr int TMEM_COLS = 64;               // S0 [0,16), S1 [16,32), O0 [32,48), O1 [48,64)
 
 struct TcHdr {
-  int32_t item, r0, nvalid, flags;          // flags: 1 = first tile of the item, 2 = last
+  int32_t item, r0, nvalid, flags;          // flags: 1 = first tile of the item, 2 = last;
+                                            // bits 8..11: log2 np (KV heads packed in the tile)
   int32_t b, part, li, g;
   int32_t iseq, mode, drow;                 // iseq: per-CTA item sequence number (O buffer = iseq & 1)
   uint32_t prog;                            // read progress this tile completes (storer)
@@ -71,11 +79,13 @@ struct TcHdr {
 };
 static_assert(sizeof(TcHdr) % 16 == 0, "TcHdr.dep must stay 16-B aligned");
 constexpr uint32_t TC_PROG_FULL = 0x80000000u;
+// KV heads g..g+np-1 share the tile, one segment of TM / np rows each
+__device__ __forceinline__ int hdr_lognp(const TcHdr& h) { return (h.flags >> 8) & 15; }
 constexpr int TC_HEAD_STRIDE = 1 << 16;      // progress = head * 2^16 + rows (unit rows < 2^16)
 
-struct TcSmem {                             // after the ring and the two P buffers
-  uint64_t kv_full[NST], kv_empty[NST], s_full[2], s_empty[2], p_full, o_done, o_fin[2], o_free[2];
-  TcHdr hdr[NST];
+struct alignas(16) TcSmem {                 // after the ring and the two P buffers
+  uint64_t kv_full[NST], kv_empty[NST], s_full[2], s_empty[2], p_full[2], o_done, o_fin[2], o_free[2];
+  alignas(16) TcHdr hdr[NST];               // hdr.dep is a 16-B bulk-copy destination
   float red[2][4][NQ];
   int32_t flag[4];
   uint32_t tmem_base;
@@ -285,9 +295,12 @@ struct TcArgs {
   const DepDesc* desc;
   unsigned long long* progress;
   uint32_t epoch;
+  int32_t pmax;          // most KV heads one tile may pack (NC / G; 1 = no packing)
 };
 
-template <int NC>   // query columns the softmax handles: G padded to 8 or 16 (the MMA always has N = 16)
+// NC: query columns the softmax handles, G padded to 8 or 16 (the MMA always has N = 16);
+// PACK: short units may pack several KV heads into one tile (NC / G >= 2)
+template <int NC, bool PACK>
 __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMaps maps, TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-B alignment for the 128B-swizzle atoms, by pointer arithmetic so the
@@ -301,7 +314,7 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
   if (tid == 0) {
     for (int i = 0; i < NST; ++i) { mb_init(&S.kv_full[i], 1); mb_init(&S.kv_empty[i], fused ? 2 : 1); }
     for (int i = 0; i < 2; ++i) { mb_init(&S.s_full[i], 1); mb_init(&S.s_empty[i], 4); }
-    mb_init(&S.p_full, 4);
+    for (int i = 0; i < 2; ++i) mb_init(&S.p_full[i], 4);
     mb_init(&S.o_done, 1);
     for (int i = 0; i < 2; ++i) { mb_init(&S.o_fin[i], 1); mb_init(&S.o_free[i], 4); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -344,10 +357,14 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
         const bool mv = un.mode == UNIT_MOVE;
         // destination row of the unit's first row: arena row (MOVE) or staging row (STAGE)
         const int drow0 = (int)(mv ? un.dst : un.dst / a.kvpt) + un.r0;
-        for (int g = 0; g < a.Hkv; ++g, ++iseq) {
+        // short units: np KV heads share one 128-row tile, one segment of seg rows each
+        // (block-diagonal scores: segment s only meets query columns [s G, (s+1) G))
+        int np = 1;
+        if constexpr (PACK)
+          while (np * 2 <= a.pmax && nrows <= TM / (np * 2) && a.Hkv % (np * 2) == 0) np *= 2;
+        const int seg = TM / np;
+        for (int g = 0; g < a.Hkv; g += np, ++iseq) {
           const int item = w * a.Hkv + g;
-          const int colk = (a.l0 + li) * row_cols + g * DH;
-          const int colv = colk + a.Hkv * DH;
           const int qrow = (li * a.B + un.b) * a.H + g * a.G;
           for (int r = 0; r < nrows; r += TM) {
             const int st = t % NST;
@@ -358,27 +375,35 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
             h.flags = (r == 0 ? 1 : 0) | (r + TM >= nrows ? 2 : 0);
             h.b = un.b; h.part = un.part; h.li = li; h.g = g; h.iseq = iseq;
             h.mode = un.mode; h.drow = drow0 + r;
-            h.prog = (uint32_t)(g * TC_HEAD_STRIDE + r + nv) | (g == a.Hkv - 1 && r + TM >= nrows ? TC_PROG_FULL : 0u);
+            h.flags |= (31 - __clz(np)) << 8;
+            const int glast = g + np - 1;  // heads g..glast are read up to r + nv rows once this tile lands
+            h.prog = (uint32_t)(glast * TC_HEAD_STRIDE + r + nv) |
+                     (glast == a.Hkv - 1 && r + TM >= nrows ? TC_PROG_FULL : 0u);
             const int groups = (nv + 15) / 16;
             uint8_t* sk = smem + st * STAGE_BYTES;
             uint8_t* sv = sk + KV_BYTES;
             uint8_t* sq = sv + KV_BYTES;
             const bool dep = fused && mv;
-            mb_expect(&S.kv_full[st], (uint32_t)(groups * 16 * 128 * 2 * 2 + Q_BYTES + (dep ? 16 : 0)));
+            mb_expect(&S.kv_full[st], (uint32_t)(np * groups * 16 * 128 * 2 * 2 + Q_BYTES + (dep ? 16 : 0)));
             if (dep) bulk_g2s16(&h.dep, a.desc + un.stage_base + r / TM, &S.kv_full[st]);
             const int row0 = un.off + un.r0 + r;
-            int done = 0;                 // 16-row groups, largest boxes first
+            for (int sgi = 0; sgi < np; ++sgi) {
+              const int colk = (a.l0 + li) * row_cols + (g + sgi) * DH;
+              const int colv = colk + a.Hkv * DH;
+              const int sro = sgi * seg * 128;   // segment's first shared-memory row (bytes)
+              int done = 0;                 // 16-row groups, largest boxes first
 #pragma unroll
-            for (int i = 0; i < NBOX; ++i) {
-              const int bg = 8 >> i;
-              if (groups - done >= bg) {
-                const CUtensorMap* m = &maps.kv[i];
+              for (int i = 0; i < NBOX; ++i) {
+                const int bg = 8 >> i;
+                if (groups - done >= bg) {
+                  const CUtensorMap* m = &maps.kv[i];
 #pragma unroll
-                for (int kb = 0; kb < 2; ++kb) {
-                  tma2d(sk + kb * 16384 + done * 2048, m, colk + kb * 64, row0 + done * 16, &S.kv_full[st]);
-                  tma2d(sv + kb * 16384 + done * 2048, m, colv + kb * 64, row0 + done * 16, &S.kv_full[st]);
+                  for (int kb = 0; kb < 2; ++kb) {
+                    tma2d(sk + kb * 16384 + sro + done * 2048, m, colk + kb * 64, row0 + done * 16, &S.kv_full[st]);
+                    tma2d(sv + kb * 16384 + sro + done * 2048, m, colv + kb * 64, row0 + done * 16, &S.kv_full[st]);
+                  }
+                  done += bg;
                 }
-                done += bg;
               }
             }
 #pragma unroll
@@ -425,7 +450,9 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
           const int iseq = S.hdr[st].iseq, ob = iseq & 1;
           if (first)   // O buffer ob must have been read by the epilogue of item iseq - 2
             mb_wait(&S.o_free[ob], ((uint32_t)(iseq >> 1) & 1u) ^ 1u);
-          mb_wait(&S.p_full, (uint32_t)t & 1u);
+          // one barrier per P buffer: the softmax may hand over P(t+1) before this
+          // wait for P(t) runs, and a single barrier would then be two phases ahead
+          mb_wait(&S.p_full[t & 1], (uint32_t)(t >> 1) & 1u);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint8_t* sv = smem + st * STAGE_BYTES + KV_BYTES;
           const uint8_t* sp = pbuf + (t & 1) * PBUF_BYTES;
@@ -458,7 +485,8 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
           // the tile's rows are in shared memory: its source rows may be overwritten
           st_rlx_u64(a.progress + w, ((unsigned long long)a.epoch << 32) | h.prog);
           if (h.mode == UNIT_MOVE && h.dep.ua >= 0) {
-            const uint32_t gbase = (uint32_t)(h.g * TC_HEAD_STRIDE);
+            // the tile overwrites heads g..g+np-1 of its destination rows
+            const uint32_t gbase = (uint32_t)((h.g + (PACK ? 1 << hdr_lognp(h) : 1) - 1) * TC_HEAD_STRIDE);
             for (int v = h.dep.ua; v <= h.dep.ub; ++v) {
               const int need = v == h.dep.ua ? h.dep.need_a : (v == h.dep.ub ? h.dep.need_b : -1);
               const int it = v * a.nl + h.li;
@@ -476,35 +504,39 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
         __syncwarp();
         const bool stores = (h.mode == UNIT_MOVE || h.mode == UNIT_STAGE) && h.nvalid > 0;
         if (stores) {
-          const uint8_t* sk = smem + st * STAGE_BYTES;
-          const int colk = (a.l0 + h.li) * 2 * a.Hkv * DH + h.g * DH;   // elements
-          const int colv = colk + a.Hkv * DH;
           const int full_groups = h.nvalid >> 4;
-          if (lane == 0) {
-            asm volatile("fence.proxy.async.global;" ::: "memory");
-            const CUtensorMap* map = h.mode == UNIT_MOVE ? maps.kv : maps.stage;
-            int done = 0;
+          if (lane == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
+          const int np = PACK ? 1 << hdr_lognp(h) : 1;
+          for (int sgi = 0; sgi < np; ++sgi) {       // one segment per packed KV head
+            const uint8_t* sk = smem + st * STAGE_BYTES + sgi * (TM / np) * 128;
+            const int colk = (a.l0 + h.li) * 2 * a.Hkv * DH + (h.g + sgi) * DH;   // elements
+            const int colv = colk + a.Hkv * DH;
+            if (lane == 0) {
+              const CUtensorMap* map = h.mode == UNIT_MOVE ? maps.kv : maps.stage;
+              int done = 0;
 #pragma unroll
-            for (int i = 0; i < NBOX; ++i) {
-              const int bg = 8 >> i;
-              if (full_groups - done >= bg) {
+              for (int i = 0; i < NBOX; ++i) {
+                const int bg = 8 >> i;
+                if (full_groups - done >= bg) {
 #pragma unroll
-                for (int kb = 0; kb < 2; ++kb) {
-                  tma2d_store(map + i, colk + kb * 64, h.drow + done * 16, sk + kb * 16384 + done * 2048);
-                  tma2d_store(map + i, colv + kb * 64, h.drow + done * 16, sk + KV_BYTES + kb * 16384 + done * 2048);
+                  for (int kb = 0; kb < 2; ++kb) {
+                    tma2d_store(map + i, colk + kb * 64, h.drow + done * 16, sk + kb * 16384 + done * 2048);
+                    tma2d_store(map + i, colv + kb * 64, h.drow + done * 16, sk + KV_BYTES + kb * 16384 + done * 2048);
+                  }
+                  done += bg;
                 }
-                done += bg;
               }
             }
-          }
-          // ragged tail rows: one 16-B chunk per lane (K/V, 64-column block, chunk)
-          const int kv = lane >> 4, kb = (lane >> 3) & 1, c = lane & 7;
-          uint8_t* gbase = (h.mode == UNIT_MOVE ? a.arena : a.staging) +
-                           (int64_t)(kv ? colv : colk) * 2 + kb * 128 + c * 16;
-          for (int row = full_groups * 16; row < h.nvalid; ++row) {
-            const uint4 x = *reinterpret_cast<const uint4*>(sk + kv * KV_BYTES + kb * 16384 + row * 128 +
-                                                            ((c ^ (row & 7)) << 4));
-            *reinterpret_cast<uint4*>(gbase + (int64_t)(h.drow + row) * a.kvpt) = x;
+            // ragged tail rows: one 16-B chunk per lane (K/V, 64-column block, chunk); segments
+            // start on 16-row boundaries, so the swizzle phase is the row's own
+            const int kv = lane >> 4, kb = (lane >> 3) & 1, c = lane & 7;
+            uint8_t* gbase = (h.mode == UNIT_MOVE ? a.arena : a.staging) +
+                             (int64_t)(kv ? colv : colk) * 2 + kb * 128 + c * 16;
+            for (int row = full_groups * 16; row < h.nvalid; ++row) {
+              const uint4 x = *reinterpret_cast<const uint4*>(sk + kv * KV_BYTES + kb * 16384 + row * 128 +
+                                                              ((c ^ (row & 7)) << 4));
+              *reinterpret_cast<uint4*>(gbase + (int64_t)(h.drow + row) * a.kvpt) = x;
+            }
           }
           __syncwarp();
         }
@@ -558,8 +590,8 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
       const int d = row;
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
-        if (c >= a.G) break;
-        const int hq = ph.g * a.G + c;
+        if (c >= (PACK ? a.G << hdr_lognp(ph) : a.G)) break;
+        const int hq = ph.g * a.G + c;            // packed heads: column c belongs to KV head g + c / G
         if (ph.part < 0) {
           a.out[((int64_t)(ph.li * a.B + ph.b) * a.H + hq) * DH + d] = o[c] / pl[c];
         } else {
@@ -582,10 +614,25 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
       __syncwarp();
       if (lane == 0) mb_arrive(&S.s_empty[sb]);
       const bool first = h.flags & 1;
-      const bool valid = row < h.nvalid;
-      const int ob = h.iseq & 1;
+      int rs = row;                                   // this lane's row inside its segment
+      bool valid;
+      const int lognp = PACK ? hdr_lognp(h) : 0;
+      if (!PACK || lognp == 0) {                               // warp-uniform: one KV head per tile
+        valid = row < h.nvalid;
 #pragma unroll
-      for (int c = 0; c < NC; ++c) s[c] = valid ? s[c] * a.qscale : -INFINITY;
+        for (int c = 0; c < NC; ++c) s[c] = valid ? s[c] * a.qscale : -INFINITY;
+      } else {
+        // block-diagonal mask of packed tiles: segment sgm only meets columns
+        // [sgm G, (sgm+1) G); columns past np G stay unmasked (finite, never written out)
+        const int sgm = row >> (7 - lognp);           // segments of TM >> lognp rows
+        rs = row - (sgm << (7 - lognp));
+        valid = rs < h.nvalid;
+        const int cg0 = sgm * a.G, cg1 = cg0 + a.G, cpad = a.G << lognp;
+#pragma unroll
+        for (int c = 0; c < NC; ++c)
+          s[c] = (valid && ((c >= cg0 && c < cg1) || c >= cpad)) ? s[c] * a.qscale : -INFINITY;
+      }
+      const int ob = h.iseq & 1;
       // does any score need a larger running max?
       bool need = first;
       if (!first) {
@@ -628,7 +675,7 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
         *reinterpret_cast<__nv_bfloat16*>(sp + sw) = hi;
         *reinterpret_cast<__nv_bfloat16*>(sp + P_BYTES + sw) = lo;
       }
-      if (!valid && row < ((h.nvalid + 15) & ~15)) { // loaded rows past the slot's resident rows: V := 0
+      if (!valid && rs < ((h.nvalid + 15) & ~15)) {  // loaded rows past the slot's resident rows: V := 0
         uint8_t* sv = smem + (t % NST) * STAGE_BYTES + KV_BYTES;
 #pragma unroll
         for (int kb = 0; kb < 2; ++kb)
@@ -648,7 +695,7 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mb_arrive(&S.p_full);
+      if (lane == 0) mb_arrive(&S.p_full[t & 1]);
       if (pend) epilogue();                         // the previous item, overlapped with this tile's MMA
       if (h.flags & 2) {
         pend = true;
@@ -720,7 +767,10 @@ bool encode_2d(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, u
 }  // namespace
 
 int attn_tc_smem() { return NST * STAGE_BYTES + 2 * PBUF_BYTES + (int)sizeof(TcSmem) + 1024; }
-const void* attn_tc_kernel_ptr(int nc) { return nc == 8 ? (const void*)k_attn_tc<8> : (const void*)k_attn_tc<16>; }
+const void* attn_tc_kernel_ptr(int nc, bool pack) {
+  if (nc == 8) return pack ? (const void*)k_attn_tc<8, true> : (const void*)k_attn_tc<8, false>;
+  return pack ? (const void*)k_attn_tc<16, true> : (const void*)k_attn_tc<16, false>;
+}
 
 bool attn_tc_supported(const Shape& sh) {
   const int G = sh.Hkv > 0 ? sh.H / sh.Hkv : 0;
@@ -761,8 +811,17 @@ cudaError_t launch_attn_tc(const Shape& sh, const uint16_t* q, uint16_t* arena, 
   a.out = out; a.partials = partials; a.units = units; a.ctrl = ctrl;
   a.arena = reinterpret_cast<uint8_t*>(arena); a.staging = staging; a.kvpt = sh.kvpt;
   a.desc = desc; a.progress = progress; a.epoch = epoch;
-  if (a.G <= 8) k_attn_tc<8><<<grid_attn, 224, attn_tc_smem(), st>>>(maps, a);
-  else k_attn_tc<16><<<grid_attn, 224, attn_tc_smem(), st>>>(maps, a);
+  static const int pack = [] { const char* e = getenv("S3_TC_PACK"); return e ? atoi(e) : 1; }();
+  a.pmax = pack ? (a.G <= 8 ? 8 : 16) / a.G : 1;   // S3_TC_PACK=0: one KV head per tile (A/B)
+  const dim3 grid(grid_attn), block(224);
+  const int smem = attn_tc_smem();
+  if (a.G <= 8) {
+    if (a.pmax > 1) k_attn_tc<8, true><<<grid, block, smem, st>>>(maps, a);
+    else k_attn_tc<8, false><<<grid, block, smem, st>>>(maps, a);
+  } else {
+    if (a.pmax > 1) k_attn_tc<16, true><<<grid, block, smem, st>>>(maps, a);
+    else k_attn_tc<16, false><<<grid, block, smem, st>>>(maps, a);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   return launch_combine(sh, splits, partials, out, ctrl, B, nl, grid_combine, st);

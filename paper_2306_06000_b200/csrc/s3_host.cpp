@@ -435,9 +435,10 @@ s3_status s3_kv_init(const s3_config* cfg, const s3_buffers* b, s3_ctx** out) {
   if (cfg->attn_variant == 2) {
     if (!attn_tc_supported(sh)) return bail("attn_variant 2 needs head_dim 128 and 2..16 query heads per KV head");
     for (int nc : {8, 16})
-      if (cudaFuncSetAttribute(attn_tc_kernel_ptr(nc), cudaFuncAttributeMaxDynamicSharedMemorySize, attn_tc_smem()) !=
-          cudaSuccess)
-        return bail("attn_tc smem attribute");
+      for (bool pack : {false, true})
+        if (cudaFuncSetAttribute(attn_tc_kernel_ptr(nc, pack), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 attn_tc_smem()) != cudaSuccess)
+          return bail("attn_tc smem attribute");
     ctx->grid_attn = ctx->num_sms;
   }
   if (cfg->attn_variant == 0 && attn_tma_stages(sh) >= 2) {

@@ -35,7 +35,11 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--case", default=None, help="run only cases whose name contains this")
+    ap.add_argument("--lib", default=None, help="A/B: load this libs3.so build instead of the in-tree one")
     args = ap.parse_args()
+    if args.lib:
+        from paper_2306_06000_b200 import s3 as abi
+        abi.LIB_PATH = os.path.abspath(args.lib)
     peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] \
         if os.path.exists(os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
     for case in CASES:
