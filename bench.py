@@ -101,6 +101,16 @@ def traffic_from_profiles(key):
         return None
 
 
+def read_ceiling():
+    """Pure-streaming HBM rates measured by tools/hbm_probe on this pool's
+    B200 (context for `peak`, which is the driver's copy figure)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_hbm_probe.json")) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
 class ClockSampler:
     def __init__(self, index):
         self.index = index
@@ -407,6 +417,7 @@ def run_s3(args):
                 "attention_bytes_per_launch": prof.attn_bytes / max(prof.attn_launches, 1),
                 "fused_shift_bytes_per_launch": prof.fused_move_bytes / max(prof.attn_launches, 1),
                 "share_of_step": prof.attn_ms / ms,
+                "context": _ceiling_context(attn_gbs),
             },
             "evict_compact": {
                 "mode": args.compact, "fused_steps": prof.fused_steps, "fused_move_bytes": prof.fused_move_bytes,
@@ -440,6 +451,16 @@ def run_s3(args):
     eng.close()
     if dist:
         dist.destroy_process_group()
+
+
+def _ceiling_context(achieved):
+    c = read_ceiling()
+    if not c:
+        return None
+    return {"read_stream_gbs": c.get("read_ld_gbs"), "read_bulk_gbs": c.get("read_bulk_gbs"),
+            "mix_read5_write1_gbs": c.get("mix_read5_write1_gbs"),
+            "frac_of_read_stream": round(achieved / c["read_ld_gbs"], 4) if c.get("read_ld_gbs") else None,
+            "source": "profiles/r01_hbm_probe.json (tools/hbm_probe, 4 GiB streams, best of 10)"}
 
 
 def model_step(eng, proxy, exchange, world):

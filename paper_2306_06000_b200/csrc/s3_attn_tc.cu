@@ -683,8 +683,10 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
           for (int ch = 0; ch < 8; ++ch)
             *reinterpret_cast<uint4*>(sv + kb * 16384 + row * 128 + ch * 16) = make_uint4(0, 0, 0, 0);
       }
+      // every phase of o_done is waited (O^T(t-1) done; it is almost always complete by now),
+      // so no completion goes unobserved -- needed before a rescale, harmless otherwise
+      if (t > 0) mb_wait(&S.o_done, (uint32_t)(t - 1) & 1u);
       if (rescale) {                                // O^T *= corr once the previous tile's MMA is done
-        mb_wait(&S.o_done, (uint32_t)(t - 1) & 1u);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         float o[NC];
         tmem_ld<NC>(lane_base + 32 + 16 * ob, o);

@@ -1273,33 +1273,29 @@ __global__ void __launch_bounds__(256) k_synth(Shape sh, uint64_t seed, const DS
                                                int32_t B, int32_t l0, int32_t nl,
                                                const int32_t* __restrict__ out_len, int64_t n_req,
                                                uint16_t* q, uint16_t* k, uint16_t* v, uint8_t* eos) {
+  // one (layer, slot) row per block iteration; 32-bit index math inside the row
   const int D8 = sh.D / 8;
-  const int64_t tq = (int64_t)nl * B * sh.H * D8;     // q: [nl][B][H][D]
-  const int64_t tk = (int64_t)nl * B * sh.Hkv * D8;   // k_new, v_new: [nl][B][Hkv][D]
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tq + tk;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const bool isq = i < tq;
-    const int64_t j = isq ? i : i - tq;
-    const int nh = isq ? sh.H : sh.Hkv;
-    int64_t r = j;
-    const int d8 = (int)(r % D8); r /= D8;
-    const int h = (int)(r % nh); r /= nh;
-    const int b = (int)(r % B);
-    const int li = (int)(r / B);
+  const int nq = sh.H * D8, nk = sh.Hkv * D8;          // 16-B vectors per row of q / of k_new, v_new
+  for (int64_t row = blockIdx.x; row < (int64_t)nl * B; row += gridDim.x) {
+    const int li = (int)(row / B), b = (int)(row - (int64_t)li * B);
     const DSlot sl = slots[b];
     const int l = l0 + li;
-    const int64_t o = j * 8;
-    if (isq) {
-      st_v4(q + o, gen8(sh, seed, 1, sl.req, l, 0, sl.len, h, d8, 1.f / 32.f));
-    } else {
-      st_v4(k + o, gen8(sh, seed, 0, sl.req, l, 0, sl.len, h, d8, 1.f / 128.f));
-      st_v4(v + o, gen8(sh, seed, 0, sl.req, l, 1, sl.len, h, d8, 1.f / 128.f));
+    for (int t = threadIdx.x; t < nq + nk; t += blockDim.x) {
+      if (t < nq) {                                     // q: [nl][B][H][D]
+        const int h = t / D8, d8 = t - h * D8;
+        st_v4(q + (row * nq + t) * 8, gen8(sh, seed, 1, sl.req, l, 0, sl.len, h, d8, 1.f / 32.f));
+      } else {                                          // k_new, v_new: [nl][B][Hkv][D]
+        const int u = t - nq, h = u / D8, d8 = u - h * D8;
+        const int64_t o = (row * nk + u) * 8;
+        st_v4(k + o, gen8(sh, seed, 0, sl.req, l, 0, sl.len, h, d8, 1.f / 128.f));
+        st_v4(v + o, gen8(sh, seed, 0, sl.req, l, 1, sl.len, h, d8, 1.f / 128.f));
+      }
     }
-    if (i < B) {
-      const DSlot s2 = slots[i];
-      const int O = (s2.req >= 0 && s2.req < n_req) ? out_len[s2.req] : 0x7fffffff;
-      eos[i] = (uint8_t)(s2.gen + 1 == O);
-    }
+  }
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < B; i += gridDim.x * blockDim.x) {
+    const DSlot s2 = slots[i];
+    const int O = (s2.req >= 0 && s2.req < n_req) ? out_len[s2.req] : 0x7fffffff;
+    eos[i] = (uint8_t)(s2.gen + 1 == O);
   }
 }
 
@@ -1440,8 +1436,7 @@ cudaError_t launch_synth(const Shape& sh, uint64_t seed, const DSlot* slots, int
                          int32_t nl, const int32_t* out_len_by_req, int64_t n_req, uint16_t* q,
                          uint16_t* k, uint16_t* v, uint8_t* eos, cudaStream_t st) {
   if (B <= 0) return cudaSuccess;
-  const int64_t total = (int64_t)nl * B * (sh.H + sh.Hkv) * (sh.D / 8);
-  const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 16);
+  const int64_t blocks = std::min<int64_t>((int64_t)nl * B, 148 * 16);
   k_synth<<<(int)blocks, 256, 0, st>>>(sh, seed, slots, B, l0, nl, out_len_by_req, n_req, q, k, v, eos);
   return cudaGetLastError();
 }
