@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-chunks", type=int, default=0, help="H2D pipeline depth of the e2e leg (0 = 16)")
+    ap.add_argument("--e2e-mapped-out", action="store_true",
+                    help="e2e: kernels store out to mapped host memory instead of per-chunk D2H copies")
     ap.add_argument("--seed", type=int, default=1)
     ap.add_argument("--shape", default="gptj", choices=sorted(SHAPES))
     ap.add_argument("--arena-gb", type=float, default=0.0, help="cap the arena (e.g. for ncu replay)")
@@ -357,7 +359,7 @@ def run_s3(args):
     # ---- e2e through the public API with host buffers ----------------------
     e2e = None
     if not args.no_e2e and proxy is None:
-        e2e = e2e_leg(eng, exchange, dist, cdev, min(args.steps, 50), world, args.e2e_chunks)
+        e2e = e2e_leg(eng, exchange, dist, cdev, min(args.steps, 50), world, args.e2e_chunks, not args.e2e_mapped_out)
 
     peak, peak_kind = load_peak()
     # the attention launches of fused steps also write the shifted / staged rows
@@ -531,7 +533,7 @@ def phase_breakdown(eng, exchange, world, steps):
     return {n: round(v / max(steps, 1), 4) for n, v in acc.items()}
 
 
-def e2e_leg(eng, exchange, dist, dev, steps, world, chunks=0):
+def e2e_leg(eng, exchange, dist, dev, steps, world, chunks=0, device_out=True):
     """Same metric through the C ABI with HOST buffers (s3_decode_step_host):
     each step's q/k_new/v_new/eos come from pinned host memory (H2D inside
     the timed region, pipelined with the attention kernel in `chunks` batch
@@ -567,7 +569,7 @@ def e2e_leg(eng, exchange, dist, dev, steps, world, chunks=0):
         if dist:
             dist.barrier()
         e0.record()
-        eng.decode_host(hq, hk, hv, he, ho, chunks=chunks)
+        eng.decode_host(hq, hk, hv, he, ho, chunks=chunks, device_out=device_out)
         eng.evict_compact()
         if world == 1:
             eng.admit()
@@ -595,7 +597,8 @@ def e2e_leg(eng, exchange, dist, dev, steps, world, chunks=0):
     return {"value": tok / (ms / 1e3) if ms > 0 else 0.0, "unit": "tokens/s",
             "h2d_bytes_per_step": h2d // max(done, 1), "d2h_bytes_per_step": d2h // max(done, 1),
             "steps": done, "api": "s3_decode_step_host (C ABI, pinned host buffers)",
-            "chunks": chunks or 16, "ms_per_step": round(total_ms / max(done, 1), 3),
+            "chunks": chunks or 16, "out_path": "device out + per-chunk D2H" if device_out else "kernel stores to mapped host",
+            "ms_per_step": round(total_ms / max(done, 1), 3),
             "attn_kernel_ms_per_step": round(prof.attn_ms / max(done, 1), 3),
             "pcie_gbs": round((h2d + d2h) / max(total_ms, 1e-9) / 1e6, 2)}
 

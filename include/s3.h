@@ -130,11 +130,18 @@ s3_status s3_decode_step(s3_ctx* ctx, int32_t l0, int32_t nl, const void* q, con
  * host and the attention output goes back to it.
  *   q, k_new, v_new, eos : pinned host (cudaHostAlloc / torch pin_memory),
  *                          layouts as s3_decode_step with nl = L, read-only;
- *   out                  : pinned host fp32 [L][B][H][D]; the attention
- *                          kernels write it directly over PCIe (mapped
- *                          pinned memory), so no separate D2H copy runs;
+ *   out                  : pinned host fp32 [L][B][H][D];
  *   q_dev, k_new_dev, v_new_dev, eos_dev : caller-owned device landing
  *                          buffers of the same sizes;
+ *   out_dev              : device fp32 [L][B][H][D] or NULL.  Given, the
+ *                          kernels write out_dev and a second copy stream
+ *                          moves each finished batch range to `out` (the
+ *                          attention warps bump a per-range counter with a
+ *                          release add; the stream waits on it with
+ *                          cuStreamWaitValue32, so D2H overlaps the kernel;
+ *                          split-K slots follow k_combine).  NULL: the
+ *                          kernels store `out` directly over PCIe (mapped
+ *                          pinned memory);
  *   chunks               : H2D pipeline depth (0 = 16, at most 64).
  * The H2D copies are split into `chunks` contiguous batch ranges on a copy
  * stream; after each range lands a stream write sets a ready word that the
@@ -150,6 +157,7 @@ typedef struct {
   float* out;
   void* q_dev; void* k_new_dev; void* v_new_dev; uint8_t* eos_dev;
   int32_t chunks;
+  float* out_dev;
 } s3_host_io;
 s3_status s3_decode_step_host(s3_ctx* ctx, const s3_host_io* io);
 

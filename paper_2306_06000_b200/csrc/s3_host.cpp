@@ -28,18 +28,24 @@ constexpr int64_t kAlign = 256;
 constexpr int32_t kMaxFeedChunks = 64;    // s3_decode_step_host pipeline depth limit
 
 // cuStreamWriteValue32 through the runtime's driver entry point (no -lcuda)
-typedef int (*WriteValue32Fn)(cudaStream_t, unsigned long long, unsigned int, unsigned int);
-WriteValue32Fn write_value32() {
-  static WriteValue32Fn fn = [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess)
-      return (WriteValue32Fn) nullptr;
-    return (WriteValue32Fn)p;
-  }();
+// cuStreamWriteValue32 / cuStreamWaitValue32 (same signature)
+typedef int (*StreamValue32Fn)(cudaStream_t, unsigned long long, unsigned int, unsigned int);
+StreamValue32Fn driver_fn(const char* name) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+    return nullptr;
+  return (StreamValue32Fn)p;
+}
+StreamValue32Fn write_value32() {
+  static StreamValue32Fn fn = driver_fn("cuStreamWriteValue32");
   return fn;
 }
+StreamValue32Fn wait_value32() {
+  static StreamValue32Fn fn = driver_fn("cuStreamWaitValue32");
+  return fn;
+}
+constexpr unsigned kWaitGeq = 0x0;   // CU_STREAM_WAIT_VALUE_GEQ: (int32_t)(*addr - value) >= 0
 inline int64_t align_up(int64_t x, int64_t a = kAlign) { return (x + a - 1) / a * a; }
 
 // FFD order: reservation (cap) descending, then req_id ascending (R7).
@@ -134,8 +140,10 @@ struct s3_ctx {
   unsigned long long* verify_count = nullptr;
   // host-fed steps (s3_decode_step_host): copy stream, per-chunk ready words
   uint32_t* ready = nullptr;
-  cudaStream_t hio = nullptr;
-  cudaEvent_t ev_hio_start = nullptr, ev_hio_done = nullptr;
+  uint32_t* done = nullptr;                 // per-chunk finished-warp counters (device out + CE D2H)
+  uint32_t done_target[kMaxFeedChunks] = {};  // cumulative values the D2H stream waits for
+  cudaStream_t hio = nullptr, d2h = nullptr;
+  cudaEvent_t ev_hio_start = nullptr, ev_hio_done = nullptr, ev_comb = nullptr, ev_d2h_done = nullptr;
   uint32_t feed_epoch = 0;
   Feed feed;                    // set only for the duration of a host-fed decode call
   // pinned host
@@ -211,7 +219,7 @@ Shape make_shape(const s3_config* c) {
 
 struct Carve {
   int64_t slots, units, splits, partials, ctrl, ctrl64, entries, keys, desc, progress, flags, report, verify, ready,
-      total;
+      done, total;
 };
 
 Carve carve(const s3_config* c) {
@@ -238,6 +246,7 @@ Carve carve(const s3_config* c) {
   k.report = o;   o += align_up(report_bytes((int32_t)Bm));
   k.verify = o;   o += align_up(8);
   k.ready = o;    o += align_up(kMaxFeedChunks * 4);
+  k.done = o;     o += align_up(kMaxFeedChunks * 4);
   k.total = o;
   return k;
 }
@@ -469,7 +478,8 @@ s3_status s3_kv_init(const s3_config* cfg, const s3_buffers* b, s3_ctx** out) {
   ctx->report_dev = ws + k.report;
   ctx->verify_count = reinterpret_cast<unsigned long long*>(ws + k.verify);
   ctx->ready = reinterpret_cast<uint32_t*>(ws + k.ready);
-  if (cudaMemsetAsync(ws + k.ready, 0, kMaxFeedChunks * 4, ctx->st) != cudaSuccess) return bail("memset");
+  ctx->done = reinterpret_cast<uint32_t*>(ws + k.done);
+  if (cudaMemsetAsync(ws + k.ready, 0, (size_t)(k.total - k.ready), ctx->st) != cudaSuccess) return bail("memset");
   if (cudaMemsetAsync(ws + k.ctrl, 0, CTRL_WORDS * 4, ctx->st) != cudaSuccess) return bail("memset");
   if (cudaMemsetAsync(ws + k.flags, 0, (size_t)(k.report - k.flags), ctx->st) != cudaSuccess) return bail("memset");
   if (cudaMemsetAsync(ws + k.progress, 0, (size_t)(k.flags - k.progress), ctx->st) != cudaSuccess) return bail("memset");
@@ -496,6 +506,9 @@ s3_status s3_kv_destroy(s3_ctx* ctx) {
   ctx->deferred_free.clear();
   if (ctx->ev_report) cudaEventDestroy(ctx->ev_report);
   if (ctx->hio) { cudaStreamSynchronize(ctx->hio); cudaStreamDestroy(ctx->hio); }
+  if (ctx->d2h) { cudaStreamSynchronize(ctx->d2h); cudaStreamDestroy(ctx->d2h); }
+  if (ctx->ev_comb) cudaEventDestroy(ctx->ev_comb);
+  if (ctx->ev_d2h_done) cudaEventDestroy(ctx->ev_d2h_done);
   if (ctx->ev_hio_start) cudaEventDestroy(ctx->ev_hio_start);
   if (ctx->ev_hio_done) cudaEventDestroy(ctx->ev_hio_done);
   if (ctx->side) cudaStreamDestroy(ctx->side);
@@ -629,16 +642,20 @@ s3_status s3_decode_step_host(s3_ctx* ctx, const s3_host_io* io) {
   if (io->chunks < 0) return fail(ctx, S3_E_INVAL, "decode_step_host: chunks < 0");
   if (!ctx->hio) {
     CK(cudaStreamCreateWithFlags(&ctx->hio, cudaStreamNonBlocking), "copy stream");
+    CK(cudaStreamCreateWithFlags(&ctx->d2h, cudaStreamNonBlocking), "copy stream");
     CK(cudaEventCreateWithFlags(&ctx->ev_hio_start, cudaEventDisableTiming), "event");
     CK(cudaEventCreateWithFlags(&ctx->ev_hio_done, cudaEventDisableTiming), "event");
+    CK(cudaEventCreateWithFlags(&ctx->ev_comb, cudaEventDisableTiming), "event");
+    CK(cudaEventCreateWithFlags(&ctx->ev_d2h_done, cudaEventDisableTiming), "event");
   }
   // the detection in k_prep reads eos first: a tiny in-stream copy
   CK(cudaMemcpyAsync(io->eos_dev, io->eos, (size_t)B, cudaMemcpyHostToDevice, ctx->st), "eos H2D");
   // the landing buffers are free once the previous step's kernels (earlier on cfg.stream) are done
   CK(cudaEventRecord(ctx->ev_hio_start, ctx->st), "event");
   CK(cudaStreamWaitEvent(ctx->hio, ctx->ev_hio_start, 0), "wait");
-  WriteValue32Fn wv = write_value32();
+  StreamValue32Fn wv = write_value32(), wt = wait_value32();
   const bool pipe = wv && ctx->cfg.attn_variant == 0 && attn_tma_stages(ctx->sh) >= 2;
+  const bool ce_out = pipe && wt && io->out_dev;   // device out + per-chunk D2H overlapped with the kernel
   int32_t nch = pipe ? std::min(io->chunks ? io->chunks : 16, kMaxFeedChunks) : 1;
   nch = std::max(1, std::min(nch, B));
   const int32_t cb = (B + nch - 1) / nch;
@@ -660,10 +677,47 @@ s3_status s3_decode_step_host(s3_ctx* ctx, const s3_host_io* io) {
   CK(cudaEventRecord(ctx->ev_hio_done, ctx->hio), "event");
   if (!pipe) CK(cudaStreamWaitEvent(ctx->st, ctx->ev_hio_done, 0), "wait");
   if (pipe) { ctx->feed.ready = ctx->ready; ctx->feed.cb = cb; ctx->feed.epoch = epoch; }
-  const s3_status rc = s3_decode_step(ctx, 0, L, io->q_dev, io->k_new_dev, io->v_new_dev, io->eos_dev,
-                                      static_cast<float*>(out_dev));
+  if (ce_out) ctx->feed.done = ctx->done;
+  // split-K slots (len + 1 > C, k_prep's rule) get their out rows from k_combine, after the kernel
+  std::vector<int32_t> split_slots;
+  uint32_t expect[kMaxFeedChunks] = {};
+  if (ce_out) {
+    const uint32_t warps = (uint32_t)(attn_block_threads(ctx->sh) / 32);
+    for (int32_t b = 0; b < B; ++b) {
+      if (ctx->slots_h[b].len + 1 > ctx->C) split_slots.push_back(b);
+      else expect[b / cb] += warps * (uint32_t)L;
+    }
+  }
+  float* kout = static_cast<float*>(io->out_dev ? io->out_dev : out_dev);
+  const s3_status rc = s3_decode_step(ctx, 0, L, io->q_dev, io->k_new_dev, io->v_new_dev, io->eos_dev, kout);
   ctx->feed = Feed{};
   if (rc != S3_OK) return rc;
+  const size_t wo = (size_t)ctx->sh.H * ctx->sh.D * 4;
+  if (io->out_dev) {
+    // enqueued after the attention and combine launches, so a wait here can never hold them up
+    cudaStream_t ds = ce_out ? ctx->d2h : ctx->st;
+    if (ce_out) {
+      CK(cudaStreamWaitEvent(ds, ctx->ev_hio_start, 0), "wait");
+      for (int32_t c = 0; c < nch; ++c) {
+        if (!expect[c]) continue;
+        ctx->done_target[c] += expect[c];
+        if (wt(ds, (unsigned long long)(uintptr_t)(ctx->done + c), ctx->done_target[c], kWaitGeq) != 0)
+          return fail(ctx, S3_E_CUDA, "decode_step_host: stream wait");
+        const int32_t b0 = c * cb, nb = std::min(B, b0 + cb) - b0;
+        CK(cudaMemcpy2DAsync((uint8_t*)io->out + b0 * wo, B * wo, (const uint8_t*)io->out_dev + b0 * wo, B * wo,
+                             nb * wo, (size_t)L, cudaMemcpyDeviceToHost, ds), "out D2H");
+      }
+      CK(cudaEventRecord(ctx->ev_comb, ctx->st), "event");
+      CK(cudaStreamWaitEvent(ds, ctx->ev_comb, 0), "wait");
+      for (int32_t b : split_slots)
+        CK(cudaMemcpy2DAsync((uint8_t*)io->out + b * wo, B * wo, (const uint8_t*)io->out_dev + b * wo, B * wo, wo,
+                             (size_t)L, cudaMemcpyDeviceToHost, ds), "out D2H");
+      CK(cudaEventRecord(ctx->ev_d2h_done, ds), "event");
+      CK(cudaStreamWaitEvent(ctx->st, ctx->ev_d2h_done, 0), "wait");
+    } else {
+      CK(cudaMemcpyAsync(io->out, io->out_dev, (size_t)L * B * wo, cudaMemcpyDeviceToHost, ds), "out D2H");
+    }
+  }
   // completion of cfg.stream implies the copies are done too
   CK(cudaStreamWaitEvent(ctx->st, ctx->ev_hio_done, 0), "wait");
   return S3_OK;

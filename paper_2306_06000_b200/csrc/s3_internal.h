@@ -117,6 +117,7 @@ struct Feed {
   const uint32_t* ready = nullptr;
   int32_t cb = 1;
   uint32_t epoch = 0;
+  uint32_t* done = nullptr;    // per-chunk count of consumer warps whose final out rows are stored
 };
 cudaError_t launch_attn(const Shape& sh, const uint16_t* q, const uint16_t* k_new, const uint16_t* v_new,
                         uint16_t* arena, uint8_t* staging, float* out, float* partials, const Unit* units,

@@ -1216,6 +1216,13 @@ __global__ void __launch_bounds__(576, 1) k_attn_tma(AttnArgs a, int32_t ns) {
           if (sub == 0) { pr[D] = m; pr[D + 1] = ssum; }
         }
       }
+      if (a.feed.done && h.part < 0) {
+        // host-fed step with a device out: count this warp's final rows for the
+        // copy stream that waits on the chunk's counter (release orders the warp's stores)
+        __syncwarp();
+        if (lane == 0)
+          asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.feed.done + h.b / a.feed.cb) : "memory");
+      }
     }
   }
 }

@@ -121,14 +121,15 @@ class S3Engine:
                            self.v_new if v_new is None else v_new, self.eos if eos is None else eos,
                            self.out if out is None else out)
 
-    def decode_host(self, q, k_new, v_new, eos, out, chunks=0):
+    def decode_host(self, q, k_new, v_new, eos, out, chunks=0, device_out=True):
         """Whole decode step fed from pinned HOST tensors (s3_decode_step_host):
         q/k_new/v_new/eos are copied into this engine's device buffers inside
-        the call, pipelined with the attention kernel, and `out` (pinned
-        fp32) is written by the kernels directly.  Synchronise the stream
-        before reading `out`."""
+        the call, pipelined with the attention kernel; `out` (pinned fp32) is
+        filled by per-chunk D2H copies from this engine's device `out`
+        (device_out) or stored by the kernels directly over PCIe.
+        Synchronise the stream before reading `out`."""
         abi.s3_decode_step_host(self.ctx, q, k_new, v_new, eos, out, self.q, self.k_new, self.v_new, self.eos,
-                                chunks)
+                                chunks, self.out if device_out else None)
 
     def evict_compact(self):
         return abi.s3_evict_compact(self.ctx, self.B)

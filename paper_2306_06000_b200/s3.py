@@ -83,7 +83,8 @@ class s3_profile(C.Structure):
 class s3_host_io(C.Structure):
     _fields_ = [("q", C.c_void_p), ("k_new", C.c_void_p), ("v_new", C.c_void_p), ("eos", C.c_void_p),
                 ("out", C.c_void_p), ("q_dev", C.c_void_p), ("k_new_dev", C.c_void_p),
-                ("v_new_dev", C.c_void_p), ("eos_dev", C.c_void_p), ("chunks", C.c_int32)]
+                ("v_new_dev", C.c_void_p), ("eos_dev", C.c_void_p), ("chunks", C.c_int32),
+                ("out_dev", C.c_void_p)]
 
 
 P = C.c_void_p
@@ -182,10 +183,12 @@ def s3_decode_step(ctx, l0, nl, q, k_new, v_new, eos, out):
            "s3_decode_step", ctx)
 
 
-def s3_decode_step_host(ctx, q, k_new, v_new, eos, out, q_dev, k_new_dev, v_new_dev, eos_dev, chunks=0):
-    """q/k_new/v_new/eos/out: pinned host tensors; *_dev: device landing buffers."""
+def s3_decode_step_host(ctx, q, k_new, v_new, eos, out, q_dev, k_new_dev, v_new_dev, eos_dev, chunks=0,
+                        out_dev=None):
+    """q/k_new/v_new/eos/out: pinned host tensors; *_dev: device landing buffers
+    (out_dev None: the kernels store `out` over PCIe)."""
     io = s3_host_io(_ptr(q), _ptr(k_new), _ptr(v_new), _ptr(eos), _ptr(out), _ptr(q_dev), _ptr(k_new_dev),
-                    _ptr(v_new_dev), _ptr(eos_dev), int(chunks))
+                    _ptr(v_new_dev), _ptr(eos_dev), int(chunks), _ptr(out_dev))
     _check(lib().s3_decode_step_host(ctx, C.byref(io)), "s3_decode_step_host", ctx)
 
 

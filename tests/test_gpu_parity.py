@@ -42,7 +42,7 @@ def u16(t: torch.Tensor) -> np.ndarray:
 
 def lockstep(trace, L, H, D, R, C=0, S=0, max_running=4096, staging=True, feed_oracle_inputs=False,
              max_steps=100000, check_arena=True, attn_variant=0, compact_mode=0, poison=False,
-             compact_policy=0, Hkv=0, host_io=False, chunks=0):
+             compact_policy=0, Hkv=0, host_io=False, chunks=0, device_out=False):
     from paper_2306_06000_b200.engine import S3Engine
     eng = S3Engine(L, H, D, trace.max_seq_len, R, max_running, chunk_rows=C, move_chunk_bytes=S,
                    staging_bytes=None if staging else 0, host_store_bytes=64 << 20, attn_variant=attn_variant,
@@ -105,9 +105,10 @@ def lockstep(trace, L, H, D, R, C=0, S=0, max_running=4096, staging=True, feed_o
                 # NaN-poison the landing buffers: a kernel that reads a chunk before
                 # its copy landed leaks NaN into out
                 eng.q.fill_(float("nan")); eng.k_new.fill_(float("nan")); eng.v_new.fill_(float("nan"))
+                eng.out.fill_(float("nan"))
                 eng.eos.fill_(0)
             torch.cuda.synchronize()
-            eng.decode_host(hq, hk, hv, he, ho, chunks=chunks)
+            eng.decode_host(hq, hk, hv, he, ho, chunks=chunks, device_out=device_out)
             torch.cuda.synchronize()
         else:
             eng.decode()
@@ -452,16 +453,22 @@ def test_grouped_query_kv_tensor_cores(H, Hkv, C, policy, mode, staging):
         assert r["fused_steps"] == 0
 
 
-@pytest.mark.parametrize("variant,chunks,C", [(0, 0, 16), (0, 64, 0), (0, 3, 16), (1, 0, 16), (2, 0, 16)])
-def test_host_fed_decode_step(variant, chunks, C):
+@pytest.mark.parametrize("variant,chunks,C,dev_out", [(0, 0, 16, False), (0, 64, 0, False), (0, 3, 16, False),
+                                                     (1, 0, 16, False), (2, 0, 16, False), (0, 0, 16, True),
+                                                     (0, 5, 8, True), (0, 64, 0, True), (2, 0, 16, True)])
+def test_host_fed_decode_step(variant, chunks, C, dev_out):
     """s3_decode_step_host: pinned host q/k_new/v_new/eos in, pinned host out,
     H2D pipelined with the attention kernel through per-chunk ready words
-    (TMA variant) or completed before it (other variants); device landing
-    buffers NaN-poisoned before every step."""
+    (TMA variant) or completed before it (other variants); out either stored
+    by the kernels over PCIe or (dev_out) copied per finished chunk by a
+    stream that waits on the kernel's per-chunk counters, split-K slots after
+    k_combine (small C makes many of them).  Device landing buffers and the
+    device out are NaN-poisoned before every step."""
     if variant == 2:
         H, Hkv, D = 8, 2, 128
     else:
         H, Hkv, D = 4, 0, 64
     t = s3synth.make_trace(48, seed=7, policy="short", p=0.3, max_seq_len=256, prompt_max=64)
-    r = lockstep(t, 2, H, D, 2048, C=C, host_io=True, chunks=chunks, attn_variant=variant, Hkv=Hkv)
+    r = lockstep(t, 2, H, D, 2048, C=C, host_io=True, chunks=chunks, attn_variant=variant, Hkv=Hkv,
+                 device_out=dev_out)
     assert r["steps"] > 20 and r["worst"] <= TOL
