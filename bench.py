@@ -459,9 +459,10 @@ def _ceiling_context(achieved):
     c = read_ceiling()
     if not c:
         return None
+    ceiling = max(c.get("read_ld_gbs") or 0.0, c.get("read_bulk_gbs") or 0.0)
     return {"read_stream_gbs": c.get("read_ld_gbs"), "read_bulk_gbs": c.get("read_bulk_gbs"),
             "mix_read5_write1_gbs": c.get("mix_read5_write1_gbs"),
-            "frac_of_read_stream": round(achieved / c["read_ld_gbs"], 4) if c.get("read_ld_gbs") else None,
+            "frac_of_read_ceiling": round(achieved / ceiling, 4) if ceiling else None,
             "source": "profiles/r01_hbm_probe.json (tools/hbm_probe, 4 GiB streams, best of 10)"}
 
 

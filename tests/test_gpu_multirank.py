@@ -125,10 +125,11 @@ def test_bench_torchrun_two_ranks_gloo():
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
            "--gpus", "2", "--steps", "10", "--warmup", "3", "--dist-backend", "gloo", "--arena-gb", "12",
-           "--requests", "1500", "--no-e2e", "--no-cpu-baseline"]
+           "--requests", "1500", "--no-cpu-baseline"]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-3000:]
     lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 1
     j = json.loads(lines[0])
     assert j["n_gpus"] == 2 and j["value"] > 0 and j["gpu_launches"] > 0
+    assert j["e2e"]["value"] > 0 and j["e2e"]["h2d_bytes_per_step"] > 0   # host-fed C ABI on both ranks
