@@ -342,6 +342,34 @@ def test_abi_error_codes_and_empty_batch():
     assert e.value.code == abi.S3_E_STATE
     rep, perm, ev, fin = eng.evict_compact()     # state intact after the errors
     assert rep.n_before == 2
+    eng.admit()
+    # host-fed step: host buffers must be pinned, landing buffers non-null
+    n = eng.q.numel()
+    pq = torch.empty(n, dtype=torch.bfloat16, pin_memory=True)
+    pk = torch.empty(n, dtype=torch.bfloat16, pin_memory=True)
+    pv = torch.empty(n, dtype=torch.bfloat16, pin_memory=True)
+    pe = torch.zeros(8, dtype=torch.uint8, pin_memory=True)
+    po = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    pageable = torch.empty(n, dtype=torch.float32)
+    with pytest.raises(abi.S3Error) as e:          # out not pinned
+        abi.s3_decode_step_host(eng.ctx, pq, pk, pv, pe, pageable, eng.q, eng.k_new, eng.v_new, eng.eos)
+    assert e.value.code == abi.S3_E_INVAL
+    with pytest.raises(abi.S3Error) as e:          # device tensor where a host buffer belongs
+        abi.s3_decode_step_host(eng.ctx, eng.q, pk, pv, pe, po, eng.q, eng.k_new, eng.v_new, eng.eos)
+    assert e.value.code == abi.S3_E_INVAL
+    with pytest.raises(abi.S3Error) as e:          # missing landing buffer
+        abi.s3_decode_step_host(eng.ctx, pq, pk, pv, pe, po, None, eng.k_new, eng.v_new, eng.eos)
+    assert e.value.code == abi.S3_E_INVAL
+    with pytest.raises(abi.S3Error) as e:          # negative pipeline depth
+        abi.s3_decode_step_host(eng.ctx, pq, pk, pv, pe, po, eng.q, eng.k_new, eng.v_new, eng.eos, chunks=-1)
+    assert e.value.code == abi.S3_E_INVAL
+    eng.synth_inputs()                             # still usable: a valid host-fed step goes through
+    m = eng.L * eng.B * eng.H * eng.D
+    pq[:m].copy_(eng.q[:m]); pk[:m].copy_(eng.k_new[:m]); pv[:m].copy_(eng.v_new[:m]); pe[:eng.B].copy_(eng.eos[:eng.B])
+    eng.decode_host(pq, pk, pv, pe, po)
+    torch.cuda.synchronize()
+    assert torch.isfinite(po[:m]).all()
+    eng.evict_compact()
     eng.close()
 
 
