@@ -10,8 +10,8 @@
 // SM) four roles:
 //   producer warp : items (unit, layer, KV head) from the atomic queue; TMA
 //                   tensor loads (128B swizzle) of the tile's K and V rows in
-//                   128/64/32/16-row boxes (only the groups holding valid
-//                   rows) and of the group's q rows, into a 3-stage ring.
+//                   128/64/32/16/8-row boxes (only the 8-row groups holding
+//                   valid rows) and of the group's q rows, into a 3-stage ring.
 //                   Short units pack np = 2..NC/G KV heads into one tile,
 //                   one segment of 128/np rows per head: the q box already
 //                   holds those heads' np*G query rows, and the softmax masks
@@ -271,10 +271,12 @@ __device__ __forceinline__ void col_reduce(float (&v)[NC], float (&red)[4][NQ], 
   softmax_bar();
 }
 
-// tensor maps: arena and staging rows in boxes of 128 / 64 / 32 / 16 rows x 64
-// columns (a tile's valid 16-row groups go out as a binary decomposition, so a
-// full tile is one box per 64-column block instead of eight)
-constexpr int NBOX = 4;
+// tensor maps: arena and staging rows in boxes of 128 / 64 / 32 / 16 / 8 rows x
+// 64 columns (a tile's valid 8-row groups come in as a binary decomposition, so
+// a full tile is one box per 64-column block; rows between the last 8-row group
+// and the 16-row MMA step are zeroed (V) / masked (K) by the softmax warps)
+constexpr int NBOX = 5;         // loads: 128/64/32/16/8-row boxes (8-row granularity);
+constexpr int NBOX_STORE = 4;   // stores: whole 16-row groups, the ragged rest by a warp copy
 struct TcMaps {
   CUtensorMap kv[NBOX];      // box rows 128 >> i
   CUtensorMap stage[NBOX];
@@ -379,28 +381,31 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
             const int glast = g + np - 1;  // heads g..glast are read up to r + nv rows once this tile lands
             h.prog = (uint32_t)(glast * TC_HEAD_STRIDE + r + nv) |
                      (glast == a.Hkv - 1 && r + TM >= nrows ? TC_PROG_FULL : 0u);
-            const int groups = (nv + 15) / 16;
+            // load granularity: 8-row groups (one 128B-swizzle atom) in the PACK kernel, whose
+            // items are short or G <= 8; 16-row groups otherwise (measured faster for MQA)
+            constexpr int GR = PACK ? 8 : 16;
+            const int groups = (nv + GR - 1) / GR;
             uint8_t* sk = smem + st * STAGE_BYTES;
             uint8_t* sv = sk + KV_BYTES;
             uint8_t* sq = sv + KV_BYTES;
             const bool dep = fused && mv;
-            mb_expect(&S.kv_full[st], (uint32_t)(np * groups * 16 * 128 * 2 * 2 + Q_BYTES + (dep ? 16 : 0)));
+            mb_expect(&S.kv_full[st], (uint32_t)(np * groups * GR * 128 * 2 * 2 + Q_BYTES + (dep ? 16 : 0)));
             if (dep) bulk_g2s16(&h.dep, a.desc + un.stage_base + r / TM, &S.kv_full[st]);
             const int row0 = un.off + un.r0 + r;
             for (int sgi = 0; sgi < np; ++sgi) {
               const int colk = (a.l0 + li) * row_cols + (g + sgi) * DH;
               const int colv = colk + a.Hkv * DH;
               const int sro = sgi * seg * 128;   // segment's first shared-memory row (bytes)
-              int done = 0;                 // 16-row groups, largest boxes first
+              int done = 0;                 // GR-row groups, largest boxes first
 #pragma unroll
-              for (int i = 0; i < NBOX; ++i) {
-                const int bg = 8 >> i;
+              for (int i = 0; i < (PACK ? NBOX : NBOX - 1); ++i) {
+                const int bg = (TM / GR) >> i;
                 if (groups - done >= bg) {
                   const CUtensorMap* m = &maps.kv[i];
 #pragma unroll
                   for (int kb = 0; kb < 2; ++kb) {
-                    tma2d(sk + kb * 16384 + sro + done * 2048, m, colk + kb * 64, row0 + done * 16, &S.kv_full[st]);
-                    tma2d(sv + kb * 16384 + sro + done * 2048, m, colv + kb * 64, row0 + done * 16, &S.kv_full[st]);
+                    tma2d(sk + kb * 16384 + sro + done * GR * 128, m, colk + kb * 64, row0 + done * GR, &S.kv_full[st]);
+                    tma2d(sv + kb * 16384 + sro + done * GR * 128, m, colv + kb * 64, row0 + done * GR, &S.kv_full[st]);
                   }
                   done += bg;
                 }
@@ -515,7 +520,7 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
               const CUtensorMap* map = h.mode == UNIT_MOVE ? maps.kv : maps.stage;
               int done = 0;
 #pragma unroll
-              for (int i = 0; i < NBOX; ++i) {
+              for (int i = 0; i < NBOX_STORE; ++i) {
                 const int bg = 8 >> i;
                 if (full_groups - done >= bg) {
 #pragma unroll
