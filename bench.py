@@ -444,6 +444,9 @@ def run_s3(args):
                 "evict_d2h_gbs": round(prof.d2h_bytes / (prof.d2h_ms / 1e3) / 1e9, 2) if prof.d2h_ms else None,
                 "reload_h2d_gbs": round(prof.h2d_bytes / (prof.h2d_ms / 1e3) / 1e9, 2) if prof.h2d_ms else None,
                 "evict_d2h_bytes": prof.d2h_bytes, "reload_h2d_bytes": prof.h2d_bytes,
+                "evict_d2h_ms": round(prof.d2h_ms, 3),
+                "evict_d2h_overlapped_with_attention_frac":
+                    round(prof.d2h_overlap_ms / prof.d2h_ms, 4) if prof.d2h_ms else None,
             },
             "clocks": clk,
             "cpu_baseline": cpu,

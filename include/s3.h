@@ -240,6 +240,8 @@ typedef struct {
   int64_t d2h_copies, h2d_copies;   /* eviction D2H batches / reload H2D copies timed   */
   double d2h_ms, d2h_bytes;         /* eviction copies (side stream, overlapped)        */
   double h2d_ms, h2d_bytes;         /* reload copies (main stream)                       */
+  double d2h_overlap_ms;            /* part of d2h_ms during which an attention kernel ran
+                                       (CUDA-event intervals on both streams)             */
 } s3_profile;
 s3_status s3_profile_enable(s3_ctx* ctx, int32_t on);   /* also resets the sums */
 s3_status s3_profile_get(s3_ctx* ctx, s3_profile* prof); /* synchronises          */

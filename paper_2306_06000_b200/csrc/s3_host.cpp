@@ -101,6 +101,10 @@ struct Prof {
   int64_t attn_launches = 0, move_launches = 0, fused_steps = 0, d2h_copies = 0, h2d_copies = 0;
   double attn_ms = 0, move_ms = 0, attn_bytes = 0, move_bytes = 0, fused_move_bytes = 0;
   double d2h_ms = 0, d2h_bytes = 0, h2d_ms = 0, h2d_bytes = 0;
+  // absolute intervals (ms after `ref`) of attention launches and eviction copies, for the
+  // overlap evidence: how much of the side-stream D2H ran while an attention kernel ran
+  cudaEvent_t ref = nullptr;
+  std::vector<std::pair<double, double>> attn_iv, d2h_iv;
   cudaEvent_t get() {
     if (!free_events.empty()) { cudaEvent_t e = free_events.back(); free_events.pop_back(); return e; }
     cudaEvent_t e;
@@ -148,6 +152,7 @@ struct s3_ctx {
   Feed feed;                    // set only for the duration of a host-fed decode call
   // pinned host
   uint8_t* h_report = nullptr;
+  uint8_t* h_report_dev = nullptr;          // the same pinned buffer as seen by kernels (UVA mapping)
   uint8_t* h_upload = nullptr;
   int64_t upload_cap = 0, upload_used = 0;
   // host mirror (arena order)
@@ -162,7 +167,11 @@ struct s3_ctx {
   struct Deferred { int64_t off, bytes; std::shared_ptr<EventBox> done; };
   std::vector<Deferred> deferred_free;      // host-store ranges freed once their reload H2D completed
   cudaEvent_t ev_report = nullptr;          // after the fused step's report readback
-  std::shared_ptr<EventBox> last_stage_d2h;
+  // eviction staging, double-buffered when it holds two maximal evictions: a step's
+  // evictees go to one half while the other half's D2H (previous step) is still running
+  bool stage_dbl = false;
+  int stage_next = 0, stage_cur = 0;
+  std::shared_ptr<EventBox> stage_d2h[2];
   // state
   bool status_pending = false;
   uint32_t epoch = 0;
@@ -297,6 +306,14 @@ void prof_collect(s3_ctx* c) {     // call when cfg.stream is idle; side-stream 
     if (cudaEventQuery(p.b) != cudaSuccess) { keep.push_back(p); continue; }
     float ms = 0.f;
     cudaEventElapsedTime(&ms, p.a, p.b);
+    if (c->prof.ref && (p.kind == 0 || p.kind == 2)) {
+      float t0 = 0.f, t1 = 0.f;
+      if (cudaEventElapsedTime(&t0, c->prof.ref, p.a) == cudaSuccess &&
+          cudaEventElapsedTime(&t1, c->prof.ref, p.b) == cudaSuccess)
+        (p.kind == 0 ? c->prof.attn_iv : c->prof.d2h_iv).emplace_back(t0, t1);
+      else
+        cudaGetLastError();
+    }
     if (p.kind == 0) { c->prof.attn_ms += ms; c->prof.attn_bytes += p.bytes; c->prof.attn_launches++; }
     else if (p.kind == 1) { c->prof.move_ms += ms; c->prof.move_bytes += p.bytes; c->prof.move_launches++; }
     else if (p.kind == 2) { c->prof.d2h_ms += ms; c->prof.d2h_bytes += p.bytes; c->prof.d2h_copies++; }
@@ -394,6 +411,14 @@ s3_status check_ctx(s3_ctx* ctx) {
   return S3_OK;
 }
 
+int64_t stage_bytes(const s3_ctx* c) {
+  if (!c->buf.staging) return 0;
+  return c->stage_dbl ? c->buf.staging_bytes / 2 / 256 * 256 : c->buf.staging_bytes;
+}
+uint8_t* stage_ptr(const s3_ctx* c, int half) {
+  return (uint8_t*)c->buf.staging + (c->stage_dbl ? (int64_t)half * stage_bytes(c) : 0);
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -484,11 +509,13 @@ s3_status s3_kv_init(const s3_config* cfg, const s3_buffers* b, s3_ctx** out) {
   if (cudaMemsetAsync(ws + k.flags, 0, (size_t)(k.report - k.flags), ctx->st) != cudaSuccess) return bail("memset");
   if (cudaMemsetAsync(ws + k.progress, 0, (size_t)(k.flags - k.progress), ctx->st) != cudaSuccess) return bail("memset");
   const int64_t rb = report_bytes(cfg->max_running) + 64;
-  if (cudaHostAlloc((void**)&ctx->h_report, (size_t)rb, cudaHostAllocDefault) != cudaSuccess) return bail("pinned");
+  if (cudaHostAlloc((void**)&ctx->h_report, (size_t)rb, cudaHostAllocMapped) != cudaSuccess) return bail("pinned");
+  if (cudaHostGetDevicePointer((void**)&ctx->h_report_dev, ctx->h_report, 0) != cudaSuccess) return bail("mapped");
   ctx->upload_cap = align_up(4 * ((int64_t)cfg->max_running * (sizeof(DSlot) + 4) + 4096));
   if (cudaHostAlloc((void**)&ctx->h_upload, (size_t)ctx->upload_cap, cudaHostAllocDefault) != cudaSuccess)
     return bail("pinned");
   ctx->free_blocks[0] = b->host_store_bytes / kAlign * kAlign;
+  ctx->stage_dbl = b->staging && b->staging_bytes / 2 / 256 * 256 >= (int64_t)cfg->max_seq_len * sh.kvpt;
   if (cudaStreamSynchronize(ctx->st) != cudaSuccess) return bail("sync");
   *out = ctx;
   return S3_OK;
@@ -500,10 +527,12 @@ s3_status s3_kv_destroy(s3_ctx* ctx) {
   if (ctx->side) cudaStreamSynchronize(ctx->side);
   ctx->pool.clear();
   ctx->home.clear();
-  ctx->last_stage_d2h.reset();
+  ctx->stage_d2h[0].reset();
+  ctx->stage_d2h[1].reset();
   for (auto& p : ctx->prof.pending) { cudaEventDestroy(p.a); cudaEventDestroy(p.b); }
   for (auto e : ctx->prof.free_events) cudaEventDestroy(e);
   ctx->deferred_free.clear();
+  if (ctx->prof.ref) cudaEventDestroy(ctx->prof.ref);
   if (ctx->ev_report) cudaEventDestroy(ctx->ev_report);
   if (ctx->hio) { cudaStreamSynchronize(ctx->hio); cudaStreamDestroy(ctx->hio); }
   if (ctx->d2h) { cudaStreamSynchronize(ctx->d2h); cudaStreamDestroy(ctx->d2h); }
@@ -554,8 +583,12 @@ s3_status s3_decode_step(s3_ctx* ctx, int32_t l0, int32_t nl, const void* q, con
                     ((ctx->cfg.attn_variant == 0 && attn_tma_stages(ctx->sh) >= 2) || ctx->cfg.attn_variant == 2);
   if (B > 0) {
     if (!q || !k_new || !v_new || !out || (finalize && !eos)) return fail(ctx, S3_E_INVAL, "decode_step: null");
-    if (fuse && ctx->last_stage_d2h)   // staging is rewritten: the previous step's D2H from it must be done
-      CK(cudaStreamWaitEvent(ctx->st, ctx->last_stage_d2h->ev, 0), "wait staging");
+    if (fuse) {
+      // this step's evictees go to staging half `stage_next`: the D2H that last read it must be done
+      ctx->stage_cur = ctx->stage_next;
+      if (ctx->stage_d2h[ctx->stage_cur])
+        CK(cudaStreamWaitEvent(ctx->st, ctx->stage_d2h[ctx->stage_cur]->ev, 0), "wait staging");
+    }
     if (ctx->cfg.attn_variant == 2) {   // the tensor-core kernel reads the new row from the arena
       CK(launch_append(ctx->sh, ctx->slots[ctx->cur], B, l0, nl, (const uint16_t*)k_new, (const uint16_t*)v_new,
                        (uint16_t*)ctx->buf.arena, ctx->st), "k_append");
@@ -566,17 +599,17 @@ s3_status s3_decode_step(s3_ctx* ctx, int32_t l0, int32_t nl, const void* q, con
     pa.eos = eos; pa.finalize = finalize ? 1 : 0; pa.fuse = fuse ? 1 : 0;
     pa.compact_policy = ctx->cfg.compact_policy;
     pa.pool_nonempty = (ctx->pool.size() + ctx->home.size()) > 0 ? 1 : 0;
-    pa.staging_bytes = ctx->buf.staging ? ctx->buf.staging_bytes : 0;
-    pa.units = ctx->units; pa.splits = ctx->splits; pa.ctrl = ctx->ctrl; pa.report = ctx->report_dev;
+    pa.staging_bytes = stage_bytes(ctx);
+    pa.units = ctx->units; pa.splits = ctx->splits; pa.ctrl = ctx->ctrl;
+    // fused: k_prep writes the keep-scan report straight into pinned host memory, so the
+    // host's eviction bookkeeping and FFD start as soon as k_prep ends (overlapping the
+    // attention kernel) and no copy engine is involved -- a report copy would queue
+    // behind the previous step's eviction D2H on the copy engine and hold up attention
+    pa.report = fuse ? ctx->h_report_dev : ctx->report_dev;
+    pa.fused_out = fuse ? reinterpret_cast<int32_t*>(ctx->h_report_dev + report_bytes(B)) : nullptr;
     CK(launch_prep(pa, ctx->st), "k_prep");
     ctx->launches += 1;
     if (fuse) {
-      // the keep-scan report is final now: read it back while attention runs, so the
-      // host's eviction bookkeeping and FFD overlap the attention kernel
-      CK(cudaMemcpyAsync(ctx->h_report, ctx->report_dev, (size_t)report_bytes(B), cudaMemcpyDeviceToHost,
-                         ctx->st), "report D2H");
-      CK(cudaMemcpyAsync(ctx->h_report + report_bytes(B), ctx->ctrl + CTRL_FUSED, 4, cudaMemcpyDeviceToHost,
-                         ctx->st), "fused flag D2H");
       CK(cudaEventRecord(ctx->ev_report, ctx->st), "event");
       CK(launch_deps(ctx->units, ctx->ctrl, ctx->desc, ctx->cfg.attn_variant == 2 ? 1 : 0, ctx->num_sms * 4,
                      ctx->st), "k_deps");
@@ -587,12 +620,13 @@ s3_status s3_decode_step(s3_ctx* ctx, int32_t l0, int32_t nl, const void* q, con
     if (ctx->prof.on) { e0 = ctx->prof.get(); e1 = ctx->prof.get(); cudaEventRecord(e0, ctx->st); }
     if (ctx->cfg.attn_variant == 2)
       CK(launch_attn_tc(ctx->sh, (const uint16_t*)q, (uint16_t*)ctx->buf.arena, ctx->cfg.arena_rows,
-                        (uint8_t*)ctx->buf.staging, ctx->buf.staging ? ctx->buf.staging_bytes : 0, out, ctx->partials,
+                        ctx->buf.staging ? stage_ptr(ctx, ctx->stage_cur) : nullptr, stage_bytes(ctx), out, ctx->partials,
                         ctx->units, ctx->splits, ctx->desc, ctx->progress, ctx->attn_epoch, ctx->ctrl, B, l0, nl,
                         ctx->grid_attn, ctx->grid_combine, ctx->st), "k_attn_tc");
     else
       CK(launch_attn(ctx->sh, (const uint16_t*)q, (const uint16_t*)k_new, (const uint16_t*)v_new,
-                     (uint16_t*)ctx->buf.arena, (uint8_t*)ctx->buf.staging, out, ctx->partials, ctx->units,
+                     (uint16_t*)ctx->buf.arena, ctx->buf.staging ? stage_ptr(ctx, ctx->stage_cur) : nullptr, out,
+                     ctx->partials, ctx->units,
                      ctx->splits, ctx->desc, ctx->progress, ctx->attn_epoch, ctx->ctrl, B, l0, nl, ctx->grid_attn,
                      ctx->grid_combine, ctx->cfg.attn_variant, ctx->feed, ctx->st), "k_attn");
     ctx->launches += 2;   // attention, combine
@@ -776,7 +810,10 @@ s3_status s3_evict_compact(s3_ctx* ctx, s3_evict_report* rep, int32_t* perm, s3_
     }
     if (hoff[i] < 0) return fail(ctx, S3_E_CUDA, "evict_compact: host store exhausted");
   }
-  const bool staged = h->n_evicted > 0 && ctx->buf.staging && h->d2h_bytes <= ctx->buf.staging_bytes;
+  // the fused step already wrote its evictees to half stage_cur; the k_move path takes the next half
+  if (!fused) ctx->stage_cur = ctx->stage_next;
+  const bool staged = h->n_evicted > 0 && ctx->buf.staging && h->d2h_bytes <= stage_bytes(ctx);
+  uint8_t* stage = ctx->buf.staging ? stage_ptr(ctx, ctx->stage_cur) : nullptr;
   if (fused && ctx->prof.on) {
     ctx->prof.fused_steps++;
     ctx->prof.fused_move_bytes += (double)h->moved_bytes + (double)h->d2h_bytes;
@@ -799,9 +836,9 @@ s3_status s3_evict_compact(s3_ctx* ctx, s3_evict_report* rep, int32_t* perm, s3_
         ctx->prof.pending.push_back({e0, e1, (double)h->d2h_bytes, 2});
       }
       CK(cudaEventRecord(d2h_done->ev, ctx->st), "event");
-    } else if (ctx->last_stage_d2h && !fused) {
-      // staging is reused: the previous step's D2H from it must be done
-      CK(cudaStreamWaitEvent(ctx->st, ctx->last_stage_d2h->ev, 0), "wait staging");
+    } else if (ctx->stage_d2h[ctx->stage_cur] && !fused) {
+      // k_move rewrites this staging half: the D2H that last read it must be done
+      CK(cudaStreamWaitEvent(ctx->st, ctx->stage_d2h[ctx->stage_cur]->ev, 0), "wait staging");
     }
   }
   if (!fused && h->n_chunks > 0) {
@@ -809,7 +846,7 @@ s3_status s3_evict_compact(s3_ctx* ctx, s3_evict_report* rep, int32_t* perm, s3_
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx->prof.on) { e0 = ctx->prof.get(); e1 = ctx->prof.get(); cudaEventRecord(e0, ctx->st); }
     const int grid = (int)std::min<int64_t>((h->n_chunks + 2 * 3 - 1) / (2 * 3), ctx->grid_move);
-    CK(launch_move((uint8_t*)ctx->buf.arena, (uint8_t*)ctx->buf.staging, ctx->entries, ctx->key_chunk0,
+    CK(launch_move((uint8_t*)ctx->buf.arena, stage, ctx->entries, ctx->key_chunk0,
                    ctx->key_src, h->n_entries, h->n_chunks, ctx->S, sh.kvpt, ctx->ctrl64, ctx->flags, ctx->epoch,
                    staged ? 1 : 0, grid, ctx->st), "k_move");
     ctx->launches += 1;
@@ -828,14 +865,15 @@ s3_status s3_evict_compact(s3_ctx* ctx, s3_evict_report* rep, int32_t* perm, s3_
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx->prof.on) { e0 = ctx->prof.get(); e1 = ctx->prof.get(); cudaEventRecord(e0, ctx->side); }
     for (int32_t i = 0; i < h->n_evicted; ++i)
-      CK(cudaMemcpyAsync((uint8_t*)ctx->buf.host_store + hoff[i], (uint8_t*)ctx->buf.staging + dev[i].stage_off,
+      CK(cudaMemcpyAsync((uint8_t*)ctx->buf.host_store + hoff[i], stage + dev[i].stage_off,
                          (size_t)dev[i].len * sh.kvpt, cudaMemcpyDeviceToHost, ctx->side), "evict D2H");
     if (ctx->prof.on) {
       cudaEventRecord(e1, ctx->side);
       ctx->prof.pending.push_back({e0, e1, (double)h->d2h_bytes, 2});
     }
     CK(cudaEventRecord(d2h_done->ev, ctx->side), "event");
-    ctx->last_stage_d2h = d2h_done;
+    ctx->stage_d2h[ctx->stage_cur] = d2h_done;
+    if (ctx->stage_dbl) ctx->stage_next = 1 - ctx->stage_cur;   // the next evictions use the other half
   }
   // requeue evicted requests with doubled reservation (R5), in batch order
   int64_t pcie = 0;
@@ -1046,6 +1084,10 @@ s3_status s3_profile_enable(s3_ctx* ctx, int32_t on) {
   CK(cudaStreamSynchronize(ctx->side), "side sync");
   prof_collect(ctx);
   ctx->prof.on = on != 0;
+  ctx->prof.attn_iv.clear();
+  ctx->prof.d2h_iv.clear();
+  if (!ctx->prof.ref) CK(cudaEventCreate(&ctx->prof.ref), "event");
+  CK(cudaEventRecord(ctx->prof.ref, ctx->st), "event");
   ctx->prof.attn_launches = ctx->prof.move_launches = ctx->prof.fused_steps = 0;
   ctx->prof.attn_ms = ctx->prof.move_ms = ctx->prof.attn_bytes = ctx->prof.move_bytes = 0;
   ctx->prof.fused_move_bytes = 0;
@@ -1072,6 +1114,10 @@ s3_status s3_profile_get(s3_ctx* ctx, s3_profile* p) {
   p->d2h_copies = ctx->prof.d2h_copies; p->h2d_copies = ctx->prof.h2d_copies;
   p->d2h_ms = ctx->prof.d2h_ms; p->d2h_bytes = ctx->prof.d2h_bytes;
   p->h2d_ms = ctx->prof.h2d_ms; p->h2d_bytes = ctx->prof.h2d_bytes;
+  double ov = 0;
+  for (const auto& d : ctx->prof.d2h_iv)
+    for (const auto& k : ctx->prof.attn_iv) ov += std::max(0.0, std::min(d.second, k.second) - std::max(d.first, k.first));
+  p->d2h_overlap_ms = ov;
   return S3_OK;
 }
 

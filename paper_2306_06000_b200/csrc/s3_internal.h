@@ -105,7 +105,8 @@ struct PrepArgs {
   Unit* units;
   Split* splits;
   int32_t* ctrl;
-  uint8_t* report;
+  uint8_t* report;      // fused: the host-mapped pinned report (written over PCIe, no copy engine)
+  int32_t* fused_out;   // host-mapped word: 1 if this step fused the row shift (or nullptr)
 };
 cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st);
 cudaError_t launch_deps(const Unit* units, const int32_t* ctrl, DepDesc* desc, int32_t tc, int32_t grid,

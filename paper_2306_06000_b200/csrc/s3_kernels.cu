@@ -315,6 +315,7 @@ __global__ void __launch_bounds__(1024) k_prep(PrepArgs a) {
     a.ctrl[CTRL_ITEM] = 0;
     a.ctrl[CTRL_SPLIT_ITEM] = 0;
     a.ctrl[CTRL_FUSED] = fused ? 1 : 0;
+    if (a.fused_out) *reinterpret_cast<volatile int32_t*>(a.fused_out) = fused ? 1 : 0;
     a.ctrl[CTRL_N_STAGES] = (int)tot[3];
     if (fused) {
       DReportHeader* h = reinterpret_cast<DReportHeader*>(a.report);
