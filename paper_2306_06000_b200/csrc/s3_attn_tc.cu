@@ -30,7 +30,9 @@
 //   storer warp   : (fused steps only) the row shift of SURVEY §8 row (d),
 //                   done on the tiles already in shared memory -- see below.
 // The new token's K/V row is appended to the arena by k_append before this
-// kernel, so every tile reads rows straight from the arena.
+// kernel, or -- in a host-fed step, where k_new / v_new stream in per chunk --
+// by the producer warp just before the unit's tiles load; either way every
+// tile reads rows straight from the arena.
 //
 // Fused row shift (same protocol as k_attn_tma, at tile granularity): when a
 // tile lands the storer publishes its unit-layer's read progress
@@ -298,11 +300,37 @@ struct TcArgs {
   unsigned long long* progress;
   uint32_t epoch;
   int32_t pmax;          // most KV heads one tile may pack (NC / G; 1 = no packing)
+  const uint16_t* k_new; // [nl][B][Hkv][D]: appended to the arena by the producer warp
+  const uint16_t* v_new;
+  Feed feed;             // host-fed step: per-chunk ready words (s3_decode_step_host)
 };
+
+// Wait until a ready word written by the copy stream reaches `epoch` (host-fed
+// step); trap after 20 s instead of hanging the device.
+__device__ __noinline__ void tc_wait_ready(const uint32_t* p, uint32_t epoch) {
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  for (;;) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    if ((int32_t)(v - epoch) >= 0) break;
+    __nanosleep(200);
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    if (t - t0 > 20000000000ull) __trap();
+  }
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+__device__ __forceinline__ uint4 ld_cg16(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p) : "memory");
+  return r;
+}
 
 // NC: query columns the softmax handles, G padded to 8 or 16 (the MMA always has N = 16);
 // PACK: short units may pack several KV heads into one tile (NC / G >= 2)
-template <int NC, bool PACK>
+// FEED: host-fed step (the producer warp waits on ready words and appends the new rows)
+template <int NC, bool PACK, bool FEED>
 __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMaps maps, TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-B alignment for the 128B-swizzle atoms, by pointer arithmetic so the
@@ -340,22 +368,56 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
   if (warp == 0) {
     // ------------------------------ producer ------------------------------
     // One atomic per (unit, layer) covers its H_kv items (item = (u*nl + li)*H_kv + g),
-    // so the queue and unit-record latencies are paid once per H_kv tiles.
-    if (lane == 0) {
-      int t = 0, iseq = 0;
-      const int groups_total = a.ctrl[CTRL_N_UNITS] * a.nl;
-      for (;;) {
-        const int w = atomicAdd(&a.ctrl[CTRL_ITEM], 1);
-        if (w >= groups_total) {
+    // so the queue and unit-record latencies are paid once per H_kv tiles.  In a host-fed
+    // step the whole warp first appends the unit's new K/V row (all KV heads of the layer)
+    // at arena row off + len -- the slot's first slack row, which no other unit reads or,
+    // before this unit's progress covers it, writes -- then lane 0 issues the tiles.
+    // Otherwise k_append has written every new row before the kernel (cheaper: the
+    // loads would stall this warp's TMA issue).
+    int t = 0, iseq = 0, ready_max = -1;
+    const int groups_total = a.ctrl[CTRL_N_UNITS] * a.nl;
+    const int kd8 = a.Hkv * DH / 8;               // 16-B vectors of one layer's new K (or V) row
+    // FEED: the whole warp runs the loop (lane 0 takes tickets and issues tiles); else lane 0 alone
+    for (; FEED || lane == 0;) {
+      int w = 0;
+      if (lane == 0) w = atomicAdd(&a.ctrl[CTRL_ITEM], 1);
+      if constexpr (FEED) w = __shfl_sync(0xffffffffu, w, 0);
+      if (w >= groups_total) {
+        if (lane == 0) {
           const int st = t % NST;
           mb_wait(&S.kv_empty[st], ((uint32_t)(t / NST) & 1u) ^ 1u);
           S.hdr[st].item = -1;
           mb_arrive(&S.kv_full[st]);
-          break;
         }
-        const int li = w % a.nl, u = w / a.nl;
-        const Unit un = a.units[u];
-        const int nrows = (un.r1 - un.r0) + (un.has_new ? 1 : 0);   // new row already in the arena
+        break;
+      }
+      const int li = w % a.nl, u = w / a.nl;
+      const Unit un = a.units[u];
+      if constexpr (FEED) {
+        // host-fed step: this slot's q / k_new / v_new have landed once its chunk's word is set
+        // (chunks land in order, so the highest chunk waited for covers every earlier one)
+        const int c = un.b / a.feed.cb;
+        if (c > ready_max) {
+          if (lane == 0) tc_wait_ready(a.feed.ready + c, a.feed.epoch);
+          ready_max = c;
+          __syncwarp();
+        }
+      }
+      if (FEED && un.has_new) {   // host-fed: k_new / v_new land during the kernel
+        const int64_t src = ((int64_t)li * a.B + un.b) * a.Hkv * DH;
+        uint16_t* dst = reinterpret_cast<uint16_t*>(a.arena) + (int64_t)(un.off + un.len) * (a.kvpt / 2) +
+                        (int64_t)(a.l0 + li) * 2 * a.Hkv * DH;
+        for (int i = lane; i < kd8; i += 32) {
+          const uint4 kk = ld_cg16(a.k_new + src + i * 8);
+          const uint4 vv = ld_cg16(a.v_new + src + i * 8);
+          *reinterpret_cast<uint4*>(dst + i * 8) = kk;
+          *reinterpret_cast<uint4*>(dst + a.Hkv * DH + i * 8) = vv;
+        }
+        asm volatile("fence.proxy.async.global;" ::: "memory");   // the tile loads below read the new row
+        __syncwarp();
+      }
+      if (lane == 0) {
+        const int nrows = (un.r1 - un.r0) + (un.has_new ? 1 : 0);   // new row now in the arena
         const bool mv = un.mode == UNIT_MOVE;
         // destination row of the unit's first row: arena row (MOVE) or staging row (STAGE)
         const int drow0 = (int)(mv ? un.dst : un.dst / a.kvpt) + un.r0;
@@ -417,6 +479,7 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
           }
         }
       }
+      if constexpr (FEED) __syncwarp();
     }
   } else if (warp == 1) {
     // -------------------------------- MMA ---------------------------------
@@ -721,6 +784,7 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
 }
 
+
 // k_append: the new token's K/V row goes to row off+len before k_attn_tc reads it
 __global__ void __launch_bounds__(256) k_append(Shape sh, const DSlot* __restrict__ slots, int32_t B, int32_t l0,
                                                 int32_t nl, const uint16_t* __restrict__ k_new,
@@ -774,15 +838,20 @@ bool encode_2d(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, u
 }  // namespace
 
 int attn_tc_smem() { return NST * STAGE_BYTES + 2 * PBUF_BYTES + (int)sizeof(TcSmem) + 1024; }
-const void* attn_tc_kernel_ptr(int nc, bool pack) {
-  if (nc == 8) return pack ? (const void*)k_attn_tc<8, true> : (const void*)k_attn_tc<8, false>;
-  return pack ? (const void*)k_attn_tc<16, true> : (const void*)k_attn_tc<16, false>;
+const void* attn_tc_kernel_ptr(int nc, bool pack, bool feed) {
+  if (feed) {
+    if (nc == 8) return pack ? (const void*)k_attn_tc<8, true, true> : (const void*)k_attn_tc<8, false, true>;
+    return pack ? (const void*)k_attn_tc<16, true, true> : (const void*)k_attn_tc<16, false, true>;
+  }
+  if (nc == 8) return pack ? (const void*)k_attn_tc<8, true, false> : (const void*)k_attn_tc<8, false, false>;
+  return pack ? (const void*)k_attn_tc<16, true, false> : (const void*)k_attn_tc<16, false, false>;
 }
 
 bool attn_tc_supported(const Shape& sh) {
   const int G = sh.Hkv > 0 ? sh.H / sh.Hkv : 0;
   return sh.D == DH && G >= 2 && G <= NQ && sh.H % sh.Hkv == 0 && encoder() != nullptr;
 }
+
 
 cudaError_t launch_append(const Shape& sh, const DSlot* slots, int32_t B, int32_t l0, int32_t nl,
                           const uint16_t* k_new, const uint16_t* v_new, uint16_t* arena, cudaStream_t st) {
@@ -792,11 +861,11 @@ cudaError_t launch_append(const Shape& sh, const DSlot* slots, int32_t B, int32_
   return cudaGetLastError();
 }
 
-cudaError_t launch_attn_tc(const Shape& sh, const uint16_t* q, uint16_t* arena, int64_t arena_rows,
-                           uint8_t* staging, int64_t staging_bytes, float* out, float* partials, const Unit* units,
-                           const Split* splits, const DepDesc* desc, unsigned long long* progress, uint32_t epoch,
-                           int32_t* ctrl, int32_t B, int32_t l0, int32_t nl, int32_t grid_attn, int32_t grid_combine,
-                           cudaStream_t st) {
+cudaError_t launch_attn_tc(const Shape& sh, const uint16_t* q, const uint16_t* k_new, const uint16_t* v_new,
+                           uint16_t* arena, int64_t arena_rows, uint8_t* staging, int64_t staging_bytes, float* out,
+                           float* partials, const Unit* units, const Split* splits, const DepDesc* desc,
+                           unsigned long long* progress, uint32_t epoch, int32_t* ctrl, int32_t B, int32_t l0,
+                           int32_t nl, int32_t grid_attn, int32_t grid_combine, const Feed& feed, cudaStream_t st) {
   TcMaps maps;
   // staging rows (evicted slots' KV, token-major like the arena); without staging k_prep never fuses an eviction
   const int64_t stage_rows = staging ? staging_bytes / sh.kvpt : 0;
@@ -818,17 +887,15 @@ cudaError_t launch_attn_tc(const Shape& sh, const uint16_t* q, uint16_t* arena, 
   a.out = out; a.partials = partials; a.units = units; a.ctrl = ctrl;
   a.arena = reinterpret_cast<uint8_t*>(arena); a.staging = staging; a.kvpt = sh.kvpt;
   a.desc = desc; a.progress = progress; a.epoch = epoch;
+  a.k_new = k_new; a.v_new = v_new; a.feed = feed;
   static const int pack = [] { const char* e = getenv("S3_TC_PACK"); return e ? atoi(e) : 1; }();
   a.pmax = pack ? (a.G <= 8 ? 8 : 16) / a.G : 1;   // S3_TC_PACK=0: one KV head per tile (A/B)
   const dim3 grid(grid_attn), block(224);
   const int smem = attn_tc_smem();
-  if (a.G <= 8) {
-    if (a.pmax > 1) k_attn_tc<8, true><<<grid, block, smem, st>>>(maps, a);
-    else k_attn_tc<8, false><<<grid, block, smem, st>>>(maps, a);
-  } else {
-    if (a.pmax > 1) k_attn_tc<16, true><<<grid, block, smem, st>>>(maps, a);
-    else k_attn_tc<16, false><<<grid, block, smem, st>>>(maps, a);
-  }
+  const void* kfn = attn_tc_kernel_ptr(a.G <= 8 ? 8 : 16, a.pmax > 1, feed.ready != nullptr);
+  void* args[] = {(void*)&maps, (void*)&a};
+  cudaError_t le = cudaLaunchKernel(kfn, grid, block, args, (size_t)smem, st);
+  if (le != cudaSuccess) return le;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   return launch_combine(sh, splits, partials, out, ctrl, B, nl, grid_combine, st);

@@ -470,9 +470,10 @@ s3_status s3_kv_init(const s3_config* cfg, const s3_buffers* b, s3_ctx** out) {
     if (!attn_tc_supported(sh)) return bail("attn_variant 2 needs head_dim 128 and 2..16 query heads per KV head");
     for (int nc : {8, 16})
       for (bool pack : {false, true})
-        if (cudaFuncSetAttribute(attn_tc_kernel_ptr(nc, pack), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 attn_tc_smem()) != cudaSuccess)
-          return bail("attn_tc smem attribute");
+        for (bool feed : {false, true})
+          if (cudaFuncSetAttribute(attn_tc_kernel_ptr(nc, pack, feed), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   attn_tc_smem()) != cudaSuccess)
+            return bail("attn_tc smem attribute");
     ctx->grid_attn = ctx->num_sms;
   }
   if (cfg->attn_variant == 0 && attn_tma_stages(sh) >= 2) {
@@ -589,7 +590,7 @@ s3_status s3_decode_step(s3_ctx* ctx, int32_t l0, int32_t nl, const void* q, con
       if (ctx->stage_d2h[ctx->stage_cur])
         CK(cudaStreamWaitEvent(ctx->st, ctx->stage_d2h[ctx->stage_cur]->ev, 0), "wait staging");
     }
-    if (ctx->cfg.attn_variant == 2) {   // the tensor-core kernel reads the new row from the arena
+    if (ctx->cfg.attn_variant == 2 && !ctx->feed.ready) {   // the tensor-core kernel reads the new row from the arena
       CK(launch_append(ctx->sh, ctx->slots[ctx->cur], B, l0, nl, (const uint16_t*)k_new, (const uint16_t*)v_new,
                        (uint16_t*)ctx->buf.arena, ctx->st), "k_append");
       ctx->launches += 1;
@@ -619,10 +620,11 @@ s3_status s3_decode_step(s3_ctx* ctx, int32_t l0, int32_t nl, const void* q, con
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx->prof.on) { e0 = ctx->prof.get(); e1 = ctx->prof.get(); cudaEventRecord(e0, ctx->st); }
     if (ctx->cfg.attn_variant == 2)
-      CK(launch_attn_tc(ctx->sh, (const uint16_t*)q, (uint16_t*)ctx->buf.arena, ctx->cfg.arena_rows,
+      CK(launch_attn_tc(ctx->sh, (const uint16_t*)q, (const uint16_t*)k_new, (const uint16_t*)v_new,
+                        (uint16_t*)ctx->buf.arena, ctx->cfg.arena_rows,
                         ctx->buf.staging ? stage_ptr(ctx, ctx->stage_cur) : nullptr, stage_bytes(ctx), out, ctx->partials,
                         ctx->units, ctx->splits, ctx->desc, ctx->progress, ctx->attn_epoch, ctx->ctrl, B, l0, nl,
-                        ctx->grid_attn, ctx->grid_combine, ctx->st), "k_attn_tc");
+                        ctx->grid_attn, ctx->grid_combine, ctx->feed, ctx->st), "k_attn_tc");
     else
       CK(launch_attn(ctx->sh, (const uint16_t*)q, (const uint16_t*)k_new, (const uint16_t*)v_new,
                      (uint16_t*)ctx->buf.arena, ctx->buf.staging ? stage_ptr(ctx, ctx->stage_cur) : nullptr, out,
@@ -688,8 +690,10 @@ s3_status s3_decode_step_host(s3_ctx* ctx, const s3_host_io* io) {
   CK(cudaEventRecord(ctx->ev_hio_start, ctx->st), "event");
   CK(cudaStreamWaitEvent(ctx->hio, ctx->ev_hio_start, 0), "wait");
   StreamValue32Fn wv = write_value32(), wt = wait_value32();
-  const bool pipe = wv && ctx->cfg.attn_variant == 0 && attn_tma_stages(ctx->sh) >= 2;
-  const bool ce_out = pipe && wt && io->out_dev;   // device out + per-chunk D2H overlapped with the kernel
+  // the TMA-ring and tensor-core kernels wait on ready words; the register-streaming one cannot
+  const bool pipe = wv && ((ctx->cfg.attn_variant == 0 && attn_tma_stages(ctx->sh) >= 2) || ctx->cfg.attn_variant == 2);
+  // device out + per-chunk D2H overlapped with the kernel (counters in k_attn_tma's consumers)
+  const bool ce_out = pipe && wt && io->out_dev && ctx->cfg.attn_variant == 0;
   int32_t nch = pipe ? std::min(io->chunks ? io->chunks : 16, kMaxFeedChunks) : 1;
   nch = std::max(1, std::min(nch, B));
   const int32_t cb = (B + nch - 1) / nch;
@@ -722,12 +726,14 @@ s3_status s3_decode_step_host(s3_ctx* ctx, const s3_host_io* io) {
       else expect[b / cb] += warps * (uint32_t)L;
     }
   }
-  float* kout = static_cast<float*>(io->out_dev ? io->out_dev : out_dev);
+  // pipelined without counters: the kernels store `out` to mapped host memory as items finish
+  const bool dev_out = io->out_dev && (ce_out || !pipe);
+  float* kout = static_cast<float*>(dev_out ? io->out_dev : out_dev);
   const s3_status rc = s3_decode_step(ctx, 0, L, io->q_dev, io->k_new_dev, io->v_new_dev, io->eos_dev, kout);
   ctx->feed = Feed{};
   if (rc != S3_OK) return rc;
   const size_t wo = (size_t)ctx->sh.H * ctx->sh.D * 4;
-  if (io->out_dev) {
+  if (dev_out) {
     // enqueued after the attention and combine launches, so a wait here can never hold them up
     cudaStream_t ds = ce_out ? ctx->d2h : ctx->st;
     if (ce_out) {

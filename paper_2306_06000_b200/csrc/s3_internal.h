@@ -142,16 +142,17 @@ cudaError_t launch_verify(const Shape& sh, uint64_t seed, const DSlot* slots, in
                           const uint16_t* arena, unsigned long long* bad, cudaStream_t st);
 
 // grouped-KV tensor-core path (s3_attn_tc.cu), attn_variant 2
-bool attn_tc_supported(const Shape& sh);
-int attn_tc_smem();
-const void* attn_tc_kernel_ptr(int nc, bool pack);
 cudaError_t launch_append(const Shape& sh, const DSlot* slots, int32_t B, int32_t l0, int32_t nl,
                           const uint16_t* k_new, const uint16_t* v_new, uint16_t* arena, cudaStream_t st);
-cudaError_t launch_attn_tc(const Shape& sh, const uint16_t* q, uint16_t* arena, int64_t arena_rows,
-                           uint8_t* staging, int64_t staging_bytes, float* out, float* partials, const Unit* units,
-                           const Split* splits, const DepDesc* desc, unsigned long long* progress, uint32_t epoch,
-                           int32_t* ctrl, int32_t B, int32_t l0, int32_t nl, int32_t grid_attn, int32_t grid_combine,
-                           cudaStream_t st);
+bool attn_tc_supported(const Shape& sh);
+int attn_tc_smem();
+const void* attn_tc_kernel_ptr(int nc, bool pack, bool feed);
+
+cudaError_t launch_attn_tc(const Shape& sh, const uint16_t* q, const uint16_t* k_new, const uint16_t* v_new,
+                           uint16_t* arena, int64_t arena_rows, uint8_t* staging, int64_t staging_bytes, float* out,
+                           float* partials, const Unit* units, const Split* splits, const DepDesc* desc,
+                           unsigned long long* progress, uint32_t epoch, int32_t* ctrl, int32_t B, int32_t l0,
+                           int32_t nl, int32_t grid_attn, int32_t grid_combine, const Feed& feed, cudaStream_t st);
 cudaError_t launch_combine(const Shape& sh, const Split* splits, float* partials, float* out, int32_t* ctrl,
                            int32_t B, int32_t nl, int32_t grid, cudaStream_t st);
 

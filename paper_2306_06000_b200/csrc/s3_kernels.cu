@@ -343,8 +343,11 @@ __global__ void __launch_bounds__(1024) k_prep(PrepArgs a) {
 // unit's last stage).  Sources are the units' arena rows [off+r0, off+r1),
 // sorted and disjoint in unit order, so a binary search finds the first.
 // One warp per unit, lanes over its stages.
-// tc = 1 (k_attn_tc): stages are 128-row tiles and the new row is already in
-// the arena (k_append), so it is a source row of its unit and a tile row.
+// tc = 1 (k_attn_tc): stages are 128-row tiles and the new row is in the
+// arena (row off+len; written by k_append, or in a host-fed step by the
+// unit's producer warp just before its tiles load), so it is a source row of
+// its unit and a tile row: no other unit stores into it before this unit's
+// progress covers it.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_deps(const Unit* __restrict__ units, const int32_t* __restrict__ ctrl,
                                               DepDesc* __restrict__ desc, int32_t tc) {
