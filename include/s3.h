@@ -133,21 +133,23 @@ s3_status s3_decode_step(s3_ctx* ctx, int32_t l0, int32_t nl, const void* q, con
  *   out                  : pinned host fp32 [L][B][H][D];
  *   q_dev, k_new_dev, v_new_dev, eos_dev : caller-owned device landing
  *                          buffers of the same sizes;
- *   out_dev              : device fp32 [L][B][H][D] or NULL.  Given, the
- *                          kernels write out_dev and a second copy stream
- *                          moves each finished batch range to `out` (the
- *                          attention warps bump a per-range counter with a
- *                          release add; the stream waits on it with
- *                          cuStreamWaitValue32, so D2H overlaps the kernel;
- *                          split-K slots follow k_combine).  NULL: the
+ *   out_dev              : device fp32 [L][B][H][D] or NULL.  Given (and
+ *                          attn_variant 0), the kernels write out_dev and a
+ *                          second copy stream moves each finished batch
+ *                          range to `out` (the attention warps bump a
+ *                          per-range counter with a release add; the stream
+ *                          waits on it with cuStreamWaitValue32, so D2H
+ *                          overlaps the kernel; split-K slots follow
+ *                          k_combine).  NULL (or attn_variant 2): the
  *                          kernels store `out` directly over PCIe (mapped
  *                          pinned memory);
  *   chunks               : H2D pipeline depth (0 = 16, at most 64).
  * The H2D copies are split into `chunks` contiguous batch ranges on a copy
  * stream; after each range lands a stream write sets a ready word that the
  * attention kernel's producer waits on (acquire) before it touches that
- * range, so the copies overlap the HBM stream of earlier ranges.  Where the
- * attention variant cannot wait on ready words (attn_variant 1 / 2, or no
+ * range, so the copies overlap the HBM stream of earlier ranges (the
+ * tensor-core kernel also appends each unit's new K/V row itself).  Where
+ * the attention variant cannot wait on ready words (attn_variant 1, or no
  * stream-memory-operation support), the copies complete before the kernel.
  * All buffers are in use until cfg.stream reaches the end of this call's
  * work (synchronise cfg.stream before reading `out` or reusing inputs).
