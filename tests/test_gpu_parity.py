@@ -242,6 +242,9 @@ def test_bench_configuration_sampled():
     kvpt = 4 * L * H * D
     t = s3synth.make_trace(8192, seed=1, policy="short", p=0.1, max_seq_len=M)
     max_running = 8192
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()
     free_b, _ = torch.cuda.mem_get_info()
     R = int((free_b - max_running * L * H * D * 10 - (4 << 30) - (8 << 30)) // kvpt)
     eng = S3Engine(L, H, D, M, R, max_running, staging_bytes=4 << 30, host_store_bytes=8 << 30)
@@ -274,6 +277,59 @@ def test_bench_configuration_sampled():
         if step % 10 == 9:
             assert eng.verify_resident() == 0, step
     print("evictions", evictions)
+    eng.close()
+
+
+def test_bench_configuration_sampled_host_fed():
+    """The e2e leg's path at full size: the same C1-sized configuration driven
+    through s3_decode_step_host (pinned host q/k_new/v_new/eos, 16 chunks,
+    device out + per-chunk D2H); device landing buffers NaN-poisoned before
+    every step; sampled outputs from the HOST buffer against the oracle."""
+    from paper_2306_06000_b200.engine import S3Engine
+    L, H, D, M = 28, 16, 256, 2048
+    kvpt = 4 * L * H * D
+    t = s3synth.make_trace(8192, seed=2, policy="short", p=0.1, max_seq_len=M)
+    max_running = 8192
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()                       # arenas of earlier tests go back to the device
+    free_b, _ = torch.cuda.mem_get_info()
+    R = int((free_b - max_running * L * H * D * 10 - (4 << 30) - (8 << 30)) // kvpt)
+    eng = S3Engine(L, H, D, M, R, max_running, staging_bytes=4 << 30, host_store_bytes=8 << 30)
+    eng.submit(t.req_id, t.prompt, t.alloc, t.out)
+    eng.admit()
+    rows = min(max_running, 2 * eng.B + 64)
+    n = L * rows * H * D
+    hq, hk, hv = (torch.empty(n, dtype=torch.bfloat16, pin_memory=True) for _ in range(3))
+    ho = torch.empty(n, dtype=torch.float32, pin_memory=True)
+    he = torch.empty(max_running, dtype=torch.uint8, pin_memory=True)
+    rng = np.random.default_rng(1)
+    for step in range(24):
+        slots = eng.batch_view()
+        B = len(slots)
+        assert B <= rows
+        m = L * B * H * D
+        eng.synth_inputs()
+        hq[:m].copy_(eng.q[:m]); hk[:m].copy_(eng.k_new[:m]); hv[:m].copy_(eng.v_new[:m]); he[:B].copy_(eng.eos[:B])
+        eng.q.fill_(float("nan")); eng.k_new.fill_(float("nan")); eng.v_new.fill_(float("nan"))
+        eng.out.fill_(float("nan"))
+        torch.cuda.synchronize()
+        eng.decode_host(hq, hk, hv, he, ho)
+        torch.cuda.synchronize()
+        out = ho[:m].view(L, B, H, D)
+        assert torch.isfinite(out).all(), step
+        if step % 6 == 0:
+            lens = np.array([s[3] for s in slots])
+            pick = set(rng.choice(B, 6, replace=False).tolist()) | {int(lens.argmax()), int(lens.argmin()), B - 1}
+            for b in sorted(pick):
+                req, P, gen, ln, cap, off = slots[b]
+                for l in (0, 27):
+                    ref = oracle.attend_generated(L, H, D, M, 1, req, ln, l)
+                    err = rel_err(out[l, b].numpy().astype(np.float64)[None], ref[None])
+                    assert err <= TOL, (step, req, ln, l, err)
+        eng.evict_compact()
+        eng.admit()
+    assert eng.verify_resident() == 0
     eng.close()
 
 
