@@ -36,7 +36,13 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--case", default=None, help="run only cases whose name contains this")
     ap.add_argument("--lib", default=None, help="A/B: load this libs3.so build instead of the in-tree one")
+    ap.add_argument("--custom", action="append", default=[],
+                    help="extra case 'name:L,H,Hkv,D,B,P,variant' (repeatable)")
     args = ap.parse_args()
+    for c in args.custom:
+        name, vals = c.split(":")
+        v = [int(x) for x in vals.split(",")]
+        CASES.append((name, *v))
     if args.lib:
         from paper_2306_06000_b200 import s3 as abi
         abi.LIB_PATH = os.path.abspath(args.lib)
