@@ -59,6 +59,21 @@
 namespace s3 {
 namespace {
 
+// Diagnostic build only (-DTC_TRACE): SM-clock timestamps of CTA 0's tiles at
+// fixed points of each role (0 producer got a stage, 1 producer issued the
+// tile, 3 MMA saw the tile land, 4 MMA got P, 5 MMA committed O, 6 softmax got
+// S, 7 softmax handed over P), read back with s3_debug_tc_trace.
+#ifdef TC_TRACE
+constexpr int TC_TRACE_TILES = 8192;
+__device__ unsigned long long g_tc_trace[TC_TRACE_TILES * 8];
+#define TC_TRACE_AT(t, slot)                                                        \
+  do {                                                                             \
+    if (blockIdx.x == 0 && (t) < TC_TRACE_TILES) g_tc_trace[(t) * 8 + (slot)] = clock64(); \
+  } while (0)
+#else
+#define TC_TRACE_AT(t, slot) do { } while (0)
+#endif
+
 constexpr int TM = 128;                     // rows per tile (MMA M)
 constexpr int NQ = 16;                      // query columns per KV head (MMA N)
 constexpr int DH = 128;                     // head dim
@@ -433,6 +448,7 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
           for (int r = 0; r < nrows; r += TM) {
             const int st = t % NST;
             mb_wait(&S.kv_empty[st], ((uint32_t)(t / NST) & 1u) ^ 1u);
+            TC_TRACE_AT(t, 0);
             const int nv = min(TM, nrows - r);
             TcHdr& h = S.hdr[st];
             h.item = item; h.r0 = un.r0 + r; h.nvalid = nv;
@@ -476,6 +492,7 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
 #pragma unroll
             for (int kb = 0; kb < 2; ++kb) tma2d(sq + kb * 2048, &maps.q, kb * 64, qrow, &S.kv_full[st]);
             ++t;
+            TC_TRACE_AT(t - 1, 1);
           }
         }
       }
@@ -511,6 +528,7 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
         for (int t = 0;; ++t) {
           const int st = t % NST, st1 = (t + 1) % NST;
           mb_wait(&S.kv_full[st1], (uint32_t)((t + 1) / NST) & 1u);
+          TC_TRACE_AT(t + 1, 3);
           const bool end = S.hdr[st1].item < 0;
           if (!end) issue_s(t + 1);
           const bool first = S.hdr[st].flags & 1;
@@ -521,6 +539,7 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
           // one barrier per P buffer: the softmax may hand over P(t+1) before this
           // wait for P(t) runs, and a single barrier would then be two phases ahead
           mb_wait(&S.p_full[t & 1], (uint32_t)(t >> 1) & 1u);
+          TC_TRACE_AT(t, 4);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint8_t* sv = smem + st * STAGE_BYTES + KV_BYTES;
           const uint8_t* sp = pbuf + (t & 1) * PBUF_BYTES;
@@ -535,6 +554,7 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
           commit(&S.o_done);
           if (last) commit(&S.o_fin[ob]);
           commit(&S.kv_empty[st]);
+          TC_TRACE_AT(t, 5);
           if (end) { mb_arrive(&S.s_full[(t + 1) & 1]); break; }
         }
       }
@@ -673,6 +693,7 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
     for (int t = 0;; ++t) {
       const int sb = t & 1;
       mb_wait(&S.s_full[sb], (uint32_t)(t >> 1) & 1u);
+      if (lane == 0 && warp == 2) TC_TRACE_AT(t, 6);
       const TcHdr h = S.hdr[t % NST];
       if (h.item < 0) break;
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -766,6 +787,7 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mb_arrive(&S.p_full[t & 1]);
+      if (lane == 0 && warp == 2) TC_TRACE_AT(t, 7);
       if (pend) epilogue();                         // the previous item, overlapped with this tile's MMA
       if (h.flags & 2) {
         pend = true;
@@ -836,6 +858,12 @@ bool encode_2d(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, u
 }
 
 }  // namespace
+
+#ifdef TC_TRACE
+extern "C" int s3_debug_tc_trace(unsigned long long* host, int n) {
+  return (int)cudaMemcpyFromSymbol(host, g_tc_trace, sizeof(unsigned long long) * (size_t)std::min(n, TC_TRACE_TILES * 8));
+}
+#endif
 
 int attn_tc_smem() { return NST * STAGE_BYTES + 2 * PBUF_BYTES + (int)sizeof(TcSmem) + 1024; }
 const void* attn_tc_kernel_ptr(int nc, bool pack, bool feed) {
