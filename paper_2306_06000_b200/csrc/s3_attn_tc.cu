@@ -81,10 +81,14 @@ constexpr int NST = 3;                      // K/V ring stages
 constexpr int KV_BYTES = TM * DH * 2;       // 32 KB: two 64-column blocks of [128 rows x 128 B]
 constexpr int Q_BYTES = NQ * DH * 2;        // 4 KB:  two blocks of [16 rows x 128 B]
 constexpr int STAGE_BYTES = 2 * KV_BYTES + Q_BYTES;   // 68 KB (multiple of 1024)
-constexpr int P_BYTES = NQ * TM * 2;        // 4 KB:  two blocks (j 0-63, 64-127) of [16 rows x 128 B]
-constexpr int PBUF_BYTES = 2 * P_BYTES;     // P as bf16 hi + lo parts (P = hi + lo to ~16 bits)
+// P as bf16 hi + lo parts (P = hi + lo to ~16 bits), one MMA operand [hi | lo] of N = 32:
+// two K blocks (tile rows j 0-63, 64-127) of [32 rows x 128 B] (rows 0-15 hi, 16-31 lo)
+constexpr int PBLK_BYTES = 2 * NQ * 64 * 2;  // 4 KB per K block
+constexpr int PBUF_BYTES = 2 * PBLK_BYTES;   // 8 KB
 constexpr float LAZY_THR = 8.0f;            // rescale only if a score beats the running max by 2^8
-constexpr int TMEM_COLS = 64;               // S0 [0,16), S1 [16,32), O0 [32,48), O1 [48,64)
+// S0 [0,16), S1 [16,32); O buffer b at 32 + 32b: columns [0,16) = V.P_hi, [16,32) = V.P_lo
+constexpr int TMEM_COLS = 128;
+__host__ __device__ constexpr uint32_t ocol(int ob) { return 32u + 32u * (uint32_t)ob; }
 
 struct TcHdr {
   int32_t item, r0, nvalid, flags;          // flags: 1 = first tile of the item, 2 = last;
@@ -156,9 +160,9 @@ __device__ __forceinline__ uint64_t sdesc(const void* p, uint32_t lbo, uint32_t 
   return (uint64_t)((su32(p) >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
          ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
-// instruction descriptor: bf16 x bf16 -> f32, M 128, N 16
-__host__ __device__ constexpr uint32_t idesc(int a_mn_major) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn_major << 15) | ((uint32_t)(NQ >> 3) << 17) |
+// instruction descriptor: bf16 x bf16 -> f32, M 128, N = n
+__host__ __device__ constexpr uint32_t idesc(int a_mn_major, int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)a_mn_major << 15) | ((uint32_t)(n >> 3) << 17) |
          ((uint32_t)(TM >> 4) << 24);
 }
 __device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
@@ -505,7 +509,8 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
     // earlier MMA, so s_full(t+2) still implies O^T(t) is done (P buffer t&1
     // free) and o_done orders the rescale / epilogue reads of O^T.
     if (lane == 0) {
-      constexpr uint32_t id_s = idesc(0), id_o = idesc(1);
+      // S: N = 16 query columns; O: N = 32 ([P_hi | P_lo] in one MMA, halving the PV issue count)
+      constexpr uint32_t id_s = idesc(0, NQ), id_o = idesc(1, 2 * NQ);
       auto issue_s = [&](int t) {
         const int st = t % NST, sb = t & 1;
         mb_wait(&S.s_empty[sb], ((uint32_t)(t >> 1) & 1u) ^ 1u);
@@ -544,13 +549,11 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
           const uint8_t* sv = smem + st * STAGE_BYTES + KV_BYTES;
           const uint8_t* sp = pbuf + (t & 1) * PBUF_BYTES;
 #pragma unroll
-          for (int part = 0; part < 2; ++part)     // O^T += V^T . (P_hi + P_lo)^T over rows in steps of 16
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-              const int kb = k >> 2, ko = (k & 3) * 32;
-              mma(tmem + 32 + 16 * ob, sdesc(sv + k * 2048, 16384, 1024),
-                  sdesc(sp + part * P_BYTES + kb * 2048 + ko, 16, 1024), id_o, (first && part == 0 && k == 0) ? 0u : 1u);
-            }
+          for (int k = 0; k < 8; ++k) {              // [O_hi | O_lo]^T += V^T . [P_hi | P_lo]^T, rows in steps of 16
+            const int kb = k >> 2, ko = (k & 3) * 32;
+            mma(tmem + ocol(ob), sdesc(sv + k * 2048, 16384, 1024), sdesc(sp + kb * PBLK_BYTES + ko, 16, 1024), id_o,
+                (first && k == 0) ? 0u : 1u);
+          }
           commit(&S.o_done);
           if (last) commit(&S.o_fin[ob]);
           commit(&S.kv_empty[st]);
@@ -670,11 +673,14 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
       const int ob = ph.iseq & 1;
       mb_wait(&S.o_fin[ob], (uint32_t)(ph.iseq >> 1) & 1u);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      float o[NC];
-      tmem_ld<NC>(lane_base + 32 + 16 * ob, o);
+      float o[NC], olo[NC];
+      tmem_ld<NC>(lane_base + ocol(ob), o);
+      tmem_ld<NC>(lane_base + ocol(ob) + NQ, olo);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mb_arrive(&S.o_free[ob]);
+#pragma unroll
+      for (int c = 0; c < NC; ++c) o[c] += olo[c];
       const int d = row;
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
@@ -751,7 +757,7 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
         rescale = !first;
       }
       // P = 2^(s - m) as bf16 hi + lo; row c (query column), column j = row; 128B swizzle
-      uint8_t* sp = pbuf + (t & 1) * PBUF_BYTES + (row >> 6) * 2048;
+      uint8_t* sp = pbuf + (t & 1) * PBUF_BYTES + (row >> 6) * PBLK_BYTES;
       const uint32_t jj2 = (uint32_t)(row & 63) * 2u;
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
@@ -762,7 +768,7 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
         const uint32_t byte = (uint32_t)c * 128u + jj2;
         const uint32_t sw = byte ^ ((uint32_t)(c & 7) << 4);
         *reinterpret_cast<__nv_bfloat16*>(sp + sw) = hi;
-        *reinterpret_cast<__nv_bfloat16*>(sp + P_BYTES + sw) = lo;
+        *reinterpret_cast<__nv_bfloat16*>(sp + NQ * 128 + sw) = lo;   // row 16 + c: same swizzle phase
       }
       if (!valid && rs < ((h.nvalid + 15) & ~15)) {  // loaded rows past the slot's resident rows: V := 0
         uint8_t* sv = smem + (t % NST) * STAGE_BYTES + KV_BYTES;
@@ -777,11 +783,13 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
       if (t > 0) mb_wait(&S.o_done, (uint32_t)(t - 1) & 1u);
       if (rescale) {                                // O^T *= corr once the previous tile's MMA is done
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        float o[NC];
-        tmem_ld<NC>(lane_base + 32 + 16 * ob, o);
+        float o[NC], olo[NC];
+        tmem_ld<NC>(lane_base + ocol(ob), o);
+        tmem_ld<NC>(lane_base + ocol(ob) + NQ, olo);
 #pragma unroll
-        for (int c = 0; c < NC; ++c) o[c] *= corr[c];
-        tmem_st<NC>(lane_base + 32 + 16 * ob, o);
+        for (int c = 0; c < NC; ++c) { o[c] *= corr[c]; olo[c] *= corr[c]; }
+        tmem_st<NC>(lane_base + ocol(ob), o);
+        tmem_st<NC>(lane_base + ocol(ob) + NQ, olo);
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
