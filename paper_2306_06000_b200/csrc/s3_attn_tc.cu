@@ -148,6 +148,13 @@ __device__ __forceinline__ unsigned long long ld_acq_u64(const unsigned long lon
 __device__ __forceinline__ void st_rlx_u64(unsigned long long* p, unsigned long long v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ void tma3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
+          "r"(su32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar))
+      : "memory");
+}
 __device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
@@ -494,7 +501,7 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
               }
             }
 #pragma unroll
-            for (int kb = 0; kb < 2; ++kb) tma2d(sq + kb * 2048, &maps.q, kb * 64, qrow, &S.kv_full[st]);
+            tma3d(sq, &maps.q, 0, qrow, 0, &S.kv_full[st]);   // both 64-column blocks of the 16 q rows
             ++t;
             TC_TRACE_AT(t - 1, 1);
           }
@@ -853,6 +860,20 @@ EncodeTiledFn encoder() {
 }
 
 // 2-D bf16 map: `cols` elements per row, `rows` rows, `pitch` bytes; boxes of 64 x box_rows, 128B swizzle
+// q as a 3-D bf16 map {64 columns, rows, 2 column blocks (stride 128 B)}: one box of 16 rows lands
+// as [block][16 rows][64] -- the layout the S MMA reads -- in one instruction instead of two
+bool encode_q3(CUtensorMap* m, const void* base, uint64_t rows, uint64_t pitch) {
+  EncodeTiledFn enc = encoder();
+  if (!enc) return false;
+  cuuint64_t dims[3] = {64, rows, 2};
+  cuuint64_t strides[2] = {pitch, 128};
+  cuuint32_t box[3] = {64, 16, 2};
+  cuuint32_t es[3] = {1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool encode_2d(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint64_t pitch, uint32_t box_rows = 16) {
   EncodeTiledFn enc = encoder();
   if (!enc) return false;
@@ -916,7 +937,7 @@ cudaError_t launch_attn_tc(const Shape& sh, const uint16_t* q, const uint16_t* k
       maps.stage[i] = maps.kv[i];
     }
   }
-  if (!encode_2d(&maps.q, q, (uint64_t)sh.D, (uint64_t)nl * B * sh.H, (uint64_t)sh.D * 2)) return cudaErrorInvalidValue;
+  if (!encode_q3(&maps.q, q, (uint64_t)nl * B * sh.H, (uint64_t)sh.D * 2)) return cudaErrorInvalidValue;
   TcArgs a;
   a.H = sh.H; a.Hkv = sh.Hkv; a.G = sh.H / sh.Hkv; a.B = B; a.l0 = l0; a.nl = nl;
   a.qscale = 1.4426950408889634f / sqrtf((float)sh.D);
