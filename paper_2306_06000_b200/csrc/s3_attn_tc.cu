@@ -500,7 +500,6 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
                 }
               }
             }
-#pragma unroll
             tma3d(sq, &maps.q, 0, qrow, 0, &S.kv_full[st]);   // both 64-column blocks of the 16 q rows
             ++t;
             TC_TRACE_AT(t - 1, 1);
