@@ -1,4 +1,4 @@
-# tensor-core ping-pong softmax groups (after N=32 PV): parity, trace, A/B
+# tensor-core interleaved tile layout, one 4-D TMA per K/V segment: parity, trace, A/B
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
 timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "tensor_cores" > gpurun_out/pytest_tc.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_tc.log
