@@ -42,10 +42,11 @@ def u16(t: torch.Tensor) -> np.ndarray:
 
 def lockstep(trace, L, H, D, R, C=0, S=0, max_running=4096, staging=True, feed_oracle_inputs=False,
              max_steps=100000, check_arena=True, attn_variant=0, compact_mode=0, poison=False,
-             compact_policy=0, Hkv=0, host_io=False, chunks=0, device_out=False):
+             compact_policy=0, Hkv=0, host_io=False, chunks=0, device_out=False, staging_mult=1):
     from paper_2306_06000_b200.engine import S3Engine
     eng = S3Engine(L, H, D, trace.max_seq_len, R, max_running, chunk_rows=C, move_chunk_bytes=S,
-                   staging_bytes=None if staging else 0, host_store_bytes=64 << 20, attn_variant=attn_variant,
+                   staging_bytes=(None if staging_mult == 1 else staging_mult * trace.max_seq_len * 4 * L * (Hkv or H) * D)
+                   if staging else 0, host_store_bytes=64 << 20, attn_variant=attn_variant,
                    compact_mode=compact_mode, compact_policy=compact_policy, num_kv_heads=Hkv)
     eng.profile(True)
     orc = oracle.Oracle(L, H, D, trace.max_seq_len, R, max_running=max_running, compact_policy=compact_policy,
@@ -556,3 +557,14 @@ def test_host_fed_decode_step(variant, chunks, C, dev_out):
     r = lockstep(t, 2, H, D, 2048, C=C, host_io=True, chunks=chunks, attn_variant=variant, Hkv=Hkv,
                  device_out=dev_out)
     assert r["steps"] > 20 and r["worst"] <= TOL
+
+
+@pytest.mark.parametrize("variant,Hkv,D,H", [(0, 0, 64, 4), (2, 2, 128, 8)])
+def test_double_buffered_staging_heavy_evictions(variant, Hkv, D, H):
+    """Staging large enough for two maximal evictions is used as two halves
+    that alternate per step (a step's evictees are staged while the previous
+    step's D2H still reads the other half).  Heavy short predictions; every
+    evicted host copy, resident row and output checked against the oracle."""
+    t = s3synth.make_trace(60, seed=11, policy="short", p=0.6, max_seq_len=192, prompt_max=48)
+    r = lockstep(t, 2, H, D, 1200, C=32, attn_variant=variant, Hkv=Hkv, staging_mult=3, poison=True)
+    assert r["evictions"] >= 20 and r["fused_steps"] >= 0.9 * r["steps"]
