@@ -147,6 +147,24 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
 }
 // 8 bf16 values (one 16-byte vector) for element group d8 of (req,l,kv,pos,h).
 // tag 0 (K/V rows) indexes the Hkv KV heads, tag 1 (q) the H query heads.
+// 8 generator values from counter g: bytes of splitmix64 minus 128, times scale
+__device__ __forceinline__ uint4 gen8_at(uint64_t seed, uint64_t tag, uint64_t g, float scale) {
+  const uint64_t z = splitmix64(seed ^ (tag << 60) ^ g);
+  uint32_t w[4];
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const int k0 = (int)((z >> (16 * p)) & 0xFF) - 128;
+    const int k1 = (int)((z >> (16 * p + 8)) & 0xFF) - 128;
+    const uint32_t b0 = __float_as_uint((float)k0 * scale) >> 16;
+    const uint32_t b1 = __float_as_uint((float)k1 * scale) >> 16;
+    w[p] = b0 | (b1 << 16);
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+// counter of the first 16-B vector of row (req, l, kv, pos): g = ((((req L + l) 2 + kv) M + pos) nh + h) D/8 + d8
+__device__ __forceinline__ uint64_t gen_row_base(const Shape& sh, uint64_t nh, int64_t req, int l, int kv, int pos) {
+  return ((((uint64_t)req * sh.L + l) * 2u + kv) * (uint64_t)sh.max_len + pos) * nh * (uint64_t)(sh.D / 8);
+}
 __device__ __forceinline__ uint4 gen8(const Shape& sh, uint64_t seed, uint64_t tag, int64_t req,
                                       int l, int kv, int pos, int h, int d8, float scale) {
   const uint64_t nh = tag == 0 ? (uint64_t)sh.Hkv : (uint64_t)sh.H;
@@ -1291,15 +1309,18 @@ __global__ void __launch_bounds__(256) k_synth(Shape sh, uint64_t seed, const DS
     const int li = (int)(row / B), b = (int)(row - (int64_t)li * B);
     const DSlot sl = slots[b];
     const int l = l0 + li;
+    // vector t of a row has counter row_base + t (h D/8 + d8 == t), so only the row bases are multiplied out
+    const uint64_t gq = gen_row_base(sh, (uint64_t)sh.H, sl.req, l, 0, sl.len);
+    const uint64_t gk = gen_row_base(sh, (uint64_t)sh.Hkv, sl.req, l, 0, sl.len);
+    const uint64_t gv = gen_row_base(sh, (uint64_t)sh.Hkv, sl.req, l, 1, sl.len);
     for (int t = threadIdx.x; t < nq + nk; t += blockDim.x) {
       if (t < nq) {                                     // q: [nl][B][H][D]
-        const int h = t / D8, d8 = t - h * D8;
-        st_v4(q + (row * nq + t) * 8, gen8(sh, seed, 1, sl.req, l, 0, sl.len, h, d8, 1.f / 32.f));
+        st_v4(q + (row * nq + t) * 8, gen8_at(seed, 1, gq + (uint64_t)t, 1.f / 32.f));
       } else {                                          // k_new, v_new: [nl][B][Hkv][D]
-        const int u = t - nq, h = u / D8, d8 = u - h * D8;
+        const int u = t - nq;
         const int64_t o = (row * nk + u) * 8;
-        st_v4(k + o, gen8(sh, seed, 0, sl.req, l, 0, sl.len, h, d8, 1.f / 128.f));
-        st_v4(v + o, gen8(sh, seed, 0, sl.req, l, 1, sl.len, h, d8, 1.f / 128.f));
+        st_v4(k + o, gen8_at(seed, 0, gk + (uint64_t)u, 1.f / 128.f));
+        st_v4(v + o, gen8_at(seed, 0, gv + (uint64_t)u, 1.f / 128.f));
       }
     }
   }
