@@ -1283,15 +1283,14 @@ __global__ void __launch_bounds__(256) k_fill(Shape sh, uint64_t seed, const DSl
   const int D8 = sh.D / 8;
   const int per_row = sh.L * 2 * sh.Hkv * D8;   // 16-byte vectors per row
   const int total = (p1 - p0) * per_row;
+  const int seg = sh.Hkv * D8;                  // vectors of one (layer, K/V) piece: counter base + u
   for (int i = threadIdx.x; i < total; i += blockDim.x) {
     const int pos = p0 + i / per_row;
-    int r = i % per_row;
-    const int d8 = r % D8; r /= D8;
-    const int h = r % sh.Hkv; r /= sh.Hkv;
-    const int kv = r % 2;
-    const int l = r / 2;
-    const uint4 v = gen8(sh, seed, 0, sl.req, l, kv, pos, h, d8, 1.f / 128.f);
-    st_v4(arena + ((int64_t)sl.off + pos) * sh.row_elems + ((int64_t)(l * 2 + kv) * sh.Hkv + h) * sh.D + d8 * 8, v);
+    const int r = i % per_row;
+    const int lkv = r / seg, u = r - lkv * seg;   // lkv = 2 l + kv; u = h D/8 + d8
+    const uint4 v = gen8_at(seed, 0, gen_row_base(sh, (uint64_t)sh.Hkv, sl.req, lkv >> 1, lkv & 1, pos) + (uint64_t)u,
+                            1.f / 128.f);
+    st_v4(arena + ((int64_t)sl.off + pos) * sh.row_elems + (int64_t)r * 8, v);
   }
 }
 
