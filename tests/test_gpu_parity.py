@@ -334,14 +334,17 @@ def test_bench_configuration_sampled_host_fed():
     eng.close()
 
 
-def test_layer_group_calls():
+@pytest.mark.parametrize("H,Hkv,variant", [(4, 0, 0), (8, 2, 2)])
+def test_layer_group_calls(H, Hkv, variant):
     """s3_decode_step over layer groups [0,1), [1,3), [3,4): the append and the
-    detection happen only with the last group; results equal one full call."""
+    detection happen only with the last group; results equal one full call
+    (CUDA-core MHA and the tensor-core grouped-KV kernel)."""
     from paper_2306_06000_b200.engine import S3Engine
-    L, H, D, M, R = 4, 4, 128, 96, 600
+    L, D, M, R = 4, 128, 96, 600
     t = s3synth.make_trace(30, seed=12, policy="short", p=0.3, max_seq_len=M, prompt_max=20)
-    eng = S3Engine(L, H, D, M, R, 64, chunk_rows=8, move_chunk_bytes=2048, host_store_bytes=16 << 20)
-    orc = oracle.Oracle(L, H, D, M, R, max_running=64)
+    eng = S3Engine(L, H, D, M, R, 64, chunk_rows=8, move_chunk_bytes=2048, host_store_bytes=16 << 20,
+                   num_kv_heads=Hkv, attn_variant=variant)
+    orc = oracle.Oracle(L, H, D, M, R, max_running=64, Hkv=Hkv)
     eng.submit(t.req_id, t.prompt, t.alloc, t.out)
     orc.submit(t.req_id, t.prompt, t.alloc)
     assert eng.admit()[1] == orc.admit()
@@ -353,9 +356,10 @@ def test_layer_group_calls():
         q, k, v, eos = orc.make_inputs(t.out)
         ref, _ = orc.decode(q, k, v, eos)
         eng.synth_inputs()
+        KD = (Hkv or H) * D
         for (l0, nl) in [(0, 1), (1, 2), (3, 1)]:
-            o = l0 * B * HD
-            eng.decode(l0, nl, q=eng.q[o:], k_new=eng.k_new[o:], v_new=eng.v_new[o:], out=eng.out[o:])
+            o, ok = l0 * B * HD, l0 * B * KD
+            eng.decode(l0, nl, q=eng.q[o:], k_new=eng.k_new[ok:], v_new=eng.v_new[ok:], out=eng.out[o:])
         got = eng.out[:L * B * HD].cpu().numpy().reshape(L, B, H, D).astype(np.float64)
         assert rel_err(got, ref) <= TOL
         rg = eng.evict_compact()
