@@ -542,16 +542,18 @@ def test_grouped_query_kv_tensor_cores(H, Hkv, C, policy, mode, staging):
         assert r["fused_steps"] == 0
 
 
-@pytest.mark.parametrize("variant,chunks,C,dev_out", [(0, 0, 16, False), (0, 64, 0, False), (0, 3, 16, False),
-                                                     (1, 0, 16, False), (2, 0, 16, False), (0, 0, 16, True),
-                                                     (0, 5, 8, True), (0, 64, 0, True), (2, 0, 16, True)])
-def test_host_fed_decode_step(variant, chunks, C, dev_out):
+@pytest.mark.parametrize("variant,chunks,C,dev_out,mode", [
+    (0, 0, 16, False, 0), (0, 64, 0, False, 0), (0, 3, 16, False, 0), (1, 0, 16, False, 1), (2, 0, 16, False, 0),
+    (0, 0, 16, True, 0), (0, 5, 8, True, 0), (0, 64, 0, True, 0), (2, 0, 16, True, 0), (0, 0, 16, True, 1),
+    (2, 4, 16, False, 1)])
+def test_host_fed_decode_step(variant, chunks, C, dev_out, mode):
     """s3_decode_step_host: pinned host q/k_new/v_new/eos in, pinned host out,
     H2D pipelined with the attention kernel through per-chunk ready words
     (TMA variant) or completed before it (other variants); out either stored
     by the kernels over PCIe or (dev_out) copied per finished chunk by a
     stream that waits on the kernel's per-chunk counters, split-K slots after
-    k_combine (small C makes many of them).  Device landing buffers and the
+    k_combine (small C makes many of them); mode 1 = the separate k_move
+    row shift instead of the fused one.  Device landing buffers and the
     device out are NaN-poisoned before every step."""
     if variant == 2:
         H, Hkv, D = 8, 2, 128
@@ -559,7 +561,7 @@ def test_host_fed_decode_step(variant, chunks, C, dev_out):
         H, Hkv, D = 4, 0, 64
     t = s3synth.make_trace(48, seed=7, policy="short", p=0.3, max_seq_len=256, prompt_max=64)
     r = lockstep(t, 2, H, D, 2048, C=C, host_io=True, chunks=chunks, attn_variant=variant, Hkv=Hkv,
-                 device_out=dev_out)
+                 device_out=dev_out, compact_mode=mode)
     assert r["steps"] > 20 and r["worst"] <= TOL
 
 
