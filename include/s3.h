@@ -88,7 +88,7 @@ typedef struct {
 } s3_config;
 
 typedef struct {                            /* caller-owned memory                             */
-  void* arena;      int64_t arena_bytes;    /* device, >= R * kvpt, 256-B aligned              */
+  void* arena;      int64_t arena_bytes;    /* device, >= (R + 8) * kvpt (8 guard rows), 256-B aligned */
   void* workspace;  int64_t workspace_bytes;/* device, >= s3_workspace_query's figure          */
   void* staging;    int64_t staging_bytes;  /* device eviction staging (0 => synchronous D2H)  */
   void* host_store; int64_t host_store_bytes; /* pinned host memory for evicted KV             */

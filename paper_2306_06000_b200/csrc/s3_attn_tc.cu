@@ -86,9 +86,13 @@ constexpr int STAGE_BYTES = 2 * KV_BYTES + Q_BYTES;   // 68 KB (multiple of 1024
 constexpr int PBLK_BYTES = 2 * NQ * 64 * 2;  // 4 KB per K block
 constexpr int PBUF_BYTES = 2 * PBLK_BYTES;   // 8 KB
 constexpr float LAZY_THR = 8.0f;            // rescale only if a score beats the running max by 2^8
-// S0 [0,16), S1 [16,32); O buffer b at 32 + 32b: columns [0,16) = V.P_hi, [16,32) = V.P_lo
+// Two softmax groups ("ping-pong"): group g takes the items with iseq & 1 == g, so while one
+// group runs a tile's softmax and epilogue the other runs its own.  TMEM: S slot (g, b) at
+// columns (2g + b)*16 in [0, 64); O buffer g at 64 + 32g: [0,16) = V.P_hi, [16,32) = V.P_lo.
 constexpr int TMEM_COLS = 128;
-__host__ __device__ constexpr uint32_t ocol(int ob) { return 32u + 32u * (uint32_t)ob; }
+__host__ __device__ constexpr uint32_t scol(int g, int b) { return (uint32_t)((2 * g + b) * 16); }
+__host__ __device__ constexpr uint32_t ocol(int g) { return 64u + 32u * (uint32_t)g; }
+constexpr int TC_THREADS = 32 * 11;   // producer, MMA, 4 softmax (group 0), storer, 4 softmax (group 1)
 
 struct TcHdr {
   int32_t item, r0, nvalid, flags;          // flags: 1 = first tile of the item, 2 = last;
@@ -104,11 +108,14 @@ constexpr uint32_t TC_PROG_FULL = 0x80000000u;
 __device__ __forceinline__ int hdr_lognp(const TcHdr& h) { return (h.flags >> 8) & 15; }
 constexpr int TC_HEAD_STRIDE = 1 << 16;      // progress = head * 2^16 + rows (unit rows < 2^16)
 
-struct alignas(16) TcSmem {                 // after the ring and the two P buffers
-  uint64_t kv_full[NST], kv_empty[NST], s_full[2], s_empty[2], p_full[2], o_done, o_fin[2], o_free[2];
+struct alignas(16) TcSmem {                 // after the ring and the two P buffers (one per group)
+  uint64_t kv_full[NST], kv_empty[NST];
+  uint64_t s_full[2][2], s_empty[2][2];     // [group][S slot]; s_full: MMA commit + the MMA thread's arrive
+  uint64_t p_full[2], o_done[2], o_fin[2], o_free[2];   // [group] (= O buffer = item parity)
   alignas(16) TcHdr hdr[NST];               // hdr.dep is a 16-B bulk-copy destination
-  float red[2][4][NQ];
-  int32_t flag[4];
+  float red[2][2][4][NQ];                   // [group][max / sum][warp][column]
+  int32_t flag[2][4];
+  int32_t gt[2][2];                         // ring tile index in group g's S slot b (-1: no more tiles)
   uint32_t tmem_base;
 };
 
@@ -135,11 +142,6 @@ __device__ __forceinline__ void bulk_g2s16(void* dst, const void* src, uint64_t*
                "l"(src), "r"(su32(bar))
                : "memory");
 }
-__device__ __forceinline__ void tma2d_store(const CUtensorMap* map, int c0, int c1, const void* src) {
-  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(map), "r"(c0),
-               "r"(c1), "r"(su32(src))
-               : "memory");
-}
 __device__ __forceinline__ unsigned long long ld_acq_u64(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -148,18 +150,23 @@ __device__ __forceinline__ unsigned long long ld_acq_u64(const unsigned long lon
 __device__ __forceinline__ void st_rlx_u64(unsigned long long* p, unsigned long long v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+__device__ __forceinline__ void tma4d(void* dst, const CUtensorMap* map, int c1, int c2, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];" ::
+          "r"(su32(dst)),
+      "l"(map), "r"(0), "r"(c1), "r"(c2), "r"(0), "r"(su32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma4d_store(const CUtensorMap* map, int c1, int c2, const void* src) {
+  asm volatile("cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%1, %2, %3, %4}], [%5];" ::"l"(map), "r"(0),
+               "r"(c1), "r"(c2), "r"(0), "r"(su32(src))
+               : "memory");
+}
 __device__ __forceinline__ void tma3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::
           "r"(su32(dst)),
       "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(su32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void tma2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
-          "r"(su32(dst)),
-      "l"(map), "r"(c0), "r"(c1), "r"(su32(bar))
       : "memory");
 }
 // UMMA shared-memory descriptor: 128B swizzle, version 1 (sm_100)
@@ -235,7 +242,8 @@ __device__ __forceinline__ float ex2f(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-__device__ __forceinline__ void softmax_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+// named barrier of one softmax group (4 warps); ids 1, 2
+__device__ __forceinline__ void softmax_bar(int grp) { asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory"); }
 
 // Column-wise reduction of 16 values per lane over the 128 softmax lanes.
 // Within a warp a transposed butterfly halves the vector at each step (8 + 4
@@ -245,7 +253,7 @@ template <bool MAX>
 __device__ __forceinline__ float rop(float x, float y) { return MAX ? fmaxf(x, y) : x + y; }
 
 template <bool MAX, int NC>
-__device__ __forceinline__ void col_reduce(float (&v)[NC], float (&red)[4][NQ], int wq, int lane) {
+__device__ __forceinline__ void col_reduce(float (&v)[NC], float (&red)[4][NQ], int wq, int lane, int grp) {
   // NC = 16: 8 + 4 + 2 + 1 + 1 shuffles; NC = 8: 4 + 2 + 1 + 1 + 1
   float a8[8], a4[4], a2[2], a1;
   const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4, h2 = lane & 2;
@@ -293,22 +301,26 @@ __device__ __forceinline__ void col_reduce(float (&v)[NC], float (&red)[4][NQ], 
     col = (h16 ? 4 : 0) + (h8 ? 2 : 0) + (h4 ? 1 : 0);
   }
   if (!(lane & (NC == 16 ? 1 : 3))) red[wq][col] = a1;
-  softmax_bar();
+  softmax_bar(grp);
 #pragma unroll
   for (int c = 0; c < NC; ++c) v[c] = rop<MAX>(rop<MAX>(red[0][c], red[1][c]), rop<MAX>(red[2][c], red[3][c]));
-  softmax_bar();
+  softmax_bar(grp);
 }
 
-// tensor maps: arena and staging rows in boxes of 128 / 64 / 32 / 16 / 8 rows x
-// 64 columns (a tile's valid 8-row groups come in as a binary decomposition, so
-// a full tile is one box per 64-column block; rows between the last 8-row group
-// and the 16-row MMA step are zeroed (V) / masked (K) by the softmax warps)
-constexpr int NBOX = 5;         // loads: 128/64/32/16/8-row boxes (8-row granularity);
-constexpr int NBOX_STORE = 4;   // stores: whole 16-row groups, the ragged rest by a warp copy
+// Shared-memory tile layout: 16 groups of 8 rows; group j holds both 64-column
+// blocks as adjacent 1 KB 128B-swizzle atoms, [j][block][8 rows][128 B], so a
+// tile's K (or V) rows for one KV head arrive in ONE 4-D TMA box
+// {64 columns, 8 rows, 2 blocks, n groups} whose row-group dimension (stride
+// 8 rows) overlaps the row dimension -- a box may start at any row (see
+// tools/tma_probe/tma4d.cu).  The UMMA descriptors read it with an 8-row-group
+// stride of 2 KB and the second column block 1 KB after the first.
+constexpr int NGRP = TM / 8;     // 8-row groups per tile
+constexpr int NSTB = 5;          // store boxes of 16 / 8 / 4 / 2 / 1 groups (valid rows only)
 struct TcMaps {
-  CUtensorMap kv[NBOX];      // box rows 128 >> i
-  CUtensorMap stage[NBOX];
-  CUtensorMap q;             // 16 rows
+  CUtensorMap kvg[NGRP];         // loads: box of n + 1 groups
+  CUtensorMap st_kv[NSTB];       // row-shift stores into the arena: box of 16 >> i groups
+  CUtensorMap st_stage[NSTB];    // evictee stores into staging
+  CUtensorMap q;                 // 16 q rows x both column blocks
 };
 
 struct TcArgs {
@@ -357,7 +369,7 @@ __device__ __forceinline__ uint4 ld_cg16(const void* p) {
 // PACK: short units may pack several KV heads into one tile (NC / G >= 2)
 // FEED: host-fed step (the producer warp waits on ready words and appends the new rows)
 template <int NC, bool PACK, bool FEED>
-__global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMaps maps, TcArgs a) {
+__global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant__ TcMaps maps, TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-B alignment for the 128B-swizzle atoms, by pointer arithmetic so the
   // compiler keeps the shared-memory address space (LDS/STS, not generic LD/ST)
@@ -369,10 +381,13 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
   const bool fused = a.ctrl[CTRL_FUSED] != 0;
   if (tid == 0) {
     for (int i = 0; i < NST; ++i) { mb_init(&S.kv_full[i], 1); mb_init(&S.kv_empty[i], fused ? 2 : 1); }
-    for (int i = 0; i < 2; ++i) { mb_init(&S.s_full[i], 1); mb_init(&S.s_empty[i], 4); }
-    for (int i = 0; i < 2; ++i) mb_init(&S.p_full[i], 4);
-    mb_init(&S.o_done, 1);
-    for (int i = 0; i < 2; ++i) { mb_init(&S.o_fin[i], 1); mb_init(&S.o_free[i], 4); }
+    for (int g = 0; g < 2; ++g) {
+      for (int b = 0; b < 2; ++b) { mb_init(&S.s_full[g][b], 2); mb_init(&S.s_empty[g][b], 4); }
+      mb_init(&S.p_full[g], 4);
+      mb_init(&S.o_done[g], 1);
+      mb_init(&S.o_fin[g], 1);
+      mb_init(&S.o_free[g], 4);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // V buffers start at zero: rows a tile does not load keep finite (zero or earlier valid) data
@@ -470,35 +485,19 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
             const int glast = g + np - 1;  // heads g..glast are read up to r + nv rows once this tile lands
             h.prog = (uint32_t)(glast * TC_HEAD_STRIDE + r + nv) |
                      (glast == a.Hkv - 1 && r + TM >= nrows ? TC_PROG_FULL : 0u);
-            // load granularity: 8-row groups (one 128B-swizzle atom) in the PACK kernel, whose
-            // items are short or G <= 8; 16-row groups otherwise (measured faster for MQA)
-            constexpr int GR = PACK ? 8 : 16;
-            const int groups = (nv + GR - 1) / GR;
+            const int groups = (nv + 7) / 8;   // 8-row groups (one 128B-swizzle atom per column block)
             uint8_t* sk = smem + st * STAGE_BYTES;
             uint8_t* sv = sk + KV_BYTES;
             uint8_t* sq = sv + KV_BYTES;
             const bool dep = fused && mv;
-            mb_expect(&S.kv_full[st], (uint32_t)(np * groups * GR * 128 * 2 * 2 + Q_BYTES + (dep ? 16 : 0)));
+            mb_expect(&S.kv_full[st], (uint32_t)(np * groups * 8 * 128 * 2 * 2 + Q_BYTES + (dep ? 16 : 0)));
             if (dep) bulk_g2s16(&h.dep, a.desc + un.stage_base + r / TM, &S.kv_full[st]);
             const int row0 = un.off + un.r0 + r;
-            for (int sgi = 0; sgi < np; ++sgi) {
+            for (int sgi = 0; sgi < np; ++sgi) {    // one 4-D box per segment for K and one for V
               const int colk = (a.l0 + li) * row_cols + (g + sgi) * DH;
-              const int colv = colk + a.Hkv * DH;
-              const int sro = sgi * seg * 128;   // segment's first shared-memory row (bytes)
-              int done = 0;                 // GR-row groups, largest boxes first
-#pragma unroll
-              for (int i = 0; i < (PACK ? NBOX : NBOX - 1); ++i) {
-                const int bg = (TM / GR) >> i;
-                if (groups - done >= bg) {
-                  const CUtensorMap* m = &maps.kv[i];
-#pragma unroll
-                  for (int kb = 0; kb < 2; ++kb) {
-                    tma2d(sk + kb * 16384 + sro + done * GR * 128, m, colk + kb * 64, row0 + done * GR, &S.kv_full[st]);
-                    tma2d(sv + kb * 16384 + sro + done * GR * 128, m, colv + kb * 64, row0 + done * GR, &S.kv_full[st]);
-                  }
-                  done += bg;
-                }
-              }
+              const int sgo = sgi * (seg / 8) * 2048;   // segment's first group
+              tma4d(sk + sgo, &maps.kvg[groups - 1], row0, colk / 64, &S.kv_full[st]);
+              tma4d(sv + sgo, &maps.kvg[groups - 1], row0, (colk + a.Hkv * DH) / 64, &S.kv_full[st]);
             }
             tma3d(sq, &maps.q, 0, qrow, 0, &S.kv_full[st]);   // both 64-column blocks of the 16 q rows
             ++t;
@@ -510,61 +509,76 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
     }
   } else if (warp == 1) {
     // -------------------------------- MMA ---------------------------------
-    // One tile of lookahead: S^T(t+1) is issued before O^T(t), so the softmax
-    // of tile t overlaps the next tile's QK^T.  tcgen05.commit covers every
-    // earlier MMA, so s_full(t+2) still implies O^T(t) is done (P buffer t&1
-    // free) and o_done orders the rescale / epilogue reads of O^T.
+    // Tiles in ring order; tile t belongs to softmax group g = iseq & 1 (its
+    // item's parity, which is also its O buffer) and is that group's k-th
+    // tile.  One tile of lookahead: S^T(t+1) is issued before O^T(t), so the
+    // other group's softmax runs while this tile's P is being made.
     if (lane == 0) {
       // S: N = 16 query columns; O: N = 32 ([P_hi | P_lo] in one MMA, halving the PV issue count)
       constexpr uint32_t id_s = idesc(0, NQ), id_o = idesc(1, 2 * NQ);
-      auto issue_s = [&](int t) {
-        const int st = t % NST, sb = t & 1;
-        mb_wait(&S.s_empty[sb], ((uint32_t)(t >> 1) & 1u) ^ 1u);
+      int kc[2] = {0, 0};                       // tiles handed to each group so far
+      auto issue_s = [&](int t) -> int {        // returns the tile's index within its group
+        const int st = t % NST;
+        const int g = S.hdr[st].iseq & 1;
+        const int k = kc[g]++;
+        const int sb = k & 1;
+        mb_wait(&S.s_empty[g][sb], ((uint32_t)(k >> 1) & 1u) ^ 1u);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint8_t* sk = smem + st * STAGE_BYTES;
         const uint8_t* sq = sk + 2 * KV_BYTES;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {            // S^T = K . Q^T over d in steps of 16
-          const int kb = k >> 2, ko = (k & 3) * 32;
-          mma(tmem + sb * 16, sdesc(sk + kb * 16384 + ko, 16, 1024), sdesc(sq + kb * 2048 + ko, 16, 1024), id_s,
-              k > 0);
+        for (int kk = 0; kk < 8; ++kk) {        // S^T = K . Q^T over d in steps of 16
+          const int kb = kk >> 2, ko = (kk & 3) * 32;
+          mma(tmem + scol(g, sb), sdesc(sk + kb * 1024 + ko, 16, 2048), sdesc(sq + kb * 2048 + ko, 16, 1024), id_s,
+              kk > 0);
         }
-        commit(&S.s_full[sb]);
+        commit(&S.s_full[g][sb]);
+        S.gt[g][sb] = t;
+        mb_arrive(&S.s_full[g][sb]);            // releases gt together with the slot
+        return k;
+      };
+      auto finish = [&]() {                     // tell both groups there are no more tiles
+        for (int g = 0; g < 2; ++g) {
+          const int sb = kc[g] & 1;
+          mb_wait(&S.s_empty[g][sb], ((uint32_t)(kc[g] >> 1) & 1u) ^ 1u);
+          S.gt[g][sb] = -1;
+          mb_arrive(&S.s_full[g][sb]);
+          mb_arrive(&S.s_full[g][sb]);
+        }
       };
       mb_wait(&S.kv_full[0], 0u);
       if (S.hdr[0].item < 0) {
-        mb_arrive(&S.s_full[0]);
+        finish();
       } else {
-        issue_s(0);
+        int kt = issue_s(0);
         for (int t = 0;; ++t) {
           const int st = t % NST, st1 = (t + 1) % NST;
           mb_wait(&S.kv_full[st1], (uint32_t)((t + 1) / NST) & 1u);
           TC_TRACE_AT(t + 1, 3);
           const bool end = S.hdr[st1].item < 0;
-          if (!end) issue_s(t + 1);
+          const int kt1 = end ? 0 : issue_s(t + 1);
           const bool first = S.hdr[st].flags & 1;
           const bool last = S.hdr[st].flags & 2;
-          const int iseq = S.hdr[st].iseq, ob = iseq & 1;
-          if (first)   // O buffer ob must have been read by the epilogue of item iseq - 2
-            mb_wait(&S.o_free[ob], ((uint32_t)(iseq >> 1) & 1u) ^ 1u);
-          // one barrier per P buffer: the softmax may hand over P(t+1) before this
-          // wait for P(t) runs, and a single barrier would then be two phases ahead
-          mb_wait(&S.p_full[t & 1], (uint32_t)(t >> 1) & 1u);
+          const int iseq = S.hdr[st].iseq, g = iseq & 1;
+          if (first)   // O buffer g must have been read by the epilogue of item iseq - 2
+            mb_wait(&S.o_free[g], ((uint32_t)(iseq >> 1) & 1u) ^ 1u);
+          mb_wait(&S.p_full[g], (uint32_t)kt & 1u);
           TC_TRACE_AT(t, 4);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint8_t* sv = smem + st * STAGE_BYTES + KV_BYTES;
-          const uint8_t* sp = pbuf + (t & 1) * PBUF_BYTES;
+          const uint8_t* sp = pbuf + g * PBUF_BYTES;
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {              // [O_hi | O_lo]^T += V^T . [P_hi | P_lo]^T, rows in steps of 16
-            const int kb = k >> 2, ko = (k & 3) * 32;
-            mma(tmem + ocol(ob), sdesc(sv + k * 2048, 16384, 1024), sdesc(sp + kb * PBLK_BYTES + ko, 16, 1024), id_o,
-                (first && k == 0) ? 0u : 1u);
+          for (int kk = 0; kk < 8; ++kk) {          // [O_hi | O_lo]^T += V^T . [P_hi | P_lo]^T, rows in steps of 16
+            const int kb = kk >> 2, ko = (kk & 3) * 32;
+            mma(tmem + ocol(g), sdesc(sv + kk * 4096, 1024, 2048), sdesc(sp + kb * PBLK_BYTES + ko, 16, 1024), id_o,
+                (first && kk == 0) ? 0u : 1u);
           }
-          commit(&S.o_done);
-          if (last) commit(&S.o_fin[ob]);
+          commit(&S.o_done[g]);
+          if (last) commit(&S.o_fin[g]);
           commit(&S.kv_empty[st]);
           TC_TRACE_AT(t, 5);
-          if (end) { mb_arrive(&S.s_full[(t + 1) & 1]); break; }
+          if (end) { finish(); break; }
+          kt = kt1;
         }
       }
     }
@@ -601,37 +615,33 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
         __syncwarp();
         const bool stores = (h.mode == UNIT_MOVE || h.mode == UNIT_STAGE) && h.nvalid > 0;
         if (stores) {
-          const int full_groups = h.nvalid >> 4;
+          const int full_groups = h.nvalid >> 3;     // whole 8-row groups go out as 4-D boxes
           if (lane == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
           const int np = PACK ? 1 << hdr_lognp(h) : 1;
+          const int seg = TM / np;
           for (int sgi = 0; sgi < np; ++sgi) {       // one segment per packed KV head
-            const uint8_t* sk = smem + st * STAGE_BYTES + sgi * (TM / np) * 128;
+            const uint8_t* sk = smem + st * STAGE_BYTES + sgi * (seg / 8) * 2048;
             const int colk = (a.l0 + h.li) * 2 * a.Hkv * DH + (h.g + sgi) * DH;   // elements
             const int colv = colk + a.Hkv * DH;
             if (lane == 0) {
-              const CUtensorMap* map = h.mode == UNIT_MOVE ? maps.kv : maps.stage;
-              int done = 0;
+              const CUtensorMap* map = h.mode == UNIT_MOVE ? maps.st_kv : maps.st_stage;
 #pragma unroll
-              for (int i = 0; i < NBOX_STORE; ++i) {
-                const int bg = 8 >> i;
-                if (full_groups - done >= bg) {
-#pragma unroll
-                  for (int kb = 0; kb < 2; ++kb) {
-                    tma2d_store(map + i, colk + kb * 64, h.drow + done * 16, sk + kb * 16384 + done * 2048);
-                    tma2d_store(map + i, colv + kb * 64, h.drow + done * 16, sk + KV_BYTES + kb * 16384 + done * 2048);
-                  }
-                  done += bg;
+              for (int i = 0; i < NSTB; ++i) {
+                const int bg = NGRP >> i;
+                if (full_groups & bg) {
+                  const int done = full_groups & ~(2 * bg - 1);
+                  tma4d_store(map + i, h.drow + done * 8, colk / 64, sk + done * 2048);
+                  tma4d_store(map + i, h.drow + done * 8, colv / 64, sk + KV_BYTES + done * 2048);
                 }
               }
             }
-            // ragged tail rows: one 16-B chunk per lane (K/V, 64-column block, chunk); segments
-            // start on 16-row boundaries, so the swizzle phase is the row's own
+            // ragged tail rows: one 16-B chunk per lane (K/V, 64-column block, chunk)
             const int kv = lane >> 4, kb = (lane >> 3) & 1, c = lane & 7;
             uint8_t* gbase = (h.mode == UNIT_MOVE ? a.arena : a.staging) +
                              (int64_t)(kv ? colv : colk) * 2 + kb * 128 + c * 16;
-            for (int row = full_groups * 16; row < h.nvalid; ++row) {
-              const uint4 x = *reinterpret_cast<const uint4*>(sk + kv * KV_BYTES + kb * 16384 + row * 128 +
-                                                              ((c ^ (row & 7)) << 4));
+            for (int row = full_groups * 8; row < h.nvalid; ++row) {
+              const uint4 x = *reinterpret_cast<const uint4*>(sk + kv * KV_BYTES + (row >> 3) * 2048 + kb * 1024 +
+                                                              (row & 7) * 128 + ((c ^ (row & 7)) << 4));
               *reinterpret_cast<uint4*>(gbase + (int64_t)(h.drow + row) * a.kvpt) = x;
             }
           }
@@ -658,62 +668,37 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
     }
   } else {
     // ------------------------------ softmax -------------------------------
-    // Lazy running max (log2 domain): the column max is reduced across the
-    // 128 lanes only on an item's first tile or when some score exceeds the
-    // running max by more than LAZY_THR; otherwise p = 2^(s - m) <= 2^8 and
-    // nothing is rescaled.  Each lane keeps its own row's partial sums; they
-    // are reduced once, in the epilogue.
-    const int wq = warp - 2;                          // 0..3
+    // Two groups of 4 warps (warps 2-5: group 0, warps 7-10: group 1); group
+    // g takes the tiles of items with iseq & 1 == g, in order, so the two
+    // groups' per-tile chains (TMEM load, reductions, P, hand-over,
+    // epilogue) overlap.  Lazy running max (log2 domain): the column max is
+    // reduced across the 128 lanes only on an item's first tile or when some
+    // score exceeds the running max by more than LAZY_THR; otherwise
+    // p = 2^(s - m) <= 2^8 and nothing is rescaled.  Each lane keeps its own
+    // row's partial sums; they are reduced once, in the epilogue.
+    const int grp = warp < 6 ? 0 : 1;
+    const int wq = warp - (grp == 0 ? 2 : 7);         // 0..3 within the group
     const int lq = warp & 3;                          // TMEM lane quarter this warp may access
     const int row = lq * 32 + lane;                   // TMEM lane = tile row (S) = head-dim index (O)
     const uint32_t lane_base = tmem + ((uint32_t)(lq * 32) << 16);
+    const uint32_t oc = ocol(grp);                    // this group's O buffer
+    uint8_t* const pgrp = pbuf + grp * PBUF_BYTES;    // this group's P buffer
     float m[NC], lrow[NC];
 #pragma unroll
     for (int c = 0; c < NC; ++c) { m[c] = -INFINITY; lrow[c] = 0.f; }
-    // the finished item whose epilogue waits until the next tile's P is handed over
-    bool pend = false;
-    TcHdr ph = {};
-    float pm[NC], pl[NC];
-    auto epilogue = [&]() {
-      col_reduce<false, NC>(pl, S.red[1], wq, lane);
-      const int ob = ph.iseq & 1;
-      mb_wait(&S.o_fin[ob], (uint32_t)(ph.iseq >> 1) & 1u);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      float o[NC], olo[NC];
-      tmem_ld<NC>(lane_base + ocol(ob), o);
-      tmem_ld<NC>(lane_base + ocol(ob) + NQ, olo);
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      __syncwarp();
-      if (lane == 0) mb_arrive(&S.o_free[ob]);
-#pragma unroll
-      for (int c = 0; c < NC; ++c) o[c] += olo[c];
-      const int d = row;
-#pragma unroll
-      for (int c = 0; c < NC; ++c) {
-        if (c >= (PACK ? a.G << hdr_lognp(ph) : a.G)) break;
-        const int hq = ph.g * a.G + c;            // packed heads: column c belongs to KV head g + c / G
-        if (ph.part < 0) {
-          a.out[((int64_t)(ph.li * a.B + ph.b) * a.H + hq) * DH + d] = o[c] / pl[c];
-        } else {
-          float* pr = a.partials + (((int64_t)ph.part * a.nl + ph.li) * a.H + hq) * (DH + 4);
-          pr[d] = o[c];
-          if (d == 0) { pr[DH] = pm[c]; pr[DH + 1] = pl[c]; }
-        }
-      }
-      pend = false;
-    };
-    for (int t = 0;; ++t) {
-      const int sb = t & 1;
-      mb_wait(&S.s_full[sb], (uint32_t)(t >> 1) & 1u);
+    for (int k = 0;; ++k) {
+      const int sb = k & 1;
+      mb_wait(&S.s_full[grp][sb], (uint32_t)(k >> 1) & 1u);
+      const int t = S.gt[grp][sb];
+      if (t < 0) break;
       if (lane == 0 && warp == 2) TC_TRACE_AT(t, 6);
       const TcHdr h = S.hdr[t % NST];
-      if (h.item < 0) break;
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       float s[NC];
-      tmem_ld<NC>(lane_base + sb * 16, s);
+      tmem_ld<NC>(lane_base + scol(grp, sb), s);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mb_arrive(&S.s_empty[sb]);
+      if (lane == 0) mb_arrive(&S.s_empty[grp][sb]);
       const bool first = h.flags & 1;
       int rs = row;                                   // this lane's row inside its segment
       bool valid;
@@ -733,7 +718,6 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
         for (int c = 0; c < NC; ++c)
           s[c] = (valid && ((c >= cg0 && c < cg1) || c >= cpad)) ? s[c] * a.qscale : -INFINITY;
       }
-      const int ob = h.iseq & 1;
       // does any score need a larger running max?
       bool need = first;
       if (!first) {
@@ -741,10 +725,10 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
 #pragma unroll
         for (int c = 0; c < NC; ++c) over |= s[c] > m[c] + LAZY_THR;
         const bool wover = __any_sync(0xffffffffu, over);
-        if (lane == 0) S.flag[wq] = wover;
-        softmax_bar();
-        need = S.flag[0] | S.flag[1] | S.flag[2] | S.flag[3];
-        softmax_bar();
+        if (lane == 0) S.flag[grp][wq] = wover;
+        softmax_bar(grp);
+        need = S.flag[grp][0] | S.flag[grp][1] | S.flag[grp][2] | S.flag[grp][3];
+        softmax_bar(grp);
       }
       float corr[NC];
       bool rescale = false;
@@ -752,7 +736,7 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
         float mt[NC];
 #pragma unroll
         for (int c = 0; c < NC; ++c) mt[c] = s[c];
-        col_reduce<true, NC>(mt, S.red[0], wq, lane);
+        col_reduce<true, NC>(mt, S.red[grp][0], wq, lane, grp);
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
           const float mn = first ? mt[c] : fmaxf(m[c], mt[c]);
@@ -762,8 +746,14 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
         }
         rescale = !first;
       }
+      // this group's previous O MMA has read its P buffer (and O^T may be touched):
+      // every o_done phase is waited, so no completion goes unobserved
+      if (k > 0) {
+        mb_wait(&S.o_done[grp], (uint32_t)(k - 1) & 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      }
       // P = 2^(s - m) as bf16 hi + lo; row c (query column), column j = row; 128B swizzle
-      uint8_t* sp = pbuf + (t & 1) * PBUF_BYTES + (row >> 6) * PBLK_BYTES;
+      uint8_t* sp = pgrp + (row >> 6) * PBLK_BYTES;
       const uint32_t jj2 = (uint32_t)(row & 63) * 2u;
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
@@ -782,35 +772,53 @@ __global__ void __launch_bounds__(224, 1) k_attn_tc(const __grid_constant__ TcMa
         for (int kb = 0; kb < 2; ++kb)
 #pragma unroll
           for (int ch = 0; ch < 8; ++ch)
-            *reinterpret_cast<uint4*>(sv + kb * 16384 + row * 128 + ch * 16) = make_uint4(0, 0, 0, 0);
+            *reinterpret_cast<uint4*>(sv + (row >> 3) * 2048 + kb * 1024 + (row & 7) * 128 + ch * 16) =
+                make_uint4(0, 0, 0, 0);
       }
-      // every phase of o_done is waited (O^T(t-1) done; it is almost always complete by now),
-      // so no completion goes unobserved -- needed before a rescale, harmless otherwise
-      if (t > 0) mb_wait(&S.o_done, (uint32_t)(t - 1) & 1u);
-      if (rescale) {                                // O^T *= corr once the previous tile's MMA is done
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (rescale) {                                // O^T *= corr (this item's previous tile is done)
         float o[NC], olo[NC];
-        tmem_ld<NC>(lane_base + ocol(ob), o);
-        tmem_ld<NC>(lane_base + ocol(ob) + NQ, olo);
+        tmem_ld<NC>(lane_base + oc, o);
+        tmem_ld<NC>(lane_base + oc + NQ, olo);
 #pragma unroll
         for (int c = 0; c < NC; ++c) { o[c] *= corr[c]; olo[c] *= corr[c]; }
-        tmem_st<NC>(lane_base + ocol(ob), o);
-        tmem_st<NC>(lane_base + ocol(ob) + NQ, olo);
+        tmem_st<NC>(lane_base + oc, o);
+        tmem_st<NC>(lane_base + oc + NQ, olo);
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mb_arrive(&S.p_full[t & 1]);
+      if (lane == 0) mb_arrive(&S.p_full[grp]);
       if (lane == 0 && warp == 2) TC_TRACE_AT(t, 7);
-      if (pend) epilogue();                         // the previous item, overlapped with this tile's MMA
       if (h.flags & 2) {
-        pend = true;
-        ph = h;
+        // epilogue of the finished item: the other group keeps the tensor pipe busy meanwhile
+        float pl[NC];
 #pragma unroll
-        for (int c = 0; c < NC; ++c) { pm[c] = m[c]; pl[c] = lrow[c]; }
+        for (int c = 0; c < NC; ++c) pl[c] = lrow[c];
+        col_reduce<false, NC>(pl, S.red[grp][1], wq, lane, grp);
+        mb_wait(&S.o_fin[grp], (uint32_t)(h.iseq >> 1) & 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        float o[NC], olo[NC];
+        tmem_ld<NC>(lane_base + oc, o);
+        tmem_ld<NC>(lane_base + oc + NQ, olo);
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mb_arrive(&S.o_free[grp]);
+        const int d = row;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          if (c >= (PACK ? a.G << hdr_lognp(h) : a.G)) break;
+          const int hq = h.g * a.G + c;             // packed heads: column c belongs to KV head g + c / G
+          const float ov = o[c] + olo[c];
+          if (h.part < 0) {
+            a.out[((int64_t)(h.li * a.B + h.b) * a.H + hq) * DH + d] = ov / pl[c];
+          } else {
+            float* pr = a.partials + (((int64_t)h.part * a.nl + h.li) * a.H + hq) * (DH + 4);
+            pr[d] = ov;
+            if (d == 0) { pr[DH] = m[c]; pr[DH + 1] = pl[c]; }
+          }
+        }
       }
     }
-    if (pend) epilogue();
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -858,7 +866,24 @@ EncodeTiledFn encoder() {
   return fn;
 }
 
-// 2-D bf16 map: `cols` elements per row, `rows` rows, `pitch` bytes; boxes of 64 x box_rows, 128B swizzle
+
+// K/V rows as a 4-D bf16 map {64 columns, rows (pitch), 64-column blocks of the row (128 B),
+// 8-row groups (8 pitches)}; box {64, 8, 2, groups}.  The group dimension overlaps the row
+// dimension, so a box starting at row r covers rows r .. r + 8 groups - 1; its extent is kept
+// generous (the row dimension bounds the start row; reads past the arena's last row land in
+// the 8 guard rows s3_workspace_query adds).
+bool encode_4d(CUtensorMap* m, const void* base, uint64_t row_elems, uint64_t rows, uint64_t pitch, int groups) {
+  EncodeTiledFn enc = encoder();
+  if (!enc) return false;
+  cuuint64_t dims[4] = {64, rows, row_elems / 64, rows / 8 + 2};
+  cuuint64_t strides[3] = {pitch, 128, 8 * pitch};
+  cuuint32_t box[4] = {64, 8, 2, (cuuint32_t)groups};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 // q as a 3-D bf16 map {64 columns, rows, 2 column blocks (stride 128 B)}: one box of 16 rows lands
 // as [block][16 rows][64] -- the layout the S MMA reads -- in one instruction instead of two
 bool encode_q3(CUtensorMap* m, const void* base, uint64_t rows, uint64_t pitch) {
@@ -869,18 +894,6 @@ bool encode_q3(CUtensorMap* m, const void* base, uint64_t rows, uint64_t pitch) 
   cuuint32_t box[3] = {64, 16, 2};
   cuuint32_t es[3] = {1, 1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
-}
-
-bool encode_2d(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint64_t pitch, uint32_t box_rows = 16) {
-  EncodeTiledFn enc = encoder();
-  if (!enc) return false;
-  cuuint64_t dims[2] = {cols, rows};
-  cuuint64_t strides[1] = {pitch};
-  cuuint32_t box[2] = {64, box_rows};
-  cuuint32_t es[2] = {1, 1};
-  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -925,15 +938,18 @@ cudaError_t launch_attn_tc(const Shape& sh, const uint16_t* q, const uint16_t* k
   TcMaps maps;
   // staging rows (evicted slots' KV, token-major like the arena); without staging k_prep never fuses an eviction
   const int64_t stage_rows = staging ? staging_bytes / sh.kvpt : 0;
-  for (int i = 0; i < NBOX; ++i) {
-    if (!encode_2d(&maps.kv[i], arena, (uint64_t)sh.row_elems, (uint64_t)arena_rows, (uint64_t)sh.kvpt, 128u >> i))
+  for (int n = 1; n <= NGRP; ++n)
+    if (!encode_4d(&maps.kvg[n - 1], arena, (uint64_t)sh.row_elems, (uint64_t)arena_rows, (uint64_t)sh.kvpt, n))
+      return cudaErrorInvalidValue;
+  for (int i = 0; i < NSTB; ++i) {
+    if (!encode_4d(&maps.st_kv[i], arena, (uint64_t)sh.row_elems, (uint64_t)arena_rows, (uint64_t)sh.kvpt, NGRP >> i))
       return cudaErrorInvalidValue;
     if (stage_rows > 0) {
-      if (!encode_2d(&maps.stage[i], staging, (uint64_t)sh.row_elems, (uint64_t)stage_rows, (uint64_t)sh.kvpt,
-                     128u >> i))
+      if (!encode_4d(&maps.st_stage[i], staging, (uint64_t)sh.row_elems, (uint64_t)stage_rows, (uint64_t)sh.kvpt,
+                     NGRP >> i))
         return cudaErrorInvalidValue;
     } else {
-      maps.stage[i] = maps.kv[i];
+      maps.st_stage[i] = maps.st_kv[i];
     }
   }
   if (!encode_q3(&maps.q, q, (uint64_t)nl * B * sh.H, (uint64_t)sh.D * 2)) return cudaErrorInvalidValue;
@@ -946,7 +962,7 @@ cudaError_t launch_attn_tc(const Shape& sh, const uint16_t* q, const uint16_t* k
   a.k_new = k_new; a.v_new = v_new; a.feed = feed;
   static const int pack = [] { const char* e = getenv("S3_TC_PACK"); return e ? atoi(e) : 1; }();
   a.pmax = pack ? (a.G <= 8 ? 8 : 16) / a.G : 1;   // S3_TC_PACK=0: one KV head per tile (A/B)
-  const dim3 grid(grid_attn), block(224);
+  const dim3 grid(grid_attn), block(TC_THREADS);
   const int smem = attn_tc_smem();
   const void* kfn = attn_tc_kernel_ptr(a.G <= 8 ? 8 : 16, a.pmax > 1, feed.ready != nullptr);
   void* args[] = {(void*)&maps, (void*)&a};

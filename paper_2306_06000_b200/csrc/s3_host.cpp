@@ -430,7 +430,8 @@ s3_status s3_workspace_query(const s3_config* cfg, int64_t* arena_b, int64_t* ws
                              int64_t* host_min) {
   if (!validate(cfg)) return S3_E_INVAL;
   const Shape sh = make_shape(cfg);
-  if (arena_b) *arena_b = cfg->arena_rows * sh.kvpt;
+  // + 8 guard rows: the tensor-core kernel loads whole 8-row groups, up to 7 rows past a slot's end
+  if (arena_b) *arena_b = (cfg->arena_rows + 8) * sh.kvpt;
   if (ws_b) *ws_b = carve(cfg).total;
   if (staging_min) *staging_min = (int64_t)cfg->max_seq_len * sh.kvpt;
   if (host_min) *host_min = align_up((int64_t)cfg->max_seq_len * sh.kvpt);
@@ -442,7 +443,7 @@ s3_status s3_kv_init(const s3_config* cfg, const s3_buffers* b, s3_ctx** out) {
   *out = nullptr;
   const Shape sh = make_shape(cfg);
   const Carve k = carve(cfg);
-  if (!b->arena || b->arena_bytes < cfg->arena_rows * sh.kvpt) return S3_E_NOMEM;
+  if (!b->arena || b->arena_bytes < (cfg->arena_rows + 8) * sh.kvpt) return S3_E_NOMEM;
   if (!b->workspace || b->workspace_bytes < k.total) return S3_E_NOMEM;
   if (((uintptr_t)b->arena | (uintptr_t)b->workspace) % kAlign) return S3_E_INVAL;
   if (b->staging && ((uintptr_t)b->staging % 16)) return S3_E_INVAL;

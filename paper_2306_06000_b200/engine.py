@@ -195,8 +195,8 @@ class S3Engine:
 
     def arena_rows_view(self) -> torch.Tensor:
         """The arena as bf16 [R][L][2][H][D] (a view, no copy)."""
-        R = self.cfg.arena_rows
-        return self.arena.view(torch.bfloat16).view(R, self.L, 2, self.Hkv, self.D)
+        R = self.cfg.arena_rows                    # (the allocation ends with 8 guard rows)
+        return self.arena[:R * self.kvpt].view(torch.bfloat16).view(R, self.L, 2, self.Hkv, self.D)
 
     def host_rows(self, host_off: int, rows: int) -> torch.Tensor:
         n = rows * self.kvpt

@@ -76,7 +76,7 @@ def _cfg(**kw):
 
 def test_workspace_query_and_validation(s3lib):
     a, w, s, h = abi.s3_workspace_query(_cfg())
-    assert a == 300000 * 458752
+    assert a == (300000 + 8) * 458752            # R rows + 8 guard rows (tensor-core 8-row group loads)
     assert s == 2048 * 458752
     assert 0 < w < 2 * 1024**3           # workspace stays small next to the arena
     for bad in [dict(head_dim=96), dict(arena_rows=1000), dict(max_running=0), dict(world=0),
