@@ -4,29 +4,32 @@
 //
 // With grouped KV the G query heads that share KV head g turn the decode
 // GEMV into a real contraction per 128-row tile of that head's rows:
-//     S^T [128 x 16]  = K_tile [128 x D] . Q_g^T [D x 16]      (A K-major, B K-major)
-//     O^T [D x 16]   += V_tile^T [D x 128] . P^T [128 x 16]    (A MN-major, B K-major)
-// (16 = G padded to the MMA N granularity).  Per CTA (persistent, one per
-// SM) four roles:
-//   producer warp : items (unit, layer, KV head) from the atomic queue; TMA
-//                   tensor loads (128B swizzle) of the tile's K and V rows in
-//                   128/64/32/16/8-row boxes (only the 8-row groups holding
-//                   valid rows) and of the group's q rows, into a 3-stage ring.
-//                   Short units pack np = 2..NC/G KV heads into one tile,
-//                   one segment of 128/np rows per head: the q box already
-//                   holds those heads' np*G query rows, and the softmax masks
-//                   S^T block-diagonally (segment s meets only columns
-//                   [sG, (s+1)G)), so one MMA pair and one softmax pass serve
-//                   np heads;
-//   MMA warp      : one thread issues tcgen05.mma (kind::f16, M 128, N 16,
-//                   K 16 per instruction), commits to mbarriers;
-//   softmax warps : 4 warps = 128 TMEM lanes; lane j holds row j of S^T:
-//                   mask rows >= nvalid, column max / sum across the 128
-//                   lanes, online softmax in the log2 domain, P (bf16,
-//                   swizzled) to shared memory, zero V rows >= nvalid (NaN
-//                   safety), rescale O^T in TMEM; after the last tile of an
-//                   item lane d holds O^T[d][:] and writes out / the split-K
-//                   partial (same records as k_combine reads).
+//     S^T [128 x 16]  = K_tile [128 x D] . Q_g^T [D x 16]                 (A K-major, B K-major)
+//     [O_hi|O_lo]^T  += V_tile^T [D x 128] . [P_hi|P_lo]^T [128 x 32]     (A MN-major, B K-major)
+// (16 = G padded to the MMA N granularity; P is split into bf16 hi + lo so
+// the product keeps ~16 bits, one N = 32 MMA per 16 rows).  Per CTA
+// (persistent, one per SM, 11 warps) these roles:
+//   producer warp : items (unit, layer, KV head) from the atomic queue; per
+//                   tile ONE 4-D TMA box for K and one for V (all valid 8-row
+//                   groups, both 64-column blocks; the smem tile layout is
+//                   [8-row group][column block][8 rows][128 B]) and one 3-D box
+//                   for the 16 q rows, into a 3-stage ring.  Short units pack
+//                   np = 2..NC/G KV heads into one tile, one segment of 128/np
+//                   rows per head: the q box already holds those heads' np*G
+//                   query rows, and the softmax masks S^T block-diagonally
+//                   (segment s meets only columns [sG, (s+1)G)), so one MMA
+//                   pair and one softmax pass serve np heads;
+//   MMA warp      : one thread issues tcgen05.mma (kind::f16, M 128, K 16 per
+//                   instruction) and routes tile t to softmax group iseq & 1;
+//   softmax warps : two groups of 4 warps ("ping-pong", warps 2-5 and 7-10),
+//                   each owning alternate items with its own S slots, P
+//                   buffer and O buffer in TMEM; 4 warps = 128 TMEM lanes,
+//                   lane j holds row j of S^T: mask rows >= nvalid, column
+//                   max / sum across the 128 lanes, online softmax in the log2
+//                   domain, P (bf16 hi / lo, swizzled) to shared memory, zero V
+//                   rows >= nvalid (NaN safety), rescale O^T in TMEM; after the
+//                   last tile of an item lane d holds O^T[d][:] and writes out
+//                   / the split-K partial (same records as k_combine reads).
 //   storer warp   : (fused steps only) the row shift of SURVEY §8 row (d),
 //                   done on the tiles already in shared memory -- see below.
 // The new token's K/V row is appended to the arena by k_append before this
@@ -39,8 +42,8 @@
 // (head * 2^16 + rows, monotone because a CTA walks a unit-layer's KV heads
 // in order); for a MOVE tile it waits until every other unit whose source
 // rows overlap the tile's destination rows (k_deps, tc mode) has read that
-// far, then writes the tile's whole 16-row groups back with TMA tensor stores
-// through the same swizzled map and the ragged tail rows with a warp copy
+// far, then writes the tile's whole 8-row groups back with 4-D TMA tensor stores
+// through the same layout and the ragged tail rows with a warp copy
 // that undoes the 128B swizzle; STAGE (evicted) tiles go to the staging
 // buffer the same way.  The stage is released (kv_empty) only after the
 // stores have read shared memory.  Deadlock freedom is the k_attn_tma
