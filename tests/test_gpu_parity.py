@@ -522,7 +522,8 @@ def test_grouped_query_kv(H, Hkv, D, variant, mode):
 
 @pytest.mark.parametrize("H,Hkv,C,policy,mode,staging", [
     (8, 2, 512, "short", 0, True), (32, 8, 48, "short", 0, True), (16, 1, 128, "bucket", 0, True),
-    (4, 2, 7, "short", 0, True), (8, 2, 64, "short", 1, True), (8, 2, 512, "short", 0, False)])
+    (4, 2, 7, "short", 0, True), (8, 2, 64, "short", 1, True), (8, 2, 512, "short", 0, False),
+    (12, 4, 40, "short", 0, True), (24, 3, 96, "short", 0, True), (8, 4, 33, "short", 0, True)])
 def test_grouped_query_kv_tensor_cores(H, Hkv, C, policy, mode, staging):
     """attn_variant 2: tcgen05/TMEM/TMA kernel for grouped KV (D = 128); C
     small -> split-K units and tile tails; NaN-poisoned slack rows.  mode 0:
