@@ -85,6 +85,11 @@ typedef struct {
   int32_t num_kv_heads;                     /* KV heads H_kv (0 = num_heads; must divide it):
                                                grouped-query / multi-query KV, query head h
                                                reads KV head h / (H / H_kv); kvpt = 4*L*H_kv*D */
+  int32_t reserve_sms;                      /* SMs the persistent attention grid leaves free so
+                                               kernels on other streams (the counter all-reduce
+                                               of a multi-GPU step) run DURING attention instead
+                                               of after it: 0 = default (none at world 1, 4 at
+                                               world > 1), -1 = none, else that many (< #SMs/2) */
 } s3_config;
 
 typedef struct {                            /* caller-owned memory                             */
@@ -108,9 +113,11 @@ const char* s3_last_error(const s3_ctx* ctx);   /* static text; never NULL */
  * request pool in the host DRAM") -------------------------------------- */
 typedef struct { int64_t req_id; int32_t prompt_len, alloc_out; } s3_request;
 /* Adds fresh requests; reservation cap = prompt_len + alloc_out rows
- * (R4).  S3_E_INVAL if prompt_len < 0, alloc_out < 1 or the cap
- * exceeds max_seq_len; S3_E_UNSCHEDULABLE if cap > arena_rows.  With
- * world > 1 every rank must submit the same requests in the same order.   */
+ * (R4).  S3_E_INVAL if prompt_len < 0, alloc_out < 1, the cap
+ * exceeds max_seq_len, or a req_id is already live (queued, running or
+ * evicted and not yet finished) or repeats within the call; nothing is added
+ * then.  S3_E_UNSCHEDULABLE if cap > arena_rows.  With world > 1 every rank
+ * must submit the same requests in the same order.                         */
 s3_status s3_submit(s3_ctx* ctx, const s3_request* reqs, int32_t n);
 
 /* ---- (a)+(b): decode attention + append + overrun detection -----------
@@ -119,8 +126,10 @@ s3_status s3_submit(s3_ctx* ctx, const s3_request* reqs, int32_t n);
  *     out[l][b][h] = softmax( q K^T / sqrt(D) ) V   over rows 0..len_b
  * (PAPER.md:106 [§2.1]; R1 self-inclusive, R2 per-head D).
  * eos (device uint8 [B]) is read only when l0+nl == L: then len, gen += 1
- * and status_b = FINISHED if eos_b, else OVERRUN if len_b == cap_b, else
- * RUNNING ("not finished but used up its reserved memory").
+ * and status_b = FINISHED if eos_b or len_b == max_seq_len (a length stop,
+ * DESIGN.md R28), else OVERRUN if len_b == cap_b, else RUNNING (PAPER.md:174
+ * "not finished but used up its reserved memory").  S3_E_STATE if a slot has
+ * no free row (len >= cap; cannot happen through this API).
  * Stream-ordered on cfg.stream, no host synchronisation.                   */
 s3_status s3_decode_step(s3_ctx* ctx, int32_t l0, int32_t nl, const void* q, const void* k_new,
                          const void* v_new, const uint8_t* eos, float* out);
@@ -187,7 +196,12 @@ typedef struct {
  * evicted requests re-enter the pool with cap <- min(2 cap, max_seq_len)
  * (R5).  perm[b] = new batch index or -1; evicted / finished_ids list the
  * leavers in batch order.  Each output array may be NULL, else it must hold
- * n_before entries.  Synchronises the host once on a small report readback. */
+ * n_before entries.  Synchronises the host once on a small report readback.
+ * S3_E_NOMEM if the host store cannot take this step's evictees (state
+ * unchanged; retry after s3_evict_wait frees reloaded ranges).  A fused step
+ * only stages evictions that fit the largest free host-store block, so this
+ * cannot follow a fused step unless the store fragments; if it does, the
+ * evictees' rows have already left the arena and the context is poisoned.   */
 s3_status s3_evict_compact(s3_ctx* ctx, s3_evict_report* rep, int32_t* perm, s3_evicted* evicted,
                            int64_t* finished_ids);
 /* Blocks until the host copy of every eviction so far is complete.        */
@@ -199,8 +213,14 @@ typedef struct {
   int64_t tail_rows;
   int64_t fill_bytes;        /* prompt rows written for fresh admissions (prefill stand-in) */
   int64_t h2d_bytes;         /* evicted KV reloaded from host_store                        */
+  int64_t moved_bytes;       /* compact_policy 1 (R27): rows shifted over holes a step with an
+                                empty pool left in place, before this admission (one way)  */
 } s3_admit_report;
-/* world == 1: one FFD over the whole pool, fresh and evicted alike, sorted
+/* compact_policy 1 (R27): when requests wait and an earlier step left holes
+ * (its pool was empty), s3_admit / s3_admit_home first shift the survivors
+ * up (keep-scan + ordered move), so the FFD sees the free rows of the
+ * every-step policy; the bytes are reported in moved_bytes.
+ * world == 1: one FFD over the whole pool, fresh and evicted alike, sorted
  * by (cap desc, req_id asc), skip-and-continue, into free = R - tail rows
  * (R7-R9).  Admitted slots are appended at the
  * tail in scan order; fresh ones get their P prompt rows, evicted ones get
@@ -212,7 +232,9 @@ s3_status s3_admit(s3_ctx* ctx, s3_admit_report* rep, int64_t* admitted_ids);
  *   s3_counters_local + an all-reduce(sum) of the [world][S3_NCOUNTERS]
  *                    matrix by the caller (torch.distributed / NCCL);
  *   s3_admit_shared  multi-bin FFD of the shared fresh pool over ranks
- *                    (free rows = column 0, free slots = column 2). */
+ *                    (free rows = column 0, free slots = column 2): items in
+ *                    FFD order, each to the rank with the most free rows
+ *                    among ranks with a free slot (ties: lowest rank). */
 s3_status s3_admit_home(s3_ctx* ctx, s3_admit_report* rep, int64_t* admitted_ids);
 s3_status s3_admit_shared(s3_ctx* ctx, const int64_t* counters_all /* [world][S3_NCOUNTERS] */,
                           s3_admit_report* rep, int64_t* admitted_ids);
@@ -222,7 +244,8 @@ s3_status s3_counters_local(const s3_ctx* ctx, int64_t row[S3_NCOUNTERS]);
 /* Single-bin FFD: admitted[i] = 1 if item i is admitted.  Returns count.  */
 int32_t s3_plan_ffd(int32_t n, const int64_t* cap, const int64_t* req_id, int64_t free_rows,
                     int32_t max_items, uint8_t* admitted);
-/* Multi-bin FFD: rank[i] = bin or -1; free_rows / free_slots updated.      */
+/* Multi-bin FFD (worst fit over bins, R26): rank[i] = bin or -1;
+ * free_rows / free_slots updated.                                          */
 int32_t s3_plan_ffd_multibin(int32_t n, const int64_t* cap, const int64_t* req_id, int32_t world,
                              int64_t* free_rows, int64_t* free_slots, int32_t* rank);
 

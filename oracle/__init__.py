@@ -85,6 +85,7 @@ def lib():
             "s3o_admit_home": (i32, [P, P]),
             "s3o_admit_shared": (i32, [P, i32, i32, P, P, P]),
             "s3o_counters": (None, [P, P]),
+            "s3o_moved_at_admit": (i64, [P]),
             "s3o_attend_generated": (None, [P, i64, i32, i32, P]),
         }
         for name, (res, args) in sig.items():
@@ -278,6 +279,10 @@ class Oracle:
         fr = np.ascontiguousarray(free_by_rank, dtype=np.int64)
         sl = np.ascontiguousarray(slots_by_rank, dtype=np.int64)
         return self._admit_call(lib().s3o_admit_shared, world, rank, _p(fr), _p(sl))
+
+    def moved_at_admit(self) -> int:
+        """Bytes shifted by R27's admission-time compactions (on-demand policy)."""
+        return int(lib().s3o_moved_at_admit(self.h))
 
     def counters(self) -> np.ndarray:
         row = np.zeros(8, np.int64)

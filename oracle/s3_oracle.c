@@ -143,24 +143,28 @@ int32_t s3o_ffd(int32_t n, const int64_t* cap, const int64_t* req, int64_t free_
   return count;
 }
 
-/* Multi-bin FFD over ranks (R26): items in FFD order, bins in rank
- * order, each item goes to the first rank with room (free rows and a free
- * metadata slot).  assigned_rank[i] = rank or -1.  free_rows / slots_left are
- * updated in place.                                                        */
+/* Multi-bin FFD over ranks (R26): items in FFD order (PAPER.md:166,
+ * "sorts ... in a decreasing order"); each item goes to the rank with the MOST
+ * free rows among the ranks with a free metadata slot, ties to the lowest
+ * rank (worst fit), if it fits there -- otherwise it fits nowhere and is
+ * skipped.  The paper has one bin; the bin choice is R26's
+ * reading for several GPUs in lockstep, where a step lasts as long as the
+ * busiest rank, so the freed rows are filled evenly.  assigned_rank[i] =
+ * rank or -1.  free_rows / slots_left are updated in place.                */
 int32_t s3o_ffd_multibin(int32_t n, const int64_t* cap, const int64_t* req, int32_t world,
                          int64_t* free_rows, int64_t* slots_left, int32_t* assigned_rank) {
   ffd_key* k = sorted_keys(n, cap, req);
   int32_t count = 0;
   for (int32_t i = 0; i < n; ++i) assigned_rank[i] = -1;
   for (int32_t i = 0; i < n; ++i) {
-    for (int32_t r = 0; r < world; ++r) {
-      if (slots_left[r] > 0 && k[i].cap <= free_rows[r]) {
-        free_rows[r] -= k[i].cap;
-        slots_left[r] -= 1;
-        assigned_rank[k[i].idx] = r;
-        ++count;
-        break;
-      }
+    int32_t best = -1;
+    for (int32_t r = 0; r < world; ++r)
+      if (slots_left[r] > 0 && (best < 0 || free_rows[r] > free_rows[best])) best = r;
+    if (best >= 0 && k[i].cap <= free_rows[best]) {
+      free_rows[best] -= k[i].cap;
+      slots_left[best] -= 1;
+      assigned_rank[k[i].idx] = best;
+      ++count;
     }
   }
   free(k);
@@ -191,6 +195,7 @@ struct s3o_state {
   item* pool;
   int32_t npool, pool_cap;
   int64_t finished_total, evicted_total, tokens_total;
+  int64_t moved_at_admit;  /* R27: bytes shifted by admission-time compactions */
 };
 
 s3o_state* s3o_create(const s3o_config* c) {
@@ -347,7 +352,10 @@ int s3o_decode(s3o_state* s, const uint16_t* q, const uint16_t* k, const uint16_
     sl->len += 1;
     sl->gen += 1;
     s->tokens_total += 1;
-    if (eos[b]) s->status[b] = S3O_FINISHED;
+    /* R28: a sequence at the maximum length stops like one that emitted EOS
+     * ("prompt_tokens + output_tokens <= max_seq_len"; PAPER.md:127
+     * "a maximum sequence length of 2048 tokens"): its reservation cannot grow. */
+    if (eos[b] || sl->len == s->c.max_len) s->status[b] = S3O_FINISHED;
     else if (sl->len == sl->cap) s->status[b] = S3O_OVERRUN;
     else s->status[b] = S3O_RUNNING;
     if (status_out) status_out[b] = s->status[b];
@@ -473,6 +481,32 @@ static void place(s3o_state* s, const item* it) {
   s->B += 1;
 }
 
+/* R27 at admission: under the on-demand policy a step with an empty pool
+ * leaves its holes in place; once requests wait again (a later submit), the
+ * survivors are shifted up before the FFD so it sees the same free rows as
+ * under the every-step policy ("shifts the rows below the blank
+ * one so that all rows are stored contiguously").  Returns bytes moved.     */
+static int64_t compact_holes(s3o_state* s) {
+  const int64_t kvpt = s3o_kv_bytes_per_token(s->c.L, s->c.Hkv, s->c.D);
+  int64_t new_tail = 0, moved = 0;
+  for (int32_t b = 0; b < s->B; ++b) {
+    s3o_slot* sl = &s->slots[b];
+    if (sl->off != new_tail) {
+      memmove(s->arena + new_tail * s->row_elems, s->arena + sl->off * s->row_elems,
+              sizeof(uint16_t) * (size_t)(sl->len * s->row_elems));
+      moved += (int64_t)sl->len * kvpt;
+      sl->off = new_tail;
+    }
+    new_tail += sl->cap;
+  }
+  s->tail = new_tail;
+  return moved;
+}
+
+static void compact_if_waiting(s3o_state* s) {
+  if (s->c.compact_policy == 1 && s->npool > 0) s->moved_at_admit += compact_holes(s);
+}
+
 /* FFD over the pool items selected by `want` into this arena's free rows. */
 static int32_t admit_selected(s3o_state* s, const uint8_t* want, int64_t* admitted) {
   int32_t n = 0;
@@ -509,6 +543,7 @@ static int32_t admit_selected(s3o_state* s, const uint8_t* want, int64_t* admitt
  * placement order.                                                         */
 int32_t s3o_admit(s3o_state* s, int64_t* admitted) {
   if (s->status_valid) return -5;
+  compact_if_waiting(s);
   uint8_t* want = (uint8_t*)malloc((size_t)(s->npool + 1));
   for (int32_t i = 0; i < s->npool; ++i) want[i] = 1;
   int32_t n = admit_selected(s, want, admitted);
@@ -520,6 +555,7 @@ int32_t s3o_admit(s3o_state* s, int64_t* admitted) {
  * requests (their KV is in this rank's host store) by local FFD.          */
 int32_t s3o_admit_home(s3o_state* s, int64_t* admitted) {
   if (s->status_valid) return -5;
+  compact_if_waiting(s);      /* before the counters are exchanged (free rows = R - tail) */
   uint8_t* want = (uint8_t*)malloc((size_t)(s->npool + 1));
   for (int32_t i = 0; i < s->npool; ++i) want[i] = (uint8_t)s->pool[i].evicted;
   int32_t n = admit_selected(s, want, admitted);
@@ -566,6 +602,8 @@ int32_t s3o_admit_shared(s3o_state* s, int32_t world, int32_t rank, const int64_
  * information to the scheduler"):
  *   0 free_rows, 1 running, 2 free_slots, 3 evicted_waiting, 4 fresh_waiting,
  *   5 finished_total, 6 evicted_total, 7 tokens_total                      */
+int64_t s3o_moved_at_admit(const s3o_state* s) { return s->moved_at_admit; }
+
 void s3o_counters(const s3o_state* s, int64_t row[8]) {
   int64_t ev = 0, fr = 0;
   for (int32_t i = 0; i < s->npool; ++i) { if (s->pool[i].evicted) ++ev; else ++fr; }

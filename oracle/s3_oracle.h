@@ -78,6 +78,7 @@ int32_t s3o_admit_home(s3o_state* s, int64_t* admitted);
 int32_t s3o_admit_shared(s3o_state* s, int32_t world, int32_t rank, const int64_t* free_by_rank,
                          const int64_t* slots_left_by_rank, int64_t* admitted);
 void s3o_counters(const s3o_state* s, int64_t row[8]);
+int64_t s3o_moved_at_admit(const s3o_state* s);   /* R27 admission-time shifts, bytes */
 void s3o_attend_generated(const s3o_config* c, int64_t req, int32_t pos, int32_t l, double* out_hd);
 
 #ifdef __cplusplus

@@ -15,6 +15,7 @@
 #include <map>
 #include <memory>
 #include <new>
+#include <unordered_set>
 #include <vector>
 
 #include "../../include/s3.h"
@@ -93,6 +94,17 @@ int64_t ffd_scan(Pool& pool, MaxFit max_fit, Fit fit, Take take) {
   return count;
 }
 
+// Multi-bin placement (R26): the rank with the most free rows among
+// the ranks with a free slot (ties: lowest rank), or -1 if the item does not
+// fit there.  Worst fit spreads the freed rows evenly, so the lockstep step --
+// as long as the busiest rank's attention pass -- stays balanced.
+int worst_fit(int world, const int64_t* free_rows, const int64_t* free_slots, int64_t cap) {
+  int best = -1;
+  for (int r = 0; r < world; ++r)
+    if (free_slots[r] > 0 && (best < 0 || free_rows[r] > free_rows[best])) best = r;
+  return best >= 0 && cap <= free_rows[best] ? best : -1;
+}
+
 struct Prof {
   bool on = false;
   std::vector<cudaEvent_t> free_events;
@@ -161,6 +173,7 @@ struct s3_ctx {
   // pools
   Pool pool;        // world == 1: everything; world > 1: the shared fresh pool
   Pool home;        // world > 1: this rank's evicted requests
+  std::unordered_set<int64_t> live;   // req ids queued, running or evicted (not yet finished)
   int64_t n_evicted_waiting = 0;
   // host store allocator (first fit) + deferred frees
   std::map<int64_t, int64_t> free_blocks;
@@ -213,6 +226,7 @@ bool validate(const s3_config* c) {
   if (c->attn_variant < 0 || c->attn_variant > 2) return false;
   if (c->compact_mode < 0 || c->compact_mode > 1) return false;
   if (c->compact_policy < 0 || c->compact_policy > 1) return false;
+  if (c->reserve_sms < -1 || c->reserve_sms > 64) return false;
   return true;
 }
 
@@ -419,6 +433,48 @@ uint8_t* stage_ptr(const s3_ctx* c, int half) {
   return (uint8_t*)c->buf.staging + (c->stage_dbl ? (int64_t)half * stage_bytes(c) : 0);
 }
 
+// R27 at admission: under the on-demand policy a step whose pool was empty left
+// its holes in place; when requests wait again (a later s3_submit), shift the
+// survivors up before the FFD so it sees the free rows of the every-step
+// policy.  A keep-scan with every slot RUNNING and the ordered k_move.
+s3_status compact_holes(s3_ctx* ctx, int64_t* moved) {
+  *moved = 0;
+  const int32_t B = (int32_t)ctx->slots_h.size();
+  int64_t sum_cap = 0;
+  for (const DSlot& sl : ctx->slots_h) sum_cap += sl.cap;
+  if (sum_cap == ctx->tail) return S3_OK;        // no holes
+  const Shape& sh = ctx->sh;
+  CK(launch_keep_scan(sh, ctx->slots[ctx->cur], ctx->slots[1 - ctx->cur], B, ctx->S, ctx->report_dev, ctx->entries,
+                      ctx->key_chunk0, ctx->key_src, ctx->ctrl64, 0, 1, ctx->st), "k_keep_scan");
+  ctx->launches += 1;
+  CK(cudaMemcpyAsync(ctx->h_report, ctx->report_dev, (size_t)report_bytes(B), cudaMemcpyDeviceToHost, ctx->st),
+     "report D2H");
+  CK(cudaStreamSynchronize(ctx->st), "report sync");
+  const DReportHeader* h = reinterpret_cast<const DReportHeader*>(ctx->h_report);
+  if (h->n_before != B || h->n_kept != B || h->tail != sum_cap)
+    return fail(ctx, S3_E_CUDA, "admit: inconsistent compaction report");
+  if (h->n_chunks > 0) {
+    ctx->epoch++;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (ctx->prof.on) { e0 = ctx->prof.get(); e1 = ctx->prof.get(); cudaEventRecord(e0, ctx->st); }
+    const int grid = (int)std::min<int64_t>((h->n_chunks + 2 * 3 - 1) / (2 * 3), ctx->grid_move);
+    CK(launch_move((uint8_t*)ctx->buf.arena, (uint8_t*)ctx->buf.staging, ctx->entries, ctx->key_chunk0,
+                   ctx->key_src, h->n_entries, h->n_chunks, ctx->S, sh.kvpt, ctx->ctrl64, ctx->flags, ctx->epoch, 0,
+                   grid, ctx->st), "k_move");
+    ctx->launches += 1;
+    if (ctx->prof.on) {
+      cudaEventRecord(e1, ctx->st);
+      ctx->prof.pending.push_back({e0, e1, 2.0 * (double)h->moved_bytes, 1});
+    }
+  }
+  int64_t run = 0;
+  for (DSlot& sl : ctx->slots_h) { sl.off = (int32_t)run; run += sl.cap; }
+  ctx->tail = run;
+  ctx->cur = 1 - ctx->cur;
+  *moved = h->moved_bytes;
+  return S3_OK;
+}
+
 }  // namespace
 
 // ===========================================================================
@@ -484,6 +540,14 @@ s3_status s3_kv_init(const s3_config* cfg, const s3_buffers* b, s3_ctx** out) {
     int occ2 = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ2, attn_tma_kernel_ptr(sh), attn_block_threads(sh) + 64, smem);
     ctx->grid_attn = ctx->num_sms * std::max(1, occ2);
+  }
+  // persistent attention grids leave `reserve` SMs free for other streams' kernels (the
+  // multi-GPU counter all-reduce must not queue behind the whole attention pass)
+  {
+    const int reserve = cfg->reserve_sms > 0 ? cfg->reserve_sms : (cfg->reserve_sms == 0 && cfg->world > 1 ? 4 : 0);
+    const int per_sm = std::max(1, ctx->grid_attn / ctx->num_sms);
+    if (reserve >= ctx->num_sms / 2) return bail("reserve_sms too large");
+    ctx->grid_attn = (ctx->num_sms - reserve) * per_sm;
   }
   ctx->grid_combine = ctx->num_sms * 4;
   cudaFuncSetAttribute(move_kernel_ptr(), cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -560,8 +624,13 @@ s3_status s3_submit(s3_ctx* ctx, const s3_request* reqs, int32_t n) {
       return fail(ctx, S3_E_INVAL, "submit: bad request");
     if ((int64_t)r.prompt_len + r.alloc_out > ctx->cfg.arena_rows)
       return fail(ctx, S3_E_UNSCHEDULABLE, "submit: reservation larger than the arena");
-    if (ctx->pool.count(Key{(int64_t)r.prompt_len + r.alloc_out, r.req_id}))
-      return fail(ctx, S3_E_INVAL, "submit: duplicate request");
+  }
+  {  // a req id may be live only once: not already queued / running / evicted, not twice in this call
+    std::unordered_set<int64_t> seen;
+    seen.reserve((size_t)n);
+    for (int32_t i = 0; i < n; ++i)
+      if (ctx->live.count(reqs[i].req_id) || !seen.insert(reqs[i].req_id).second)
+        return fail(ctx, S3_E_INVAL, "submit: duplicate request id");
   }
   for (int32_t i = 0; i < n; ++i) {
     const s3_request& r = reqs[i];
@@ -569,6 +638,7 @@ s3_status s3_submit(s3_ctx* ctx, const s3_request* reqs, int32_t n) {
     it.req = r.req_id; it.prompt = r.prompt_len; it.gen = 0; it.cap = r.prompt_len + r.alloc_out;
     it.evicted = 0; it.host_off = -1;
     ctx->pool.emplace(Key{it.cap, it.req}, it);
+    ctx->live.insert(it.req);
   }
   return S3_OK;
 }
@@ -580,6 +650,9 @@ s3_status s3_decode_step(s3_ctx* ctx, int32_t l0, int32_t nl, const void* q, con
   if (l0 < 0 || nl < 1 || l0 + nl > ctx->sh.L) return fail(ctx, S3_E_INVAL, "decode_step: layer range");
   const bool finalize = (l0 + nl == ctx->sh.L);
   const int32_t B = (int32_t)ctx->slots_h.size();
+  if (l0 == 0)   // the append row off+len must lie inside the slot (R28 stops sequences at max_len)
+    for (const DSlot& s : ctx->slots_h)
+      if (s.len >= s.cap) return fail(ctx, S3_E_STATE, "decode_step: a slot has no free row (len >= cap)");
   // fuse the row shift into this attention pass when the step is whole
   const bool fuse = finalize && l0 == 0 && ctx->cfg.compact_mode == 0 && B > 0 &&
                     ((ctx->cfg.attn_variant == 0 && attn_tma_stages(ctx->sh) >= 2) || ctx->cfg.attn_variant == 2);
@@ -601,7 +674,13 @@ s3_status s3_decode_step(s3_ctx* ctx, int32_t l0, int32_t nl, const void* q, con
     pa.eos = eos; pa.finalize = finalize ? 1 : 0; pa.fuse = fuse ? 1 : 0;
     pa.compact_policy = ctx->cfg.compact_policy;
     pa.pool_nonempty = (ctx->pool.size() + ctx->home.size()) > 0 ? 1 : 0;
-    pa.staging_bytes = stage_bytes(ctx);
+    // fuse the evictions only when their rows also fit the host store: the largest free
+    // block takes every evictee, so s3_evict_compact cannot run out of host store after
+    // the kernel has already moved them out of the arena
+    flush_deferred(ctx);
+    int64_t largest = 0;
+    for (const auto& fb : ctx->free_blocks) largest = std::max(largest, fb.second);
+    pa.staging_bytes = std::min(stage_bytes(ctx), largest);
     pa.units = ctx->units; pa.splits = ctx->splits; pa.ctrl = ctx->ctrl;
     // fused: k_prep writes the keep-scan report straight into pinned host memory, so the
     // host's eviction bookkeeping and FFD start as soon as k_prep ends (overlapping the
@@ -815,7 +894,14 @@ s3_status s3_evict_compact(s3_ctx* ctx, s3_evict_report* rep, int32_t* perm, s3_
       flush_deferred(ctx);
       hoff[i] = hs_alloc(ctx, (int64_t)dev[i].len * sh.kvpt);
     }
-    if (hoff[i] < 0) return fail(ctx, S3_E_CUDA, "evict_compact: host store exhausted");
+    if (hoff[i] < 0) {
+      for (int32_t j = 0; j < i; ++j) hs_free(ctx, hoff[j], (int64_t)dev[j].len * sh.kvpt);
+      if (fused) {   // the decode step already took the evictees' rows out of the arena
+        ctx->poisoned = true;
+        return fail(ctx, S3_E_NOMEM, "evict_compact: host store exhausted after a fused step (context poisoned)");
+      }
+      return fail(ctx, S3_E_NOMEM, "evict_compact: host store too small for this step's evictions");
+    }
   }
   // the fused step already wrote its evictees to half stage_cur; the k_move path takes the next half
   if (!fused) ctx->stage_cur = ctx->stage_next;
@@ -927,6 +1013,7 @@ s3_status s3_evict_compact(s3_ctx* ctx, s3_evict_report* rep, int32_t* perm, s3_
   ctx->cur = 1 - ctx->cur;
   ctx->status_pending = false;
   if (finished_ids) std::memcpy(finished_ids, dfin, sizeof(int64_t) * (size_t)h->n_finished);
+  for (int32_t i = 0; i < h->n_finished; ++i) ctx->live.erase(dfin[i]);
   ctx->finished_total += h->n_finished;
   ctx->evicted_total += h->n_evicted;
   r.n_finished = h->n_finished;
@@ -955,6 +1042,9 @@ s3_status s3_admit(s3_ctx* ctx, s3_admit_report* rep, int64_t* admitted_ids) {
   if (s3_status s = check_ctx(ctx)) return s;
   if (ctx->status_pending) return fail(ctx, S3_E_STATE, "admit: statuses not consumed");
   if (ctx->cfg.world != 1) return fail(ctx, S3_E_STATE, "admit: world > 1 uses admit_home/admit_shared");
+  int64_t moved = 0;
+  if (ctx->cfg.compact_policy == 1 && !ctx->pool.empty())
+    if (s3_status s = compact_holes(ctx, &moved)) return s;
   int64_t free_rows = ctx->cfg.arena_rows - ctx->tail;
   int64_t slots_left = ctx->cfg.max_running - (int64_t)ctx->slots_h.size();
   std::vector<Item> taken;
@@ -962,12 +1052,17 @@ s3_status s3_admit(s3_ctx* ctx, s3_admit_report* rep, int64_t* admitted_ids) {
       ctx->pool, [&] { return slots_left > 0 ? free_rows : 0; },
       [&](int64_t cap) { return cap <= free_rows ? 0 : -1; },
       [&](int, const Item& it) { free_rows -= it.cap; slots_left--; taken.push_back(it); });
-  return place_items(ctx, taken, rep, admitted_ids);
+  const s3_status st = place_items(ctx, taken, rep, admitted_ids);
+  if (rep) rep->moved_bytes = moved;
+  return st;
 }
 
 s3_status s3_admit_home(s3_ctx* ctx, s3_admit_report* rep, int64_t* admitted_ids) {
   if (s3_status s = check_ctx(ctx)) return s;
   if (ctx->status_pending) return fail(ctx, S3_E_STATE, "admit_home: statuses not consumed");
+  int64_t moved = 0;   // before the counters are exchanged: free rows = R - tail
+  if (ctx->cfg.compact_policy == 1 && (!ctx->pool.empty() || !ctx->home.empty()))
+    if (s3_status s = compact_holes(ctx, &moved)) return s;
   int64_t free_rows = ctx->cfg.arena_rows - ctx->tail;
   int64_t slots_left = ctx->cfg.max_running - (int64_t)ctx->slots_h.size();
   std::vector<Item> taken;
@@ -975,7 +1070,9 @@ s3_status s3_admit_home(s3_ctx* ctx, s3_admit_report* rep, int64_t* admitted_ids
       ctx->home, [&] { return slots_left > 0 ? free_rows : 0; },
       [&](int64_t cap) { return cap <= free_rows ? 0 : -1; },
       [&](int, const Item& it) { free_rows -= it.cap; slots_left--; taken.push_back(it); });
-  return place_items(ctx, taken, rep, admitted_ids);
+  const s3_status st = place_items(ctx, taken, rep, admitted_ids);
+  if (rep) rep->moved_bytes = moved;
+  return st;
 }
 
 s3_status s3_admit_shared(s3_ctx* ctx, const int64_t* counters_all, s3_admit_report* rep,
@@ -996,10 +1093,7 @@ s3_status s3_admit_shared(s3_ctx* ctx, const int64_t* counters_all, s3_admit_rep
         for (int r = 0; r < W; ++r) if (sl[r] > 0) m = std::max(m, fr[r]);
         return m;
       },
-      [&](int64_t cap) {
-        for (int r = 0; r < W; ++r) if (sl[r] > 0 && cap <= fr[r]) return r;
-        return -1;
-      },
+      [&](int64_t cap) { return worst_fit(W, fr.data(), sl.data(), cap); },
       [&](int bin, const Item& it) {
         fr[bin] -= it.cap;
         sl[bin]--;
@@ -1056,10 +1150,7 @@ int32_t s3_plan_ffd_multibin(int32_t n, const int64_t* cap, const int64_t* req_i
         for (int r = 0; r < world; ++r) if (free_slots[r] > 0) m = std::max(m, free_rows[r]);
         return m;
       },
-      [&](int64_t c) {
-        for (int r = 0; r < world; ++r) if (free_slots[r] > 0 && c <= free_rows[r]) return r;
-        return -1;
-      },
+      [&](int64_t c) { return worst_fit(world, free_rows, free_slots, c); },
       [&](int bin, const Item& it) {
         free_rows[bin] -= it.cap;
         free_slots[bin]--;

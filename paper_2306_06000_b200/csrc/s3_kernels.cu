@@ -186,8 +186,9 @@ __device__ __forceinline__ uint4 gen8(const Shape& sh, uint64_t seed, uint64_t t
 
 // ---------------------------------------------------------------------------
 // k_prep: one CTA of 1024 threads (B <= max_running; a few microseconds).
-//  * detection (R11): when finalize, status_b = FINISHED if
-//    eos_b, else OVERRUN if len_b + 1 == cap_b, else RUNNING;
+//  * detection (R11, R28): when finalize, status_b = FINISHED
+//    if eos_b or len_b + 1 == max_len, else OVERRUN if len_b + 1 == cap_b,
+//    else RUNNING;
 //  * work list: slot b's len_b + 1 rows (with the new one) are cut into
 //    ceil((len_b+1)/C) units (split-K); per unit, ceil(rows/AT_RPS) ring
 //    stages;
@@ -199,6 +200,16 @@ __device__ __forceinline__ uint4 gen8(const Shape& sh, uint64_t seed, uint64_t t
 //    (sum of kept caps before b), the permutation, evicted / finished lists
 //    and the packed report; the gathered slot table goes to `next`.
 // ---------------------------------------------------------------------------
+// Detection after the step's append (len + 1 rows): FINISHED on EOS or at the
+// maximum length (R28: the reservation cannot grow past max_len, so
+// the sequence stops like one that emitted EOS), else OVERRUN when the
+// reservation is used up, else RUNNING.
+__device__ __forceinline__ int detect(const PrepArgs& a, const DSlot& sl, int b) {
+  if (!a.finalize) return 0;
+  if (a.eos[b] || sl.len + 1 >= a.sh.max_len) return 1;
+  return sl.len + 1 == sl.cap ? 2 : 0;
+}
+
 __global__ void __launch_bounds__(1024) k_prep(PrepArgs a) {
   __shared__ int s_first_hole;
   __shared__ unsigned long long s_hbm, s_moved;
@@ -220,7 +231,7 @@ __global__ void __launch_bounds__(1024) k_prep(PrepArgs a) {
       const int rows = min((i + 1) * C, sl.len) - i * C;
       x[3] += rows > 0 ? (rows + AT_RPS - 1) / AT_RPS : 1;
     }
-    const int st = !a.finalize ? 0 : (a.eos[b] ? 1 : (sl.len + 1 == sl.cap ? 2 : 0));
+    const int st = detect(a, sl, b);
     x[4] += st == 0;
     x[5] += st == 0 ? sl.cap : 0;
     x[6] += st == 1;
@@ -244,7 +255,7 @@ __global__ void __launch_bounds__(1024) k_prep(PrepArgs a) {
   for (int b = b0; b < b1; ++b) {
     DSlot sl = a.slots[b];
     const int k = (sl.len + 1 + C - 1) / C;
-    const int st = !a.finalize ? 0 : (a.eos[b] ? 1 : (sl.len + 1 == sl.cap ? 2 : 0));
+    const int st = detect(a, sl, b);
     int mode = UNIT_STAY;
     int64_t dst = sl.off;
     if (fused) {

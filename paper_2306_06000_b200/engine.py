@@ -39,7 +39,7 @@ class S3Engine:
     def __init__(self, num_layers, num_heads, head_dim, max_seq_len, arena_rows, max_running,
                  chunk_rows=0, move_chunk_bytes=0, device=0, rank=0, world=1, seed=1,
                  staging_bytes=None, host_store_bytes=None, io_rows=None, attn_variant=0, compact_mode=0,
-                 compact_policy=0, num_kv_heads=0):
+                 compact_policy=0, num_kv_heads=0, reserve_sms=0):
         if not torch.cuda.is_available():
             raise RuntimeError("S3Engine needs a CUDA device (no CPU fallback)")
         self.device = torch.device("cuda", device)
@@ -54,7 +54,7 @@ class S3Engine:
             arena_rows=arena_rows, max_running=max_running, chunk_rows=chunk_rows,
             move_chunk_bytes=move_chunk_bytes, device=device, stream=self.stream.cuda_stream,
             rank=rank, world=world, synth_seed=seed, attn_variant=attn_variant, compact_mode=compact_mode,
-            compact_policy=compact_policy, num_kv_heads=num_kv_heads)
+            compact_policy=compact_policy, num_kv_heads=num_kv_heads, reserve_sms=reserve_sms)
         arena_b, ws_b, st_min, hs_min = abi.s3_workspace_query(self.cfg)
         self.kvpt = 4 * num_layers * self.Hkv * head_dim
         self.arena = torch.empty(arena_b, dtype=torch.uint8, device=self.device)
@@ -76,6 +76,8 @@ class S3Engine:
         self.out = torch.empty(n, dtype=torch.float32, device=self.device)
         self.eos = torch.empty(max(rows, 1), dtype=torch.uint8, device=self.device)
         self.out_len = None
+        self._out_len_h = None
+        self.max_seq_len = max_seq_len
         self.counters = np.zeros(abi.S3_NCOUNTERS, np.int64)
 
     # ---- lifecycle -----------------------------------------------------
@@ -101,10 +103,20 @@ class S3Engine:
             arr[i].prompt_len = int(prompt[i])
             arr[i].alloc_out = int(alloc[i])
         abi.s3_submit(self.ctx, arr)
-        if out_len is not None:
-            o = np.full(int(np.max(req_id)) + 1, 1 << 30, np.int32)
-            o[np.asarray(req_id)] = np.asarray(out_len, np.int32)
-            self.out_len = torch.from_numpy(o).to(self.device)
+        # the sampler stand-in's table (indexed by req_id), kept across submit calls;
+        # requests without an out_len run to the maximum length (R28)
+        ids = np.asarray(req_id, np.int64)
+        if n == 0:
+            return
+        need = int(ids.max()) + 1
+        if self._out_len_h is None or self._out_len_h.shape[0] < need:
+            grown = np.zeros(max(need, 2 * (0 if self._out_len_h is None else self._out_len_h.shape[0])), np.int32)
+            if self._out_len_h is not None:
+                grown[:self._out_len_h.shape[0]] = self._out_len_h
+            self._out_len_h = grown
+        self._out_len_h[ids] = (np.asarray(out_len, np.int32) if out_len is not None
+                                else self.max_seq_len - np.asarray(prompt, np.int32))
+        self.out_len = torch.from_numpy(self._out_len_h).to(self.device)
 
     # ---- the four calls --------------------------------------------------
     @property

@@ -34,7 +34,7 @@ class s3_config(C.Structure):
                 ("chunk_rows", C.c_int32), ("move_chunk_bytes", C.c_int32), ("device", C.c_int32),
                 ("stream", C.c_void_p), ("rank", C.c_int32), ("world", C.c_int32),
                 ("synth_seed", C.c_uint64), ("attn_variant", C.c_int32), ("compact_mode", C.c_int32),
-                ("compact_policy", C.c_int32), ("num_kv_heads", C.c_int32)]
+                ("compact_policy", C.c_int32), ("num_kv_heads", C.c_int32), ("reserve_sms", C.c_int32)]
 
 
 class s3_buffers(C.Structure):
@@ -64,7 +64,7 @@ class s3_evict_report(C.Structure):
 class s3_admit_report(C.Structure):
     _fields_ = [("n_admitted", C.c_int32), ("n_fresh", C.c_int32), ("n_reloaded", C.c_int32),
                 ("n_batch", C.c_int32), ("tail_rows", C.c_int64), ("fill_bytes", C.c_int64),
-                ("h2d_bytes", C.c_int64)]
+                ("h2d_bytes", C.c_int64), ("moved_bytes", C.c_int64)]
 
 
 class s3_slot(C.Structure):

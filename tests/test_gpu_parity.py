@@ -42,17 +42,24 @@ def u16(t: torch.Tensor) -> np.ndarray:
 
 def lockstep(trace, L, H, D, R, C=0, S=0, max_running=4096, staging=True, feed_oracle_inputs=False,
              max_steps=100000, check_arena=True, attn_variant=0, compact_mode=0, poison=False,
-             compact_policy=0, Hkv=0, host_io=False, chunks=0, device_out=False, staging_mult=1):
+             compact_policy=0, Hkv=0, host_io=False, chunks=0, device_out=False, staging_mult=1, late=None,
+             reserve_sms=0):
     from paper_2306_06000_b200.engine import S3Engine
     eng = S3Engine(L, H, D, trace.max_seq_len, R, max_running, chunk_rows=C, move_chunk_bytes=S,
                    staging_bytes=(None if staging_mult == 1 else staging_mult * trace.max_seq_len * 4 * L * (Hkv or H) * D)
                    if staging else 0, host_store_bytes=64 << 20, attn_variant=attn_variant,
-                   compact_mode=compact_mode, compact_policy=compact_policy, num_kv_heads=Hkv)
+                   compact_mode=compact_mode, compact_policy=compact_policy, num_kv_heads=Hkv,
+                   reserve_sms=reserve_sms)
     eng.profile(True)
     orc = oracle.Oracle(L, H, D, trace.max_seq_len, R, max_running=max_running, compact_policy=compact_policy,
                         Hkv=Hkv)
-    eng.submit(trace.req_id, trace.prompt, trace.alloc, trace.out)
-    orc.submit(trace.req_id, trace.prompt, trace.alloc)
+    # late = (step, request indices): those requests are submitted only at that
+    # step, between evict_compact and admit (R27's admission-time shift)
+    first = np.ones(trace.n, bool)
+    if late is not None:
+        first[late[1]] = False
+    eng.submit(trace.req_id[first], trace.prompt[first], trace.alloc[first], trace.out[first])
+    orc.submit(trace.req_id[first], trace.prompt[first], trace.alloc[first])
     _, adm_g = eng.admit()
     adm_o = orc.admit()
     assert adm_g == adm_o
@@ -66,9 +73,10 @@ def lockstep(trace, L, H, D, R, C=0, S=0, max_running=4096, staging=True, feed_o
         hv = torch.empty(eng.v_new.numel(), dtype=torch.bfloat16, pin_memory=True)
         he = torch.empty(eng.eos.numel(), dtype=torch.uint8, pin_memory=True)
         ho = torch.empty(eng.out.numel(), dtype=torch.float32, pin_memory=True)
+    moved_admit = 0
     while True:
         c = orc.counters()
-        if orc.B == 0 and c[3] + c[4] == 0:
+        if orc.B == 0 and c[3] + c[4] == 0 and (late is None or steps > late[0]):
             assert eng.B == 0
             break
         assert steps < max_steps
@@ -135,8 +143,14 @@ def lockstep(trace, L, H, D, R, C=0, S=0, max_running=4096, staging=True, feed_o
                 assert np.array_equal(host_g, orc.host_kv(e.req_id).reshape(-1))
         stats["evictions"] += rep_o.n_evicted
         stats["moved"] += rep_o.moved_bytes
-        _, adm_g = eng.admit()
+        if late is not None and steps == late[0]:
+            i = late[1]
+            eng.submit(trace.req_id[i], trace.prompt[i], trace.alloc[i], trace.out[i])
+            orc.submit(trace.req_id[i], trace.prompt[i], trace.alloc[i])
+        arep, adm_g = eng.admit()
+        moved_admit += arep.moved_bytes
         adm_o = orc.admit()
+        assert moved_admit == orc.moved_at_admit()
         assert adm_g == adm_o, f"step {steps}: admissions differ"
         if check_arena:
             A_o = orc.arena()
@@ -147,6 +161,7 @@ def lockstep(trace, L, H, D, R, C=0, S=0, max_running=4096, staging=True, feed_o
         steps += 1
     assert eng.verify_resident() == 0
     stats["fused_steps"] = eng.profile_get().fused_steps
+    stats["moved_at_admit"] = moved_admit
     eng.close()
     return dict(steps=steps, worst=worst, **stats)
 
@@ -575,3 +590,74 @@ def test_double_buffered_staging_heavy_evictions(variant, Hkv, D, H):
     t = s3synth.make_trace(60, seed=11, policy="short", p=0.6, max_seq_len=192, prompt_max=48)
     r = lockstep(t, 2, H, D, 1200, C=32, attn_variant=variant, Hkv=Hkv, staging_mult=3, poison=True)
     assert r["evictions"] >= 20 and r["fused_steps"] >= 0.9 * r["steps"]
+
+
+# ---------------------------------------------------------------------------
+# round 2: length stop (R28), admission-time compaction (R27), error paths
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("variant,mode", [(0, 0), (0, 1), (1, 1)])
+def test_no_eos_length_stop(variant, mode):
+    # the sampler never emits EOS: every request runs to max_len, is evicted and
+    # doubled on the way, and finishes by the length stop (never len > cap)
+    t = s3synth.make_trace(40, seed=13, policy="short", p=0.6, max_seq_len=48, prompt_max=12)
+    t.out[:] = 1 << 30
+    r = lockstep(t, 2, 4, 64, 300, C=8, S=1024, attn_variant=variant, compact_mode=mode)
+    assert r["evictions"] > 0
+
+
+def test_no_eos_length_stop_tensor_cores():
+    t = s3synth.make_trace(40, seed=14, policy="short", p=0.6, max_seq_len=64, prompt_max=12)
+    t.out[:] = 1 << 30
+    r = lockstep(t, 2, 8, 128, 400, C=16, attn_variant=2, Hkv=2)
+    assert r["evictions"] > 0
+
+
+@pytest.mark.parametrize("variant,mode", [(0, 0), (0, 1), (2, 0)])
+def test_on_demand_late_submit(variant, mode):
+    # maxlen caps (all equal) -> finishes leave interior holes; the pool empties;
+    # 20 requests arrive between a step's evict_compact and its admission
+    t = s3synth.make_trace(60, seed=31, policy="maxlen", max_seq_len=128, prompt_max=20)
+    Hkv = 2 if variant == 2 else 0
+    r = lockstep(t, 2, 8 if variant == 2 else 4, 128 if variant == 2 else 64, 40 * 128 + 100, C=16,
+                 attn_variant=variant, compact_mode=mode, compact_policy=1, Hkv=Hkv,
+                 late=(40, np.arange(40, 60)))
+    assert r["moved_at_admit"] > 0
+
+
+def test_duplicate_submit_and_host_store_exhaustion():
+    from paper_2306_06000_b200 import s3 as abi
+    from paper_2306_06000_b200.engine import S3Engine
+    t = s3synth.make_trace(30, seed=2, policy="short", p=1.0, max_seq_len=64, prompt_max=8)
+    L, H, D = 1, 2, 64
+    kvpt = 4 * L * H * D
+    # host store for ~1 eviction only: the fused step must not stage more than fits
+    eng = S3Engine(L, H, D, 64, 2000, 64, host_store_bytes=64 * kvpt)
+    eng.submit(t.req_id, t.prompt, t.alloc, t.out)
+    with pytest.raises(abi.S3Error) as e:
+        eng.submit(t.req_id[:1], t.prompt[:1], t.alloc[:1], t.out[:1])      # already live
+    assert e.value.code == 1
+    with pytest.raises(abi.S3Error) as e:
+        eng.submit(np.array([100, 100]), np.array([3, 3]), np.array([4, 4]), np.array([4, 4]))
+    assert e.value.code == 1
+    eng.admit()
+    hit = False
+    for _ in range(200):
+        if not eng.B:
+            break
+        eng.synth_inputs()
+        eng.decode()
+        try:
+            eng.evict_compact()
+        except abi.S3Error as err:
+            assert err.code == 2                         # S3_E_NOMEM, context still usable
+            hit = True
+            break
+        eng.evict_wait()
+        eng.admit()
+    assert hit
+    assert eng.B > 0                                     # state unchanged, not poisoned
+    with pytest.raises(abi.S3Error) as e:
+        eng.evict_compact()
+    assert e.value.code == 2
+    eng.close()

@@ -606,3 +606,88 @@ def test_gqa_attention_matches_sdpa_with_repeated_kv(oracle_lib, H, Hkv):
             assert np.allclose(out[l, b], ref, rtol=0, atol=1e-12)
     # kvpt shrinks with the KV heads (PAPER.md:111 formula with d_h -> Hkv*D)
     assert o.kvpt == 4 * L * Hkv * D
+
+
+# ---------------------------------------------------------------------------
+# R28 length stop, R26 worst-fit placement, R27 admission-time compaction
+# ---------------------------------------------------------------------------
+
+def test_length_stop_without_eos(oracle_lib):
+    # R28: with no EOS ever, a request generates until len == max_len and
+    # finishes there (SPEC.md:44 P + O <= max_seq_len); on the way its
+    # reservation doubles (P3's closed form with O = max_len - P), and the
+    # run terminates with sum_t B_t = sum_r (max_len - P_r).
+    t = s3synth.make_trace(120, seed=23, policy="short", p=0.5, max_seq_len=64, prompt_max=20)
+    never = s3synth.Trace(t.req_id, t.prompt, np.full(t.n, 1 << 30, np.int32), t.alloc, t.max_seq_len)
+    res = run_oracle(never, R=600)
+    for r in range(t.n):
+        O = t.max_seq_len - int(t.prompt[r])
+        assert res["evict_gens"].get(r, []) == expected_evictions(int(t.cap[r]), int(t.prompt[r]), O,
+                                                                   t.max_seq_len)
+    assert len(res["finished_step"]) == t.n
+    assert sum(res["batch_sizes"]) == int((t.max_seq_len - t.prompt.astype(np.int64)).sum())
+
+
+def test_multibin_worst_fit_placement(oracle_lib):
+    # R26: an item goes to the rank with the most free rows (ties: lowest
+    # rank) -- first fit would fill rank 0 first.
+    who = oracle.ffd_multibin([5, 4, 3], [0, 1, 2], [10, 20, 20], [4, 4, 4])
+    # free [10, 20, 20]: 5 -> rank 1 (tie, lower rank) -> [10, 15, 20]; 4 -> rank 2 -> [10, 15, 16];
+    # 3 -> rank 2 (16 > 15).  First fit would give [1, 1, 0].
+    assert list(who) == [1, 2, 2]
+    rng = np.random.default_rng(29)
+    for _ in range(300):
+        n = int(rng.integers(1, 40))
+        G = int(rng.integers(2, 9))
+        caps = rng.integers(1, 50, n)
+        reqs = rng.permutation(n)
+        free = rng.integers(0, 200, G)
+        slots = np.full(G, 1 << 20)
+        who = oracle.ffd_multibin(caps, reqs, free, slots)
+        left = free - np.array([caps[who == r].sum() for r in range(G)])
+        assert (left >= 0).all()
+        # LPT-style balance bound of greedy worst fit: a rank that received an
+        # item had the most free rows when its last item arrived, so it ends at
+        # most (that item's cap) below the final maximum.  First fit breaks it.
+        for r in range(G):
+            if (who == r).any():
+                order = np.lexsort((reqs[who == r], -caps[who == r]))
+                last_cap = caps[who == r][order[-1]]
+                assert left[r] >= left.max() - last_cap
+
+
+def test_on_demand_compaction_late_submit(oracle_lib):
+    # R27 at admission: a step with an empty pool leaves holes; a request
+    # submitted later must see the every-step free rows (the advisor's case:
+    # without the admission-time shift it would be admitted later or not at all).
+    # max-length caps (all 128 rows): finishes leave interior holes
+    t = s3synth.make_trace(60, seed=31, policy="maxlen", max_seq_len=128, prompt_max=20)
+    first, late = np.arange(40), np.arange(40, 60)
+    logs = {}
+    for pol in (0, 1):
+        o = oracle.Oracle(1, 2, 64, 128, 40 * 128 + 100, compact_policy=pol)
+        o.submit(t.req_id[first], t.prompt[first], t.alloc[first])
+        ev = [tuple(o.admit())]
+        views = []
+        step = 0
+        while True:
+            c = o.counters()
+            if o.B == 0 and c[3] + c[4] == 0 and step > 40:
+                break
+            if o.B:
+                q, k, v, eos = o.make_inputs(t.out)
+                o.decode(q, k, v, eos)
+                o.evict_compact()
+            if step == 40:      # between the step's evict_compact (empty pool) and the admission
+                o.submit(t.req_id[late], t.prompt[late], t.alloc[late])
+            waiting = o.counters()[4] > 0
+            ev.append(tuple(o.admit()))
+            views.append(tuple(o.batch()) if waiting else None)
+            step += 1
+        logs[pol] = (ev, views, o.moved_at_admit())
+    assert logs[0][0] == logs[1][0]          # identical admissions
+    # identical layouts after every admission that had requests waiting (holes
+    # stay only while nobody could use them)
+    assert logs[0][1] == logs[1][1]
+    assert logs[1][1][40] is not None
+    assert logs[0][2] == 0 and logs[1][2] > 0
