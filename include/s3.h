@@ -215,6 +215,8 @@ typedef struct {
   int64_t h2d_bytes;         /* evicted KV reloaded from host_store                        */
   int64_t moved_bytes;       /* compact_policy 1 (R27): rows shifted over holes a step with an
                                 empty pool left in place, before this admission (one way)  */
+  int64_t stage_reload_bytes;/* evicted KV re-admitted in the step that evicted it, reloaded
+                                from the device staging copy (HBM) instead of host_store   */
 } s3_admit_report;
 /* compact_policy 1 (R27): when requests wait and an earlier step left holes
  * (its pool was empty), s3_admit / s3_admit_home first shift the survivors

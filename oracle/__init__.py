@@ -21,11 +21,12 @@ RUNNING, FINISHED, OVERRUN = 0, 1, 2
 
 
 def build(force: bool = False) -> str:
-    """Compile the oracle with gcc (plain -O2, no OpenMP, no vectorisation tricks)."""
+    """Compile the oracle with gcc (plain -O2; -fopenmp only for the optional
+    thread split of the attention loop, off unless set_threads(n > 1))."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(
             os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "s3_oracle.h"))):
         tmp = _LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-shared", "-fPIC", "-o", tmp, _SRC, "-lm"])
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fopenmp", "-shared", "-fPIC", "-o", tmp, _SRC, "-lm"])
         os.replace(tmp, _LIB)
     return _LIB
 
@@ -80,6 +81,7 @@ def lib():
             "s3o_host_kv": (i64, [P, i64, P]),
             "s3o_make_inputs": (None, [P, P, P, P, P, P]),
             "s3o_decode": (C.c_int, [P, P, P, P, P, P, P]),
+            "s3o_set_threads": (None, [C.c_int]),
             "s3o_evict_compact": (C.c_int, [P, P, P, P, P]),
             "s3o_admit": (i32, [P, P]),
             "s3o_admit_home": (i32, [P, P]),
@@ -159,6 +161,11 @@ def attend_generated(L, H, D, max_len, seed, req, pos, l, Hkv=0) -> np.ndarray:
     out = np.zeros(H * D, dtype=np.float64)
     lib().s3o_attend_generated(C.byref(cfg), req, pos, l, _p(out))
     return out.reshape(H, D)
+
+
+def set_threads(n: int) -> None:
+    """Threads of the oracle's attention loop (1 = the plain sequential oracle)."""
+    lib().s3o_set_threads(int(n))
 
 
 def bf16_bits_to_f64(bits: np.ndarray) -> np.ndarray:

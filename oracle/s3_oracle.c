@@ -329,26 +329,46 @@ static void attend(const uint16_t* q_hd, const uint16_t* K0, const uint16_t* V0,
  * PAPER.md:174 [§3 Supervisor]: a sequence that is "not finished but used up
  * its reserved memory" is an overrun; R11: EOS at len == cap is FINISHED.
  * out: double [L][B][H][D].  status_out (optional): uint8 [B].            */
+/* Threads for the attention loop of s3o_decode (1 = the plain sequential
+ * oracle; used by bench.py's cpu_baseline to time it on all host cores).   */
+static int s3o_threads = 1;
+void s3o_set_threads(int n) { s3o_threads = n > 0 ? n : 1; }
+
 int s3o_decode(s3o_state* s, const uint16_t* q, const uint16_t* k, const uint16_t* v,
                const uint8_t* eos, double* out, uint8_t* status_out) {
   if (s->status_valid) return 5;  /* previous statuses not yet consumed */
   const int32_t H = s->c.H, D = s->c.D, L = s->c.L, Hkv = s->c.Hkv;
   const int64_t HD = (int64_t)H * D, KD = (int64_t)Hkv * D;
-  double* sc = (double*)malloc(sizeof(double) * (size_t)(s->c.max_len + 1));
+  for (int32_t b = 0; b < s->B; ++b)
+    if (s->slots[b].len >= s->slots[b].cap) return 5;
+  /* append: row off+pos <- (k_new, v_new) for every (b, l) */
   for (int32_t b = 0; b < s->B; ++b) {
-    s3o_slot* sl = &s->slots[b];
-    if (sl->len >= sl->cap) { free(sc); return 5; }
-    const int32_t pos = sl->len;
+    const s3o_slot* sl = &s->slots[b];
     for (int32_t l = 0; l < L; ++l) {
-      const int64_t io = ((int64_t)l * s->B + b) * HD;
       const int64_t ko = ((int64_t)l * s->B + b) * KD;
-      /* append: row off+pos <- (k_new, v_new) */
-      memcpy(row_ptr(s, sl->off + pos, l, 0), k + ko, sizeof(uint16_t) * (size_t)KD);
-      memcpy(row_ptr(s, sl->off + pos, l, 1), v + ko, sizeof(uint16_t) * (size_t)KD);
-      /* attend over rows 0..pos (self included, R1) */
-      attend(q + io, row_ptr(s, sl->off, l, 0), row_ptr(s, sl->off, l, 1), s->row_elems, pos + 1,
+      memcpy(row_ptr(s, sl->off + sl->len, l, 0), k + ko, sizeof(uint16_t) * (size_t)KD);
+      memcpy(row_ptr(s, sl->off + sl->len, l, 1), v + ko, sizeof(uint16_t) * (size_t)KD);
+    }
+  }
+  /* attend over rows 0..pos (self included, R1).  The (b, l) pairs are
+   * independent (each reads only its own slot's rows), so the optional
+   * threads of s3o_set_threads split them; the arithmetic is unchanged.    */
+  const int64_t pairs = (int64_t)s->B * L;
+#pragma omp parallel num_threads(s3o_threads)
+  {
+    double* sc = (double*)malloc(sizeof(double) * (size_t)(s->c.max_len + 1));
+#pragma omp for schedule(dynamic, 1)
+    for (int64_t pr = 0; pr < pairs; ++pr) {
+      const int32_t b = (int32_t)(pr / L), l = (int32_t)(pr % L);
+      const s3o_slot* sl = &s->slots[b];
+      const int64_t io = ((int64_t)l * s->B + b) * HD;
+      attend(q + io, row_ptr(s, sl->off, l, 0), row_ptr(s, sl->off, l, 1), s->row_elems, sl->len + 1,
              H, Hkv, D, sc, out + io);
     }
+    free(sc);
+  }
+  for (int32_t b = 0; b < s->B; ++b) {
+    s3o_slot* sl = &s->slots[b];
     sl->len += 1;
     sl->gen += 1;
     s->tokens_total += 1;
@@ -360,7 +380,6 @@ int s3o_decode(s3o_state* s, const uint16_t* q, const uint16_t* k, const uint16_
     else s->status[b] = S3O_RUNNING;
     if (status_out) status_out[b] = s->status[b];
   }
-  free(sc);
   s->status_valid = 1;
   return 0;
 }

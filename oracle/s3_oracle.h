@@ -69,6 +69,7 @@ const uint16_t* s3o_arena(const s3o_state* s);
 int64_t s3o_host_kv(const s3o_state* s, int64_t req, const uint16_t** kv);  /* rows or -1 */
 void s3o_make_inputs(const s3o_state* s, const int32_t* out_len_by_req, uint16_t* q,
                      uint16_t* k, uint16_t* v, uint8_t* eos);
+void s3o_set_threads(int n);   /* attention loop threads (1 = sequential, the default) */
 int  s3o_decode(s3o_state* s, const uint16_t* q, const uint16_t* k, const uint16_t* v,
                 const uint8_t* eos, double* out, uint8_t* status_out);
 int  s3o_evict_compact(s3o_state* s, s3o_report* rep, int32_t* perm, s3o_evicted* ev,

@@ -343,6 +343,7 @@ struct TcArgs {
   int32_t pmax;          // most KV heads one tile may pack (NC / G; 1 = no packing)
   const uint16_t* k_new; // [nl][B][Hkv][D]: appended to the arena by the producer warp
   const uint16_t* v_new;
+  uint32_t* evdone;      // per-evictee staged-row counters (cumulative; the D2H stream waits on them)
   Feed feed;             // host-fed step: per-chunk ready words (s3_decode_step_host)
 };
 
@@ -484,6 +485,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
             h.flags = (r == 0 ? 1 : 0) | (r + TM >= nrows ? 2 : 0);
             h.b = un.b; h.part = un.part; h.li = li; h.g = g; h.iseq = iseq;
             h.mode = un.mode; h.drow = drow0 + r;
+            if (un.mode == UNIT_STAGE) h.dep.ua = un.pad;   // eviction index (dep is only loaded for MOVE)
             h.flags |= (31 - __clz(np)) << 8;
             const int glast = g + np - 1;  // heads g..glast are read up to r + nv rows once this tile lands
             h.prog = (uint32_t)(glast * TC_HEAD_STRIDE + r + nv) |
@@ -661,6 +663,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
           }
           if (stores) pending = st;
           else mb_arrive(&S.kv_empty[st]);
+          if (h.mode == UNIT_STAGE && a.evdone) {
+            // the tile's evictee rows are final in staging once its stores complete (the
+            // ragged rows' generic stores are ordered by the __syncwarp above): count them
+            // for the D2H stream, which copies each evictee as soon as its count is complete
+            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            const uint32_t rows = (uint32_t)(h.nvalid * (PACK ? 1 << hdr_lognp(h) : 1));
+            asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(a.evdone + h.dep.ua), "r"(rows) : "memory");
+          }
         }
       }
       if (lane == 0) {
@@ -937,7 +948,8 @@ cudaError_t launch_attn_tc(const Shape& sh, const uint16_t* q, const uint16_t* k
                            uint16_t* arena, int64_t arena_rows, uint8_t* staging, int64_t staging_bytes, float* out,
                            float* partials, const Unit* units, const Split* splits, const DepDesc* desc,
                            unsigned long long* progress, uint32_t epoch, int32_t* ctrl, int32_t B, int32_t l0,
-                           int32_t nl, int32_t grid_attn, int32_t grid_combine, const Feed& feed, cudaStream_t st) {
+                           int32_t nl, int32_t grid_attn, int32_t grid_combine, const Feed& feed, uint32_t* evdone,
+                           cudaStream_t st) {
   TcMaps maps;
   // staging rows (evicted slots' KV, token-major like the arena); without staging k_prep never fuses an eviction
   const int64_t stage_rows = staging ? staging_bytes / sh.kvpt : 0;
@@ -962,7 +974,7 @@ cudaError_t launch_attn_tc(const Shape& sh, const uint16_t* q, const uint16_t* k
   a.out = out; a.partials = partials; a.units = units; a.ctrl = ctrl;
   a.arena = reinterpret_cast<uint8_t*>(arena); a.staging = staging; a.kvpt = sh.kvpt;
   a.desc = desc; a.progress = progress; a.epoch = epoch;
-  a.k_new = k_new; a.v_new = v_new; a.feed = feed;
+  a.k_new = k_new; a.v_new = v_new; a.feed = feed; a.evdone = evdone;
   static const int pack = [] { const char* e = getenv("S3_TC_PACK"); return e ? atoi(e) : 1; }();
   a.pmax = pack ? (a.G <= 8 ? 8 : 16) / a.G : 1;   // S3_TC_PACK=0: one KV head per tile (A/B)
   const dim3 grid(grid_attn), block(TC_THREADS);

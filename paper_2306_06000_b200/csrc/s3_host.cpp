@@ -68,6 +68,8 @@ struct Item {
   int64_t host_off, host_bytes;
   int32_t host_rows;
   std::shared_ptr<EventBox> ready;   // D2H completion
+  const uint8_t* stage_src = nullptr;  // its rows in the eviction staging buffer, valid during
+  uint64_t evict_seq = 0;              // the s3_evict_compact call that staged them
 };
 
 using Pool = std::map<Key, Item>;
@@ -157,6 +159,8 @@ struct s3_ctx {
   // host-fed steps (s3_decode_step_host): copy stream, per-chunk ready words
   uint32_t* ready = nullptr;
   uint32_t* done = nullptr;                 // per-chunk finished-warp counters (device out + CE D2H)
+  uint32_t* evdone = nullptr;               // per-evictee staged-row counters (fused eviction D2H)
+  std::vector<uint32_t> ev_target;          // their cumulative targets
   uint32_t done_target[kMaxFeedChunks] = {};  // cumulative values the D2H stream waits for
   cudaStream_t hio = nullptr, d2h = nullptr;
   cudaEvent_t ev_hio_start = nullptr, ev_hio_done = nullptr, ev_comb = nullptr, ev_d2h_done = nullptr;
@@ -187,6 +191,7 @@ struct s3_ctx {
   std::shared_ptr<EventBox> stage_d2h[2];
   // state
   bool status_pending = false;
+  uint64_t evict_seq = 0;       // s3_evict_compact calls (staging of the current call is reusable)
   uint32_t epoch = 0;
   int64_t finished_total = 0, evicted_total = 0, tokens_total = 0;
   int64_t launches = 0;     // kernels launched by this context
@@ -242,7 +247,7 @@ Shape make_shape(const s3_config* c) {
 
 struct Carve {
   int64_t slots, units, splits, partials, ctrl, ctrl64, entries, keys, desc, progress, flags, report, verify, ready,
-      done, total;
+      done, evdone, total;
 };
 
 Carve carve(const s3_config* c) {
@@ -270,6 +275,7 @@ Carve carve(const s3_config* c) {
   k.verify = o;   o += align_up(8);
   k.ready = o;    o += align_up(kMaxFeedChunks * 4);
   k.done = o;     o += align_up(kMaxFeedChunks * 4);
+  k.evdone = o;   o += align_up(Bm * 4);
   k.total = o;
   return k;
 }
@@ -369,20 +375,29 @@ s3_status place_items(s3_ctx* ctx, const std::vector<Item>& items, s3_admit_repo
       if (it.evicted) {
         s.gen = it.gen;
         s.len = it.host_rows;
-        CK(cudaStreamWaitEvent(ctx->st, it.ready->ev, 0), "wait D2H event");
-        cudaEvent_t e0 = nullptr, e1 = nullptr;
-        if (ctx->prof.on) { e0 = ctx->prof.get(); e1 = ctx->prof.get(); cudaEventRecord(e0, ctx->st); }
-        CK(cudaMemcpyAsync((uint8_t*)ctx->buf.arena + (int64_t)s.off * ctx->sh.kvpt,
-                           (uint8_t*)ctx->buf.host_store + it.host_off, it.host_bytes,
-                           cudaMemcpyHostToDevice, ctx->st), "reload H2D");
-        if (ctx->prof.on) {
-          cudaEventRecord(e1, ctx->st);
-          ctx->prof.pending.push_back({e0, e1, (double)it.host_bytes, 3});
+        uint8_t* dst = (uint8_t*)ctx->buf.arena + (int64_t)s.off * ctx->sh.kvpt;
+        if (it.stage_src && it.evict_seq == ctx->evict_seq) {
+          // re-admitted in the step that evicted it (R10): its rows are still in the
+          // staging buffer (stream-ordered after the attention pass that staged them),
+          // so the reload is an HBM copy and PCIe stays off the critical path; the host
+          // copy is made all the same (the eviction D2H is already queued)
+          CK(cudaMemcpyAsync(dst, it.stage_src, it.host_bytes, cudaMemcpyDeviceToDevice, ctx->st), "reload D2D");
+          r.stage_reload_bytes += it.host_bytes;
+        } else {
+          CK(cudaStreamWaitEvent(ctx->st, it.ready->ev, 0), "wait D2H event");
+          cudaEvent_t e0 = nullptr, e1 = nullptr;
+          if (ctx->prof.on) { e0 = ctx->prof.get(); e1 = ctx->prof.get(); cudaEventRecord(e0, ctx->st); }
+          CK(cudaMemcpyAsync(dst, (uint8_t*)ctx->buf.host_store + it.host_off, it.host_bytes,
+                             cudaMemcpyHostToDevice, ctx->st), "reload H2D");
+          if (ctx->prof.on) {
+            cudaEventRecord(e1, ctx->st);
+            ctx->prof.pending.push_back({e0, e1, (double)it.host_bytes, 3});
+          }
+          r.h2d_bytes += it.host_bytes;
         }
         ctx->deferred_free.push_back({it.host_off, it.host_bytes, nullptr});
         ctx->n_evicted_waiting--;
         r.n_reloaded++;
-        r.h2d_bytes += it.host_bytes;
       } else {
         s.gen = 0;
         s.len = it.prompt;
@@ -432,6 +447,12 @@ int64_t stage_bytes(const s3_ctx* c) {
 uint8_t* stage_ptr(const s3_ctx* c, int half) {
   return (uint8_t*)c->buf.staging + (c->stage_dbl ? (int64_t)half * stage_bytes(c) : 0);
 }
+
+// Per-evictee staged-row counters: the fused attention kernels count each
+// evictee's rows as they become final in staging, and the eviction D2H of
+// that evictee waits for its count (cuStreamWaitValue32) instead of for the
+// end of the attention pass.  Needs the stream memory operations.
+uint32_t* ev_counters(const s3_ctx* c) { return wait_value32() ? c->evdone : nullptr; }
 
 // R27 at admission: under the on-demand policy a step whose pool was empty left
 // its holes in place; when requests wait again (a later s3_submit), shift the
@@ -570,6 +591,8 @@ s3_status s3_kv_init(const s3_config* cfg, const s3_buffers* b, s3_ctx** out) {
   ctx->verify_count = reinterpret_cast<unsigned long long*>(ws + k.verify);
   ctx->ready = reinterpret_cast<uint32_t*>(ws + k.ready);
   ctx->done = reinterpret_cast<uint32_t*>(ws + k.done);
+  ctx->evdone = reinterpret_cast<uint32_t*>(ws + k.evdone);
+  ctx->ev_target.assign((size_t)cfg->max_running, 0u);
   if (cudaMemsetAsync(ws + k.ready, 0, (size_t)(k.total - k.ready), ctx->st) != cudaSuccess) return bail("memset");
   if (cudaMemsetAsync(ws + k.ctrl, 0, CTRL_WORDS * 4, ctx->st) != cudaSuccess) return bail("memset");
   if (cudaMemsetAsync(ws + k.flags, 0, (size_t)(k.report - k.flags), ctx->st) != cudaSuccess) return bail("memset");
@@ -704,13 +727,13 @@ s3_status s3_decode_step(s3_ctx* ctx, int32_t l0, int32_t nl, const void* q, con
                         (uint16_t*)ctx->buf.arena, ctx->cfg.arena_rows,
                         ctx->buf.staging ? stage_ptr(ctx, ctx->stage_cur) : nullptr, stage_bytes(ctx), out, ctx->partials,
                         ctx->units, ctx->splits, ctx->desc, ctx->progress, ctx->attn_epoch, ctx->ctrl, B, l0, nl,
-                        ctx->grid_attn, ctx->grid_combine, ctx->feed, ctx->st), "k_attn_tc");
+                        ctx->grid_attn, ctx->grid_combine, ctx->feed, ev_counters(ctx), ctx->st), "k_attn_tc");
     else
       CK(launch_attn(ctx->sh, (const uint16_t*)q, (const uint16_t*)k_new, (const uint16_t*)v_new,
                      (uint16_t*)ctx->buf.arena, ctx->buf.staging ? stage_ptr(ctx, ctx->stage_cur) : nullptr, out,
                      ctx->partials, ctx->units,
                      ctx->splits, ctx->desc, ctx->progress, ctx->attn_epoch, ctx->ctrl, B, l0, nl, ctx->grid_attn,
-                     ctx->grid_combine, ctx->cfg.attn_variant, ctx->feed, ctx->st), "k_attn");
+                     ctx->grid_combine, ctx->cfg.attn_variant, ctx->feed, ev_counters(ctx), ctx->st), "k_attn");
     ctx->launches += 2;   // attention, combine
     if (ctx->prof.on) {
       cudaEventRecord(e1, ctx->st);
@@ -849,6 +872,7 @@ s3_status s3_evict_compact(s3_ctx* ctx, s3_evict_report* rep, int32_t* perm, s3_
   if (!rep) return fail(ctx, S3_E_INVAL, "evict_compact: null report");
   if (!ctx->status_pending) return fail(ctx, S3_E_STATE, "evict_compact: no completed decode step");
   const int32_t B = (int32_t)ctx->slots_h.size();
+  ctx->evict_seq++;
   s3_evict_report r{};
   r.n_before = B;
   r.first_hole = B;
@@ -950,19 +974,40 @@ s3_status s3_evict_compact(s3_ctx* ctx, s3_evict_report* rep, int32_t* perm, s3_
     }
   }
   if (staged) {
-    cudaEvent_t k4;
-    CK(cudaEventCreateWithFlags(&k4, cudaEventDisableTiming), "event");
-    CK(cudaEventRecord(k4, ctx->st), "event");
-    CK(cudaStreamWaitEvent(ctx->side, k4, 0), "side wait");
-    cudaEventDestroy(k4);
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (ctx->prof.on) { e0 = ctx->prof.get(); e1 = ctx->prof.get(); cudaEventRecord(e0, ctx->side); }
-    for (int32_t i = 0; i < h->n_evicted; ++i)
+    // fused step: each evictee's copy starts as soon as the attention kernel has
+    // staged all its rows (per-evictee counters), overlapping the rest of the pass;
+    // otherwise (k_move staging) after the staging pass
+    StreamValue32Fn wt = wait_value32();
+    const bool counted = fused && ev_counters(ctx) != nullptr;
+    if (!counted) {
+      cudaEvent_t k4;
+      CK(cudaEventCreateWithFlags(&k4, cudaEventDisableTiming), "event");
+      CK(cudaEventRecord(k4, ctx->st), "event");
+      CK(cudaStreamWaitEvent(ctx->side, k4, 0), "side wait");
+      cudaEventDestroy(k4);
+    } else {
+      // the staging half must not be read before this step's k_prep wrote its plan
+      CK(cudaStreamWaitEvent(ctx->side, ctx->ev_report, 0), "side wait");
+    }
+    const int nwc = attn_block_threads(sh) / 32;    // CUDA-core kernel: consumer warps that append the new row
+    for (int32_t i = 0; i < h->n_evicted; ++i) {
+      if (counted) {
+        // rows each kernel counts for this evictee over the step's L layers
+        const uint32_t target = ctx->cfg.attn_variant == 2
+                                    ? (uint32_t)((int64_t)sh.L * sh.Hkv * dev[i].len)
+                                    : (uint32_t)((int64_t)sh.L * ((dev[i].len - 1) + nwc));
+        ctx->ev_target[i] += target;
+        if (wt(ctx->side, (unsigned long long)(uintptr_t)(ctx->evdone + i), ctx->ev_target[i], kWaitGeq) != 0)
+          return fail(ctx, S3_E_CUDA, "evict_compact: stream wait");
+      }
+      cudaEvent_t e0 = nullptr, e1 = nullptr;
+      if (ctx->prof.on) { e0 = ctx->prof.get(); e1 = ctx->prof.get(); cudaEventRecord(e0, ctx->side); }
       CK(cudaMemcpyAsync((uint8_t*)ctx->buf.host_store + hoff[i], stage + dev[i].stage_off,
                          (size_t)dev[i].len * sh.kvpt, cudaMemcpyDeviceToHost, ctx->side), "evict D2H");
-    if (ctx->prof.on) {
-      cudaEventRecord(e1, ctx->side);
-      ctx->prof.pending.push_back({e0, e1, (double)h->d2h_bytes, 2});
+      if (ctx->prof.on) {
+        cudaEventRecord(e1, ctx->side);
+        ctx->prof.pending.push_back({e0, e1, (double)dev[i].len * sh.kvpt, 2});
+      }
     }
     CK(cudaEventRecord(d2h_done->ev, ctx->side), "event");
     ctx->stage_d2h[ctx->stage_cur] = d2h_done;
@@ -980,6 +1025,7 @@ s3_status s3_evict_compact(s3_ctx* ctx, s3_evict_report* rep, int32_t* perm, s3_
     it.host_bytes = (int64_t)e.len * sh.kvpt;
     it.host_rows = e.len;
     it.ready = d2h_done;
+    if (staged) { it.stage_src = stage + e.stage_off; it.evict_seq = ctx->evict_seq; }
     pcie += 2LL * e.cap * sh.kvpt;
     (ctx->cfg.world > 1 ? ctx->home : ctx->pool).emplace(Key{it.cap, it.req}, it);
     ctx->n_evicted_waiting++;

@@ -26,7 +26,7 @@ struct Unit {
   int32_t b, r0, r1, part;
   int32_t off, len, has_new, mode;
   int64_t dst;
-  int32_t stage_base, pad;
+  int32_t stage_base, pad;   // pad: eviction index of a STAGE unit (its staged-row counter)
 };
 static_assert(sizeof(Unit) == 48, "Unit must be 48 B");
 
@@ -124,7 +124,7 @@ cudaError_t launch_attn(const Shape& sh, const uint16_t* q, const uint16_t* k_ne
                         uint16_t* arena, uint8_t* staging, float* out, float* partials, const Unit* units,
                         const Split* splits, const DepDesc* desc, unsigned long long* progress, uint32_t epoch,
                         int32_t* ctrl, int32_t B, int32_t l0, int32_t nl, int32_t grid_attn, int32_t grid_combine,
-                        int32_t variant, const Feed& feed, cudaStream_t st);
+                        int32_t variant, const Feed& feed, uint32_t* evdone, cudaStream_t st);
 cudaError_t launch_keep_scan(const Shape& sh, const DSlot* cur, DSlot* next, int32_t B, int64_t S,
                              void* report, MoveEntry* entries, int32_t* key_chunk0, int32_t* key_src,
                              int64_t* ctrl64, int32_t compact_policy, int32_t pool_nonempty, cudaStream_t st);
@@ -152,7 +152,8 @@ cudaError_t launch_attn_tc(const Shape& sh, const uint16_t* q, const uint16_t* k
                            uint16_t* arena, int64_t arena_rows, uint8_t* staging, int64_t staging_bytes, float* out,
                            float* partials, const Unit* units, const Split* splits, const DepDesc* desc,
                            unsigned long long* progress, uint32_t epoch, int32_t* ctrl, int32_t B, int32_t l0,
-                           int32_t nl, int32_t grid_attn, int32_t grid_combine, const Feed& feed, cudaStream_t st);
+                           int32_t nl, int32_t grid_attn, int32_t grid_combine, const Feed& feed, uint32_t* evdone,
+                           cudaStream_t st);
 cudaError_t launch_combine(const Shape& sh, const Split* splits, float* partials, float* out, int32_t* ctrl,
                            int32_t B, int32_t nl, int32_t grid, cudaStream_t st);
 

@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(1024) k_prep(PrepArgs a) {
       un.mode = mode;
       un.dst = dst;
       un.stage_base = (int)stg;
-      un.pad = 0;
+      un.pad = mode == UNIT_STAGE ? (int)ev_i : 0;   // eviction index: per-evictee completion counter
       a.units[u + i] = un;
       const int rows = un.r1 - un.r0;
       stg += rows > 0 ? (rows + AT_RPS - 1) / AT_RPS : 1;
@@ -442,6 +442,7 @@ struct AttnArgs {
   int32_t B, l0, nl;
   float qscale;
   Feed feed;             // host-fed step: per-chunk ready words (s3_decode_step_host)
+  uint32_t* evdone;      // per-evictee staged-row counters (cumulative; the D2H stream waits on them)
 };
 
 template <int D, int G>
@@ -974,7 +975,8 @@ struct StageHdr {
   DepDesc dep;                 // filled by the TMA engine (16 B, same transaction as the rows)
   int32_t item, r0, n, flags;  // flags: 1 = first stage of the item, 2 = last, 4 = unit has the new row
   int32_t b, part, off, len;   // the item's unit (so consumers never load it from global)
-  int32_t mode, unit_r0, dep_ok, pad;   // dep_ok: storer's "destination free" stamp (stage seq + 1)
+  int32_t mode, unit_r0, dep_ok, ev;    // dep_ok: storer's "destination free" stamp (stage seq + 1);
+                                        // ev: eviction index of a STAGE unit
   int64_t dst, pad2;
 };
 static_assert(sizeof(StageHdr) % 16 == 0, "StageHdr must keep 16-B alignment");
@@ -1071,7 +1073,7 @@ __global__ void __launch_bounds__(576, 1) k_attn_tma(AttnArgs a, int32_t ns) {
           h.item = item; h.r0 = r; h.n = n;
           h.flags = (first ? 1 : 0) | (r + n >= un.r1 ? 2 : 0) | (un.has_new ? 4 : 0);
           h.b = un.b; h.part = un.part; h.off = un.off; h.len = un.len;
-          h.mode = un.mode; h.unit_r0 = un.r0; h.dst = un.dst;
+          h.mode = un.mode; h.unit_r0 = un.r0; h.dst = un.dst; h.ev = un.pad;
           const bool mv = un.mode == UNIT_MOVE;
           const uint32_t tx = (uint32_t)(n * rowB + (first ? 2 * HD : 0) + (mv ? sizeof(DepDesc) : 0));
           uint8_t* sb = smem + st * stageB;
@@ -1096,6 +1098,7 @@ __global__ void __launch_bounds__(576, 1) k_attn_tma(AttnArgs a, int32_t ns) {
     // ------------------------------- storer -------------------------------
     if (lane == 0 && fused) {
       int pending = -1;                 // stage whose stores may still read shared memory
+      uint32_t ev_rows = 0;             // rows of the current STAGE item written to staging so far
       int64_t seen_item = -1;           // progress cache: last observed source item / value
       unsigned long long seen_val = 0;
       for (int k = 0;; ++k) {
@@ -1154,6 +1157,18 @@ __global__ void __launch_bounds__(576, 1) k_attn_tma(AttnArgs a, int32_t ns) {
         }
         if (stores) pending = st;
         else mbar_arrive(&empty[st]);
+        if (h.mode == UNIT_STAGE && a.evdone) {
+          // an evictee's rows are final in staging once the item's stores have
+          // completed (not just read shared memory): count them for the D2H
+          // stream, which copies each evictee as soon as its count is complete
+          ev_rows += (uint32_t)h.n;
+          if (h.flags & 2) {
+            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(a.evdone + h.ev), "r"(ev_rows) : "memory");
+            ev_rows = 0;
+          }
+        }
       }
       asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       if (pending >= 0) mbar_arrive(&empty[pending]);
@@ -1231,6 +1246,10 @@ __global__ void __launch_bounds__(576, 1) k_attn_tma(AttnArgs a, int32_t ns) {
         if (kv_writer && kdst) {
           st_v4(kdst, kr);
           st_v4(kdst + KD, vr);
+        }
+        if (h.mode == UNIT_STAGE && a.evdone) {   // this warp's part of the evictee's new row is stored
+          __syncwarp();
+          if (lane == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.evdone + h.ev) : "memory");
         }
         uint4 k1[1] = {kr}, v1[1] = {vr};
         attn_rows<D, 1>(k1, v1, 1, qf, m, ssum, acc);
@@ -1401,9 +1420,10 @@ cudaError_t launch_attn(const Shape& sh, const uint16_t* q, const uint16_t* k_ne
                         uint16_t* arena, uint8_t* staging, float* out, float* partials, const Unit* units,
                         const Split* splits, const DepDesc* desc, unsigned long long* progress, uint32_t epoch,
                         int32_t* ctrl, int32_t B, int32_t l0, int32_t nl, int32_t grid_attn, int32_t grid_combine,
-                        int32_t variant, const Feed& feed, cudaStream_t st) {
+                        int32_t variant, const Feed& feed, uint32_t* evdone, cudaStream_t st) {
   AttnArgs a;
   a.feed = feed;
+  a.evdone = evdone;
   a.sh = sh; a.q = q; a.k_new = k_new; a.v_new = v_new; a.arena = arena; a.staging = staging; a.out = out;
   a.partials = partials; a.units = units; a.desc = desc; a.progress = progress; a.epoch = epoch;
   a.ctrl = ctrl; a.B = B; a.l0 = l0; a.nl = nl;

@@ -33,6 +33,7 @@ class StepStats:
     paper_hbm_bytes: int
     reload_bytes: int
     fill_bytes: int
+    stage_reload_bytes: int = 0
 
 
 class S3Engine:
@@ -82,9 +83,14 @@ class S3Engine:
 
     # ---- lifecycle -----------------------------------------------------
     def close(self):
+        """Destroy the context and drop every caller-owned buffer (the device
+        memory returns to torch's allocator once no other reference holds it)."""
         if getattr(self, "ctx", None):
             abi.s3_kv_destroy(self.ctx)
             self.ctx = None
+        for name in ("arena", "workspace", "staging", "host_store", "q", "k_new", "v_new", "out", "eos", "out_len"):
+            if hasattr(self, name):
+                setattr(self, name, None)
 
     def __del__(self):
         try:
@@ -188,16 +194,16 @@ class S3Engine:
         rep, perm, ev, fin = self.evict_compact()
         if self.world == 1:
             arep, _ = self.admit()
-            reload_b, fill_b, n_adm = arep.h2d_bytes, arep.fill_bytes, arep.n_admitted
+            reps = [arep]
         else:
             hrep, _ = self.admit_home()
             allrows = exchange(self.counters_local())
             srep, _ = self.admit_shared(allrows)
-            reload_b = hrep.h2d_bytes + srep.h2d_bytes
-            fill_b = hrep.fill_bytes + srep.fill_bytes
-            n_adm = hrep.n_admitted + srep.n_admitted
-        return StepStats(B, B, rep.n_finished, rep.n_evicted, n_adm, rep.d2h_bytes, rep.moved_bytes,
-                         rep.paper_pcie_bytes, rep.paper_hbm_bytes, reload_b, fill_b)
+            reps = [hrep, srep]
+        return StepStats(B, B, rep.n_finished, rep.n_evicted, sum(r.n_admitted for r in reps), rep.d2h_bytes,
+                         rep.moved_bytes + sum(r.moved_bytes for r in reps), rep.paper_pcie_bytes,
+                         rep.paper_hbm_bytes, sum(r.h2d_bytes for r in reps), sum(r.fill_bytes for r in reps),
+                         sum(r.stage_reload_bytes for r in reps))
 
     def initial_admit(self, exchange=None):
         if self.world == 1:

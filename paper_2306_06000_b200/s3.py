@@ -64,7 +64,7 @@ class s3_evict_report(C.Structure):
 class s3_admit_report(C.Structure):
     _fields_ = [("n_admitted", C.c_int32), ("n_fresh", C.c_int32), ("n_reloaded", C.c_int32),
                 ("n_batch", C.c_int32), ("tail_rows", C.c_int64), ("fill_bytes", C.c_int64),
-                ("h2d_bytes", C.c_int64), ("moved_bytes", C.c_int64)]
+                ("h2d_bytes", C.c_int64), ("moved_bytes", C.c_int64), ("stage_reload_bytes", C.c_int64)]
 
 
 class s3_slot(C.Structure):
