@@ -197,13 +197,21 @@ SLICE_SEQ, SLICE_STEPS = 256, 8
 
 
 def slice_trace(policy, p, seed):
-    """The cpu_baseline slice: the first 256 requests of the
-    8192-request GPT-J trace, in an arena that admits all of them at once."""
+    """The cpu_baseline slice: 256 consecutive requests of the
+    8192-request GPT-J trace -- the first aligned window in which at least two
+    requests overrun within the slice's 8 steps (alloc <= 8 < O), so that
+    eviction and compaction run -- in an arena that admits all of them."""
     import numpy as np
 
     import s3synth
     t = s3synth.make_trace(REQ_PER_GPU, seed=seed, policy=policy, p=p, max_seq_len=GPTJ["max_len"])
-    idx = np.arange(SLICE_SEQ)
+    early = (t.alloc <= SLICE_STEPS) & (t.alloc < t.out)
+    start = 0
+    for s0 in range(0, REQ_PER_GPU - SLICE_SEQ + 1, SLICE_SEQ):
+        if early[s0:s0 + SLICE_SEQ].sum() >= 2:
+            start = s0
+            break
+    idx = np.arange(start, start + SLICE_SEQ)
     return t, idx, int(t.cap[idx].sum())
 
 
@@ -230,7 +238,7 @@ def oracle_slice(policy, p, seed, threads=1, steps=SLICE_STEPS, budget_s=None):
         done += 1
         evicted += rep.n_evicted
     oracle.set_threads(1)
-    desc = (f"GPT-J-shaped slice: first {SLICE_SEQ} requests of the 8192-request {policy}"
+    desc = (f"GPT-J-shaped slice: requests {int(idx[0])}..{int(idx[-1])} of the 8192-request {policy}"
             f"{'(' + str(p) + ')' if p else ''} trace (seed {seed}), {done} whole steps from admission "
             f"(inputs, decode, evict+compact, admit), {tokens} tokens, {evicted} evictions; plain C, fp64 "
             f"attention, {threads} thread(s)")

@@ -57,7 +57,7 @@ def _attention_vs_probe(probe, reserve_sms):
     # warm-up: module load and attribute setting of the probe happen on its first launch
     assert probe.probe_launch(C.c_void_p(side.cuda_stream), 100 * 1024, 1000, C.c_void_p(ts.data_ptr())) == 0
     torch.cuda.synchronize()
-    for _ in range(3):
+    for _ in range(4):                                   # the first step also warms launch configurations
         eng.synth_inputs()
         torch.cuda.synchronize()
         ev[0].record()
@@ -74,7 +74,7 @@ def _attention_vs_probe(probe, reserve_sms):
         eng.evict_compact()
         eng.admit()
     eng.close()
-    return res
+    return res[1:]
 
 
 def test_reserved_sms_let_a_side_stream_kernel_run_during_attention(probe):

@@ -256,7 +256,7 @@ def test_bench_configuration_sampled():
     from paper_2306_06000_b200.engine import S3Engine
     L, H, D, M = 28, 16, 256, 2048
     kvpt = 4 * L * H * D
-    t = s3synth.make_trace(8192, seed=1, policy="short", p=0.1, max_seq_len=M)
+    t = s3synth.make_trace(8192, seed=1, policy="short", p=0.3, max_seq_len=M)
     max_running = 8192
     import gc
     gc.collect()
@@ -268,7 +268,7 @@ def test_bench_configuration_sampled():
     eng.admit()
     rng = np.random.default_rng(0)
     evictions = 0
-    for step in range(40):
+    for step in range(60):
         slots = eng.batch_view()
         B = len(slots)
         offs = [s[5] for s in slots]
@@ -293,6 +293,7 @@ def test_bench_configuration_sampled():
         if step % 10 == 9:
             assert eng.verify_resident() == 0, step
     print("evictions", evictions)
+    assert evictions > 0            # the full-size eviction path (staging, D2H, doubling) ran
     eng.close()
 
 
