@@ -285,6 +285,32 @@ s3_status s3_synth_inputs(s3_ctx* ctx, int32_t l0, int32_t nl, const int32_t* ou
  * generator (invariant P2).  Synchronises.                                  */
 s3_status s3_verify_resident(s3_ctx* ctx, int64_t* bad_rows);
 
+/* ---- batch-dependent decode cost ------------------------
+ * The projections around attention share their weights across the batch, so
+ * their cost per token falls as the batch grows -- the effect behind the
+ * paper's ORCA vs S^3 vs Oracle throughput gap ("the
+ * feed-forward layers ... batched", 247-249).  s3_gemm runs one such
+ * projection on the tcgen05 tensor cores:
+ *     D[M][N] = epi( A[M][K] . W[N][K]^T ),  bf16 operands, fp32 accumulate,
+ *     epi 0: D = acc;  1: D = gelu_tanh(acc);  2: D = C + acc   (bf16 out).
+ *   a      device bf16 [M][K] row-major (the batch's activations, M = B);
+ *   w      device bf16 [N][K] row-major (the weight, nn.Linear layout);
+ *   d[i]   device bf16 [M][seg_cols]: column segment i = columns
+ *          [i seg_cols, (i+1) seg_cols) of D (N / seg_cols <= 3 segments, e.g.
+ *          the QKV projection straight into q, k_new, v_new); unused = NULL;
+ *   c      epi 2: device bf16 [M][N] (may be d[0], in place), else NULL.
+ * K % 64 == 0, N % 128 == 0, seg_cols % 128 == 0; 16-B aligned pointers.
+ * Stream-ordered on `stream` (a cudaStream_t); no context needed.
+ * S3_E_INVAL on a bad shape or pointer, S3_E_CUDA on a launch error.      */
+typedef struct {
+  const void* a; const void* w; void* d[3]; const void* c;
+  int32_t M, N, K, seg_cols, epi;
+} s3_gemm_args;
+s3_status s3_gemm(void* stream, const s3_gemm_args* g);
+/* dst (bf16, device) = round-to-nearest(src (fp32, device)), n elements
+ * (n % 4 == 0, 16-B aligned): the attention output as the next GEMM's A.  */
+s3_status s3_cast_bf16(void* stream, const float* src, void* dst, int64_t n);
+
 #ifdef __cplusplus
 }
 #endif

@@ -89,6 +89,7 @@ def lib():
             "s3o_counters": (None, [P, P]),
             "s3o_moved_at_admit": (i64, [P]),
             "s3o_attend_generated": (None, [P, i64, i32, i32, P]),
+            "s3o_attend_rows": (None, [P, P, P, i64, i32, i32, i32, i32, P]),
         }
         for name, (res, args) in sig.items():
             f = getattr(_lib, name)
@@ -166,6 +167,19 @@ def attend_generated(L, H, D, max_len, seed, req, pos, l, Hkv=0) -> np.ndarray:
 def set_threads(n: int) -> None:
     """Threads of the oracle's attention loop (1 = the plain sequential oracle)."""
     lib().s3o_set_threads(int(n))
+
+
+def attend_rows(q, K, V):
+    """fp64 attention of one layer's query heads q [H][D] (bf16 bits) over the
+    rows K, V [n][Hkv][D] (bf16 bits); returns [H][D]."""
+    q = np.ascontiguousarray(q, dtype=np.uint16)
+    K = np.ascontiguousarray(K, dtype=np.uint16)
+    V = np.ascontiguousarray(V, dtype=np.uint16)
+    n, Hkv, D = K.shape
+    H = q.shape[0]
+    out = np.zeros(H * D, dtype=np.float64)
+    lib().s3o_attend_rows(_p(q), _p(K), _p(V), Hkv * D, n, H, Hkv, D, _p(out))
+    return out.reshape(H, D)
 
 
 def bf16_bits_to_f64(bits: np.ndarray) -> np.ndarray:

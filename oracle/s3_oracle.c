@@ -636,6 +636,16 @@ void s3o_counters(const s3o_state* s, int64_t row[8]) {
   row[7] = s->tokens_total;
 }
 
+/* softmax(q K^T / sqrt(D)) V over n given rows, for inputs
+ * that do not come from the generator (the GEMM-fed proxy model's q and
+ * appended rows): row j's K at K0 + j*stride, V at V0 + j*stride.         */
+void s3o_attend_rows(const uint16_t* q_hd, const uint16_t* K0, const uint16_t* V0, int64_t stride, int32_t n,
+                     int32_t H, int32_t Hkv, int32_t D, double* out_hd) {
+  double* sc = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+  attend(q_hd, K0, V0, stride, n, H, Hkv, D, sc, out_hd);
+  free(sc);
+}
+
 /* Attention of request `req` at position `pos` of layer l when its rows are
  * the generator's (invariant P2): K_j = G(req,l,0,j), V_j = G(req,l,1,j) for
  * j = 0..pos, q = Q(req,l,pos).  Lets tests check sampled outputs of a

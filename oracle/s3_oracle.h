@@ -80,6 +80,8 @@ int32_t s3o_admit_shared(s3o_state* s, int32_t world, int32_t rank, const int64_
                          const int64_t* slots_left_by_rank, int64_t* admitted);
 void s3o_counters(const s3o_state* s, int64_t row[8]);
 int64_t s3o_moved_at_admit(const s3o_state* s);   /* R27 admission-time shifts, bytes */
+void s3o_attend_rows(const uint16_t* q_hd, const uint16_t* K0, const uint16_t* V0, int64_t stride, int32_t n,
+                     int32_t H, int32_t Hkv, int32_t D, double* out_hd);
 void s3o_attend_generated(const s3o_config* c, int64_t req, int32_t pos, int32_t l, double* out_hd);
 
 #ifdef __cplusplus

@@ -11,7 +11,7 @@ LIBDIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIBDIR, "libs3.so")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 SOURCES = [os.path.join(CSRC, "s3_kernels.cu"), os.path.join(CSRC, "s3_attn_tc.cu"),
-           os.path.join(CSRC, "s3_host.cpp")]
+           os.path.join(CSRC, "s3_gemm.cu"), os.path.join(CSRC, "s3_host.cpp")]
 DEPS = SOURCES + [os.path.join(CSRC, "s3_internal.h"), os.path.join(INCLUDE, "s3.h")]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -1,0 +1,344 @@
+// s3_gemm.cu -- bf16 GEMM on the 5th-gen tensor cores (tcgen05 + TMEM + TMA)
+// for the batch-dependent part of a decode step: the QKV,
+// output and feed-forward projections of a GPT-J-shaped layer at M = B
+// running sequences.  Their weights are shared by the whole batch, which is
+// why a larger batch -- what S^3's length prediction buys (PAPER.md:168,
+// 247-249) -- raises throughput; attention is the part that does not batch.
+//
+//   D[M][N] = epi( A[M][K] . W[N][K]^T )     A, W bf16 (K-major), fp32 accumulate
+//   epi: STORE (bf16), GELU (tanh form, then bf16), ADD (D = C + acc, bf16; C may alias D)
+//   D may be split into column segments of seg_cols columns (QKV -> q, k, v buffers).
+//
+// One persistent CTA per SM, 6 warps:
+//   warp 0  TMA producer: per K block one 2-D box of A [128 x 64] and one of W
+//           [BN x 64] (128B swizzle) into a 4-stage ring (mbarrier full / empty);
+//   warp 1  MMA issuer: one thread issues tcgen05.mma.cta_group::1.kind::f16,
+//           M 128, N BN, K 16 (4 per K block), into one of two TMEM
+//           accumulators (2 x BN fp32 columns), commits the stage back to the
+//           producer and the finished accumulator to the epilogue;
+//   warps 2-5 epilogue: tcgen05.ld 32 columns at a time (warp w reads TMEM
+//           lanes 32 (w % 4) ..), applies the epilogue, stores bf16 rows; the
+//           accumulator is released as soon as it has been read, so the next
+//           tile's MMAs overlap this tile's stores.
+// Tiles are walked n-major (the M tiles of one W column block run on
+// neighbouring CTAs at the same time, so W streams from HBM once and the
+// small A operand stays in L2).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+
+#include "s3_internal.h"
+
+namespace s3 {
+namespace {
+
+constexpr int GM = 128;          // tile rows (MMA M)
+constexpr int GK = 64;           // K block: one 128-byte swizzle atom of bf16
+constexpr int GSTAGES = 4;
+constexpr int G_THREADS = 6 * 32;
+
+__device__ __forceinline__ uint32_t gsu32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void g_mb_init(uint64_t* b, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(gsu32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void g_mb_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(gsu32(b)) : "memory");
+}
+__device__ __forceinline__ void g_mb_expect(uint64_t* b, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(gsu32(b)), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void g_mb_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\nW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra W_%=;\n}\n" ::"r"(
+          gsu32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void g_tma2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+          "r"(gsu32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(gsu32(bar))
+      : "memory");
+}
+// K-major operand in 128B-swizzled smem: rows of 128 B, 8-row groups 1024 B apart
+__device__ __forceinline__ uint64_t g_desc(const void* p) {
+  return (uint64_t)((gsu32(p) >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+// instruction descriptor: bf16 x bf16 -> f32, both K-major, M 128, N n
+__host__ __device__ constexpr uint32_t g_idesc(int n) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(GM >> 4) << 24);
+}
+__device__ __forceinline__ void g_mma(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(id), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void g_commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.b64 [%0];" ::"l"((uint64_t)gsu32(b)) : "memory");
+}
+__device__ __forceinline__ void g_tmem_ld32(uint32_t addr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(addr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ float gelu_tanh(float x) {
+  // 0.5 x (1 + tanh( sqrt(2/pi) (x + 0.044715 x^3) ))  (GPT-J's "gelu_new")
+  const float u = 0.7978845608028654f * fmaf(0.044715f * x, x * x, x);
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(u));
+  return 0.5f * x * (1.f + t);
+}
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+__device__ __forceinline__ float bf16_lo(uint32_t u) { return __uint_as_float(u << 16); }
+__device__ __forceinline__ float bf16_hi(uint32_t u) { return __uint_as_float(u & 0xffff0000u); }
+
+struct GemmMaps {
+  CUtensorMap a, w;
+};
+struct GemmArgs {
+  int32_t M, N, K, epi, seg_cols, m_tiles, n_tiles;
+  uint16_t* d[3];
+  const uint16_t* c;
+};
+
+template <int BN>
+__global__ void __launch_bounds__(G_THREADS, 1) k_gemm(const __grid_constant__ GemmMaps maps, GemmArgs a) {
+  constexpr int A_BYTES = GM * GK * 2, W_BYTES = BN * GK * 2, STAGE = A_BYTES + W_BYTES;
+  constexpr int TMEM_COLS = 2 * BN;
+  extern __shared__ __align__(1024) uint8_t gsmem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(gsmem_raw) + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + GSTAGES * STAGE);
+  uint64_t* empty = full + GSTAGES;
+  uint64_t* tfull = empty + GSTAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_base = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < GSTAGES; ++i) { g_mb_init(&full[i], 1); g_mb_init(&empty[i], 1); }
+    for (int i = 0; i < 2; ++i) { g_mb_init(&tfull[i], 1); g_mb_init(&tempty[i], 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.a) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.w) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(gsu32(tmem_base)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_base;
+  const int tiles = a.m_tiles * a.n_tiles;
+  const int kblocks = a.K / GK;
+
+  if (warp == 0) {
+    // ------------------------------ TMA producer ------------------------------
+    if (lane == 0) {
+      int s = 0;
+      uint32_t ph = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const int m0 = (t % a.m_tiles) * GM, n0 = (t / a.m_tiles) * BN;
+        for (int kb = 0; kb < kblocks; ++kb) {
+          g_mb_wait(&empty[s], ph ^ 1u);
+          uint8_t* sa = smem + s * STAGE;
+          g_mb_expect(&full[s], (uint32_t)STAGE);
+          g_tma2d(sa, &maps.a, kb * GK, m0, &full[s]);
+          g_tma2d(sa + A_BYTES, &maps.w, kb * GK, n0, &full[s]);
+          if (++s == GSTAGES) { s = 0; ph ^= 1u; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------- MMA issuer -------------------------------
+    if (lane == 0) {
+      constexpr uint32_t id = g_idesc(BN);
+      int s = 0;
+      uint32_t ph = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+        const int acc = it & 1;
+        g_mb_wait(&tempty[acc], ((uint32_t)(it >> 1) & 1u) ^ 1u);   // the epilogue drained this accumulator
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t d = tmem + (uint32_t)(acc * BN);
+        for (int kb = 0; kb < kblocks; ++kb) {
+          g_mb_wait(&full[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint8_t* sa = smem + s * STAGE;
+          const uint64_t da = g_desc(sa), dw = g_desc(sa + A_BYTES);
+#pragma unroll
+          for (int k = 0; k < GK / 16; ++k)          // +32 B per K = 16 inside the swizzle atom
+            g_mma(d, da + (uint64_t)(k * 2), dw + (uint64_t)(k * 2), id, (kb | k) != 0);
+          g_commit(&empty[s]);                         // the stage is free once these MMAs have read it
+          if (++s == GSTAGES) { s = 0; ph ^= 1u; }
+        }
+        g_commit(&tfull[acc]);                         // accumulator complete
+      }
+    }
+  } else {
+    // -------------------------------- epilogue --------------------------------
+    const int quarter = warp & 3;                      // TMEM lanes 32*quarter .. +31
+    const int row = quarter * 32 + lane;
+    int it = 0;
+    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+      const int acc = it & 1;
+      const int m0 = (t % a.m_tiles) * GM, n0 = (t / a.m_tiles) * BN;
+      g_mb_wait(&tfull[acc], (uint32_t)(it >> 1) & 1u);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int m = m0 + row;
+      const int seg = n0 / a.seg_cols, col0 = n0 - seg * a.seg_cols;
+      uint16_t* drow = a.d[seg] + (int64_t)m * a.seg_cols + col0;
+      const uint16_t* crow = a.c ? a.c + (int64_t)m * a.N + n0 : nullptr;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        g_tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + c), r);
+        if (m < a.M) {
+          float v[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+          if (a.epi == 1) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = gelu_tanh(v[i]);
+          } else if (a.epi == 2) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint4 x = *reinterpret_cast<const uint4*>(crow + c + q * 8);
+              v[q * 8 + 0] += bf16_lo(x.x); v[q * 8 + 1] += bf16_hi(x.x);
+              v[q * 8 + 2] += bf16_lo(x.y); v[q * 8 + 3] += bf16_hi(x.y);
+              v[q * 8 + 4] += bf16_lo(x.z); v[q * 8 + 5] += bf16_hi(x.z);
+              v[q * 8 + 6] += bf16_lo(x.w); v[q * 8 + 7] += bf16_hi(x.w);
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint4 o;
+            o.x = pack_bf16(v[q * 8 + 0], v[q * 8 + 1]);
+            o.y = pack_bf16(v[q * 8 + 2], v[q * 8 + 3]);
+            o.z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]);
+            o.w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
+            *reinterpret_cast<uint4*>(drow + c + q * 8) = o;
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) g_mb_arrive(&tempty[acc]);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+}
+
+typedef CUresult (*GEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+GEncodeFn g_encoder() {
+  static GEncodeFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (GEncodeFn)p;
+  }
+  return fn;
+}
+// row-major bf16 [rows][K]: box {64, box_rows}, 128B swizzle; rows past the end read as zero
+bool encode_kmajor(CUtensorMap* m, const void* base, uint64_t rows, uint64_t K, uint32_t box_rows) {
+  GEncodeFn enc = g_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {K, rows};
+  cuuint64_t strides[1] = {K * 2};
+  cuuint32_t box[2] = {(cuuint32_t)GK, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int BN>
+int gemm_smem() {
+  return GSTAGES * (GM * GK * 2 + BN * GK * 2) + 1024 + 256;
+}
+
+__global__ void __launch_bounds__(256) k_cast_bf16(const float4* __restrict__ src, uint2* __restrict__ dst, int64_t n4) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = src[i];
+    dst[i] = make_uint2(pack_bf16(v.x, v.y), pack_bf16(v.z, v.w));
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_cast_bf16(const float* src, void* dst, int64_t n, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  if (n % 4 || ((uintptr_t)src | (uintptr_t)dst) % 16) return cudaErrorInvalidValue;
+  const int64_t n4 = n / 4;
+  const int grid = (int)std::min<int64_t>((n4 + 255) / 256, 148 * 8);
+  k_cast_bf16<<<grid, 256, 0, st>>>(reinterpret_cast<const float4*>(src), reinterpret_cast<uint2*>(dst), n4);
+  return cudaGetLastError();
+}
+
+int gemm_num_sms() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+
+// tile width: 256 columns when that still gives every SM a tile, else 128
+cudaError_t launch_gemm(const GemmCall& g, cudaStream_t st) {
+  if (g.M < 1 || g.N < 128 || g.K < GK || g.K % GK || g.N % 128 || g.seg_cols < 128 || g.seg_cols % 128 ||
+      g.N % g.seg_cols || g.N / g.seg_cols > 3 || g.epi < 0 || g.epi > 2 || !g.a || !g.w || !g.d[0] ||
+      (g.epi == 2 && !g.c))
+    return cudaErrorInvalidValue;
+  const int sms = gemm_num_sms();
+  const int m_tiles = (g.M + GM - 1) / GM;
+  const bool wide = g.N % 256 == 0 && g.seg_cols % 256 == 0 && (int64_t)m_tiles * (g.N / 256) >= sms;
+  const int BN = wide ? 256 : 128;
+  GemmMaps maps;
+  if (!encode_kmajor(&maps.a, g.a, (uint64_t)g.M, (uint64_t)g.K, GM)) return cudaErrorInvalidValue;
+  if (!encode_kmajor(&maps.w, g.w, (uint64_t)g.N, (uint64_t)g.K, (uint32_t)BN)) return cudaErrorInvalidValue;
+  GemmArgs a;
+  a.M = g.M; a.N = g.N; a.K = g.K; a.epi = g.epi; a.seg_cols = g.seg_cols;
+  a.m_tiles = m_tiles; a.n_tiles = g.N / BN;
+  for (int i = 0; i < 3; ++i) a.d[i] = static_cast<uint16_t*>(g.d[i] ? g.d[i] : g.d[0]);
+  a.c = static_cast<const uint16_t*>(g.c);
+  const int tiles = a.m_tiles * a.n_tiles;
+  const int grid = tiles < sms ? tiles : sms;
+  if (wide) {
+    static bool attr = cudaFuncSetAttribute(k_gemm<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            gemm_smem<256>()) == cudaSuccess;
+    if (!attr) return cudaErrorInvalidValue;
+    k_gemm<256><<<grid, G_THREADS, gemm_smem<256>(), st>>>(maps, a);
+  } else {
+    static bool attr = cudaFuncSetAttribute(k_gemm<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            gemm_smem<128>()) == cudaSuccess;
+    if (!attr) return cudaErrorInvalidValue;
+    k_gemm<128><<<grid, G_THREADS, gemm_smem<128>(), st>>>(maps, a);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace s3

@@ -1292,4 +1292,22 @@ s3_status s3_verify_resident(s3_ctx* ctx, int64_t* bad) {
   return S3_OK;
 }
 
+s3_status s3_gemm(void* stream, const s3_gemm_args* g) {
+  if (!g) return S3_E_INVAL;
+  GemmCall c;
+  c.a = g->a; c.w = g->w; c.c = g->c;
+  for (int i = 0; i < 3; ++i) c.d[i] = g->d[i];
+  c.M = g->M; c.N = g->N; c.K = g->K; c.seg_cols = g->seg_cols; c.epi = g->epi;
+  const cudaError_t e = launch_gemm(c, (cudaStream_t)stream);
+  if (e == cudaErrorInvalidValue) return S3_E_INVAL;
+  return e == cudaSuccess ? S3_OK : S3_E_CUDA;
+}
+
+s3_status s3_cast_bf16(void* stream, const float* src, void* dst, int64_t n) {
+  if (n < 0 || (n > 0 && (!src || !dst))) return S3_E_INVAL;
+  const cudaError_t e = launch_cast_bf16(src, dst, n, (cudaStream_t)stream);
+  if (e == cudaErrorInvalidValue) return S3_E_INVAL;
+  return e == cudaSuccess ? S3_OK : S3_E_CUDA;
+}
+
 }  // extern "C"

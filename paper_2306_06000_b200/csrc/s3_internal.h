@@ -157,6 +157,17 @@ cudaError_t launch_attn_tc(const Shape& sh, const uint16_t* q, const uint16_t* k
 cudaError_t launch_combine(const Shape& sh, const Split* splits, float* partials, float* out, int32_t* ctrl,
                            int32_t B, int32_t nl, int32_t grid, cudaStream_t st);
 
+// bf16 tcgen05 GEMM (s3_gemm.cu): D = epi(A . W^T); see include/s3.h s3_gemm
+struct GemmCall {
+  const void* a;       // [M][K] bf16
+  const void* w;       // [N][K] bf16
+  void* d[3];          // output column segments [M][seg_cols] bf16
+  const void* c;       // epi 2: [M][N] bf16 addend (may equal d[0])
+  int32_t M, N, K, seg_cols, epi;
+};
+cudaError_t launch_gemm(const GemmCall& g, cudaStream_t st);
+cudaError_t launch_cast_bf16(const float* src, void* dst, int64_t n, cudaStream_t st);
+
 int attn_block_threads(const Shape& sh);
 int attn_tma_stages(const Shape& sh);
 int attn_tma_smem(const Shape& sh, int ns);

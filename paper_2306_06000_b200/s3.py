@@ -81,6 +81,11 @@ class s3_profile(C.Structure):
                 ("d2h_overlap_ms", C.c_double)]
 
 
+class s3_gemm_args(C.Structure):
+    _fields_ = [("a", C.c_void_p), ("w", C.c_void_p), ("d", C.c_void_p * 3), ("c", C.c_void_p),
+                ("M", C.c_int32), ("N", C.c_int32), ("K", C.c_int32), ("seg_cols", C.c_int32), ("epi", C.c_int32)]
+
+
 class s3_host_io(C.Structure):
     _fields_ = [("q", C.c_void_p), ("k_new", C.c_void_p), ("v_new", C.c_void_p), ("eos", C.c_void_p),
                 ("out", C.c_void_p), ("q_dev", C.c_void_p), ("k_new_dev", C.c_void_p),
@@ -112,6 +117,8 @@ _SIGS = {
     "s3_profile_get": (C.c_int, [P, P]),
     "s3_synth_inputs": (C.c_int, [P, _i32, _i32, P, _i64, P, P, P, P]),
     "s3_verify_resident": (C.c_int, [P, P]),
+    "s3_gemm": (C.c_int, [P, P]),
+    "s3_cast_bf16": (C.c_int, [P, P, P, _i64]),
 }
 
 _lib = None
@@ -275,3 +282,28 @@ def s3_verify_resident(ctx) -> int:
     bad = C.c_int64()
     _check(lib().s3_verify_resident(ctx, C.byref(bad)), "s3_verify_resident", ctx)
     return bad.value
+
+
+def s3_gemm(stream, a, w, d, c=None, epi=0, seg_cols=None):
+    """D = epi(A . W^T) on the tensor cores (include/s3.h s3_gemm).  a: [M][K]
+    bf16, w: [N][K] bf16, d: one [M][N] tensor or a list of up to 3 column
+    segments [M][seg_cols]; epi 0 store, 1 gelu_tanh, 2 add c."""
+    segs = list(d) if isinstance(d, (list, tuple)) else [d]
+    M, K = a.shape[-2], a.shape[-1]
+    N = w.shape[0]
+    g = s3_gemm_args()
+    g.a, g.w = _ptr(a), _ptr(w)
+    for i, t in enumerate(segs):
+        g.d[i] = _ptr(t)
+    g.c = _ptr(c)
+    g.M, g.N, g.K, g.epi = int(M), int(N), int(K), int(epi)
+    g.seg_cols = int(seg_cols if seg_cols is not None else N // len(segs))
+    _check(lib().s3_gemm(_ptr(stream) if not hasattr(stream, "cuda_stream") else stream.cuda_stream,
+                         C.byref(g)), "s3_gemm")
+
+
+def s3_cast_bf16(stream, src, dst, n=None):
+    """dst (bf16) = src (fp32), n elements (default: src.numel())."""
+    n = int(src.numel() if n is None else n)
+    _check(lib().s3_cast_bf16(stream.cuda_stream if hasattr(stream, "cuda_stream") else _ptr(stream), _ptr(src),
+                              _ptr(dst), n), "s3_cast_bf16")

@@ -1,0 +1,125 @@
+"""NEXT-2: the tcgen05 GEMM behind the batch-dependent decode
+cost, and the GPT-J-shaped proxy model that runs on it (-m gpu).
+
+* s3_gemm against an fp64 host-side product of the same bf16 operands, for
+  ragged M (one row up to many tiles), both tile widths, every epilogue and
+  the 3-segment QKV output; the bar is the bf16 rounding of the output
+  (2^-8 relative) plus fp32-accumulation slack;
+* the proxy's per-layer q / k_new / v_new (written by the QKV GEMM) and the
+  rows it appended go through the oracle's fp64 attention (s3o_attend_rows),
+  which must match the decode kernel's output at the 2e-3 bar (R20).
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import s3synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2306_06000_b200 import build
+    build.build()
+
+
+def _ref(a, w, epi, c):
+    r = a.double() @ w.double().T
+    if epi == 1:
+        r = 0.5 * r * (1 + torch.tanh(math.sqrt(2 / math.pi) * (r + 0.044715 * r ** 3)))
+    elif epi == 2:
+        r = r + c.double()
+    return r
+
+
+@pytest.mark.parametrize("M,N,K,epi,nseg", [
+    (1, 128, 64, 0, 1), (77, 384, 192, 0, 1), (128, 512, 256, 1, 1), (300, 768, 1024, 2, 1),
+    (513, 12288, 4096, 0, 3), (2048, 4096, 4096, 2, 1), (1500, 16384, 4096, 1, 1), (640, 4096, 16384, 2, 1),
+])
+def test_gemm_matches_fp64(M, N, K, epi, nseg):
+    from paper_2306_06000_b200 import s3 as abi
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K + epi)
+    a = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+    w = (torch.randn(N, K, device="cuda", generator=g) / math.sqrt(K)).to(torch.bfloat16)
+    c = torch.randn(M, N, device="cuda", generator=g).to(torch.bfloat16) if epi == 2 else None
+    ref = _ref(a, w, epi, c)
+    if nseg == 1:
+        d = torch.full((M, N), float("nan"), device="cuda", dtype=torch.bfloat16) if epi != 2 else c.clone()
+        abi.s3_gemm(torch.cuda.current_stream(), a, w, d, c=d if epi == 2 else None, epi=epi)
+        got = d
+    else:
+        seg = N // nseg
+        parts = [torch.full((M, seg), float("nan"), device="cuda", dtype=torch.bfloat16) for _ in range(nseg)]
+        abi.s3_gemm(torch.cuda.current_stream(), a, w, parts, epi=epi, seg_cols=seg)
+        got = torch.cat(parts, dim=1)
+    torch.cuda.synchronize()
+    got = got.double()
+    assert torch.isfinite(got).all()
+    err = (got - ref).abs()
+    tol = 2.0 ** -8 * ref.abs() + 1e-3 * ref.abs().max() + 1e-6
+    bad = (err > tol).sum().item()
+    assert bad == 0, f"{bad} elements off; max err {err.max().item():.3e}"
+
+
+def test_gemm_rejects_bad_shapes():
+    from paper_2306_06000_b200 import s3 as abi
+    a = torch.zeros(4, 96, device="cuda", dtype=torch.bfloat16)
+    w = torch.zeros(128, 96, device="cuda", dtype=torch.bfloat16)
+    d = torch.zeros(4, 128, device="cuda", dtype=torch.bfloat16)
+    with pytest.raises(abi.S3Error) as e:
+        abi.s3_gemm(torch.cuda.current_stream(), a, w, d)      # K % 64 != 0
+    assert e.value.code == 1
+
+
+def test_proxy_model_attention_through_oracle():
+    from paper_2306_06000_b200.engine import S3Engine
+    from paper_2306_06000_b200.model_proxy import GPTJProxy
+    L, H, D, M = 3, 4, 64, 128
+    t = s3synth.make_trace(40, seed=9, policy="short", p=0.3, max_seq_len=M, prompt_max=20)
+    eng = S3Engine(L, H, D, M, 1200, 64, chunk_rows=16, host_store_bytes=1 << 24)
+    proxy = GPTJProxy(eng, d_ff=512, seed=3)
+    eng.submit(t.req_id, t.prompt, t.alloc, t.out)
+    eng.admit()
+    HD = H * D
+    rng = np.random.default_rng(1)
+    checked, worst = 0, 0.0
+
+    def u16(x):
+        return x.view(torch.int16).cpu().numpy().view(np.uint16)
+
+    for step in range(12):
+        pre = eng.batch_view()
+        B = len(pre)
+        if not B:
+            break
+        pick = sorted(set(rng.choice(B, min(B, 4), replace=False).tolist()))
+
+        def on_layer(l, B_, pre=pre, pick=pick):
+            nonlocal checked, worst
+            torch.cuda.synchronize()
+            A = eng.arena_rows_view()
+            q = u16(eng.q[:B_ * HD]).reshape(B_, H, D)
+            out = eng.out[:B_ * HD].view(B_, H, D).cpu().numpy().astype(np.float64)
+            for b in pick:
+                req, P, gen, ln, cap, off = pre[b]
+                rows = u16(A[off:off + ln + 1, l].reshape(-1)).reshape(ln + 1, 2, H, D)   # new row appended
+                ref = oracle.attend_rows(q[b], rows[:, 0], rows[:, 1])
+                err = float((np.abs(out[b] - ref).max(-1) / np.maximum(np.abs(ref).max(-1), 2.0 ** -20)).max())
+                worst = max(worst, err)
+                assert err <= 2e-3, (step, l, b, err)
+                checked += 1
+
+        proxy.decode_step(on_layer)
+        eng.evict_compact()
+        eng.admit()
+    eng.close()
+    print("checked", checked, "worst rel err", worst)
+    assert checked >= 50

@@ -691,3 +691,23 @@ def test_on_demand_compaction_late_submit(oracle_lib):
     assert logs[0][1] == logs[1][1]
     assert logs[1][1][40] is not None
     assert logs[0][2] == 0 and logs[1][2] > 0
+
+
+def test_attend_rows_matches_sdpa_and_generated(oracle_lib):
+    # s3o_attend_rows (for GEMM-fed inputs) is the same attention: torch SDPA
+    # in fp64 on random bf16 rows, and equal to attend_generated on generator rows
+    rng = np.random.default_rng(3)
+    H, Hkv, D, n = 4, 2, 64, 37
+    bits = lambda *s: (rng.integers(-128, 128, s).astype(np.float32) / 64).view(np.uint32).__rshift__(16).astype(np.uint16)
+    q, K, V = bits(H, D), bits(n, Hkv, D), bits(n, Hkv, D)
+    got = oracle.attend_rows(q, K, V)
+    Q = torch.from_numpy(oracle.bf16_bits_to_f64(q))[:, None, :]
+    Kt = torch.from_numpy(oracle.bf16_bits_to_f64(K)).permute(1, 0, 2).repeat_interleave(H // Hkv, dim=0)
+    Vt = torch.from_numpy(oracle.bf16_bits_to_f64(V)).permute(1, 0, 2).repeat_interleave(H // Hkv, dim=0)
+    ref = torch.nn.functional.scaled_dot_product_attention(Q, Kt, Vt)[:, 0, :].numpy()
+    assert np.allclose(got, ref, rtol=0, atol=1e-12)
+    L, M = 2, 64
+    rows = np.stack([np.stack([oracle.gen_kv(L, H, D, M, 1, 5, 1, kv, j, Hkv=Hkv) for kv in (0, 1)]) for j in range(10)])
+    qg = oracle.gen_q(L, H, D, M, 1, 5, 1, 9)
+    assert np.array_equal(oracle.attend_rows(qg, rows[:, 0], rows[:, 1]),
+                          oracle.attend_generated(L, H, D, M, 1, 5, 9, 1, Hkv=Hkv))
