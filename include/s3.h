@@ -305,8 +305,15 @@ s3_status s3_verify_resident(s3_ctx* ctx, int64_t* bad_rows);
 typedef struct {
   const void* a; const void* w; void* d[3]; const void* c;
   int32_t M, N, K, seg_cols, epi;
+  void* workspace; int64_t workspace_bytes;  /* device scratch for split-K partials
+                                                (zero-filled once by the caller;
+                                                every call leaves it reusable), or
+                                                NULL: no split-K                  */
 } s3_gemm_args;
 s3_status s3_gemm(void* stream, const s3_gemm_args* g);
+/* Workspace s3_gemm would use for this shape (0: it runs without).  Small
+ * batches split K over idle SMs; a smaller workspace only limits the split. */
+s3_status s3_gemm_workspace(const s3_gemm_args* g, int64_t* bytes);
 /* dst (bf16, device) = round-to-nearest(src (fp32, device)), n elements
  * (n % 4 == 0, 16-B aligned): the attention output as the next GEMM's A.  */
 s3_status s3_cast_bf16(void* stream, const float* src, void* dst, int64_t n);

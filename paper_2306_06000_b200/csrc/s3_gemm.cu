@@ -29,6 +29,8 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <climits>
+#include <cstdlib>
 
 #include "s3_internal.h"
 
@@ -69,9 +71,9 @@ __device__ __forceinline__ uint64_t g_desc(const void* p) {
   return (uint64_t)((gsu32(p) >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
          ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
-// instruction descriptor: bf16 x bf16 -> f32, both K-major, M 128, N n
-__host__ __device__ constexpr uint32_t g_idesc(int n) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(GM >> 4) << 24);
+// instruction descriptor: bf16 x bf16 -> f32, both K-major, M m, N n
+__host__ __device__ constexpr uint32_t g_idesc(int n, int m) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
 __device__ __forceinline__ void g_mma(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
   asm volatile(
@@ -112,14 +114,59 @@ struct GemmMaps {
 };
 struct GemmArgs {
   int32_t M, N, K, epi, seg_cols, m_tiles, n_tiles;
+  int32_t S;              // split-K factor (units = tiles x S)
   uint16_t* d[3];
   const uint16_t* c;
+  float* ws;              // S > 1: fp32 partial tiles [tile][split][rows][BN]
+  int32_t* cnt;           // S > 1: per (tile, CTA of the pair) arrival counters (zero between calls)
 };
 
-template <int BN>
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// CTA pair: both CTAs' TMA loads complete on the leader's (rank 0) barrier
+__device__ __forceinline__ void g_tma2d_pair(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];" ::"r"(gsu32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(gsu32(bar) & 0xFEFFFFFFu)
+      : "memory");
+}
+__device__ __forceinline__ void g_mma_pair(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(id), "r"(acc)
+      : "memory");
+}
+// completion of the pair's MMAs arrives on the barrier at this offset in BOTH CTAs
+__device__ __forceinline__ void g_commit_pair(uint64_t* b) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          gsu32(b)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+// arrive on the leader CTA's barrier at the same offset
+__device__ __forceinline__ void g_arrive_leader(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(gsu32(b) & 0xFEFFFFFFu) : "memory");
+}
+
+// CG = 1: one CTA per 128 x BN tile (tcgen05 cta_group::1, M 128).
+// CG = 2: a CTA pair per 256 x BN tile (cta_group::2, M 256): each CTA loads
+//   its 128 rows of A and half (BN/2 rows) of the W tile, the leader issues
+//   the MMAs (the tensor cores read both CTAs' shared memory), each CTA's
+//   TMEM holds its 128 accumulator rows.  W is read from L2 once per 256 rows
+//   instead of once per 128, halving the operand traffic per flop.
+template <int BN, int CG>
 __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(const __grid_constant__ GemmMaps maps, GemmArgs a) {
-  constexpr int A_BYTES = GM * GK * 2, W_BYTES = BN * GK * 2, STAGE = A_BYTES + W_BYTES;
+  constexpr int A_BYTES = GM * GK * 2, W_BYTES = (BN / CG) * GK * 2, STAGE = A_BYTES + W_BYTES;
   constexpr int TMEM_COLS = 2 * BN;
+  constexpr int TM_ROWS = GM * CG;                     // rows per tile
   extern __shared__ __align__(1024) uint8_t gsmem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(gsmem_raw) + 1023) & ~(uintptr_t)1023);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + GSTAGES * STAGE);
@@ -128,82 +175,140 @@ __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(const __grid_constant__ G
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_base = reinterpret_cast<uint32_t*>(tempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = CG == 2 ? cluster_rank() : 0;
+  const bool leader = rank == 0;
+  const int unit0 = (int)blockIdx.x / CG, nunits = (int)gridDim.x / CG;   // tile scheduler per CTA group
   if (threadIdx.x == 0) {
     for (int i = 0; i < GSTAGES; ++i) { g_mb_init(&full[i], 1); g_mb_init(&empty[i], 1); }
-    for (int i = 0; i < 2; ++i) { g_mb_init(&tfull[i], 1); g_mb_init(&tempty[i], 4); }
+    for (int i = 0; i < 2; ++i) { g_mb_init(&tfull[i], 1); g_mb_init(&tempty[i], 4 * CG); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.a) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.w) : "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(gsu32(tmem_base)),
-                 "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if constexpr (CG == 1) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(gsu32(tmem_base)),
+                   "r"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(gsu32(tmem_base)),
+                   "r"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all(); else __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_base;
-  const int tiles = a.m_tiles * a.n_tiles;
+  const int units = a.m_tiles * a.n_tiles * a.S;
   const int kblocks = a.K / GK;
+  // unit u = (tile u / S, split u % S); split j covers K blocks [j kblocks / S, (j + 1) kblocks / S)
+  auto krange = [&](int u, int& kb0, int& kb1) {
+    const int j = u % a.S;
+    kb0 = (int)((int64_t)j * kblocks / a.S);
+    kb1 = (int)((int64_t)(j + 1) * kblocks / a.S);
+  };
 
   if (warp == 0) {
     // ------------------------------ TMA producer ------------------------------
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-        const int m0 = (t % a.m_tiles) * GM, n0 = (t / a.m_tiles) * BN;
-        for (int kb = 0; kb < kblocks; ++kb) {
+      for (int u = unit0; u < units; u += nunits) {
+        const int t = u / a.S;
+        const int m0 = (t % a.m_tiles) * TM_ROWS + (int)rank * GM;
+        const int n0 = (t / a.m_tiles) * BN + (int)rank * (BN / CG);
+        int kb0, kb1;
+        krange(u, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
           g_mb_wait(&empty[s], ph ^ 1u);
           uint8_t* sa = smem + s * STAGE;
-          g_mb_expect(&full[s], (uint32_t)STAGE);
-          g_tma2d(sa, &maps.a, kb * GK, m0, &full[s]);
-          g_tma2d(sa + A_BYTES, &maps.w, kb * GK, n0, &full[s]);
+          if constexpr (CG == 1) {
+            g_mb_expect(&full[s], (uint32_t)STAGE);
+            g_tma2d(sa, &maps.a, kb * GK, m0, &full[s]);
+            g_tma2d(sa + A_BYTES, &maps.w, kb * GK, n0, &full[s]);
+          } else {
+            if (leader) g_mb_expect(&full[s], (uint32_t)(2 * STAGE));   // both CTAs' bytes
+            g_tma2d_pair(sa, &maps.a, kb * GK, m0, &full[s]);
+            g_tma2d_pair(sa + A_BYTES, &maps.w, kb * GK, n0, &full[s]);
+          }
           if (++s == GSTAGES) { s = 0; ph ^= 1u; }
         }
       }
     }
   } else if (warp == 1) {
     // ------------------------------- MMA issuer -------------------------------
-    if (lane == 0) {
-      constexpr uint32_t id = g_idesc(BN);
+    if (lane == 0 && leader) {
+      constexpr uint32_t id = g_idesc(BN, TM_ROWS);
       int s = 0;
       uint32_t ph = 0;
       int it = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+      for (int u = unit0; u < units; u += nunits, ++it) {
         const int acc = it & 1;
-        g_mb_wait(&tempty[acc], ((uint32_t)(it >> 1) & 1u) ^ 1u);   // the epilogue drained this accumulator
+        g_mb_wait(&tempty[acc], ((uint32_t)(it >> 1) & 1u) ^ 1u);   // the epilogue(s) drained this accumulator
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + (uint32_t)(acc * BN);
-        for (int kb = 0; kb < kblocks; ++kb) {
+        int kb0, kb1;
+        krange(u, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
           g_mb_wait(&full[s], ph);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint8_t* sa = smem + s * STAGE;
           const uint64_t da = g_desc(sa), dw = g_desc(sa + A_BYTES);
 #pragma unroll
-          for (int k = 0; k < GK / 16; ++k)          // +32 B per K = 16 inside the swizzle atom
-            g_mma(d, da + (uint64_t)(k * 2), dw + (uint64_t)(k * 2), id, (kb | k) != 0);
-          g_commit(&empty[s]);                         // the stage is free once these MMAs have read it
+          for (int k = 0; k < GK / 16; ++k) {        // +32 B per K = 16 inside the swizzle atom
+            if constexpr (CG == 1) g_mma(d, da + (uint64_t)(k * 2), dw + (uint64_t)(k * 2), id, kb > kb0 || k);
+            else g_mma_pair(d, da + (uint64_t)(k * 2), dw + (uint64_t)(k * 2), id, kb > kb0 || k);
+          }
+          // the stage is free once these MMAs have read it (in both CTAs of a pair)
+          if constexpr (CG == 1) g_commit(&empty[s]); else g_commit_pair(&empty[s]);
           if (++s == GSTAGES) { s = 0; ph ^= 1u; }
         }
-        g_commit(&tfull[acc]);                         // accumulator complete
+        if constexpr (CG == 1) g_commit(&tfull[acc]); else g_commit_pair(&tfull[acc]);   // accumulator complete
       }
     }
   } else {
     // -------------------------------- epilogue --------------------------------
     const int quarter = warp & 3;                      // TMEM lanes 32*quarter .. +31
     const int row = quarter * 32 + lane;
+    __shared__ int s_last;
     int it = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+    for (int u = unit0; u < units; u += nunits, ++it) {
       const int acc = it & 1;
-      const int m0 = (t % a.m_tiles) * GM, n0 = (t / a.m_tiles) * BN;
+      const int t = u / a.S, split = u % a.S;
+      const int m0 = (t % a.m_tiles) * TM_ROWS + (int)rank * GM, n0 = (t / a.m_tiles) * BN;
       g_mb_wait(&tfull[acc], (uint32_t)(it >> 1) & 1u);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int m = m0 + row;
       const int seg = n0 / a.seg_cols, col0 = n0 - seg * a.seg_cols;
       uint16_t* drow = a.d[seg] + (int64_t)m * a.seg_cols + col0;
       const uint16_t* crow = a.c ? a.c + (int64_t)m * a.N + n0 : nullptr;
+      // split-K: this split's fp32 partial rows; the last split of the tile to arrive sums them
+      float* prow = a.S > 1 ? a.ws + (((int64_t)t * a.S + split) * TM_ROWS + rank * GM + row) * BN : nullptr;
+      auto epilogue_store = [&](float (&v)[32], int c) {
+        if (a.epi == 1) {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = gelu_tanh(v[i]);
+        } else if (a.epi == 2) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const uint4 x = *reinterpret_cast<const uint4*>(crow + c + q * 8);
+            v[q * 8 + 0] += bf16_lo(x.x); v[q * 8 + 1] += bf16_hi(x.x);
+            v[q * 8 + 2] += bf16_lo(x.y); v[q * 8 + 3] += bf16_hi(x.y);
+            v[q * 8 + 4] += bf16_lo(x.z); v[q * 8 + 5] += bf16_hi(x.z);
+            v[q * 8 + 6] += bf16_lo(x.w); v[q * 8 + 7] += bf16_hi(x.w);
+          }
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 o;
+          o.x = pack_bf16(v[q * 8 + 0], v[q * 8 + 1]);
+          o.y = pack_bf16(v[q * 8 + 2], v[q * 8 + 3]);
+          o.z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]);
+          o.w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
+          *reinterpret_cast<uint4*>(drow + c + q * 8) = o;
+        }
+      };
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         uint32_t r[32];
@@ -212,39 +317,62 @@ __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(const __grid_constant__ G
           float v[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-          if (a.epi == 1) {
+          if (a.S == 1) {
+            epilogue_store(v, c);
+          } else {
 #pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = gelu_tanh(v[i]);
-          } else if (a.epi == 2) {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              const uint4 x = *reinterpret_cast<const uint4*>(crow + c + q * 8);
-              v[q * 8 + 0] += bf16_lo(x.x); v[q * 8 + 1] += bf16_hi(x.x);
-              v[q * 8 + 2] += bf16_lo(x.y); v[q * 8 + 3] += bf16_hi(x.y);
-              v[q * 8 + 4] += bf16_lo(x.z); v[q * 8 + 5] += bf16_hi(x.z);
-              v[q * 8 + 6] += bf16_lo(x.w); v[q * 8 + 7] += bf16_hi(x.w);
-            }
-          }
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            uint4 o;
-            o.x = pack_bf16(v[q * 8 + 0], v[q * 8 + 1]);
-            o.y = pack_bf16(v[q * 8 + 2], v[q * 8 + 3]);
-            o.z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]);
-            o.w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
-            *reinterpret_cast<uint4*>(drow + c + q * 8) = o;
+            for (int q = 0; q < 8; ++q)
+              __stcg(reinterpret_cast<float4*>(prow + c) + q, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
           }
         }
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
-      if (lane == 0) g_mb_arrive(&tempty[acc]);
+      if (lane == 0) {
+        if constexpr (CG == 1) g_mb_arrive(&tempty[acc]); else g_arrive_leader(&tempty[acc]);
+      }
+      if (a.S > 1) {
+        // every epilogue thread's partial is written; one atomic per (tile, CTA) says how many splits are in
+        __threadfence();
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (threadIdx.x == 64) {
+          int* cn = a.cnt + t * CG + rank;
+          const int old = atomicAdd(cn, 1);
+          s_last = old == a.S - 1;
+          if (old == a.S - 1) *cn = 0;                  // reset for the next call (stream order)
+          __threadfence();
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (s_last && m < a.M) {
+          const float* p0 = a.ws + ((int64_t)t * a.S * TM_ROWS + rank * GM + row) * BN;
+#pragma unroll 1
+          for (int c = 0; c < BN; c += 32) {
+            float v[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = 0.f;
+            for (int j = 0; j < a.S; ++j) {
+              const float4* pj = reinterpret_cast<const float4*>(p0 + (int64_t)j * TM_ROWS * BN + c);
+#pragma unroll
+              for (int q = 0; q < 8; ++q) {
+                const float4 x = __ldcg(pj + q);
+                v[4 * q] += x.x; v[4 * q + 1] += x.y; v[4 * q + 2] += x.z; v[4 * q + 3] += x.w;
+              }
+            }
+            epilogue_store(v, c);
+          }
+        }
+      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
+  if constexpr (CG == 2) cluster_sync_all(); else __syncthreads();   // the pair's MMAs are done with both CTAs
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  if (warp == 1) {
+    if constexpr (CG == 1)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+    else
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  }
 }
 
 typedef CUresult (*GEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -274,9 +402,29 @@ bool encode_kmajor(CUtensorMap* m, const void* base, uint64_t rows, uint64_t K, 
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN>
+template <int BN, int CG>
 int gemm_smem() {
-  return GSTAGES * (GM * GK * 2 + BN * GK * 2) + 1024 + 256;
+  return GSTAGES * (GM * GK * 2 + (BN / CG) * GK * 2) + 1024 + 256;
+}
+
+template <int BN, int CG>
+cudaError_t launch_one(const GemmMaps& maps, const GemmArgs& a, int grid, cudaStream_t st) {
+  static const bool attr = cudaFuncSetAttribute(k_gemm<BN, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                gemm_smem<BN, CG>()) == cudaSuccess;
+  if (!attr) return cudaErrorInvalidValue;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(G_THREADS);
+  cfg.dynamicSmemBytes = gemm_smem<BN, CG>();
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CG;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_gemm<BN, CG>, maps, a);
 }
 
 __global__ void __launch_bounds__(256) k_cast_bf16(const float4* __restrict__ src, uint2* __restrict__ dst, int64_t n4) {
@@ -307,37 +455,80 @@ int gemm_num_sms() {
   return n;
 }
 
-// tile width: 256 columns when that still gives every SM a tile, else 128
-cudaError_t launch_gemm(const GemmCall& g, cudaStream_t st) {
+// Split-K factor: estimated time (in K blocks) = waves x (K blocks per split +
+// pipeline fill) + the last split's reduction; S = 1 unless splitting fills
+// idle SMs.  Needs S x tiles x rows x BN fp32 + counters of workspace.
+int gemm_splits(int tiles, int groups, int kblocks, int rows, int BN, int64_t ws_bytes) {
+  static const int force = [] { const char* e = getenv("S3_GEMM_S"); return e ? atoi(e) : 0; }();
+  if (force > 0) {
+    const int S = std::min(force, std::max(1, kblocks / 4));
+    return (int64_t)S * tiles * rows * BN * 4 + (int64_t)tiles * 2 * 4 <= ws_bytes ? S : 1;
+  }
+  int best = 1;
+  double best_t = 1e30;
+  for (int S = 1; S <= 8; ++S) {
+    if (S > 1 && kblocks / S < 8) break;
+    if (S > 1 && (int64_t)S * tiles * rows * BN * 4 + (int64_t)tiles * 2 * 4 > ws_bytes) break;
+    const int waves = (tiles * S + groups - 1) / groups;
+    // a split writes its fp32 partial (~7 K blocks of time) and the last one reads S of them
+    const double t = waves * ((double)kblocks / S + 3.0 + (S > 1 ? 7.0 : 0.0)) + (S > 1 ? 7.0 * S : 0.0);
+    if (t < best_t * 0.97) { best_t = t; best = S; }
+  }
+  return best;
+}
+
+// Tile choice: a CTA pair per 256 x 256 tile (half the operand traffic per
+// flop) when M > 128; one CTA per 128 x 256 tile for a single row tile; 128
+// columns when 256-wide tiles would leave SMs idle.  Then the split-K factor.
+struct GemmPlan {
+  int CG, BN, rows, m_tiles, tiles, S;
+  int64_t ws_bytes;   // workspace the plan needs (0 when S = 1)
+};
+bool gemm_plan(const GemmCall& g, int64_t ws_avail, GemmPlan& p) {
   if (g.M < 1 || g.N < 128 || g.K < GK || g.K % GK || g.N % 128 || g.seg_cols < 128 || g.seg_cols % 128 ||
-      g.N % g.seg_cols || g.N / g.seg_cols > 3 || g.epi < 0 || g.epi > 2 || !g.a || !g.w || !g.d[0] ||
-      (g.epi == 2 && !g.c))
-    return cudaErrorInvalidValue;
+      g.N % g.seg_cols || g.N / g.seg_cols > 3 || g.epi < 0 || g.epi > 2)
+    return false;
   const int sms = gemm_num_sms();
-  const int m_tiles = (g.M + GM - 1) / GM;
-  const bool wide = g.N % 256 == 0 && g.seg_cols % 256 == 0 && (int64_t)m_tiles * (g.N / 256) >= sms;
-  const int BN = wide ? 256 : 128;
+  const bool n256 = g.N % 256 == 0 && g.seg_cols % 256 == 0;
+  static const int force = [] { const char* e = getenv("S3_GEMM_CG"); return e ? atoi(e) : 0; }();
+  p.CG = force ? force : (g.M > GM && n256 ? 2 : 1);
+  if (p.CG == 2 && !n256) return false;
+  p.rows = GM * p.CG;
+  p.m_tiles = (g.M + p.rows - 1) / p.rows;
+  p.BN = p.CG == 2 ? 256 : (n256 && (int64_t)p.m_tiles * (g.N / 256) >= sms ? 256 : 128);
+  p.tiles = p.m_tiles * (g.N / p.BN);
+  p.S = gemm_splits(p.tiles, sms / p.CG, g.K / GK, p.rows, p.BN, ws_avail);
+  p.ws_bytes = p.S > 1 ? (int64_t)p.S * p.tiles * p.rows * p.BN * 4 + (int64_t)p.tiles * 2 * 4 : 0;
+  return true;
+}
+
+int64_t gemm_workspace_bytes(const GemmCall& g) {
+  GemmPlan p;
+  return gemm_plan(g, INT64_MAX, p) ? p.ws_bytes : -1;
+}
+
+cudaError_t launch_gemm(const GemmCall& g, cudaStream_t st) {
+  GemmPlan p;
+  if (!gemm_plan(g, g.workspace ? g.workspace_bytes : 0, p) || !g.a || !g.w || !g.d[0] || (g.epi == 2 && !g.c))
+    return cudaErrorInvalidValue;
   GemmMaps maps;
   if (!encode_kmajor(&maps.a, g.a, (uint64_t)g.M, (uint64_t)g.K, GM)) return cudaErrorInvalidValue;
-  if (!encode_kmajor(&maps.w, g.w, (uint64_t)g.N, (uint64_t)g.K, (uint32_t)BN)) return cudaErrorInvalidValue;
+  if (!encode_kmajor(&maps.w, g.w, (uint64_t)g.N, (uint64_t)g.K, (uint32_t)(p.BN / p.CG))) return cudaErrorInvalidValue;
   GemmArgs a;
   a.M = g.M; a.N = g.N; a.K = g.K; a.epi = g.epi; a.seg_cols = g.seg_cols;
-  a.m_tiles = m_tiles; a.n_tiles = g.N / BN;
+  a.m_tiles = p.m_tiles; a.n_tiles = g.N / p.BN;
   for (int i = 0; i < 3; ++i) a.d[i] = static_cast<uint16_t*>(g.d[i] ? g.d[i] : g.d[0]);
   a.c = static_cast<const uint16_t*>(g.c);
-  const int tiles = a.m_tiles * a.n_tiles;
-  const int grid = tiles < sms ? tiles : sms;
-  if (wide) {
-    static bool attr = cudaFuncSetAttribute(k_gemm<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            gemm_smem<256>()) == cudaSuccess;
-    if (!attr) return cudaErrorInvalidValue;
-    k_gemm<256><<<grid, G_THREADS, gemm_smem<256>(), st>>>(maps, a);
-  } else {
-    static bool attr = cudaFuncSetAttribute(k_gemm<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            gemm_smem<128>()) == cudaSuccess;
-    if (!attr) return cudaErrorInvalidValue;
-    k_gemm<128><<<grid, G_THREADS, gemm_smem<128>(), st>>>(maps, a);
-  }
+  a.S = p.S;
+  a.ws = static_cast<float*>(g.workspace);
+  a.cnt = p.S > 1 ? reinterpret_cast<int32_t*>(static_cast<uint8_t*>(g.workspace) + p.ws_bytes - (int64_t)p.tiles * 2 * 4)
+                  : nullptr;
+  const int groups = std::min(p.tiles * p.S, gemm_num_sms() / p.CG);
+  cudaError_t e;
+  if (p.CG == 2) e = launch_one<256, 2>(maps, a, 2 * groups, st);
+  else if (p.BN == 256) e = launch_one<256, 1>(maps, a, groups, st);
+  else e = launch_one<128, 1>(maps, a, groups, st);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

@@ -1298,9 +1298,20 @@ s3_status s3_gemm(void* stream, const s3_gemm_args* g) {
   c.a = g->a; c.w = g->w; c.c = g->c;
   for (int i = 0; i < 3; ++i) c.d[i] = g->d[i];
   c.M = g->M; c.N = g->N; c.K = g->K; c.seg_cols = g->seg_cols; c.epi = g->epi;
+  c.workspace = g->workspace; c.workspace_bytes = g->workspace_bytes;
   const cudaError_t e = launch_gemm(c, (cudaStream_t)stream);
   if (e == cudaErrorInvalidValue) return S3_E_INVAL;
   return e == cudaSuccess ? S3_OK : S3_E_CUDA;
+}
+
+s3_status s3_gemm_workspace(const s3_gemm_args* g, int64_t* bytes) {
+  if (!g || !bytes) return S3_E_INVAL;
+  GemmCall c{};
+  c.M = g->M; c.N = g->N; c.K = g->K; c.seg_cols = g->seg_cols; c.epi = g->epi;
+  const int64_t b = gemm_workspace_bytes(c);
+  if (b < 0) return S3_E_INVAL;
+  *bytes = b;
+  return S3_OK;
 }
 
 s3_status s3_cast_bf16(void* stream, const float* src, void* dst, int64_t n) {

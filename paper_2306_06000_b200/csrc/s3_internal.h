@@ -164,7 +164,10 @@ struct GemmCall {
   void* d[3];          // output column segments [M][seg_cols] bf16
   const void* c;       // epi 2: [M][N] bf16 addend (may equal d[0])
   int32_t M, N, K, seg_cols, epi;
+  void* workspace;     // split-K partials + counters (zeroed once), or NULL
+  int64_t workspace_bytes;
 };
+int64_t gemm_workspace_bytes(const GemmCall& g);   // -1 on a bad shape
 cudaError_t launch_gemm(const GemmCall& g, cudaStream_t st);
 cudaError_t launch_cast_bf16(const float* src, void* dst, int64_t n, cudaStream_t st);
 

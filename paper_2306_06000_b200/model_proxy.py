@@ -53,6 +53,8 @@ class GPTJProxy:
         self.x = torch.empty(eng.max_running, self.d, device=dev, dtype=torch.bfloat16)
         self.a = torch.empty(eng.max_running, self.d, device=dev, dtype=torch.bfloat16)
         self.h = torch.empty(eng.max_running, d_ff, device=dev, dtype=torch.bfloat16)
+        # split-K scratch of s3_gemm (small batches spread K over idle SMs); zeroed once
+        self.ws = torch.zeros(96 << 20, device=dev, dtype=torch.uint8)
 
     @property
     def weight_bytes(self) -> int:
@@ -66,17 +68,17 @@ class GPTJProxy:
 
     def layer_gemms(self, l: int, B: int, stream):
         """The four projections of layer l around its attention (x: [B][d])."""
-        eng, HD = self.eng, self.d
+        eng, HD, ws = self.eng, self.d, self.ws
         x, a, h = self.x[:B], self.a[:B], self.h[:B]
         return (
             # QKV straight into the decode buffers: [nl = 1][B][H][D] each
             lambda: abi.s3_gemm(stream, x, self.w_qkv[l],
-                                [eng.q[:B * HD], eng.k_new[:B * HD], eng.v_new[:B * HD]], seg_cols=HD),
+                                [eng.q[:B * HD], eng.k_new[:B * HD], eng.v_new[:B * HD]], seg_cols=HD, workspace=ws),
             # attention out (fp32) -> bf16, then x += a Wo^T ; h = gelu(x Wi^T) ; x += h W2^T
             lambda: (abi.s3_cast_bf16(stream, eng.out, a, B * HD),
-                     abi.s3_gemm(stream, x, self.w_1[l], h, epi=1),
-                     abi.s3_gemm(stream, a, self.w_o[l], x, c=x, epi=2),
-                     abi.s3_gemm(stream, h, self.w_2[l], x, c=x, epi=2)),
+                     abi.s3_gemm(stream, x, self.w_1[l], h, epi=1, workspace=ws),
+                     abi.s3_gemm(stream, a, self.w_o[l], x, c=x, epi=2, workspace=ws),
+                     abi.s3_gemm(stream, h, self.w_2[l], x, c=x, epi=2, workspace=ws)),
         )
 
     def decode_step(self, on_layer=None):

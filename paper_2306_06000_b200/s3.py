@@ -83,7 +83,8 @@ class s3_profile(C.Structure):
 
 class s3_gemm_args(C.Structure):
     _fields_ = [("a", C.c_void_p), ("w", C.c_void_p), ("d", C.c_void_p * 3), ("c", C.c_void_p),
-                ("M", C.c_int32), ("N", C.c_int32), ("K", C.c_int32), ("seg_cols", C.c_int32), ("epi", C.c_int32)]
+                ("M", C.c_int32), ("N", C.c_int32), ("K", C.c_int32), ("seg_cols", C.c_int32), ("epi", C.c_int32),
+                ("workspace", C.c_void_p), ("workspace_bytes", C.c_int64)]
 
 
 class s3_host_io(C.Structure):
@@ -118,6 +119,7 @@ _SIGS = {
     "s3_synth_inputs": (C.c_int, [P, _i32, _i32, P, _i64, P, P, P, P]),
     "s3_verify_resident": (C.c_int, [P, P]),
     "s3_gemm": (C.c_int, [P, P]),
+    "s3_gemm_workspace": (C.c_int, [P, P]),
     "s3_cast_bf16": (C.c_int, [P, P, P, _i64]),
 }
 
@@ -284,14 +286,18 @@ def s3_verify_resident(ctx) -> int:
     return bad.value
 
 
-def s3_gemm(stream, a, w, d, c=None, epi=0, seg_cols=None):
+def s3_gemm(stream, a, w, d, c=None, epi=0, seg_cols=None, workspace=None, M=None):
     """D = epi(A . W^T) on the tensor cores (include/s3.h s3_gemm).  a: [M][K]
     bf16, w: [N][K] bf16, d: one [M][N] tensor or a list of up to 3 column
-    segments [M][seg_cols]; epi 0 store, 1 gelu_tanh, 2 add c."""
+    segments [M][seg_cols]; epi 0 store, 1 gelu_tanh, 2 add c; workspace: a
+    zero-initialised uint8 device tensor for split-K (or None)."""
     segs = list(d) if isinstance(d, (list, tuple)) else [d]
-    M, K = a.shape[-2], a.shape[-1]
+    M = int(a.shape[-2] if M is None else M)
+    K = a.shape[-1]
     N = w.shape[0]
     g = s3_gemm_args()
+    if workspace is not None:
+        g.workspace, g.workspace_bytes = _ptr(workspace), int(workspace.numel())
     g.a, g.w = _ptr(a), _ptr(w)
     for i, t in enumerate(segs):
         g.d[i] = _ptr(t)
@@ -307,3 +313,12 @@ def s3_cast_bf16(stream, src, dst, n=None):
     n = int(src.numel() if n is None else n)
     _check(lib().s3_cast_bf16(stream.cuda_stream if hasattr(stream, "cuda_stream") else _ptr(stream), _ptr(src),
                               _ptr(dst), n), "s3_cast_bf16")
+
+
+def s3_gemm_workspace(M, N, K, seg_cols=None, epi=0) -> int:
+    g = s3_gemm_args()
+    g.M, g.N, g.K, g.epi = int(M), int(N), int(K), int(epi)
+    g.seg_cols = int(seg_cols or N)
+    out = C.c_int64()
+    _check(lib().s3_gemm_workspace(C.byref(g), C.byref(out)), "s3_gemm_workspace")
+    return int(out.value)

@@ -40,33 +40,39 @@ def _ref(a, w, epi, c):
     return r
 
 
-@pytest.mark.parametrize("M,N,K,epi,nseg", [
-    (1, 128, 64, 0, 1), (77, 384, 192, 0, 1), (128, 512, 256, 1, 1), (300, 768, 1024, 2, 1),
-    (513, 12288, 4096, 0, 3), (2048, 4096, 4096, 2, 1), (1500, 16384, 4096, 1, 1), (640, 4096, 16384, 2, 1),
+@pytest.mark.parametrize("M,N,K,epi,nseg,ws", [
+    (1, 128, 64, 0, 1, False), (77, 384, 192, 0, 1, True), (128, 512, 256, 1, 1, True), (300, 768, 1024, 2, 1, True),
+    (513, 12288, 4096, 0, 3, True), (2048, 4096, 4096, 2, 1, True), (1500, 16384, 4096, 1, 1, False),
+    (640, 4096, 16384, 2, 1, True), (512, 4096, 16384, 2, 1, True), (200, 4096, 4096, 1, 1, True),
+    (64, 12288, 4096, 0, 3, True), (512, 4096, 4096, 2, 1, False),
 ])
-def test_gemm_matches_fp64(M, N, K, epi, nseg):
+def test_gemm_matches_fp64(M, N, K, epi, nseg, ws):
     from paper_2306_06000_b200 import s3 as abi
     g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K + epi)
     a = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
     w = (torch.randn(N, K, device="cuda", generator=g) / math.sqrt(K)).to(torch.bfloat16)
     c = torch.randn(M, N, device="cuda", generator=g).to(torch.bfloat16) if epi == 2 else None
     ref = _ref(a, w, epi, c)
-    if nseg == 1:
-        d = torch.full((M, N), float("nan"), device="cuda", dtype=torch.bfloat16) if epi != 2 else c.clone()
-        abi.s3_gemm(torch.cuda.current_stream(), a, w, d, c=d if epi == 2 else None, epi=epi)
-        got = d
-    else:
-        seg = N // nseg
-        parts = [torch.full((M, seg), float("nan"), device="cuda", dtype=torch.bfloat16) for _ in range(nseg)]
-        abi.s3_gemm(torch.cuda.current_stream(), a, w, parts, epi=epi, seg_cols=seg)
-        got = torch.cat(parts, dim=1)
-    torch.cuda.synchronize()
-    got = got.double()
-    assert torch.isfinite(got).all()
-    err = (got - ref).abs()
-    tol = 2.0 ** -8 * ref.abs() + 1e-3 * ref.abs().max() + 1e-6
-    bad = (err > tol).sum().item()
-    assert bad == 0, f"{bad} elements off; max err {err.max().item():.3e}"
+    need = abi.s3_gemm_workspace(M, N, K, seg_cols=N // nseg, epi=epi)
+    work = torch.zeros(max(need, 16), device="cuda", dtype=torch.uint8) if ws else None
+    st = torch.cuda.current_stream()
+    for rep in range(2):                                 # the second call reuses the workspace (counters reset)
+        if nseg == 1:
+            d = torch.full((M, N), float("nan"), device="cuda", dtype=torch.bfloat16) if epi != 2 else c.clone()
+            abi.s3_gemm(st, a, w, d, c=d if epi == 2 else None, epi=epi, workspace=work)
+            got = d
+        else:
+            seg = N // nseg
+            parts = [torch.full((M, seg), float("nan"), device="cuda", dtype=torch.bfloat16) for _ in range(nseg)]
+            abi.s3_gemm(st, a, w, parts, epi=epi, seg_cols=seg, workspace=work)
+            got = torch.cat(parts, dim=1)
+        torch.cuda.synchronize()
+        got = got.double()
+        assert torch.isfinite(got).all()
+        err = (got - ref).abs()
+        tol = 2.0 ** -8 * ref.abs() + 1e-3 * ref.abs().max() + 1e-6
+        bad = (err > tol).sum().item()
+        assert bad == 0, f"call {rep}: {bad} elements off; max err {err.max().item():.3e} (workspace {need} B)"
 
 
 def test_gemm_rejects_bad_shapes():

@@ -37,9 +37,10 @@ def main():
             a = torch.randn(M, K, device="cuda").to(torch.bfloat16)
             w = (torch.randn(N, K, device="cuda") / K ** 0.5).to(torch.bfloat16)
             d = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
+            ws = torch.zeros(max(abi.s3_gemm_workspace(M, N, K, epi=epi), 16), device="cuda", dtype=torch.uint8)
 
             def ours():
-                abi.s3_gemm(st, a, w, d, c=d if epi == 2 else None, epi=epi)
+                abi.s3_gemm(st, a, w, d, c=d if epi == 2 else None, epi=epi, workspace=ws)
 
             def cublas():
                 torch.matmul(a, w.T, out=d)
