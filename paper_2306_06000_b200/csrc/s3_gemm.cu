@@ -110,16 +110,36 @@ __device__ __forceinline__ float bf16_lo(uint32_t u) { return __uint_as_float(u 
 __device__ __forceinline__ float bf16_hi(uint32_t u) { return __uint_as_float(u & 0xffff0000u); }
 
 struct GemmMaps {
-  CUtensorMap a, w;
+  CUtensorMap a, w;      // operands (loads)
+  CUtensorMap d[3];      // output column segments (stores, box {64, 32})
+  CUtensorMap c;         // epi 2 addend (loads, box {64, 32})
+  CUtensorMap p;         // split-K fp32 partials (stores / loads, box {32, 32})
 };
 struct GemmArgs {
   int32_t M, N, K, epi, seg_cols, m_tiles, n_tiles;
   int32_t S;              // split-K factor (units = tiles x S)
-  uint16_t* d[3];
-  const uint16_t* c;
-  float* ws;              // S > 1: fp32 partial tiles [tile][split][rows][BN]
-  int32_t* cnt;           // S > 1: per (tile, CTA of the pair) arrival counters (zero between calls)
+  int32_t* cnt;           // S > 1: per (tile, CTA of the pair) [claim, done] counters (zero between calls)
 };
+__device__ __forceinline__ void g_tma_store2d(const CUtensorMap* map, int c0, int c1, const void* src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(map), "r"(c0),
+               "r"(c1), "r"(gsu32(src))
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+// 128B-swizzled staging tile of 32 rows x 128 B: 16-B chunk j of row r sits at chunk j ^ (r & 7)
+__device__ __forceinline__ uint32_t swz(int r, int j) { return (uint32_t)(r * 128 + ((j ^ (r & 7)) << 4)); }
+__device__ __forceinline__ void sts128(uint8_t* base, uint32_t off, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1,%2,%3,%4};" ::"r"(gsu32(base) + off), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ uint4 lds128(const uint8_t* base, uint32_t off) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(gsu32(base) + off)
+               : "memory");
+  return v;
+}
+constexpr int EPI_WARP_BYTES = 16384;   // per epilogue warp: 2 output + 2 input staging tiles of 4 KB
 
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
@@ -165,22 +185,27 @@ __device__ __forceinline__ void g_arrive_leader(uint64_t* b) {
 template <int BN, int CG>
 __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(const __grid_constant__ GemmMaps maps, GemmArgs a) {
   constexpr int A_BYTES = GM * GK * 2, W_BYTES = (BN / CG) * GK * 2, STAGE = A_BYTES + W_BYTES;
+  constexpr int NSTG = STAGE > 32768 ? 3 : GSTAGES;
   constexpr int TMEM_COLS = 2 * BN;
   constexpr int TM_ROWS = GM * CG;                     // rows per tile
   extern __shared__ __align__(1024) uint8_t gsmem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(gsmem_raw) + 1023) & ~(uintptr_t)1023);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + GSTAGES * STAGE);
-  uint64_t* empty = full + GSTAGES;
-  uint64_t* tfull = empty + GSTAGES;
+  uint8_t* epi_smem = smem + NSTG * STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi_smem + 4 * EPI_WARP_BYTES);
+  uint64_t* empty = full + NSTG;
+  uint64_t* tfull = empty + NSTG;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_base = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* inbar = tempty + 2;                        // [4 epilogue warps][2 input tiles]
+  uint32_t* tmem_base = reinterpret_cast<uint32_t*>(inbar + 8);
+  int32_t* s_role = reinterpret_cast<int32_t*>(tmem_base + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = CG == 2 ? cluster_rank() : 0;
   const bool leader = rank == 0;
   const int unit0 = (int)blockIdx.x / CG, nunits = (int)gridDim.x / CG;   // tile scheduler per CTA group
   if (threadIdx.x == 0) {
-    for (int i = 0; i < GSTAGES; ++i) { g_mb_init(&full[i], 1); g_mb_init(&empty[i], 1); }
+    for (int i = 0; i < NSTG; ++i) { g_mb_init(&full[i], 1); g_mb_init(&empty[i], 1); }
     for (int i = 0; i < 2; ++i) { g_mb_init(&tfull[i], 1); g_mb_init(&tempty[i], 4 * CG); }
+    for (int i = 0; i < 8; ++i) g_mb_init(&inbar[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.a) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&maps.w) : "memory");
@@ -232,7 +257,7 @@ __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(const __grid_constant__ G
             g_tma2d_pair(sa, &maps.a, kb * GK, m0, &full[s]);
             g_tma2d_pair(sa + A_BYTES, &maps.w, kb * GK, n0, &full[s]);
           }
-          if (++s == GSTAGES) { s = 0; ph ^= 1u; }
+          if (++s == NSTG) { s = 0; ph ^= 1u; }
         }
       }
     }
@@ -262,107 +287,176 @@ __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(const __grid_constant__ G
           }
           // the stage is free once these MMAs have read it (in both CTAs of a pair)
           if constexpr (CG == 1) g_commit(&empty[s]); else g_commit_pair(&empty[s]);
-          if (++s == GSTAGES) { s = 0; ph ^= 1u; }
+          if (++s == NSTG) { s = 0; ph ^= 1u; }
         }
         if constexpr (CG == 1) g_commit(&tfull[acc]); else g_commit_pair(&tfull[acc]);   // accumulator complete
       }
     }
   } else {
     // -------------------------------- epilogue --------------------------------
-    const int quarter = warp & 3;                      // TMEM lanes 32*quarter .. +31
-    const int row = quarter * 32 + lane;
-    __shared__ int s_last;
-    int it = 0;
-    for (int u = unit0; u < units; u += nunits, ++it) {
-      const int acc = it & 1;
-      const int t = u / a.S, split = u % a.S;
-      const int m0 = (t % a.m_tiles) * TM_ROWS + (int)rank * GM, n0 = (t / a.m_tiles) * BN;
-      g_mb_wait(&tfull[acc], (uint32_t)(it >> 1) & 1u);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const int m = m0 + row;
-      const int seg = n0 / a.seg_cols, col0 = n0 - seg * a.seg_cols;
-      uint16_t* drow = a.d[seg] + (int64_t)m * a.seg_cols + col0;
-      const uint16_t* crow = a.c ? a.c + (int64_t)m * a.N + n0 : nullptr;
-      // split-K: this split's fp32 partial rows; the last split of the tile to arrive sums them
-      float* prow = a.S > 1 ? a.ws + (((int64_t)t * a.S + split) * TM_ROWS + rank * GM + row) * BN : nullptr;
-      auto epilogue_store = [&](float (&v)[32], int c) {
-        if (a.epi == 1) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = gelu_tanh(v[i]);
-        } else if (a.epi == 2) {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const uint4 x = *reinterpret_cast<const uint4*>(crow + c + q * 8);
-            v[q * 8 + 0] += bf16_lo(x.x); v[q * 8 + 1] += bf16_hi(x.x);
-            v[q * 8 + 2] += bf16_lo(x.y); v[q * 8 + 3] += bf16_hi(x.y);
-            v[q * 8 + 4] += bf16_lo(x.z); v[q * 8 + 5] += bf16_hi(x.z);
-            v[q * 8 + 6] += bf16_lo(x.w); v[q * 8 + 7] += bf16_hi(x.w);
-          }
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          uint4 o;
-          o.x = pack_bf16(v[q * 8 + 0], v[q * 8 + 1]);
-          o.y = pack_bf16(v[q * 8 + 2], v[q * 8 + 3]);
-          o.z = pack_bf16(v[q * 8 + 4], v[q * 8 + 5]);
-          o.w = pack_bf16(v[q * 8 + 6], v[q * 8 + 7]);
-          *reinterpret_cast<uint4*>(drow + c + q * 8) = o;
-        }
-      };
-#pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        uint32_t r[32];
-        g_tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(acc * BN + c), r);
-        if (m < a.M) {
-          float v[32];
-#pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-          if (a.S == 1) {
-            epilogue_store(v, c);
-          } else {
-#pragma unroll
-            for (int q = 0; q < 8; ++q)
-              __stcg(reinterpret_cast<float4*>(prow + c) + q, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
-          }
-        }
+    // Warp w owns TMEM lanes 32 (w % 4) .. + 31 = 32 rows of the CTA's 128.  Values go
+    // TMEM -> registers -> a 128B-swizzled staging tile -> one TMA store per 32 x 64
+    // bf16 chunk (coalesced, asynchronous); addends and partials come in by TMA loads.
+    const int quarter = warp & 3;
+    uint8_t* eb = epi_smem + quarter * EPI_WARP_BYTES;
+    uint64_t* ib = inbar + quarter * 2;
+    uint32_t iph[2] = {0u, 0u};
+    int ob = 0;
+    const uint32_t tl = tmem + ((uint32_t)(quarter * 32) << 16);
+    auto load_in = [&](int buf, const CUtensorMap* map, int x, int y) {
+      if (lane == 0) {
+        g_mb_expect(&ib[buf], 4096u);
+        g_tma2d(eb + 8192 + buf * 4096, map, x, y, &ib[buf]);
       }
+    };
+    auto wait_in = [&](int buf) { g_mb_wait(&ib[buf], iph[buf]); iph[buf] ^= 1u; };
+    auto out_tile = [&]() -> uint8_t* {        // the staging tile a TMA store finished reading
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      __syncwarp();
+      return eb + ob * 4096;
+    };
+    auto store_out = [&](const CUtensorMap* map, int x, int y) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) g_tma_store2d(map, x, y, eb + ob * 4096);
+      ob ^= 1;
+    };
+    // 64 accumulator columns -> epilogue (C already summed in for epi 2 by the caller) -> bf16 store
+    auto finish64 = [&](float (&v)[64], const CUtensorMap* dmap, int x, int y) {
+      if (a.epi == 1) {
+#pragma unroll
+        for (int i = 0; i < 64; ++i) v[i] = gelu_tanh(v[i]);
+      }
+      uint8_t* o = out_tile();
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        sts128(o, swz(lane, j), make_uint4(pack_bf16(v[8 * j], v[8 * j + 1]), pack_bf16(v[8 * j + 2], v[8 * j + 3]),
+                                           pack_bf16(v[8 * j + 4], v[8 * j + 5]),
+                                           pack_bf16(v[8 * j + 6], v[8 * j + 7])));
+      store_out(dmap, x, y);
+    };
+    auto add_c = [&](float (&v)[64], int buf) {   // v += C tile in input buffer buf
+      wait_in(buf);
+      const uint8_t* cb = eb + 8192 + buf * 4096;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint4 x = lds128(cb, swz(lane, j));
+        v[8 * j + 0] += bf16_lo(x.x); v[8 * j + 1] += bf16_hi(x.x);
+        v[8 * j + 2] += bf16_lo(x.y); v[8 * j + 3] += bf16_hi(x.y);
+        v[8 * j + 4] += bf16_lo(x.z); v[8 * j + 5] += bf16_hi(x.z);
+        v[8 * j + 6] += bf16_lo(x.w); v[8 * j + 7] += bf16_hi(x.w);
+      }
+      __syncwarp();
+    };
+    auto add_p = [&](float* v, int buf) {         // 32 values += fp32 partial tile in input buffer buf
+      wait_in(buf);
+      const uint8_t* pb = eb + 8192 + buf * 4096;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint4 x = lds128(pb, swz(lane, j));
+        v[4 * j + 0] += __uint_as_float(x.x); v[4 * j + 1] += __uint_as_float(x.y);
+        v[4 * j + 2] += __uint_as_float(x.z); v[4 * j + 3] += __uint_as_float(x.w);
+      }
+      __syncwarp();
+    };
+    auto tmem_ld64 = [&](int col, float (&v)[64]) {
+      uint32_t r[32];
+      g_tmem_ld32(tl + (uint32_t)col, r);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+      g_tmem_ld32(tl + (uint32_t)(col + 32), r);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) v[32 + i] = __uint_as_float(r[i]);
+    };
+    auto release = [&](int acc) {
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) {
         if constexpr (CG == 1) g_mb_arrive(&tempty[acc]); else g_arrive_leader(&tempty[acc]);
       }
-      if (a.S > 1) {
-        // every epilogue thread's partial is written; one atomic per (tile, CTA) says how many splits are in
-        __threadfence();
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (threadIdx.x == 64) {
-          int* cn = a.cnt + t * CG + rank;
-          const int old = atomicAdd(cn, 1);
-          s_last = old == a.S - 1;
-          if (old == a.S - 1) *cn = 0;                  // reset for the next call (stream order)
-          __threadfence();
-        }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (s_last && m < a.M) {
-          const float* p0 = a.ws + ((int64_t)t * a.S * TM_ROWS + rank * GM + row) * BN;
+    };
+    int it = 0;
+    for (int u = unit0; u < units; u += nunits, ++it) {
+      const int acc = it & 1;
+      const int t = u / a.S;
+      const int y = (t % a.m_tiles) * TM_ROWS + (int)rank * GM + quarter * 32;   // first row of this warp
+      const int n0 = (t / a.m_tiles) * BN;
+      const int seg = n0 / a.seg_cols, x0 = n0 - seg * a.seg_cols;
+      const CUtensorMap* dmap = &maps.d[seg];
+      g_mb_wait(&tfull[acc], (uint32_t)(it >> 1) & 1u);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (a.S == 1) {
+        if (a.epi == 2) load_in(0, &maps.c, n0, y);
 #pragma unroll 1
-          for (int c = 0; c < BN; c += 32) {
-            float v[32];
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = 0.f;
-            for (int j = 0; j < a.S; ++j) {
-              const float4* pj = reinterpret_cast<const float4*>(p0 + (int64_t)j * TM_ROWS * BN + c);
-#pragma unroll
-              for (int q = 0; q < 8; ++q) {
-                const float4 x = __ldcg(pj + q);
-                v[4 * q] += x.x; v[4 * q + 1] += x.y; v[4 * q + 2] += x.z; v[4 * q + 3] += x.w;
-              }
-            }
-            epilogue_store(v, c);
-          }
+        for (int c = 0, i = 0; c < BN; c += 64, ++i) {
+          if (a.epi == 2 && c + 64 < BN) load_in((i + 1) & 1, &maps.c, n0 + c + 64, y);   // prefetch the next
+          float v[64];
+          tmem_ld64(acc * BN + c, v);
+          if (c + 64 >= BN) release(acc);
+          if (a.epi == 2) add_c(v, i & 1);
+          finish64(v, dmap, x0 + c, y);
         }
+        continue;
       }
+      // ---- split-K: the last split of (tile, CTA) to arrive reduces; the others
+      // store fp32 partials into slots 0..S-2 (claim order) ----
+      int32_t* claim = a.cnt + 2 * (t * CG + (int)rank);
+      if (threadIdx.x == 64) *s_role = atomicAdd(claim, 1);
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      const int role = *s_role;
+      if (role < a.S - 1) {
+        const int prow = (t * (a.S - 1) + role) * TM_ROWS + (int)rank * GM + quarter * 32;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t r[32];
+          g_tmem_ld32(tl + (uint32_t)(acc * BN + c), r);
+          if (c + 32 >= BN) release(acc);
+          uint8_t* o = out_tile();
+#pragma unroll
+          for (int j = 0; j < 8; ++j) sts128(o, swz(lane, j), make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]));
+          store_out(&maps.p, c, prow);
+        }
+        if (lane == 0) {                               // partial in HBM/L2, then count this warp in
+          asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(claim + 1) : "memory");
+        }
+      } else {
+        if (lane == 0) {                               // every other split's 4 warps stored their partial
+          const int want = 4 * (a.S - 1);
+          for (;;) {
+            int v;
+            asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(claim + 1) : "memory");
+            if (v >= want) break;
+            __nanosleep(64);
+          }
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+        }
+        __syncwarp();
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 64) {
+          float v[64];
+          tmem_ld64(acc * BN + c, v);
+          if (c + 64 >= BN) release(acc);
+          for (int j = 0; j < a.S - 1; ++j) {
+            const int prow = (t * (a.S - 1) + j) * TM_ROWS + (int)rank * GM + quarter * 32;
+            load_in(0, &maps.p, c, prow);
+            load_in(1, &maps.p, c + 32, prow);
+            add_p(v, 0);
+            add_p(v + 32, 1);
+          }
+          if (a.epi == 2) {
+            load_in(0, &maps.c, n0 + c, y);
+            add_c(v, 0);
+          }
+          finish64(v, dmap, x0 + c, y);
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");   // all four warps saw the counts
+        if (threadIdx.x == 64) { claim[0] = 0; claim[1] = 0; }   // reusable by the next call
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");     // s_role is read; the next tile may claim
     }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   if constexpr (CG == 2) cluster_sync_all(); else __syncthreads();   // the pair's MMAs are done with both CTAs
@@ -404,7 +498,23 @@ bool encode_kmajor(CUtensorMap* m, const void* base, uint64_t rows, uint64_t K, 
 
 template <int BN, int CG>
 int gemm_smem() {
-  return GSTAGES * (GM * GK * 2 + (BN / CG) * GK * 2) + 1024 + 256;
+  constexpr int STAGE = GM * GK * 2 + (BN / CG) * GK * 2;
+  constexpr int NSTG = STAGE > 32768 ? 3 : GSTAGES;
+  return NSTG * STAGE + 4 * EPI_WARP_BYTES + 1024 + 256;
+}
+
+// bf16 or fp32 row-major [rows][cols] map with a {box_cols, 32}-row box, 128B swizzle (TMA store / load)
+bool encode_rows(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, int fp32, uint32_t box_cols) {
+  GEncodeFn enc = g_encoder();
+  if (!enc) return false;
+  const uint64_t es = fp32 ? 4 : 2;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * es};
+  cuuint32_t box[2] = {box_cols, 32};
+  cuuint32_t el[2] = {1, 1};
+  return enc(m, fp32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base),
+             dims, strides, box, el, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 template <int BN, int CG>
@@ -458,17 +568,22 @@ int gemm_num_sms() {
 // Split-K factor: estimated time (in K blocks) = waves x (K blocks per split +
 // pipeline fill) + the last split's reduction; S = 1 unless splitting fills
 // idle SMs.  Needs S x tiles x rows x BN fp32 + counters of workspace.
+// split-K scratch: S - 1 fp32 partial tiles per output tile, then [claim, done] per (tile, CTA)
+int64_t gemm_ws_bytes(int S, int tiles, int rows, int BN) {
+  return (int64_t)(S - 1) * tiles * rows * BN * 4 + (int64_t)tiles * 2 * 2 * 4;
+}
+
 int gemm_splits(int tiles, int groups, int kblocks, int rows, int BN, int64_t ws_bytes) {
   static const int force = [] { const char* e = getenv("S3_GEMM_S"); return e ? atoi(e) : 0; }();
   if (force > 0) {
     const int S = std::min(force, std::max(1, kblocks / 4));
-    return (int64_t)S * tiles * rows * BN * 4 + (int64_t)tiles * 2 * 4 <= ws_bytes ? S : 1;
+    return gemm_ws_bytes(S, tiles, rows, BN) <= ws_bytes ? S : 1;
   }
   int best = 1;
   double best_t = 1e30;
   for (int S = 1; S <= 8; ++S) {
     if (S > 1 && kblocks / S < 8) break;
-    if (S > 1 && (int64_t)S * tiles * rows * BN * 4 + (int64_t)tiles * 2 * 4 > ws_bytes) break;
+    if (S > 1 && gemm_ws_bytes(S, tiles, rows, BN) > ws_bytes) break;
     const int waves = (tiles * S + groups - 1) / groups;
     // a split writes its fp32 partial (~7 K blocks of time) and the last one reads S of them
     const double t = waves * ((double)kblocks / S + 3.0 + (S > 1 ? 7.0 : 0.0)) + (S > 1 ? 7.0 * S : 0.0);
@@ -498,7 +613,7 @@ bool gemm_plan(const GemmCall& g, int64_t ws_avail, GemmPlan& p) {
   p.BN = p.CG == 2 ? 256 : (n256 && (int64_t)p.m_tiles * (g.N / 256) >= sms ? 256 : 128);
   p.tiles = p.m_tiles * (g.N / p.BN);
   p.S = gemm_splits(p.tiles, sms / p.CG, g.K / GK, p.rows, p.BN, ws_avail);
-  p.ws_bytes = p.S > 1 ? (int64_t)p.S * p.tiles * p.rows * p.BN * 4 + (int64_t)p.tiles * 2 * 4 : 0;
+  p.ws_bytes = p.S > 1 ? gemm_ws_bytes(p.S, p.tiles, p.rows, p.BN) : 0;
   return true;
 }
 
@@ -514,14 +629,23 @@ cudaError_t launch_gemm(const GemmCall& g, cudaStream_t st) {
   GemmMaps maps;
   if (!encode_kmajor(&maps.a, g.a, (uint64_t)g.M, (uint64_t)g.K, GM)) return cudaErrorInvalidValue;
   if (!encode_kmajor(&maps.w, g.w, (uint64_t)g.N, (uint64_t)g.K, (uint32_t)(p.BN / p.CG))) return cudaErrorInvalidValue;
+  const int nseg = g.N / g.seg_cols;
+  for (int i = 0; i < 3; ++i) {
+    const void* base = g.d[i < nseg ? i : 0];
+    if (i < nseg && !g.d[i]) return cudaErrorInvalidValue;
+    if (!encode_rows(&maps.d[i], base, (uint64_t)g.M, (uint64_t)g.seg_cols, 0, 64)) return cudaErrorInvalidValue;
+  }
+  maps.c = maps.d[0];
+  if (g.epi == 2 && !encode_rows(&maps.c, g.c, (uint64_t)g.M, (uint64_t)g.N, 0, 64)) return cudaErrorInvalidValue;
+  maps.p = maps.d[0];
+  if (p.S > 1 && !encode_rows(&maps.p, g.workspace, (uint64_t)p.tiles * (p.S - 1) * p.rows, (uint64_t)p.BN, 1, 32))
+    return cudaErrorInvalidValue;
   GemmArgs a;
   a.M = g.M; a.N = g.N; a.K = g.K; a.epi = g.epi; a.seg_cols = g.seg_cols;
   a.m_tiles = p.m_tiles; a.n_tiles = g.N / p.BN;
-  for (int i = 0; i < 3; ++i) a.d[i] = static_cast<uint16_t*>(g.d[i] ? g.d[i] : g.d[0]);
-  a.c = static_cast<const uint16_t*>(g.c);
   a.S = p.S;
-  a.ws = static_cast<float*>(g.workspace);
-  a.cnt = p.S > 1 ? reinterpret_cast<int32_t*>(static_cast<uint8_t*>(g.workspace) + p.ws_bytes - (int64_t)p.tiles * 2 * 4)
+  a.cnt = p.S > 1 ? reinterpret_cast<int32_t*>(static_cast<uint8_t*>(g.workspace) + p.ws_bytes -
+                                               (int64_t)p.tiles * 2 * 2 * 4)
                   : nullptr;
   const int groups = std::min(p.tiles * p.S, gemm_num_sms() / p.CG);
   cudaError_t e;
