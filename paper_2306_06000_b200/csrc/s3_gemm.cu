@@ -117,8 +117,44 @@ struct GemmMaps {
 };
 struct GemmArgs {
   int32_t M, N, K, epi, seg_cols, m_tiles, n_tiles;
-  int32_t S;              // split-K factor (units = tiles x S)
-  int32_t* cnt;           // S > 1: per (tile, CTA of the pair) [claim, done] counters (zero between calls)
+  int32_t sk;             // 0: data parallel (whole tiles); 1: stream-K (equal K-block ranges per CTA group)
+  int32_t cmax;           // stream-K: most CTA groups contributing to one tile (partial slots = cmax - 1)
+  int32_t* cnt;           // stream-K: per (tile, CTA of the pair) [claim, done] counters (zero between calls)
+};
+
+// Work of one CTA group: whole tiles g, g + G, ... (data parallel), or the
+// K blocks [start(g), start(g+1)) of the tile-major K-block sequence
+// (stream-K), cut at tile boundaries.  A tile touched by several groups
+// (ncontrib > 1) is summed by the last group to finish its part.
+struct Work {
+  int tile, kb0, kb1, ncontrib;
+};
+struct WorkIter {
+  int64_t pos, end, total;
+  int G, g, kblocks, sk;
+  __device__ int64_t start(int grp) const { return (int64_t)grp * total / G; }
+  __device__ int group_of(int64_t x) const {   // the group whose range holds K block x
+    int grp = (int)(x * G / total);
+    while (grp + 1 < G && start(grp + 1) <= x) ++grp;
+    while (grp > 0 && start(grp) > x) --grp;
+    return grp;
+  }
+  __device__ bool next(Work& w) {
+    if (!sk) {
+      if (pos >= end) return false;
+      w.tile = (int)pos; w.kb0 = 0; w.kb1 = kblocks; w.ncontrib = 1;
+      pos += G;
+      return true;
+    }
+    if (pos >= end) return false;
+    w.tile = (int)(pos / kblocks);
+    w.kb0 = (int)(pos - (int64_t)w.tile * kblocks);
+    const int64_t rest = (int64_t)w.kb0 + (end - pos);
+    w.kb1 = rest < kblocks ? (int)rest : kblocks;
+    w.ncontrib = group_of((int64_t)(w.tile + 1) * kblocks - 1) - group_of((int64_t)w.tile * kblocks) + 1;
+    pos += w.kb1 - w.kb0;
+    return true;
+  }
 };
 __device__ __forceinline__ void g_tma_store2d(const CUtensorMap* map, int c0, int c1, const void* src) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(map), "r"(c0),
@@ -225,13 +261,15 @@ __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(const __grid_constant__ G
   if constexpr (CG == 2) cluster_sync_all(); else __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_base;
-  const int units = a.m_tiles * a.n_tiles * a.S;
+  const int tiles = a.m_tiles * a.n_tiles;
   const int kblocks = a.K / GK;
-  // unit u = (tile u / S, split u % S); split j covers K blocks [j kblocks / S, (j + 1) kblocks / S)
-  auto krange = [&](int u, int& kb0, int& kb1) {
-    const int j = u % a.S;
-    kb0 = (int)((int64_t)j * kblocks / a.S);
-    kb1 = (int)((int64_t)(j + 1) * kblocks / a.S);
+  auto work = [&]() {
+    WorkIter w;
+    w.G = nunits; w.g = unit0; w.kblocks = kblocks; w.sk = a.sk;
+    w.total = (int64_t)tiles * kblocks;
+    if (a.sk) { w.pos = w.start(unit0); w.end = w.start(unit0 + 1); }
+    else { w.pos = unit0; w.end = tiles; }
+    return w;
   };
 
   if (warp == 0) {
@@ -239,13 +277,12 @@ __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(const __grid_constant__ G
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
-      for (int u = unit0; u < units; u += nunits) {
-        const int t = u / a.S;
+      WorkIter wi = work();
+      for (Work wk; wi.next(wk);) {
+        const int t = wk.tile;
         const int m0 = (t % a.m_tiles) * TM_ROWS + (int)rank * GM;
         const int n0 = (t / a.m_tiles) * BN + (int)rank * (BN / CG);
-        int kb0, kb1;
-        krange(u, kb0, kb1);
-        for (int kb = kb0; kb < kb1; ++kb) {
+        for (int kb = wk.kb0; kb < wk.kb1; ++kb) {
           g_mb_wait(&empty[s], ph ^ 1u);
           uint8_t* sa = smem + s * STAGE;
           if constexpr (CG == 1) {
@@ -268,13 +305,13 @@ __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(const __grid_constant__ G
       int s = 0;
       uint32_t ph = 0;
       int it = 0;
-      for (int u = unit0; u < units; u += nunits, ++it) {
+      WorkIter wi = work();
+      for (Work wk; wi.next(wk); ++it) {
         const int acc = it & 1;
         g_mb_wait(&tempty[acc], ((uint32_t)(it >> 1) & 1u) ^ 1u);   // the epilogue(s) drained this accumulator
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t d = tmem + (uint32_t)(acc * BN);
-        int kb0, kb1;
-        krange(u, kb0, kb1);
+        const int kb0 = wk.kb0, kb1 = wk.kb1;
         for (int kb = kb0; kb < kb1; ++kb) {
           g_mb_wait(&full[s], ph);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -376,16 +413,18 @@ __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(const __grid_constant__ G
       }
     };
     int it = 0;
-    for (int u = unit0; u < units; u += nunits, ++it) {
+    WorkIter wi = work();
+    for (Work wk; wi.next(wk); ++it) {
       const int acc = it & 1;
-      const int t = u / a.S;
+      const int t = wk.tile;
+      const int S = wk.ncontrib;
       const int y = (t % a.m_tiles) * TM_ROWS + (int)rank * GM + quarter * 32;   // first row of this warp
       const int n0 = (t / a.m_tiles) * BN;
       const int seg = n0 / a.seg_cols, x0 = n0 - seg * a.seg_cols;
       const CUtensorMap* dmap = &maps.d[seg];
       g_mb_wait(&tfull[acc], (uint32_t)(it >> 1) & 1u);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      if (a.S == 1) {
+      if (S == 1) {
         if (a.epi == 2) load_in(0, &maps.c, n0, y);
 #pragma unroll 1
         for (int c = 0, i = 0; c < BN; c += 64, ++i) {
@@ -398,14 +437,14 @@ __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(const __grid_constant__ G
         }
         continue;
       }
-      // ---- split-K: the last split of (tile, CTA) to arrive reduces; the others
-      // store fp32 partials into slots 0..S-2 (claim order) ----
+      // ---- several groups share this tile: the last of (tile, CTA) to arrive reduces;
+      // the others store fp32 partials into slots 0..S-2 (claim order) ----
       int32_t* claim = a.cnt + 2 * (t * CG + (int)rank);
       if (threadIdx.x == 64) *s_role = atomicAdd(claim, 1);
       asm volatile("bar.sync 1, 128;" ::: "memory");
       const int role = *s_role;
-      if (role < a.S - 1) {
-        const int prow = (t * (a.S - 1) + role) * TM_ROWS + (int)rank * GM + quarter * 32;
+      if (role < S - 1) {
+        const int prow = (t * (a.cmax - 1) + role) * TM_ROWS + (int)rank * GM + quarter * 32;
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
           uint32_t r[32];
@@ -423,7 +462,7 @@ __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(const __grid_constant__ G
         }
       } else {
         if (lane == 0) {                               // every other split's 4 warps stored their partial
-          const int want = 4 * (a.S - 1);
+          const int want = 4 * (S - 1);
           for (;;) {
             int v;
             asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(claim + 1) : "memory");
@@ -438,8 +477,8 @@ __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(const __grid_constant__ G
           float v[64];
           tmem_ld64(acc * BN + c, v);
           if (c + 64 >= BN) release(acc);
-          for (int j = 0; j < a.S - 1; ++j) {
-            const int prow = (t * (a.S - 1) + j) * TM_ROWS + (int)rank * GM + quarter * 32;
+          for (int j = 0; j < S - 1; ++j) {
+            const int prow = (t * (a.cmax - 1) + j) * TM_ROWS + (int)rank * GM + quarter * 32;
             load_in(0, &maps.p, c, prow);
             load_in(1, &maps.p, c + 32, prow);
             add_p(v, 0);
@@ -568,36 +607,33 @@ int gemm_num_sms() {
 // Split-K factor: estimated time (in K blocks) = waves x (K blocks per split +
 // pipeline fill) + the last split's reduction; S = 1 unless splitting fills
 // idle SMs.  Needs S x tiles x rows x BN fp32 + counters of workspace.
-// split-K scratch: S - 1 fp32 partial tiles per output tile, then [claim, done] per (tile, CTA)
-int64_t gemm_ws_bytes(int S, int tiles, int rows, int BN) {
-  return (int64_t)(S - 1) * tiles * rows * BN * 4 + (int64_t)tiles * 2 * 2 * 4;
+// Stream-K partition: group g owns K blocks [g T / G, (g+1) T / G) of the T =
+// tiles x kblocks sequence.  Most groups sharing one tile:
+int sk_cmax(int tiles, int kblocks, int G) {
+  const int64_t T = (int64_t)tiles * kblocks;
+  auto start = [&](int g) { return (int64_t)g * T / G; };
+  auto group_of = [&](int64_t x) {
+    int g = (int)(x * G / T);
+    while (g + 1 < G && start(g + 1) <= x) ++g;
+    while (g > 0 && start(g) > x) --g;
+    return g;
+  };
+  int c = 1;
+  for (int t = 0; t < tiles; ++t)
+    c = std::max(c, group_of((int64_t)(t + 1) * kblocks - 1) - group_of((int64_t)t * kblocks) + 1);
+  return c;
 }
-
-int gemm_splits(int tiles, int groups, int kblocks, int rows, int BN, int64_t ws_bytes) {
-  static const int force = [] { const char* e = getenv("S3_GEMM_S"); return e ? atoi(e) : 0; }();
-  if (force > 0) {
-    const int S = std::min(force, std::max(1, kblocks / 4));
-    return gemm_ws_bytes(S, tiles, rows, BN) <= ws_bytes ? S : 1;
-  }
-  int best = 1;
-  double best_t = 1e30;
-  for (int S = 1; S <= 8; ++S) {
-    if (S > 1 && kblocks / S < 8) break;
-    if (S > 1 && gemm_ws_bytes(S, tiles, rows, BN) > ws_bytes) break;
-    const int waves = (tiles * S + groups - 1) / groups;
-    // a split writes its fp32 partial (~7 K blocks of time) and the last one reads S of them
-    const double t = waves * ((double)kblocks / S + 3.0 + (S > 1 ? 7.0 : 0.0)) + (S > 1 ? 7.0 * S : 0.0);
-    if (t < best_t * 0.97) { best_t = t; best = S; }
-  }
-  return best;
+// stream-K scratch: cmax - 1 fp32 partial tiles per output tile, then [claim, done] per (tile, CTA)
+int64_t gemm_ws_bytes(int cmax, int tiles, int rows, int BN, int CG) {
+  return (int64_t)(cmax - 1) * tiles * rows * BN * 4 + (int64_t)tiles * CG * 2 * 4;
 }
 
 // Tile choice: a CTA pair per 256 x 256 tile (half the operand traffic per
 // flop) when M > 128; one CTA per 128 x 256 tile for a single row tile; 128
 // columns when 256-wide tiles would leave SMs idle.  Then the split-K factor.
 struct GemmPlan {
-  int CG, BN, rows, m_tiles, tiles, S;
-  int64_t ws_bytes;   // workspace the plan needs (0 when S = 1)
+  int CG, BN, rows, m_tiles, tiles, groups, sk, cmax;
+  int64_t ws_bytes;   // workspace the plan needs (0 for data-parallel)
 };
 bool gemm_plan(const GemmCall& g, int64_t ws_avail, GemmPlan& p) {
   if (g.M < 1 || g.N < 128 || g.K < GK || g.K % GK || g.N % 128 || g.seg_cols < 128 || g.seg_cols % 128 ||
@@ -605,15 +641,30 @@ bool gemm_plan(const GemmCall& g, int64_t ws_avail, GemmPlan& p) {
     return false;
   const int sms = gemm_num_sms();
   const bool n256 = g.N % 256 == 0 && g.seg_cols % 256 == 0;
-  static const int force = [] { const char* e = getenv("S3_GEMM_CG"); return e ? atoi(e) : 0; }();
-  p.CG = force ? force : (g.M > GM && n256 ? 2 : 1);
+  static const int force_cg = [] { const char* e = getenv("S3_GEMM_CG"); return e ? atoi(e) : 0; }();
+  static const int force_sk = [] { const char* e = getenv("S3_GEMM_SK"); return e ? atoi(e) : -1; }();
+  p.CG = force_cg ? force_cg : (g.M > GM && n256 ? 2 : 1);
   if (p.CG == 2 && !n256) return false;
   p.rows = GM * p.CG;
   p.m_tiles = (g.M + p.rows - 1) / p.rows;
+  const int G = sms / p.CG;
   p.BN = p.CG == 2 ? 256 : (n256 && (int64_t)p.m_tiles * (g.N / 256) >= sms ? 256 : 128);
   p.tiles = p.m_tiles * (g.N / p.BN);
-  p.S = gemm_splits(p.tiles, sms / p.CG, g.K / GK, p.rows, p.BN, ws_avail);
-  p.ws_bytes = p.S > 1 ? gemm_ws_bytes(p.S, p.tiles, p.rows, p.BN) : 0;
+  const int kblocks = g.K / GK;
+  // data parallel unless its last wave leaves > 10 % of the groups idle and every group
+  // would still get >= 8 K blocks of a balanced stream-K partition
+  const int waves = (p.tiles + G - 1) / G;
+  const double dp_eff = (double)p.tiles / ((double)waves * G);
+  p.sk = force_sk >= 0 ? force_sk : (dp_eff < 0.9 && (int64_t)p.tiles * kblocks >= 8LL * G);
+  p.cmax = 1;
+  p.ws_bytes = 0;
+  if (p.sk) {
+    p.cmax = sk_cmax(p.tiles, kblocks, G);
+    p.ws_bytes = gemm_ws_bytes(p.cmax, p.tiles, p.rows, p.BN, p.CG);
+    if (p.cmax == 1 || p.ws_bytes > ws_avail) { p.sk = 0; p.cmax = 1; p.ws_bytes = p.cmax > 1 ? p.ws_bytes : 0; }
+  }
+  if (!p.sk) p.ws_bytes = 0;
+  p.groups = p.sk ? G : std::min(p.tiles, G);
   return true;
 }
 
@@ -638,16 +689,17 @@ cudaError_t launch_gemm(const GemmCall& g, cudaStream_t st) {
   maps.c = maps.d[0];
   if (g.epi == 2 && !encode_rows(&maps.c, g.c, (uint64_t)g.M, (uint64_t)g.N, 0, 64)) return cudaErrorInvalidValue;
   maps.p = maps.d[0];
-  if (p.S > 1 && !encode_rows(&maps.p, g.workspace, (uint64_t)p.tiles * (p.S - 1) * p.rows, (uint64_t)p.BN, 1, 32))
+  if (p.sk && !encode_rows(&maps.p, g.workspace, (uint64_t)p.tiles * (p.cmax - 1) * p.rows, (uint64_t)p.BN, 1, 32))
     return cudaErrorInvalidValue;
   GemmArgs a;
   a.M = g.M; a.N = g.N; a.K = g.K; a.epi = g.epi; a.seg_cols = g.seg_cols;
   a.m_tiles = p.m_tiles; a.n_tiles = g.N / p.BN;
-  a.S = p.S;
-  a.cnt = p.S > 1 ? reinterpret_cast<int32_t*>(static_cast<uint8_t*>(g.workspace) + p.ws_bytes -
-                                               (int64_t)p.tiles * 2 * 2 * 4)
-                  : nullptr;
-  const int groups = std::min(p.tiles * p.S, gemm_num_sms() / p.CG);
+  a.sk = p.sk;
+  a.cmax = p.cmax;
+  a.cnt = p.sk ? reinterpret_cast<int32_t*>(static_cast<uint8_t*>(g.workspace) + p.ws_bytes -
+                                            (int64_t)p.tiles * p.CG * 2 * 4)
+               : nullptr;
+  const int groups = p.groups;
   cudaError_t e;
   if (p.CG == 2) e = launch_one<256, 2>(maps, a, 2 * groups, st);
   else if (p.BN == 256) e = launch_one<256, 1>(maps, a, groups, st);
