@@ -117,41 +117,49 @@ struct GemmMaps {
 };
 struct GemmArgs {
   int32_t M, N, K, epi, seg_cols, m_tiles, n_tiles;
-  int32_t sk;             // 0: data parallel (whole tiles); 1: stream-K (equal K-block ranges per CTA group)
+  int32_t dp_tiles;       // tiles [0, dp_tiles) data parallel, the rest stream-K (equal K-block ranges per group)
   int32_t cmax;           // stream-K: most CTA groups contributing to one tile (partial slots = cmax - 1)
   int32_t* cnt;           // stream-K: per (tile, CTA of the pair) [claim, done] counters (zero between calls)
 };
 
-// Work of one CTA group: whole tiles g, g + G, ... (data parallel), or the
-// K blocks [start(g), start(g+1)) of the tile-major K-block sequence
-// (stream-K), cut at tile boundaries.  A tile touched by several groups
-// (ncontrib > 1) is summed by the last group to finish its part.
+// Work of one CTA group: whole tiles g, g + G, ... below dp_tiles (data
+// parallel, n-major, so neighbouring groups share W blocks in L2), then --
+// stream-K -- the K blocks [start(g), start(g+1)) of the remaining tiles'
+// tile-major K-block sequence, cut at tile boundaries.  A tile touched by
+// several groups (ncontrib > 1) is summed by the last group to finish its part.
 struct Work {
   int tile, kb0, kb1, ncontrib;
 };
 struct WorkIter {
-  int64_t pos, end, total;
-  int G, g, kblocks, sk;
-  __device__ int64_t start(int grp) const { return (int64_t)grp * total / G; }
-  __device__ int group_of(int64_t x) const {   // the group whose range holds K block x
+  int64_t dp_pos, pos, end, total;     // total: K blocks of the stream-K tiles
+  int G, kblocks, dp_tiles;
+  __host__ __device__ int64_t start(int grp) const { return (int64_t)grp * total / G; }
+  __host__ __device__ int group_of(int64_t x) const {   // the group whose stream-K range holds K block x
     int grp = (int)(x * G / total);
     while (grp + 1 < G && start(grp + 1) <= x) ++grp;
     while (grp > 0 && start(grp) > x) --grp;
     return grp;
   }
-  __device__ bool next(Work& w) {
-    if (!sk) {
-      if (pos >= end) return false;
-      w.tile = (int)pos; w.kb0 = 0; w.kb1 = kblocks; w.ncontrib = 1;
-      pos += G;
+  __host__ __device__ void init(int g, int groups, int tiles, int kb, int dp) {
+    G = groups; kblocks = kb; dp_tiles = dp;
+    dp_pos = g;
+    total = (int64_t)(tiles - dp) * kb;
+    pos = total ? start(g) : 0;
+    end = total ? start(g + 1) : 0;
+  }
+  __host__ __device__ bool next(Work& w) {
+    if (dp_pos < dp_tiles) {
+      w.tile = (int)dp_pos; w.kb0 = 0; w.kb1 = kblocks; w.ncontrib = 1;
+      dp_pos += G;
       return true;
     }
     if (pos >= end) return false;
-    w.tile = (int)(pos / kblocks);
-    w.kb0 = (int)(pos - (int64_t)w.tile * kblocks);
+    const int st = (int)(pos / kblocks);
+    w.tile = dp_tiles + st;
+    w.kb0 = (int)(pos - (int64_t)st * kblocks);
     const int64_t rest = (int64_t)w.kb0 + (end - pos);
     w.kb1 = rest < kblocks ? (int)rest : kblocks;
-    w.ncontrib = group_of((int64_t)(w.tile + 1) * kblocks - 1) - group_of((int64_t)w.tile * kblocks) + 1;
+    w.ncontrib = group_of((int64_t)(st + 1) * kblocks - 1) - group_of((int64_t)st * kblocks) + 1;
     pos += w.kb1 - w.kb0;
     return true;
   }
@@ -265,10 +273,7 @@ __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(const __grid_constant__ G
   const int kblocks = a.K / GK;
   auto work = [&]() {
     WorkIter w;
-    w.G = nunits; w.g = unit0; w.kblocks = kblocks; w.sk = a.sk;
-    w.total = (int64_t)tiles * kblocks;
-    if (a.sk) { w.pos = w.start(unit0); w.end = w.start(unit0 + 1); }
-    else { w.pos = unit0; w.end = tiles; }
+    w.init(unit0, nunits, tiles, kblocks, a.dp_tiles);
     return w;
   };
 
@@ -607,20 +612,13 @@ int gemm_num_sms() {
 // Split-K factor: estimated time (in K blocks) = waves x (K blocks per split +
 // pipeline fill) + the last split's reduction; S = 1 unless splitting fills
 // idle SMs.  Needs S x tiles x rows x BN fp32 + counters of workspace.
-// Stream-K partition: group g owns K blocks [g T / G, (g+1) T / G) of the T =
-// tiles x kblocks sequence.  Most groups sharing one tile:
-int sk_cmax(int tiles, int kblocks, int G) {
-  const int64_t T = (int64_t)tiles * kblocks;
-  auto start = [&](int g) { return (int64_t)g * T / G; };
-  auto group_of = [&](int64_t x) {
-    int g = (int)(x * G / T);
-    while (g + 1 < G && start(g + 1) <= x) ++g;
-    while (g > 0 && start(g) > x) --g;
-    return g;
-  };
+// Most groups sharing one stream-K tile
+int sk_cmax(int tiles, int kblocks, int G, int dp_tiles) {
+  WorkIter w;
+  w.init(0, G, tiles, kblocks, dp_tiles);
   int c = 1;
-  for (int t = 0; t < tiles; ++t)
-    c = std::max(c, group_of((int64_t)(t + 1) * kblocks - 1) - group_of((int64_t)t * kblocks) + 1);
+  for (int st = 0; st < tiles - dp_tiles; ++st)
+    c = std::max(c, w.group_of((int64_t)(st + 1) * kblocks - 1) - w.group_of((int64_t)st * kblocks) + 1);
   return c;
 }
 // stream-K scratch: cmax - 1 fp32 partial tiles per output tile, then [claim, done] per (tile, CTA)
@@ -632,7 +630,7 @@ int64_t gemm_ws_bytes(int cmax, int tiles, int rows, int BN, int CG) {
 // flop) when M > 128; one CTA per 128 x 256 tile for a single row tile; 128
 // columns when 256-wide tiles would leave SMs idle.  Then the split-K factor.
 struct GemmPlan {
-  int CG, BN, rows, m_tiles, tiles, groups, sk, cmax;
+  int CG, BN, rows, m_tiles, tiles, groups, sk, dp_tiles, cmax;
   int64_t ws_bytes;   // workspace the plan needs (0 for data-parallel)
 };
 bool gemm_plan(const GemmCall& g, int64_t ws_avail, GemmPlan& p) {
@@ -655,16 +653,23 @@ bool gemm_plan(const GemmCall& g, int64_t ws_avail, GemmPlan& p) {
   // would still get >= 8 K blocks of a balanced stream-K partition
   const int waves = (p.tiles + G - 1) / G;
   const double dp_eff = (double)p.tiles / ((double)waves * G);
-  p.sk = force_sk >= 0 ? force_sk : (dp_eff < 0.9 && (int64_t)p.tiles * kblocks >= 8LL * G);
+  // stream-K covers the ragged last wave merged with one full wave (so every group gets
+  // >= 1 tile of work); the waves before it stay data parallel
+  const int rem = p.tiles % G;
+  const int sk_tiles = rem == 0 ? 0 : (p.tiles >= G ? rem + G : p.tiles);
+  p.sk = force_sk >= 0 ? force_sk : (dp_eff < 0.9 && sk_tiles > 0 && (int64_t)sk_tiles * kblocks >= 8LL * G);
+  if (p.sk && force_sk > 0 && sk_tiles == 0) p.sk = 0;
+  p.dp_tiles = p.sk ? p.tiles - (sk_tiles ? sk_tiles : p.tiles) : p.tiles;
   p.cmax = 1;
   p.ws_bytes = 0;
+  // every stream-K group owns >= 1 K block (empty ranges would not count as contributors)
+  const int Gs = p.sk ? (int)std::min<int64_t>(G, (int64_t)(p.tiles - p.dp_tiles) * kblocks) : G;
   if (p.sk) {
-    p.cmax = sk_cmax(p.tiles, kblocks, G);
+    p.cmax = sk_cmax(p.tiles, kblocks, Gs, p.dp_tiles);
     p.ws_bytes = gemm_ws_bytes(p.cmax, p.tiles, p.rows, p.BN, p.CG);
-    if (p.cmax == 1 || p.ws_bytes > ws_avail) { p.sk = 0; p.cmax = 1; p.ws_bytes = p.cmax > 1 ? p.ws_bytes : 0; }
+    if (p.cmax == 1 || p.ws_bytes > ws_avail) { p.sk = 0; p.dp_tiles = p.tiles; p.cmax = 1; p.ws_bytes = 0; }
   }
-  if (!p.sk) p.ws_bytes = 0;
-  p.groups = p.sk ? G : std::min(p.tiles, G);
+  p.groups = p.sk ? Gs : std::min(p.tiles, G);
   return true;
 }
 
@@ -694,7 +699,7 @@ cudaError_t launch_gemm(const GemmCall& g, cudaStream_t st) {
   GemmArgs a;
   a.M = g.M; a.N = g.N; a.K = g.K; a.epi = g.epi; a.seg_cols = g.seg_cols;
   a.m_tiles = p.m_tiles; a.n_tiles = g.N / p.BN;
-  a.sk = p.sk;
+  a.dp_tiles = p.dp_tiles;
   a.cmax = p.cmax;
   a.cnt = p.sk ? reinterpret_cast<int32_t*>(static_cast<uint8_t*>(g.workspace) + p.ws_bytes -
                                             (int64_t)p.tiles * p.CG * 2 * 4)
