@@ -641,7 +641,29 @@ bool gemm_plan(const GemmCall& g, int64_t ws_avail, GemmPlan& p) {
   const bool n256 = g.N % 256 == 0 && g.seg_cols % 256 == 0;
   static const int force_cg = [] { const char* e = getenv("S3_GEMM_CG"); return e ? atoi(e) : 0; }();
   static const int force_sk = [] { const char* e = getenv("S3_GEMM_SK"); return e ? atoi(e) : -1; }();
-  p.CG = force_cg ? force_cg : (g.M > GM && n256 ? 2 : 1);
+  // Configuration rules (tools/gemm_sweep.sh on B200, GPT-J projections at M = 256 .. 2048):
+  //  * CTA-pair 256 x 256 tiles whenever M > 128 and the data-parallel waves are >= 85 % full;
+  //  * fewer pair tiles than half the SMs' pairs: long K (>= 8192) -> stream-K over the pairs,
+  //    else one CTA per 128 x 128 tile (more, smaller tiles);
+  //  * 1 - 1.5 waves of pair tiles: stream-K over the last wave merged with the full one;
+  //  * stream-K otherwise loses: groups at different K offsets of the same W block stop
+  //    sharing it in L2.
+  const int sms2 = sms / 2;
+  const int m2 = (g.M + 2 * GM - 1) / (2 * GM);
+  const int tiles2 = m2 * (g.N / 256);
+  const int waves2 = (tiles2 + sms2 - 1) / sms2;
+  const double eff2 = (double)tiles2 / ((double)waves2 * sms2);
+  int cg = 2, sk = 0;
+  if (g.M <= GM || !n256) {
+    cg = 1;
+  } else if (eff2 >= 0.85) {
+    cg = 2;
+  } else if (2 * tiles2 < sms2) {
+    if (g.K >= 8192) sk = 1; else cg = 1;
+  } else if (tiles2 > sms2 && 2 * tiles2 < 3 * sms2) {
+    sk = 1;
+  }
+  p.CG = force_cg ? force_cg : cg;
   if (p.CG == 2 && !n256) return false;
   p.rows = GM * p.CG;
   p.m_tiles = (g.M + p.rows - 1) / p.rows;
@@ -649,17 +671,12 @@ bool gemm_plan(const GemmCall& g, int64_t ws_avail, GemmPlan& p) {
   p.BN = p.CG == 2 ? 256 : (n256 && (int64_t)p.m_tiles * (g.N / 256) >= sms ? 256 : 128);
   p.tiles = p.m_tiles * (g.N / p.BN);
   const int kblocks = g.K / GK;
-  // data parallel unless its last wave leaves > 10 % of the groups idle and every group
-  // would still get >= 8 K blocks of a balanced stream-K partition
-  const int waves = (p.tiles + G - 1) / G;
-  const double dp_eff = (double)p.tiles / ((double)waves * G);
   // stream-K covers the ragged last wave merged with one full wave (so every group gets
   // >= 1 tile of work); the waves before it stay data parallel
   const int rem = p.tiles % G;
   const int sk_tiles = rem == 0 ? 0 : (p.tiles >= G ? rem + G : p.tiles);
-  p.sk = force_sk >= 0 ? force_sk : (dp_eff < 0.9 && sk_tiles > 0 && (int64_t)sk_tiles * kblocks >= 8LL * G);
-  if (p.sk && force_sk > 0 && sk_tiles == 0) p.sk = 0;
-  p.dp_tiles = p.sk ? p.tiles - (sk_tiles ? sk_tiles : p.tiles) : p.tiles;
+  p.sk = (force_sk >= 0 ? force_sk : sk) && sk_tiles > 0 && (int64_t)sk_tiles * kblocks >= 8LL * G;
+  p.dp_tiles = p.sk ? p.tiles - sk_tiles : p.tiles;
   p.cmax = 1;
   p.ws_bytes = 0;
   // every stream-K group owns >= 1 K block (empty ranges would not count as contributors)

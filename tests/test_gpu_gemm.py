@@ -44,7 +44,8 @@ def _ref(a, w, epi, c):
     (1, 128, 64, 0, 1, False), (77, 384, 192, 0, 1, True), (128, 512, 256, 1, 1, True), (300, 768, 1024, 2, 1, True),
     (513, 12288, 4096, 0, 3, True), (2048, 4096, 4096, 2, 1, True), (1500, 16384, 4096, 1, 1, False),
     (640, 4096, 16384, 2, 1, True), (512, 4096, 16384, 2, 1, True), (200, 4096, 4096, 1, 1, True),
-    (64, 12288, 4096, 0, 3, True), (512, 4096, 4096, 2, 1, False),
+    (64, 12288, 4096, 0, 3, True), (512, 4096, 4096, 2, 1, False), (512, 12288, 4096, 0, 3, True),
+    (256, 4096, 16384, 2, 1, True), (700, 12288, 4096, 1, 1, True),
 ])
 def test_gemm_matches_fp64(M, N, K, epi, nseg, ws):
     from paper_2306_06000_b200 import s3 as abi
