@@ -646,6 +646,8 @@ bool gemm_plan(const GemmCall& g, int64_t ws_avail, GemmPlan& p) {
   //  * fewer pair tiles than half the SMs' pairs: long K (>= 8192) -> stream-K over the pairs,
   //    else one CTA per 128 x 128 tile (more, smaller tiles);
   //  * 1 - 1.5 waves of pair tiles: stream-K over the last wave merged with the full one;
+  //  * single-CTA tiles (M <= 128, or few pair tiles): stream-K when they fill less than
+  //    85 % of one wave (weight streaming spread over every SM);
   //  * stream-K otherwise loses: groups at different K offsets of the same W block stop
   //    sharing it in L2.
   const int sms2 = sms / 2;
@@ -671,6 +673,10 @@ bool gemm_plan(const GemmCall& g, int64_t ws_avail, GemmPlan& p) {
   p.BN = p.CG == 2 ? 256 : (n256 && (int64_t)p.m_tiles * (g.N / 256) >= sms ? 256 : 128);
   p.tiles = p.m_tiles * (g.N / p.BN);
   const int kblocks = g.K / GK;
+  if (p.CG == 1 && force_sk < 0) {   // single-CTA tiles: stream-K when one wave of them leaves SMs idle
+    const int w1 = (p.tiles + G - 1) / G;
+    sk = (double)p.tiles / ((double)w1 * G) < 0.85 && p.tiles < G;
+  }
   // stream-K covers the ragged last wave merged with one full wave (so every group gets
   // >= 1 tile of work); the waves before it stay data parallel
   const int rem = p.tiles % G;
