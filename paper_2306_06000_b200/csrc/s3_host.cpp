@@ -161,6 +161,8 @@ struct s3_ctx {
   uint32_t* done = nullptr;                 // per-chunk finished-warp counters (device out + CE D2H)
   uint32_t* evdone = nullptr;               // per-evictee staged-row counters (fused eviction D2H)
   std::vector<uint32_t> ev_target;          // their cumulative targets
+  uint8_t* prep_scratch = nullptr;          // multi-CTA k_prep: totals, flags, header partials, done counter
+  uint32_t prep_epoch = 0;
   uint32_t done_target[kMaxFeedChunks] = {};  // cumulative values the D2H stream waits for
   cudaStream_t hio = nullptr, d2h = nullptr;
   cudaEvent_t ev_hio_start = nullptr, ev_hio_done = nullptr, ev_comb = nullptr, ev_d2h_done = nullptr;
@@ -247,7 +249,7 @@ Shape make_shape(const s3_config* c) {
 
 struct Carve {
   int64_t slots, units, splits, partials, ctrl, ctrl64, entries, keys, desc, progress, flags, report, verify, ready,
-      done, evdone, total;
+      done, evdone, prep, total;
 };
 
 Carve carve(const s3_config* c) {
@@ -276,6 +278,7 @@ Carve carve(const s3_config* c) {
   k.ready = o;    o += align_up(kMaxFeedChunks * 4);
   k.done = o;     o += align_up(kMaxFeedChunks * 4);
   k.evdone = o;   o += align_up(Bm * 4);
+  k.prep = o;     o += align_up(PREP_MAX_CTAS * (PREP_NX + 1 + 4) * 8 + 8);
   k.total = o;
   return k;
 }
@@ -592,6 +595,7 @@ s3_status s3_kv_init(const s3_config* cfg, const s3_buffers* b, s3_ctx** out) {
   ctx->ready = reinterpret_cast<uint32_t*>(ws + k.ready);
   ctx->done = reinterpret_cast<uint32_t*>(ws + k.done);
   ctx->evdone = reinterpret_cast<uint32_t*>(ws + k.evdone);
+  ctx->prep_scratch = ws + k.prep;
   ctx->ev_target.assign((size_t)cfg->max_running, 0u);
   if (cudaMemsetAsync(ws + k.ready, 0, (size_t)(k.total - k.ready), ctx->st) != cudaSuccess) return bail("memset");
   if (cudaMemsetAsync(ws + k.ctrl, 0, CTRL_WORDS * 4, ctx->st) != cudaSuccess) return bail("memset");
@@ -705,6 +709,11 @@ s3_status s3_decode_step(s3_ctx* ctx, int32_t l0, int32_t nl, const void* q, con
     for (const auto& fb : ctx->free_blocks) largest = std::max(largest, fb.second);
     pa.staging_bytes = std::min(stage_bytes(ctx), largest);
     pa.units = ctx->units; pa.splits = ctx->splits; pa.ctrl = ctx->ctrl;
+    pa.xagg = reinterpret_cast<long long*>(ctx->prep_scratch);
+    pa.xflag = reinterpret_cast<unsigned long long*>(pa.xagg + PREP_MAX_CTAS * PREP_NX);
+    pa.xpart = reinterpret_cast<long long*>(pa.xflag + PREP_MAX_CTAS);
+    pa.xdone = reinterpret_cast<int32_t*>(pa.xpart + PREP_MAX_CTAS * 4);
+    pa.epoch = ++ctx->prep_epoch;
     // fused: k_prep writes the keep-scan report straight into pinned host memory, so the
     // host's eviction bookkeeping and FFD start as soon as k_prep ends (overlapping the
     // attention kernel) and no copy engine is involved -- a report copy would queue

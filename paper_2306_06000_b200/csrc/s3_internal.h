@@ -107,7 +107,17 @@ struct PrepArgs {
   int32_t* ctrl;
   uint8_t* report;      // fused: the host-mapped pinned report (written over PCIe, no copy engine)
   int32_t* fused_out;   // host-mapped word: 1 if this step fused the row shift (or nullptr)
+  // multi-CTA scan (B > PREP_CTA_SLOTS): per-CTA totals published with an epoch flag,
+  // per-CTA header partials combined by the last CTA to finish
+  long long* xagg;      // [PREP_MAX_CTAS][PREP_NX] block totals
+  unsigned long long* xflag;   // [PREP_MAX_CTAS] epoch of the published totals
+  long long* xpart;     // [PREP_MAX_CTAS][4] first_hole, hbm, moved, end
+  int32_t* xdone;       // CTAs finished (reset by the last)
+  uint32_t epoch;
 };
+constexpr int PREP_CTA_SLOTS = 1024;   // slots per k_prep CTA when B is large (one per thread)
+constexpr int PREP_MAX_CTAS = 64;      // B <= 65535
+constexpr int PREP_NX = 10;            // scanned quantities per slot
 cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st);
 cudaError_t launch_deps(const Unit* units, const int32_t* ctrl, DepDesc* desc, int32_t tc, int32_t grid,
                         cudaStream_t st);

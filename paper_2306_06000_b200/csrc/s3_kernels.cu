@@ -214,11 +214,14 @@ __global__ void __launch_bounds__(1024) k_prep(PrepArgs a) {
   __shared__ int s_first_hole;
   __shared__ unsigned long long s_hbm, s_moved;
   __shared__ long long s_end;
+  __shared__ long long s_agg[PREP_MAX_CTAS][PREP_NX];
+  __shared__ int s_last;
   if (threadIdx.x == 0) { s_first_hole = a.B; s_hbm = 0; s_moved = 0; s_end = 0; }
   const int B = a.B, C = a.C;
   const int64_t kvpt = a.sh.kvpt;
-  const int per = (B + blockDim.x - 1) / blockDim.x;
-  const int b0 = threadIdx.x * per, b1 = min(B, b0 + per);
+  const int nb = gridDim.x;                                  // > 1: one slot per thread, decoupled totals
+  const int per = (B + nb * (int)blockDim.x - 1) / (nb * (int)blockDim.x);
+  const int b0 = ((int)blockIdx.x * (int)blockDim.x + (int)threadIdx.x) * per, b1 = min(B, b0 + per);
   // x: 0 units, 1 splits, 2 parts, 3 stages, 4 keep, 5 keep*cap, 6 fin, 7 ev, 8 ev bytes, 9 cap
   long long x[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
   for (int b = b0; b < b1; ++b) {
@@ -241,6 +244,36 @@ __global__ void __launch_bounds__(1024) k_prep(PrepArgs a) {
   }
   long long tot[10];
   block_excl_scan<10>(x, tot);
+  if (nb > 1) {
+    // publish this CTA's totals, then read every CTA's: the prefix of the CTAs before this one
+    // and the grid totals (all CTAs are co-resident: nb <= 64 one-CTA-per-SM blocks)
+    if (threadIdx.x == 0) {
+      for (int k = 0; k < PREP_NX; ++k) a.xagg[blockIdx.x * PREP_NX + k] = tot[k];
+      __threadfence();
+      asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(a.xflag + blockIdx.x), "l"((unsigned long long)a.epoch)
+                   : "memory");
+    }
+    if ((int)threadIdx.x < nb) {
+      const int c = threadIdx.x;
+      for (;;) {
+        unsigned long long f;
+        asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(f) : "l"(a.xflag + c) : "memory");
+        if (f == (unsigned long long)a.epoch) break;
+        __nanosleep(32);
+      }
+      for (int k = 0; k < PREP_NX; ++k) s_agg[c][k] = __ldcg(a.xagg + c * PREP_NX + k);
+    }
+    __syncthreads();
+    for (int k = 0; k < PREP_NX; ++k) {
+      long long pre = 0, all = 0;
+      for (int c = 0; c < nb; ++c) {
+        all += s_agg[c][k];
+        if (c < (int)blockIdx.x) pre += s_agg[c][k];
+      }
+      x[k] += pre;
+      tot[k] = all;
+    }
+  }
   const bool fused = a.fuse && a.finalize && tot[8] <= a.staging_bytes;
   // R27: shift unless the policy is on-demand and nobody could use the rows
   const bool compact = a.compact_policy == 0 || a.pool_nonempty || tot[7] > 0;
@@ -338,6 +371,33 @@ __global__ void __launch_bounds__(1024) k_prep(PrepArgs a) {
     if (end) atomicMax(&s_end, end);
   }
   __syncthreads();
+  if (nb > 1) {
+    // the header's min / sums / max over CTAs: combined by the last CTA to finish
+    if (threadIdx.x == 0) {
+      long long* pt = a.xpart + blockIdx.x * 4;
+      pt[0] = s_first_hole; pt[1] = (long long)s_hbm; pt[2] = (long long)s_moved; pt[3] = s_end;
+      __threadfence();
+      const int old = atomicAdd(a.xdone, 1);
+      s_last = old == nb - 1;
+      if (s_last) {
+        __threadfence();
+        int fh = B;
+        unsigned long long hb = 0, mv = 0;
+        long long en = 0;
+        for (int c = 0; c < nb; ++c) {
+          const long long* q = a.xpart + c * 4;
+          fh = min(fh, (int)__ldcg(q));
+          hb += (unsigned long long)__ldcg(q + 1);
+          mv += (unsigned long long)__ldcg(q + 2);
+          en = max(en, __ldcg(q + 3));
+        }
+        s_first_hole = fh; s_hbm = hb; s_moved = mv; s_end = en;
+        *a.xdone = 0;                                  // reusable by the next step
+      }
+    }
+    __syncthreads();
+    if (!s_last) return;
+  }
   if (threadIdx.x == 0) {
     a.ctrl[CTRL_N_UNITS] = (int)tot[0];
     a.ctrl[CTRL_N_SPLITS] = (int)tot[1];
@@ -1406,7 +1466,9 @@ const void* attn_kernel_ptr(const Shape& sh) {
 const void* move_kernel_ptr() { return (const void*)k_move; }
 
 cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st) {
-  k_prep<<<1, 1024, 0, st>>>(a);
+  // up to 2 slots per thread one CTA is fastest; beyond, one CTA per 1024 slots
+  const int nb = a.B <= 2 * PREP_CTA_SLOTS ? 1 : std::min((a.B + PREP_CTA_SLOTS - 1) / PREP_CTA_SLOTS, PREP_MAX_CTAS);
+  k_prep<<<nb, 1024, 0, st>>>(a);
   return cudaGetLastError();
 }
 

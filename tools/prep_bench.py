@@ -1,0 +1,40 @@
+#!/usr/bin/env python
+"""k_prep (detection + keep-scan + work list) at large batches: B tiny
+sequences (L = 1, H = 1, D = 64, so the attention pass is negligible), run
+under `ncu --metrics gpu__time_duration.sum -k regex:k_prep` to time the
+scan kernel alone (single CTA up to 2048 slots, one CTA per 1024 above)."""
+from __future__ import annotations
+
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    import numpy as np
+    import torch
+
+    import s3synth
+    from paper_2306_06000_b200.engine import S3Engine
+    B = int(sys.argv[1]) if len(sys.argv) > 1 else 16384
+    t = s3synth.make_trace(B, seed=3, policy="short", p=0.2, max_seq_len=64, prompt_max=16)
+    eng = S3Engine(1, 1, 64, 64, int(t.cap.sum()) + 64, B, host_store_bytes=1 << 26)
+    eng.submit(t.req_id, t.prompt, t.alloc, t.out)
+    eng.admit()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for _ in range(8):
+        eng.synth_inputs()
+        ev0.record()
+        eng.decode()
+        ev1.record()
+        torch.cuda.synchronize()
+        print(f"B {eng.B}: decode call (k_prep + k_deps + attention) {ev0.elapsed_time(ev1) * 1e3:.1f} us")
+        eng.evict_compact()
+        eng.admit()
+    eng.close()
+
+
+if __name__ == "__main__":
+    main()
