@@ -621,9 +621,13 @@ int sk_cmax(int tiles, int kblocks, int G, int dp_tiles) {
     c = std::max(c, w.group_of((int64_t)(st + 1) * kblocks - 1) - w.group_of((int64_t)st * kblocks) + 1);
   return c;
 }
-// stream-K scratch: cmax - 1 fp32 partial tiles per output tile, then [claim, done] per (tile, CTA)
+// stream-K scratch: [claim, done] counters per (tile, CTA) at a FIXED place -- the first
+// GEMM_CNT_BYTES, shared by every plan (each call leaves its counters zero, so GEMMs with
+// different plans can share one workspace) -- then cmax - 1 fp32 partial tiles per tile
+constexpr int64_t GEMM_CNT_BYTES = 32768;
 int64_t gemm_ws_bytes(int cmax, int tiles, int rows, int BN, int CG) {
-  return (int64_t)(cmax - 1) * tiles * rows * BN * 4 + (int64_t)tiles * CG * 2 * 4;
+  if ((int64_t)tiles * CG * 2 * 4 > GEMM_CNT_BYTES) return INT64_MAX;
+  return GEMM_CNT_BYTES + (int64_t)(cmax - 1) * tiles * rows * BN * 4;
 }
 
 // Tile choice: a CTA pair per 256 x 256 tile (half the operand traffic per
@@ -717,16 +721,15 @@ cudaError_t launch_gemm(const GemmCall& g, cudaStream_t st) {
   maps.c = maps.d[0];
   if (g.epi == 2 && !encode_rows(&maps.c, g.c, (uint64_t)g.M, (uint64_t)g.N, 0, 64)) return cudaErrorInvalidValue;
   maps.p = maps.d[0];
-  if (p.sk && !encode_rows(&maps.p, g.workspace, (uint64_t)p.tiles * (p.cmax - 1) * p.rows, (uint64_t)p.BN, 1, 32))
+  if (p.sk && !encode_rows(&maps.p, static_cast<uint8_t*>(g.workspace) + GEMM_CNT_BYTES,
+                           (uint64_t)p.tiles * (p.cmax - 1) * p.rows, (uint64_t)p.BN, 1, 32))
     return cudaErrorInvalidValue;
   GemmArgs a;
   a.M = g.M; a.N = g.N; a.K = g.K; a.epi = g.epi; a.seg_cols = g.seg_cols;
   a.m_tiles = p.m_tiles; a.n_tiles = g.N / p.BN;
   a.dp_tiles = p.dp_tiles;
   a.cmax = p.cmax;
-  a.cnt = p.sk ? reinterpret_cast<int32_t*>(static_cast<uint8_t*>(g.workspace) + p.ws_bytes -
-                                            (int64_t)p.tiles * p.CG * 2 * 4)
-               : nullptr;
+  a.cnt = p.sk ? static_cast<int32_t*>(g.workspace) : nullptr;
   const int groups = p.groups;
   cudaError_t e;
   if (p.CG == 2) e = launch_one<256, 2>(maps, a, 2 * groups, st);

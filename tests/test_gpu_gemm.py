@@ -130,3 +130,26 @@ def test_proxy_model_attention_through_oracle():
     eng.close()
     print("checked", checked, "worst rel err", worst)
     assert checked >= 50
+
+
+def test_workspace_shared_across_plans():
+    # the proxy's four projections share one split-K workspace: plans with
+    # different tile counts must leave the shared counters zero for each other
+    from paper_2306_06000_b200 import s3 as abi
+    st = torch.cuda.current_stream()
+    ws = torch.zeros(96 << 20, device="cuda", dtype=torch.uint8)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    for M in (179, 300):
+        for rep in range(2):
+            for N, K, epi in ((12288, 4096, 0), (16384, 4096, 1), (4096, 4096, 2), (4096, 16384, 2)):
+                a = torch.randn(M, K, device="cuda", generator=g).to(torch.bfloat16)
+                w = (torch.randn(N, K, device="cuda", generator=g) / math.sqrt(K)).to(torch.bfloat16)
+                c = torch.randn(M, N, device="cuda", generator=g).to(torch.bfloat16) if epi == 2 else None
+                ref = _ref(a, w, epi, c)
+                d = c.clone() if epi == 2 else torch.full((M, N), float("nan"), device="cuda", dtype=torch.bfloat16)
+                abi.s3_gemm(st, a, w, d, c=d if epi == 2 else None, epi=epi, workspace=ws)
+                torch.cuda.synchronize()
+                err = (d.double() - ref).abs()
+                tol = 2.0 ** -8 * ref.abs() + 1e-3 * ref.abs().max() + 1e-6
+                assert (err > tol).sum().item() == 0, (M, N, K, epi, rep)
+    assert int(ws[:32768].view(torch.int32).abs().sum().item()) == 0      # counters left zero
