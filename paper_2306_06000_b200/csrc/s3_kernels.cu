@@ -18,6 +18,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "s3_internal.h"
 
@@ -1467,7 +1468,9 @@ const void* move_kernel_ptr() { return (const void*)k_move; }
 
 cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st) {
   // up to 2 slots per thread one CTA is fastest; beyond, one CTA per 1024 slots
-  const int nb = a.B <= 2 * PREP_CTA_SLOTS ? 1 : std::min((a.B + PREP_CTA_SLOTS - 1) / PREP_CTA_SLOTS, PREP_MAX_CTAS);
+  static const int single = [] { const char* e = getenv("S3_PREP_SINGLE_CTA"); return e ? atoi(e) : 0; }();  // A/B
+  const int nb = (single || a.B <= 2 * PREP_CTA_SLOTS) ? 1
+                                                      : std::min((a.B + PREP_CTA_SLOTS - 1) / PREP_CTA_SLOTS, PREP_MAX_CTAS);
   k_prep<<<nb, 1024, 0, st>>>(a);
   return cudaGetLastError();
 }
