@@ -109,6 +109,14 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 __device__ __forceinline__ float bf16_lo(uint32_t u) { return __uint_as_float(u << 16); }
 __device__ __forceinline__ float bf16_hi(uint32_t u) { return __uint_as_float(u & 0xffff0000u); }
 
+// as many ring stages as fit next to the epilogue staging (227 KB per CTA; 1 KB alignment
+// slack + barriers), at most 6: deep rings keep enough weight bytes in flight when M is
+// small and the GEMM streams W at HBM speed
+__host__ __device__ constexpr int gemm_stages(int stage_bytes) {
+  return (227 * 1024 - 4 * 16384 - 1024 - 512) / stage_bytes < 6 ? (227 * 1024 - 4 * 16384 - 1024 - 512) / stage_bytes
+                                                                  : 6;
+}
+
 struct GemmMaps {
   CUtensorMap a, w;      // operands (loads)
   CUtensorMap d[3];      // output column segments (stores, box {64, 32})
@@ -229,7 +237,7 @@ __device__ __forceinline__ void g_arrive_leader(uint64_t* b) {
 template <int BN, int CG>
 __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(const __grid_constant__ GemmMaps maps, GemmArgs a) {
   constexpr int A_BYTES = GM * GK * 2, W_BYTES = (BN / CG) * GK * 2, STAGE = A_BYTES + W_BYTES;
-  constexpr int NSTG = STAGE > 32768 ? 3 : GSTAGES;
+  constexpr int NSTG = gemm_stages(STAGE);
   constexpr int TMEM_COLS = 2 * BN;
   constexpr int TM_ROWS = GM * CG;                     // rows per tile
   extern __shared__ __align__(1024) uint8_t gsmem_raw[];
@@ -543,8 +551,8 @@ bool encode_kmajor(CUtensorMap* m, const void* base, uint64_t rows, uint64_t K, 
 template <int BN, int CG>
 int gemm_smem() {
   constexpr int STAGE = GM * GK * 2 + (BN / CG) * GK * 2;
-  constexpr int NSTG = STAGE > 32768 ? 3 : GSTAGES;
-  return NSTG * STAGE + 4 * EPI_WARP_BYTES + 1024 + 256;
+  constexpr int NSTG = gemm_stages(STAGE);
+  return NSTG * STAGE + 4 * EPI_WARP_BYTES + 1024 + 512;
 }
 
 // bf16 or fp32 row-major [rows][cols] map with a {box_cols, 32}-row box, 128B swizzle (TMA store / load)
