@@ -682,7 +682,9 @@ bool gemm_plan(const GemmCall& g, int64_t ws_avail, GemmPlan& p) {
   p.rows = GM * p.CG;
   p.m_tiles = (g.M + p.rows - 1) / p.rows;
   const int G = sms / p.CG;
+  static const int force_bn = [] { const char* e = getenv("S3_GEMM_BN"); return e ? atoi(e) : 0; }();
   p.BN = p.CG == 2 ? 256 : (n256 && (int64_t)p.m_tiles * (g.N / 256) >= sms ? 256 : 128);
+  if (p.CG == 1 && (force_bn == 64 || force_bn == 128 || (force_bn == 256 && n256))) p.BN = force_bn;
   p.tiles = p.m_tiles * (g.N / p.BN);
   const int kblocks = g.K / GK;
   if (p.CG == 1 && force_sk < 0) {   // single-CTA tiles: stream-K when one wave of them leaves SMs idle
@@ -742,7 +744,8 @@ cudaError_t launch_gemm(const GemmCall& g, cudaStream_t st) {
   cudaError_t e;
   if (p.CG == 2) e = launch_one<256, 2>(maps, a, 2 * groups, st);
   else if (p.BN == 256) e = launch_one<256, 1>(maps, a, groups, st);
-  else e = launch_one<128, 1>(maps, a, groups, st);
+  else if (p.BN == 128) e = launch_one<128, 1>(maps, a, groups, st);
+  else e = launch_one<64, 1>(maps, a, groups, st);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
