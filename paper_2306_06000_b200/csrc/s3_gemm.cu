@@ -659,7 +659,8 @@ bool gemm_plan(const GemmCall& g, int64_t ws_avail, GemmPlan& p) {
   //    else one CTA per 128 x 128 tile (more, smaller tiles);
   //  * 1 - 1.5 waves of pair tiles: stream-K over the last wave merged with the full one;
   //  * single-CTA tiles (M <= 128, or few pair tiles): stream-K when they fill less than
-  //    85 % of one wave (weight streaming spread over every SM);
+  //    half a wave (tools/gemm_sweep_small.sh: above that, data parallel streams the
+  //    weights faster than stream-K's partial sums);
   //  * stream-K otherwise loses: groups at different K offsets of the same W block stop
   //    sharing it in L2.
   const int sms2 = sms / 2;
@@ -687,10 +688,7 @@ bool gemm_plan(const GemmCall& g, int64_t ws_avail, GemmPlan& p) {
   if (p.CG == 1 && (force_bn == 64 || force_bn == 128 || (force_bn == 256 && n256))) p.BN = force_bn;
   p.tiles = p.m_tiles * (g.N / p.BN);
   const int kblocks = g.K / GK;
-  if (p.CG == 1 && force_sk < 0) {   // single-CTA tiles: stream-K when one wave of them leaves SMs idle
-    const int w1 = (p.tiles + G - 1) / G;
-    sk = (double)p.tiles / ((double)w1 * G) < 0.85 && p.tiles < G;
-  }
+  if (p.CG == 1 && force_sk < 0) sk = 2 * p.tiles < G;   // single-CTA tiles: stream-K below half a wave
   // stream-K covers the ragged last wave merged with one full wave (so every group gets
   // >= 1 tile of work); the waves before it stay data parallel
   const int rem = p.tiles % G;
