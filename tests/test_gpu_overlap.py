@@ -78,6 +78,8 @@ def _attention_vs_probe(probe, reserve_sms):
 
 
 def test_reserved_sms_let_a_side_stream_kernel_run_during_attention(probe):
+    if os.environ.get("CUDA_INJECTION64_PATH"):
+        pytest.skip("timing evidence is meaningless under compute-sanitizer")
     with_res = _attention_vs_probe(probe, 4)
     without = _attention_vs_probe(probe, -1)
     print("attention ms, probe done ms (reserve 4):", with_res, " (none):", without)
@@ -93,8 +95,10 @@ def test_eviction_d2h_overlaps_attention():
     "asynchronously").  GPT-J-shaped rows, short(0.3) mispredictions."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
+    if os.environ.get("CUDA_INJECTION64_PATH"):
+        pytest.skip("timing evidence is meaningless under compute-sanitizer")
     from paper_2306_06000_b200.engine import S3Engine
-    t = s3synth.make_trace(3000, seed=7, policy="short", p=0.3, max_seq_len=2048)
+    t = s3synth.make_trace(3000, seed=7, policy="short", p=0.5, max_seq_len=2048)
     L, H, D = 28, 16, 256
     R = 60000                                           # ~27.5 GB of GPT-J KV rows
     eng = S3Engine(L, H, D, 2048, R, 4096, device=0, staging_bytes=4 << 30, host_store_bytes=8 << 30)
@@ -113,5 +117,5 @@ def test_eviction_d2h_overlaps_attention():
     frac = prof.d2h_overlap_ms / prof.d2h_ms
     print(f"evictions {ev}, d2h {prof.d2h_bytes / 1e9:.2f} GB in {prof.d2h_ms:.2f} ms, overlap {frac:.3f}, "
           f"reloaded from staging {stage / 1e9:.2f} GB")
-    assert ev > 0 and prof.d2h_copies >= ev
+    assert ev >= 10 and prof.d2h_copies >= ev
     assert frac >= 0.5
