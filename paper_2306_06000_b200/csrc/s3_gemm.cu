@@ -39,7 +39,7 @@ namespace {
 
 constexpr int GM = 128;          // tile rows (MMA M)
 constexpr int GK = 64;           // K block: one 128-byte swizzle atom of bf16
-constexpr int GSTAGES = 4;
+
 constexpr int G_THREADS = 6 * 32;
 
 __device__ __forceinline__ uint32_t gsu32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
