@@ -340,6 +340,25 @@ class Ctx:
         self.dist.all_reduce(tk)
         return float(tt.item()), int(tk.item())
 
+    def rank_balance(self, attn_bytes, attn_ms, tokens):
+        """Per-rank attention bytes / time / tokens over the timed window (world > 1):
+        lockstep makes every step as long as the busiest rank's attention pass, so
+        max / mean of the bytes each rank streamed is the placement's balance."""
+        import torch
+        if not self.dist:
+            return None
+        v = torch.tensor([float(attn_bytes), float(attn_ms), float(tokens)], dtype=torch.float64, device=self.cdev)
+        allv = [torch.zeros_like(v) for _ in range(self.world)]
+        self.dist.all_gather(allv, v)
+        rows = [x.cpu().tolist() for x in allv]
+        b = [r[0] for r in rows]
+        mean = sum(b) / len(b)
+        return {"attn_gb_per_rank": [round(x / 1e9, 2) for x in b],
+                "attn_ms_per_rank": [round(r[1], 2) for r in rows],
+                "tokens_per_rank": [int(r[2]) for r in rows],
+                "attn_bytes_max_over_mean": round(max(b) / mean, 4) if mean else None,
+                "placement": "worst fit over ranks (DESIGN.md R26)"}
+
     def new_engine(self, policy, p, n_req=None, compact_mode=None, arena_gb=None, trace=None, max_running=None,
                    R=None, host_store=None):
         """A fresh engine over a fresh trace (one per leg; the previous one must be closed)."""
@@ -462,6 +481,7 @@ def run_s3(args):
     eng.profile(False)
     ms_max, tok_sum = cx.max_over_ranks(ms, tokens)
     value = tok_sum / (ms_max / 1e3)
+    balance = cx.rank_balance(prof.attn_bytes, prof.attn_ms, tokens)
     launches = prof.kernel_launches - p0.kernel_launches
     mean_batch_window = float(np.mean(batch_sizes))
 
@@ -578,6 +598,7 @@ def run_s3(args):
                     round(prof.d2h_overlap_ms / prof.d2h_ms, 4) if prof.d2h_ms else None,
             },
             "clocks": cx.clocks.summary(),
+            "rank_balance": balance,
             "cpu_baseline": cpu,
             "e2e": e2e,
         }

@@ -133,3 +133,9 @@ def test_bench_torchrun_two_ranks_gloo():
     j = json.loads(lines[0])
     assert j["n_gpus"] == 2 and j["value"] > 0 and j["gpu_launches"] > 0
     assert j["e2e"]["value"] > 0 and j["e2e"]["h2d_bytes_per_step"] > 0   # host-fed C ABI on both ranks
+    rb = j["rank_balance"]
+    assert len(rb["attn_gb_per_rank"]) == 2 and rb["attn_bytes_max_over_mean"] >= 1.0
+    # the whole-run leg serves every request to completion across both ranks: tokens = sum O
+    import s3synth
+    t = s3synth.make_trace(3000, seed=1, policy="oracle", max_seq_len=2048)
+    assert j["wholerun"]["tokens"] == int(t.out.sum())
