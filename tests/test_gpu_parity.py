@@ -664,12 +664,12 @@ def test_duplicate_submit_and_host_store_exhaustion():
     eng.close()
 
 
-@pytest.mark.parametrize("variant", [0, 2])
-def test_large_batch_multi_cta_prep(variant):
+@pytest.mark.parametrize("variant,mode", [(0, 0), (2, 0), (0, 1)])
+def test_large_batch_multi_cta_prep(variant, mode):
     # B > 2048 slots: k_prep runs as several CTAs (totals published per CTA,
     # header partials combined by the last); lockstep against the oracle
     t = s3synth.make_trace(6000, seed=17, policy="short", p=0.2, max_seq_len=48, prompt_max=10)
     Hkv = 1 if variant == 2 else 0
     r = lockstep(t, 1, 2 if variant == 2 else 2, 128 if variant == 2 else 64, int(t.cap.sum()) + 64,
-                 C=16, max_running=8192, attn_variant=variant, Hkv=Hkv, check_arena=False)
-    assert r["evictions"] > 0 and r["fused_steps"] > 0
+                 C=16, max_running=8192, attn_variant=variant, Hkv=Hkv, check_arena=False, compact_mode=mode)
+    assert r["evictions"] > 0 and (r["fused_steps"] > 0) == (mode == 0)
