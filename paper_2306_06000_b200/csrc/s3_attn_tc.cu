@@ -9,11 +9,13 @@
 // (16 = G padded to the MMA N granularity; P is split into bf16 hi + lo so
 // the product keeps ~16 bits, one N = 32 MMA per 16 rows).  Per CTA
 // (persistent, one per SM, 11 warps) these roles:
-//   producer warp : items (unit, layer, KV head) from the atomic queue; per
+//   producer warp : items (unit, layer, KV head) from the atomic queue (the
+//                   next ticket and unit record fetched one ticket ahead); per
 //                   tile ONE 4-D TMA box for K and one for V (all valid 8-row
 //                   groups, both 64-column blocks; the smem tile layout is
 //                   [8-row group][column block][8 rows][128 B]) and one 3-D box
-//                   for the 16 q rows, into a 3-stage ring.  Short units pack
+//                   for the 16 q rows; K + q go to a 2-slot K ring that the S
+//                   MMA releases, V to a 4-slot V ring that the O MMA releases.  Short units pack
 //                   np = 2..NC/G KV heads into one tile, one segment of 128/np
 //                   rows per head: the q box already holds those heads' np*G
 //                   query rows, and the softmax masks S^T block-diagonally
@@ -45,7 +47,7 @@
 // far, then writes the tile's whole 8-row groups back with 4-D TMA tensor stores
 // through the same layout and the ragged tail rows with a warp copy
 // that undoes the 128B swizzle; STAGE (evicted) tiles go to the staging
-// buffer the same way.  The stage is released (kv_empty) only after the
+// buffer the same way.  The K and V slots are released (kempty, vempty) only after the
 // stores have read shared memory.  Deadlock freedom is the k_attn_tma
 // argument: tickets are taken in unit order and destinations lie at or below
 // their sources.
@@ -80,10 +82,21 @@ __device__ unsigned long long g_tc_trace[TC_TRACE_TILES * 8];
 constexpr int TM = 128;                     // rows per tile (MMA M)
 constexpr int NQ = 16;                      // query columns per KV head (MMA N)
 constexpr int DH = 128;                     // head dim
-constexpr int NST = 3;                      // K/V ring stages
+// K and V ride separate rings: a K slot (with the tile's q) is free as soon as the S
+// MMA has read it, a V slot only after the O MMA, so the V ring is the deeper one.
+// With one 3-stage K|V ring a short tile held its stage for the whole chain (load,
+// S, softmax, P hand-over, O: ~7.7k cycles) and 3 stages bounded the period.
+constexpr int NK = 2;                       // K (+ q) ring slots
+constexpr int NV = 4;                       // V ring slots (tile t's header lives at hdr[t % NV])
 constexpr int KV_BYTES = TM * DH * 2;       // 32 KB: two 64-column blocks of [128 rows x 128 B]
 constexpr int Q_BYTES = NQ * DH * 2;        // 4 KB:  two blocks of [16 rows x 128 B]
-constexpr int STAGE_BYTES = 2 * KV_BYTES + Q_BYTES;   // 68 KB (multiple of 1024)
+constexpr int KSLOT_BYTES = KV_BYTES + Q_BYTES;   // 36 KB (multiple of 1024)
+constexpr int VSLOT_BYTES = KV_BYTES;             // 32 KB
+constexpr int RING_BYTES = NK * KSLOT_BYTES + NV * VSLOT_BYTES;
+__device__ __forceinline__ uint8_t* kslot(uint8_t* smem, int t) { return smem + (t % NK) * KSLOT_BYTES; }
+__device__ __forceinline__ uint8_t* vslot(uint8_t* smem, int t) {
+  return smem + NK * KSLOT_BYTES + (t % NV) * VSLOT_BYTES;
+}
 // P as bf16 hi + lo parts (P = hi + lo to ~16 bits), one MMA operand [hi | lo] of N = 32:
 // two K blocks (tile rows j 0-63, 64-127) of [32 rows x 128 B] (rows 0-15 hi, 16-31 lo)
 constexpr int PBLK_BYTES = 2 * NQ * 64 * 2;  // 4 KB per K block
@@ -112,10 +125,10 @@ __device__ __forceinline__ int hdr_lognp(const TcHdr& h) { return (h.flags >> 8)
 constexpr int TC_HEAD_STRIDE = 1 << 16;      // progress = head * 2^16 + rows (unit rows < 2^16)
 
 struct alignas(16) TcSmem {                 // after the ring and the two P buffers (one per group)
-  uint64_t kv_full[NST], kv_empty[NST];
+  uint64_t kfull[NK], kempty[NK], vfull[NV], vempty[NV];
   uint64_t s_full[2][2], s_empty[2][2];     // [group][S slot]; s_full: MMA commit + the MMA thread's arrive
   uint64_t p_full[2], o_done[2], o_fin[2], o_free[2];   // [group] (= O buffer = item parity)
-  alignas(16) TcHdr hdr[NST];               // hdr.dep is a 16-B bulk-copy destination
+  alignas(16) TcHdr hdr[NV];                // tile t at hdr[t % NV]; hdr.dep is a 16-B bulk-copy destination
   float red[2][2][4][NQ];                   // [group][max / sum][warp][column]
   int32_t flag[2][4];
   int32_t gt[2][2];                         // ring tile index in group g's S slot b (-1: no more tiles)
@@ -378,13 +391,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
   // 1024-B alignment for the 128B-swizzle atoms, by pointer arithmetic so the
   // compiler keeps the shared-memory address space (LDS/STS, not generic LD/ST)
   uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
-  uint8_t* pbuf = smem + NST * STAGE_BYTES;
+  uint8_t* pbuf = smem + RING_BYTES;
   TcSmem& S = *reinterpret_cast<TcSmem*>(pbuf + 2 * PBUF_BYTES);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // the storer takes part in the ring only when this step shifts rows
   const bool fused = a.ctrl[CTRL_FUSED] != 0;
   if (tid == 0) {
-    for (int i = 0; i < NST; ++i) { mb_init(&S.kv_full[i], 1); mb_init(&S.kv_empty[i], fused ? 2 : 1); }
+    for (int i = 0; i < NK; ++i) { mb_init(&S.kfull[i], 1); mb_init(&S.kempty[i], fused ? 2 : 1); }
+    for (int i = 0; i < NV; ++i) { mb_init(&S.vfull[i], 1); mb_init(&S.vempty[i], fused ? 2 : 1); }
     for (int g = 0; g < 2; ++g) {
       for (int b = 0; b < 2; ++b) { mb_init(&S.s_full[g][b], 2); mb_init(&S.s_empty[g][b], 4); }
       mb_init(&S.p_full[g], 4);
@@ -395,9 +409,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // V buffers start at zero: rows a tile does not load keep finite (zero or earlier valid) data
-  for (int st = 0; st < NST; ++st)
+  for (int st = 0; st < NV; ++st)
     for (int i = tid; i < KV_BYTES / 16; i += blockDim.x)
-      reinterpret_cast<uint4*>(smem + st * STAGE_BYTES + KV_BYTES)[i] = make_uint4(0, 0, 0, 0);
+      reinterpret_cast<uint4*>(vslot(smem, st))[i] = make_uint4(0, 0, 0, 0);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&S.tmem_base)),
@@ -423,21 +437,35 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
     const int groups_total = a.ctrl[CTRL_N_UNITS] * a.nl;
     const int kd8 = a.Hkv * DH / 8;               // 16-B vectors of one layer's new K (or V) row
     // FEED: the whole warp runs the loop (lane 0 takes tickets and issues tiles); else lane 0 alone
+    // The next ticket and its unit record are fetched one ticket ahead, so the
+    // atomic and the dependent load (~2 us together) overlap this ticket's tile
+    // issue instead of stalling the ring between tickets (short units have only a
+    // few tiles per ticket).  Deadlock freedom is unchanged: the smallest
+    // unfinished ticket is always some CTA's current one.
+    int w_next = 0;
+    if (lane == 0) w_next = atomicAdd(&a.ctrl[CTRL_ITEM], 1);
+    if constexpr (FEED) w_next = __shfl_sync(0xffffffffu, w_next, 0);
+    Unit un_next{};
+    if ((FEED || lane == 0) && w_next < groups_total) un_next = a.units[w_next / a.nl];
     for (; FEED || lane == 0;) {
-      int w = 0;
-      if (lane == 0) w = atomicAdd(&a.ctrl[CTRL_ITEM], 1);
-      if constexpr (FEED) w = __shfl_sync(0xffffffffu, w, 0);
+      const int w = w_next;
+      const Unit un = un_next;
+      if (w < groups_total) {
+        if (lane == 0) w_next = atomicAdd(&a.ctrl[CTRL_ITEM], 1);
+        if constexpr (FEED) w_next = __shfl_sync(0xffffffffu, w_next, 0);
+        if (w_next < groups_total) un_next = a.units[w_next / a.nl];
+      }
       if (w >= groups_total) {
         if (lane == 0) {
-          const int st = t % NST;
-          mb_wait(&S.kv_empty[st], ((uint32_t)(t / NST) & 1u) ^ 1u);
-          S.hdr[st].item = -1;
-          mb_arrive(&S.kv_full[st]);
+          mb_wait(&S.kempty[t % NK], ((uint32_t)(t / NK) & 1u) ^ 1u);
+          mb_wait(&S.vempty[t % NV], ((uint32_t)(t / NV) & 1u) ^ 1u);
+          S.hdr[t % NV].item = -1;
+          mb_arrive(&S.kfull[t % NK]);
+          mb_arrive(&S.vfull[t % NV]);
         }
         break;
       }
-      const int li = w % a.nl, u = w / a.nl;
-      const Unit un = a.units[u];
+      const int li = w % a.nl;
       if constexpr (FEED) {
         // host-fed step: this slot's q / k_new / v_new have landed once its chunk's word is set
         // (chunks land in order, so the highest chunk waited for covers every earlier one)
@@ -476,11 +504,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
           const int item = w * a.Hkv + g;
           const int qrow = (li * a.B + un.b) * a.H + g * a.G;
           for (int r = 0; r < nrows; r += TM) {
-            const int st = t % NST;
-            mb_wait(&S.kv_empty[st], ((uint32_t)(t / NST) & 1u) ^ 1u);
+            const int ks = t % NK, vs = t % NV;
+            mb_wait(&S.kempty[ks], ((uint32_t)(t / NK) & 1u) ^ 1u);
+            mb_wait(&S.vempty[vs], ((uint32_t)(t / NV) & 1u) ^ 1u);
             TC_TRACE_AT(t, 0);
             const int nv = min(TM, nrows - r);
-            TcHdr& h = S.hdr[st];
+            TcHdr& h = S.hdr[vs];
             h.item = item; h.r0 = un.r0 + r; h.nvalid = nv;
             h.flags = (r == 0 ? 1 : 0) | (r + TM >= nrows ? 2 : 0);
             h.b = un.b; h.part = un.part; h.li = li; h.g = g; h.iseq = iseq;
@@ -491,20 +520,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
             h.prog = (uint32_t)(glast * TC_HEAD_STRIDE + r + nv) |
                      (glast == a.Hkv - 1 && r + TM >= nrows ? TC_PROG_FULL : 0u);
             const int groups = (nv + 7) / 8;   // 8-row groups (one 128B-swizzle atom per column block)
-            uint8_t* sk = smem + st * STAGE_BYTES;
-            uint8_t* sv = sk + KV_BYTES;
-            uint8_t* sq = sv + KV_BYTES;
+            uint8_t* sk = kslot(smem, t);
+            uint8_t* sv = vslot(smem, t);
+            uint8_t* sq = sk + KV_BYTES;
             const bool dep = fused && mv;
-            mb_expect(&S.kv_full[st], (uint32_t)(np * groups * 8 * 128 * 2 * 2 + Q_BYTES + (dep ? 16 : 0)));
-            if (dep) bulk_g2s16(&h.dep, a.desc + un.stage_base + r / TM, &S.kv_full[st]);
+            mb_expect(&S.kfull[ks], (uint32_t)(np * groups * 8 * 128 * 2 + Q_BYTES + (dep ? 16 : 0)));
+            mb_expect(&S.vfull[vs], (uint32_t)(np * groups * 8 * 128 * 2));
+            if (dep) bulk_g2s16(&h.dep, a.desc + un.stage_base + r / TM, &S.kfull[ks]);
             const int row0 = un.off + un.r0 + r;
             for (int sgi = 0; sgi < np; ++sgi) {    // one 4-D box per segment for K and one for V
               const int colk = (a.l0 + li) * row_cols + (g + sgi) * DH;
               const int sgo = sgi * (seg / 8) * 2048;   // segment's first group
-              tma4d(sk + sgo, &maps.kvg[groups - 1], row0, colk / 64, &S.kv_full[st]);
-              tma4d(sv + sgo, &maps.kvg[groups - 1], row0, (colk + a.Hkv * DH) / 64, &S.kv_full[st]);
+              tma4d(sk + sgo, &maps.kvg[groups - 1], row0, colk / 64, &S.kfull[ks]);
+              tma4d(sv + sgo, &maps.kvg[groups - 1], row0, (colk + a.Hkv * DH) / 64, &S.vfull[vs]);
             }
-            tma3d(sq, &maps.q, 0, qrow, 0, &S.kv_full[st]);   // both 64-column blocks of the 16 q rows
+            tma3d(sq, &maps.q, 0, qrow, 0, &S.kfull[ks]);   // both 64-column blocks of the 16 q rows
             ++t;
             TC_TRACE_AT(t - 1, 1);
           }
@@ -523,14 +553,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
       constexpr uint32_t id_s = idesc(0, NQ), id_o = idesc(1, 2 * NQ);
       int kc[2] = {0, 0};                       // tiles handed to each group so far
       auto issue_s = [&](int t) -> int {        // returns the tile's index within its group
-        const int st = t % NST;
-        const int g = S.hdr[st].iseq & 1;
+        const int g = S.hdr[t % NV].iseq & 1;
         const int k = kc[g]++;
         const int sb = k & 1;
         mb_wait(&S.s_empty[g][sb], ((uint32_t)(k >> 1) & 1u) ^ 1u);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint8_t* sk = smem + st * STAGE_BYTES;
-        const uint8_t* sq = sk + 2 * KV_BYTES;
+        const uint8_t* sk = kslot(smem, t);
+        const uint8_t* sq = sk + KV_BYTES;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {        // S^T = K . Q^T over d in steps of 16
           const int kb = kk >> 2, ko = (kk & 3) * 32;
@@ -538,6 +567,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
               kk > 0);
         }
         commit(&S.s_full[g][sb]);
+        commit(&S.kempty[t % NK]);              // the K slot is free once these MMAs have read it
         S.gt[g][sb] = t;
         mb_arrive(&S.s_full[g][sb]);            // releases gt together with the slot
         return k;
@@ -551,26 +581,27 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
           mb_arrive(&S.s_full[g][sb]);
         }
       };
-      mb_wait(&S.kv_full[0], 0u);
+      mb_wait(&S.kfull[0], 0u);
       if (S.hdr[0].item < 0) {
         finish();
       } else {
         int kt = issue_s(0);
         for (int t = 0;; ++t) {
-          const int st = t % NST, st1 = (t + 1) % NST;
-          mb_wait(&S.kv_full[st1], (uint32_t)((t + 1) / NST) & 1u);
+          const int vs = t % NV;
+          mb_wait(&S.kfull[(t + 1) % NK], (uint32_t)((t + 1) / NK) & 1u);
           TC_TRACE_AT(t + 1, 3);
-          const bool end = S.hdr[st1].item < 0;
+          const bool end = S.hdr[(t + 1) % NV].item < 0;
           const int kt1 = end ? 0 : issue_s(t + 1);
-          const bool first = S.hdr[st].flags & 1;
-          const bool last = S.hdr[st].flags & 2;
-          const int iseq = S.hdr[st].iseq, g = iseq & 1;
+          const bool first = S.hdr[vs].flags & 1;
+          const bool last = S.hdr[vs].flags & 2;
+          const int iseq = S.hdr[vs].iseq, g = iseq & 1;
           if (first)   // O buffer g must have been read by the epilogue of item iseq - 2
             mb_wait(&S.o_free[g], ((uint32_t)(iseq >> 1) & 1u) ^ 1u);
           mb_wait(&S.p_full[g], (uint32_t)kt & 1u);
+          mb_wait(&S.vfull[vs], (uint32_t)(t / NV) & 1u);   // V landed (the softmax waited too if it zeroed rows)
           TC_TRACE_AT(t, 4);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint8_t* sv = smem + st * STAGE_BYTES + KV_BYTES;
+          const uint8_t* sv = vslot(smem, t);
           const uint8_t* sp = pbuf + g * PBUF_BYTES;
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {          // [O_hi | O_lo]^T += V^T . [P_hi | P_lo]^T, rows in steps of 16
@@ -580,7 +611,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
           }
           commit(&S.o_done[g]);
           if (last) commit(&S.o_fin[g]);
-          commit(&S.kv_empty[st]);
+          commit(&S.vempty[vs]);
           TC_TRACE_AT(t, 5);
           if (end) { finish(); break; }
           kt = kt1;
@@ -590,11 +621,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
   } else if (warp == 6) {
     // ------------------------------- storer -------------------------------
     if (fused) {
-      int pending = -1;                   // stage whose bulk stores may still read shared memory
+      int pending = -1;                   // tile whose bulk stores may still read shared memory
       for (int t = 0;; ++t) {
-        const int st = t % NST;
-        mb_wait(&S.kv_full[st], (uint32_t)(t / NST) & 1u);
-        const TcHdr h = S.hdr[st];
+        mb_wait(&S.kfull[t % NK], (uint32_t)(t / NK) & 1u);
+        mb_wait(&S.vfull[t % NV], (uint32_t)(t / NV) & 1u);
+        const TcHdr h = S.hdr[t % NV];
         if (h.item < 0) break;
         const int w = h.item / a.Hkv;     // unit-layer ticket = progress slot
         if (lane == 0) {
@@ -625,7 +656,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
           const int np = PACK ? 1 << hdr_lognp(h) : 1;
           const int seg = TM / np;
           for (int sgi = 0; sgi < np; ++sgi) {       // one segment per packed KV head
-            const uint8_t* sk = smem + st * STAGE_BYTES + sgi * (seg / 8) * 2048;
+            const uint8_t* sk = kslot(smem, t) + sgi * (seg / 8) * 2048;
+            const uint8_t* sv = vslot(smem, t) + sgi * (seg / 8) * 2048;
             const int colk = (a.l0 + h.li) * 2 * a.Hkv * DH + (h.g + sgi) * DH;   // elements
             const int colv = colk + a.Hkv * DH;
             if (lane == 0) {
@@ -636,7 +668,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
                 if (full_groups & bg) {
                   const int done = full_groups & ~(2 * bg - 1);
                   tma4d_store(map + i, h.drow + done * 8, colk / 64, sk + done * 2048);
-                  tma4d_store(map + i, h.drow + done * 8, colv / 64, sk + KV_BYTES + done * 2048);
+                  tma4d_store(map + i, h.drow + done * 8, colv / 64, sv + done * 2048);
                 }
               }
             }
@@ -645,7 +677,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
             uint8_t* gbase = (h.mode == UNIT_MOVE ? a.arena : a.staging) +
                              (int64_t)(kv ? colv : colk) * 2 + kb * 128 + c * 16;
             for (int row = full_groups * 8; row < h.nvalid; ++row) {
-              const uint4 x = *reinterpret_cast<const uint4*>(sk + kv * KV_BYTES + (row >> 3) * 2048 + kb * 1024 +
+              const uint4 x = *reinterpret_cast<const uint4*>((kv ? sv : sk) + (row >> 3) * 2048 + kb * 1024 +
                                                               (row & 7) * 128 + ((c ^ (row & 7)) << 4));
               *reinterpret_cast<uint4*>(gbase + (int64_t)(h.drow + row) * a.kvpt) = x;
             }
@@ -654,15 +686,20 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
         }
         if (lane == 0) {
           if (stores) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-          // release the previous stage once its stores have read shared memory
+          // release the previous tile's K and V slots once its stores have read shared memory
           if (pending >= 0) {
             if (stores) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
             else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-            mb_arrive(&S.kv_empty[pending]);
+            mb_arrive(&S.kempty[pending % NK]);
+            mb_arrive(&S.vempty[pending % NV]);
             pending = -1;
           }
-          if (stores) pending = st;
-          else mb_arrive(&S.kv_empty[st]);
+          if (stores) {
+            pending = t;
+          } else {
+            mb_arrive(&S.kempty[t % NK]);
+            mb_arrive(&S.vempty[t % NV]);
+          }
           if (h.mode == UNIT_STAGE && a.evdone) {
             // the tile's evictee rows are final in staging once its stores complete (the
             // ragged rows' generic stores are ordered by the __syncwarp above): count them
@@ -676,7 +713,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
       }
       if (lane == 0) {
         asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-        if (pending >= 0) mb_arrive(&S.kv_empty[pending]);
+        if (pending >= 0) {
+          mb_arrive(&S.kempty[pending % NK]);
+          mb_arrive(&S.vempty[pending % NV]);
+        }
         asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
       }
     }
@@ -706,7 +746,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
       const int t = S.gt[grp][sb];
       if (t < 0) break;
       if (lane == 0 && warp == 2) TC_TRACE_AT(t, 6);
-      const TcHdr h = S.hdr[t % NST];
+      const TcHdr h = S.hdr[t % NV];
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       float s[NC];
       tmem_ld<NC>(lane_base + scol(grp, sb), s);
@@ -781,7 +821,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
         *reinterpret_cast<__nv_bfloat16*>(sp + NQ * 128 + sw) = lo;   // row 16 + c: same swizzle phase
       }
       if (!valid && rs < ((h.nvalid + 15) & ~15)) {  // loaded rows past the slot's resident rows: V := 0
-        uint8_t* sv = smem + (t % NST) * STAGE_BYTES + KV_BYTES;
+        mb_wait(&S.vfull[t % NV], (uint32_t)(t / NV) & 1u);   // after the V load has landed
+        uint8_t* sv = vslot(smem, t);
 #pragma unroll
         for (int kb = 0; kb < 2; ++kb)
 #pragma unroll
@@ -920,7 +961,7 @@ extern "C" int s3_debug_tc_trace(unsigned long long* host, int n) {
 }
 #endif
 
-int attn_tc_smem() { return NST * STAGE_BYTES + 2 * PBUF_BYTES + (int)sizeof(TcSmem) + 1024; }
+int attn_tc_smem() { return RING_BYTES + 2 * PBUF_BYTES + (int)sizeof(TcSmem) + 1024; }
 const void* attn_tc_kernel_ptr(int nc, bool pack, bool feed) {
   if (feed) {
     if (nc == 8) return pack ? (const void*)k_attn_tc<8, true, true> : (const void*)k_attn_tc<8, false, true>;

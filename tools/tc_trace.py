@@ -58,6 +58,16 @@ def main():
         "stage_reuse_gap(O commit t -> producer got stage t+3)": float(np.median(tr[idx + 3, 0] - t[:, 5])),
         "issue_end_t_to_stage_t+1": float(np.median(tr[idx + 1, 0] - t[:, 1])),
     }
+    # per-tile stage life and occupancy from the raw timestamps (CTA 0)
+    life = t[:, 5] - t[:, 0]
+    span = float(t[:, 5].max() - t[:, 0].min())
+    res["stage_life_mean"] = float(life.mean())
+    res["period_mean"] = span / len(idx)
+    res["tiles_in_flight_mean"] = float(life.sum()) / span
+    # gaps where the producer held no stage: got-stage(t+1) minus issue-end(t), split by whether t+1
+    # starts a new (unit, layer) ticket (slot-0 of t+1 after an atomic) -- flags not traced, so report all
+    res["producer_gap_p90"] = float(np.percentile(tr[idx + 1, 0] - t[:, 1], 90))
+    res["softmax_group_busy_frac"] = float(((t[:, 7] - t[:, 6]).sum()) / span / 2)
     print(json.dumps(res))
     eng.close()
 
