@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-legs", action="store_true", help="skip the wholerun / c2 / c3 legs")
+    ap.add_argument("--lib", default=None, help="A/B: load this libs3.so instead of the in-tree build")
     ap.add_argument("--e2e-chunks", type=int, default=0, help="H2D pipeline depth of the e2e leg (0 = 16)")
     ap.add_argument("--e2e-mapped-out", action="store_true",
                     help="e2e: kernels store out to mapped host memory instead of per-chunk D2H copies")
@@ -421,6 +422,9 @@ def run_s3(args):
     world, rank = cx.world, cx.rank
     from paper_2306_06000_b200 import build
     build.build()
+    if args.lib:                                   # A/B: another libs3.so build
+        from paper_2306_06000_b200 import s3 as abi
+        abi.LIB_PATH = os.path.abspath(args.lib)
 
     policy, p = workload(args)
     # weak scaling (fixed work per GPU) except C4, a fixed 65,536-request pool

@@ -86,16 +86,21 @@ constexpr int DH = 128;                     // head dim
 // MMA has read it, a V slot only after the O MMA, so the V ring is the deeper one.
 // With one 3-stage K|V ring a short tile held its stage for the whole chain (load,
 // S, softmax, P hand-over, O: ~7.7k cycles) and 3 stages bounded the period.
-constexpr int NK = 2;                       // K (+ q) ring slots
-constexpr int NV = 4;                       // V ring slots (tile t's header lives at hdr[t % NV])
+// Ring shapes (per launch, TcArgs.nk / nv): 2 K + 4 V slots when the step's items are short
+// (mostly one tile), 3 + 3 otherwise -- with the fused row shift the storer holds a K slot
+// while it waits for a MOVE tile's destination rows, which starves a 2-slot K ring on
+// long, moving items (LLaMA-3-8B whole run: 0.66 vs 0.84 of the copy peak).
+constexpr int NK_MAX = 3;                   // K (+ q) ring slots
+constexpr int NV_MAX = 4;                   // V ring slots (tile t's header lives at hdr[t % nv])
 constexpr int KV_BYTES = TM * DH * 2;       // 32 KB: two 64-column blocks of [128 rows x 128 B]
 constexpr int Q_BYTES = NQ * DH * 2;        // 4 KB:  two blocks of [16 rows x 128 B]
 constexpr int KSLOT_BYTES = KV_BYTES + Q_BYTES;   // 36 KB (multiple of 1024)
 constexpr int VSLOT_BYTES = KV_BYTES;             // 32 KB
-constexpr int RING_BYTES = NK * KSLOT_BYTES + NV * VSLOT_BYTES;
-__device__ __forceinline__ uint8_t* kslot(uint8_t* smem, int t) { return smem + (t % NK) * KSLOT_BYTES; }
-__device__ __forceinline__ uint8_t* vslot(uint8_t* smem, int t) {
-  return smem + NK * KSLOT_BYTES + (t % NV) * VSLOT_BYTES;
+constexpr int RING_BYTES = 3 * KSLOT_BYTES + 3 * VSLOT_BYTES;   // >= 2 * KSLOT_BYTES + 4 * VSLOT_BYTES
+static_assert(2 * KSLOT_BYTES + 4 * VSLOT_BYTES <= RING_BYTES, "ring shapes must fit the same bytes");
+__device__ __forceinline__ uint8_t* kslot(uint8_t* smem, int t, int nk) { return smem + (t % nk) * KSLOT_BYTES; }
+__device__ __forceinline__ uint8_t* vslot(uint8_t* smem, int t, int nk, int nv) {
+  return smem + nk * KSLOT_BYTES + (t % nv) * VSLOT_BYTES;
 }
 // P as bf16 hi + lo parts (P = hi + lo to ~16 bits), one MMA operand [hi | lo] of N = 32:
 // two K blocks (tile rows j 0-63, 64-127) of [32 rows x 128 B] (rows 0-15 hi, 16-31 lo)
@@ -125,10 +130,10 @@ __device__ __forceinline__ int hdr_lognp(const TcHdr& h) { return (h.flags >> 8)
 constexpr int TC_HEAD_STRIDE = 1 << 16;      // progress = head * 2^16 + rows (unit rows < 2^16)
 
 struct alignas(16) TcSmem {                 // after the ring and the two P buffers (one per group)
-  uint64_t kfull[NK], kempty[NK], vfull[NV], vempty[NV];
+  uint64_t kfull[NK_MAX], kempty[NK_MAX], vfull[NV_MAX], vempty[NV_MAX];
   uint64_t s_full[2][2], s_empty[2][2];     // [group][S slot]; s_full: MMA commit + the MMA thread's arrive
   uint64_t p_full[2], o_done[2], o_fin[2], o_free[2];   // [group] (= O buffer = item parity)
-  alignas(16) TcHdr hdr[NV];                // tile t at hdr[t % NV]; hdr.dep is a 16-B bulk-copy destination
+  alignas(16) TcHdr hdr[NV_MAX];            // tile t at hdr[t % nv]; hdr.dep is a 16-B bulk-copy destination
   float red[2][2][4][NQ];                   // [group][max / sum][warp][column]
   int32_t flag[2][4];
   int32_t gt[2][2];                         // ring tile index in group g's S slot b (-1: no more tiles)
@@ -357,6 +362,7 @@ struct TcArgs {
   const uint16_t* k_new; // [nl][B][Hkv][D]: appended to the arena by the producer warp
   const uint16_t* v_new;
   uint32_t* evdone;      // per-evictee staged-row counters (cumulative; the D2H stream waits on them)
+  int32_t nk, nv;        // ring shape of this launch (2 + 4 or 3 + 3 slots)
   Feed feed;             // host-fed step: per-chunk ready words (s3_decode_step_host)
 };
 
@@ -396,9 +402,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // the storer takes part in the ring only when this step shifts rows
   const bool fused = a.ctrl[CTRL_FUSED] != 0;
+  const int nk = a.nk, nv = a.nv;
   if (tid == 0) {
-    for (int i = 0; i < NK; ++i) { mb_init(&S.kfull[i], 1); mb_init(&S.kempty[i], fused ? 2 : 1); }
-    for (int i = 0; i < NV; ++i) { mb_init(&S.vfull[i], 1); mb_init(&S.vempty[i], fused ? 2 : 1); }
+    for (int i = 0; i < nk; ++i) { mb_init(&S.kfull[i], 1); mb_init(&S.kempty[i], fused ? 2 : 1); }
+    for (int i = 0; i < nv; ++i) { mb_init(&S.vfull[i], 1); mb_init(&S.vempty[i], fused ? 2 : 1); }
     for (int g = 0; g < 2; ++g) {
       for (int b = 0; b < 2; ++b) { mb_init(&S.s_full[g][b], 2); mb_init(&S.s_empty[g][b], 4); }
       mb_init(&S.p_full[g], 4);
@@ -409,9 +416,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   // V buffers start at zero: rows a tile does not load keep finite (zero or earlier valid) data
-  for (int st = 0; st < NV; ++st)
+  for (int st = 0; st < nv; ++st)
     for (int i = tid; i < KV_BYTES / 16; i += blockDim.x)
-      reinterpret_cast<uint4*>(vslot(smem, st))[i] = make_uint4(0, 0, 0, 0);
+      reinterpret_cast<uint4*>(vslot(smem, st, nk, nv))[i] = make_uint4(0, 0, 0, 0);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(su32(&S.tmem_base)),
@@ -457,11 +464,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
       }
       if (w >= groups_total) {
         if (lane == 0) {
-          mb_wait(&S.kempty[t % NK], ((uint32_t)(t / NK) & 1u) ^ 1u);
-          mb_wait(&S.vempty[t % NV], ((uint32_t)(t / NV) & 1u) ^ 1u);
-          S.hdr[t % NV].item = -1;
-          mb_arrive(&S.kfull[t % NK]);
-          mb_arrive(&S.vfull[t % NV]);
+          mb_wait(&S.kempty[t % nk], ((uint32_t)(t / nk) & 1u) ^ 1u);
+          mb_wait(&S.vempty[t % nv], ((uint32_t)(t / nv) & 1u) ^ 1u);
+          S.hdr[t % nv].item = -1;
+          mb_arrive(&S.kfull[t % nk]);
+          mb_arrive(&S.vfull[t % nv]);
         }
         break;
       }
@@ -504,9 +511,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
           const int item = w * a.Hkv + g;
           const int qrow = (li * a.B + un.b) * a.H + g * a.G;
           for (int r = 0; r < nrows; r += TM) {
-            const int ks = t % NK, vs = t % NV;
-            mb_wait(&S.kempty[ks], ((uint32_t)(t / NK) & 1u) ^ 1u);
-            mb_wait(&S.vempty[vs], ((uint32_t)(t / NV) & 1u) ^ 1u);
+            const int ks = t % nk, vs = t % nv;
+            mb_wait(&S.kempty[ks], ((uint32_t)(t / nk) & 1u) ^ 1u);
+            mb_wait(&S.vempty[vs], ((uint32_t)(t / nv) & 1u) ^ 1u);
             TC_TRACE_AT(t, 0);
             const int nv = min(TM, nrows - r);
             TcHdr& h = S.hdr[vs];
@@ -520,8 +527,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
             h.prog = (uint32_t)(glast * TC_HEAD_STRIDE + r + nv) |
                      (glast == a.Hkv - 1 && r + TM >= nrows ? TC_PROG_FULL : 0u);
             const int groups = (nv + 7) / 8;   // 8-row groups (one 128B-swizzle atom per column block)
-            uint8_t* sk = kslot(smem, t);
-            uint8_t* sv = vslot(smem, t);
+            uint8_t* sk = kslot(smem, t, nk);
+            uint8_t* sv = vslot(smem, t, nk, nv);
             uint8_t* sq = sk + KV_BYTES;
             const bool dep = fused && mv;
             mb_expect(&S.kfull[ks], (uint32_t)(np * groups * 8 * 128 * 2 + Q_BYTES + (dep ? 16 : 0)));
@@ -553,12 +560,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
       constexpr uint32_t id_s = idesc(0, NQ), id_o = idesc(1, 2 * NQ);
       int kc[2] = {0, 0};                       // tiles handed to each group so far
       auto issue_s = [&](int t) -> int {        // returns the tile's index within its group
-        const int g = S.hdr[t % NV].iseq & 1;
+        const int g = S.hdr[t % nv].iseq & 1;
         const int k = kc[g]++;
         const int sb = k & 1;
         mb_wait(&S.s_empty[g][sb], ((uint32_t)(k >> 1) & 1u) ^ 1u);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint8_t* sk = kslot(smem, t);
+        const uint8_t* sk = kslot(smem, t, nk);
         const uint8_t* sq = sk + KV_BYTES;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {        // S^T = K . Q^T over d in steps of 16
@@ -567,7 +574,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
               kk > 0);
         }
         commit(&S.s_full[g][sb]);
-        commit(&S.kempty[t % NK]);              // the K slot is free once these MMAs have read it
+        commit(&S.kempty[t % nk]);              // the K slot is free once these MMAs have read it
         S.gt[g][sb] = t;
         mb_arrive(&S.s_full[g][sb]);            // releases gt together with the slot
         return k;
@@ -587,10 +594,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
       } else {
         int kt = issue_s(0);
         for (int t = 0;; ++t) {
-          const int vs = t % NV;
-          mb_wait(&S.kfull[(t + 1) % NK], (uint32_t)((t + 1) / NK) & 1u);
+          const int vs = t % nv;
+          mb_wait(&S.kfull[(t + 1) % nk], (uint32_t)((t + 1) / nk) & 1u);
           TC_TRACE_AT(t + 1, 3);
-          const bool end = S.hdr[(t + 1) % NV].item < 0;
+          const bool end = S.hdr[(t + 1) % nv].item < 0;
           const int kt1 = end ? 0 : issue_s(t + 1);
           const bool first = S.hdr[vs].flags & 1;
           const bool last = S.hdr[vs].flags & 2;
@@ -598,10 +605,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
           if (first)   // O buffer g must have been read by the epilogue of item iseq - 2
             mb_wait(&S.o_free[g], ((uint32_t)(iseq >> 1) & 1u) ^ 1u);
           mb_wait(&S.p_full[g], (uint32_t)kt & 1u);
-          mb_wait(&S.vfull[vs], (uint32_t)(t / NV) & 1u);   // V landed (the softmax waited too if it zeroed rows)
+          mb_wait(&S.vfull[vs], (uint32_t)(t / nv) & 1u);   // V landed (the softmax waited too if it zeroed rows)
           TC_TRACE_AT(t, 4);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          const uint8_t* sv = vslot(smem, t);
+          const uint8_t* sv = vslot(smem, t, nk, nv);
           const uint8_t* sp = pbuf + g * PBUF_BYTES;
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {          // [O_hi | O_lo]^T += V^T . [P_hi | P_lo]^T, rows in steps of 16
@@ -623,9 +630,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
     if (fused) {
       int pending = -1;                   // tile whose bulk stores may still read shared memory
       for (int t = 0;; ++t) {
-        mb_wait(&S.kfull[t % NK], (uint32_t)(t / NK) & 1u);
-        mb_wait(&S.vfull[t % NV], (uint32_t)(t / NV) & 1u);
-        const TcHdr h = S.hdr[t % NV];
+        mb_wait(&S.kfull[t % nk], (uint32_t)(t / nk) & 1u);
+        mb_wait(&S.vfull[t % nv], (uint32_t)(t / nv) & 1u);
+        const TcHdr h = S.hdr[t % nv];
         if (h.item < 0) break;
         const int w = h.item / a.Hkv;     // unit-layer ticket = progress slot
         if (lane == 0) {
@@ -656,8 +663,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
           const int np = PACK ? 1 << hdr_lognp(h) : 1;
           const int seg = TM / np;
           for (int sgi = 0; sgi < np; ++sgi) {       // one segment per packed KV head
-            const uint8_t* sk = kslot(smem, t) + sgi * (seg / 8) * 2048;
-            const uint8_t* sv = vslot(smem, t) + sgi * (seg / 8) * 2048;
+            const uint8_t* sk = kslot(smem, t, nk) + sgi * (seg / 8) * 2048;
+            const uint8_t* sv = vslot(smem, t, nk, nv) + sgi * (seg / 8) * 2048;
             const int colk = (a.l0 + h.li) * 2 * a.Hkv * DH + (h.g + sgi) * DH;   // elements
             const int colv = colk + a.Hkv * DH;
             if (lane == 0) {
@@ -690,15 +697,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
           if (pending >= 0) {
             if (stores) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
             else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-            mb_arrive(&S.kempty[pending % NK]);
-            mb_arrive(&S.vempty[pending % NV]);
+            mb_arrive(&S.kempty[pending % nk]);
+            mb_arrive(&S.vempty[pending % nv]);
             pending = -1;
           }
           if (stores) {
             pending = t;
           } else {
-            mb_arrive(&S.kempty[t % NK]);
-            mb_arrive(&S.vempty[t % NV]);
+            mb_arrive(&S.kempty[t % nk]);
+            mb_arrive(&S.vempty[t % nv]);
           }
           if (h.mode == UNIT_STAGE && a.evdone) {
             // the tile's evictee rows are final in staging once its stores complete (the
@@ -714,8 +721,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
       if (lane == 0) {
         asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         if (pending >= 0) {
-          mb_arrive(&S.kempty[pending % NK]);
-          mb_arrive(&S.vempty[pending % NV]);
+          mb_arrive(&S.kempty[pending % nk]);
+          mb_arrive(&S.vempty[pending % nv]);
         }
         asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
       }
@@ -746,7 +753,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
       const int t = S.gt[grp][sb];
       if (t < 0) break;
       if (lane == 0 && warp == 2) TC_TRACE_AT(t, 6);
-      const TcHdr h = S.hdr[t % NV];
+      const TcHdr h = S.hdr[t % nv];
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       float s[NC];
       tmem_ld<NC>(lane_base + scol(grp, sb), s);
@@ -821,8 +828,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
         *reinterpret_cast<__nv_bfloat16*>(sp + NQ * 128 + sw) = lo;   // row 16 + c: same swizzle phase
       }
       if (!valid && rs < ((h.nvalid + 15) & ~15)) {  // loaded rows past the slot's resident rows: V := 0
-        mb_wait(&S.vfull[t % NV], (uint32_t)(t / NV) & 1u);   // after the V load has landed
-        uint8_t* sv = vslot(smem, t);
+        mb_wait(&S.vfull[t % nv], (uint32_t)(t / nv) & 1u);   // after the V load has landed
+        uint8_t* sv = vslot(smem, t, nk, nv);
 #pragma unroll
         for (int kb = 0; kb < 2; ++kb)
 #pragma unroll
@@ -990,7 +997,7 @@ cudaError_t launch_attn_tc(const Shape& sh, const uint16_t* q, const uint16_t* k
                            float* partials, const Unit* units, const Split* splits, const DepDesc* desc,
                            unsigned long long* progress, uint32_t epoch, int32_t* ctrl, int32_t B, int32_t l0,
                            int32_t nl, int32_t grid_attn, int32_t grid_combine, const Feed& feed, uint32_t* evdone,
-                           cudaStream_t st) {
+                           int32_t short_items, cudaStream_t st) {
   TcMaps maps;
   // staging rows (evicted slots' KV, token-major like the arena); without staging k_prep never fuses an eviction
   const int64_t stage_rows = staging ? staging_bytes / sh.kvpt : 0;
@@ -1016,6 +1023,10 @@ cudaError_t launch_attn_tc(const Shape& sh, const uint16_t* q, const uint16_t* k
   a.arena = reinterpret_cast<uint8_t*>(arena); a.staging = staging; a.kvpt = sh.kvpt;
   a.desc = desc; a.progress = progress; a.epoch = epoch;
   a.k_new = k_new; a.v_new = v_new; a.feed = feed; a.evdone = evdone;
+  static const int ring = [] { const char* e = getenv("S3_TC_RING"); return e ? atoi(e) : 0; }();   // A/B: 24 or 33
+  const bool two_four = ring ? ring == 24 : short_items != 0;
+  a.nk = two_four ? 2 : 3;
+  a.nv = two_four ? 4 : 3;
   static const int pack = [] { const char* e = getenv("S3_TC_PACK"); return e ? atoi(e) : 1; }();
   a.pmax = pack ? (a.G <= 8 ? 8 : 16) / a.G : 1;   // S3_TC_PACK=0: one KV head per tile (A/B)
   const dim3 grid(grid_attn), block(TC_THREADS);

@@ -731,12 +731,21 @@ s3_status s3_decode_step(s3_ctx* ctx, int32_t l0, int32_t nl, const void* q, con
     ctx->attn_epoch++;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx->prof.on) { e0 = ctx->prof.get(); e1 = ctx->prof.get(); cudaEventRecord(e0, ctx->st); }
+    // tensor-core kernel's ring shape: items mostly one tile long (mean resident rows <= 96)
+    // take 2 K + 4 V slots, longer ones 3 + 3 (see s3_attn_tc.cu)
+    int32_t short_items = 0;
+    if (ctx->cfg.attn_variant == 2) {
+      int64_t rows = 0;
+      for (const DSlot& sl : ctx->slots_h) rows += sl.len + 1;
+      short_items = rows <= 96LL * B ? 1 : 0;
+    }
     if (ctx->cfg.attn_variant == 2)
       CK(launch_attn_tc(ctx->sh, (const uint16_t*)q, (const uint16_t*)k_new, (const uint16_t*)v_new,
                         (uint16_t*)ctx->buf.arena, ctx->cfg.arena_rows,
                         ctx->buf.staging ? stage_ptr(ctx, ctx->stage_cur) : nullptr, stage_bytes(ctx), out, ctx->partials,
                         ctx->units, ctx->splits, ctx->desc, ctx->progress, ctx->attn_epoch, ctx->ctrl, B, l0, nl,
-                        ctx->grid_attn, ctx->grid_combine, ctx->feed, ev_counters(ctx), ctx->st), "k_attn_tc");
+                        ctx->grid_attn, ctx->grid_combine, ctx->feed, ev_counters(ctx), short_items, ctx->st),
+         "k_attn_tc");
     else
       CK(launch_attn(ctx->sh, (const uint16_t*)q, (const uint16_t*)k_new, (const uint16_t*)v_new,
                      (uint16_t*)ctx->buf.arena, ctx->buf.staging ? stage_ptr(ctx, ctx->stage_cur) : nullptr, out,

@@ -1106,8 +1106,19 @@ __global__ void __launch_bounds__(576, 1) k_attn_tma(AttnArgs a, int32_t ns) {
     if (lane == 0) {
       int k = 0;
       int ready_max = -1;               // host-fed step: highest chunk known to have landed
+      // the next ticket and its unit record are fetched one item ahead, so their latency
+      // overlaps this item's row loads (the smallest unfinished ticket is still always
+      // some CTA's current item: deadlock freedom unchanged)
+      int item_next = atomicAdd(&a.ctrl[CTRL_ITEM], 1);
+      Unit un_next{};
+      if (item_next < total) un_next = a.units[item_next / a.nl];
       for (;;) {
-        const int item = atomicAdd(&a.ctrl[CTRL_ITEM], 1);
+        const int item = item_next;
+        const Unit un = un_next;
+        if (item < total) {
+          item_next = atomicAdd(&a.ctrl[CTRL_ITEM], 1);
+          if (item_next < total) un_next = a.units[item_next / a.nl];
+        }
         if (item >= total) {
           const int st = k % ns;
           mbar_wait(&empty[st], ((uint32_t)(k / ns) & 1u) ^ 1u);
@@ -1115,8 +1126,7 @@ __global__ void __launch_bounds__(576, 1) k_attn_tma(AttnArgs a, int32_t ns) {
           mbar_arrive(&full[st]);
           break;
         }
-        const int u = item / a.nl, li = item - u * a.nl;
-        const Unit un = a.units[u];
+        const int li = item % a.nl;
         if (a.feed.ready) {
           // chunks land in order: waiting for this unit's chunk covers every earlier one
           const int c = un.b / a.feed.cb;
