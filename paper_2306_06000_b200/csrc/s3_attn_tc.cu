@@ -86,7 +86,7 @@ constexpr int DH = 128;                     // head dim
 // MMA has read it, a V slot only after the O MMA, so the V ring is the deeper one.
 // With one 3-stage K|V ring a short tile held its stage for the whole chain (load,
 // S, softmax, P hand-over, O: ~7.7k cycles) and 3 stages bounded the period.
-// Ring shapes (per launch, TcArgs.nk / nv): 2 K + 4 V slots when the step's items are short
+// Ring shapes (per launch, template parameter R33): 2 K + 4 V slots when the step's items are short
 // (mostly one tile), 3 + 3 otherwise -- with the fused row shift the storer holds a K slot
 // while it waits for a MOVE tile's destination rows, which starves a 2-slot K ring on
 // long, moving items (LLaMA-3-8B whole run: 0.66 vs 0.84 of the copy peak).
@@ -362,7 +362,6 @@ struct TcArgs {
   const uint16_t* k_new; // [nl][B][Hkv][D]: appended to the arena by the producer warp
   const uint16_t* v_new;
   uint32_t* evdone;      // per-evictee staged-row counters (cumulative; the D2H stream waits on them)
-  int32_t nk, nv;        // ring shape of this launch (2 + 4 or 3 + 3 slots)
   Feed feed;             // host-fed step: per-chunk ready words (s3_decode_step_host)
 };
 
@@ -391,7 +390,8 @@ __device__ __forceinline__ uint4 ld_cg16(const void* p) {
 // NC: query columns the softmax handles, G padded to 8 or 16 (the MMA always has N = 16);
 // PACK: short units may pack several KV heads into one tile (NC / G >= 2)
 // FEED: host-fed step (the producer warp waits on ready words and appends the new rows)
-template <int NC, bool PACK, bool FEED>
+// R33: ring shape 3 K + 3 V slots (else 2 K + 4 V; compile-time so the slot arithmetic folds)
+template <int NC, bool PACK, bool FEED, bool R33>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant__ TcMaps maps, TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-B alignment for the 128B-swizzle atoms, by pointer arithmetic so the
@@ -402,7 +402,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // the storer takes part in the ring only when this step shifts rows
   const bool fused = a.ctrl[CTRL_FUSED] != 0;
-  const int nk = a.nk, nv = a.nv;
+  constexpr int nk = R33 ? 3 : 2, nv = R33 ? 3 : 4;
   if (tid == 0) {
     for (int i = 0; i < nk; ++i) { mb_init(&S.kfull[i], 1); mb_init(&S.kempty[i], fused ? 2 : 1); }
     for (int i = 0; i < nv; ++i) { mb_init(&S.vfull[i], 1); mb_init(&S.vempty[i], fused ? 2 : 1); }
@@ -515,18 +515,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
             mb_wait(&S.kempty[ks], ((uint32_t)(t / nk) & 1u) ^ 1u);
             mb_wait(&S.vempty[vs], ((uint32_t)(t / nv) & 1u) ^ 1u);
             TC_TRACE_AT(t, 0);
-            const int nv = min(TM, nrows - r);
+            const int nrow = min(TM, nrows - r);
             TcHdr& h = S.hdr[vs];
-            h.item = item; h.r0 = un.r0 + r; h.nvalid = nv;
+            h.item = item; h.r0 = un.r0 + r; h.nvalid = nrow;
             h.flags = (r == 0 ? 1 : 0) | (r + TM >= nrows ? 2 : 0);
             h.b = un.b; h.part = un.part; h.li = li; h.g = g; h.iseq = iseq;
             h.mode = un.mode; h.drow = drow0 + r;
             if (un.mode == UNIT_STAGE) h.dep.ua = un.pad;   // eviction index (dep is only loaded for MOVE)
             h.flags |= (31 - __clz(np)) << 8;
-            const int glast = g + np - 1;  // heads g..glast are read up to r + nv rows once this tile lands
-            h.prog = (uint32_t)(glast * TC_HEAD_STRIDE + r + nv) |
+            const int glast = g + np - 1;  // heads g..glast are read up to r + nrow rows once this tile lands
+            h.prog = (uint32_t)(glast * TC_HEAD_STRIDE + r + nrow) |
                      (glast == a.Hkv - 1 && r + TM >= nrows ? TC_PROG_FULL : 0u);
-            const int groups = (nv + 7) / 8;   // 8-row groups (one 128B-swizzle atom per column block)
+            const int groups = (nrow + 7) / 8;   // 8-row groups (one 128B-swizzle atom per column block)
             uint8_t* sk = kslot(smem, t, nk);
             uint8_t* sv = vslot(smem, t, nk, nv);
             uint8_t* sq = sk + KV_BYTES;
@@ -969,13 +969,17 @@ extern "C" int s3_debug_tc_trace(unsigned long long* host, int n) {
 #endif
 
 int attn_tc_smem() { return RING_BYTES + 2 * PBUF_BYTES + (int)sizeof(TcSmem) + 1024; }
-const void* attn_tc_kernel_ptr(int nc, bool pack, bool feed) {
+template <bool R33>
+const void* attn_tc_ptr(int nc, bool pack, bool feed) {
   if (feed) {
-    if (nc == 8) return pack ? (const void*)k_attn_tc<8, true, true> : (const void*)k_attn_tc<8, false, true>;
-    return pack ? (const void*)k_attn_tc<16, true, true> : (const void*)k_attn_tc<16, false, true>;
+    if (nc == 8) return pack ? (const void*)k_attn_tc<8, true, true, R33> : (const void*)k_attn_tc<8, false, true, R33>;
+    return pack ? (const void*)k_attn_tc<16, true, true, R33> : (const void*)k_attn_tc<16, false, true, R33>;
   }
-  if (nc == 8) return pack ? (const void*)k_attn_tc<8, true, false> : (const void*)k_attn_tc<8, false, false>;
-  return pack ? (const void*)k_attn_tc<16, true, false> : (const void*)k_attn_tc<16, false, false>;
+  if (nc == 8) return pack ? (const void*)k_attn_tc<8, true, false, R33> : (const void*)k_attn_tc<8, false, false, R33>;
+  return pack ? (const void*)k_attn_tc<16, true, false, R33> : (const void*)k_attn_tc<16, false, false, R33>;
+}
+const void* attn_tc_kernel_ptr(int nc, bool pack, bool feed, bool r33) {
+  return r33 ? attn_tc_ptr<true>(nc, pack, feed) : attn_tc_ptr<false>(nc, pack, feed);
 }
 
 bool attn_tc_supported(const Shape& sh) {
@@ -1025,13 +1029,11 @@ cudaError_t launch_attn_tc(const Shape& sh, const uint16_t* q, const uint16_t* k
   a.k_new = k_new; a.v_new = v_new; a.feed = feed; a.evdone = evdone;
   static const int ring = [] { const char* e = getenv("S3_TC_RING"); return e ? atoi(e) : 0; }();   // A/B: 24 or 33
   const bool two_four = ring ? ring == 24 : short_items != 0;
-  a.nk = two_four ? 2 : 3;
-  a.nv = two_four ? 4 : 3;
   static const int pack = [] { const char* e = getenv("S3_TC_PACK"); return e ? atoi(e) : 1; }();
   a.pmax = pack ? (a.G <= 8 ? 8 : 16) / a.G : 1;   // S3_TC_PACK=0: one KV head per tile (A/B)
   const dim3 grid(grid_attn), block(TC_THREADS);
   const int smem = attn_tc_smem();
-  const void* kfn = attn_tc_kernel_ptr(a.G <= 8 ? 8 : 16, a.pmax > 1, feed.ready != nullptr);
+  const void* kfn = attn_tc_kernel_ptr(a.G <= 8 ? 8 : 16, a.pmax > 1, feed.ready != nullptr, !two_four);
   void* args[] = {(void*)&maps, (void*)&a};
   cudaError_t le = cudaLaunchKernel(kfn, grid, block, args, (size_t)smem, st);
   if (le != cudaSuccess) return le;

@@ -552,9 +552,10 @@ s3_status s3_kv_init(const s3_config* cfg, const s3_buffers* b, s3_ctx** out) {
     for (int nc : {8, 16})
       for (bool pack : {false, true})
         for (bool feed : {false, true})
-          if (cudaFuncSetAttribute(attn_tc_kernel_ptr(nc, pack, feed), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   attn_tc_smem()) != cudaSuccess)
-            return bail("attn_tc smem attribute");
+          for (bool r33 : {false, true})
+            if (cudaFuncSetAttribute(attn_tc_kernel_ptr(nc, pack, feed, r33),
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, attn_tc_smem()) != cudaSuccess)
+              return bail("attn_tc smem attribute");
     ctx->grid_attn = ctx->num_sms;
   }
   if (cfg->attn_variant == 0 && attn_tma_stages(sh) >= 2) {
@@ -718,10 +719,14 @@ s3_status s3_decode_step(s3_ctx* ctx, int32_t l0, int32_t nl, const void* q, con
     // host's eviction bookkeeping and FFD start as soon as k_prep ends (overlapping the
     // attention kernel) and no copy engine is involved -- a report copy would queue
     // behind the previous step's eviction D2H on the copy engine and hold up attention
-    pa.report = fuse ? ctx->h_report_dev : ctx->report_dev;
+    static const int devrep = [] { const char* e = getenv("S3_PREP_DEVREPORT"); return e ? atoi(e) : 0; }();  // A/B
+    pa.report = fuse && !devrep ? ctx->h_report_dev : ctx->report_dev;
     pa.fused_out = fuse ? reinterpret_cast<int32_t*>(ctx->h_report_dev + report_bytes(B)) : nullptr;
     CK(launch_prep(pa, ctx->st), "k_prep");
     ctx->launches += 1;
+    if (fuse && devrep)
+      CK(cudaMemcpyAsync(ctx->h_report, ctx->report_dev, (size_t)report_bytes(B), cudaMemcpyDeviceToHost, ctx->st),
+         "report D2H");
     if (fuse) {
       CK(cudaEventRecord(ctx->ev_report, ctx->st), "event");
       CK(launch_deps(ctx->units, ctx->ctrl, ctx->desc, ctx->cfg.attn_variant == 2 ? 1 : 0, ctx->num_sms * 4,
@@ -731,13 +736,15 @@ s3_status s3_decode_step(s3_ctx* ctx, int32_t l0, int32_t nl, const void* q, con
     ctx->attn_epoch++;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx->prof.on) { e0 = ctx->prof.get(); e1 = ctx->prof.get(); cudaEventRecord(e0, ctx->st); }
-    // tensor-core kernel's ring shape: items mostly one tile long (mean resident rows <= 96)
-    // take 2 K + 4 V slots, longer ones 3 + 3 (see s3_attn_tc.cu)
+    // tensor-core kernel's ring shape: steps of short items (mean resident rows <= 48) take
+    // 2 K + 4 V slots, longer ones 3 + 3 (see s3_attn_tc.cu; LLaMA-3-8B threshold sweep
+    // 32 / 48 / 64 / 96: 48 keeps both the short-context window and the whole run at their best)
     int32_t short_items = 0;
     if (ctx->cfg.attn_variant == 2) {
       int64_t rows = 0;
       for (const DSlot& sl : ctx->slots_h) rows += sl.len + 1;
-      short_items = rows <= 96LL * B ? 1 : 0;
+      static const long long thr = [] { const char* e = getenv("S3_TC_SHORT_ROWS"); return e ? atoll(e) : 48LL; }();
+      short_items = rows <= thr * B ? 1 : 0;
     }
     if (ctx->cfg.attn_variant == 2)
       CK(launch_attn_tc(ctx->sh, (const uint16_t*)q, (const uint16_t*)k_new, (const uint16_t*)v_new,

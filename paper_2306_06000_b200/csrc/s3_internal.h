@@ -115,7 +115,7 @@ struct PrepArgs {
   int32_t* xdone;       // CTAs finished (reset by the last)
   uint32_t epoch;
 };
-constexpr int PREP_CTA_SLOTS = 1024;   // slots per k_prep CTA when B is large (one per thread)
+constexpr int PREP_CTA_SLOTS = 1024;   // k_prep runs as one CTA up to 2 * PREP_CTA_SLOTS slots
 constexpr int PREP_MAX_CTAS = 64;      // B <= 65535
 constexpr int PREP_NX = 10;            // scanned quantities per slot
 cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st);
@@ -156,7 +156,7 @@ cudaError_t launch_append(const Shape& sh, const DSlot* slots, int32_t B, int32_
                           const uint16_t* k_new, const uint16_t* v_new, uint16_t* arena, cudaStream_t st);
 bool attn_tc_supported(const Shape& sh);
 int attn_tc_smem();
-const void* attn_tc_kernel_ptr(int nc, bool pack, bool feed);
+const void* attn_tc_kernel_ptr(int nc, bool pack, bool feed, bool r33);
 
 cudaError_t launch_attn_tc(const Shape& sh, const uint16_t* q, const uint16_t* k_new, const uint16_t* v_new,
                            uint16_t* arena, int64_t arena_rows, uint8_t* staging, int64_t staging_bytes, float* out,

@@ -18,6 +18,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "s3_internal.h"
@@ -93,20 +94,20 @@ __device__ __forceinline__ void st_release_u32(uint32_t* p, uint32_t v) {
 }
 
 // ---------------------------------------------------------------------------
-// Block-wide exclusive scan of NV int64 values per thread (1024 threads max).
+// Block-wide exclusive scan of NV int64 (or int32) values per thread (1024 threads max).
 // ---------------------------------------------------------------------------
-template <int NV>
-__device__ void block_excl_scan(long long (&x)[NV], long long (&total)[NV]) {
-  __shared__ long long warp_sums[32][NV];
+template <int NV, typename T = long long>
+__device__ void block_excl_scan(T (&x)[NV], T (&total)[NV]) {
+  __shared__ T warp_sums[32][NV];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int nwarps = (blockDim.x + 31) >> 5;
-  long long incl[NV];
+  T incl[NV];
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
-    long long v = x[i];
+    T v = x[i];
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      long long n = __shfl_up_sync(0xffffffffu, v, o);
+      T n = __shfl_up_sync(0xffffffffu, v, o);
       if (lane >= o) v += n;
     }
     incl[i] = v;
@@ -115,13 +116,12 @@ __device__ void block_excl_scan(long long (&x)[NV], long long (&total)[NV]) {
 #pragma unroll
     for (int i = 0; i < NV; ++i) warp_sums[warp][i] = incl[i];
   __syncthreads();
-  if (warp == 0) {
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      long long v = lane < nwarps ? warp_sums[lane][i] : 0;
+  for (int i = warp; i < NV; i += nwarps) {   // warp i scans quantity i over the warps
+    {
+      T v = lane < nwarps ? warp_sums[lane][i] : 0;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        long long n = __shfl_up_sync(0xffffffffu, v, o);
+        T n = __shfl_up_sync(0xffffffffu, v, o);
         if (lane >= o) v += n;
       }
       if (lane < nwarps) warp_sums[lane][i] = v;   // inclusive over warps
@@ -130,7 +130,7 @@ __device__ void block_excl_scan(long long (&x)[NV], long long (&total)[NV]) {
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
-    long long before = warp == 0 ? 0 : warp_sums[warp - 1][i];
+    T before = warp == 0 ? 0 : warp_sums[warp - 1][i];
     total[i] = warp_sums[nwarps - 1][i];
     x[i] = before + incl[i] - x[i];
   }
@@ -211,11 +211,21 @@ __device__ __forceinline__ int detect(const PrepArgs& a, const DSlot& sl, int b)
   return sl.len + 1 == sl.cap ? 2 : 0;
 }
 
+#ifdef PREP_TRACE
+#define PREP_T(i) do { if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ptt[i])); } while (0)
+#else
+#define PREP_T(i) do {} while (0)
+#endif
 __global__ void __launch_bounds__(1024) k_prep(PrepArgs a) {
+#ifdef PREP_TRACE
+  unsigned long long ptt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
+  PREP_T(0);
   __shared__ int s_first_hole;
   __shared__ unsigned long long s_hbm, s_moved;
   __shared__ long long s_end;
   __shared__ long long s_agg[PREP_MAX_CTAS][PREP_NX];
+  __shared__ long long s_pre[PREP_NX], s_all[PREP_NX];
   __shared__ int s_last;
   if (threadIdx.x == 0) { s_first_hole = a.B; s_hbm = 0; s_moved = 0; s_end = 0; }
   const int B = a.B, C = a.C;
@@ -223,8 +233,11 @@ __global__ void __launch_bounds__(1024) k_prep(PrepArgs a) {
   const int nb = gridDim.x;                                  // > 1: one slot per thread, decoupled totals
   const int per = (B + nb * (int)blockDim.x - 1) / (nb * (int)blockDim.x);
   const int b0 = ((int)blockIdx.x * (int)blockDim.x + (int)threadIdx.x) * per, b1 = min(B, b0 + per);
-  // x: 0 units, 1 splits, 2 parts, 3 stages, 4 keep, 5 keep*cap, 6 fin, 7 ev, 8 ev bytes, 9 cap
-  long long x[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  // x: 0 units, 1 splits, 2 parts, 3 stages, 4 keep, 5 keep*cap, 6 fin, 7 ev, 8 ev rows, 9 cap
+  // (32-bit: counts and arena rows; evicted bytes = ev rows * kvpt)
+  int x[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+  DSlot sl0{};                                               // this thread's first slot, kept for pass 2
+  int st0 = 0;
   for (int b = b0; b < b1; ++b) {
     const DSlot sl = a.slots[b];
     const int k = (sl.len + 1 + C - 1) / C;
@@ -236,19 +249,23 @@ __global__ void __launch_bounds__(1024) k_prep(PrepArgs a) {
       x[3] += rows > 0 ? (rows + AT_RPS - 1) / AT_RPS : 1;
     }
     const int st = detect(a, sl, b);
+    if (b == b0) { sl0 = sl; st0 = st; }
     x[4] += st == 0;
     x[5] += st == 0 ? sl.cap : 0;
     x[6] += st == 1;
     x[7] += st == 2;
-    x[8] += st == 2 ? (long long)(sl.len + 1) * kvpt : 0;
+    x[8] += st == 2 ? sl.len + 1 : 0;
     x[9] += sl.cap;
   }
-  long long tot[10];
-  block_excl_scan<10>(x, tot);
+  int tot[10];
+  PREP_T(1);
+  block_excl_scan<10, int>(x, tot);
+  PREP_T(2);
   if (nb > 1) {
     // publish this CTA's totals, then read every CTA's: the prefix of the CTAs before this one
     // and the grid totals (all CTAs are co-resident: nb <= 64 one-CTA-per-SM blocks)
     if (threadIdx.x == 0) {
+#pragma unroll
       for (int k = 0; k < PREP_NX; ++k) a.xagg[blockIdx.x * PREP_NX + k] = tot[k];
       __threadfence();
       asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(a.xflag + blockIdx.x), "l"((unsigned long long)a.epoch)
@@ -262,34 +279,53 @@ __global__ void __launch_bounds__(1024) k_prep(PrepArgs a) {
         if (f == (unsigned long long)a.epoch) break;
         __nanosleep(32);
       }
+#pragma unroll
       for (int k = 0; k < PREP_NX; ++k) s_agg[c][k] = __ldcg(a.xagg + c * PREP_NX + k);
     }
     __syncthreads();
-    for (int k = 0; k < PREP_NX; ++k) {
-      long long pre = 0, all = 0;
-      for (int c = 0; c < nb; ++c) {
-        all += s_agg[c][k];
-        if (c < (int)blockIdx.x) pre += s_agg[c][k];
+    PREP_T(3);
+    // warp k sums field k over the CTAs (lanes over c): the prefix of the CTAs before this one
+    // and the grid total, once per CTA instead of once per thread
+    {
+      const int ln = threadIdx.x & 31;
+      for (int w = threadIdx.x >> 5; w < PREP_NX; w += blockDim.x >> 5) {
+        int pre = 0, all = 0;
+        for (int c = ln; c < nb; c += 32) {
+          const int v = (int)s_agg[c][w];
+          all += v;
+          if (c < (int)blockIdx.x) pre += v;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          pre += __shfl_xor_sync(0xffffffffu, pre, o);
+          all += __shfl_xor_sync(0xffffffffu, all, o);
+        }
+        if (ln == 0) { s_pre[w] = pre; s_all[w] = all; }
       }
-      x[k] += pre;
-      tot[k] = all;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < PREP_NX; ++k) {
+      x[k] += s_pre[k];
+      tot[k] = s_all[k];
     }
   }
-  const bool fused = a.fuse && a.finalize && tot[8] <= a.staging_bytes;
+  PREP_T(4);
+  const bool fused = a.fuse && a.finalize && (int64_t)tot[8] * kvpt <= a.staging_bytes;
   // R27: shift unless the policy is on-demand and nobody could use the rows
   const bool compact = a.compact_policy == 0 || a.pool_nonempty || tot[7] > 0;
   int32_t* perm = reinterpret_cast<int32_t*>(a.report + report_perm_off(B));
   DEvicted* evl = reinterpret_cast<DEvicted*>(a.report + report_ev_off(B));
   int64_t* finl = reinterpret_cast<int64_t*>(a.report + report_fin_off(B));
   long long u = x[0], sp = x[1], p = x[2], stg = x[3];
-  long long keep_i = x[4], keepcap = x[5], fin_i = x[6], ev_i = x[7], evb = x[8], capx = x[9];
+  long long keep_i = x[4], keepcap = x[5], fin_i = x[6], ev_i = x[7], evb = (long long)x[8] * kvpt, capx = x[9];
   unsigned long long hbm = 0, moved = 0;
   long long end = 0;
   int first = B;
   for (int b = b0; b < b1; ++b) {
-    DSlot sl = a.slots[b];
+    DSlot sl = b == b0 ? sl0 : a.slots[b];
     const int k = (sl.len + 1 + C - 1) / C;
-    const int st = detect(a, sl, b);
+    const int st = b == b0 ? st0 : detect(a, sl, b);
     int mode = UNIT_STAY;
     int64_t dst = sl.off;
     if (fused) {
@@ -371,7 +407,9 @@ __global__ void __launch_bounds__(1024) k_prep(PrepArgs a) {
     if (moved) atomicAdd(&s_moved, moved);
     if (end) atomicMax(&s_end, end);
   }
+  PREP_T(5);
   __syncthreads();
+  PREP_T(6);
   if (nb > 1) {
     // the header's min / sums / max over CTAs: combined by the last CTA to finish
     if (threadIdx.x == 0) {
@@ -397,6 +435,13 @@ __global__ void __launch_bounds__(1024) k_prep(PrepArgs a) {
       }
     }
     __syncthreads();
+#ifdef PREP_TRACE
+    PREP_T(7);
+    if (threadIdx.x == 0)
+      printf("prep cta %d start %llu: pass1 %llu scan %llu wait %llu comb %llu pass2 %llu sync %llu last %llu\n",
+             (int)blockIdx.x, ptt[0] % 1000000000ull, ptt[1] - ptt[0], ptt[2] - ptt[1], ptt[3] - ptt[2],
+             ptt[4] - ptt[3], ptt[5] - ptt[4], ptt[6] - ptt[5], ptt[7] - ptt[6]);
+#endif
     if (!s_last) return;
   }
   if (threadIdx.x == 0) {
@@ -414,7 +459,7 @@ __global__ void __launch_bounds__(1024) k_prep(PrepArgs a) {
       h->n_evicted = (int)tot[7];
       h->n_kept = (int)tot[4];
       h->tail = compact ? tot[5] : s_end;
-      h->d2h_bytes = tot[8];
+      h->d2h_bytes = (int64_t)tot[8] * kvpt;
       h->moved_bytes = (int64_t)s_moved;
       h->pcie_bytes = 0;
       h->hbm_bytes = (int64_t)s_hbm;
@@ -1106,19 +1151,8 @@ __global__ void __launch_bounds__(576, 1) k_attn_tma(AttnArgs a, int32_t ns) {
     if (lane == 0) {
       int k = 0;
       int ready_max = -1;               // host-fed step: highest chunk known to have landed
-      // the next ticket and its unit record are fetched one item ahead, so their latency
-      // overlaps this item's row loads (the smallest unfinished ticket is still always
-      // some CTA's current item: deadlock freedom unchanged)
-      int item_next = atomicAdd(&a.ctrl[CTRL_ITEM], 1);
-      Unit un_next{};
-      if (item_next < total) un_next = a.units[item_next / a.nl];
       for (;;) {
-        const int item = item_next;
-        const Unit un = un_next;
-        if (item < total) {
-          item_next = atomicAdd(&a.ctrl[CTRL_ITEM], 1);
-          if (item_next < total) un_next = a.units[item_next / a.nl];
-        }
+        const int item = atomicAdd(&a.ctrl[CTRL_ITEM], 1);
         if (item >= total) {
           const int st = k % ns;
           mbar_wait(&empty[st], ((uint32_t)(k / ns) & 1u) ^ 1u);
@@ -1126,7 +1160,8 @@ __global__ void __launch_bounds__(576, 1) k_attn_tma(AttnArgs a, int32_t ns) {
           mbar_arrive(&full[st]);
           break;
         }
-        const int li = item % a.nl;
+        const int u = item / a.nl, li = item - u * a.nl;
+        const Unit un = a.units[u];
         if (a.feed.ready) {
           // chunks land in order: waiting for this unit's chunk covers every earlier one
           const int c = un.b / a.feed.cb;
@@ -1477,11 +1512,13 @@ const void* attn_kernel_ptr(const Shape& sh) {
 const void* move_kernel_ptr() { return (const void*)k_move; }
 
 cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st) {
-  // up to 2 slots per thread one CTA is fastest; beyond, one CTA per 1024 slots
+  // up to 2 slots per thread one CTA is fastest; beyond, one CTA per 512 slots (B = 16384: 32
+  // CTAs; 1024-slot CTAs measured 1.6x slower in-kernel: longer block scans and store queues)
   static const int single = [] { const char* e = getenv("S3_PREP_SINGLE_CTA"); return e ? atoi(e) : 0; }();  // A/B
-  const int nb = (single || a.B <= 2 * PREP_CTA_SLOTS) ? 1
-                                                      : std::min((a.B + PREP_CTA_SLOTS - 1) / PREP_CTA_SLOTS, PREP_MAX_CTAS);
-  k_prep<<<nb, 1024, 0, st>>>(a);
+  static const int thr = [] { const char* e = getenv("S3_PREP_THREADS"); return e ? atoi(e) : 512; }();
+  static const int single_max = [] { const char* e = getenv("S3_PREP_SINGLE_MAX"); return e ? atoi(e) : 2 * PREP_CTA_SLOTS; }();
+  const int nb = (single || a.B <= single_max) ? 1 : std::min((a.B + thr - 1) / thr, PREP_MAX_CTAS);
+  k_prep<<<nb, nb == 1 ? 1024 : thr, 0, st>>>(a);
   return cudaGetLastError();
 }
 
