@@ -587,6 +587,9 @@ def run_s3(args):
                 "note": "this window of C1 (oracle predictor) has no evictions by construction (P4); "
                         "see 'c2' for the eviction leg",
             },
+            "k_prep": {"us_per_launch": round(prof.prep_ms * 1e3 / prof.prep_launches, 2) if prof.prep_launches else None,
+                       "launches": prof.prep_launches, "mean_batch": mean_batch_window,
+                       "note": "detection + keep-scan + work list (CUDA events around each launch)"},
             "tokens": tok_sum, "finished": totals["finished"], "admitted": totals["admitted"],
             "gpu_launches": launches,
             "phases_ms_per_step": phases,

@@ -269,6 +269,8 @@ typedef struct {
   double h2d_ms, h2d_bytes;         /* reload copies (main stream)                       */
   double d2h_overlap_ms;            /* part of d2h_ms during which an attention kernel ran
                                        (CUDA-event intervals on both streams)             */
+  int64_t prep_launches;            /* k_prep launches timed (detection + keep-scan)     */
+  double prep_ms;                   /* their summed durations                           */
 } s3_profile;
 s3_status s3_profile_enable(s3_ctx* ctx, int32_t on);   /* also resets the sums */
 s3_status s3_profile_get(s3_ctx* ctx, s3_profile* prof); /* synchronises          */

@@ -112,8 +112,8 @@ struct Prof {
   std::vector<cudaEvent_t> free_events;
   struct Pending { cudaEvent_t a, b; double bytes; int kind; };
   std::vector<Pending> pending;
-  int64_t attn_launches = 0, move_launches = 0, fused_steps = 0, d2h_copies = 0, h2d_copies = 0;
-  double attn_ms = 0, move_ms = 0, attn_bytes = 0, move_bytes = 0, fused_move_bytes = 0;
+  int64_t attn_launches = 0, move_launches = 0, fused_steps = 0, d2h_copies = 0, h2d_copies = 0, prep_launches = 0;
+  double attn_ms = 0, move_ms = 0, attn_bytes = 0, move_bytes = 0, fused_move_bytes = 0, prep_ms = 0;
   double d2h_ms = 0, d2h_bytes = 0, h2d_ms = 0, h2d_bytes = 0;
   // absolute intervals (ms after `ref`) of attention launches and eviction copies, for the
   // overlap evidence: how much of the side-stream D2H ran while an attention kernel ran
@@ -340,6 +340,7 @@ void prof_collect(s3_ctx* c) {     // call when cfg.stream is idle; side-stream 
     if (p.kind == 0) { c->prof.attn_ms += ms; c->prof.attn_bytes += p.bytes; c->prof.attn_launches++; }
     else if (p.kind == 1) { c->prof.move_ms += ms; c->prof.move_bytes += p.bytes; c->prof.move_launches++; }
     else if (p.kind == 2) { c->prof.d2h_ms += ms; c->prof.d2h_bytes += p.bytes; c->prof.d2h_copies++; }
+    else if (p.kind == 4) { c->prof.prep_ms += ms; c->prof.prep_launches++; }
     else { c->prof.h2d_ms += ms; c->prof.h2d_bytes += p.bytes; c->prof.h2d_copies++; }
     c->prof.free_events.push_back(p.a);
     c->prof.free_events.push_back(p.b);
@@ -722,8 +723,14 @@ s3_status s3_decode_step(s3_ctx* ctx, int32_t l0, int32_t nl, const void* q, con
     static const int devrep = [] { const char* e = getenv("S3_PREP_DEVREPORT"); return e ? atoi(e) : 0; }();  // A/B
     pa.report = fuse && !devrep ? ctx->h_report_dev : ctx->report_dev;
     pa.fused_out = fuse ? reinterpret_cast<int32_t*>(ctx->h_report_dev + report_bytes(B)) : nullptr;
+    cudaEvent_t p0 = nullptr, p1 = nullptr;
+    if (ctx->prof.on) { p0 = ctx->prof.get(); p1 = ctx->prof.get(); cudaEventRecord(p0, ctx->st); }
     CK(launch_prep(pa, ctx->st), "k_prep");
     ctx->launches += 1;
+    if (ctx->prof.on) {
+      cudaEventRecord(p1, ctx->st);
+      ctx->prof.pending.push_back({p0, p1, 0.0, 4});
+    }
     if (fuse && devrep)
       CK(cudaMemcpyAsync(ctx->h_report, ctx->report_dev, (size_t)report_bytes(B), cudaMemcpyDeviceToHost, ctx->st),
          "report D2H");
@@ -1262,6 +1269,8 @@ s3_status s3_profile_enable(s3_ctx* ctx, int32_t on) {
   ctx->prof.fused_move_bytes = 0;
   ctx->prof.d2h_copies = ctx->prof.h2d_copies = 0;
   ctx->prof.d2h_ms = ctx->prof.d2h_bytes = ctx->prof.h2d_ms = ctx->prof.h2d_bytes = 0;
+  ctx->prof.prep_launches = 0;
+  ctx->prof.prep_ms = 0;
   return S3_OK;
 }
 
@@ -1287,6 +1296,8 @@ s3_status s3_profile_get(s3_ctx* ctx, s3_profile* p) {
   for (const auto& d : ctx->prof.d2h_iv)
     for (const auto& k : ctx->prof.attn_iv) ov += std::max(0.0, std::min(d.second, k.second) - std::max(d.first, k.first));
   p->d2h_overlap_ms = ov;
+  p->prep_launches = ctx->prof.prep_launches;
+  p->prep_ms = ctx->prof.prep_ms;
   return S3_OK;
 }
 

@@ -267,17 +267,16 @@ __global__ void __launch_bounds__(1024) k_prep(PrepArgs a) {
     if (threadIdx.x == 0) {
 #pragma unroll
       for (int k = 0; k < PREP_NX; ++k) a.xagg[blockIdx.x * PREP_NX + k] = tot[k];
-      __threadfence();
+      // the release orders this thread's xagg stores before the flag (no separate fence)
       asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(a.xflag + blockIdx.x), "l"((unsigned long long)a.epoch)
                    : "memory");
     }
     if ((int)threadIdx.x < nb) {
       const int c = threadIdx.x;
-      for (;;) {
+      for (;;) {                          // all CTAs are co-resident and publish within microseconds: spin
         unsigned long long f;
         asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(f) : "l"(a.xflag + c) : "memory");
         if (f == (unsigned long long)a.epoch) break;
-        __nanosleep(32);
       }
 #pragma unroll
       for (int k = 0; k < PREP_NX; ++k) s_agg[c][k] = __ldcg(a.xagg + c * PREP_NX + k);
@@ -415,11 +414,10 @@ __global__ void __launch_bounds__(1024) k_prep(PrepArgs a) {
     if (threadIdx.x == 0) {
       long long* pt = a.xpart + blockIdx.x * 4;
       pt[0] = s_first_hole; pt[1] = (long long)s_hbm; pt[2] = (long long)s_moved; pt[3] = s_end;
-      __threadfence();
-      const int old = atomicAdd(a.xdone, 1);
+      int old;                            // acq_rel: publishes pt, and the last CTA sees every CTA's
+      asm volatile("atom.acq_rel.gpu.global.add.s32 %0, [%1], 1;" : "=r"(old) : "l"(a.xdone) : "memory");
       s_last = old == nb - 1;
       if (s_last) {
-        __threadfence();
         int fh = B;
         unsigned long long hb = 0, mv = 0;
         long long en = 0;

@@ -78,7 +78,7 @@ class s3_profile(C.Structure):
                 ("attn_bytes", C.c_double), ("move_bytes", C.c_double), ("fused_move_bytes", C.c_double),
                 ("d2h_copies", C.c_int64), ("h2d_copies", C.c_int64), ("d2h_ms", C.c_double),
                 ("d2h_bytes", C.c_double), ("h2d_ms", C.c_double), ("h2d_bytes", C.c_double),
-                ("d2h_overlap_ms", C.c_double)]
+                ("d2h_overlap_ms", C.c_double), ("prep_launches", C.c_int64), ("prep_ms", C.c_double)]
 
 
 class s3_gemm_args(C.Structure):

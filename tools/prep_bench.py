@@ -31,7 +31,11 @@ def main():
     eng.submit(t.req_id, t.prompt, t.alloc, t.out)
     eng.admit()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    busy = torch.randn(4096, 4096, device="cuda").to(torch.bfloat16)
+    eng.profile(True)
     for _ in range(8):
+        for _ in range(20):                          # keep the SM clocks up between steps
+            busy @ busy
         eng.synth_inputs()
         ev0.record()
         eng.decode()
@@ -40,6 +44,9 @@ def main():
         print(f"B {eng.B}: decode call (k_prep + k_deps + attention) {ev0.elapsed_time(ev1) * 1e3:.1f} us")
         eng.evict_compact()
         eng.admit()
+    pr = eng.profile_get()
+    print(f"k_prep (CUDA events around each launch): {pr.prep_ms * 1e3 / max(pr.prep_launches, 1):.1f} us "
+          f"mean over {pr.prep_launches} launches")
     eng.close()
 
 
