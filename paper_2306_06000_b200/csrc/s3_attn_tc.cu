@@ -117,7 +117,8 @@ constexpr int TC_THREADS = 32 * 11;   // producer, MMA, 4 softmax (group 0), sto
 
 struct TcHdr {
   int32_t item, r0, nvalid, flags;          // flags: 1 = first tile of the item, 2 = last;
-                                            // bits 8..11: log2 np (KV heads packed in the tile)
+                                            // bits 8..12: np (KV heads packed in the tile),
+                                            // bits 16..20: seg / 8 (rows per packed head's segment)
   int32_t b, part, li, g;
   int32_t iseq, mode, drow;                 // iseq: per-CTA item sequence number (O buffer = iseq & 1)
   uint32_t prog;                            // read progress this tile completes (storer)
@@ -125,8 +126,9 @@ struct TcHdr {
 };
 static_assert(sizeof(TcHdr) % 16 == 0, "TcHdr.dep must stay 16-B aligned");
 constexpr uint32_t TC_PROG_FULL = 0x80000000u;
-// KV heads g..g+np-1 share the tile, one segment of TM / np rows each
-__device__ __forceinline__ int hdr_lognp(const TcHdr& h) { return (h.flags >> 8) & 15; }
+// KV heads g..g+np-1 share the tile, one segment of seg rows each (segment s at rows [s seg, (s+1) seg))
+__device__ __forceinline__ int hdr_np(const TcHdr& h) { return (h.flags >> 8) & 31; }
+__device__ __forceinline__ int hdr_seg(const TcHdr& h) { return ((h.flags >> 16) & 31) * 8; }
 constexpr int TC_HEAD_STRIDE = 1 << 16;      // progress = head * 2^16 + rows (unit rows < 2^16)
 
 struct alignas(16) TcSmem {                 // after the ring and the two P buffers (one per group)
@@ -501,13 +503,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
         const bool mv = un.mode == UNIT_MOVE;
         // destination row of the unit's first row: arena row (MOVE) or staging row (STAGE)
         const int drow0 = (int)(mv ? un.dst : un.dst / a.kvpt) + un.r0;
-        // short units: np KV heads share one 128-row tile, one segment of seg rows each
-        // (block-diagonal scores: segment s only meets query columns [s G, (s+1) G))
-        int np = 1;
-        if constexpr (PACK)
-          while (np * 2 <= a.pmax && nrows <= TM / (np * 2) && a.Hkv % (np * 2) == 0) np *= 2;
-        const int seg = TM / np;
-        for (int g = 0; g < a.Hkv; g += np, ++iseq) {
+        // short units: up to pmax KV heads share one 128-row tile, one segment of seg =
+        // nrows rounded up to 8 rows each, back to back (block-diagonal scores: segment s
+        // only meets query columns [s G, (s+1) G)); the last tile of a unit-layer may hold
+        // fewer heads (Hkv need not be a multiple of the packing)
+        int npk = 1, seg = TM;
+        if constexpr (PACK) {
+          const int rg = (nrows + 7) & ~7;
+          if (2 * rg <= TM) { npk = min(min(a.pmax, TM / rg), a.Hkv); seg = rg; }
+        }
+        for (int g = 0; g < a.Hkv; g += npk, ++iseq) {
+          const int np = min(npk, a.Hkv - g);
           const int item = w * a.Hkv + g;
           const int qrow = (li * a.B + un.b) * a.H + g * a.G;
           for (int r = 0; r < nrows; r += TM) {
@@ -522,7 +528,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
             h.b = un.b; h.part = un.part; h.li = li; h.g = g; h.iseq = iseq;
             h.mode = un.mode; h.drow = drow0 + r;
             if (un.mode == UNIT_STAGE) h.dep.ua = un.pad;   // eviction index (dep is only loaded for MOVE)
-            h.flags |= (31 - __clz(np)) << 8;
+            h.flags |= (np << 8) | ((seg >> 3) << 16);
             const int glast = g + np - 1;  // heads g..glast are read up to r + nrow rows once this tile lands
             h.prog = (uint32_t)(glast * TC_HEAD_STRIDE + r + nrow) |
                      (glast == a.Hkv - 1 && r + TM >= nrows ? TC_PROG_FULL : 0u);
@@ -531,8 +537,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
             uint8_t* sv = vslot(smem, t, nk, nv);
             uint8_t* sq = sk + KV_BYTES;
             const bool dep = fused && mv;
-            mb_expect(&S.kfull[ks], (uint32_t)(np * groups * 8 * 128 * 2 + Q_BYTES + (dep ? 16 : 0)));
-            mb_expect(&S.vfull[vs], (uint32_t)(np * groups * 8 * 128 * 2));
+            mb_expect(&S.kfull[ks], (uint32_t)(np * groups * 2048 + Q_BYTES + (dep ? 16 : 0)));
+            mb_expect(&S.vfull[vs], (uint32_t)(np * groups * 2048));
             if (dep) bulk_g2s16(&h.dep, a.desc + un.stage_base + r / TM, &S.kfull[ks]);
             const int row0 = un.off + un.r0 + r;
             for (int sgi = 0; sgi < np; ++sgi) {    // one 4-D box per segment for K and one for V
@@ -640,7 +646,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
           st_rlx_u64(a.progress + w, ((unsigned long long)a.epoch << 32) | h.prog);
           if (h.mode == UNIT_MOVE && h.dep.ua >= 0) {
             // the tile overwrites heads g..g+np-1 of its destination rows
-            const uint32_t gbase = (uint32_t)((h.g + (PACK ? 1 << hdr_lognp(h) : 1) - 1) * TC_HEAD_STRIDE);
+            const uint32_t gbase = (uint32_t)((h.g + (PACK ? hdr_np(h) : 1) - 1) * TC_HEAD_STRIDE);
             for (int v = h.dep.ua; v <= h.dep.ub; ++v) {
               const int need = v == h.dep.ua ? h.dep.need_a : (v == h.dep.ub ? h.dep.need_b : -1);
               const int it = v * a.nl + h.li;
@@ -660,8 +666,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
         if (stores) {
           const int full_groups = h.nvalid >> 3;     // whole 8-row groups go out as 4-D boxes
           if (lane == 0) asm volatile("fence.proxy.async.global;" ::: "memory");
-          const int np = PACK ? 1 << hdr_lognp(h) : 1;
-          const int seg = TM / np;
+          const int np = PACK ? hdr_np(h) : 1;
+          const int seg = PACK ? hdr_seg(h) : TM;
           for (int sgi = 0; sgi < np; ++sgi) {       // one segment per packed KV head
             const uint8_t* sk = kslot(smem, t, nk) + sgi * (seg / 8) * 2048;
             const uint8_t* sv = vslot(smem, t, nk, nv) + sgi * (seg / 8) * 2048;
@@ -713,7 +719,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
             // for the D2H stream, which copies each evictee as soon as its count is complete
             asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
             asm volatile("fence.proxy.async.global;" ::: "memory");
-            const uint32_t rows = (uint32_t)(h.nvalid * (PACK ? 1 << hdr_lognp(h) : 1));
+            const uint32_t rows = (uint32_t)(h.nvalid * (PACK ? hdr_np(h) : 1));
             asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(a.evdone + h.dep.ua), "r"(rows) : "memory");
           }
         }
@@ -761,20 +767,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
       __syncwarp();
       if (lane == 0) mb_arrive(&S.s_empty[grp][sb]);
       const bool first = h.flags & 1;
-      int rs = row;                                   // this lane's row inside its segment
-      bool valid;
-      const int lognp = PACK ? hdr_lognp(h) : 0;
-      if (!PACK || lognp == 0) {                               // warp-uniform: one KV head per tile
+      bool valid, loaded;                             // loaded: row holds this item's (or slack) data
+      const int np = PACK ? hdr_np(h) : 1;
+      if (!PACK || np == 1) {                          // warp-uniform: one KV head per tile
         valid = row < h.nvalid;
+        loaded = row < ((h.nvalid + 15) & ~15);
 #pragma unroll
         for (int c = 0; c < NC; ++c) s[c] = valid ? s[c] * a.qscale : -INFINITY;
       } else {
         // block-diagonal mask of packed tiles: segment sgm only meets columns
-        // [sgm G, (sgm+1) G); columns past np G stay unmasked (finite, never written out)
-        const int sgm = row >> (7 - lognp);           // segments of TM >> lognp rows
-        rs = row - (sgm << (7 - lognp));
-        valid = rs < h.nvalid;
-        const int cg0 = sgm * a.G, cg1 = cg0 + a.G, cpad = a.G << lognp;
+        // [sgm G, (sgm+1) G); columns past np G stay unmasked (finite, never written out);
+        // rows past the last segment are masked
+        const int seg = hdr_seg(h);
+        const int sgm = row / seg;
+        const int rs = row - sgm * seg;
+        loaded = sgm < np;
+        valid = loaded && rs < h.nvalid;
+        const int cg0 = sgm * a.G, cg1 = cg0 + a.G, cpad = a.G * np;
 #pragma unroll
         for (int c = 0; c < NC; ++c)
           s[c] = (valid && ((c >= cg0 && c < cg1) || c >= cpad)) ? s[c] * a.qscale : -INFINITY;
@@ -827,7 +836,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
         *reinterpret_cast<__nv_bfloat16*>(sp + sw) = hi;
         *reinterpret_cast<__nv_bfloat16*>(sp + NQ * 128 + sw) = lo;   // row 16 + c: same swizzle phase
       }
-      if (!valid && rs < ((h.nvalid + 15) & ~15)) {  // loaded rows past the slot's resident rows: V := 0
+      if (!valid && loaded) {                         // loaded rows past the slot's resident rows: V := 0
         mb_wait(&S.vfull[t % nv], (uint32_t)(t / nv) & 1u);   // after the V load has landed
         uint8_t* sv = vslot(smem, t, nk, nv);
 #pragma unroll
@@ -868,7 +877,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
         const int d = row;
 #pragma unroll
         for (int c = 0; c < NC; ++c) {
-          if (c >= (PACK ? a.G << hdr_lognp(h) : a.G)) break;
+          if (c >= (PACK ? a.G * hdr_np(h) : a.G)) break;
           const int hq = h.g * a.G + c;             // packed heads: column c belongs to KV head g + c / G
           const float ov = o[c] + olo[c];
           if (h.part < 0) {
@@ -1030,10 +1039,12 @@ cudaError_t launch_attn_tc(const Shape& sh, const uint16_t* q, const uint16_t* k
   static const int ring = [] { const char* e = getenv("S3_TC_RING"); return e ? atoi(e) : 0; }();   // A/B: 24 or 33
   const bool two_four = ring ? ring == 24 : short_items != 0;
   static const int pack = [] { const char* e = getenv("S3_TC_PACK"); return e ? atoi(e) : 1; }();
-  a.pmax = pack ? (a.G <= 8 ? 8 : 16) / a.G : 1;   // S3_TC_PACK=0: one KV head per tile (A/B)
+  static const int nc_env = [] { const char* e = getenv("S3_TC_NC"); return e ? atoi(e) : 0; }();
+  const int nc = (a.G > 8 || nc_env == 16) ? 16 : 8;   // softmax columns (S3_TC_NC=16: pack 16 / G heads)
+  a.pmax = pack ? nc / a.G : 1;   // S3_TC_PACK=0: one KV head per tile (A/B)
   const dim3 grid(grid_attn), block(TC_THREADS);
   const int smem = attn_tc_smem();
-  const void* kfn = attn_tc_kernel_ptr(a.G <= 8 ? 8 : 16, a.pmax > 1, feed.ready != nullptr, !two_four);
+  const void* kfn = attn_tc_kernel_ptr(nc, a.pmax > 1, feed.ready != nullptr, !two_four);
   void* args[] = {(void*)&maps, (void*)&a};
   cudaError_t le = cudaLaunchKernel(kfn, grid, block, args, (size_t)smem, st);
   if (le != cudaSuccess) return le;
