@@ -66,8 +66,8 @@ namespace {
 
 // Diagnostic build only (-DTC_TRACE): SM-clock timestamps of CTA 0's tiles at
 // fixed points of each role (0 producer got a stage, 1 producer issued the
-// tile, 3 MMA saw the tile land, 4 MMA got P, 5 MMA committed O, 6 softmax got
-// S, 7 softmax handed over P), read back with s3_debug_tc_trace.
+// tile, 2 softmax finished the item's epilogue (last tiles only), 3 MMA saw the
+// tile land, 4 MMA got P, 5 MMA committed O, 6 softmax got S, 7 softmax handed over P), read back with s3_debug_tc_trace.
 #ifdef TC_TRACE
 constexpr int TC_TRACE_TILES = 8192;
 __device__ unsigned long long g_tc_trace[TC_TRACE_TILES * 8];
@@ -143,6 +143,18 @@ struct alignas(16) TcSmem {                 // after the ring and the two P buff
 };
 
 __device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// Warp-uniform issue of tcgen05 / TMA instructions.  Their operands live in uniform
+// registers; a value the compiler cannot prove warp-uniform (anything loaded from memory,
+// or computed in a lane-0-only branch) is moved there by an ELECT / R2UR.BROADCAST loop
+// around EVERY instruction (~90 cycles per tcgen05.mma or cp.async.bulk.tensor, measured
+// with the TC_TRACE build).  So the producer and MMA roles run warp-wide: memory values are
+// broadcast with uni() (shfl from lane 0: provably uniform), and one elected lane issues.
+__device__ __forceinline__ int uni(int x) { return __shfl_sync(0xffffffffu, x, 0); }
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p;
+  asm volatile("{\n .reg .pred P;\n elect.sync _|P, 0xffffffff;\n selp.u32 %0, 1, 0, P;\n}\n" : "=r"(p));
+  return p != 0;
+}
 __device__ __forceinline__ void mb_init(uint64_t* b, uint32_t n) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n) : "memory");
 }
@@ -401,7 +413,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
   uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   uint8_t* pbuf = smem + RING_BYTES;
   TcSmem& S = *reinterpret_cast<TcSmem*>(pbuf + 2 * PBUF_BYTES);
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int tid = threadIdx.x, warp = uni(tid >> 5), lane = tid & 31;
   // the storer takes part in the ring only when this step shifts rows
   const bool fused = a.ctrl[CTRL_FUSED] != 0;
   constexpr int nk = R33 ? 3 : 2, nv = R33 ? 3 : 4;
@@ -443,35 +455,43 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
     // Otherwise k_append has written every new row before the kernel (cheaper: the
     // loads would stall this warp's TMA issue).
     int t = 0, iseq = 0, ready_max = -1;
-    const int groups_total = a.ctrl[CTRL_N_UNITS] * a.nl;
+    const int groups_total = uni(a.ctrl[CTRL_N_UNITS]) * a.nl;
     const int kd8 = a.Hkv * DH / 8;               // 16-B vectors of one layer's new K (or V) row
-    // FEED: the whole warp runs the loop (lane 0 takes tickets and issues tiles); else lane 0 alone
     // The next ticket and its unit record are fetched one ticket ahead, so the
     // atomic and the dependent load (~2 us together) overlap this ticket's tile
     // issue instead of stalling the ring between tickets (short units have only a
     // few tiles per ticket).  Deadlock freedom is unchanged: the smallest
     // unfinished ticket is always some CTA's current one.
-    int w_next = 0;
-    if (lane == 0) w_next = atomicAdd(&a.ctrl[CTRL_ITEM], 1);
-    if constexpr (FEED) w_next = __shfl_sync(0xffffffffu, w_next, 0);
+    // The whole warp runs the loop with warp-uniform values (uni()); elected lanes issue.
+    auto load_unit = [&](int w) {
+      const Unit* p = a.units + w / a.nl;
+      Unit u;
+      u.b = uni(p->b); u.r0 = uni(p->r0); u.r1 = uni(p->r1); u.part = uni(p->part);
+      u.off = uni(p->off); u.len = uni(p->len); u.has_new = uni(p->has_new); u.mode = uni(p->mode);
+      const long long d = p->dst;
+      u.dst = (int64_t)(((unsigned long long)(uint32_t)uni((int)(d >> 32)) << 32) | (uint32_t)uni((int)d));
+      u.stage_base = uni(p->stage_base); u.pad = uni(p->pad);
+      return u;
+    };
+    int w_next = uni(lane == 0 ? atomicAdd(&a.ctrl[CTRL_ITEM], 1) : 0);
     Unit un_next{};
-    if ((FEED || lane == 0) && w_next < groups_total) un_next = a.units[w_next / a.nl];
-    for (; FEED || lane == 0;) {
+    if (w_next < groups_total) un_next = load_unit(w_next);
+    for (;;) {
       const int w = w_next;
       const Unit un = un_next;
       if (w < groups_total) {
-        if (lane == 0) w_next = atomicAdd(&a.ctrl[CTRL_ITEM], 1);
-        if constexpr (FEED) w_next = __shfl_sync(0xffffffffu, w_next, 0);
-        if (w_next < groups_total) un_next = a.units[w_next / a.nl];
+        w_next = uni(lane == 0 ? atomicAdd(&a.ctrl[CTRL_ITEM], 1) : 0);
+        if (w_next < groups_total) un_next = load_unit(w_next);
       }
       if (w >= groups_total) {
-        if (lane == 0) {
-          mb_wait(&S.kempty[t % nk], ((uint32_t)(t / nk) & 1u) ^ 1u);
-          mb_wait(&S.vempty[t % nv], ((uint32_t)(t / nv) & 1u) ^ 1u);
+        mb_wait(&S.kempty[t % nk], ((uint32_t)(t / nk) & 1u) ^ 1u);
+        mb_wait(&S.vempty[t % nv], ((uint32_t)(t / nv) & 1u) ^ 1u);
+        if (elect_one()) {
           S.hdr[t % nv].item = -1;
           mb_arrive(&S.kfull[t % nk]);
           mb_arrive(&S.vfull[t % nv]);
         }
+        __syncwarp();
         break;
       }
       const int li = w % a.nl;
@@ -498,7 +518,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
         asm volatile("fence.proxy.async.global;" ::: "memory");   // the tile loads below read the new row
         __syncwarp();
       }
-      if (lane == 0) {
+      {
         const int nrows = (un.r1 - un.r0) + (un.has_new ? 1 : 0);   // new row now in the arena
         const bool mv = un.mode == UNIT_MOVE;
         // destination row of the unit's first row: arena row (MOVE) or staging row (STAGE)
@@ -520,8 +540,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
             const int ks = t % nk, vs = t % nv;
             mb_wait(&S.kempty[ks], ((uint32_t)(t / nk) & 1u) ^ 1u);
             mb_wait(&S.vempty[vs], ((uint32_t)(t / nv) & 1u) ^ 1u);
-            TC_TRACE_AT(t, 0);
             const int nrow = min(TM, nrows - r);
+            if (elect_one()) {
+            TC_TRACE_AT(t, 0);
             TcHdr& h = S.hdr[vs];
             h.item = item; h.r0 = un.r0 + r; h.nvalid = nrow;
             h.flags = (r == 0 ? 1 : 0) | (r + TM >= nrows ? 2 : 0);
@@ -548,12 +569,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
               tma4d(sv + sgo, &maps.kvg[groups - 1], row0, (colk + a.Hkv * DH) / 64, &S.vfull[vs]);
             }
             tma3d(sq, &maps.q, 0, qrow, 0, &S.kfull[ks]);   // both 64-column blocks of the 16 q rows
+            TC_TRACE_AT(t, 1);
+            }
+            __syncwarp();
             ++t;
-            TC_TRACE_AT(t - 1, 1);
           }
         }
       }
-      if constexpr (FEED) __syncwarp();
+      __syncwarp();
     }
   } else if (warp == 1) {
     // -------------------------------- MMA ---------------------------------
@@ -561,71 +584,83 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
     // item's parity, which is also its O buffer) and is that group's k-th
     // tile.  One tile of lookahead: S^T(t+1) is issued before O^T(t), so the
     // other group's softmax runs while this tile's P is being made.
-    if (lane == 0) {
+    {
+      // warp-wide with uniform values; one elected lane issues the MMAs and commits
       // S: N = 16 query columns; O: N = 32 ([P_hi | P_lo] in one MMA, halving the PV issue count)
       constexpr uint32_t id_s = idesc(0, NQ), id_o = idesc(1, 2 * NQ);
+      const uint32_t tm = (uint32_t)uni((int)tmem);
       int kc[2] = {0, 0};                       // tiles handed to each group so far
       auto issue_s = [&](int t) -> int {        // returns the tile's index within its group
-        const int g = S.hdr[t % nv].iseq & 1;
+        const int g = uni(S.hdr[t % nv].iseq) & 1;
         const int k = kc[g]++;
         const int sb = k & 1;
         mb_wait(&S.s_empty[g][sb], ((uint32_t)(k >> 1) & 1u) ^ 1u);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint8_t* sk = kslot(smem, t, nk);
         const uint8_t* sq = sk + KV_BYTES;
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {        // S^T = K . Q^T over d in steps of 16
-          const int kb = kk >> 2, ko = (kk & 3) * 32;
-          mma(tmem + scol(g, sb), sdesc(sk + kb * 1024 + ko, 16, 2048), sdesc(sq + kb * 2048 + ko, 16, 1024), id_s,
-              kk > 0);
+          for (int kk = 0; kk < 8; ++kk) {      // S^T = K . Q^T over d in steps of 16
+            const int kb = kk >> 2, ko = (kk & 3) * 32;
+            mma(tm + scol(g, sb), sdesc(sk + kb * 1024 + ko, 16, 2048), sdesc(sq + kb * 2048 + ko, 16, 1024), id_s,
+                kk > 0);
+          }
+          commit(&S.s_full[g][sb]);
+          commit(&S.kempty[t % nk]);            // the K slot is free once these MMAs have read it
+          S.gt[g][sb] = t;
+          mb_arrive(&S.s_full[g][sb]);          // releases gt together with the slot
         }
-        commit(&S.s_full[g][sb]);
-        commit(&S.kempty[t % nk]);              // the K slot is free once these MMAs have read it
-        S.gt[g][sb] = t;
-        mb_arrive(&S.s_full[g][sb]);            // releases gt together with the slot
+        __syncwarp();
         return k;
       };
       auto finish = [&]() {                     // tell both groups there are no more tiles
         for (int g = 0; g < 2; ++g) {
           const int sb = kc[g] & 1;
           mb_wait(&S.s_empty[g][sb], ((uint32_t)(kc[g] >> 1) & 1u) ^ 1u);
-          S.gt[g][sb] = -1;
-          mb_arrive(&S.s_full[g][sb]);
-          mb_arrive(&S.s_full[g][sb]);
+          if (elect_one()) {
+            S.gt[g][sb] = -1;
+            mb_arrive(&S.s_full[g][sb]);
+            mb_arrive(&S.s_full[g][sb]);
+          }
+          __syncwarp();
         }
       };
       mb_wait(&S.kfull[0], 0u);
-      if (S.hdr[0].item < 0) {
+      if (uni(S.hdr[0].item) < 0) {
         finish();
       } else {
         int kt = issue_s(0);
         for (int t = 0;; ++t) {
           const int vs = t % nv;
           mb_wait(&S.kfull[(t + 1) % nk], (uint32_t)((t + 1) / nk) & 1u);
-          TC_TRACE_AT(t + 1, 3);
-          const bool end = S.hdr[(t + 1) % nv].item < 0;
+          if (lane == 0) TC_TRACE_AT(t + 1, 3);
+          const bool end = uni(S.hdr[(t + 1) % nv].item) < 0;
           const int kt1 = end ? 0 : issue_s(t + 1);
-          const bool first = S.hdr[vs].flags & 1;
-          const bool last = S.hdr[vs].flags & 2;
-          const int iseq = S.hdr[vs].iseq, g = iseq & 1;
+          const int flags = uni(S.hdr[vs].flags);
+          const bool first = flags & 1;
+          const bool last = flags & 2;
+          const int iseq = uni(S.hdr[vs].iseq), g = iseq & 1;
           if (first)   // O buffer g must have been read by the epilogue of item iseq - 2
             mb_wait(&S.o_free[g], ((uint32_t)(iseq >> 1) & 1u) ^ 1u);
           mb_wait(&S.p_full[g], (uint32_t)kt & 1u);
           mb_wait(&S.vfull[vs], (uint32_t)(t / nv) & 1u);   // V landed (the softmax waited too if it zeroed rows)
-          TC_TRACE_AT(t, 4);
+          if (lane == 0) TC_TRACE_AT(t, 4);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint8_t* sv = vslot(smem, t, nk, nv);
           const uint8_t* sp = pbuf + g * PBUF_BYTES;
+          if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {          // [O_hi | O_lo]^T += V^T . [P_hi | P_lo]^T, rows in steps of 16
-            const int kb = kk >> 2, ko = (kk & 3) * 32;
-            mma(tmem + ocol(g), sdesc(sv + kk * 4096, 1024, 2048), sdesc(sp + kb * PBLK_BYTES + ko, 16, 1024), id_o,
-                (first && kk == 0) ? 0u : 1u);
+            for (int kk = 0; kk < 8; ++kk) {        // [O_hi | O_lo]^T += V^T . [P_hi | P_lo]^T, rows in steps of 16
+              const int kb = kk >> 2, ko = (kk & 3) * 32;
+              mma(tm + ocol(g), sdesc(sv + kk * 4096, 1024, 2048), sdesc(sp + kb * PBLK_BYTES + ko, 16, 1024), id_o,
+                  (first && kk == 0) ? 0u : 1u);
+            }
+            commit(&S.o_done[g]);
+            if (last) commit(&S.o_fin[g]);
+            commit(&S.vempty[vs]);
+            TC_TRACE_AT(t, 5);
           }
-          commit(&S.o_done[g]);
-          if (last) commit(&S.o_fin[g]);
-          commit(&S.vempty[vs]);
-          TC_TRACE_AT(t, 5);
+          __syncwarp();
           if (end) { finish(); break; }
           kt = kt1;
         }
@@ -638,7 +673,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
       for (int t = 0;; ++t) {
         mb_wait(&S.kfull[t % nk], (uint32_t)(t / nk) & 1u);
         mb_wait(&S.vfull[t % nv], (uint32_t)(t / nv) & 1u);
-        const TcHdr h = S.hdr[t % nv];
+        TcHdr h = S.hdr[t % nv];
+        // fields that feed the TMA stores' operands: warp-uniform (see uni())
+        h.item = uni(h.item); h.nvalid = uni(h.nvalid); h.flags = uni(h.flags); h.li = uni(h.li);
+        h.g = uni(h.g); h.mode = uni(h.mode); h.drow = uni(h.drow);
         if (h.item < 0) break;
         const int w = h.item / a.Hkv;     // unit-layer ticket = progress slot
         if (lane == 0) {
@@ -758,7 +796,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
       mb_wait(&S.s_full[grp][sb], (uint32_t)(k >> 1) & 1u);
       const int t = S.gt[grp][sb];
       if (t < 0) break;
-      if (lane == 0 && warp == 2) TC_TRACE_AT(t, 6);
+      if (lane == 0 && wq == 0) TC_TRACE_AT(t, 6);
       const TcHdr h = S.hdr[t % nv];
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       float s[NC];
@@ -859,7 +897,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mb_arrive(&S.p_full[grp]);
-      if (lane == 0 && warp == 2) TC_TRACE_AT(t, 7);
+      if (lane == 0 && wq == 0) TC_TRACE_AT(t, 7);
       if (h.flags & 2) {
         // epilogue of the finished item: the other group keeps the tensor pipe busy meanwhile
         float pl[NC];
@@ -888,6 +926,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
             if (d == 0) { pr[DH] = m[c]; pr[DH + 1] = pl[c]; }
           }
         }
+        if (lane == 0 && wq == 0) TC_TRACE_AT(t, 2);
       }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");

@@ -1,8 +1,8 @@
 """Per-role timeline of the tensor-core kernel's tiles on CTA 0 (diagnostic;
-needs a -DTC_TRACE build of libs3.so, see tools/gpu_check51.sh).
+needs a -DTC_TRACE build of libs3.so: the build.py nvcc line with -DTC_TRACE).
 
 Slots (SM clock): 0 producer got a stage, 1 producer issued the tile's loads,
-3 MMA saw the tile land, 4 MMA got P, 5 MMA committed O, 6 softmax got S,
+2 softmax finished the item's epilogue (last tiles), 3 MMA saw the tile land, 4 MMA got P, 5 MMA committed O, 6 softmax got S,
 7 softmax handed over P."""
 import argparse
 import ctypes as C
@@ -68,6 +68,18 @@ def main():
     # starts a new (unit, layer) ticket (slot-0 of t+1 after an atomic) -- flags not traced, so report all
     res["producer_gap_p90"] = float(np.percentile(tr[idx + 1, 0] - t[:, 1], 90))
     res["softmax_group_busy_frac"] = float(((t[:, 7] - t[:, 6]).sum()) / span / 2)
+    # short items (one tile per item): tile t belongs to softmax group t & 1; slot 2 = its
+    # epilogue end.  Per group: S -> P, P -> epilogue end, and the idle gap until the group's
+    # next S (waiting for the MMA thread / the ring)
+    ep = tr[idx, 2]
+    if (ep > 0).mean() > 0.9:
+        res["group_S_to_P"] = float(np.median(t[:, 7] - t[:, 6]))
+        res["group_P_to_epilogue_end"] = float(np.median(ep - t[:, 7]))
+        nxt = tr[idx + 2, 6]
+        res["group_idle_epilogue_end_to_next_S"] = float(np.median(nxt - ep))
+        res["group_busy_frac"] = float(((ep - t[:, 6]).sum()) / span / 2)
+        res["MMA_got_P_to_epilogue_end"] = float(np.median(ep - t[:, 4]))
+        res["O_commit_to_epilogue_end"] = float(np.median(ep - t[:, 5]))
     print(json.dumps(res))
     eng.close()
 
