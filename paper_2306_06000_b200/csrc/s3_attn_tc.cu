@@ -102,25 +102,34 @@ __device__ __forceinline__ uint8_t* kslot(uint8_t* smem, int t, int nk) { return
 __device__ __forceinline__ uint8_t* vslot(uint8_t* smem, int t, int nk, int nv) {
   return smem + nk * KSLOT_BYTES + (t % nv) * VSLOT_BYTES;
 }
-// P as bf16 hi + lo parts (P = hi + lo to ~16 bits), one MMA operand [hi | lo] of N = 32:
-// two K blocks (tile rows j 0-63, 64-127) of [32 rows x 128 B] (rows 0-15 hi, 16-31 lo)
-constexpr int PBLK_BYTES = 2 * NQ * 64 * 2;  // 4 KB per K block
-constexpr int PBUF_BYTES = 2 * PBLK_BYTES;   // 8 KB
+// P as bf16 hi + lo parts (P = hi + lo to ~16 bits), one MMA operand [hi | lo] of N = 2 NC:
+// two K blocks (tile rows j 0-63, 64-127) of [2 NC rows x 128 B] (rows 0..NC-1 hi, NC..2NC-1 lo)
+__host__ __device__ constexpr int pblk_bytes(int nc) { return 2 * nc * 64 * 2; }   // per K block
+__host__ __device__ constexpr int pbuf_bytes(int nc) { return 2 * pblk_bytes(nc); }  // 4 KB (NC 8) / 8 KB (NC 16)
 constexpr float LAZY_THR = 8.0f;            // rescale only if a score beats the running max by 2^8
-// Two softmax groups ("ping-pong"): group g takes the items with iseq & 1 == g, so while one
-// group runs a tile's softmax and epilogue the other runs its own.  TMEM: S slot (g, b) at
-// columns (2g + b)*16 in [0, 64); O buffer g at 64 + 32g: [0,16) = V.P_hi, [16,32) = V.P_lo.
-constexpr int TMEM_COLS = 128;
+// NG softmax groups: group g takes the items with iseq % NG == g, so while one group runs a
+// tile's softmax and epilogue the others run theirs (a short tile's chain -- S load, max,
+// P, the O MMA round trip, epilogue -- is ~4k cycles, so two groups left the period at half
+// of it).  NG = 3 with NC = 8 (P buffers of 4 KB fit next to the 204 KB ring), 2 with NC = 16.
+// TMEM: S slot (g, b) at columns (2g + b)*16 in [0, 128); O buffer g at 128 + 32g:
+// [0, NC) = V.P_hi, [NC, 2NC) = V.P_lo.
+constexpr int NG_MAX = 4;
+#ifndef TC_NG8
+#define TC_NG8 3
+#endif
+__host__ __device__ constexpr int tc_groups(int nc) { return nc == 8 ? TC_NG8 : 2; }
+constexpr int TMEM_COLS = 256;
 __host__ __device__ constexpr uint32_t scol(int g, int b) { return (uint32_t)((2 * g + b) * 16); }
-__host__ __device__ constexpr uint32_t ocol(int g) { return 64u + 32u * (uint32_t)g; }
-constexpr int TC_THREADS = 32 * 11;   // producer, MMA, 4 softmax (group 0), storer, 4 softmax (group 1)
+__host__ __device__ constexpr uint32_t ocol(int g) { return 32u * NG_MAX + 32u * (uint32_t)g; }
+// warps: producer, MMA, 4 softmax (group 0), storer, then 4 softmax per further group
+__host__ __device__ constexpr int tc_threads(int nc) { return 32 * (3 + 4 * tc_groups(nc)); }
 
 struct TcHdr {
   int32_t item, r0, nvalid, flags;          // flags: 1 = first tile of the item, 2 = last;
                                             // bits 8..12: np (KV heads packed in the tile),
                                             // bits 16..20: seg / 8 (rows per packed head's segment)
   int32_t b, part, li, g;
-  int32_t iseq, mode, drow;                 // iseq: per-CTA item sequence number (O buffer = iseq & 1)
+  int32_t iseq, mode, drow;                 // iseq: per-CTA item sequence number (group / O buffer = iseq % NG)
   uint32_t prog;                            // read progress this tile completes (storer)
   DepDesc dep;                              // MOVE tiles: filled by the TMA engine with the tile
 };
@@ -133,12 +142,12 @@ constexpr int TC_HEAD_STRIDE = 1 << 16;      // progress = head * 2^16 + rows (u
 
 struct alignas(16) TcSmem {                 // after the ring and the two P buffers (one per group)
   uint64_t kfull[NK_MAX], kempty[NK_MAX], vfull[NV_MAX], vempty[NV_MAX];
-  uint64_t s_full[2][2], s_empty[2][2];     // [group][S slot]; s_full: MMA commit + the MMA thread's arrive
-  uint64_t p_full[2], o_done[2], o_fin[2], o_free[2];   // [group] (= O buffer = item parity)
+  uint64_t s_full[NG_MAX][2], s_empty[NG_MAX][2];   // [group][S slot]; s_full: MMA commit + the MMA thread's arrive
+  uint64_t p_full[NG_MAX], o_done[NG_MAX], o_fin[NG_MAX], o_free[NG_MAX];   // [group] (= O buffer)
   alignas(16) TcHdr hdr[NV_MAX];            // tile t at hdr[t % nv]; hdr.dep is a 16-B bulk-copy destination
-  float red[2][2][4][NQ];                   // [group][max / sum][warp][column]
-  int32_t flag[2][4];
-  int32_t gt[2][2];                         // ring tile index in group g's S slot b (-1: no more tiles)
+  float red[NG_MAX][2][4][NQ];              // [group][max / sum][warp][column]
+  int32_t flag[NG_MAX][4];
+  int32_t gt[NG_MAX][2];                    // ring tile index in group g's S slot b (-1: no more tiles)
   uint32_t tmem_base;
 };
 
@@ -406,13 +415,15 @@ __device__ __forceinline__ uint4 ld_cg16(const void* p) {
 // FEED: host-fed step (the producer warp waits on ready words and appends the new rows)
 // R33: ring shape 3 K + 3 V slots (else 2 K + 4 V; compile-time so the slot arithmetic folds)
 template <int NC, bool PACK, bool FEED, bool R33>
-__global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant__ TcMaps maps, TcArgs a) {
+__global__ void __launch_bounds__(tc_threads(NC), 1) k_attn_tc(const __grid_constant__ TcMaps maps, TcArgs a) {
+  constexpr int NG = tc_groups(NC);
+  constexpr int PBLK = pblk_bytes(NC), PBUF = pbuf_bytes(NC);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-B alignment for the 128B-swizzle atoms, by pointer arithmetic so the
   // compiler keeps the shared-memory address space (LDS/STS, not generic LD/ST)
   uint8_t* smem = smem_raw + ((1024u - (su32(smem_raw) & 1023u)) & 1023u);
   uint8_t* pbuf = smem + RING_BYTES;
-  TcSmem& S = *reinterpret_cast<TcSmem*>(pbuf + 2 * PBUF_BYTES);
+  TcSmem& S = *reinterpret_cast<TcSmem*>(pbuf + NG * PBUF);
   const int tid = threadIdx.x, warp = uni(tid >> 5), lane = tid & 31;
   // the storer takes part in the ring only when this step shifts rows
   const bool fused = a.ctrl[CTRL_FUSED] != 0;
@@ -420,7 +431,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
   if (tid == 0) {
     for (int i = 0; i < nk; ++i) { mb_init(&S.kfull[i], 1); mb_init(&S.kempty[i], fused ? 2 : 1); }
     for (int i = 0; i < nv; ++i) { mb_init(&S.vfull[i], 1); mb_init(&S.vempty[i], fused ? 2 : 1); }
-    for (int g = 0; g < 2; ++g) {
+    for (int g = 0; g < NG; ++g) {
       for (int b = 0; b < 2; ++b) { mb_init(&S.s_full[g][b], 2); mb_init(&S.s_empty[g][b], 4); }
       mb_init(&S.p_full[g], 4);
       mb_init(&S.o_done[g], 1);
@@ -580,19 +591,27 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
     }
   } else if (warp == 1) {
     // -------------------------------- MMA ---------------------------------
-    // Tiles in ring order; tile t belongs to softmax group g = iseq & 1 (its
-    // item's parity, which is also its O buffer) and is that group's k-th
-    // tile.  One tile of lookahead: S^T(t+1) is issued before O^T(t), so the
-    // other group's softmax runs while this tile's P is being made.
+    // Tiles in ring order; tile t belongs to softmax group g = iseq % NG (its
+    // item's group, which is also its O buffer) and is that group's k-th tile.
+    // LA tiles of lookahead: S^T(t+LA) is issued before O^T(t), so the other
+    // groups' softmax runs while this tile's P is being made.  LA < nv: the
+    // tile t+LA must be able to land while O^T(t) is still pending.
     {
       // warp-wide with uniform values; one elected lane issues the MMAs and commits
-      // S: N = 16 query columns; O: N = 32 ([P_hi | P_lo] in one MMA, halving the PV issue count)
-      constexpr uint32_t id_s = idesc(0, NQ), id_o = idesc(1, 2 * NQ);
+      // S: N = 16 query columns; O: N = 2 NC ([P_hi | P_lo] in one MMA, halving the PV issue count)
+      constexpr uint32_t id_s = idesc(0, NQ), id_o = idesc(1, 2 * NC);
+      constexpr int LA = (NG - 1) < (nv - 1) ? (NG - 1) : (nv - 1);
       const uint32_t tm = (uint32_t)uni((int)tmem);
-      int kc[2] = {0, 0};                       // tiles handed to each group so far
+      int kc[NG];                               // tiles handed to each group so far
+#pragma unroll
+      for (int g = 0; g < NG; ++g) kc[g] = 0;
+      int kq[4] = {0, 0, 0, 0};                 // tile t's index within its group, at kq[t & 3]
       auto issue_s = [&](int t) -> int {        // returns the tile's index within its group
-        const int g = uni(S.hdr[t % nv].iseq) & 1;
-        const int k = kc[g]++;
+        const int g = uni(S.hdr[t % nv].iseq) % NG;
+        int k = 0;
+#pragma unroll
+        for (int i = 0; i < NG; ++i)
+          if (i == g) k = kc[i]++;
         const int sb = k & 1;
         mb_wait(&S.s_empty[g][sb], ((uint32_t)(k >> 1) & 1u) ^ 1u);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -613,8 +632,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
         __syncwarp();
         return k;
       };
-      auto finish = [&]() {                     // tell both groups there are no more tiles
-        for (int g = 0; g < 2; ++g) {
+      auto finish = [&]() {                     // tell every group there are no more tiles
+#pragma unroll
+        for (int g = 0; g < NG; ++g) {
           const int sb = kc[g] & 1;
           mb_wait(&S.s_empty[g][sb], ((uint32_t)(kc[g] >> 1) & 1u) ^ 1u);
           if (elect_one()) {
@@ -625,34 +645,43 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
           __syncwarp();
         }
       };
-      mb_wait(&S.kfull[0], 0u);
-      if (uni(S.hdr[0].item) < 0) {
+      // is tile j the end marker?  (waits for it to land)
+      auto landed_end = [&](int j) -> bool {
+        mb_wait(&S.kfull[j % nk], (uint32_t)(j / nk) & 1u);
+        if (lane == 0) TC_TRACE_AT(j, 3);
+        return uni(S.hdr[j % nv].item) < 0;
+      };
+      int end_t = 0x7fffffff;                   // the end marker's ring index, once seen
+      for (int j = 0; j < LA && end_t > j; ++j) {
+        if (landed_end(j)) end_t = j; else kq[j & 3] = issue_s(j);
+      }
+      if (end_t == 0) {
         finish();
       } else {
-        int kt = issue_s(0);
         for (int t = 0;; ++t) {
           const int vs = t % nv;
-          mb_wait(&S.kfull[(t + 1) % nk], (uint32_t)((t + 1) / nk) & 1u);
-          if (lane == 0) TC_TRACE_AT(t + 1, 3);
-          const bool end = uni(S.hdr[(t + 1) % nv].item) < 0;
-          const int kt1 = end ? 0 : issue_s(t + 1);
+          const int j = t + LA;
+          if (end_t > j) {
+            if (landed_end(j)) end_t = j; else kq[j & 3] = issue_s(j);
+          }
+          const int kt = kq[t & 3];
           const int flags = uni(S.hdr[vs].flags);
           const bool first = flags & 1;
           const bool last = flags & 2;
-          const int iseq = uni(S.hdr[vs].iseq), g = iseq & 1;
-          if (first)   // O buffer g must have been read by the epilogue of item iseq - 2
-            mb_wait(&S.o_free[g], ((uint32_t)(iseq >> 1) & 1u) ^ 1u);
+          const int iseq = uni(S.hdr[vs].iseq), g = iseq % NG;
+          if (first)   // O buffer g must have been read by the epilogue of item iseq - NG
+            mb_wait(&S.o_free[g], ((uint32_t)(iseq / NG) & 1u) ^ 1u);
           mb_wait(&S.p_full[g], (uint32_t)kt & 1u);
           mb_wait(&S.vfull[vs], (uint32_t)(t / nv) & 1u);   // V landed (the softmax waited too if it zeroed rows)
           if (lane == 0) TC_TRACE_AT(t, 4);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint8_t* sv = vslot(smem, t, nk, nv);
-          const uint8_t* sp = pbuf + g * PBUF_BYTES;
+          const uint8_t* sp = pbuf + g * PBUF;
           if (elect_one()) {
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk) {        // [O_hi | O_lo]^T += V^T . [P_hi | P_lo]^T, rows in steps of 16
               const int kb = kk >> 2, ko = (kk & 3) * 32;
-              mma(tm + ocol(g), sdesc(sv + kk * 4096, 1024, 2048), sdesc(sp + kb * PBLK_BYTES + ko, 16, 1024), id_o,
+              mma(tm + ocol(g), sdesc(sv + kk * 4096, 1024, 2048), sdesc(sp + kb * PBLK + ko, 16, 1024), id_o,
                   (first && kk == 0) ? 0u : 1u);
             }
             commit(&S.o_done[g]);
@@ -661,8 +690,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
             TC_TRACE_AT(t, 5);
           }
           __syncwarp();
-          if (end) { finish(); break; }
-          kt = kt1;
+          if (t + 1 == end_t) { finish(); break; }
         }
       }
     }
@@ -781,13 +809,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
     // score exceeds the running max by more than LAZY_THR; otherwise
     // p = 2^(s - m) <= 2^8 and nothing is rescaled.  Each lane keeps its own
     // row's partial sums; they are reduced once, in the epilogue.
-    const int grp = warp < 6 ? 0 : 1;
-    const int wq = warp - (grp == 0 ? 2 : 7);         // 0..3 within the group
+    const int grp = warp < 6 ? 0 : 1 + (warp - 7) / 4;
+    const int wq = warp < 6 ? warp - 2 : (warp - 7) % 4;   // 0..3 within the group
     const int lq = warp & 3;                          // TMEM lane quarter this warp may access
     const int row = lq * 32 + lane;                   // TMEM lane = tile row (S) = head-dim index (O)
     const uint32_t lane_base = tmem + ((uint32_t)(lq * 32) << 16);
     const uint32_t oc = ocol(grp);                    // this group's O buffer
-    uint8_t* const pgrp = pbuf + grp * PBUF_BYTES;    // this group's P buffer
+    uint8_t* const pgrp = pbuf + grp * PBUF;          // this group's P buffer
     float m[NC], lrow[NC];
 #pragma unroll
     for (int c = 0; c < NC; ++c) { m[c] = -INFINITY; lrow[c] = 0.f; }
@@ -861,7 +889,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       }
       // P = 2^(s - m) as bf16 hi + lo; row c (query column), column j = row; 128B swizzle
-      uint8_t* sp = pgrp + (row >> 6) * PBLK_BYTES;
+      uint8_t* sp = pgrp + (row >> 6) * PBLK;
       const uint32_t jj2 = (uint32_t)(row & 63) * 2u;
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
@@ -872,7 +900,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
         const uint32_t byte = (uint32_t)c * 128u + jj2;
         const uint32_t sw = byte ^ ((uint32_t)(c & 7) << 4);
         *reinterpret_cast<__nv_bfloat16*>(sp + sw) = hi;
-        *reinterpret_cast<__nv_bfloat16*>(sp + NQ * 128 + sw) = lo;   // row 16 + c: same swizzle phase
+        *reinterpret_cast<__nv_bfloat16*>(sp + NC * 128 + sw) = lo;   // row NC + c: same swizzle phase
       }
       if (!valid && loaded) {                         // loaded rows past the slot's resident rows: V := 0
         mb_wait(&S.vfull[t % nv], (uint32_t)(t / nv) & 1u);   // after the V load has landed
@@ -887,11 +915,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
       if (rescale) {                                // O^T *= corr (this item's previous tile is done)
         float o[NC], olo[NC];
         tmem_ld<NC>(lane_base + oc, o);
-        tmem_ld<NC>(lane_base + oc + NQ, olo);
+        tmem_ld<NC>(lane_base + oc + NC, olo);
 #pragma unroll
         for (int c = 0; c < NC; ++c) { o[c] *= corr[c]; olo[c] *= corr[c]; }
         tmem_st<NC>(lane_base + oc, o);
-        tmem_st<NC>(lane_base + oc + NQ, olo);
+        tmem_st<NC>(lane_base + oc + NC, olo);
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -904,11 +932,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_attn_tc(const __grid_constant
 #pragma unroll
         for (int c = 0; c < NC; ++c) pl[c] = lrow[c];
         col_reduce<false, NC>(pl, S.red[grp][1], wq, lane, grp);
-        mb_wait(&S.o_fin[grp], (uint32_t)(h.iseq >> 1) & 1u);
+        mb_wait(&S.o_fin[grp], (uint32_t)(h.iseq / NG) & 1u);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         float o[NC], olo[NC];
         tmem_ld<NC>(lane_base + oc, o);
-        tmem_ld<NC>(lane_base + oc + NQ, olo);
+        tmem_ld<NC>(lane_base + oc + NC, olo);
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
         if (lane == 0) mb_arrive(&S.o_free[grp]);
@@ -1016,7 +1044,7 @@ extern "C" int s3_debug_tc_trace(unsigned long long* host, int n) {
 }
 #endif
 
-int attn_tc_smem() { return RING_BYTES + 2 * PBUF_BYTES + (int)sizeof(TcSmem) + 1024; }
+int attn_tc_smem(int nc) { return RING_BYTES + tc_groups(nc) * pbuf_bytes(nc) + (int)sizeof(TcSmem) + 1024; }
 template <bool R33>
 const void* attn_tc_ptr(int nc, bool pack, bool feed) {
   if (feed) {
@@ -1081,8 +1109,8 @@ cudaError_t launch_attn_tc(const Shape& sh, const uint16_t* q, const uint16_t* k
   static const int nc_env = [] { const char* e = getenv("S3_TC_NC"); return e ? atoi(e) : 0; }();
   const int nc = (a.G > 8 || nc_env == 16) ? 16 : 8;   // softmax columns (S3_TC_NC=16: pack 16 / G heads)
   a.pmax = pack ? nc / a.G : 1;   // S3_TC_PACK=0: one KV head per tile (A/B)
-  const dim3 grid(grid_attn), block(TC_THREADS);
-  const int smem = attn_tc_smem();
+  const dim3 grid(grid_attn), block(tc_threads(nc));
+  const int smem = attn_tc_smem(nc);
   const void* kfn = attn_tc_kernel_ptr(nc, a.pmax > 1, feed.ready != nullptr, !two_four);
   void* args[] = {(void*)&maps, (void*)&a};
   cudaError_t le = cudaLaunchKernel(kfn, grid, block, args, (size_t)smem, st);

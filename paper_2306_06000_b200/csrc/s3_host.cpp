@@ -555,7 +555,7 @@ s3_status s3_kv_init(const s3_config* cfg, const s3_buffers* b, s3_ctx** out) {
         for (bool feed : {false, true})
           for (bool r33 : {false, true})
             if (cudaFuncSetAttribute(attn_tc_kernel_ptr(nc, pack, feed, r33),
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, attn_tc_smem()) != cudaSuccess)
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, attn_tc_smem(nc)) != cudaSuccess)
               return bail("attn_tc smem attribute");
     ctx->grid_attn = ctx->num_sms;
   }

@@ -155,7 +155,7 @@ cudaError_t launch_verify(const Shape& sh, uint64_t seed, const DSlot* slots, in
 cudaError_t launch_append(const Shape& sh, const DSlot* slots, int32_t B, int32_t l0, int32_t nl,
                           const uint16_t* k_new, const uint16_t* v_new, uint16_t* arena, cudaStream_t st);
 bool attn_tc_supported(const Shape& sh);
-int attn_tc_smem();
+int attn_tc_smem(int nc);
 const void* attn_tc_kernel_ptr(int nc, bool pack, bool feed, bool r33);
 
 cudaError_t launch_attn_tc(const Shape& sh, const uint16_t* q, const uint16_t* k_new, const uint16_t* v_new,

@@ -22,6 +22,7 @@ def main():
     ap.add_argument("--B", type=int, default=8192)
     ap.add_argument("--P", type=int, default=40)
     ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--groups", type=int, default=3, help="softmax groups of the traced build (NG)")
     args = ap.parse_args()
     from paper_2306_06000_b200 import s3 as abi
     abi.LIB_PATH = os.path.abspath(args.lib)
@@ -44,6 +45,7 @@ def main():
     valid = (tr[:, 5] > 0) & (tr[:, 0] > 0) & (tr[:, 6] > 0)
     idx = np.nonzero(valid)[0]
     idx = idx[(idx > 16) & (idx < idx.max() - 16)]
+    idx = idx[tr[idx + args.groups, 6] > 0]
     t = tr[idx]
     per = np.diff(tr[idx, 5])
     res = {
@@ -68,16 +70,16 @@ def main():
     # starts a new (unit, layer) ticket (slot-0 of t+1 after an atomic) -- flags not traced, so report all
     res["producer_gap_p90"] = float(np.percentile(tr[idx + 1, 0] - t[:, 1], 90))
     res["softmax_group_busy_frac"] = float(((t[:, 7] - t[:, 6]).sum()) / span / 2)
-    # short items (one tile per item): tile t belongs to softmax group t & 1; slot 2 = its
+    # short items (one tile per item): tile t belongs to softmax group t % groups; slot 2 = its
     # epilogue end.  Per group: S -> P, P -> epilogue end, and the idle gap until the group's
     # next S (waiting for the MMA thread / the ring)
     ep = tr[idx, 2]
     if (ep > 0).mean() > 0.9:
         res["group_S_to_P"] = float(np.median(t[:, 7] - t[:, 6]))
         res["group_P_to_epilogue_end"] = float(np.median(ep - t[:, 7]))
-        nxt = tr[idx + 2, 6]
+        nxt = tr[idx + args.groups, 6]
         res["group_idle_epilogue_end_to_next_S"] = float(np.median(nxt - ep))
-        res["group_busy_frac"] = float(((ep - t[:, 6]).sum()) / span / 2)
+        res["group_busy_frac"] = float(((ep - t[:, 6]).sum()) / span / args.groups)
         res["MMA_got_P_to_epilogue_end"] = float(np.median(ep - t[:, 4]))
         res["O_commit_to_epilogue_end"] = float(np.median(ep - t[:, 5]))
     print(json.dumps(res))
