@@ -108,14 +108,16 @@ __host__ __device__ constexpr int pblk_bytes(int nc) { return 2 * nc * 64 * 2; }
 __host__ __device__ constexpr int pbuf_bytes(int nc) { return 2 * pblk_bytes(nc); }  // 4 KB (NC 8) / 8 KB (NC 16)
 constexpr float LAZY_THR = 8.0f;            // rescale only if a score beats the running max by 2^8
 // NG softmax groups: group g takes the items with iseq % NG == g, so while one group runs a
-// tile's softmax and epilogue the others run theirs (a short tile's chain -- S load, max,
-// P, the O MMA round trip, epilogue -- is ~4k cycles, so two groups left the period at half
-// of it).  NG = 3 with NC = 8 (P buffers of 4 KB fit next to the 204 KB ring), 2 with NC = 16.
+// tile's softmax and epilogue the other runs its own.  NG = 2 ("ping-pong").  Measured on
+// B200 (tools/attn_sweep.py, -DTC_NG8=3 / 4 builds with 4 KB P buffers and S^T issued NG - 1
+// tiles ahead): 3 groups 0.64 / 0.79 / 0.66 and 4 groups 0.64 / 0.59 / 0.40 of the copy peak
+// (400-row / 40-row / 20-row items) against 2 groups 1.00 / 0.94 / 0.70 -- the idle groups'
+// mbarrier polling takes issue slots from the producer, MMA and working softmax warps.
 // TMEM: S slot (g, b) at columns (2g + b)*16 in [0, 128); O buffer g at 128 + 32g:
 // [0, NC) = V.P_hi, [NC, 2NC) = V.P_lo.
 constexpr int NG_MAX = 4;
 #ifndef TC_NG8
-#define TC_NG8 3
+#define TC_NG8 2
 #endif
 __host__ __device__ constexpr int tc_groups(int nc) { return nc == 8 ? TC_NG8 : 2; }
 constexpr int TMEM_COLS = 256;
