@@ -1079,7 +1079,7 @@ cudaError_t launch_attn_tc(const Shape& sh, const uint16_t* q, const uint16_t* k
                            float* partials, const Unit* units, const Split* splits, const DepDesc* desc,
                            unsigned long long* progress, uint32_t epoch, int32_t* ctrl, int32_t B, int32_t l0,
                            int32_t nl, int32_t grid_attn, int32_t grid_combine, const Feed& feed, uint32_t* evdone,
-                           int32_t short_items, cudaStream_t st) {
+                           int32_t mean_rows, cudaStream_t st) {
   TcMaps maps;
   // staging rows (evicted slots' KV, token-major like the arena); without staging k_prep never fuses an eviction
   const int64_t stage_rows = staging ? staging_bytes / sh.kvpt : 0;
@@ -1105,11 +1105,20 @@ cudaError_t launch_attn_tc(const Shape& sh, const uint16_t* q, const uint16_t* k
   a.arena = reinterpret_cast<uint8_t*>(arena); a.staging = staging; a.kvpt = sh.kvpt;
   a.desc = desc; a.progress = progress; a.epoch = epoch;
   a.k_new = k_new; a.v_new = v_new; a.feed = feed; a.evdone = evdone;
+  // Per launch, from the step's mean resident rows per slot (+1 for the new row):
+  // * ring shape: 2 K + 4 V slots for short items (mostly one tile; <= 48 rows), else 3 + 3
+  //   (the fused row shift holds K slots on long, moving items); LLaMA-3-8B threshold sweep
+  //   32 / 48 / 64 / 96: 48 keeps both the short-context window and the whole run at their best;
+  // * softmax columns NC: 16 (G > 8, or G <= 8 with very short items, <= 28 rows: 16 / G KV
+  //   heads per tile instead of 8 / G, twice the rows per tile) else 8.  tools/attn_sweep.py,
+  //   LLaMA-3-8B shape: 25-row items 0.84 (NC 16) vs 0.70 (NC 8); 33 rows 0.83 both; longer: NC 8.
   static const int ring = [] { const char* e = getenv("S3_TC_RING"); return e ? atoi(e) : 0; }();   // A/B: 24 or 33
-  const bool two_four = ring ? ring == 24 : short_items != 0;
+  static const int short_rows = [] { const char* e = getenv("S3_TC_SHORT_ROWS"); return e ? atoi(e) : 48; }();
+  static const int nc16_rows = [] { const char* e = getenv("S3_TC_NC16_ROWS"); return e ? atoi(e) : 28; }();
+  const bool two_four = ring ? ring == 24 : mean_rows <= short_rows;
   static const int pack = [] { const char* e = getenv("S3_TC_PACK"); return e ? atoi(e) : 1; }();
-  static const int nc_env = [] { const char* e = getenv("S3_TC_NC"); return e ? atoi(e) : 0; }();
-  const int nc = (a.G > 8 || nc_env == 16) ? 16 : 8;   // softmax columns (S3_TC_NC=16: pack 16 / G heads)
+  static const int nc_env = [] { const char* e = getenv("S3_TC_NC"); return e ? atoi(e) : 0; }();   // A/B: 8 or 16
+  const int nc = a.G > 8 ? 16 : nc_env ? (nc_env == 16 ? 16 : 8) : (pack && mean_rows <= nc16_rows ? 16 : 8);
   a.pmax = pack ? nc / a.G : 1;   // S3_TC_PACK=0: one KV head per tile (A/B)
   const dim3 grid(grid_attn), block(tc_threads(nc));
   const int smem = attn_tc_smem(nc);

@@ -743,22 +743,20 @@ s3_status s3_decode_step(s3_ctx* ctx, int32_t l0, int32_t nl, const void* q, con
     ctx->attn_epoch++;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx->prof.on) { e0 = ctx->prof.get(); e1 = ctx->prof.get(); cudaEventRecord(e0, ctx->st); }
-    // tensor-core kernel's ring shape: steps of short items (mean resident rows <= 48) take
-    // 2 K + 4 V slots, longer ones 3 + 3 (see s3_attn_tc.cu; LLaMA-3-8B threshold sweep
-    // 32 / 48 / 64 / 96: 48 keeps both the short-context window and the whole run at their best)
-    int32_t short_items = 0;
-    if (ctx->cfg.attn_variant == 2) {
+    // the tensor-core kernel picks its ring shape and softmax width per launch from the
+    // step's mean rows per slot (see launch_attn_tc)
+    int32_t mean_rows = 0;
+    if (ctx->cfg.attn_variant == 2 && B > 0) {
       int64_t rows = 0;
       for (const DSlot& sl : ctx->slots_h) rows += sl.len + 1;
-      static const long long thr = [] { const char* e = getenv("S3_TC_SHORT_ROWS"); return e ? atoll(e) : 48LL; }();
-      short_items = rows <= thr * B ? 1 : 0;
+      mean_rows = (int32_t)std::min<int64_t>((rows + B - 1) / B, 1 << 30);
     }
     if (ctx->cfg.attn_variant == 2)
       CK(launch_attn_tc(ctx->sh, (const uint16_t*)q, (const uint16_t*)k_new, (const uint16_t*)v_new,
                         (uint16_t*)ctx->buf.arena, ctx->cfg.arena_rows,
                         ctx->buf.staging ? stage_ptr(ctx, ctx->stage_cur) : nullptr, stage_bytes(ctx), out, ctx->partials,
                         ctx->units, ctx->splits, ctx->desc, ctx->progress, ctx->attn_epoch, ctx->ctrl, B, l0, nl,
-                        ctx->grid_attn, ctx->grid_combine, ctx->feed, ev_counters(ctx), short_items, ctx->st),
+                        ctx->grid_attn, ctx->grid_combine, ctx->feed, ev_counters(ctx), mean_rows, ctx->st),
          "k_attn_tc");
     else
       CK(launch_attn(ctx->sh, (const uint16_t*)q, (const uint16_t*)k_new, (const uint16_t*)v_new,
