@@ -193,6 +193,11 @@ __device__ __forceinline__ uint4 lds128(const uint8_t* base, uint32_t off) {
 }
 constexpr int EPI_WARP_BYTES = 16384;   // per epilogue warp: 2 output + 2 input staging tiles of 4 KB
 
+__device__ __forceinline__ bool g_elect_one() {
+  uint32_t p;
+  asm volatile("{\n .reg .pred P;\n elect.sync _|P, 0xffffffff;\n selp.u32 %0, 1, 0, P;\n}\n" : "=r"(p));
+  return p != 0;
+}
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -250,7 +255,7 @@ __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(const __grid_constant__ G
   uint64_t* inbar = tempty + 2;                        // [4 epilogue warps][2 input tiles]
   uint32_t* tmem_base = reinterpret_cast<uint32_t*>(inbar + 8);
   int32_t* s_role = reinterpret_cast<int32_t*>(tmem_base + 1);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
   const uint32_t rank = CG == 2 ? cluster_rank() : 0;
   const bool leader = rank == 0;
   const int unit0 = (int)blockIdx.x / CG, nunits = (int)gridDim.x / CG;   // tile scheduler per CTA group
@@ -285,19 +290,22 @@ __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(const __grid_constant__ G
     return w;
   };
 
+  // The producer and MMA roles run warp-wide with warp-uniform operands and one elected
+  // lane issuing: a tcgen05.mma / TMA operand the compiler cannot prove uniform costs an
+  // ELECT / R2UR.BROADCAST loop around every instruction (see s3_attn_tc.cu, uni()).
   if (warp == 0) {
     // ------------------------------ TMA producer ------------------------------
-    if (lane == 0) {
-      int s = 0;
-      uint32_t ph = 0;
-      WorkIter wi = work();
-      for (Work wk; wi.next(wk);) {
-        const int t = wk.tile;
-        const int m0 = (t % a.m_tiles) * TM_ROWS + (int)rank * GM;
-        const int n0 = (t / a.m_tiles) * BN + (int)rank * (BN / CG);
-        for (int kb = wk.kb0; kb < wk.kb1; ++kb) {
-          g_mb_wait(&empty[s], ph ^ 1u);
-          uint8_t* sa = smem + s * STAGE;
+    int s = 0;
+    uint32_t ph = 0;
+    WorkIter wi = work();
+    for (Work wk; wi.next(wk);) {
+      const int t = wk.tile;
+      const int m0 = (t % a.m_tiles) * TM_ROWS + (int)rank * GM;
+      const int n0 = (t / a.m_tiles) * BN + (int)rank * (BN / CG);
+      for (int kb = wk.kb0; kb < wk.kb1; ++kb) {
+        g_mb_wait(&empty[s], ph ^ 1u);
+        uint8_t* sa = smem + s * STAGE;
+        if (g_elect_one()) {
           if constexpr (CG == 1) {
             g_mb_expect(&full[s], (uint32_t)STAGE);
             g_tma2d(sa, &maps.a, kb * GK, m0, &full[s]);
@@ -307,14 +315,16 @@ __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(const __grid_constant__ G
             g_tma2d_pair(sa, &maps.a, kb * GK, m0, &full[s]);
             g_tma2d_pair(sa + A_BYTES, &maps.w, kb * GK, n0, &full[s]);
           }
-          if (++s == NSTG) { s = 0; ph ^= 1u; }
         }
+        __syncwarp();
+        if (++s == NSTG) { s = 0; ph ^= 1u; }
       }
     }
   } else if (warp == 1) {
     // ------------------------------- MMA issuer -------------------------------
-    if (lane == 0 && leader) {
+    if (leader) {
       constexpr uint32_t id = g_idesc(BN, TM_ROWS);
+      const uint32_t tm = (uint32_t)__shfl_sync(0xffffffffu, (int)tmem, 0);
       int s = 0;
       uint32_t ph = 0;
       int it = 0;
@@ -323,23 +333,28 @@ __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(const __grid_constant__ G
         const int acc = it & 1;
         g_mb_wait(&tempty[acc], ((uint32_t)(it >> 1) & 1u) ^ 1u);   // the epilogue(s) drained this accumulator
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t d = tmem + (uint32_t)(acc * BN);
+        const uint32_t d = tm + (uint32_t)(acc * BN);
         const int kb0 = wk.kb0, kb1 = wk.kb1;
         for (int kb = kb0; kb < kb1; ++kb) {
           g_mb_wait(&full[s], ph);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint8_t* sa = smem + s * STAGE;
           const uint64_t da = g_desc(sa), dw = g_desc(sa + A_BYTES);
+          if (g_elect_one()) {   // MMAs and their commits from the same lane
 #pragma unroll
-          for (int k = 0; k < GK / 16; ++k) {        // +32 B per K = 16 inside the swizzle atom
-            if constexpr (CG == 1) g_mma(d, da + (uint64_t)(k * 2), dw + (uint64_t)(k * 2), id, kb > kb0 || k);
-            else g_mma_pair(d, da + (uint64_t)(k * 2), dw + (uint64_t)(k * 2), id, kb > kb0 || k);
+            for (int k = 0; k < GK / 16; ++k) {      // +32 B per K = 16 inside the swizzle atom
+              if constexpr (CG == 1) g_mma(d, da + (uint64_t)(k * 2), dw + (uint64_t)(k * 2), id, kb > kb0 || k);
+              else g_mma_pair(d, da + (uint64_t)(k * 2), dw + (uint64_t)(k * 2), id, kb > kb0 || k);
+            }
+            // the stage is free once these MMAs have read it (in both CTAs of a pair)
+            if constexpr (CG == 1) g_commit(&empty[s]); else g_commit_pair(&empty[s]);
+            if (kb == kb1 - 1) {   // accumulator complete
+              if constexpr (CG == 1) g_commit(&tfull[acc]); else g_commit_pair(&tfull[acc]);
+            }
           }
-          // the stage is free once these MMAs have read it (in both CTAs of a pair)
-          if constexpr (CG == 1) g_commit(&empty[s]); else g_commit_pair(&empty[s]);
+          __syncwarp();
           if (++s == NSTG) { s = 0; ph ^= 1u; }
         }
-        if constexpr (CG == 1) g_commit(&tfull[acc]); else g_commit_pair(&tfull[acc]);   // accumulator complete
       }
     }
   } else {

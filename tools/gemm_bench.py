@@ -27,7 +27,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--m", default="128,256,512,1024,2048,4096")
     ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--lib", default=None, help="A/B: load this libs3.so build instead of the in-tree one")
     args = ap.parse_args()
+    if args.lib:
+        abi.LIB_PATH = os.path.abspath(args.lib)
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     st = torch.cuda.current_stream()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
