@@ -65,11 +65,14 @@ def parse():
     ap.add_argument("--compact-policy", default="every", choices=["every", "on-demand"],
                     help="row shift every step (the paper) or only when the pool could use the rows (R27)")
     ap.add_argument("--model", default="none", choices=["none", "gptj"],
-                    help="gptj: random-weight GPT-J layers (cuBLAS GEMMs) around the path (SURVEY NEXT-2)")
+                    help="gptj: random-weight GPT-J layers (libs3 tcgen05 GEMMs) around the path (SURVEY NEXT-2)")
     ap.add_argument("--compact", default="fused", choices=["fused", "pass"],
                     help="row shift as a separate k_move pass, or fused into the attention pass")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend of the counter exchange (gloo: tests sharing one GPU)")
+    ap.add_argument("--dist-always", action="store_true",
+                    help="world 1: still create the process group and run every step's counter all-reduce "
+                         "through the multi-rank admission path (the N > 1 exchange on one GPU)")
     return ap.parse_args()
 
 
@@ -290,8 +293,15 @@ class Ctx:
         torch.cuda.set_device(self.local)
         self.dev = torch.device("cuda", self.local)
         self.dist = None
-        if self.world > 1:
+        # the exchange runs at world > 1, or at world 1 with --dist-always (same schedule: one bin)
+        self.dist_on = self.world > 1 or args.dist_always
+        if self.dist_on:
             import torch.distributed as dist
+            if self.world == 1:
+                os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+                os.environ.setdefault("MASTER_PORT", "29531")
+                os.environ.setdefault("RANK", "0")
+                os.environ.setdefault("WORLD_SIZE", "1")
             if args.dist_backend == "nccl":
                 dist.init_process_group("nccl", device_id=self.dev)
             else:
@@ -301,7 +311,8 @@ class Ctx:
         self.shape = SHAPES[args.shape]
         self.clocks = ClockSampler(self.local)
         self.last_counters = None
-        self.exchange = self._make_exchange() if self.world > 1 else None
+        self.exchange = self._make_exchange() if self.dist_on else None
+        self.exchange_ms = []          # host wall time of each exchange (all-reduce + read-back)
 
     def _make_exchange(self):
         import torch
@@ -312,6 +323,12 @@ class Ctx:
         xstream = torch.cuda.Stream(device=self.dev) if self.cdev.type == "cuda" else None
 
         def exchange(row):
+            t0 = time.perf_counter()
+            out = _exchange(row)
+            self.exchange_ms.append((time.perf_counter() - t0) * 1e3)
+            return out
+
+        def _exchange(row):
             if xstream is None:
                 mat.zero_()
                 mat[rank] = torch.from_numpy(row)
@@ -387,7 +404,8 @@ class Ctx:
             if cap_gb > 0:
                 R = min(R, int(cap_gb * 1e9 // kvpt))
         eng = S3Engine(L, H, D, GPTJ["max_len"], R, max_running, device=self.local, rank=self.rank,
-                       world=self.world, num_kv_heads=0 if Hkv == H else Hkv, seed=a.seed, staging_bytes=staging,
+                       world=self.world, exchange_admission=self.dist_on,
+                       reserve_sms=4 if self.dist_on else 0, num_kv_heads=0 if Hkv == H else Hkv, seed=a.seed, staging_bytes=staging,
                        host_store_bytes=host_store or ((16 << 30) if (p > 0 or policy == "short") else (1 << 30)),
                        attn_variant={"tma": 0, "regs": 1, "tc": 2}[a.attn],
                        compact_mode=(0 if a.compact == "fused" else 1) if compact_mode is None else compact_mode,
@@ -407,7 +425,7 @@ class Ctx:
 
     def done(self, eng):
         """Global termination (identical on every rank: the last exchanged counters)."""
-        if self.world == 1:
+        if self.exchange is None:
             c = eng.counters_local()
             return eng.B == 0 and c[3] + c[4] == 0
         m = self.last_counters
@@ -606,6 +624,11 @@ def run_s3(args):
             },
             "clocks": cx.clocks.summary(),
             "rank_balance": balance,
+            "exchange": None if cx.exchange is None else {
+                "backend": cx.dist.get_backend(), "world": world, "exchanges": len(cx.exchange_ms),
+                "host_ms_median": round(sorted(cx.exchange_ms)[len(cx.exchange_ms) // 2], 4) if cx.exchange_ms else None,
+                "note": "per step: [world][8] int64 counter all-reduce on its own stream (attention grid leaves "
+                        "reserve_sms SMs free), read back by the host for the shared multi-bin FFD"},
             "cpu_baseline": cpu,
             "e2e": e2e,
         }
@@ -671,7 +694,7 @@ def leg_c2(cx, peak, pcie, p=0.1, steps=150, warmup=5):
     import numpy as np
     eng, t, R, kvpt = cx.new_engine("short", p, REQ_PER_GPU)
     eng.submit(t.req_id, t.prompt, t.alloc, t.out)
-    eng.initial_admit(None)
+    eng.initial_admit(cx.exchange)
     ms, tokens, n, batches, stats, prof = timed_run(cx, eng, steps=steps, warmup=warmup)
     cx.free_engine(eng)
     ev = sum(s.evicted for s in stats)
@@ -695,7 +718,7 @@ def leg_c2(cx, peak, pcie, p=0.1, steps=150, warmup=5):
     # the paper's separate row-shift pass (k_move), same trace, for its own GB/s
     eng, t, R, kvpt = cx.new_engine("short", p, REQ_PER_GPU, compact_mode=1)
     eng.submit(t.req_id, t.prompt, t.alloc, t.out)
-    eng.initial_admit(None)
+    eng.initial_admit(cx.exchange)
     ms2, tok2, n2, _, st2, prof2 = timed_run(cx, eng, steps=60, warmup=warmup)
     cx.free_engine(eng)
     kgbs = prof2.move_bytes / (prof2.move_ms / 1e3) / 1e9 if prof2.move_ms else None
@@ -724,7 +747,7 @@ def leg_c3(cx, mean_batch_oracle, n_req, R_main, steps=30, warmup=3):
             lw = float((sa * tr.out).sum() / (sp * tr.out).sum())
     eng, t, R, kvpt = cx.new_engine("maxlen", 0.0, n_req)
     eng.submit(t.req_id, t.prompt, t.alloc, t.out)
-    eng.initial_admit(None)
+    eng.initial_admit(cx.exchange)
     ms, tokens, n, batches, stats, prof = timed_run(cx, eng, steps=steps, warmup=warmup)
     cx.free_engine(eng)
     b_max = float(np.mean(batches))
@@ -759,7 +782,7 @@ def cpu_baseline_leg(cx):
     for rep in range(2):                                   # the first pass warms modules and allocations
         eng, _, _, _ = cx.new_engine(pol, p, trace=sub, max_running=SLICE_SEQ, R=R, host_store=1 << 30)
         eng.submit(sub.req_id, sub.prompt, sub.alloc, sub.out)
-        eng.initial_admit(None)
+        eng.initial_admit(cx.exchange)
         ms, tok, n, _, stats, _ = timed_run(cx, eng, steps=SLICE_STEPS)
         cx.free_engine(eng)
         gpu = {"value": tok / (ms / 1e3), "unit": "tokens/s", "steps": n, "tokens": tok,
@@ -787,11 +810,7 @@ def model_step(eng, proxy, exchange, world):
     from paper_2306_06000_b200.engine import StepStats
     B = proxy.decode_step()
     rep, perm, ev, fin = eng.evict_compact()
-    if world == 1:
-        reps = [eng.admit()[0]]
-    else:
-        reps = [eng.admit_home()[0]]
-        reps.append(eng.admit_shared(exchange(eng.counters_local()))[0])
+    reps = eng.admit_step(exchange)
     return StepStats(B, B, rep.n_finished, rep.n_evicted, sum(r.n_admitted for r in reps), rep.d2h_bytes,
                      rep.moved_bytes + sum(r.moved_bytes for r in reps), rep.paper_pcie_bytes, rep.paper_hbm_bytes,
                      sum(r.h2d_bytes for r in reps), sum(r.fill_bytes for r in reps),
@@ -836,11 +855,7 @@ def phase_breakdown(eng, exchange, world, steps):
         ev[2].record()
         eng.evict_compact()
         ev[3].record()
-        if world == 1:
-            eng.admit()
-        else:
-            eng.admit_home()
-            eng.admit_shared(exchange(eng.counters_local()))
+        eng.admit_step(exchange)
         ev[4].record()
         torch.cuda.synchronize()
         for i, n in enumerate(names):
@@ -886,11 +901,7 @@ def e2e_leg(eng, exchange, dist, dev, steps, world, chunks=0, device_out=True):
         e0.record()
         eng.decode_host(hq, hk, hv, he, ho, chunks=chunks, device_out=device_out)
         eng.evict_compact()
-        if world == 1:
-            eng.admit()
-        else:
-            eng.admit_home()
-            eng.admit_shared(exchange(eng.counters_local()))
+        eng.admit_step(exchange)
         e1.record()
         torch.cuda.synchronize()
         total_ms += e0.elapsed_time(e1)

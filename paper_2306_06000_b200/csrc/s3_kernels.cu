@@ -442,6 +442,11 @@ __global__ void __launch_bounds__(1024) k_prep(PrepArgs a) {
 #endif
     if (!s_last) return;
   }
+#ifdef PREP_TRACE
+  if (nb == 1 && threadIdx.x == 0)
+    printf("prep 1 cta B %d: pass1 %llu scan %llu pass2 %llu sync %llu\n", B, ptt[1] - ptt[0], ptt[2] - ptt[1],
+           ptt[5] - ptt[4], ptt[6] - ptt[5]);
+#endif
   if (threadIdx.x == 0) {
     a.ctrl[CTRL_N_UNITS] = (int)tot[0];
     a.ctrl[CTRL_N_SPLITS] = (int)tot[1];

@@ -40,7 +40,7 @@ class S3Engine:
     def __init__(self, num_layers, num_heads, head_dim, max_seq_len, arena_rows, max_running,
                  chunk_rows=0, move_chunk_bytes=0, device=0, rank=0, world=1, seed=1,
                  staging_bytes=None, host_store_bytes=None, io_rows=None, attn_variant=0, compact_mode=0,
-                 compact_policy=0, num_kv_heads=0, reserve_sms=0):
+                 compact_policy=0, num_kv_heads=0, reserve_sms=0, exchange_admission=False):
         if not torch.cuda.is_available():
             raise RuntimeError("S3Engine needs a CUDA device (no CPU fallback)")
         self.device = torch.device("cuda", device)
@@ -49,6 +49,10 @@ class S3Engine:
         self.Hkv = num_kv_heads or num_heads
         self.max_running = max_running
         self.world, self.rank = world, rank
+        # the multi-rank admission (home re-admission -> counter all-reduce -> shared multi-bin
+        # FFD) also at world 1 when asked: with one bin it admits exactly what s3_admit does,
+        # and it puts the caller's process-group exchange (NCCL) on the step's path
+        self.split_admit = world > 1 or exchange_admission
         self.stream = torch.cuda.current_stream(self.device)
         self.cfg = abi.s3_config(
             num_layers=num_layers, num_heads=num_heads, head_dim=head_dim, max_seq_len=max_seq_len,
@@ -157,6 +161,16 @@ class S3Engine:
             return abi.s3_admit(self.ctx, self.max_running)
         raise RuntimeError("world > 1: use admit_home / exchange / admit_shared")
 
+    def admit_step(self, exchange=None):
+        """The step's admission: s3_admit (world 1), or s3_admit_home, the caller's
+        all-reduce of the counter rows (`exchange`), s3_admit_shared.  Returns the
+        admission reports."""
+        if not self.split_admit:
+            return [self.admit()[0]]
+        hrep, _ = self.admit_home()
+        srep, _ = self.admit_shared(exchange(self.counters_local()))
+        return [hrep, srep]
+
     def admit_home(self):
         return abi.s3_admit_home(self.ctx, self.max_running)
 
@@ -192,21 +206,14 @@ class S3Engine:
             self.synth_inputs()
         self.decode()
         rep, perm, ev, fin = self.evict_compact()
-        if self.world == 1:
-            arep, _ = self.admit()
-            reps = [arep]
-        else:
-            hrep, _ = self.admit_home()
-            allrows = exchange(self.counters_local())
-            srep, _ = self.admit_shared(allrows)
-            reps = [hrep, srep]
+        reps = self.admit_step(exchange)
         return StepStats(B, B, rep.n_finished, rep.n_evicted, sum(r.n_admitted for r in reps), rep.d2h_bytes,
                          rep.moved_bytes + sum(r.moved_bytes for r in reps), rep.paper_pcie_bytes,
                          rep.paper_hbm_bytes, sum(r.h2d_bytes for r in reps), sum(r.fill_bytes for r in reps),
                          sum(r.stage_reload_bytes for r in reps))
 
     def initial_admit(self, exchange=None):
-        if self.world == 1:
+        if not self.split_admit:
             return self.admit()
         self.admit_home()
         return self.admit_shared(exchange(self.counters_local()))

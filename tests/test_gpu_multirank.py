@@ -139,3 +139,32 @@ def test_bench_torchrun_two_ranks_gloo():
     import s3synth
     t = s3synth.make_trace(3000, seed=1, policy="oracle", max_seq_len=2048)
     assert j["wholerun"]["tokens"] == int(t.out.sum())
+
+
+def test_bench_nccl_exchange_world1():
+    """The N > 1 exchange on the one GPU this pool has: --dist-always creates an NCCL
+    process group of one rank and runs every step's counter all-reduce (its own stream,
+    reserve_sms left free by the attention grid) through the multi-rank admission path
+    (s3_admit_home -> all-reduce -> s3_admit_shared).  With one bin the shared multi-bin
+    FFD admits exactly what s3_admit does, so the schedule -- tokens in the window and
+    over the whole run -- equals the plain world-1 run's."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    base = [os.path.join(ROOT, "bench.py"), "--gpus", "1", "--steps", "10", "--warmup", "3",
+            "--arena-gb", "12", "--requests", "1500", "--no-cpu-baseline"]
+    port = _free_port()
+    runs = {}
+    for name, cmd in (("nccl", [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+                                "--master-addr", "127.0.0.1", "--master-port", str(port), *base, "--dist-always"]),
+                      ("plain", [sys.executable, *base])):
+        out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+        assert out.returncode == 0, out.stderr[-3000:]
+        lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+        assert len(lines) == 1
+        runs[name] = json.loads(lines[0])
+    x = runs["nccl"]["exchange"]
+    assert x["backend"] == "nccl" and x["world"] == 1 and x["exchanges"] >= 13
+    assert runs["plain"]["exchange"] is None
+    assert runs["nccl"]["tokens"] == runs["plain"]["tokens"]
+    assert runs["nccl"]["wholerun"]["tokens"] == runs["plain"]["wholerun"]["tokens"]
+    assert runs["nccl"]["wholerun"]["steps"] == runs["plain"]["wholerun"]["steps"]
