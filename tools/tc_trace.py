@@ -22,7 +22,7 @@ def main():
     ap.add_argument("--B", type=int, default=8192)
     ap.add_argument("--P", type=int, default=40)
     ap.add_argument("--steps", type=int, default=3)
-    ap.add_argument("--groups", type=int, default=3, help="softmax groups of the traced build (NG)")
+    ap.add_argument("--groups", type=int, default=2, help="softmax groups of the traced build (NG)")
     args = ap.parse_args()
     from paper_2306_06000_b200 import s3 as abi
     abi.LIB_PATH = os.path.abspath(args.lib)
