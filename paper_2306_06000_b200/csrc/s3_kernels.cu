@@ -401,10 +401,20 @@ __global__ void __launch_bounds__(1024) k_prep(PrepArgs a) {
     capx += sl.cap;
   }
   if (fused) {
-    if (first < B) atomicMin(&s_first_hole, first);
-    if (hbm) atomicAdd(&s_hbm, hbm);
-    if (moved) atomicAdd(&s_moved, moved);
-    if (end) atomicMax(&s_end, end);
+    // warp-reduce first: one shared atomic per warp instead of per thread
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
+      hbm += __shfl_xor_sync(0xffffffffu, hbm, o);
+      moved += __shfl_xor_sync(0xffffffffu, moved, o);
+      end = max(end, __shfl_xor_sync(0xffffffffu, end, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+      if (first < B) atomicMin(&s_first_hole, first);
+      if (hbm) atomicAdd(&s_hbm, hbm);
+      if (moved) atomicAdd(&s_moved, moved);
+      if (end) atomicMax(&s_end, end);
+    }
   }
   PREP_T(5);
   __syncthreads();
@@ -804,9 +814,17 @@ __global__ void __launch_bounds__(1024) k_keep_scan(Shape sh, const DSlot* __res
       }
       capx += sl.cap;
     }
-    if (first < B) atomicMin(&s_first_hole, first);
-    if (hbm) atomicAdd(&s_hbm, hbm);
-    if (end) atomicMax(&s_end, end);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {   // warp-reduce before the shared atomics (see k_prep)
+      first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
+      hbm += __shfl_xor_sync(0xffffffffu, hbm, o);
+      end = max(end, __shfl_xor_sync(0xffffffffu, end, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+      if (first < B) atomicMin(&s_first_hole, first);
+      if (hbm) atomicAdd(&s_hbm, hbm);
+      if (end) atomicMax(&s_end, end);
+    }
   }
   long long ytot[3];
   block_excl_scan<3>(y, ytot);
