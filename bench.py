@@ -70,6 +70,9 @@ def parse():
                     help="row shift as a separate k_move pass, or fused into the attention pass")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend of the counter exchange (gloo: tests sharing one GPU)")
+    ap.add_argument("--exchange", default="native", choices=["native", "torch"],
+                    help="counter all-reduce: libs3's own NCCL communicator (s3_comm_init / "
+                         "s3_exchange_counters; nccl backend only) or torch.distributed")
     ap.add_argument("--dist-always", action="store_true",
                     help="world 1: still create the process group and run every step's counter all-reduce "
                          "through the multi-rank admission path (the N > 1 exchange on one GPU)")
@@ -311,6 +314,10 @@ class Ctx:
         self.shape = SHAPES[args.shape]
         self.clocks = ClockSampler(self.local)
         self.last_counters = None
+        # native: every engine binds libs3's own NCCL communicator (s3_comm_init) and the
+        # exchange below is s3_exchange_counters on the current engine
+        self.native = self.dist_on and args.dist_backend == "nccl" and args.exchange == "native"
+        self.engine = None
         self.exchange = self._make_exchange() if self.dist_on else None
         self.exchange_ms = []          # host wall time of each exchange (all-reduce + read-back)
 
@@ -324,8 +331,9 @@ class Ctx:
 
         def exchange(row):
             t0 = time.perf_counter()
-            out = _exchange(row)
+            out = self.engine.exchange_counters() if self.native else _exchange(row)
             self.exchange_ms.append((time.perf_counter() - t0) * 1e3)
+            self.last_counters = out       # global termination test (done())
             return out
 
         def _exchange(row):
@@ -340,7 +348,6 @@ class Ctx:
                     mat[rank].copy_(torch.from_numpy(row))
                     dist.all_reduce(mat)                      # NCCL over NVLink: the counter exchange
                     out = mat.cpu().numpy()
-            self.last_counters = out
             return out
         return exchange
 
@@ -410,6 +417,13 @@ class Ctx:
                        attn_variant={"tma": 0, "regs": 1, "tc": 2}[a.attn],
                        compact_mode=(0 if a.compact == "fused" else 1) if compact_mode is None else compact_mode,
                        compact_policy=0 if a.compact_policy == "every" else 1)
+        if self.native:
+            # a fresh communicator per engine: rank 0's id broadcast over the process group
+            from paper_2306_06000_b200 import s3 as abi
+            obj = [abi.s3_nccl_get_unique_id() if self.rank == 0 else None]
+            self.dist.broadcast_object_list(obj, src=0)
+            eng.comm_init(obj[0])
+        self.engine = eng
         return eng, trace, R, kvpt
 
     @staticmethod
@@ -625,7 +639,9 @@ def run_s3(args):
             "clocks": cx.clocks.summary(),
             "rank_balance": balance,
             "exchange": None if cx.exchange is None else {
-                "backend": cx.dist.get_backend(), "world": world, "exchanges": len(cx.exchange_ms),
+                "backend": cx.dist.get_backend() + (" (libs3 communicator: s3_exchange_counters)" if cx.native
+                                                    else " (torch.distributed all_reduce)"),
+                "world": world, "exchanges": len(cx.exchange_ms),
                 "host_ms_median": round(sorted(cx.exchange_ms)[len(cx.exchange_ms) // 2], 4) if cx.exchange_ms else None,
                 "note": "per step: [world][8] int64 counter all-reduce on its own stream (attention grid leaves "
                         "reserve_sms SMs free), read back by the host for the shared multi-bin FFD"},
@@ -654,6 +670,8 @@ def timed_run(cx, eng, steps=None, until_done=False, warmup=0):
     e0.record()
     n, tokens, batches, stats = 0, 0, [], []
     while (until_done and not cx.done(eng)) or (not until_done and n < steps):
+        if n > 200_000:
+            raise RuntimeError("timed_run: no global termination after 200k steps")
         s = eng.step(cx.exchange)
         tokens += s.tokens
         batches.append(s.batch)

@@ -48,6 +48,7 @@ typedef enum {
   S3_E_INVAL = 1,          /* bad argument or config                                 */
   S3_E_NOMEM = 2,          /* caller buffer / host store too small                   */
   S3_E_CUDA = 3,           /* CUDA runtime error (context poisoned)                  */
+  S3_E_NCCL = 4,           /* NCCL error or NCCL not loadable (s3_comm_*; poisons)    */
   S3_E_STATE = 5,          /* call out of order / logic error          */
   S3_E_UNSCHEDULABLE = 6   /* reservation larger than the whole arena  */
 } s3_status;
@@ -241,6 +242,44 @@ s3_status s3_admit_home(s3_ctx* ctx, s3_admit_report* rep, int64_t* admitted_ids
 s3_status s3_admit_shared(s3_ctx* ctx, const int64_t* counters_all /* [world][S3_NCOUNTERS] */,
                           s3_admit_report* rep, int64_t* admitted_ids);
 s3_status s3_counters_local(const s3_ctx* ctx, int64_t row[S3_NCOUNTERS]);
+
+/* ---- (a8): the counter exchange over a library-owned NCCL communicator --
+ * The supervisor "passes the information to the scheduler":
+ * with ranks partitioned by sequence (R26) that is one all-reduce
+ * (sum) of the [world][S3_NCOUNTERS] int64 matrix per step, between
+ * s3_admit_home and s3_admit_shared.  NCCL is loaded at run time
+ * (dlopen "libnccl.so.2" -- in a torch process, torch's copy); without it the
+ * calls return S3_E_NCCL and the caller may all-reduce s3_counters_local
+ * rows itself (torch.distributed) instead.
+ *   s3_nccl_get_unique_id  rank 0 creates the id; the caller broadcasts its
+ *                          S3_NCCL_ID_BYTES bytes to every rank (e.g.
+ *                          torch.distributed.broadcast_object_list);
+ *   s3_comm_init           every rank binds it (collective; rank / world from
+ *                          s3_config).  The communicator, its stream (highest
+ *                          priority, non-blocking) and a [world][S3_NCOUNTERS]
+ *                          device + pinned host buffer belong to the context
+ *                          (freed by s3_kv_destroy).  S3_E_STATE if already bound;
+ *   s3_exchange_counters   fills this rank's row (s3_counters_local), all-reduces
+ *                          the matrix on the communicator's stream -- which does
+ *                          not wait for cfg.stream, so it runs while this step's
+ *                          attention pass still streams (the persistent attention
+ *                          grids leave s3_config.reserve_sms SMs free) -- and
+ *                          returns it in counters_all (blocking until it is back);
+ *   s3_counters_get        the last exchanged matrix as per-rank / total counters
+ *                          (before any exchange: this rank's row alone).        */
+#define S3_NCCL_ID_BYTES 128
+#define S3_MAX_RANKS 64
+s3_status s3_nccl_get_unique_id(uint8_t id[S3_NCCL_ID_BYTES]);
+s3_status s3_comm_init(s3_ctx* ctx, const uint8_t id[S3_NCCL_ID_BYTES]);
+s3_status s3_exchange_counters(s3_ctx* ctx, int64_t* counters_all /* [world][S3_NCOUNTERS] */);
+typedef struct {
+  int32_t world, exchanges;                       /* ranks; exchanges so far                  */
+  int64_t rank_free_rows[S3_MAX_RANKS], rank_running[S3_MAX_RANKS];
+  int64_t free_rows_total, running_total, evicted_waiting_total;
+  int64_t fresh_waiting;                          /* the shared pool (identical on every rank) */
+  int64_t finished_total, evicted_total, tokens_total;
+} s3_counters;
+s3_status s3_counters_get(const s3_ctx* ctx, s3_counters* counters);
 
 /* ---- pure host planning helpers (no device work; callable without a GPU) */
 /* Single-bin FFD: admitted[i] = 1 if item i is admitted.  Returns count.  */

@@ -21,6 +21,7 @@ FLAGS = [
     "-Xcompiler", "-fPIC,-O3", "-shared",
     "-cudart", "static",
     "-I", INCLUDE,
+    "-ldl",
 ]
 
 

@@ -7,6 +7,8 @@
 // D2H copies ride a side stream.  One host synchronisation per step: the
 // keep-scan report readback in s3_evict_compact.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <climits>
@@ -200,6 +202,13 @@ struct s3_ctx {
   bool poisoned = false;
   const char* err = "ok";
   Prof prof;
+  // (a8) library-owned NCCL communicator for the per-step counter all-reduce
+  ncclComm_t comm = nullptr;
+  cudaStream_t xs = nullptr;                // its stream (highest priority, non-blocking)
+  int64_t* x_dev = nullptr;                 // [world][S3_NCOUNTERS] device matrix
+  int64_t* x_host = nullptr;                // pinned staging of the same
+  std::vector<int64_t> x_last;              // the last exchanged matrix
+  int32_t exchanges = 0;
 };
 
 namespace {
@@ -207,10 +216,37 @@ namespace {
 s3_status fail(s3_ctx* c, s3_status s, const char* msg) {
   if (c) {
     c->err = msg;
-    if (s == S3_E_CUDA) c->poisoned = true;
+    if (s == S3_E_CUDA || s == S3_E_NCCL) c->poisoned = true;
   }
   return s;
 }
+
+// NCCL, resolved at run time: the library loads without it, and in a torch process
+// "libnccl.so.2" is torch's already-loaded copy
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                             cudaStream_t) = nullptr;
+  ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+};
+const NcclApi& nccl_api() {
+  static const NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+    a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+    a.comm_init_rank = reinterpret_cast<decltype(a.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+    a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(h, "ncclAllReduce"));
+    a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+    a.ok = a.get_unique_id && a.comm_init_rank && a.all_reduce && a.comm_destroy;
+    return a;
+  }();
+  return api;
+}
+static_assert(sizeof(ncclUniqueId) == S3_NCCL_ID_BYTES, "ncclUniqueId size");
 
 #define CK(expr, msg)                                             \
   do {                                                            \
@@ -638,6 +674,10 @@ s3_status s3_kv_destroy(s3_ctx* ctx) {
   if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->h_report) cudaFreeHost(ctx->h_report);
   if (ctx->h_upload) cudaFreeHost(ctx->h_upload);
+  if (ctx->comm) nccl_api().comm_destroy(ctx->comm);
+  if (ctx->xs) { cudaStreamSynchronize(ctx->xs); cudaStreamDestroy(ctx->xs); }
+  if (ctx->x_dev) cudaFree(ctx->x_dev);
+  if (ctx->x_host) cudaFreeHost(ctx->x_host);
   delete ctx;
   return S3_OK;
 }
@@ -1188,6 +1228,85 @@ s3_status s3_counters_local(const s3_ctx* ctx, int64_t row[S3_NCOUNTERS]) {
   row[5] = ctx->finished_total;
   row[6] = ctx->evicted_total;
   row[7] = ctx->tokens_total;
+  return S3_OK;
+}
+
+s3_status s3_nccl_get_unique_id(uint8_t id[S3_NCCL_ID_BYTES]) {
+  if (!id) return S3_E_INVAL;
+  const NcclApi& api = nccl_api();
+  if (!api.ok) return S3_E_NCCL;
+  ncclUniqueId u;
+  if (api.get_unique_id(&u) != ncclSuccess) return S3_E_NCCL;
+  std::memcpy(id, &u, sizeof(u));
+  return S3_OK;
+}
+
+s3_status s3_comm_init(s3_ctx* ctx, const uint8_t id[S3_NCCL_ID_BYTES]) {
+  if (s3_status s = check_ctx(ctx)) return s;
+  if (!id) return fail(ctx, S3_E_INVAL, "comm_init: null id");
+  if (ctx->comm) return fail(ctx, S3_E_STATE, "comm_init: communicator already bound");
+  if (ctx->cfg.world > S3_MAX_RANKS) return fail(ctx, S3_E_INVAL, "comm_init: world > S3_MAX_RANKS");
+  const NcclApi& api = nccl_api();
+  if (!api.ok) return S3_E_NCCL;   // not loadable: nothing bound, the context stays usable
+  CK(cudaSetDevice(ctx->cfg.device), "cudaSetDevice");
+  int lo = 0, hi = 0;
+  CK(cudaDeviceGetStreamPriorityRange(&lo, &hi), "stream priorities");
+  CK(cudaStreamCreateWithPriority(&ctx->xs, cudaStreamNonBlocking, hi), "exchange stream");
+  const size_t bytes = sizeof(int64_t) * S3_NCOUNTERS * (size_t)ctx->cfg.world;
+  CK(cudaMalloc(&ctx->x_dev, bytes), "exchange buffer");
+  CK(cudaHostAlloc(&ctx->x_host, bytes, cudaHostAllocDefault), "exchange host buffer");
+  ncclUniqueId u;
+  std::memcpy(&u, id, sizeof(u));
+  if (api.comm_init_rank(&ctx->comm, ctx->cfg.world, u, ctx->cfg.rank) != ncclSuccess) {
+    ctx->comm = nullptr;
+    return fail(ctx, S3_E_NCCL, "ncclCommInitRank");
+  }
+  return S3_OK;
+}
+
+s3_status s3_exchange_counters(s3_ctx* ctx, int64_t* counters_all) {
+  if (s3_status s = check_ctx(ctx)) return s;
+  if (!counters_all) return fail(ctx, S3_E_INVAL, "exchange_counters: null output");
+  if (!ctx->comm) return fail(ctx, S3_E_STATE, "exchange_counters: no communicator (s3_comm_init)");
+  const int W = ctx->cfg.world;
+  const size_t n = (size_t)S3_NCOUNTERS * W, bytes = n * sizeof(int64_t);
+  std::memset(ctx->x_host, 0, bytes);
+  s3_counters_local(ctx, ctx->x_host + (size_t)ctx->cfg.rank * S3_NCOUNTERS);
+  CK(cudaMemcpyAsync(ctx->x_dev, ctx->x_host, bytes, cudaMemcpyHostToDevice, ctx->xs), "exchange H2D");
+  if (nccl_api().all_reduce(ctx->x_dev, ctx->x_dev, n, ncclInt64, ncclSum, ctx->comm, ctx->xs) != ncclSuccess)
+    return fail(ctx, S3_E_NCCL, "ncclAllReduce");
+  CK(cudaMemcpyAsync(ctx->x_host, ctx->x_dev, bytes, cudaMemcpyDeviceToHost, ctx->xs), "exchange D2H");
+  CK(cudaStreamSynchronize(ctx->xs), "exchange sync");
+  std::memcpy(counters_all, ctx->x_host, bytes);
+  ctx->x_last.assign(ctx->x_host, ctx->x_host + n);
+  ctx->exchanges++;
+  return S3_OK;
+}
+
+s3_status s3_counters_get(const s3_ctx* ctx, s3_counters* c) {
+  if (!ctx || !c) return S3_E_INVAL;
+  *c = s3_counters{};
+  std::vector<int64_t> m = ctx->x_last;
+  int W = ctx->cfg.world;
+  if (m.empty()) {   // no exchange yet: this rank's row alone
+    W = 1;
+    m.assign(S3_NCOUNTERS, 0);
+    s3_counters_local(ctx, m.data());
+  }
+  c->world = W;
+  c->exchanges = ctx->exchanges;
+  for (int r = 0; r < W && r < S3_MAX_RANKS; ++r) {
+    const int64_t* row = m.data() + (size_t)r * S3_NCOUNTERS;
+    c->rank_free_rows[r] = row[0];
+    c->rank_running[r] = row[1];
+    c->free_rows_total += row[0];
+    c->running_total += row[1];
+    c->evicted_waiting_total += row[3];
+    c->finished_total += row[5];
+    c->evicted_total += row[6];
+    c->tokens_total += row[7];
+  }
+  c->fresh_waiting = m[4];   // the shared pool is replicated on every rank
   return S3_OK;
 }
 

@@ -53,6 +53,7 @@ class S3Engine:
         # FFD) also at world 1 when asked: with one bin it admits exactly what s3_admit does,
         # and it puts the caller's process-group exchange (NCCL) on the step's path
         self.split_admit = world > 1 or exchange_admission
+        self.native_comm = False        # counters all-reduced by libs3's own NCCL communicator
         self.stream = torch.cuda.current_stream(self.device)
         self.cfg = abi.s3_config(
             num_layers=num_layers, num_heads=num_heads, head_dim=head_dim, max_seq_len=max_seq_len,
@@ -161,14 +162,36 @@ class S3Engine:
             return abi.s3_admit(self.ctx, self.max_running)
         raise RuntimeError("world > 1: use admit_home / exchange / admit_shared")
 
+    # ---- (a8) the counter exchange over libs3's NCCL communicator ------------------
+    def comm_init(self, uid: bytes):
+        """Bind the library-owned NCCL communicator (collective over the ranks; uid from
+        abi.s3_nccl_get_unique_id on rank 0, broadcast by the caller)."""
+        abi.s3_comm_init(self.ctx, uid)
+        self.native_comm = True
+
+    def exchange_counters(self) -> np.ndarray:
+        mat = np.zeros((self.world, abi.S3_NCOUNTERS), np.int64)
+        abi.s3_exchange_counters(self.ctx, mat)
+        return mat
+
+    def counters_get(self):
+        return abi.s3_counters_get(self.ctx)
+
+    def _exchange(self, exchange):
+        if exchange is None:           # libs3's communicator (comm_init) does the all-reduce
+            if not self.native_comm:
+                raise RuntimeError("world > 1: pass an exchange callable or call comm_init first")
+            return self.exchange_counters()
+        return exchange(self.counters_local())
+
     def admit_step(self, exchange=None):
-        """The step's admission: s3_admit (world 1), or s3_admit_home, the caller's
-        all-reduce of the counter rows (`exchange`), s3_admit_shared.  Returns the
-        admission reports."""
+        """The step's admission: s3_admit (world 1), or s3_admit_home, the all-reduce of the
+        counter rows (the caller's `exchange`, or with none libs3's communicator after
+        comm_init), s3_admit_shared.  Returns the admission reports."""
         if not self.split_admit:
             return [self.admit()[0]]
         hrep, _ = self.admit_home()
-        srep, _ = self.admit_shared(exchange(self.counters_local()))
+        srep, _ = self.admit_shared(self._exchange(exchange))
         return [hrep, srep]
 
     def admit_home(self):
@@ -216,7 +239,7 @@ class S3Engine:
         if not self.split_admit:
             return self.admit()
         self.admit_home()
-        return self.admit_shared(exchange(self.counters_local()))
+        return self.admit_shared(self._exchange(exchange))
 
     def arena_rows_view(self) -> torch.Tensor:
         """The arena as bf16 [R][L][2][H][D] (a view, no copy)."""

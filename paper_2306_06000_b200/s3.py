@@ -15,10 +15,12 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "lib", "libs3.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "s3.h")
 
-S3_OK, S3_E_INVAL, S3_E_NOMEM, S3_E_CUDA, S3_E_STATE, S3_E_UNSCHEDULABLE = 0, 1, 2, 3, 5, 6
+S3_OK, S3_E_INVAL, S3_E_NOMEM, S3_E_CUDA, S3_E_NCCL, S3_E_STATE, S3_E_UNSCHEDULABLE = 0, 1, 2, 3, 4, 5, 6
 S3_RUNNING, S3_FINISHED, S3_OVERRUN = 0, 1, 2
 S3_NCOUNTERS = 8
-_NAMES = {0: "S3_OK", 1: "S3_E_INVAL", 2: "S3_E_NOMEM", 3: "S3_E_CUDA", 5: "S3_E_STATE",
+S3_NCCL_ID_BYTES = 128
+S3_MAX_RANKS = 64
+_NAMES = {0: "S3_OK", 1: "S3_E_INVAL", 2: "S3_E_NOMEM", 3: "S3_E_CUDA", 4: "S3_E_NCCL", 5: "S3_E_STATE",
           6: "S3_E_UNSCHEDULABLE"}
 
 
@@ -67,6 +69,14 @@ class s3_admit_report(C.Structure):
                 ("h2d_bytes", C.c_int64), ("moved_bytes", C.c_int64), ("stage_reload_bytes", C.c_int64)]
 
 
+class s3_counters(C.Structure):
+    _fields_ = [("world", C.c_int32), ("exchanges", C.c_int32),
+                ("rank_free_rows", C.c_int64 * S3_MAX_RANKS), ("rank_running", C.c_int64 * S3_MAX_RANKS),
+                ("free_rows_total", C.c_int64), ("running_total", C.c_int64), ("evicted_waiting_total", C.c_int64),
+                ("fresh_waiting", C.c_int64), ("finished_total", C.c_int64), ("evicted_total", C.c_int64),
+                ("tokens_total", C.c_int64)]
+
+
 class s3_slot(C.Structure):
     _fields_ = [("req_id", C.c_int64), ("prompt_len", C.c_int32), ("gen_len", C.c_int32),
                 ("len", C.c_int32), ("cap_rows", C.c_int32), ("off", C.c_int64)]
@@ -110,6 +120,10 @@ _SIGS = {
     "s3_admit_home": (C.c_int, [P, P, P]),
     "s3_admit_shared": (C.c_int, [P, P, P, P]),
     "s3_counters_local": (C.c_int, [P, P]),
+    "s3_nccl_get_unique_id": (C.c_int, [P]),
+    "s3_comm_init": (C.c_int, [P, P]),
+    "s3_exchange_counters": (C.c_int, [P, P]),
+    "s3_counters_get": (C.c_int, [P, P]),
     "s3_plan_ffd": (_i32, [_i32, P, P, _i64, _i32, P]),
     "s3_plan_ffd_multibin": (_i32, [_i32, P, P, _i32, P, P, P]),
     "s3_batch_size": (C.c_int, [P, P]),
@@ -240,6 +254,29 @@ def s3_admit_shared(ctx, max_running: int, counters_all):
 def s3_counters_local(ctx, row):
     """row: int64 numpy array [S3_NCOUNTERS]."""
     _check(lib().s3_counters_local(ctx, _ptr(row)), "s3_counters_local", ctx)
+
+
+def s3_nccl_get_unique_id() -> bytes:
+    buf = (C.c_uint8 * S3_NCCL_ID_BYTES)()
+    _check(lib().s3_nccl_get_unique_id(C.cast(buf, P)), "s3_nccl_get_unique_id", None)
+    return bytes(buf)
+
+
+def s3_comm_init(ctx, uid: bytes):
+    assert len(uid) == S3_NCCL_ID_BYTES
+    buf = (C.c_uint8 * S3_NCCL_ID_BYTES).from_buffer_copy(uid)
+    _check(lib().s3_comm_init(ctx, C.cast(buf, P)), "s3_comm_init", ctx)
+
+
+def s3_exchange_counters(ctx, counters_all):
+    """counters_all: int64 numpy array [world, S3_NCOUNTERS] (contiguous), overwritten."""
+    _check(lib().s3_exchange_counters(ctx, _ptr(counters_all)), "s3_exchange_counters", ctx)
+
+
+def s3_counters_get(ctx) -> s3_counters:
+    c = s3_counters()
+    _check(lib().s3_counters_get(ctx, C.byref(c)), "s3_counters_get", ctx)
+    return c
 
 
 def s3_plan_ffd(cap, req, free_rows, max_items, admitted):

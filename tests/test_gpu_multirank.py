@@ -143,9 +143,12 @@ def test_bench_torchrun_two_ranks_gloo():
 
 def test_bench_nccl_exchange_world1():
     """The N > 1 exchange on the one GPU this pool has: --dist-always creates an NCCL
-    process group of one rank and runs every step's counter all-reduce (its own stream,
-    reserve_sms left free by the attention grid) through the multi-rank admission path
-    (s3_admit_home -> all-reduce -> s3_admit_shared).  With one bin the shared multi-bin
+    process group of one rank, every engine binds libs3's own NCCL communicator
+    (s3_nccl_get_unique_id on rank 0, broadcast, s3_comm_init), and every step's counter
+    all-reduce (s3_exchange_counters: its own stream, reserve_sms left free by the
+    attention grid) runs through the multi-rank admission path (s3_admit_home ->
+    all-reduce -> s3_admit_shared); a second run uses torch.distributed's all_reduce
+    (--exchange torch).  With one bin the shared multi-bin
     FFD admits exactly what s3_admit does, so the schedule -- tokens in the window and
     over the whole run -- equals the plain world-1 run's."""
     if not torch.cuda.is_available():
@@ -154,8 +157,10 @@ def test_bench_nccl_exchange_world1():
             "--arena-gb", "12", "--requests", "1500", "--no-cpu-baseline"]
     port = _free_port()
     runs = {}
-    for name, cmd in (("nccl", [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
-                                "--master-addr", "127.0.0.1", "--master-port", str(port), *base, "--dist-always"]),
+    tr = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+          "--master-addr", "127.0.0.1"]
+    for name, cmd in (("nccl", [*tr, "--master-port", str(port), *base, "--dist-always"]),
+                      ("torch", [*tr, "--master-port", str(_free_port()), *base, "--dist-always", "--exchange", "torch"]),
                       ("plain", [sys.executable, *base])):
         out = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
         assert out.returncode == 0, out.stderr[-3000:]
@@ -163,8 +168,10 @@ def test_bench_nccl_exchange_world1():
         assert len(lines) == 1
         runs[name] = json.loads(lines[0])
     x = runs["nccl"]["exchange"]
-    assert x["backend"] == "nccl" and x["world"] == 1 and x["exchanges"] >= 13
+    assert x["backend"].startswith("nccl (libs3 communicator") and x["world"] == 1 and x["exchanges"] >= 13
     assert runs["plain"]["exchange"] is None
-    assert runs["nccl"]["tokens"] == runs["plain"]["tokens"]
-    assert runs["nccl"]["wholerun"]["tokens"] == runs["plain"]["wholerun"]["tokens"]
-    assert runs["nccl"]["wholerun"]["steps"] == runs["plain"]["wholerun"]["steps"]
+    assert runs["torch"]["exchange"]["backend"].startswith("nccl (torch.distributed")
+    for name in ("nccl", "torch"):
+        assert runs[name]["tokens"] == runs["plain"]["tokens"]
+        assert runs[name]["wholerun"]["tokens"] == runs["plain"]["wholerun"]["tokens"]
+        assert runs[name]["wholerun"]["steps"] == runs["plain"]["wholerun"]["steps"]
