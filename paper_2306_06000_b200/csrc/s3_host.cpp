@@ -17,6 +17,7 @@
 #include <map>
 #include <memory>
 #include <new>
+#include <unordered_map>
 #include <unordered_set>
 #include <vector>
 
@@ -182,6 +183,7 @@ struct s3_ctx {
   Pool pool;        // world == 1: everything; world > 1: the shared fresh pool
   Pool home;        // world > 1: this rank's evicted requests
   std::unordered_set<int64_t> live;   // req ids queued, running or evicted (not yet finished)
+  std::unordered_map<int64_t, std::shared_ptr<EventBox>> evict_done;   // req -> its eviction D2H's completion
   int64_t n_evicted_waiting = 0;
   // host store allocator (first fit) + deferred frees
   std::map<int64_t, int64_t> free_blocks;
@@ -1006,6 +1008,7 @@ s3_status s3_evict_compact(s3_ctx* ctx, s3_evict_report* rep, int32_t* perm, s3_
     ctx->prof.fused_move_bytes += (double)h->moved_bytes + (double)h->d2h_bytes;
   }
   std::shared_ptr<EventBox> d2h_done;
+  std::vector<std::shared_ptr<EventBox>> per_ev;   // staged path: one completion event per evictee
   if (h->n_evicted > 0) {
     d2h_done = std::make_shared<EventBox>();
     if (!staged) {
@@ -1060,6 +1063,7 @@ s3_status s3_evict_compact(s3_ctx* ctx, s3_evict_report* rep, int32_t* perm, s3_
       CK(cudaStreamWaitEvent(ctx->side, ctx->ev_report, 0), "side wait");
     }
     const int nwc = attn_block_threads(sh) / 32;    // CUDA-core kernel: consumer warps that append the new row
+    per_ev.resize(h->n_evicted);
     for (int32_t i = 0; i < h->n_evicted; ++i) {
       if (counted) {
         // rows each kernel counts for this evictee over the step's L layers
@@ -1078,6 +1082,8 @@ s3_status s3_evict_compact(s3_ctx* ctx, s3_evict_report* rep, int32_t* perm, s3_
         cudaEventRecord(e1, ctx->side);
         ctx->prof.pending.push_back({e0, e1, (double)dev[i].len * sh.kvpt, 2});
       }
+      per_ev[i] = std::make_shared<EventBox>();   // this evictee's host copy (s3_evict_wait_req, reload gate)
+      CK(cudaEventRecord(per_ev[i]->ev, ctx->side), "event");
     }
     CK(cudaEventRecord(d2h_done->ev, ctx->side), "event");
     ctx->stage_d2h[ctx->stage_cur] = d2h_done;
@@ -1094,7 +1100,8 @@ s3_status s3_evict_compact(s3_ctx* ctx, s3_evict_report* rep, int32_t* perm, s3_
     it.host_off = hoff[i];
     it.host_bytes = (int64_t)e.len * sh.kvpt;
     it.host_rows = e.len;
-    it.ready = d2h_done;
+    it.ready = (size_t)i < per_ev.size() ? per_ev[i] : d2h_done;
+    ctx->evict_done[e.req] = it.ready;
     if (staged) { it.stage_src = stage + e.stage_off; it.evict_seq = ctx->evict_seq; }
     pcie += 2LL * e.cap * sh.kvpt;
     (ctx->cfg.world > 1 ? ctx->home : ctx->pool).emplace(Key{it.cap, it.req}, it);
@@ -1151,6 +1158,16 @@ s3_status s3_evict_wait(s3_ctx* ctx) {
   CK(cudaStreamSynchronize(ctx->side), "side sync");
   CK(cudaStreamSynchronize(ctx->st), "sync");
   flush_deferred(ctx);
+  ctx->evict_done.clear();
+  return S3_OK;
+}
+
+s3_status s3_evict_wait_req(s3_ctx* ctx, int64_t req_id) {
+  if (s3_status s = check_ctx(ctx)) return s;
+  auto it = ctx->evict_done.find(req_id);
+  if (it == ctx->evict_done.end()) return S3_OK;   // no host copy pending for this request
+  CK(cudaEventSynchronize(it->second->ev), "evict wait");
+  ctx->evict_done.erase(it);
   return S3_OK;
 }
 

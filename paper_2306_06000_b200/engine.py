@@ -213,6 +213,9 @@ class S3Engine:
     def evict_wait(self):
         abi.s3_evict_wait(self.ctx)
 
+    def evict_wait_req(self, req_id: int):
+        abi.s3_evict_wait_req(self.ctx, req_id)
+
     def profile(self, on: bool):
         abi.s3_profile_enable(self.ctx, on)
 

@@ -120,6 +120,7 @@ _SIGS = {
     "s3_admit_home": (C.c_int, [P, P, P]),
     "s3_admit_shared": (C.c_int, [P, P, P, P]),
     "s3_counters_local": (C.c_int, [P, P]),
+    "s3_evict_wait_req": (C.c_int, [P, _i64]),
     "s3_nccl_get_unique_id": (C.c_int, [P]),
     "s3_comm_init": (C.c_int, [P, P]),
     "s3_exchange_counters": (C.c_int, [P, P]),
@@ -229,6 +230,10 @@ def s3_evict_compact(ctx, n_before: int):
 
 def s3_evict_wait(ctx):
     _check(lib().s3_evict_wait(ctx), "s3_evict_wait", ctx)
+
+
+def s3_evict_wait_req(ctx, req_id: int):
+    _check(lib().s3_evict_wait_req(ctx, int(req_id)), "s3_evict_wait_req", ctx)
 
 
 def _admit(fn, name, ctx, cap, *args):

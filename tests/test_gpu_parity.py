@@ -137,8 +137,8 @@ def lockstep(trace, L, H, D, R, C=0, S=0, max_running=4096, staging=True, feed_o
         assert [(e.req_id, e.batch_index, e.prompt_len, e.gen_len, e.len, e.cap_rows, e.new_cap_rows)
                 for e in ev_g] == [tuple(e) for e in ev_o]
         if ev_g:
-            eng.evict_wait()
-            for e in ev_g:
+            for e in ev_g:                      # per-request wait (each evictee's own D2H event)
+                eng.evict_wait_req(e.req_id)
                 host_g = u16(eng.host_rows(e.host_off, e.len).reshape(-1))
                 assert np.array_equal(host_g, orc.host_kv(e.req_id).reshape(-1))
         stats["evictions"] += rep_o.n_evicted
