@@ -420,9 +420,18 @@ class Ctx:
         if self.native:
             # a fresh communicator per engine: rank 0's id broadcast over the process group
             from paper_2306_06000_b200 import s3 as abi
-            obj = [abi.s3_nccl_get_unique_id() if self.rank == 0 else None]
+            try:
+                uid = abi.s3_nccl_get_unique_id() if self.rank == 0 else None
+            except abi.S3Error as e:                  # libnccl.so.2 not loadable: torch's all-reduce
+                print(f"[bench] libs3 NCCL communicator unavailable ({e}); using torch.distributed",
+                      file=sys.stderr)
+                uid = b""
+            obj = [uid]
             self.dist.broadcast_object_list(obj, src=0)
-            eng.comm_init(obj[0])
+            if obj[0]:
+                eng.comm_init(obj[0])
+            else:
+                self.native = False
         self.engine = eng
         return eng, trace, R, kvpt
 
