@@ -209,7 +209,8 @@ s3_status s3_evict_compact(s3_ctx* ctx, s3_evict_report* rep, int32_t* perm, s3_
 s3_status s3_evict_wait(s3_ctx* ctx);
 /* Blocks until the host copy of request req_id's last eviction is complete
  * (each evictee's D2H records its own event on the side stream); S3_OK at
- * once when no copy of req_id is pending.  SURVEY §8(b)'s s3_evict_wait(req).  */
+ * once when no copy of req_id is pending (never evicted, already waited for,
+ * or re-admitted since).  SURVEY §8(b)'s s3_evict_wait(req).               */
 s3_status s3_evict_wait_req(s3_ctx* ctx, int64_t req_id);
 
 /* ---- (e): admission by first-fit decreasing --------------------------- */

@@ -417,6 +417,7 @@ s3_status place_items(s3_ctx* ctx, const std::vector<Item>& items, s3_admit_repo
       if (it.evicted) {
         s.gen = it.gen;
         s.len = it.host_rows;
+        ctx->evict_done.erase(it.req);   // re-admitted: its host copy is no longer waited for
         uint8_t* dst = (uint8_t*)ctx->buf.arena + (int64_t)s.off * ctx->sh.kvpt;
         if (it.stage_src && it.evict_seq == ctx->evict_seq) {
           // re-admitted in the step that evicted it (R10): its rows are still in the
