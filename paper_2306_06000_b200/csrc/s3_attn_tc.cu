@@ -23,9 +23,10 @@
 //                   pair and one softmax pass serve np heads;
 //   MMA warp      : one thread issues tcgen05.mma (kind::f16, M 128, K 16 per
 //                   instruction) and routes tile t to softmax group iseq & 1;
-//   softmax warps : two groups of 4 warps ("ping-pong", warps 2-5 and 7-10),
-//                   each owning alternate items with its own S slots, P
-//                   buffer and O buffer in TMEM; 4 warps = 128 TMEM lanes,
+//   softmax warps : two groups ("ping-pong"), each owning alternate items with
+//                   its own S slots, P buffer and O buffer in TMEM; a group is
+//                   4 warps per 8 query columns (NC = 16: two quads, one per
+//                   column half, never synchronising); 4 warps = 128 TMEM lanes,
 //                   lane j holds row j of S^T: mask rows >= nvalid, column
 //                   max / sum across the 128 lanes, online softmax in the log2
 //                   domain, P (bf16 hi / lo, swizzled) to shared memory, zero V
@@ -124,7 +125,15 @@ constexpr int TMEM_COLS = 256;
 __host__ __device__ constexpr uint32_t scol(int g, int b) { return (uint32_t)((2 * g + b) * 16); }
 __host__ __device__ constexpr uint32_t ocol(int g) { return 32u * NG_MAX + 32u * (uint32_t)g; }
 // warps: producer, MMA, 4 softmax (group 0), storer, then 4 softmax per further group
-__host__ __device__ constexpr int tc_threads(int nc) { return 32 * (3 + 4 * tc_groups(nc)); }
+// A softmax group is 4 warps per 8 query columns: NC = 16 groups have two column halves
+// (8 warps), each half running the 8-column chain on its own columns with its own named
+// barrier -- softmax columns are independent (column max / sum), so the halves never
+// synchronise -- which keeps the per-tile chain of the NC = 16 kernels (16 / G KV heads per
+// short tile) at the 8-column latency.  Warps: producer, MMA, group 0 half 0, storer,
+// group 1 half 0, then group 0 half 1, group 1 half 1.
+__host__ __device__ constexpr int tc_halves(int nc) { return nc / 8; }
+__host__ __device__ constexpr int tc_threads(int nc) { return 32 * (3 + 4 * tc_groups(nc) * tc_halves(nc)); }
+constexpr int CW = 8;                       // query columns per softmax warp
 
 struct TcHdr {
   int32_t item, r0, nvalid, flags;          // flags: 1 = first tile of the item, 2 = last;
@@ -147,8 +156,8 @@ struct alignas(16) TcSmem {                 // after the ring and the two P buff
   uint64_t s_full[NG_MAX][2], s_empty[NG_MAX][2];   // [group][S slot]; s_full: MMA commit + the MMA thread's arrive
   uint64_t p_full[NG_MAX], o_done[NG_MAX], o_fin[NG_MAX], o_free[NG_MAX];   // [group] (= O buffer)
   alignas(16) TcHdr hdr[NV_MAX];            // tile t at hdr[t % nv]; hdr.dep is a 16-B bulk-copy destination
-  float red[NG_MAX][2][4][NQ];              // [group][max / sum][warp][column]
-  int32_t flag[NG_MAX][4];
+  float red[2 * NG_MAX][2][4][CW];          // [group + NG half][max / sum][warp][column]
+  int32_t flag[2 * NG_MAX][4];
   int32_t gt[NG_MAX][2];                    // ring tile index in group g's S slot b (-1: no more tiles)
   uint32_t tmem_base;
 };
@@ -234,17 +243,6 @@ __device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t
 __device__ __forceinline__ void commit(uint64_t* b) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.b64 [%0];" ::"l"((uint64_t)su32(b)) : "memory");
 }
-__device__ __forceinline__ void tmem_ld16(uint32_t addr, float (&v)[NQ]) {
-  uint32_t r[16];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(addr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-}
 __device__ __forceinline__ void tmem_ld8(uint32_t addr, float (&v)[8]) {
   uint32_t r[8];
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -262,34 +260,13 @@ __device__ __forceinline__ void tmem_st8(uint32_t addr, const float (&v)[8]) {
                : "memory");
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
-__device__ __forceinline__ void tmem_st16(uint32_t addr, const float (&v)[NQ]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
-          addr),
-      "r"(__float_as_uint(v[0])), "r"(__float_as_uint(v[1])), "r"(__float_as_uint(v[2])),
-      "r"(__float_as_uint(v[3])), "r"(__float_as_uint(v[4])), "r"(__float_as_uint(v[5])),
-      "r"(__float_as_uint(v[6])), "r"(__float_as_uint(v[7])), "r"(__float_as_uint(v[8])),
-      "r"(__float_as_uint(v[9])), "r"(__float_as_uint(v[10])), "r"(__float_as_uint(v[11])),
-      "r"(__float_as_uint(v[12])), "r"(__float_as_uint(v[13])), "r"(__float_as_uint(v[14])),
-      "r"(__float_as_uint(v[15]))
-      : "memory");
-  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-}
-template <int NC>
-__device__ __forceinline__ void tmem_ld(uint32_t addr, float (&v)[NC]) {
-  if constexpr (NC == 16) tmem_ld16(addr, v); else tmem_ld8(addr, v);
-}
-template <int NC>
-__device__ __forceinline__ void tmem_st(uint32_t addr, const float (&v)[NC]) {
-  if constexpr (NC == 16) tmem_st16(addr, v); else tmem_st8(addr, v);
-}
 __device__ __forceinline__ float ex2f(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// named barrier of one softmax group (4 warps); ids 1, 2
-__device__ __forceinline__ void softmax_bar(int grp) { asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory"); }
+// named barrier of one softmax group's column half (4 warps); ids 1..4
+__device__ __forceinline__ void softmax_bar(int bq) { asm volatile("bar.sync %0, 128;" ::"r"(1 + bq) : "memory"); }
 
 // Column-wise reduction of 16 values per lane over the 128 softmax lanes.
 // Within a warp a transposed butterfly halves the vector at each step (8 + 4
@@ -299,7 +276,8 @@ template <bool MAX>
 __device__ __forceinline__ float rop(float x, float y) { return MAX ? fmaxf(x, y) : x + y; }
 
 template <bool MAX, int NC>
-__device__ __forceinline__ void col_reduce(float (&v)[NC], float (&red)[4][NQ], int wq, int lane, int grp) {
+__device__ __forceinline__ void col_reduce(float (&v)[NC], float (&red)[4][CW], int wq, int lane, int grp) {
+  static_assert(NC <= CW, "one warp reduces at most CW columns");
   // NC = 16: 8 + 4 + 2 + 1 + 1 shuffles; NC = 8: 4 + 2 + 1 + 1 + 1
   float a8[8], a4[4], a2[2], a1;
   const bool h16 = lane & 16, h8 = lane & 8, h4 = lane & 4, h2 = lane & 2;
@@ -434,11 +412,11 @@ __global__ void __launch_bounds__(tc_threads(NC), 1) k_attn_tc(const __grid_cons
     for (int i = 0; i < nk; ++i) { mb_init(&S.kfull[i], 1); mb_init(&S.kempty[i], fused ? 2 : 1); }
     for (int i = 0; i < nv; ++i) { mb_init(&S.vfull[i], 1); mb_init(&S.vempty[i], fused ? 2 : 1); }
     for (int g = 0; g < NG; ++g) {
-      for (int b = 0; b < 2; ++b) { mb_init(&S.s_full[g][b], 2); mb_init(&S.s_empty[g][b], 4); }
-      mb_init(&S.p_full[g], 4);
+      for (int b = 0; b < 2; ++b) { mb_init(&S.s_full[g][b], 2); mb_init(&S.s_empty[g][b], 4 * tc_halves(NC)); }
+      mb_init(&S.p_full[g], 4 * tc_halves(NC));
       mb_init(&S.o_done[g], 1);
       mb_init(&S.o_fin[g], 1);
-      mb_init(&S.o_free[g], 4);
+      mb_init(&S.o_free[g], 4 * tc_halves(NC));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -803,34 +781,40 @@ __global__ void __launch_bounds__(tc_threads(NC), 1) k_attn_tc(const __grid_cons
     }
   } else {
     // ------------------------------ softmax -------------------------------
-    // Two groups of 4 warps (warps 2-5: group 0, warps 7-10: group 1); group
-    // g takes the tiles of items with iseq & 1 == g, in order, so the two
+    // Two groups (warps 2-5 + 11-14: group 0, warps 7-10 + 15-18: group 1; the
+    // second quad of each exists for NC = 16 and takes columns 8-15); group g
+    // takes the tiles of items with iseq & 1 == g, in order, so the two
     // groups' per-tile chains (TMEM load, reductions, P, hand-over,
     // epilogue) overlap.  Lazy running max (log2 domain): the column max is
     // reduced across the 128 lanes only on an item's first tile or when some
     // score exceeds the running max by more than LAZY_THR; otherwise
     // p = 2^(s - m) <= 2^8 and nothing is rescaled.  Each lane keeps its own
     // row's partial sums; they are reduced once, in the epilogue.
-    const int grp = warp < 6 ? 0 : 1 + (warp - 7) / 4;
-    const int wq = warp < 6 ? warp - 2 : (warp - 7) % 4;   // 0..3 within the group
+    constexpr int HV = tc_halves(NC);
+    const int sidx = warp < 6 ? warp - 2 : warp - 3;  // 0..3 g0 h0, 4..7 g1 h0, 8..11 g0 h1, 12..15 g1 h1
+    const int grp = (sidx >> 2) & 1;
+    const int hf = sidx >> 3;                         // column half: columns [CW hf, CW hf + CW)
+    const int bq = grp + 2 * hf;                      // this quad's barrier / reduction slot
+    const int co = CW * hf;
+    const int wq = sidx & 3;                          // 0..3 within the quad
     const int lq = warp & 3;                          // TMEM lane quarter this warp may access
     const int row = lq * 32 + lane;                   // TMEM lane = tile row (S) = head-dim index (O)
     const uint32_t lane_base = tmem + ((uint32_t)(lq * 32) << 16);
     const uint32_t oc = ocol(grp);                    // this group's O buffer
     uint8_t* const pgrp = pbuf + grp * PBUF;          // this group's P buffer
-    float m[NC], lrow[NC];
+    float m[CW], lrow[CW];
 #pragma unroll
-    for (int c = 0; c < NC; ++c) { m[c] = -INFINITY; lrow[c] = 0.f; }
+    for (int c = 0; c < CW; ++c) { m[c] = -INFINITY; lrow[c] = 0.f; }
     for (int k = 0;; ++k) {
       const int sb = k & 1;
       mb_wait(&S.s_full[grp][sb], (uint32_t)(k >> 1) & 1u);
       const int t = S.gt[grp][sb];
       if (t < 0) break;
-      if (lane == 0 && wq == 0) TC_TRACE_AT(t, 6);
+      if (lane == 0 && sidx == 0) TC_TRACE_AT(t, 6);
       const TcHdr h = S.hdr[t % nv];
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      float s[NC];
-      tmem_ld<NC>(lane_base + scol(grp, sb), s);
+      float s[CW];
+      tmem_ld8(lane_base + scol(grp, sb) + co, s);
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mb_arrive(&S.s_empty[grp][sb]);
@@ -841,7 +825,7 @@ __global__ void __launch_bounds__(tc_threads(NC), 1) k_attn_tc(const __grid_cons
         valid = row < h.nvalid;
         loaded = row < ((h.nvalid + 15) & ~15);
 #pragma unroll
-        for (int c = 0; c < NC; ++c) s[c] = valid ? s[c] * a.qscale : -INFINITY;
+        for (int c = 0; c < CW; ++c) s[c] = valid ? s[c] * a.qscale : -INFINITY;
       } else {
         // block-diagonal mask of packed tiles: segment sgm only meets columns
         // [sgm G, (sgm+1) G); columns past np G stay unmasked (finite, never written out);
@@ -851,9 +835,9 @@ __global__ void __launch_bounds__(tc_threads(NC), 1) k_attn_tc(const __grid_cons
         const int rs = row - sgm * seg;
         loaded = sgm < np;
         valid = loaded && rs < h.nvalid;
-        const int cg0 = sgm * a.G, cg1 = cg0 + a.G, cpad = a.G * np;
+        const int cg0 = sgm * a.G - co, cg1 = cg0 + a.G, cpad = a.G * np - co;   // in this half's columns
 #pragma unroll
-        for (int c = 0; c < NC; ++c)
+        for (int c = 0; c < CW; ++c)
           s[c] = (valid && ((c >= cg0 && c < cg1) || c >= cpad)) ? s[c] * a.qscale : -INFINITY;
       }
       // does any score need a larger running max?
@@ -861,22 +845,22 @@ __global__ void __launch_bounds__(tc_threads(NC), 1) k_attn_tc(const __grid_cons
       if (!first) {
         bool over = false;
 #pragma unroll
-        for (int c = 0; c < NC; ++c) over |= s[c] > m[c] + LAZY_THR;
+        for (int c = 0; c < CW; ++c) over |= s[c] > m[c] + LAZY_THR;
         const bool wover = __any_sync(0xffffffffu, over);
-        if (lane == 0) S.flag[grp][wq] = wover;
-        softmax_bar(grp);
-        need = S.flag[grp][0] | S.flag[grp][1] | S.flag[grp][2] | S.flag[grp][3];
-        softmax_bar(grp);
+        if (lane == 0) S.flag[bq][wq] = wover;
+        softmax_bar(bq);
+        need = S.flag[bq][0] | S.flag[bq][1] | S.flag[bq][2] | S.flag[bq][3];
+        softmax_bar(bq);
       }
-      float corr[NC];
+      float corr[CW];
       bool rescale = false;
       if (need) {
-        float mt[NC];
+        float mt[CW];
 #pragma unroll
-        for (int c = 0; c < NC; ++c) mt[c] = s[c];
-        col_reduce<true, NC>(mt, S.red[grp][0], wq, lane, grp);
+        for (int c = 0; c < CW; ++c) mt[c] = s[c];
+        col_reduce<true, CW>(mt, S.red[bq][0], wq, lane, bq);
 #pragma unroll
-        for (int c = 0; c < NC; ++c) {
+        for (int c = 0; c < CW; ++c) {
           const float mn = first ? mt[c] : fmaxf(m[c], mt[c]);
           corr[c] = first ? 0.f : ex2f(m[c] - mn);
           m[c] = mn;
@@ -890,63 +874,66 @@ __global__ void __launch_bounds__(tc_threads(NC), 1) k_attn_tc(const __grid_cons
         mb_wait(&S.o_done[grp], (uint32_t)(k - 1) & 1u);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       }
-      // P = 2^(s - m) as bf16 hi + lo; row c (query column), column j = row; 128B swizzle
+      // P = 2^(s - m) as bf16 hi + lo; row co + c (query column), column j = row; 128B swizzle
       uint8_t* sp = pgrp + (row >> 6) * PBLK;
       const uint32_t jj2 = (uint32_t)(row & 63) * 2u;
 #pragma unroll
-      for (int c = 0; c < NC; ++c) {
+      for (int c = 0; c < CW; ++c) {
         const float pv = ex2f(s[c] - m[c]);
         lrow[c] += pv;
         const __nv_bfloat16 hi = __float2bfloat16_rn(pv);
         const __nv_bfloat16 lo = __float2bfloat16_rn(pv - __bfloat162float(hi));
-        const uint32_t byte = (uint32_t)c * 128u + jj2;
-        const uint32_t sw = byte ^ ((uint32_t)(c & 7) << 4);
+        const uint32_t byte = (uint32_t)(co + c) * 128u + jj2;
+        const uint32_t sw = byte ^ ((uint32_t)(c & 7) << 4);          // (co + c) & 7 == c
         *reinterpret_cast<__nv_bfloat16*>(sp + sw) = hi;
-        *reinterpret_cast<__nv_bfloat16*>(sp + NC * 128 + sw) = lo;   // row NC + c: same swizzle phase
+        *reinterpret_cast<__nv_bfloat16*>(sp + NC * 128 + sw) = lo;   // row NC + co + c: same swizzle phase
       }
       if (!valid && loaded) {                         // loaded rows past the slot's resident rows: V := 0
         mb_wait(&S.vfull[t % nv], (uint32_t)(t / nv) & 1u);   // after the V load has landed
         uint8_t* sv = vslot(smem, t, nk, nv);
 #pragma unroll
-        for (int kb = 0; kb < 2; ++kb)
+        for (int kb = 0; kb < 2; ++kb) {
+          if (HV == 2 && kb != hf) continue;          // the two halves zero one 64-column block each
 #pragma unroll
           for (int ch = 0; ch < 8; ++ch)
             *reinterpret_cast<uint4*>(sv + (row >> 3) * 2048 + kb * 1024 + (row & 7) * 128 + ch * 16) =
                 make_uint4(0, 0, 0, 0);
+        }
       }
       if (rescale) {                                // O^T *= corr (this item's previous tile is done)
-        float o[NC], olo[NC];
-        tmem_ld<NC>(lane_base + oc, o);
-        tmem_ld<NC>(lane_base + oc + NC, olo);
+        float o[CW], olo[CW];
+        tmem_ld8(lane_base + oc + co, o);
+        tmem_ld8(lane_base + oc + NC + co, olo);
 #pragma unroll
-        for (int c = 0; c < NC; ++c) { o[c] *= corr[c]; olo[c] *= corr[c]; }
-        tmem_st<NC>(lane_base + oc, o);
-        tmem_st<NC>(lane_base + oc + NC, olo);
+        for (int c = 0; c < CW; ++c) { o[c] *= corr[c]; olo[c] *= corr[c]; }
+        tmem_st8(lane_base + oc + co, o);
+        tmem_st8(lane_base + oc + NC + co, olo);
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
       if (lane == 0) mb_arrive(&S.p_full[grp]);
-      if (lane == 0 && wq == 0) TC_TRACE_AT(t, 7);
+      if (lane == 0 && sidx == 0) TC_TRACE_AT(t, 7);
       if (h.flags & 2) {
         // epilogue of the finished item: the other group keeps the tensor pipe busy meanwhile
-        float pl[NC];
+        float pl[CW];
 #pragma unroll
-        for (int c = 0; c < NC; ++c) pl[c] = lrow[c];
-        col_reduce<false, NC>(pl, S.red[grp][1], wq, lane, grp);
+        for (int c = 0; c < CW; ++c) pl[c] = lrow[c];
+        col_reduce<false, CW>(pl, S.red[bq][1], wq, lane, bq);
         mb_wait(&S.o_fin[grp], (uint32_t)(h.iseq / NG) & 1u);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        float o[NC], olo[NC];
-        tmem_ld<NC>(lane_base + oc, o);
-        tmem_ld<NC>(lane_base + oc + NC, olo);
+        float o[CW], olo[CW];
+        tmem_ld8(lane_base + oc + co, o);
+        tmem_ld8(lane_base + oc + NC + co, olo);
         asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
         __syncwarp();
         if (lane == 0) mb_arrive(&S.o_free[grp]);
         const int d = row;
+        const int ncol = PACK ? a.G * hdr_np(h) : a.G;
 #pragma unroll
-        for (int c = 0; c < NC; ++c) {
-          if (c >= (PACK ? a.G * hdr_np(h) : a.G)) break;
-          const int hq = h.g * a.G + c;             // packed heads: column c belongs to KV head g + c / G
+        for (int c = 0; c < CW; ++c) {
+          if (co + c >= ncol) break;
+          const int hq = h.g * a.G + co + c;        // packed heads: column c belongs to KV head g + c / G
           const float ov = o[c] + olo[c];
           if (h.part < 0) {
             a.out[((int64_t)(h.li * a.B + h.b) * a.H + hq) * DH + d] = ov / pl[c];
@@ -956,7 +943,7 @@ __global__ void __launch_bounds__(tc_threads(NC), 1) k_attn_tc(const __grid_cons
             if (d == 0) { pr[DH] = m[c]; pr[DH + 1] = pl[c]; }
           }
         }
-        if (lane == 0 && wq == 0) TC_TRACE_AT(t, 2);
+        if (lane == 0 && sidx == 0) TC_TRACE_AT(t, 2);
       }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1079,7 +1066,7 @@ cudaError_t launch_attn_tc(const Shape& sh, const uint16_t* q, const uint16_t* k
                            float* partials, const Unit* units, const Split* splits, const DepDesc* desc,
                            unsigned long long* progress, uint32_t epoch, int32_t* ctrl, int32_t B, int32_t l0,
                            int32_t nl, int32_t grid_attn, int32_t grid_combine, const Feed& feed, uint32_t* evdone,
-                           int32_t mean_rows, cudaStream_t st) {
+                           int32_t mean_rows, int32_t nc_pick, cudaStream_t st) {
   TcMaps maps;
   // staging rows (evicted slots' KV, token-major like the arena); without staging k_prep never fuses an eviction
   const int64_t stage_rows = staging ? staging_bytes / sh.kvpt : 0;
@@ -1105,20 +1092,20 @@ cudaError_t launch_attn_tc(const Shape& sh, const uint16_t* q, const uint16_t* k
   a.arena = reinterpret_cast<uint8_t*>(arena); a.staging = staging; a.kvpt = sh.kvpt;
   a.desc = desc; a.progress = progress; a.epoch = epoch;
   a.k_new = k_new; a.v_new = v_new; a.feed = feed; a.evdone = evdone;
-  // Per launch, from the step's mean resident rows per slot (+1 for the new row):
-  // * ring shape: 2 K + 4 V slots for short items (mostly one tile; <= 48 rows), else 3 + 3
-  //   (the fused row shift holds K slots on long, moving items); LLaMA-3-8B threshold sweep
-  //   32 / 48 / 64 / 96: 48 keeps both the short-context window and the whole run at their best;
-  // * softmax columns NC: 16 (G > 8, or G <= 8 with very short items, <= 28 rows: 16 / G KV
-  //   heads per tile instead of 8 / G, twice the rows per tile) else 8.  tools/attn_sweep.py,
-  //   LLaMA-3-8B shape: 25-row items 0.84 (NC 16) vs 0.70 (NC 8); 33 rows 0.83 both; longer: NC 8.
+  // Per launch, from the step's rows (s3_host.cpp):
+  // * ring shape: 2 K + 4 V slots for short items (mostly one tile; mean <= 48 rows), else
+  //   3 + 3 (the fused row shift holds K slots on long, moving items); LLaMA-3-8B threshold
+  //   sweep 32 / 48 / 64 / 96: 48 keeps both the short-context window and the whole run best;
+  // * softmax columns NC (nc_pick): 16 when G > 8, or when it needs fewer tiles than NC = 8
+  //   (16 / G instead of 8 / G KV heads per short tile).  tools/attn_sweep.py, LLaMA-3-8B
+  //   shape, NC 16 / NC 8: 25-row items 0.961 / 0.864, 33-row 0.943 / 0.837, 45-row 0.876 /
+  //   0.915 (same tile count), 400-row 0.945 / 0.972.
   static const int ring = [] { const char* e = getenv("S3_TC_RING"); return e ? atoi(e) : 0; }();   // A/B: 24 or 33
   static const int short_rows = [] { const char* e = getenv("S3_TC_SHORT_ROWS"); return e ? atoi(e) : 48; }();
-  static const int nc16_rows = [] { const char* e = getenv("S3_TC_NC16_ROWS"); return e ? atoi(e) : 28; }();
   const bool two_four = ring ? ring == 24 : mean_rows <= short_rows;
   static const int pack = [] { const char* e = getenv("S3_TC_PACK"); return e ? atoi(e) : 1; }();
   static const int nc_env = [] { const char* e = getenv("S3_TC_NC"); return e ? atoi(e) : 0; }();   // A/B: 8 or 16
-  const int nc = a.G > 8 ? 16 : nc_env ? (nc_env == 16 ? 16 : 8) : (pack && mean_rows <= nc16_rows ? 16 : 8);
+  const int nc = a.G > 8 ? 16 : nc_env ? (nc_env == 16 ? 16 : 8) : (pack && nc_pick == 16 ? 16 : 8);
   a.pmax = pack ? nc / a.G : 1;   // S3_TC_PACK=0: one KV head per tile (A/B)
   const dim3 grid(grid_attn), block(tc_threads(nc));
   const int smem = attn_tc_smem(nc);

@@ -786,20 +786,37 @@ s3_status s3_decode_step(s3_ctx* ctx, int32_t l0, int32_t nl, const void* q, con
     ctx->attn_epoch++;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (ctx->prof.on) { e0 = ctx->prof.get(); e1 = ctx->prof.get(); cudaEventRecord(e0, ctx->st); }
-    // the tensor-core kernel picks its ring shape and softmax width per launch from the
-    // step's mean rows per slot (see launch_attn_tc)
-    int32_t mean_rows = 0;
+    // the tensor-core kernel picks its ring shape per launch from the step's mean rows per
+    // slot, and its softmax width from the tile counts the two widths would give: NC = 16
+    // packs up to 16 / G KV heads of a short unit into one 128-row tile (8 / G with NC = 8)
+    // at ~4 % more per tile (tools/attn_sweep.py: equal-tile cases 0.876 / 0.915 at 45 rows,
+    // 0.929 / 0.952 at 105), so it is launched when it needs < 1 / 1.04 of NC = 8's tiles
+    int32_t mean_rows = 0, nc_pick = 8;
     if (ctx->cfg.attn_variant == 2 && B > 0) {
-      int64_t rows = 0;
-      for (const DSlot& sl : ctx->slots_h) rows += sl.len + 1;
+      const int G = ctx->sh.H / ctx->sh.Hkv, Hkv = ctx->sh.Hkv;
+      auto tiles = [&](int pmax, int r) -> int64_t {   // one (slot, layer): the kernel's packing rule
+        const int rg = (r + 7) & ~7;
+        if (pmax > 1 && 2 * rg <= 128) {
+          const int np = std::min(std::min(pmax, 128 / rg), Hkv);
+          return (Hkv + np - 1) / np;
+        }
+        return (int64_t)Hkv * ((r + 127) / 128);
+      };
+      int64_t rows = 0, t8 = 0, t16 = 0;
+      for (const DSlot& sl : ctx->slots_h) {
+        const int r = sl.len + 1;
+        rows += r;
+        if (G <= 8) { t8 += tiles(8 / G, r); t16 += tiles(16 / G, r); }
+      }
       mean_rows = (int32_t)std::min<int64_t>((rows + B - 1) / B, 1 << 30);
+      nc_pick = G > 8 || (double)t16 * 1.04 < (double)t8 ? 16 : 8;
     }
     if (ctx->cfg.attn_variant == 2)
       CK(launch_attn_tc(ctx->sh, (const uint16_t*)q, (const uint16_t*)k_new, (const uint16_t*)v_new,
                         (uint16_t*)ctx->buf.arena, ctx->cfg.arena_rows,
                         ctx->buf.staging ? stage_ptr(ctx, ctx->stage_cur) : nullptr, stage_bytes(ctx), out, ctx->partials,
                         ctx->units, ctx->splits, ctx->desc, ctx->progress, ctx->attn_epoch, ctx->ctrl, B, l0, nl,
-                        ctx->grid_attn, ctx->grid_combine, ctx->feed, ev_counters(ctx), mean_rows, ctx->st),
+                        ctx->grid_attn, ctx->grid_combine, ctx->feed, ev_counters(ctx), mean_rows, nc_pick, ctx->st),
          "k_attn_tc");
     else
       CK(launch_attn(ctx->sh, (const uint16_t*)q, (const uint16_t*)k_new, (const uint16_t*)v_new,

@@ -163,7 +163,7 @@ cudaError_t launch_attn_tc(const Shape& sh, const uint16_t* q, const uint16_t* k
                            float* partials, const Unit* units, const Split* splits, const DepDesc* desc,
                            unsigned long long* progress, uint32_t epoch, int32_t* ctrl, int32_t B, int32_t l0,
                            int32_t nl, int32_t grid_attn, int32_t grid_combine, const Feed& feed, uint32_t* evdone,
-                           int32_t mean_rows, cudaStream_t st);
+                           int32_t mean_rows, int32_t nc_pick, cudaStream_t st);
 cudaError_t launch_combine(const Shape& sh, const Split* splits, float* partials, float* out, int32_t* ctrl,
                            int32_t B, int32_t nl, int32_t grid, cudaStream_t st);
 
