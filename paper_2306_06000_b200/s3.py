@@ -12,7 +12,7 @@ import os
 import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libs3.so")
+LIB_PATH = os.environ.get("S3_LIB") or os.path.join(HERE, "lib", "libs3.so")   # S3_LIB: A/B builds
 HEADER = os.path.join(os.path.dirname(HERE), "include", "s3.h")
 
 S3_OK, S3_E_INVAL, S3_E_NOMEM, S3_E_CUDA, S3_E_NCCL, S3_E_STATE, S3_E_UNSCHEDULABLE = 0, 1, 2, 3, 4, 5, 6
