@@ -139,6 +139,7 @@ struct TcHdr {
   int32_t item, r0, nvalid, flags;          // flags: 1 = first tile of the item, 2 = last;
                                             // bits 8..12: np (KV heads packed in the tile),
                                             // bits 16..20: seg / 8 (rows per packed head's segment)
+                                            // bits 24..28: hoff + 1 (tail-packed items' full tiles)
   int32_t b, part, li, g;
   int32_t iseq, mode, drow;                 // iseq: per-CTA item sequence number (group / O buffer = iseq % NG)
   uint32_t prog;                            // read progress this tile completes (storer)
@@ -149,6 +150,8 @@ constexpr uint32_t TC_PROG_FULL = 0x80000000u;
 // KV heads g..g+np-1 share the tile, one segment of seg rows each (segment s at rows [s seg, (s+1) seg))
 __device__ __forceinline__ int hdr_np(const TcHdr& h) { return (h.flags >> 8) & 31; }
 __device__ __forceinline__ int hdr_seg(const TcHdr& h) { return ((h.flags >> 16) & 31) * 8; }
+// tail-packed items (below): a full tile of head g + hoff inside the item of heads g.. (-1: none)
+__device__ __forceinline__ int hdr_hoff(const TcHdr& h) { return ((h.flags >> 24) & 31) - 1; }
 constexpr int TC_HEAD_STRIDE = 1 << 16;      // progress = head * 2^16 + rows (unit rows < 2^16)
 
 struct alignas(16) TcSmem {                 // after the ring and the two P buffers (one per group)
@@ -518,52 +521,83 @@ __global__ void __launch_bounds__(tc_threads(NC), 1) k_attn_tc(const __grid_cons
         // nrows rounded up to 8 rows each, back to back (block-diagonal scores: segment s
         // only meets query columns [s G, (s+1) G)); the last tile of a unit-layer may hold
         // fewer heads (Hkv need not be a multiple of the packing)
-        int npk = 1, seg = TM;
+        int npk = 1, seg = TM, tl = 0;
+        bool tailpack = false;
         if constexpr (PACK) {
           const int rg = (nrows + 7) & ~7;
-          if (2 * rg <= TM) { npk = min(min(a.pmax, TM / rg), a.Hkv); seg = rg; }
+          if (2 * rg <= TM) {
+            npk = min(min(a.pmax, TM / rg), a.Hkv);
+            seg = rg;
+          } else {
+            // longer units: each head's rows past its last full 128-row tile (the tail) would
+            // be a tile of its own; tails of up to 64 rows are packed instead, np heads per
+            // tile, and those heads' full tiles come first in the same item (the item then
+            // spans the np heads' query columns: a full tile of head g + hoff only meets
+            // columns [hoff G, (hoff+1) G), the packed tail tile is block-diagonal)
+            tl = nrows % TM;
+            const int tg = (tl + 7) & ~7;
+            if (tl > 0 && 2 * tg <= TM && a.pmax > 1) {
+              npk = min(min(a.pmax, TM / tg), a.Hkv);
+              seg = tg;
+              tailpack = npk > 1;
+            }
+          }
         }
-        for (int g = 0; g < a.Hkv; g += npk, ++iseq) {
-          const int np = min(npk, a.Hkv - g);
-          const int item = w * a.Hkv + g;
-          const int qrow = (li * a.B + un.b) * a.H + g * a.G;
-          for (int r = 0; r < nrows; r += TM) {
-            const int ks = t % nk, vs = t % nv;
-            mb_wait(&S.kempty[ks], ((uint32_t)(t / nk) & 1u) ^ 1u);
-            mb_wait(&S.vempty[vs], ((uint32_t)(t / nv) & 1u) ^ 1u);
-            const int nrow = min(TM, nrows - r);
-            if (elect_one()) {
+        // one tile: segments np_t of seg_t rows for heads hd.., rows [r, r + nrow) of the unit
+        auto emit = [&](int g, int hd, int hoff, int np_t, int seg_t, int r, int nrow, bool first, bool last,
+                        uint32_t prog) {
+          const int ks = t % nk, vs = t % nv;
+          mb_wait(&S.kempty[ks], ((uint32_t)(t / nk) & 1u) ^ 1u);
+          mb_wait(&S.vempty[vs], ((uint32_t)(t / nv) & 1u) ^ 1u);
+          if (elect_one()) {
             TC_TRACE_AT(t, 0);
             TcHdr& h = S.hdr[vs];
-            h.item = item; h.r0 = un.r0 + r; h.nvalid = nrow;
-            h.flags = (r == 0 ? 1 : 0) | (r + TM >= nrows ? 2 : 0);
+            h.item = w * a.Hkv + g; h.r0 = un.r0 + r; h.nvalid = nrow;
+            h.flags = (first ? 1 : 0) | (last ? 2 : 0) | (np_t << 8) | ((seg_t >> 3) << 16) | ((hoff + 1) << 24);
             h.b = un.b; h.part = un.part; h.li = li; h.g = g; h.iseq = iseq;
             h.mode = un.mode; h.drow = drow0 + r;
             if (un.mode == UNIT_STAGE) h.dep.ua = un.pad;   // eviction index (dep is only loaded for MOVE)
-            h.flags |= (np << 8) | ((seg >> 3) << 16);
-            const int glast = g + np - 1;  // heads g..glast are read up to r + nrow rows once this tile lands
-            h.prog = (uint32_t)(glast * TC_HEAD_STRIDE + r + nrow) |
-                     (glast == a.Hkv - 1 && r + TM >= nrows ? TC_PROG_FULL : 0u);
+            h.prog = prog;
             const int groups = (nrow + 7) / 8;   // 8-row groups (one 128B-swizzle atom per column block)
             uint8_t* sk = kslot(smem, t, nk);
             uint8_t* sv = vslot(smem, t, nk, nv);
             uint8_t* sq = sk + KV_BYTES;
             const bool dep = fused && mv;
-            mb_expect(&S.kfull[ks], (uint32_t)(np * groups * 2048 + Q_BYTES + (dep ? 16 : 0)));
-            mb_expect(&S.vfull[vs], (uint32_t)(np * groups * 2048));
+            mb_expect(&S.kfull[ks], (uint32_t)(np_t * groups * 2048 + Q_BYTES + (dep ? 16 : 0)));
+            mb_expect(&S.vfull[vs], (uint32_t)(np_t * groups * 2048));
             if (dep) bulk_g2s16(&h.dep, a.desc + un.stage_base + r / TM, &S.kfull[ks]);
             const int row0 = un.off + un.r0 + r;
-            for (int sgi = 0; sgi < np; ++sgi) {    // one 4-D box per segment for K and one for V
-              const int colk = (a.l0 + li) * row_cols + (g + sgi) * DH;
-              const int sgo = sgi * (seg / 8) * 2048;   // segment's first group
+            for (int sgi = 0; sgi < np_t; ++sgi) {   // one 4-D box per segment for K and one for V
+              const int colk = (a.l0 + li) * row_cols + (hd + sgi) * DH;
+              const int sgo = sgi * (seg_t / 8) * 2048;   // segment's first group
               tma4d(sk + sgo, &maps.kvg[groups - 1], row0, colk / 64, &S.kfull[ks]);
               tma4d(sv + sgo, &maps.kvg[groups - 1], row0, (colk + a.Hkv * DH) / 64, &S.vfull[vs]);
             }
+            const int qrow = (li * a.B + un.b) * a.H + g * a.G;
             tma3d(sq, &maps.q, 0, qrow, 0, &S.kfull[ks]);   // both 64-column blocks of the 16 q rows
             TC_TRACE_AT(t, 1);
+          }
+          __syncwarp();
+          ++t;
+        };
+        for (int g = 0; g < a.Hkv; g += npk, ++iseq) {
+          const int np = min(npk, a.Hkv - g);
+          const int glast = g + np - 1;
+          const uint32_t full = glast == a.Hkv - 1 ? TC_PROG_FULL : 0u;
+          if (!tailpack) {
+            for (int r = 0; r < nrows; r += TM) {
+              const int nrow = min(TM, nrows - r);
+              // heads g..glast are read up to r + nrow rows once this tile lands
+              emit(g, g, -1, np, seg, r, nrow, r == 0, r + TM >= nrows,
+                   (uint32_t)(glast * TC_HEAD_STRIDE + r + nrow) | (r + TM >= nrows ? full : 0u));
             }
-            __syncwarp();
-            ++t;
+          } else {
+            const int rfull = nrows - tl;
+            // read progress: heads < g complete until the packed tail tile lands (conservative)
+            for (int hh = 0; hh < np; ++hh)
+              for (int r = 0; r < rfull; r += TM)
+                emit(g, g + hh, hh, 1, TM, r, TM, hh == 0 && r == 0, false, (uint32_t)(g * TC_HEAD_STRIDE));
+            emit(g, g, -1, np, seg, rfull, tl, false, true, (uint32_t)(glast * TC_HEAD_STRIDE + nrows) | full);
           }
         }
       }
@@ -692,7 +726,8 @@ __global__ void __launch_bounds__(tc_threads(NC), 1) k_attn_tc(const __grid_cons
           st_rlx_u64(a.progress + w, ((unsigned long long)a.epoch << 32) | h.prog);
           if (h.mode == UNIT_MOVE && h.dep.ua >= 0) {
             // the tile overwrites heads g..g+np-1 of its destination rows
-            const uint32_t gbase = (uint32_t)((h.g + (PACK ? hdr_np(h) : 1) - 1) * TC_HEAD_STRIDE);
+            const uint32_t gbase =
+                (uint32_t)((h.g + (PACK ? max(hdr_hoff(h), 0) + hdr_np(h) : 1) - 1) * TC_HEAD_STRIDE);
             for (int v = h.dep.ua; v <= h.dep.ub; ++v) {
               const int need = v == h.dep.ua ? h.dep.need_a : (v == h.dep.ub ? h.dep.need_b : -1);
               const int it = v * a.nl + h.li;
@@ -717,7 +752,7 @@ __global__ void __launch_bounds__(tc_threads(NC), 1) k_attn_tc(const __grid_cons
           for (int sgi = 0; sgi < np; ++sgi) {       // one segment per packed KV head
             const uint8_t* sk = kslot(smem, t, nk) + sgi * (seg / 8) * 2048;
             const uint8_t* sv = vslot(smem, t, nk, nv) + sgi * (seg / 8) * 2048;
-            const int colk = (a.l0 + h.li) * 2 * a.Hkv * DH + (h.g + sgi) * DH;   // elements
+            const int colk = (a.l0 + h.li) * 2 * a.Hkv * DH + (h.g + (PACK ? max(hdr_hoff(h), 0) : 0) + sgi) * DH;
             const int colv = colk + a.Hkv * DH;
             if (lane == 0) {
               const CUtensorMap* map = h.mode == UNIT_MOVE ? maps.st_kv : maps.st_stage;
@@ -821,11 +856,18 @@ __global__ void __launch_bounds__(tc_threads(NC), 1) k_attn_tc(const __grid_cons
       const bool first = h.flags & 1;
       bool valid, loaded;                             // loaded: row holds this item's (or slack) data
       const int np = PACK ? hdr_np(h) : 1;
+      const int hoff = PACK ? hdr_hoff(h) : -1;
       if (!PACK || np == 1) {                          // warp-uniform: one KV head per tile
         valid = row < h.nvalid;
         loaded = row < ((h.nvalid + 15) & ~15);
+        if (hoff < 0) {
 #pragma unroll
-        for (int c = 0; c < CW; ++c) s[c] = valid ? s[c] * a.qscale : -INFINITY;
+          for (int c = 0; c < CW; ++c) s[c] = valid ? s[c] * a.qscale : -INFINITY;
+        } else {                                       // tail-packed item: head g + hoff's full tile
+          const int c0 = hoff * a.G - co, c1 = c0 + a.G;
+#pragma unroll
+          for (int c = 0; c < CW; ++c) s[c] = (valid && c >= c0 && c < c1) ? s[c] * a.qscale : -INFINITY;
+        }
       } else {
         // block-diagonal mask of packed tiles: segment sgm only meets columns
         // [sgm G, (sgm+1) G); columns past np G stay unmasked (finite, never written out);
@@ -862,7 +904,8 @@ __global__ void __launch_bounds__(tc_threads(NC), 1) k_attn_tc(const __grid_cons
 #pragma unroll
         for (int c = 0; c < CW; ++c) {
           const float mn = first ? mt[c] : fmaxf(m[c], mt[c]);
-          corr[c] = first ? 0.f : ex2f(m[c] - mn);
+          // a column no tile of the item has met yet keeps m = -inf (tail-packed items)
+          corr[c] = first ? 0.f : (mn == -INFINITY ? 1.f : ex2f(m[c] - mn));
           m[c] = mn;
           lrow[c] = first ? 0.f : lrow[c] * corr[c];
         }
@@ -879,7 +922,7 @@ __global__ void __launch_bounds__(tc_threads(NC), 1) k_attn_tc(const __grid_cons
       const uint32_t jj2 = (uint32_t)(row & 63) * 2u;
 #pragma unroll
       for (int c = 0; c < CW; ++c) {
-        const float pv = ex2f(s[c] - m[c]);
+        const float pv = s[c] == -INFINITY ? 0.f : ex2f(s[c] - m[c]);
         lrow[c] += pv;
         const __nv_bfloat16 hi = __float2bfloat16_rn(pv);
         const __nv_bfloat16 lo = __float2bfloat16_rn(pv - __bfloat162float(hi));
