@@ -794,11 +794,16 @@ s3_status s3_decode_step(s3_ctx* ctx, int32_t l0, int32_t nl, const void* q, con
     int32_t mean_rows = 0, nc_pick = 8;
     if (ctx->cfg.attn_variant == 2 && B > 0) {
       const int G = ctx->sh.H / ctx->sh.Hkv, Hkv = ctx->sh.Hkv;
-      auto tiles = [&](int pmax, int r) -> int64_t {   // one (slot, layer): the kernel's packing rule
+      auto tiles = [&](int pmax, int r) -> int64_t {   // one (slot, layer): the kernel's packing rules
         const int rg = (r + 7) & ~7;
-        if (pmax > 1 && 2 * rg <= 128) {
+        if (pmax > 1 && 2 * rg <= 128) {                 // short unit: heads packed
           const int np = std::min(std::min(pmax, 128 / rg), Hkv);
           return (Hkv + np - 1) / np;
+        }
+        const int tl = r % 128, tg = (tl + 7) & ~7;
+        if (pmax > 1 && tl > 0 && 2 * tg <= 128) {       // long unit: full tiles + packed tails
+          const int np = std::min(std::min(pmax, 128 / tg), Hkv);
+          if (np > 1) return (int64_t)Hkv * (r / 128) + (Hkv + np - 1) / np;
         }
         return (int64_t)Hkv * ((r + 127) / 128);
       };
