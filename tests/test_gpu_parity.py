@@ -559,6 +559,18 @@ def test_grouped_query_kv_tensor_cores(H, Hkv, C, policy, mode, staging):
         assert r["fused_steps"] == 0
 
 
+@pytest.mark.parametrize("H,Hkv,seed", [(32, 8, 61), (8, 4, 62), (12, 2, 63)])
+def test_tensor_core_tail_packing(H, Hkv, seed):
+    """Units longer than one 128-row tile: each head's rows past its last full tile
+    (<= 64) share a tile with np other heads' tails, those heads' full tiles first in
+    the same item (columns of heads a full tile does not belong to stay -inf until
+    their own tiles arrive).  Long prompts so most units have full tiles + a tail of
+    every size; fused row shift with evictions and NaN-poisoned slack rows."""
+    t = s3synth.make_trace(30, seed=seed, policy="short", p=0.3, max_seq_len=640, prompt_max=420)
+    r = lockstep(t, 2, H, 128, 6000, C=512, S=4096, attn_variant=2, Hkv=Hkv, poison=True)
+    assert r["evictions"] > 0 and r["worst"] <= TOL
+
+
 @pytest.mark.parametrize("variant,chunks,C,dev_out,mode", [
     (0, 0, 16, False, 0), (0, 64, 0, False, 0), (0, 3, 16, False, 0), (1, 0, 16, False, 1), (2, 0, 16, False, 0),
     (0, 0, 16, True, 0), (0, 5, 8, True, 0), (0, 64, 0, True, 0), (2, 0, 16, True, 0), (0, 0, 16, True, 1),
