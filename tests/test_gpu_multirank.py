@@ -175,3 +175,38 @@ def test_bench_nccl_exchange_world1():
         assert runs[name]["tokens"] == runs["plain"]["tokens"]
         assert runs[name]["wholerun"]["tokens"] == runs["plain"]["wholerun"]["tokens"]
         assert runs[name]["wholerun"]["steps"] == runs["plain"]["wholerun"]["steps"]
+
+
+def test_library_nccl_exchange_in_process():
+    """libs3's own NCCL communicator without torch.distributed: a one-rank
+    communicator (s3_nccl_get_unique_id -> s3_comm_init), every step's counter
+    all-reduce by s3_exchange_counters inside the multi-rank admission path; the
+    schedule equals the plain world-1 engine's step by step, and s3_counters_get
+    reports the last exchanged matrix."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    sys.path.insert(0, ROOT)
+    import s3synth
+    from paper_2306_06000_b200 import s3 as abi
+    from paper_2306_06000_b200.engine import S3Engine
+    t = s3synth.make_trace(60, seed=5, policy="short", p=0.3, max_seq_len=128, prompt_max=24)
+    L, H, D, R = 2, 4, 64, 1500
+    engs = [S3Engine(L, H, D, 128, R, 32, device=0, host_store_bytes=64 << 20, exchange_admission=x,
+                     reserve_sms=4 if x else 0) for x in (False, True)]
+    engs[1].comm_init(abi.s3_nccl_get_unique_id())
+    for e in engs:
+        e.submit(t.req_id, t.prompt, t.alloc, t.out)
+        e.initial_admit()
+    steps = 0
+    while engs[0].B or engs[0].counters_local()[3] + engs[0].counters_local()[4]:
+        stats = [e.step() for e in engs]
+        assert stats[0] == stats[1], (steps, stats)
+        assert engs[0].batch_view() == engs[1].batch_view()
+        steps += 1
+        assert steps < 2000
+    c = engs[1].counters_get()
+    row = engs[1].counters_local()
+    assert c.world == 1 and c.exchanges == steps + 1
+    assert c.rank_free_rows[0] == row[0] and c.tokens_total == row[7] == int(t.out.sum())
+    for e in engs:
+        e.close()
