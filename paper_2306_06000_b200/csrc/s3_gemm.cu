@@ -23,6 +23,12 @@
 // Tiles are walked n-major (the M tiles of one W column block run on
 // neighbouring CTAs at the same time, so W streams from HBM once and the
 // small A operand stays in L2).
+// Small batches (M <= 64, SW = true): the operands swap roles -- the MMA's
+// 128-row M side is a block of W rows and its N side (BN = 64) the
+// batch, so a K block moves 16 KB of weights plus only BN x 128 B of
+// activations (instead of a 128-row activation tile mostly zero-filled), and
+// TMEM holds D^T: the epilogue transposes 32 x 32 blocks through shared memory
+// into the row-major output.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -239,8 +245,12 @@ __device__ __forceinline__ void g_arrive_leader(uint64_t* b) {
 //   the MMAs (the tensor cores read both CTAs' shared memory), each CTA's
 //   TMEM holds its 128 accumulator rows.  W is read from L2 once per 256 rows
 //   instead of once per 128, halving the operand traffic per flop.
-template <int BN, int CG>
+// SW (CG = 1 only): maps.a is W (128-row boxes), maps.w the activations (BN-row
+//   boxes); tile t covers W rows (t % m_tiles) x 128 and batch rows (t / m_tiles) x BN,
+//   and the accumulator is D^T (TMEM lane = output column, column = batch row).
+template <int BN, int CG, bool SW = false>
 __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(const __grid_constant__ GemmMaps maps, GemmArgs a) {
+  static_assert(!SW || CG == 1, "swapped operands use single-CTA tiles");
   constexpr int A_BYTES = GM * GK * 2, W_BYTES = (BN / CG) * GK * 2, STAGE = A_BYTES + W_BYTES;
   constexpr int NSTG = gemm_stages(STAGE);
   constexpr int TMEM_COLS = 2 * BN;
@@ -368,9 +378,9 @@ __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(const __grid_constant__ G
     uint32_t iph[2] = {0u, 0u};
     int ob = 0;
     const uint32_t tl = tmem + ((uint32_t)(quarter * 32) << 16);
-    auto load_in = [&](int buf, const CUtensorMap* map, int x, int y) {
+    auto load_in = [&](int buf, const CUtensorMap* map, int x, int y, uint32_t bytes = 4096u) {
       if (lane == 0) {
-        g_mb_expect(&ib[buf], 4096u);
+        g_mb_expect(&ib[buf], bytes);
         g_tma2d(eb + 8192 + buf * 4096, map, x, y, &ib[buf]);
       }
     };
@@ -424,6 +434,34 @@ __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(const __grid_constant__ G
       }
       __syncwarp();
     };
+    // SW: 32 accumulator columns (batch rows y .. y+31) of this lane's output column ->
+    // a [32 rows][32 columns] bf16 staging block (64 B rows, unswizzled) -> one TMA store
+    auto finishT = [&](float* v, const CUtensorMap* dmap, int x, int y) {
+      if (a.epi == 1) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = gelu_tanh(v[i]);
+      }
+      uint8_t* o = out_tile();
+      const uint32_t ob_s = gsu32(o) + (uint32_t)(lane * 2);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const __nv_bfloat16 h = __float2bfloat16_rn(v[i]);
+        asm volatile("st.shared.u16 [%0], %1;" ::"r"(ob_s + (uint32_t)(i * 64)), "h"(*reinterpret_cast<const uint16_t*>(&h))
+                     : "memory");
+      }
+      store_out(dmap, x, y);
+    };
+    auto add_cT = [&](float* v, int buf) {        // v += C^T block in input buffer buf
+      wait_in(buf);
+      const uint32_t cb = gsu32(eb + 8192 + buf * 4096) + (uint32_t)(lane * 2);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        uint16_t u;
+        asm volatile("ld.shared.u16 %0, [%1];" : "=h"(u) : "r"(cb + (uint32_t)(i * 64)) : "memory");
+        v[i] += __uint_as_float((uint32_t)u << 16);
+      }
+      __syncwarp();
+    };
     auto tmem_ld64 = [&](int col, float (&v)[64]) {
       uint32_t r[32];
       g_tmem_ld32(tl + (uint32_t)col, r);
@@ -448,10 +486,30 @@ __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(const __grid_constant__ G
       const int S = wk.ncontrib;
       const int y = (t % a.m_tiles) * TM_ROWS + (int)rank * GM + quarter * 32;   // first row of this warp
       const int n0 = (t / a.m_tiles) * BN;
-      const int seg = n0 / a.seg_cols, x0 = n0 - seg * a.seg_cols;
+      // SW: this warp's 32 output columns start at wn = y, the tile's batch rows at n0
+      const int wn = SW ? y : n0;
+      const int seg = wn / a.seg_cols, x0 = wn - seg * a.seg_cols;
       const CUtensorMap* dmap = &maps.d[seg];
       g_mb_wait(&tfull[acc], (uint32_t)(it >> 1) & 1u);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (SW && S == 1) {
+        const int rows = a.M - n0 < BN ? a.M - n0 : BN;   // batch rows present in this tile
+        const int nch = (rows + 31) >> 5;
+        if (a.epi == 2) load_in(0, &maps.c, wn, n0, 2048u);
+#pragma unroll 1
+        for (int i = 0; i < nch; ++i) {
+          if (a.epi == 2 && i + 1 < nch) load_in((i + 1) & 1, &maps.c, wn, n0 + 32 * (i + 1), 2048u);
+          uint32_t r[32];
+          float v[32];
+          g_tmem_ld32(tl + (uint32_t)(acc * BN + 32 * i), r);
+          if (i + 1 == nch) release(acc);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+          if (a.epi == 2) add_cT(v, i & 1);
+          finishT(v, dmap, x0, n0 + 32 * i);
+        }
+        continue;
+      }
       if (S == 1) {
         if (a.epi == 2) load_in(0, &maps.c, n0, y);
 #pragma unroll 1
@@ -512,6 +570,18 @@ __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(const __grid_constant__ G
             add_p(v, 0);
             add_p(v + 32, 1);
           }
+          if constexpr (SW) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              if (n0 + c + 32 * h >= a.M) break;   // batch rows past M: nothing to store
+              if (a.epi == 2) {
+                load_in(0, &maps.c, wn, n0 + c + 32 * h, 2048u);
+                add_cT(v + 32 * h, 0);
+              }
+              finishT(v + 32 * h, dmap, x0, n0 + c + 32 * h);
+            }
+            continue;
+          }
           if (a.epi == 2) {
             load_in(0, &maps.c, n0 + c, y);
             add_c(v, 0);
@@ -571,7 +641,8 @@ int gemm_smem() {
 }
 
 // bf16 or fp32 row-major [rows][cols] map with a {box_cols, 32}-row box, 128B swizzle (TMA store / load)
-bool encode_rows(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, int fp32, uint32_t box_cols) {
+bool encode_rows(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, int fp32, uint32_t box_cols,
+                 bool swizzle = true) {
   GEncodeFn enc = g_encoder();
   if (!enc) return false;
   const uint64_t es = fp32 ? 4 : 2;
@@ -580,13 +651,14 @@ bool encode_rows(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols,
   cuuint32_t box[2] = {box_cols, 32};
   cuuint32_t el[2] = {1, 1};
   return enc(m, fp32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base),
-             dims, strides, box, el, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+             dims, strides, box, el, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, int CG>
+template <int BN, int CG, bool SW = false>
 cudaError_t launch_one(const GemmMaps& maps, const GemmArgs& a, int grid, cudaStream_t st) {
-  static const bool attr = cudaFuncSetAttribute(k_gemm<BN, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  static const bool attr = cudaFuncSetAttribute(k_gemm<BN, CG, SW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                 gemm_smem<BN, CG>()) == cudaSuccess;
   if (!attr) return cudaErrorInvalidValue;
   cudaLaunchConfig_t cfg = {};
@@ -601,7 +673,7 @@ cudaError_t launch_one(const GemmMaps& maps, const GemmArgs& a, int grid, cudaSt
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_gemm<BN, CG>, maps, a);
+  return cudaLaunchKernelEx(&cfg, k_gemm<BN, CG, SW>, maps, a);
 }
 
 __global__ void __launch_bounds__(256) k_cast_bf16(const float4* __restrict__ src, uint2* __restrict__ dst, int64_t n4) {
@@ -658,6 +730,7 @@ int64_t gemm_ws_bytes(int cmax, int tiles, int rows, int BN, int CG) {
 // columns when 256-wide tiles would leave SMs idle.  Then the split-K factor.
 struct GemmPlan {
   int CG, BN, rows, m_tiles, tiles, groups, sk, dp_tiles, cmax;
+  bool SW;            // swapped operands (small batch): 128 W rows x BN batch rows per tile
   int64_t ws_bytes;   // workspace the plan needs (0 for data-parallel)
 };
 bool gemm_plan(const GemmCall& g, int64_t ws_avail, GemmPlan& p) {
@@ -678,6 +751,36 @@ bool gemm_plan(const GemmCall& g, int64_t ws_avail, GemmPlan& p) {
   //    weights faster than stream-K's partial sums);
   //  * stream-K otherwise loses: groups at different K offsets of the same W block stop
   //    sharing it in L2.
+  // Small batches (M <= 64): swapped operands, 64 batch columns per tile
+  // (tools/gemm_sweep_swap.sh: 1.1-1.3x the unswapped tiles at M <= 64 on GPT-J's
+  // projections, slower from M = 96 where the 128-row activation tile is mostly real rows);
+  // stream-K for long K (>= 8192: N / 128 tiles of 256 K blocks each).  S3_GEMM_SWAP=0
+  // turns it off (A/B).
+  static const int swap_on = [] { const char* e = getenv("S3_GEMM_SWAP"); return e ? atoi(e) : 1; }();
+  if (g.M <= 64 && swap_on && !force_cg) {
+    p.SW = true;
+    p.CG = 1;
+    p.BN = 64;
+    p.rows = GM;
+    p.m_tiles = g.N / GM;
+    p.tiles = p.m_tiles;                 // one batch tile
+    const int kblocks = g.K / GK;
+    const int rem = p.tiles % sms;
+    const int sk_tiles = rem == 0 ? 0 : (p.tiles >= sms ? rem + sms : p.tiles);
+    p.sk = (force_sk >= 0 ? force_sk : kblocks >= 128) && sk_tiles > 0 && (int64_t)sk_tiles * kblocks >= 8LL * sms;
+    p.dp_tiles = p.sk ? p.tiles - sk_tiles : p.tiles;
+    p.cmax = 1;
+    p.ws_bytes = 0;
+    const int Gs = p.sk ? (int)std::min<int64_t>(sms, (int64_t)(p.tiles - p.dp_tiles) * kblocks) : sms;
+    if (p.sk) {
+      p.cmax = sk_cmax(p.tiles, kblocks, Gs, p.dp_tiles);
+      p.ws_bytes = gemm_ws_bytes(p.cmax, p.tiles, p.rows, p.BN, 1);
+      if (p.cmax == 1 || p.ws_bytes > ws_avail) { p.sk = 0; p.dp_tiles = p.tiles; p.cmax = 1; p.ws_bytes = 0; }
+    }
+    p.groups = p.sk ? Gs : std::min(p.tiles, sms);
+    return true;
+  }
+  p.SW = false;
   const int sms2 = sms / 2;
   const int m2 = (g.M + 2 * GM - 1) / (2 * GM);
   const int tiles2 = m2 * (g.N / 256);
@@ -733,29 +836,37 @@ cudaError_t launch_gemm(const GemmCall& g, cudaStream_t st) {
   if (!gemm_plan(g, g.workspace ? g.workspace_bytes : 0, p) || !g.a || !g.w || !g.d[0] || (g.epi == 2 && !g.c))
     return cudaErrorInvalidValue;
   GemmMaps maps;
-  if (!encode_kmajor(&maps.a, g.a, (uint64_t)g.M, (uint64_t)g.K, GM)) return cudaErrorInvalidValue;
-  if (!encode_kmajor(&maps.w, g.w, (uint64_t)g.N, (uint64_t)g.K, (uint32_t)(p.BN / p.CG))) return cudaErrorInvalidValue;
+  if (p.SW) {   // the MMA's M side is W (128-row boxes), its N side the batch (BN-row boxes)
+    if (!encode_kmajor(&maps.a, g.w, (uint64_t)g.N, (uint64_t)g.K, GM)) return cudaErrorInvalidValue;
+    if (!encode_kmajor(&maps.w, g.a, (uint64_t)g.M, (uint64_t)g.K, (uint32_t)p.BN)) return cudaErrorInvalidValue;
+  } else {
+    if (!encode_kmajor(&maps.a, g.a, (uint64_t)g.M, (uint64_t)g.K, GM)) return cudaErrorInvalidValue;
+    if (!encode_kmajor(&maps.w, g.w, (uint64_t)g.N, (uint64_t)g.K, (uint32_t)(p.BN / p.CG))) return cudaErrorInvalidValue;
+  }
+  // SW: 32 x 32 unswizzled output / addend blocks (the epilogue's transposed staging)
+  const uint32_t obox = p.SW ? 32 : 64;
   const int nseg = g.N / g.seg_cols;
   for (int i = 0; i < 3; ++i) {
     const void* base = g.d[i < nseg ? i : 0];
     if (i < nseg && !g.d[i]) return cudaErrorInvalidValue;
-    if (!encode_rows(&maps.d[i], base, (uint64_t)g.M, (uint64_t)g.seg_cols, 0, 64)) return cudaErrorInvalidValue;
+    if (!encode_rows(&maps.d[i], base, (uint64_t)g.M, (uint64_t)g.seg_cols, 0, obox, !p.SW)) return cudaErrorInvalidValue;
   }
   maps.c = maps.d[0];
-  if (g.epi == 2 && !encode_rows(&maps.c, g.c, (uint64_t)g.M, (uint64_t)g.N, 0, 64)) return cudaErrorInvalidValue;
+  if (g.epi == 2 && !encode_rows(&maps.c, g.c, (uint64_t)g.M, (uint64_t)g.N, 0, obox, !p.SW)) return cudaErrorInvalidValue;
   maps.p = maps.d[0];
   if (p.sk && !encode_rows(&maps.p, static_cast<uint8_t*>(g.workspace) + GEMM_CNT_BYTES,
                            (uint64_t)p.tiles * (p.cmax - 1) * p.rows, (uint64_t)p.BN, 1, 32))
     return cudaErrorInvalidValue;
   GemmArgs a;
   a.M = g.M; a.N = g.N; a.K = g.K; a.epi = g.epi; a.seg_cols = g.seg_cols;
-  a.m_tiles = p.m_tiles; a.n_tiles = g.N / p.BN;
+  a.m_tiles = p.m_tiles; a.n_tiles = p.SW ? 1 : g.N / p.BN;
   a.dp_tiles = p.dp_tiles;
   a.cmax = p.cmax;
   a.cnt = p.sk ? static_cast<int32_t*>(g.workspace) : nullptr;
   const int groups = p.groups;
   cudaError_t e;
-  if (p.CG == 2) e = launch_one<256, 2>(maps, a, 2 * groups, st);
+  if (p.SW) e = launch_one<64, 1, true>(maps, a, groups, st);
+  else if (p.CG == 2) e = launch_one<256, 2>(maps, a, 2 * groups, st);
   else if (p.BN == 256) e = launch_one<256, 1>(maps, a, groups, st);
   else if (p.BN == 128) e = launch_one<128, 1>(maps, a, groups, st);
   else e = launch_one<64, 1>(maps, a, groups, st);

@@ -46,6 +46,13 @@ def _ref(a, w, epi, c):
     (640, 4096, 16384, 2, 1, True), (512, 4096, 16384, 2, 1, True), (200, 4096, 4096, 1, 1, True),
     (64, 12288, 4096, 0, 3, True), (512, 4096, 4096, 2, 1, False), (512, 12288, 4096, 0, 3, True),
     (256, 4096, 16384, 2, 1, True), (700, 12288, 4096, 1, 1, True),
+    # small batches (M <= 64): swapped operands (W rows on the MMA's M side), ragged batch
+    # columns, stream-K partials reduced through the transposed epilogue; then the
+    # unswapped single-CTA / pair tiles just above
+    (1, 4096, 4096, 2, 1, True), (33, 12288, 4096, 0, 3, True), (100, 4096, 16384, 2, 1, True),
+    (128, 16384, 4096, 1, 1, True), (96, 4096, 4096, 1, 1, False), (65, 384, 192, 2, 1, True),
+    (17, 4096, 16384, 1, 1, True), (127, 12288, 4096, 0, 3, False),
+    (64, 4096, 16384, 2, 1, True), (48, 4096, 4096, 1, 1, True), (161, 12288, 4096, 0, 3, True), (255, 4096, 16384, 2, 1, True), (129, 16384, 4096, 1, 1, False),
 ])
 def test_gemm_matches_fp64(M, N, K, epi, nseg, ws):
     from paper_2306_06000_b200 import s3 as abi

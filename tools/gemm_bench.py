@@ -27,6 +27,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--m", default="128,256,512,1024,2048,4096")
     ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--copies", type=int, default=1,
+                    help="cycle through this many weight copies (> L2 in total: weights streamed from HBM)")
     ap.add_argument("--lib", default=None, help="A/B: load this libs3.so build instead of the in-tree one")
     args = ap.parse_args()
     if args.lib:
@@ -38,15 +40,21 @@ def main():
         tot_flop, tot_ms, tot_ms_cb = 0.0, 0.0, 0.0
         for name, (N, K, epi) in SHAPES.items():
             a = torch.randn(M, K, device="cuda").to(torch.bfloat16)
-            w = (torch.randn(N, K, device="cuda") / K ** 0.5).to(torch.bfloat16)
+            ws_ = [(torch.randn(N, K, device="cuda") / K ** 0.5).to(torch.bfloat16) for _ in range(args.copies)]
+            w = ws_[0]
+            it = [0]
             d = torch.zeros(M, N, device="cuda", dtype=torch.bfloat16)
             ws = torch.zeros(max(abi.s3_gemm_workspace(M, N, K, epi=epi), 16), device="cuda", dtype=torch.uint8)
 
+            def nxt():
+                it[0] += 1
+                return ws_[it[0] % len(ws_)]
+
             def ours():
-                abi.s3_gemm(st, a, w, d, c=d if epi == 2 else None, epi=epi, workspace=ws)
+                abi.s3_gemm(st, a, nxt(), d, c=d if epi == 2 else None, epi=epi, workspace=ws)
 
             def cublas():
-                torch.matmul(a, w.T, out=d)
+                torch.matmul(a, nxt().T, out=d)
 
             res = {}
             for tag, fn in (("s3_gemm", ours), ("cublas", cublas)):
