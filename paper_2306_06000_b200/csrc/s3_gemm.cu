@@ -134,6 +134,8 @@ struct GemmArgs {
   int32_t dp_tiles;       // tiles [0, dp_tiles) data parallel, the rest stream-K (equal K-block ranges per group)
   int32_t cmax;           // stream-K: most CTA groups contributing to one tile (partial slots = cmax - 1)
   int32_t* cnt;           // stream-K: per (tile, CTA of the pair) [claim, done] counters (zero between calls)
+  int32_t red;            // stream-K: 1 = contributors TMA-reduce-add into one fp32 tile per tile (zero between
+                          //   calls; the reducer reads it once and re-zeroes it), 0 = one partial slot each
 };
 
 // Work of one CTA group: whole tiles g, g + G, ... below dp_tiles (data
@@ -178,6 +180,12 @@ struct WorkIter {
     return true;
   }
 };
+__device__ __forceinline__ void g_tma_reduce_add2d(const CUtensorMap* map, int c0, int c1, const void* src) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2}], [%3];" ::"l"(map),
+               "r"(c0), "r"(c1), "r"(gsu32(src))
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
 __device__ __forceinline__ void g_tma_store2d(const CUtensorMap* map, int c0, int c1, const void* src) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(map), "r"(c0),
                "r"(c1), "r"(gsu32(src))
@@ -390,10 +398,13 @@ __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(const __grid_constant__ G
       __syncwarp();
       return eb + ob * 4096;
     };
-    auto store_out = [&](const CUtensorMap* map, int x, int y) {
+    auto store_out = [&](const CUtensorMap* map, int x, int y, bool reduce_add = false) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncwarp();
-      if (lane == 0) g_tma_store2d(map, x, y, eb + ob * 4096);
+      if (lane == 0) {
+        if (reduce_add) g_tma_reduce_add2d(map, x, y, eb + ob * 4096);
+        else g_tma_store2d(map, x, y, eb + ob * 4096);
+      }
       ob ^= 1;
     };
     // 64 accumulator columns -> epilogue (C already summed in for epi 2 by the caller) -> bf16 store
@@ -530,7 +541,7 @@ __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(const __grid_constant__ G
       asm volatile("bar.sync 1, 128;" ::: "memory");
       const int role = *s_role;
       if (role < S - 1) {
-        const int prow = (t * (a.cmax - 1) + role) * TM_ROWS + (int)rank * GM + quarter * 32;
+        const int prow = (a.red ? t : t * (a.cmax - 1) + role) * TM_ROWS + (int)rank * GM + quarter * 32;
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
           uint32_t r[32];
@@ -539,7 +550,7 @@ __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(const __grid_constant__ G
           uint8_t* o = out_tile();
 #pragma unroll
           for (int j = 0; j < 8; ++j) sts128(o, swz(lane, j), make_uint4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]));
-          store_out(&maps.p, c, prow);
+          store_out(&maps.p, c, prow, a.red != 0);
         }
         if (lane == 0) {                               // partial in HBM/L2, then count this warp in
           asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
@@ -563,12 +574,27 @@ __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(const __grid_constant__ G
           float v[64];
           tmem_ld64(acc * BN + c, v);
           if (c + 64 >= BN) release(acc);
-          for (int j = 0; j < S - 1; ++j) {
-            const int prow = (t * (a.cmax - 1) + j) * TM_ROWS + (int)rank * GM + quarter * 32;
+          if (a.red) {   // the other splits' sum, one TMA round trip; then zero it for the next call
+            const int prow = t * TM_ROWS + (int)rank * GM + quarter * 32;
             load_in(0, &maps.p, c, prow);
             load_in(1, &maps.p, c + 32, prow);
             add_p(v, 0);
             add_p(v + 32, 1);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {   // zeros back by TMA stores (generic stores here cost ~8 %)
+              uint8_t* o = out_tile();
+#pragma unroll
+              for (int j = 0; j < 8; ++j) sts128(o, swz(lane, j), make_uint4(0u, 0u, 0u, 0u));
+              store_out(&maps.p, c + 32 * h, prow);
+            }
+          } else {
+            for (int j = 0; j < S - 1; ++j) {
+              const int prow = (t * (a.cmax - 1) + j) * TM_ROWS + (int)rank * GM + quarter * 32;
+              load_in(0, &maps.p, c, prow);
+              load_in(1, &maps.p, c + 32, prow);
+              add_p(v, 0);
+              add_p(v + 32, 1);
+            }
           }
           if constexpr (SW) {
 #pragma unroll
@@ -720,9 +746,18 @@ int sk_cmax(int tiles, int kblocks, int G, int dp_tiles) {
 // GEMM_CNT_BYTES, shared by every plan (each call leaves its counters zero, so GEMMs with
 // different plans can share one workspace) -- then cmax - 1 fp32 partial tiles per tile
 constexpr int64_t GEMM_CNT_BYTES = 32768;
+// (or, reduce-add mode, one fp32 accumulation tile per tile)
+static int gemm_red_mode() {
+  static const int r = [] { const char* e = getenv("S3_GEMM_RED"); return e ? atoi(e) : 1; }();
+  return r;
+}
+// Reduce-add for every stream-K plan (tools/gemm_sweep_red.sh: long-K projections
+// 1.1-1.2x; with 2 contributors per tile about 3 % slower than a slot); one mode per
+// process, so plans sharing a workspace agree on what it holds between calls.
+bool gemm_red(int) { return gemm_red_mode() != 0; }
 int64_t gemm_ws_bytes(int cmax, int tiles, int rows, int BN, int CG) {
   if ((int64_t)tiles * CG * 2 * 4 > GEMM_CNT_BYTES) return INT64_MAX;
-  return GEMM_CNT_BYTES + (int64_t)(cmax - 1) * tiles * rows * BN * 4;
+  return GEMM_CNT_BYTES + (int64_t)(gemm_red(cmax) ? 1 : cmax - 1) * tiles * rows * BN * 4;
 }
 
 // Tile choice: a CTA pair per 256 x 256 tile (half the operand traffic per
@@ -754,8 +789,8 @@ bool gemm_plan(const GemmCall& g, int64_t ws_avail, GemmPlan& p) {
   // Small batches (M <= 64): swapped operands, 64 batch columns per tile
   // (tools/gemm_sweep_swap.sh: 1.1-1.3x the unswapped tiles at M <= 64 on GPT-J's
   // projections, slower from M = 96 where the 128-row activation tile is mostly real rows);
-  // stream-K for long K (>= 8192: N / 128 tiles of 256 K blocks each).  S3_GEMM_SWAP=0
-  // turns it off (A/B).
+  // stream-K when the N / 128 tiles fill at most half the SMs (GPT-J's output and
+  // down projections: 32 tiles).  S3_GEMM_SWAP=0 turns it off (A/B).
   static const int swap_on = [] { const char* e = getenv("S3_GEMM_SWAP"); return e ? atoi(e) : 1; }();
   if (g.M <= 64 && swap_on && !force_cg) {
     p.SW = true;
@@ -767,7 +802,7 @@ bool gemm_plan(const GemmCall& g, int64_t ws_avail, GemmPlan& p) {
     const int kblocks = g.K / GK;
     const int rem = p.tiles % sms;
     const int sk_tiles = rem == 0 ? 0 : (p.tiles >= sms ? rem + sms : p.tiles);
-    p.sk = (force_sk >= 0 ? force_sk : kblocks >= 128) && sk_tiles > 0 && (int64_t)sk_tiles * kblocks >= 8LL * sms;
+    p.sk = (force_sk >= 0 ? force_sk : 2 * p.tiles <= sms) && sk_tiles > 0 && (int64_t)sk_tiles * kblocks >= 8LL * sms;
     p.dp_tiles = p.sk ? p.tiles - sk_tiles : p.tiles;
     p.cmax = 1;
     p.ws_bytes = 0;
@@ -855,7 +890,7 @@ cudaError_t launch_gemm(const GemmCall& g, cudaStream_t st) {
   if (g.epi == 2 && !encode_rows(&maps.c, g.c, (uint64_t)g.M, (uint64_t)g.N, 0, obox, !p.SW)) return cudaErrorInvalidValue;
   maps.p = maps.d[0];
   if (p.sk && !encode_rows(&maps.p, static_cast<uint8_t*>(g.workspace) + GEMM_CNT_BYTES,
-                           (uint64_t)p.tiles * (p.cmax - 1) * p.rows, (uint64_t)p.BN, 1, 32))
+                           (uint64_t)p.tiles * (gemm_red(p.cmax) ? 1 : p.cmax - 1) * p.rows, (uint64_t)p.BN, 1, 32))
     return cudaErrorInvalidValue;
   GemmArgs a;
   a.M = g.M; a.N = g.N; a.K = g.K; a.epi = g.epi; a.seg_cols = g.seg_cols;
@@ -863,6 +898,7 @@ cudaError_t launch_gemm(const GemmCall& g, cudaStream_t st) {
   a.dp_tiles = p.dp_tiles;
   a.cmax = p.cmax;
   a.cnt = p.sk ? static_cast<int32_t*>(g.workspace) : nullptr;
+  a.red = p.sk && gemm_red(p.cmax);
   const int groups = p.groups;
   cudaError_t e;
   if (p.SW) e = launch_one<64, 1, true>(maps, a, groups, st);

@@ -160,3 +160,4 @@ def test_workspace_shared_across_plans():
                 tol = 2.0 ** -8 * ref.abs() + 1e-3 * ref.abs().max() + 1e-6
                 assert (err > tol).sum().item() == 0, (M, N, K, epi, rep)
     assert int(ws[:32768].view(torch.int32).abs().sum().item()) == 0      # counters left zero
+    assert int((ws != 0).sum().item()) == 0        # reduce-add tiles left zero too

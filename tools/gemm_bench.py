@@ -29,6 +29,8 @@ def main():
     ap.add_argument("--iters", type=int, default=20)
     ap.add_argument("--copies", type=int, default=1,
                     help="cycle through this many weight copies (> L2 in total: weights streamed from HBM)")
+    ap.add_argument("--graph", action="store_true",
+                    help="time a CUDA graph of the iterations (device time without host launch gaps)")
     ap.add_argument("--lib", default=None, help="A/B: load this libs3.so build instead of the in-tree one")
     args = ap.parse_args()
     if args.lib:
@@ -61,10 +63,29 @@ def main():
                 for _ in range(3):
                     fn()
                 torch.cuda.synchronize()
-                e0.record()
-                for _ in range(args.iters):
-                    fn()
-                e1.record()
+                if args.graph:
+                    gs = torch.cuda.Stream()
+                    gs.wait_stream(torch.cuda.current_stream())
+                    graph = torch.cuda.CUDAGraph()
+                    with torch.cuda.stream(gs):
+                        stc = torch.cuda.current_stream()
+                        with torch.cuda.graph(graph, stream=gs):
+                            for _ in range(args.iters):
+                                if tag == "s3_gemm":
+                                    abi.s3_gemm(stc, a, nxt(), d, c=d if epi == 2 else None, epi=epi, workspace=ws)
+                                else:
+                                    fn()
+                    torch.cuda.synchronize()
+                    graph.replay()
+                    torch.cuda.synchronize()
+                    e0.record()
+                    graph.replay()
+                    e1.record()
+                else:
+                    e0.record()
+                    for _ in range(args.iters):
+                        fn()
+                    e1.record()
                 torch.cuda.synchronize()
                 res[tag] = e0.elapsed_time(e1) / args.iters
             flop = 2.0 * M * N * K
