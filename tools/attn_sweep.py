@@ -36,6 +36,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--case", default=None, help="run only cases whose name contains this")
     ap.add_argument("--lib", default=None, help="A/B: load this libs3.so build instead of the in-tree one")
+    ap.add_argument("--chunk", type=int, default=0, help="split-K unit rows C (0: the library default, 512)")
     ap.add_argument("--custom", action="append", default=[],
                     help="extra case 'name:L,H,Hkv,D,B,P,variant' (repeatable)")
     args = ap.parse_args()
@@ -58,7 +59,7 @@ def main():
         if R * kvpt > 150e9:
             continue
         eng = S3Engine(L, H, D, 2048, R, max(B, 16), num_kv_heads=0 if Hkv == H else Hkv,
-                       host_store_bytes=64 << 20, attn_variant=variant)
+                       host_store_bytes=64 << 20, attn_variant=variant, chunk_rows=args.chunk)
         n = B
         eng.submit(np.arange(n), np.full(n, P), np.full(n, args.steps + 8), np.full(n, 10_000))
         eng.admit()
@@ -68,7 +69,7 @@ def main():
             eng.step()
         p = eng.profile_get()
         gbs = (p.attn_bytes + p.fused_move_bytes) / (p.attn_ms / 1e3) / 1e9
-        print(json.dumps({"case": name, "L": L, "H": H, "Hkv": Hkv, "D": D, "B": B, "len": P,
+        print(json.dumps({"case": name, "chunk": args.chunk or 512, "L": L, "H": H, "Hkv": Hkv, "D": D, "B": B, "len": P,
                           "attn_ms_per_step": round(p.attn_ms / args.steps, 4), "gbs": round(gbs, 1),
                           "frac_of_peak": round(gbs / peak, 3)}), flush=True)
         eng.close()
