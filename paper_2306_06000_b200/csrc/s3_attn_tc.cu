@@ -345,6 +345,7 @@ constexpr int NGRP = TM / 8;     // 8-row groups per tile
 constexpr int NSTB = 5;          // store boxes of 16 / 8 / 4 / 2 / 1 groups (valid rows only)
 struct TcMaps {
   CUtensorMap kvg[NGRP];         // loads: box of n + 1 groups
+  CUtensorMap kvt[7];            // loads of a partial last group: box {64, r + 1 rows, 1 block, 1 group}
   CUtensorMap st_kv[NSTB];       // row-shift stores into the arena: box of 16 >> i groups
   CUtensorMap st_stage[NSTB];    // evictee stores into staging
   CUtensorMap q;                 // 16 q rows x both column blocks
@@ -369,6 +370,7 @@ struct TcArgs {
   const uint16_t* v_new;
   uint32_t* evdone;      // per-evictee staged-row counters (cumulative; the D2H stream waits on them)
   Feed feed;             // host-fed step: per-chunk ready words (s3_decode_step_host)
+  int32_t exact;         // 1: a segment's last, partial 8-row group loads only its valid rows
 };
 
 // Wait until a ready word written by the copy stream reaches `epoch` (host-fed
@@ -558,20 +560,37 @@ __global__ void __launch_bounds__(tc_threads(NC), 1) k_attn_tc(const __grid_cons
             h.mode = un.mode; h.drow = drow0 + r;
             if (un.mode == UNIT_STAGE) h.dep.ua = un.pad;   // eviction index (dep is only loaded for MOVE)
             h.prog = prog;
-            const int groups = (nrow + 7) / 8;   // 8-row groups (one 128B-swizzle atom per column block)
+            // 8-row groups (one 128B-swizzle atom per column block): fg whole groups in one
+            // 4-D box, then (exact) the tr rows of a partial last group as one box per column
+            // block -- the rows past nrow are never read (short items: ~5 % of the DRAM
+            // traffic); the smem rows they leave stale are masked (K) / zeroed (V) like the
+            // rows past a tile's last group
+            const int fg = a.exact ? nrow >> 3 : (nrow + 7) >> 3;
+            const int tr = a.exact ? nrow & 7 : 0;
             uint8_t* sk = kslot(smem, t, nk);
             uint8_t* sv = vslot(smem, t, nk, nv);
             uint8_t* sq = sk + KV_BYTES;
             const bool dep = fused && mv;
-            mb_expect(&S.kfull[ks], (uint32_t)(np_t * groups * 2048 + Q_BYTES + (dep ? 16 : 0)));
-            mb_expect(&S.vfull[vs], (uint32_t)(np_t * groups * 2048));
+            const uint32_t sbytes = (uint32_t)(fg * 2048 + tr * 256);   // per segment, K (or V)
+            mb_expect(&S.kfull[ks], (uint32_t)np_t * sbytes + (uint32_t)(Q_BYTES + (dep ? 16 : 0)));
+            mb_expect(&S.vfull[vs], (uint32_t)np_t * sbytes);
             if (dep) bulk_g2s16(&h.dep, a.desc + un.stage_base + r / TM, &S.kfull[ks]);
             const int row0 = un.off + un.r0 + r;
             for (int sgi = 0; sgi < np_t; ++sgi) {   // one 4-D box per segment for K and one for V
               const int colk = (a.l0 + li) * row_cols + (hd + sgi) * DH;
+              const int colv = colk + a.Hkv * DH;
               const int sgo = sgi * (seg_t / 8) * 2048;   // segment's first group
-              tma4d(sk + sgo, &maps.kvg[groups - 1], row0, colk / 64, &S.kfull[ks]);
-              tma4d(sv + sgo, &maps.kvg[groups - 1], row0, (colk + a.Hkv * DH) / 64, &S.vfull[vs]);
+              if (fg > 0) {
+                tma4d(sk + sgo, &maps.kvg[fg - 1], row0, colk / 64, &S.kfull[ks]);
+                tma4d(sv + sgo, &maps.kvg[fg - 1], row0, colv / 64, &S.vfull[vs]);
+              }
+              if (tr > 0) {
+                const int to = sgo + fg * 2048, tr0 = row0 + fg * 8;
+                tma4d(sk + to, &maps.kvt[tr - 1], tr0, colk / 64, &S.kfull[ks]);
+                tma4d(sk + to + 1024, &maps.kvt[tr - 1], tr0, colk / 64 + 1, &S.kfull[ks]);
+                tma4d(sv + to, &maps.kvt[tr - 1], tr0, colv / 64, &S.vfull[vs]);
+                tma4d(sv + to + 1024, &maps.kvt[tr - 1], tr0, colv / 64 + 1, &S.vfull[vs]);
+              }
             }
             const int qrow = (li * a.B + un.b) * a.H + g * a.G;
             tma3d(sq, &maps.q, 0, qrow, 0, &S.kfull[ks]);   // both 64-column blocks of the 16 q rows
@@ -1042,12 +1061,13 @@ EncodeTiledFn encoder() {
 // dimension, so a box starting at row r covers rows r .. r + 8 groups - 1; its extent is kept
 // generous (the row dimension bounds the start row; reads past the arena's last row land in
 // the 8 guard rows s3_workspace_query adds).
-bool encode_4d(CUtensorMap* m, const void* base, uint64_t row_elems, uint64_t rows, uint64_t pitch, int groups) {
+bool encode_4d(CUtensorMap* m, const void* base, uint64_t row_elems, uint64_t rows, uint64_t pitch, int groups,
+               int box_rows = 8, int blocks = 2) {
   EncodeTiledFn enc = encoder();
   if (!enc) return false;
   cuuint64_t dims[4] = {64, rows, row_elems / 64, rows / 8 + 2};
   cuuint64_t strides[3] = {pitch, 128, 8 * pitch};
-  cuuint32_t box[4] = {64, 8, 2, (cuuint32_t)groups};
+  cuuint32_t box[4] = {64, (cuuint32_t)box_rows, (cuuint32_t)blocks, (cuuint32_t)groups};
   cuuint32_t es[4] = {1, 1, 1, 1};
   return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box, es,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -1116,6 +1136,9 @@ cudaError_t launch_attn_tc(const Shape& sh, const uint16_t* q, const uint16_t* k
   for (int n = 1; n <= NGRP; ++n)
     if (!encode_4d(&maps.kvg[n - 1], arena, (uint64_t)sh.row_elems, (uint64_t)arena_rows, (uint64_t)sh.kvpt, n))
       return cudaErrorInvalidValue;
+  for (int r = 1; r <= 7; ++r)
+    if (!encode_4d(&maps.kvt[r - 1], arena, (uint64_t)sh.row_elems, (uint64_t)arena_rows, (uint64_t)sh.kvpt, 1, r, 1))
+      return cudaErrorInvalidValue;
   for (int i = 0; i < NSTB; ++i) {
     if (!encode_4d(&maps.st_kv[i], arena, (uint64_t)sh.row_elems, (uint64_t)arena_rows, (uint64_t)sh.kvpt, NGRP >> i))
       return cudaErrorInvalidValue;
@@ -1135,6 +1158,8 @@ cudaError_t launch_attn_tc(const Shape& sh, const uint16_t* q, const uint16_t* k
   a.arena = reinterpret_cast<uint8_t*>(arena); a.staging = staging; a.kvpt = sh.kvpt;
   a.desc = desc; a.progress = progress; a.epoch = epoch;
   a.k_new = k_new; a.v_new = v_new; a.feed = feed; a.evdone = evdone;
+  static const int exact = [] { const char* e = getenv("S3_TC_EXACT"); return e ? atoi(e) : 1; }();   // A/B
+  a.exact = exact;
   // Per launch, from the step's rows (s3_host.cpp):
   // * ring shape: 2 K + 4 V slots for short items (mostly one tile; mean <= 48 rows), else
   //   3 + 3 (the fused row shift holds K slots on long, moving items); LLaMA-3-8B threshold
