@@ -86,6 +86,25 @@ def test_workspace_query_and_validation(s3lib):
         assert e.value.code == abi.S3_E_INVAL
 
 
+def test_gemm_workspace_plans(s3lib):
+    # host-side GEMM planning (no device: 148 SMs assumed): the workspace a plan asks
+    # for pins its choices -- 32 KB of stream-K counters plus ONE fp32 reduce-add tile
+    # per tile (rows x BN x 4 B) when it splits K, nothing when it does not
+    cnt = 32768
+    # M <= 64: swapped operands, 128 W rows x 64 batch columns per tile; stream-K only
+    # when the N / 128 tiles fill at most half the SMs (output / down projections)
+    assert abi.s3_gemm_workspace(8, 4096, 4096, epi=2) == cnt + (4096 // 128) * 128 * 64 * 4
+    assert abi.s3_gemm_workspace(64, 4096, 16384, epi=2) == cnt + (4096 // 128) * 128 * 64 * 4
+    assert abi.s3_gemm_workspace(8, 12288, 4096, seg_cols=4096) == 0        # 96 tiles: data parallel
+    assert abi.s3_gemm_workspace(1, 16384, 4096, epi=1) == 0                # 128 tiles
+    # M = 161: single-CTA 128 x 128 tiles (2 x 32 of them), stream-K over the SMs
+    assert abi.s3_gemm_workspace(161, 4096, 4096, epi=2) == cnt + 2 * 32 * 128 * 128 * 4
+    # large M, full waves of CTA-pair tiles: data parallel
+    assert abi.s3_gemm_workspace(4096, 4096, 4096, epi=2) == 0
+    with pytest.raises(abi.S3Error):
+        abi.s3_gemm_workspace(8, 100, 4096)                                # N not a multiple of 128
+
+
 def test_init_rejects_missing_buffers(s3lib):
     ctx = C.c_void_p()
     bufs = abi.s3_buffers()
