@@ -311,18 +311,57 @@ __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(const __grid_constant__ G
   // The producer and MMA roles run warp-wide with warp-uniform operands and one elected
   // lane issuing: a tcgen05.mma / TMA operand the compiler cannot prove uniform costs an
   // ELECT / R2UR.BROADCAST loop around every instruction (see s3_attn_tc.cu, uni()).
+  // Programmatic dependent launch: let the next kernel on the stream start its CTAs on the
+  // SMs this grid leaves (its prologue and weight prefetch overlap our tail); everything
+  // that reads or writes data another kernel produces or consumes waits for the previous
+  // grid (griddepcontrol.wait returns at once without a PDL launch).
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (warp == 0) {
     // ------------------------------ TMA producer ------------------------------
     int s = 0;
     uint32_t ph = 0;
     WorkIter wi = work();
+    // CG = 1: the weight boxes of the first ring stages are loaded BEFORE waiting for the
+    // previous grid (weights are constant); their stages' activation boxes follow the wait
+    int pre = 0;
+    bool waited = false;
+    if constexpr (CG == 1) {
+      WorkIter w0 = wi;
+      Work wk;
+      if (w0.next(wk)) {
+        const int t = wk.tile;
+        const int m0 = (t % a.m_tiles) * TM_ROWS, n0 = (t / a.m_tiles) * BN;
+        pre = min(NSTG, wk.kb1 - wk.kb0);
+        if (g_elect_one()) {
+          for (int i = 0; i < pre; ++i) {
+            uint8_t* sa = smem + i * STAGE;
+            const int kb = wk.kb0 + i;
+            g_mb_expect(&full[i], (uint32_t)STAGE);
+            if constexpr (SW) g_tma2d(sa, &maps.a, kb * GK, m0, &full[i]);            // W rows
+            else g_tma2d(sa + A_BYTES, &maps.w, kb * GK, n0, &full[i]);
+          }
+        }
+        __syncwarp();
+      }
+    }
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     for (Work wk; wi.next(wk);) {
       const int t = wk.tile;
       const int m0 = (t % a.m_tiles) * TM_ROWS + (int)rank * GM;
       const int n0 = (t / a.m_tiles) * BN + (int)rank * (BN / CG);
       for (int kb = wk.kb0; kb < wk.kb1; ++kb) {
-        g_mb_wait(&empty[s], ph ^ 1u);
         uint8_t* sa = smem + s * STAGE;
+        if (!waited && pre > 0) {   // a prefetched stage: its activation box only
+          if (g_elect_one()) {
+            if constexpr (SW) g_tma2d(sa + A_BYTES, &maps.w, kb * GK, n0, &full[s]);
+            else g_tma2d(sa, &maps.a, kb * GK, m0, &full[s]);
+          }
+          __syncwarp();
+          if (--pre == 0) waited = true;
+          if (++s == NSTG) { s = 0; ph ^= 1u; }
+          continue;
+        }
+        g_mb_wait(&empty[s], ph ^ 1u);
         if (g_elect_one()) {
           if constexpr (CG == 1) {
             g_mb_expect(&full[s], (uint32_t)STAGE);
@@ -380,6 +419,7 @@ __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(const __grid_constant__ G
     // Warp w owns TMEM lanes 32 (w % 4) .. + 31 = 32 rows of the CTA's 128.  Values go
     // TMEM -> registers -> a 128B-swizzled staging tile -> one TMA store per 32 x 64
     // bf16 chunk (coalesced, asynchronous); addends and partials come in by TMA loads.
+    asm volatile("griddepcontrol.wait;" ::: "memory");   // C, D, workspace: the previous grid is done
     const int quarter = warp & 3;
     uint8_t* eb = epi_smem + quarter * EPI_WARP_BYTES;
     uint64_t* ib = inbar + quarter * 2;
@@ -692,13 +732,17 @@ cudaError_t launch_one(const GemmMaps& maps, const GemmArgs& a, int grid, cudaSt
   cfg.blockDim = dim3(G_THREADS);
   cfg.dynamicSmemBytes = gemm_smem<BN, CG>();
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = CG;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  // programmatic dependent launch (S3_GEMM_PDL=0 turns it off: A/B)
+  static const int pdl = [] { const char* e = getenv("S3_GEMM_PDL"); return e ? atoi(e) : 1; }();
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, k_gemm<BN, CG, SW>, maps, a);
 }
 

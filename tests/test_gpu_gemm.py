@@ -139,6 +139,51 @@ def test_proxy_model_attention_through_oracle():
     assert checked >= 50
 
 
+@pytest.mark.parametrize("M", [8, 64, 161, 700])
+def test_dependent_chain_without_sync(M):
+    # back-to-back GEMMs on one stream with no sync in between (programmatic dependent
+    # launch: each kernel's prologue and weight prefetch overlap the previous one's tail):
+    # read-after-write (h, qkv feed later GEMMs) and write-after-read (the residual x is
+    # read by the first two and rewritten in place by the last two) must both hold
+    from paper_2306_06000_b200 import s3 as abi
+    st = torch.cuda.current_stream()
+    g = torch.Generator(device="cuda").manual_seed(M + 11)
+    d, dff = 4096, 16384
+
+    def wgt(n, k):
+        return (torch.randn(n, k, device="cuda", generator=g) / math.sqrt(k)).to(torch.bfloat16)
+
+    wqkv, w1, wo, w2 = wgt(3 * d, d), wgt(dff, d), wgt(d, d), wgt(d, dff)
+    x = torch.randn(M, d, device="cuda", generator=g).to(torch.bfloat16)
+    x0 = x.clone()
+    ws = torch.zeros(96 << 20, device="cuda", dtype=torch.uint8)
+    q, k, v = (torch.full((M, d), float("nan"), device="cuda", dtype=torch.bfloat16) for _ in range(3))
+    h = torch.full((M, dff), float("nan"), device="cuda", dtype=torch.bfloat16)
+    torch.cuda.synchronize()
+    for _ in range(2):
+        x.copy_(x0)
+        abi.s3_gemm(st, x, wqkv, [q, k, v], seg_cols=d, workspace=ws)
+        abi.s3_gemm(st, x, w1, h, epi=1, workspace=ws)
+        abi.s3_gemm(st, q, wo, x, c=x, epi=2, workspace=ws)           # reads q, rewrites x
+        abi.s3_gemm(st, h, w2, x, c=x, epi=2, workspace=ws)           # reads h and the new x
+    torch.cuda.synchronize()
+    qkv = torch.cat([q, k, v], dim=1)
+
+    def close(got, ref, what, extra=0.0):
+        got = got.double()
+        err = (got - ref).abs()
+        tol = 2.0 ** -8 * ref.abs() + extra + 1e-3 * ref.abs().max() + 1e-6
+        assert torch.isfinite(got).all() and (err > tol).sum().item() == 0, (M, what, err.max().item())
+
+    close(qkv, _ref(x0, wqkv, 0, None), "qkv")
+    close(h, _ref(x0, w1, 1, None), "h")
+    x1 = _ref(q, wo, 2, x0).to(torch.bfloat16)                    # the in-place residual, bf16
+    # the kernel's own bf16 rounding of that intermediate may differ from this one by one
+    # unit in the last place (<= 2^-7 |x1|): allowed on top of the final rounding (a hazard
+    # is O(1) off; the single-GEMM cases above hold the plain bar at every one of these M)
+    close(x, _ref(h, w2, 2, x1), "x", extra=2.0 ** -7 * x1.double().abs())
+
+
 def test_workspace_shared_across_plans():
     # the proxy's four projections share one split-K workspace: plans with
     # different tile counts must leave the shared counters zero for each other
