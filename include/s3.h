@@ -346,7 +346,10 @@ s3_status s3_verify_resident(s3_ctx* ctx, int64_t* bad_rows);
  *          the QKV projection straight into q, k_new, v_new); unused = NULL;
  *   c      epi 2: device bf16 [M][N] (may be d[0], in place), else NULL.
  * K % 64 == 0, N % 128 == 0, seg_cols % 128 == 0; 16-B aligned pointers.
- * Stream-ordered on `stream` (a cudaStream_t); no context needed.
+ * Stream-ordered on `stream` (a cudaStream_t); no context needed.  Launched
+ * with programmatic dependent launch: a following s3_gemm's CTAs may start
+ * (prologue only; every global access waits for this grid) on SMs this one
+ * has left; the ordering a stream guarantees is unchanged.
  * S3_E_INVAL on a bad shape or pointer, S3_E_CUDA on a launch error.      */
 typedef struct {
   const void* a; const void* w; void* d[3]; const void* c;

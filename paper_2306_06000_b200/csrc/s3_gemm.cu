@@ -134,6 +134,7 @@ struct GemmArgs {
   int32_t dp_tiles;       // tiles [0, dp_tiles) data parallel, the rest stream-K (equal K-block ranges per group)
   int32_t cmax;           // stream-K: most CTA groups contributing to one tile (partial slots = cmax - 1)
   int32_t* cnt;           // stream-K: per (tile, CTA of the pair) [claim, done] counters (zero between calls)
+  int32_t wpre;           // PDL: load the first stages' weight boxes before waiting for the previous grid
   int32_t red;            // stream-K: 1 = contributors TMA-reduce-add into one fp32 tile per tile (zero between
                           //   calls; the reducer reads it once and re-zeroes it), 0 = one partial slot each
 };
@@ -321,14 +322,15 @@ __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(const __grid_constant__ G
     int s = 0;
     uint32_t ph = 0;
     WorkIter wi = work();
-    // CG = 1: the weight boxes of the first ring stages are loaded BEFORE waiting for the
-    // previous grid (weights are constant); their stages' activation boxes follow the wait
+    // opt-in (S3_GEMM_PDL=2), CG = 1: the weight boxes of the first ring stages are loaded
+    // BEFORE waiting for the previous grid -- only valid when the kernel just before this one
+    // on the stream did not write W (off by default); their activation boxes follow the wait
     int pre = 0;
     bool waited = false;
     if constexpr (CG == 1) {
       WorkIter w0 = wi;
       Work wk;
-      if (w0.next(wk)) {
+      if (a.wpre && w0.next(wk)) {
         const int t = wk.tile;
         const int m0 = (t % a.m_tiles) * TM_ROWS, n0 = (t / a.m_tiles) * BN;
         pre = min(NSTG, wk.kb1 - wk.kb0);
@@ -737,7 +739,7 @@ cudaError_t launch_one(const GemmMaps& maps, const GemmArgs& a, int grid, cudaSt
   at[0].val.clusterDim.x = CG;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
-  // programmatic dependent launch (S3_GEMM_PDL=0 turns it off: A/B)
+  // programmatic dependent launch (S3_GEMM_PDL=0 turns it off: A/B; =2 adds the weight prefetch)
   static const int pdl = [] { const char* e = getenv("S3_GEMM_PDL"); return e ? atoi(e) : 1; }();
   at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[1].val.programmaticStreamSerializationAllowed = 1;
@@ -943,6 +945,8 @@ cudaError_t launch_gemm(const GemmCall& g, cudaStream_t st) {
   a.cmax = p.cmax;
   a.cnt = p.sk ? static_cast<int32_t*>(g.workspace) : nullptr;
   a.red = p.sk && gemm_red(p.cmax);
+  static const int pdl_mode = [] { const char* e = getenv("S3_GEMM_PDL"); return e ? atoi(e) : 1; }();
+  a.wpre = pdl_mode == 2;   // opt-in: the caller guarantees the previous kernel did not write W
   const int groups = p.groups;
   cudaError_t e;
   if (p.SW) e = launch_one<64, 1, true>(maps, a, groups, st);
