@@ -11,7 +11,7 @@
 //
 // One persistent CTA per SM, 6 warps:
 //   warp 0  TMA producer: per K block one 2-D box of A [128 x 64] and one of W
-//           [BN x 64] (128B swizzle) into a 4-stage ring (mbarrier full / empty);
+//           [BN x 64] (128B swizzle) into a ring of up to 6 stages (mbarrier full / empty);
 //   warp 1  MMA issuer: one thread issues tcgen05.mma.cta_group::1.kind::f16,
 //           M 128, N BN, K 16 (4 per K block), into one of two TMEM
 //           accumulators (2 x BN fp32 columns), commits the stage back to the
@@ -29,6 +29,11 @@
 // activations (instead of a 128-row activation tile mostly zero-filled), and
 // TMEM holds D^T: the epilogue transposes 32 x 32 blocks through shared memory
 // into the row-major output.
+// CTA pairs (cta_group::2, 256 x 256 tiles) for large M; stream-K over the
+// ragged last wave, the groups sharing a tile adding their fp32 partials into
+// one workspace tile by TMA reduce-add (the last to arrive reads it once).
+// Programmatic dependent launch: the next GEMM's prologue overlaps this one's
+// tail; every global access waits in griddepcontrol.wait.  DESIGN.md §10 NEXT-2.
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
