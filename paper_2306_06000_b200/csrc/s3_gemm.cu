@@ -605,6 +605,17 @@ __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(const __grid_constant__ G
           asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(claim + 1) : "memory");
         }
       } else {
+        // reduce-add mode, epi 2: the residual of the first 64 columns is requested before
+        // waiting for the other splits, so its round trip overlaps the wait (BN = 64 when SW)
+        const bool cpre = a.red && a.epi == 2;
+        if (cpre) {
+          if constexpr (SW) {
+            load_in(0, &maps.c, wn, n0, 2048u);
+            if (n0 + 32 < a.M) load_in(1, &maps.c, wn, n0 + 32, 2048u);
+          } else {
+            load_in(1, &maps.c, n0, y);
+          }
+        }
         if (lane == 0) {                               // every other split's 4 warps stored their partial
           const int want = 4 * (S - 1);
           for (;;) {
@@ -623,10 +634,19 @@ __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(const __grid_constant__ G
           if (c + 64 >= BN) release(acc);
           if (a.red) {   // the other splits' sum, one TMA round trip; then zero it for the next call
             const int prow = t * TM_ROWS + (int)rank * GM + quarter * 32;
+            if (cpre) {  // the residual first: it was requested before the wait above
+              if constexpr (SW) {
+                add_cT(v, 0);
+                if (n0 + c + 32 < a.M) add_cT(v + 32, 1);
+              } else {
+                add_c(v, 1);
+              }
+            }
             load_in(0, &maps.p, c, prow);
             load_in(1, &maps.p, c + 32, prow);
             add_p(v, 0);
             add_p(v + 32, 1);
+            if (!SW && cpre && c + 64 < BN) load_in(1, &maps.c, n0 + c + 64, y);   // next chunk's residual
 #pragma unroll
             for (int h = 0; h < 2; ++h) {   // zeros back by TMA stores (generic stores here cost ~8 %)
               uint8_t* o = out_tile();
@@ -647,7 +667,7 @@ __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(const __grid_constant__ G
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
               if (n0 + c + 32 * h >= a.M) break;   // batch rows past M: nothing to store
-              if (a.epi == 2) {
+              if (a.epi == 2 && !cpre) {
                 load_in(0, &maps.c, wn, n0 + c + 32 * h, 2048u);
                 add_cT(v + 32 * h, 0);
               }
@@ -655,7 +675,7 @@ __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(const __grid_constant__ G
             }
             continue;
           }
-          if (a.epi == 2) {
+          if (a.epi == 2 && !cpre) {
             load_in(0, &maps.c, n0 + c, y);
             add_c(v, 0);
           }
