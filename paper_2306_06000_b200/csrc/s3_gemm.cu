@@ -136,6 +136,9 @@ struct GemmMaps {
 };
 struct GemmArgs {
   int32_t M, N, K, epi, seg_cols, m_tiles, n_tiles;
+  int32_t stage_tx;       // bytes one ring stage receives (SW: the activation box holds only the
+                          //   batch's rows rounded to 8; the rest of its BN rows stay stale and
+                          //   only feed D^T columns past M, which are never stored)
   int32_t dp_tiles;       // tiles [0, dp_tiles) data parallel, the rest stream-K (equal K-block ranges per group)
   int32_t cmax;           // stream-K: most CTA groups contributing to one tile (partial slots = cmax - 1)
   int32_t* cnt;           // stream-K: per (tile, CTA of the pair) [claim, done] counters (zero between calls)
@@ -343,7 +346,7 @@ __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(const __grid_constant__ G
           for (int i = 0; i < pre; ++i) {
             uint8_t* sa = smem + i * STAGE;
             const int kb = wk.kb0 + i;
-            g_mb_expect(&full[i], (uint32_t)STAGE);
+            g_mb_expect(&full[i], (uint32_t)a.stage_tx);
             if constexpr (SW) g_tma2d(sa, &maps.a, kb * GK, m0, &full[i]);            // W rows
             else g_tma2d(sa + A_BYTES, &maps.w, kb * GK, n0, &full[i]);
           }
@@ -371,7 +374,7 @@ __global__ void __launch_bounds__(G_THREADS, 1) k_gemm(const __grid_constant__ G
         g_mb_wait(&empty[s], ph ^ 1u);
         if (g_elect_one()) {
           if constexpr (CG == 1) {
-            g_mb_expect(&full[s], (uint32_t)STAGE);
+            g_mb_expect(&full[s], (uint32_t)a.stage_tx);
             g_tma2d(sa, &maps.a, kb * GK, m0, &full[s]);
             g_tma2d(sa + A_BYTES, &maps.w, kb * GK, n0, &full[s]);
           } else {
@@ -932,6 +935,10 @@ bool gemm_plan(const GemmCall& g, int64_t ws_avail, GemmPlan& p) {
   return true;
 }
 
+// SW: rows of the activation box -- the batch rounded up to 8 (TMA zero-fill of the
+// remaining rows of a 64-row box made M = 8 ~30 % slower than M = 32)
+int swap_box_rows(int M, int BN) { return std::min(BN, (M + 7) & ~7); }
+
 int64_t gemm_workspace_bytes(const GemmCall& g) {
   GemmPlan p;
   return gemm_plan(g, INT64_MAX, p) ? p.ws_bytes : -1;
@@ -944,7 +951,8 @@ cudaError_t launch_gemm(const GemmCall& g, cudaStream_t st) {
   GemmMaps maps;
   if (p.SW) {   // the MMA's M side is W (128-row boxes), its N side the batch (BN-row boxes)
     if (!encode_kmajor(&maps.a, g.w, (uint64_t)g.N, (uint64_t)g.K, GM)) return cudaErrorInvalidValue;
-    if (!encode_kmajor(&maps.w, g.a, (uint64_t)g.M, (uint64_t)g.K, (uint32_t)p.BN)) return cudaErrorInvalidValue;
+    if (!encode_kmajor(&maps.w, g.a, (uint64_t)g.M, (uint64_t)g.K, (uint32_t)swap_box_rows(g.M, p.BN)))
+      return cudaErrorInvalidValue;
   } else {
     if (!encode_kmajor(&maps.a, g.a, (uint64_t)g.M, (uint64_t)g.K, GM)) return cudaErrorInvalidValue;
     if (!encode_kmajor(&maps.w, g.w, (uint64_t)g.N, (uint64_t)g.K, (uint32_t)(p.BN / p.CG))) return cudaErrorInvalidValue;
@@ -966,6 +974,7 @@ cudaError_t launch_gemm(const GemmCall& g, cudaStream_t st) {
   GemmArgs a;
   a.M = g.M; a.N = g.N; a.K = g.K; a.epi = g.epi; a.seg_cols = g.seg_cols;
   a.m_tiles = p.m_tiles; a.n_tiles = p.SW ? 1 : g.N / p.BN;
+  a.stage_tx = GM * GK * 2 + (p.SW ? swap_box_rows(g.M, p.BN) : p.BN / p.CG) * GK * 2;
   a.dp_tiles = p.dp_tiles;
   a.cmax = p.cmax;
   a.cnt = p.sk ? static_cast<int32_t*>(g.workspace) : nullptr;
