@@ -52,7 +52,12 @@ def _ref(a, w, epi, c):
     (1, 4096, 4096, 2, 1, True), (33, 12288, 4096, 0, 3, True), (100, 4096, 16384, 2, 1, True),
     (128, 16384, 4096, 1, 1, True), (96, 4096, 4096, 1, 1, False), (65, 384, 192, 2, 1, True),
     (17, 4096, 16384, 1, 1, True), (127, 12288, 4096, 0, 3, False),
-    (64, 4096, 16384, 2, 1, True), (48, 4096, 4096, 1, 1, True), (161, 12288, 4096, 0, 3, True), (255, 4096, 16384, 2, 1, True), (129, 16384, 4096, 1, 1, False),
+    (64, 4096, 16384, 2, 1, True), (48, 4096, 4096, 1, 1, True), (161, 12288, 4096, 0, 3, True),
+    (255, 4096, 16384, 2, 1, True), (129, 16384, 4096, 1, 1, False),
+    # batch-sized activation boxes (rows rounded to 8; stale rows past M), residual requested
+    # before the stream-K wait with one or both 32-row halves present
+    (1, 12288, 4096, 0, 3, True), (5, 4096, 16384, 2, 1, True), (40, 4096, 4096, 2, 1, True),
+    (9, 16384, 4096, 1, 1, True),
 ])
 def test_gemm_matches_fp64(M, N, K, epi, nseg, ws):
     from paper_2306_06000_b200 import s3 as abi
@@ -142,7 +147,8 @@ def test_proxy_model_attention_through_oracle():
 @pytest.mark.parametrize("M", [8, 64, 161, 700])
 def test_dependent_chain_without_sync(M):
     # back-to-back GEMMs on one stream with no sync in between (programmatic dependent
-    # launch: each kernel's prologue and weight prefetch overlap the previous one's tail):
+    # launch: each kernel's prologue overlaps the previous one's tail; S3_GEMM_PDL=2 adds
+    # the opt-in weight prefetch):
     # read-after-write (h, qkv feed later GEMMs) and write-after-read (the residual x is
     # read by the first two and rewritten in place by the last two) must both hold
     from paper_2306_06000_b200 import s3 as abi
