@@ -146,21 +146,29 @@ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
   z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
   return z ^ (z >> 31);
 }
+// One byte of a 32-bit word as the float 2^23 + byte (PRMT with the 0x4B000000 exponent),
+// then (byte - 128) * scale in one exact FFMA (scale a power of two); the bf16 of two such
+// floats is their high halves, packed by one more PRMT.  Integer-pipe work per 16-B vector
+// drops by ~2/3 against shift / mask / I2F / shift per element (k_synth is ALU-pipe bound).
+__device__ __forceinline__ float byte_float(uint32_t word, uint32_t j, float scale) {
+  const float f = __uint_as_float(__byte_perm(word, 0x4B000000u, 0x7540u + j));
+  return fmaf(f, scale, -8388736.0f * scale);
+}
+__device__ __forceinline__ uint32_t pack_hi(float lo, float hi) {
+  return __byte_perm(__float_as_uint(lo), __float_as_uint(hi), 0x7632u);
+}
+__device__ __forceinline__ uint4 bytes_to_bf16x8(uint64_t z, float scale) {
+  const uint32_t a = (uint32_t)z, b = (uint32_t)(z >> 32);
+  return make_uint4(pack_hi(byte_float(a, 0, scale), byte_float(a, 1, scale)),
+                    pack_hi(byte_float(a, 2, scale), byte_float(a, 3, scale)),
+                    pack_hi(byte_float(b, 0, scale), byte_float(b, 1, scale)),
+                    pack_hi(byte_float(b, 2, scale), byte_float(b, 3, scale)));
+}
 // 8 bf16 values (one 16-byte vector) for element group d8 of (req,l,kv,pos,h).
 // tag 0 (K/V rows) indexes the Hkv KV heads, tag 1 (q) the H query heads.
 // 8 generator values from counter g: bytes of splitmix64 minus 128, times scale
 __device__ __forceinline__ uint4 gen8_at(uint64_t seed, uint64_t tag, uint64_t g, float scale) {
-  const uint64_t z = splitmix64(seed ^ (tag << 60) ^ g);
-  uint32_t w[4];
-#pragma unroll
-  for (int p = 0; p < 4; ++p) {
-    const int k0 = (int)((z >> (16 * p)) & 0xFF) - 128;
-    const int k1 = (int)((z >> (16 * p + 8)) & 0xFF) - 128;
-    const uint32_t b0 = __float_as_uint((float)k0 * scale) >> 16;
-    const uint32_t b1 = __float_as_uint((float)k1 * scale) >> 16;
-    w[p] = b0 | (b1 << 16);
-  }
-  return make_uint4(w[0], w[1], w[2], w[3]);
+  return bytes_to_bf16x8(splitmix64(seed ^ (tag << 60) ^ g), scale);
 }
 // counter of the first 16-B vector of row (req, l, kv, pos): g = ((((req L + l) 2 + kv) M + pos) nh + h) D/8 + d8
 __device__ __forceinline__ uint64_t gen_row_base(const Shape& sh, uint64_t nh, int64_t req, int l, int kv, int pos) {
@@ -172,17 +180,7 @@ __device__ __forceinline__ uint4 gen8(const Shape& sh, uint64_t seed, uint64_t t
   const uint64_t g =
       (((((uint64_t)req * sh.L + l) * 2u + kv) * (uint64_t)sh.max_len + pos) * nh + h) *
           (uint64_t)(sh.D / 8) + d8;
-  const uint64_t z = splitmix64(seed ^ (tag << 60) ^ g);
-  uint32_t w[4];
-#pragma unroll
-  for (int p = 0; p < 4; ++p) {
-    const int k0 = (int)((z >> (16 * p)) & 0xFF) - 128;
-    const int k1 = (int)((z >> (16 * p + 8)) & 0xFF) - 128;
-    const uint32_t b0 = __float_as_uint((float)k0 * scale) >> 16;
-    const uint32_t b1 = __float_as_uint((float)k1 * scale) >> 16;
-    w[p] = b0 | (b1 << 16);
-  }
-  return make_uint4(w[0], w[1], w[2], w[3]);
+  return bytes_to_bf16x8(splitmix64(seed ^ (tag << 60) ^ g), scale);
 }
 
 // ---------------------------------------------------------------------------
